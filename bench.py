@@ -1,0 +1,373 @@
+#!/usr/bin/env python
+"""SPMESL hot-path benchmark (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 5]
+
+One step = one whole SPMESL fit of the BASELINE.json workload (config 5: n=500, p=20000,
+Erdos-Renyi precision, lambda0 = lambda_ub, tol 1e-4): standardize -> persistent CD over all
+p column problems -> CSC export -> Theta assembly + symmetrization (and, for N > 1, the CSC
+all-gather).  value = algorithmic coordinate updates (sum_k sweeps_k (p-1)) per second of
+device time, whole job.  e2e = the same through the host C-ABI entry point spmesl_fit_ex
+with pinned host buffers (H2D of X and D2H of Theta/sigma/iters inside the timed region).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SPMESL fit time (s) + CD coord-updates/s at p=5k-20k, 1/2/4/8 B200 vs roofline"
+UNIT = "coord-updates/s"
+TOL = 1e-4
+MAX_ITER = 100
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--family", default=None)
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--p", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def workload(args):
+    from synth import generators as G
+    over = {k: v for k, v in dict(family=args.family, n=args.n, p=args.p).items() if v}
+    X, gt, spec = G.make_config(args.config, **over)
+    return X, spec
+
+
+def lambda0_for(spec, n, p):
+    # the product's own penalty helper (rule per config)
+    import paper_2203_15031_b200 as S
+    return S.lambda_ub(n, p) if spec["rule"] == "ub" else S.lambda_univ(n, p)
+
+
+def config_dict(spec, world, lam, extra=None):
+    d = {"workload": f"BASELINE config {spec.get('idx', '?')}: n={spec['n']}, p={spec['p']}, "
+                     f"{spec['family']} precision, lambda0={spec['rule']}",
+         "n": spec["n"], "p": spec["p"], "family": spec["family"], "penalty_rule": spec["rule"],
+         "lambda0": lam, "tol": TOL, "max_iter": MAX_ITER, "seed": spec["seed"],
+         "parallelism": f"column-blocks x{world}",
+         "l2": "flushed between timed steps (256 MiB write); Theta (8p^2 B) also exceeds L2"}
+    if extra:
+        d.update(extra)
+    return d
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": sorted(reasons)}
+        load = [x for x in sm if x > 500] or sm
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- peaks
+def fp64_peak():
+    """Measured FP64 tensor (DMMA m8n8k4) peak of this pool's B200 (profiles/)."""
+    path = os.path.join(ROOT, "profiles", "r01_peaks_microbench.json")
+    try:
+        d = json.load(open(path))
+        keys = [k for k in d if k.startswith("dmma_") and k.endswith("_tflops")]
+        return max(d[k] for k in keys), "profiles/r01_peaks_microbench.json (DMMA f64, measured)"
+    except Exception:
+        return 36.8, "fallback 36.8 TFLOP/s (microbench value)"
+
+
+def cd_traffic():
+    path = os.path.join(ROOT, "profiles", "cd_traffic.json")
+    try:
+        return json.load(open(path))
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------- oracle baseline
+def cpu_baseline(X, lam, seconds, seed=0):
+    """The oracle (as it stands) on a bounded random sample of columns of the same workload."""
+    from oracle import oracle as O
+    n, p = X.shape
+    Xs, mu, s = O.standardize(X)
+    rng = np.random.default_rng(seed)
+    order = rng.permutation(p)
+    threads = O.num_threads()
+    done, t_tot, sweeps = 0, 0.0, 0
+    batch = max(threads * 4, 16)
+    while t_tot < seconds and done < p:
+        cols = np.sort(order[done:done + batch])
+        t0 = time.perf_counter()
+        r = O.spmesl_columns(Xs, cols, lam, delta=TOL, max_outer=MAX_ITER, want_margin=False)
+        t_tot += time.perf_counter() - t0
+        sweeps += int(r.sweeps.sum())
+        done += len(cols)
+    v = sweeps * (p - 1)
+    return {"value": v / t_tot, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"{done} of {p} columns (each with all p-1 predictors), {t_tot:.1f} s",
+            "seconds": t_tot, "columns": done, "sweeps": sweeps}
+
+
+# ----------------------------------------------------------------------------- main arms
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    X, spec = workload(args)
+    spec["idx"] = args.config
+    n, p = X.shape
+    from oracle import oracle as O
+    lam = O.lambda_ub(n, p) if spec["rule"] == "ub" else O.lambda_univ(n, p)
+    per_step = max(2.0, min(20.0, 120.0 / max(args.steps + args.warmup, 1)))
+    for _ in range(args.warmup):
+        cpu_baseline(X, lam, per_step / 4, seed=1)
+    vals, secs = [], []
+    base = None
+    for k in range(args.steps):
+        b = cpu_baseline(X, lam, per_step, seed=100 + k)
+        vals.append(b["value"])
+        secs.append(b["seconds"])
+        base = b
+    v = float(np.mean(vals))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000 * float(np.mean(secs)), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(spec, 1, lam, {"reference": "CPU oracle (oracle/spmesl_oracle.c), "
+                                                  "bounded column sample per step"}),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": base["cores"], "kind": "oracle",
+                             "sample": base["sample"]},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2203_15031_b200 as S
+    from paper_2203_15031_b200 import distributed as D
+    S.load()
+    X, spec = workload(args)
+    spec["idx"] = args.config
+    n, p = X.shape
+    lam = lambda0_for(spec, n, p)
+    dev = torch.device("cuda", local)
+    Xd = torch.from_numpy(np.ascontiguousarray(X.T)).to(dev).t()   # (n, p) column-major
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    def step():
+        if world == 1:
+            r = S.fit_device(Xd, lam, TOL, MAX_ITER, stream=stream)
+            return r.stats, r
+        r = D.fit_distributed(Xd, lam, TOL, MAX_ITER, stream=stream)
+        return r["stats"], r
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    cd_ms, updates, stats_last = [], 0, None
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.fill_(k & 0xff)
+            torch.cuda.synchronize()
+            barrier()
+            torch.cuda.synchronize()
+            ev0[k].record(stream)
+            st, res = step()
+            ev1[k].record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            cd_ms.append(st["ms_cd"])
+            updates += st["coord_updates"]
+            stats_last = st
+    step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
+    tot_ms = sum(step_ms)
+    cd_tot = sum(cd_ms)
+    if dist:
+        t = torch.tensor([tot_ms, cd_tot], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms, cd_tot = float(t[0]), float(t[1])
+        u = torch.tensor([updates], dtype=torch.int64, device=dev)
+        dist.all_reduce(u)
+        updates = int(u[0])
+    value = updates / (tot_ms / 1000.0)
+    upd_per_step = updates / args.steps
+    # roofline of the dominant kernel (CD sweep): 2n flops per coordinate update (§8(d))
+    peak, peak_src = fp64_peak()
+    flops_per_step_rank = 2.0 * n * (stats_last["coord_updates"])
+    achieved = flops_per_step_rank / (float(np.mean(cd_ms)) / 1000.0) / 1e12
+    traffic = cd_traffic()
+    roof = {"kernel": "cd_sweep_kernel", "bound": "tensor", "achieved": achieved, "peak": peak,
+            "unit": "TFLOP/s", "frac": achieved / peak,
+            "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+            "peak_source": peak_src, "dtype": "fp64 (DMMA m8n8k4)",
+            "cd_share_of_step": float(np.mean(cd_ms)) / (tot_ms / args.steps),
+            "algorithmic": "2n flops per coordinate update"}
+    # e2e through the host C-ABI entry point (pinned host buffers)
+    e2e = None
+    if not args.no_e2e:
+        c0, c1 = D.column_range(p, rank, world) if world > 1 else (0, p)
+        Xh = torch.from_numpy(np.ascontiguousarray(X.T)).pin_memory()   # col-major X
+        if world == 1:
+            Th = torch.empty((p, p), dtype=torch.float64).pin_memory()
+            sh = torch.empty(p, dtype=torch.float64).pin_memory()
+            ih = torch.empty(p, dtype=torch.int32).pin_memory()
+            import ctypes
+            L = S.load()
+            o = S.default_options()
+
+            def e2e_step():
+                rc = L.spmesl_fit_ex(ctypes.c_void_p(Xh.data_ptr()), n, p, lam, TOL, MAX_ITER,
+                                     ctypes.byref(o), ctypes.c_void_p(Th.data_ptr()),
+                                     ctypes.c_void_p(sh.data_ptr()),
+                                     ctypes.c_void_p(ih.data_ptr()), None, None, None)
+                assert rc >= 0, L.spmesl_last_error()
+            h2d, d2h = 8 * n * p, 8 * p * p + 8 * p + 4 * p
+        else:
+            m = c1 - c0
+            Th = torch.empty((m, p), dtype=torch.float64).pin_memory()
+            sh = torch.empty(m, dtype=torch.float64).pin_memory()
+            ih = torch.empty(m, dtype=torch.int32).pin_memory()
+
+            def e2e_step():
+                Xg = Xh.to(dev, non_blocking=True).t()
+                r = D.fit_distributed(Xg, lam, TOL, MAX_ITER, stream=stream)
+                Th.copy_(r["theta"].t(), non_blocking=True)
+                sh.copy_(r["sigma"], non_blocking=True)
+                ih.copy_(r["iters"], non_blocking=True)
+                torch.cuda.synchronize()
+            h2d, d2h = 8 * n * p, 8 * m * p + 8 * m + 4 * m
+        for _ in range(2):
+            e2e_step()
+        e_ms = []
+        for k in range(max(1, min(args.steps, 3))):
+            flush.fill_(k)
+            torch.cuda.synchronize()
+            barrier()
+            t0 = time.perf_counter()
+            e2e_step()
+            torch.cuda.synchronize()
+            e_ms.append(1000 * (time.perf_counter() - t0))
+            barrier()
+        e_tot = float(np.mean(e_ms))
+        if dist:
+            t = torch.tensor([e_tot], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_tot = float(t[0])
+        e2e = {"value": upd_per_step / (e_tot / 1000.0), "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e_tot,
+               "api": "spmesl_fit_ex (host pointers)" if world == 1 else
+                      "fit_distributed with host pinned H2D/D2H"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(X, lam, args.cpu_seconds)
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
+                "fit_time_s": tot_ms / args.steps / 1000.0, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": config_dict(spec, world, lam, {
+                    "sweeps_total": stats_last["total_sweeps"],
+                    "max_sweeps": stats_last["max_sweeps"], "max_outer": stats_last["max_outer"],
+                    "nnz": stats_last["nnz"], "tile_cols": stats_last["tile_cols"],
+                    "num_ctas": stats_last["num_ctas"]}),
+                "roofline": roof, "clocks": clk.summary(), "e2e": e2e,
+                "gpu_launches": int(stats_last["kernel_launches"]) * args.steps,
+                "ms_breakdown": {"standardize": stats_last["ms_standardize"],
+                                 "cd": stats_last["ms_cd"], "assemble": stats_last["ms_assemble"]}}
+        if cpu:
+            line["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

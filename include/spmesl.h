@@ -1,0 +1,165 @@
+/*
+ * spmesl.h — C ABI of the B200-native SPMESL hot path.
+ *
+ * SPMESL (sparse precision matrix estimation via the scaled lasso), as computed by the
+ * column-parallel coordinate descent of arXiv 2203.15031 (PAPER.md lines cited as P:<n>):
+ *
+ *   for every column k (Eq. spmesl):
+ *     (b_k, sigma_k) = argmin ||x_k - X b||^2/(2 n sigma) + sigma/2 + lambda0 ||b||_1,  b_kk = 0
+ *   solved by Algorithm 1 per column (inner CD sweeps j = 1..p ascending with
+ *   a_j = x_j^T e / n + b_j, b_j <- Soft_{sigma lambda0}(a_j), inner stop
+ *   max_j |db_j| < tol, sigma refit ||e||_2/sqrt(n) and outer stop |dsigma| < tol
+ *   ); all columns advance together row by row (Proposition 2);
+ *   then Theta1_jk = -b_jk / sigma_k^2, Theta1_kk = 1/sigma_k^2 (Eq. relation P:268-272,
+ *   Alg. 2), Proposition 1 rescaling to the data's scale, and the
+ *   minimum-magnitude symmetrization of Eq. (symm) (Alg. 2).
+ *
+ * Conventions (all entry points):
+ *   - X is n x p, COLUMN-MAJOR, fp64, leading dimension n (column x_k contiguous).
+ *   - Theta is p x p, column-major, fp64, leading dimension p.  It is symmetric on return
+ *     unless opt->symmetrize == 0 (then Theta holds Theta1, the assembled and rescaled
+ *     but unsymmetrized estimate).
+ *   - sigma[p] is on the scale of the input data (sigma_k^o = s_k sigma_k^C) when
+ *     opt->standardize == 1 (default); iters[p] = outer iterations r per column;
+ *     sweeps[p] = inner CD sweeps summed over all outer iterations; converged[p] = 1 iff
+ *     the column met |dsigma| < tol before max_iter and no inner loop hit max_inner.
+ *   - Every pointer is caller-owned and never retained after return.  The library
+ *     allocates its device scratch per device and reuses it across calls
+ *     (spmesl_release_workspace frees it).  Calls on one device are serialised.
+ *   - Return codes below.  On a negative code the contents of output buffers are
+ *     unspecified (the host entry points leave host outputs untouched); the message is
+ *     available from spmesl_last_error() (thread-local).
+ *   - Paper-silent points follow the readings listed in DESIGN.md §3 (tolerances are
+ *     absolute; the residual is recomputed at each outer boundary; sigma floor; the
+ *     (j,k), j<k entry wins a symmetrization tie; constant columns are an error).
+ */
+#ifndef SPMESL_H
+#define SPMESL_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPMESL_OK                   0
+#define SPMESL_WARN_NOT_CONVERGED   1   /* outputs valid; >= 1 column hit max_iter or max_inner */
+#define SPMESL_ERR_ARG             -1   /* n < 2, p < 2, lambda0 < 0 or non-finite, tol <= 0,
+                                           max_iter < 1, NULL pointer, bad column range */
+#define SPMESL_ERR_CONSTANT_COLUMN -2   /* s_k <= 1e-13 max_i |x_ik|; index in stats->bad_column */
+#define SPMESL_ERR_NONFINITE       -3   /* NaN/Inf in X; column index in stats->bad_column */
+#define SPMESL_ERR_CUDA            -4   /* CUDA runtime error (message in spmesl_last_error) */
+#define SPMESL_ERR_OOM             -6   /* device allocation failed (or p*p*8 overflows) */
+#define SPMESL_ERR_UNSUPPORTED     -7   /* n too large for the on-chip residual tile (n > 2688),
+                                           or no sm_100 device */
+
+typedef struct {
+  int32_t struct_size;    /* sizeof(spmesl_options); set by spmesl_default_options */
+  int32_t max_inner;      /* cap on inner sweeps per outer iteration (default 10000) */
+  int32_t standardize;    /* 1: centre + scale columns inside and return Theta and
+                             sigma on the input scale (Prop. 1); 0: X is used as given */
+  int32_t symmetrize;     /* 1 (default): Eq. (symm); 0: return Theta1 */
+  double  sigma_floor;    /* sigma_k >= sigma_floor (default 1e-8; reading g5) */
+  int32_t mode;           /* 0: per-column stop (Alg. 1/2 semantics) — the only mode so far */
+  int32_t tile_cols;      /* 0: auto; 8, 16 or 32 resident columns per SM (tests) */
+  int32_t device;         /* host entry points: CUDA device ordinal (-1: current device) */
+  int32_t reserved[9];
+} spmesl_options;
+
+typedef struct {
+  int64_t coord_updates;  /* algorithmic coordinate updates V = sum_k sweeps_k (p - 1) */
+  int64_t total_sweeps;   /* sum_k sweeps_k */
+  int32_t max_sweeps;     /* max_k sweeps_k */
+  int32_t max_outer;      /* max_k iters_k */
+  int32_t n_unconverged;  /* columns with converged_k == 0 */
+  int32_t tile_cols;      /* resident columns per CTA actually used */
+  int32_t num_ctas;       /* persistent CTAs launched by the CD kernel */
+  int32_t kernel_launches;/* kernels launched by this call (excluding memsets/copies) */
+  int64_t bad_column;     /* column index for SPMESL_ERR_CONSTANT_COLUMN / _NONFINITE, else -1 */
+  int64_t nnz;            /* nonzero off-diagonal coefficients b_jk over the fitted columns */
+  double  ms_standardize; /* device time of standardization + Gram band (CUDA events) */
+  double  ms_cd;          /* device time of the persistent CD kernel */
+  double  ms_assemble;    /* device time of assembly + symmetrization (incl. CSC build) */
+  double  ms_total;       /* device time of the whole call on the stream */
+} spmesl_stats;
+
+/* Fill *opt with the defaults listed above. */
+void spmesl_default_options(spmesl_options* opt);
+
+/*
+ * Host-memory entry point (BASELINE.json: spmesl_fit(X, n, p, lambda0, tol, max_iter ->
+ * Theta, sigma, iters)).  X: host n x p; Theta: host p x p; sigma: host [p]; iters: host [p].
+ * Copies X to the current device, runs the whole path there and copies the results back.
+ * Host buffers may be pageable or pinned (pinned is faster).  Blocking.
+ */
+int spmesl_fit(const double* X, int64_t n, int64_t p, double lambda0, double tol,
+               int32_t max_iter, double* Theta, double* sigma, int32_t* iters);
+
+/* As spmesl_fit with options, optional per-column sweeps[p] / converged[p] (nullable) and
+ * optional statistics (nullable). */
+int spmesl_fit_ex(const double* X, int64_t n, int64_t p, double lambda0, double tol,
+                  int32_t max_iter, const spmesl_options* opt, double* Theta, double* sigma,
+                  int32_t* iters, int32_t* sweeps, uint8_t* converged, spmesl_stats* st);
+
+/*
+ * Device-memory entry point: every array pointer is a device pointer on the current
+ * device (e.g. a torch tensor's data_ptr()); work is enqueued on cuda_stream (a
+ * cudaStream_t; NULL = legacy default stream).  dSweeps / dConverged nullable.
+ * Blocking: returns after the work completes (it must read the error flags).
+ */
+int spmesl_fit_device(const double* dX, int64_t n, int64_t p, double lambda0, double tol,
+                      int32_t max_iter, const spmesl_options* opt, double* dTheta,
+                      double* dSigma, int32_t* dIters, int32_t* dSweeps, uint8_t* dConverged,
+                      void* cuda_stream, spmesl_stats* st);
+
+/*
+ * Multi-GPU building blocks (one process per GPU; columns [col_begin, col_end) on this rank,
+ * X replicated; BASELINE.json north_star "column-block sharding ... one all-gather").
+ *
+ * spmesl_fit_columns_device: standardize X (all p columns, needed as predictors), solve the
+ *   scaled lassos of columns [col_begin, col_end) and export them as CSC on the device:
+ *   dColCount[m] (m = col_end - col_begin) = nonzeros of column k (off-diagonal b_jk != 0),
+ *   dRows/dVals (capacity `cap` entries, caller-allocated) hold the entries of all m columns
+ *   concatenated in column order, rows ascending within a column; dSigmaStd[m] = sigma_k on
+ *   the standardized scale; dScale[p] = s_k (column scales, 1 when standardize == 0).
+ *   *nnz_out = total entries; if it exceeds cap, returns SPMESL_ERR_ARG and *nnz_out holds the
+ *   capacity needed.  Blocking.
+ *
+ * spmesl_assemble_device: from the GLOBAL CSC of all p columns (dColPtr[p+1], dRows, dVals),
+ *   dSigmaStd[p] and dScale[p], write columns [col_begin, col_end) of Theta (symmetrized or
+ *   Theta1 as opt->symmetrize says) into dTheta (p x (col_end-col_begin), ld p) and
+ *   dSigmaOut[col_end-col_begin] = s_k sigma_k.  Enqueued on cuda_stream, non-blocking.
+ */
+int spmesl_fit_columns_device(const double* dX, int64_t n, int64_t p, int64_t col_begin,
+                              int64_t col_end, double lambda0, double tol, int32_t max_iter,
+                              const spmesl_options* opt, int32_t* dColCount, int32_t* dRows,
+                              double* dVals, int64_t cap, int64_t* nnz_out, double* dSigmaStd,
+                              double* dScale, int32_t* dIters, int32_t* dSweeps,
+                              uint8_t* dConverged, void* cuda_stream, spmesl_stats* st);
+
+int spmesl_assemble_device(int64_t p, int64_t col_begin, int64_t col_end, const int64_t* dColPtr,
+                           const int32_t* dRows, const double* dVals, const double* dSigmaStd,
+                           const double* dScale, const spmesl_options* opt, double* dTheta,
+                           double* dSigmaOut, void* cuda_stream);
+
+/* Penalty levels of §2.2 (host helpers, not on the device path):
+ *   lambda_univ = sqrt(2 log(p-1) / n)
+ *   lambda_ub   = A sqrt(4 log p / n)
+ *   lambda_pb   = A Phi^{-1}(1 - k/p) / sqrt(n),  k = L_1^4(k/p) + 2 L_1^2(k/p)
+ * Return NaN on invalid arguments. */
+double spmesl_lambda_univ(int64_t n, int64_t p);
+double spmesl_lambda_ub(int64_t n, int64_t p, double A);
+double spmesl_lambda_pb(int64_t n, int64_t p, double A);
+double spmesl_solve_k(int64_t p);
+
+/* Thread-local message for the last non-OK return on this thread. */
+const char* spmesl_last_error(void);
+/* Free the cached device workspaces of all devices.  Returns SPMESL_OK. */
+int spmesl_release_workspace(void);
+/* Library version string. */
+const char* spmesl_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPMESL_H */

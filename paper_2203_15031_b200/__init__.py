@@ -1,0 +1,189 @@
+"""B200-native SPMESL hot path (arXiv 2203.15031): Python binding of libspmesl.so.
+
+Every step of the path runs in the CUDA kernels behind the C ABI (include/spmesl.h); this
+module only marshals arguments (numpy host arrays or torch CUDA tensors) and names the
+results.  There is no CPU fallback: without the built library every call raises.
+
+Public API (same names as the C ABI):
+    fit(X, lambda0, tol, max_iter, ...)          host arrays in/out   -> FitResult
+    fit_device(X, lambda0, tol, max_iter, ...)   torch CUDA tensors   -> FitResult (tensors)
+    fit_columns_device / assemble_device         multi-GPU building blocks (see distributed.py)
+    lambda_univ / lambda_ub / lambda_pb / solve_k  penalty levels
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Any
+
+import numpy as np
+
+from . import _lib
+from ._lib import SpmeslError, Stats, default_options, load  # noqa: F401
+
+__all__ = ["fit", "fit_device", "fit_columns_device", "assemble_device", "lambda_univ",
+           "lambda_ub", "lambda_pb", "solve_k", "FitResult", "SpmeslError", "load",
+           "release_workspace", "version"]
+
+
+@dataclass
+class FitResult:
+    code: int
+    Theta: Any            # p x p (numpy Fortran array or torch tensor view, column-major)
+    sigma: Any
+    iters: Any
+    sweeps: Any
+    converged: Any
+    stats: dict = field(default_factory=dict)
+
+
+def _vp(a) -> ctypes.c_void_p:
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return ctypes.c_void_p(a.ctypes.data)
+    return ctypes.c_void_p(a.data_ptr())
+
+
+def _opts(max_inner=10000, standardize=True, symmetrize=True, sigma_floor=1e-8, tile_cols=0,
+          device=-1) -> _lib.Options:
+    return default_options(max_inner=int(max_inner), standardize=int(bool(standardize)),
+                           symmetrize=int(bool(symmetrize)), sigma_floor=float(sigma_floor),
+                           tile_cols=int(tile_cols), device=int(device))
+
+
+def fit(X, lambda0: float, tol: float = 1e-4, max_iter: int = 100, *, out_theta=None,
+        **options) -> FitResult:
+    """spmesl_fit_ex on host memory.  X: n x p (any numpy layout; copied to column-major)."""
+    X = np.asfortranarray(np.asarray(X, dtype=np.float64))
+    n, p = X.shape
+    Theta = out_theta if out_theta is not None else np.empty((p, p), order="F")
+    sigma = np.empty(p)
+    iters = np.empty(p, np.int32)
+    sweeps = np.empty(p, np.int32)
+    conv = np.empty(p, np.uint8)
+    st = Stats()
+    o = _opts(**options)
+    rc = load().spmesl_fit_ex(_vp(X), n, p, float(lambda0), float(tol), int(max_iter),
+                              ctypes.byref(o), _vp(Theta), _vp(sigma), _vp(iters), _vp(sweeps),
+                              _vp(conv), ctypes.byref(st))
+    _lib.check(rc, st)
+    return FitResult(rc, Theta, sigma, iters, sweeps, conv.astype(bool), st.asdict())
+
+
+def as_colmajor(X):
+    """torch (n, p) tensor -> same values with column-major (Fortran) strides."""
+    if X.dim() != 2:
+        raise ValueError("X must be 2-D")
+    if X.stride(0) == 1 and X.stride(1) == X.shape[0]:
+        return X
+    return X.t().contiguous().t()
+
+
+def fit_device(X, lambda0: float, tol: float = 1e-4, max_iter: int = 100, *, stream=None,
+               out=None, **options) -> FitResult:
+    """spmesl_fit_device on torch CUDA tensors.  X: (n, p) float64 on the current device."""
+    import torch
+    if not X.is_cuda or X.dtype != torch.float64:
+        raise TypeError("X must be a float64 CUDA tensor")
+    X = as_colmajor(X)
+    n, p = X.shape
+    dev = X.device
+    if out is None:
+        out = dict(
+            theta=torch.empty((p, p), dtype=torch.float64, device=dev),
+            sigma=torch.empty(p, dtype=torch.float64, device=dev),
+            iters=torch.empty(p, dtype=torch.int32, device=dev),
+            sweeps=torch.empty(p, dtype=torch.int32, device=dev),
+            conv=torch.empty(p, dtype=torch.uint8, device=dev))
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    st = Stats()
+    o = _opts(**options)
+    with torch.cuda.device(dev):
+        rc = load().spmesl_fit_device(_vp(X), n, p, float(lambda0), float(tol), int(max_iter),
+                                      ctypes.byref(o), _vp(out["theta"]), _vp(out["sigma"]),
+                                      _vp(out["iters"]), _vp(out["sweeps"]), _vp(out["conv"]),
+                                      ctypes.c_void_p(s.cuda_stream), ctypes.byref(st))
+    _lib.check(rc, st)
+    # the buffer holds Theta column-major: element (j, k) at j + k p -> view as its transpose
+    return FitResult(rc, out["theta"].t(), out["sigma"], out["iters"], out["sweeps"],
+                     out["conv"].bool(), st.asdict())
+
+
+def fit_columns_device(X, col_begin: int, col_end: int, lambda0: float, tol: float = 1e-4,
+                       max_iter: int = 100, *, stream=None, cap=None, **options):
+    """spmesl_fit_columns_device: CSC coefficients of columns [col_begin, col_end)."""
+    import torch
+    X = as_colmajor(X)
+    n, p = X.shape
+    m = col_end - col_begin
+    dev = X.device
+    if cap is None:
+        cap = m * min(p, ((n + 31) // 32) * 32 + 64)
+    counts = torch.empty(m, dtype=torch.int32, device=dev)
+    rows = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+    vals = torch.empty(max(cap, 1), dtype=torch.float64, device=dev)
+    sigma_std = torch.empty(m, dtype=torch.float64, device=dev)
+    scale = torch.empty(p, dtype=torch.float64, device=dev)
+    iters = torch.empty(m, dtype=torch.int32, device=dev)
+    sweeps = torch.empty(m, dtype=torch.int32, device=dev)
+    conv = torch.empty(m, dtype=torch.uint8, device=dev)
+    nnz = ctypes.c_int64(0)
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    st = Stats()
+    o = _opts(**options)
+    with torch.cuda.device(dev):
+        rc = load().spmesl_fit_columns_device(
+            _vp(X), n, p, col_begin, col_end, float(lambda0), float(tol), int(max_iter),
+            ctypes.byref(o), _vp(counts), _vp(rows), _vp(vals), cap, ctypes.byref(nnz),
+            _vp(sigma_std), _vp(scale), _vp(iters), _vp(sweeps), _vp(conv),
+            ctypes.c_void_p(s.cuda_stream), ctypes.byref(st))
+    _lib.check(rc, st)
+    k = nnz.value
+    return dict(code=rc, counts=counts, rows=rows[:k], vals=vals[:k], sigma_std=sigma_std,
+                scale=scale, iters=iters, sweeps=sweeps, converged=conv.bool(),
+                stats=st.asdict())
+
+
+def assemble_device(p: int, col_begin: int, col_end: int, col_ptr, rows, vals, sigma_std, scale,
+                    *, stream=None, out_theta=None, out_sigma=None, **options):
+    """spmesl_assemble_device: columns [col_begin, col_end) of Theta from the global CSC."""
+    import torch
+    dev = col_ptr.device
+    m = col_end - col_begin
+    theta = out_theta if out_theta is not None else torch.empty((m, p), dtype=torch.float64,
+                                                                device=dev)
+    sig = out_sigma if out_sigma is not None else torch.empty(m, dtype=torch.float64, device=dev)
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    o = _opts(**options)
+    with torch.cuda.device(dev):
+        rc = load().spmesl_assemble_device(p, col_begin, col_end, _vp(col_ptr), _vp(rows),
+                                           _vp(vals), _vp(sigma_std), _vp(scale),
+                                           ctypes.byref(o), _vp(theta), _vp(sig),
+                                           ctypes.c_void_p(s.cuda_stream))
+    _lib.check(rc)
+    return theta.t(), sig   # (p, m) column block, column-major
+
+
+def lambda_univ(n: int, p: int) -> float:
+    return load().spmesl_lambda_univ(n, p)
+
+
+def lambda_ub(n: int, p: int, A: float = 1.0) -> float:
+    return load().spmesl_lambda_ub(n, p, A)
+
+
+def lambda_pb(n: int, p: int, A: float = 2 ** 0.5) -> float:
+    return load().spmesl_lambda_pb(n, p, A)
+
+
+def solve_k(p: int) -> float:
+    return load().spmesl_solve_k(p)
+
+
+def release_workspace() -> int:
+    return load().spmesl_release_workspace()
+
+
+def version() -> str:
+    return load().spmesl_version().decode()

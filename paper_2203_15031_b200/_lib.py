@@ -1,0 +1,135 @@
+"""ctypes binding of libspmesl.so (include/spmesl.h).  Argument marshalling only.
+
+The library must exist in-tree (built by ``paper_2203_15031_b200.build`` /
+``__graft_entry__.build()``); there is no fallback of any kind: a missing library raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libspmesl.so")
+
+OK = 0
+WARN_NOT_CONVERGED = 1
+ERR_ARG = -1
+ERR_CONSTANT_COLUMN = -2
+ERR_NONFINITE = -3
+ERR_CUDA = -4
+ERR_OOM = -6
+ERR_UNSUPPORTED = -7
+
+
+class Options(ctypes.Structure):
+    _fields_ = [
+        ("struct_size", ctypes.c_int32),
+        ("max_inner", ctypes.c_int32),
+        ("standardize", ctypes.c_int32),
+        ("symmetrize", ctypes.c_int32),
+        ("sigma_floor", ctypes.c_double),
+        ("mode", ctypes.c_int32),
+        ("tile_cols", ctypes.c_int32),
+        ("device", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 9),
+    ]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [
+        ("coord_updates", ctypes.c_int64),
+        ("total_sweeps", ctypes.c_int64),
+        ("max_sweeps", ctypes.c_int32),
+        ("max_outer", ctypes.c_int32),
+        ("n_unconverged", ctypes.c_int32),
+        ("tile_cols", ctypes.c_int32),
+        ("num_ctas", ctypes.c_int32),
+        ("kernel_launches", ctypes.c_int32),
+        ("bad_column", ctypes.c_int64),
+        ("nnz", ctypes.c_int64),
+        ("ms_standardize", ctypes.c_double),
+        ("ms_cd", ctypes.c_double),
+        ("ms_assemble", ctypes.c_double),
+        ("ms_total", ctypes.c_double),
+    ]
+
+    def asdict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+EXPORTS = [
+    "spmesl_default_options", "spmesl_fit", "spmesl_fit_ex", "spmesl_fit_device",
+    "spmesl_fit_columns_device", "spmesl_assemble_device", "spmesl_lambda_univ",
+    "spmesl_lambda_ub", "spmesl_lambda_pb", "spmesl_solve_k", "spmesl_last_error",
+    "spmesl_release_workspace", "spmesl_version",
+]
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libspmesl.so (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: build it with `python -m "
+                           "paper_2203_15031_b200.build` (no CPU fallback exists)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i64, i32, dbl = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double
+    popt = ctypes.POINTER(Options)
+    pst = ctypes.POINTER(Stats)
+    L.spmesl_default_options.argtypes = [popt]
+    L.spmesl_default_options.restype = None
+    L.spmesl_fit.argtypes = [vp, i64, i64, dbl, dbl, i32, vp, vp, vp]
+    L.spmesl_fit.restype = ctypes.c_int
+    L.spmesl_fit_ex.argtypes = [vp, i64, i64, dbl, dbl, i32, popt, vp, vp, vp, vp, vp, pst]
+    L.spmesl_fit_ex.restype = ctypes.c_int
+    L.spmesl_fit_device.argtypes = [vp, i64, i64, dbl, dbl, i32, popt, vp, vp, vp, vp, vp, vp, pst]
+    L.spmesl_fit_device.restype = ctypes.c_int
+    L.spmesl_fit_columns_device.argtypes = [vp, i64, i64, i64, i64, dbl, dbl, i32, popt, vp, vp,
+                                            vp, i64, ctypes.POINTER(i64), vp, vp, vp, vp, vp, vp,
+                                            pst]
+    L.spmesl_fit_columns_device.restype = ctypes.c_int
+    L.spmesl_assemble_device.argtypes = [i64, i64, i64, vp, vp, vp, vp, vp, popt, vp, vp, vp]
+    L.spmesl_assemble_device.restype = ctypes.c_int
+    for f in ("spmesl_lambda_univ",):
+        getattr(L, f).argtypes = [i64, i64]
+        getattr(L, f).restype = dbl
+    for f in ("spmesl_lambda_ub", "spmesl_lambda_pb"):
+        getattr(L, f).argtypes = [i64, i64, dbl]
+        getattr(L, f).restype = dbl
+    L.spmesl_solve_k.argtypes = [i64]
+    L.spmesl_solve_k.restype = dbl
+    L.spmesl_last_error.argtypes = []
+    L.spmesl_last_error.restype = ctypes.c_char_p
+    L.spmesl_release_workspace.restype = ctypes.c_int
+    L.spmesl_version.restype = ctypes.c_char_p
+    _lib = L
+    return L
+
+
+def default_options(**kw) -> Options:
+    o = Options()
+    load().spmesl_default_options(ctypes.byref(o))
+    for k, v in kw.items():
+        if v is None:
+            continue
+        if not hasattr(o, k):
+            raise TypeError(f"unknown option {k}")
+        setattr(o, k, v)
+    return o
+
+
+class SpmeslError(RuntimeError):
+    def __init__(self, code: int, msg: str, bad_column: int = -1):
+        super().__init__(f"spmesl error {code}: {msg}")
+        self.code = code
+        self.bad_column = bad_column
+
+
+def check(rc: int, stats: Stats | None = None) -> int:
+    if rc < 0:
+        msg = load().spmesl_last_error().decode()
+        raise SpmeslError(rc, msg, stats.bad_column if stats is not None else -1)
+    return rc

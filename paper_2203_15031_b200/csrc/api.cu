@@ -1,0 +1,549 @@
+// Host orchestration and C ABI (include/spmesl.h).  Validation, per-device cached
+// workspace, kernel sequencing on the caller's stream, error/stat readback.
+//
+// Device sequence of one fit:
+//   memset scratch -> standardize_kernel (a2) -> gram_kernel -> cd_sweep_kernel (a3-a7)
+//   -> csc_scan + csc_copy -> memset Theta + assemble_entries + assemble_diag (a8, a10)
+//   -> one 64-byte readback of flags/counters.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "spmesl.h"
+#include "spmesl_internal.cuh"
+
+using namespace spmesl;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                     \
+  do {                                                                                     \
+    cudaError_t e_ = (expr);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail(e_ == cudaErrorMemoryAllocation ? SPMESL_ERR_OOM : SPMESL_ERR_CUDA,      \
+                  std::string(#expr) + ": " + cudaGetErrorString(e_));                     \
+  } while (0)
+
+// Device counters written by the kernels and read back once per call.
+struct DevCounters {
+  int err;                      // standardization error seen
+  int overflow;                 // a coefficient list exceeded nzcap
+  int pad[2];
+  unsigned long long bad_key;   // 2*col + (0 nonfinite | 1 constant)
+  int64_t csc_total;
+};
+
+struct Buffer {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+int ensure(Buffer& b, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (b.bytes >= bytes) return SPMESL_OK;
+  if (b.ptr) cudaFree(b.ptr);
+  b.ptr = nullptr;
+  b.bytes = 0;
+  cudaError_t e = cudaMalloc(&b.ptr, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(SPMESL_ERR_OOM, "cudaMalloc(" + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+  }
+  b.bytes = bytes;
+  return SPMESL_OK;
+}
+
+struct Workspace {
+  std::mutex mu;
+  int device = -1;
+  int sms = 0;
+  int smem_optin = 0;
+  int cc_major = 0;
+  Buffer xb, gband, mean, scale, counters, queue, sigma_std, iters, sweeps, conv, nz_count, nz_cur,
+      nz_rows, nz_vals, col_ptr, csc_rows, csc_vals;
+  // host-API staging
+  Buffer hx, htheta, hsigma, hiters, hsweeps, hconv;
+  DevCounters* host_counters = nullptr;   // pinned
+  cudaEvent_t ev[6] = {};
+  bool init = false;
+};
+
+std::mutex g_ws_mu;
+std::vector<Workspace*> g_ws;
+
+Workspace* workspace_for(int dev) {
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  if ((int)g_ws.size() <= dev) g_ws.resize(dev + 1, nullptr);
+  if (!g_ws[dev]) g_ws[dev] = new Workspace();
+  return g_ws[dev];
+}
+
+int ws_init(Workspace& W, int dev) {
+  if (W.init) return SPMESL_OK;
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, dev));
+  W.device = dev;
+  W.sms = prop.multiProcessorCount;
+  W.smem_optin = (int)prop.sharedMemPerBlockOptin;
+  W.cc_major = prop.major;
+  CUDA_TRY(cudaMallocHost((void**)&W.host_counters, sizeof(DevCounters)));
+  for (auto& e : W.ev) CUDA_TRY(cudaEventCreate(&e));
+  W.init = true;
+  return SPMESL_OK;
+}
+
+int validate(const void* X, int64_t n, int64_t p, double lambda0, double tol, int32_t max_iter,
+             const spmesl_options& o) {
+  if (!X) return fail(SPMESL_ERR_ARG, "X is NULL");
+  if (n < 2) return fail(SPMESL_ERR_ARG, "n must be >= 2");
+  if (p < 2) return fail(SPMESL_ERR_ARG, "p must be >= 2");
+  if (p > (int64_t)0x7fffffff) return fail(SPMESL_ERR_ARG, "p must be < 2^31");
+  if (!(lambda0 >= 0.0) || !std::isfinite(lambda0)) return fail(SPMESL_ERR_ARG, "lambda0 must be finite and >= 0");
+  if (!(tol > 0.0) || !std::isfinite(tol)) return fail(SPMESL_ERR_ARG, "tol must be finite and > 0");
+  if (max_iter < 1) return fail(SPMESL_ERR_ARG, "max_iter must be >= 1");
+  if (o.max_inner < 1) return fail(SPMESL_ERR_ARG, "max_inner must be >= 1");
+  if (!(o.sigma_floor > 0.0)) return fail(SPMESL_ERR_ARG, "sigma_floor must be > 0");
+  if (o.mode != 0) return fail(SPMESL_ERR_ARG, "only mode 0 (per-column stop) is implemented");
+  if (o.tile_cols != 0 && o.tile_cols != 8 && o.tile_cols != 16 && o.tile_cols != 32)
+    return fail(SPMESL_ERR_ARG, "tile_cols must be 0, 8, 16 or 32");
+  const double pp = (double)p * (double)p * 8.0;
+  if (pp > 9.0e18) return fail(SPMESL_ERR_OOM, "p*p*8 overflows");
+  return SPMESL_OK;
+}
+
+spmesl_options resolve(const spmesl_options* opt) {
+  spmesl_options o;
+  spmesl_default_options(&o);
+  if (opt) {
+    if (opt->struct_size != (int32_t)sizeof(spmesl_options)) {
+      // tolerate older/newer callers by copying the common prefix
+      size_t m = opt->struct_size > 0 ? std::min((size_t)opt->struct_size, sizeof(o)) : sizeof(o);
+      std::memcpy(&o, opt, m);
+      o.struct_size = sizeof(o);
+    } else {
+      o = *opt;
+    }
+  }
+  return o;
+}
+
+int choose_T(const Workspace& W, int64_t ncols, int n_pad, int requested) {
+  const int cands[3] = {32, 16, 8};
+  int fallback = 0;
+  for (int T : cands) {
+    if (requested && T != requested) continue;
+    if (cd_smem_bytes(T, n_pad) > (size_t)W.smem_optin) continue;
+    if (!fallback) fallback = T;
+    if (requested || (ncols + T - 1) / T >= W.sms || T == 8) return T;
+  }
+  return fallback;
+}
+
+struct FitOut {
+  int64_t col_begin, col_end;
+  double* sigma_std;
+  int32_t* iters;
+  int32_t* sweeps;
+  uint8_t* conv;
+};
+
+// Core: standardize + gram + CD for columns [cb, ce) on stream s.  Leaves the coefficient
+// lists in the workspace (nz_*), per-column results in `out`.  Returns after enqueueing.
+int run_cd(Workspace& W, const double* dX, int64_t n, int64_t p, int64_t cb, int64_t ce,
+           double lambda0, double tol, int32_t max_iter, const spmesl_options& o, int nzcap,
+           const FitOut& out, cudaStream_t s, int T, Layout& L, int* num_ctas) {
+  const int64_t m = ce - cb;
+  CUDA_TRY(cudaMemsetAsync(W.xb.ptr, 0, L.xb_doubles() * 8, s));
+  CUDA_TRY(cudaMemsetAsync(W.counters.ptr, 0, sizeof(DevCounters), s));
+  CUDA_TRY(cudaMemsetAsync((char*)W.counters.ptr + offsetof(DevCounters, bad_key), 0xff, 8, s));
+  CUDA_TRY(cudaMemsetAsync(W.queue.ptr, 0, 16, s));
+  CUDA_TRY(cudaMemsetAsync(W.nz_count.ptr, 0, sizeof(int) * (size_t)m, s));
+  CUDA_TRY(cudaMemsetAsync(W.nz_cur.ptr, 0, sizeof(int) * (size_t)m, s));
+  CUDA_TRY(cudaEventRecord(W.ev[0], s));
+  DevCounters* dc = (DevCounters*)W.counters.ptr;
+  CUDA_TRY(launch_standardize(dX, L, o.standardize, (double*)W.xb.ptr, (double*)W.mean.ptr,
+                              (double*)W.scale.ptr, &dc->err, &dc->bad_key, s));
+  CUDA_TRY(launch_gram((const double*)W.xb.ptr, L, (double*)W.gband.ptr, s));
+  CUDA_TRY(cudaEventRecord(W.ev[1], s));
+  CDParams P{};
+  P.Xb = (const double*)W.xb.ptr;
+  P.Gband = (const double*)W.gband.ptr;
+  P.n = (int)n;
+  P.n_pad = L.n_pad;
+  P.nchunk = L.nchunk;
+  P.p = (int)p;
+  P.nblk = (int)L.nblk;
+  P.col_begin = cb;
+  P.ncols = (int)m;
+  P.lambda0 = lambda0;
+  P.tol = tol;
+  P.sigma_floor = o.sigma_floor;
+  P.sqrt_n = std::sqrt((double)n);
+  P.max_outer = max_iter;
+  P.max_inner = o.max_inner;
+  P.T = T;
+  P.nzcap = nzcap;
+  P.queue = (int*)W.queue.ptr;
+  P.flags = &dc->err;   // FLAG_CODE (unused by CD), FLAG_OVERFLOW at +1
+  P.err_in = &dc->err;
+  P.nz_rows = (int*)W.nz_rows.ptr;
+  P.nz_vals = (double*)W.nz_vals.ptr;
+  P.nz_count = (int*)W.nz_count.ptr;
+  P.nz_cur = (int*)W.nz_cur.ptr;
+  P.sigma_std = out.sigma_std;
+  P.iters = out.iters;
+  P.sweeps = out.sweeps;
+  P.converged = out.conv;
+  const int ctas = (int)std::min<int64_t>(W.sms, (m + T - 1) / T);
+  *num_ctas = ctas;
+  CUDA_TRY(launch_cd(P, ctas, s));
+  CUDA_TRY(cudaEventRecord(W.ev[2], s));
+  return SPMESL_OK;
+}
+
+int alloc_core(Workspace& W, const Layout& L, int64_t m, int nzcap) {
+  int rc;
+  if ((rc = ensure(W.xb, L.xb_doubles() * 8))) return rc;
+  if ((rc = ensure(W.gband, (size_t)L.nblk * J * J * 8))) return rc;
+  if ((rc = ensure(W.mean, (size_t)L.p * 8))) return rc;
+  if ((rc = ensure(W.scale, (size_t)L.p * 8))) return rc;
+  if ((rc = ensure(W.counters, sizeof(DevCounters)))) return rc;
+  if ((rc = ensure(W.queue, 16))) return rc;
+  if ((rc = ensure(W.nz_count, (size_t)m * 4))) return rc;
+  if ((rc = ensure(W.nz_cur, (size_t)m * 4))) return rc;
+  if ((rc = ensure(W.nz_rows, (size_t)m * 2 * nzcap * 4))) return rc;
+  if ((rc = ensure(W.nz_vals, (size_t)m * 2 * nzcap * 8))) return rc;
+  if ((rc = ensure(W.col_ptr, (size_t)(m + 1) * 8))) return rc;
+  return SPMESL_OK;
+}
+
+int read_counters(Workspace& W, cudaStream_t s) {
+  CUDA_TRY(cudaMemcpyAsync(W.host_counters, W.counters.ptr, sizeof(DevCounters),
+                           cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return SPMESL_OK;
+}
+
+int std_error(Workspace& W, spmesl_stats* st) {
+  const unsigned long long key = W.host_counters->bad_key;
+  const int64_t col = (int64_t)(key >> 1);
+  if (st) st->bad_column = col;
+  if (key & 1ull)
+    return fail(SPMESL_ERR_CONSTANT_COLUMN, "constant column " + std::to_string(col));
+  return fail(SPMESL_ERR_NONFINITE, "non-finite value in column " + std::to_string(col));
+}
+
+int initial_nzcap(int64_t n, int64_t p) {
+  int64_t c = ((n + 31) / 32) * 32 + 64;
+  if (c > p) c = p;
+  if (c < 8) c = 8;
+  return (int)c;
+}
+
+// Per-column statistics (host side) from device arrays.
+int collect_stats(const int32_t* dIters, const int32_t* dSweeps, const uint8_t* dConv, int64_t m,
+                  int64_t p, cudaStream_t s, spmesl_stats* st, int* any_unconv) {
+  std::vector<int32_t> it(m), sw(m);
+  std::vector<uint8_t> cv(m);
+  CUDA_TRY(cudaMemcpyAsync(it.data(), dIters, 4 * m, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(sw.data(), dSweeps, 4 * m, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(cv.data(), dConv, m, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  int64_t tot = 0;
+  int mx = 0, mo = 0, nu = 0;
+  for (int64_t k = 0; k < m; ++k) {
+    tot += sw[k];
+    mx = std::max(mx, sw[k]);
+    mo = std::max(mo, it[k]);
+    nu += cv[k] ? 0 : 1;
+  }
+  *any_unconv = nu > 0;
+  if (st) {
+    st->total_sweeps = tot;
+    st->coord_updates = tot * (p - 1);
+    st->max_sweeps = mx;
+    st->max_outer = mo;
+    st->n_unconverged = nu;
+  }
+  return SPMESL_OK;
+}
+
+float ev_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) { cudaGetLastError(); return 0.f; }
+  return ms;
+}
+
+int current_device(int requested, int* dev) {
+  if (requested >= 0) CUDA_TRY(cudaSetDevice(requested));
+  CUDA_TRY(cudaGetDevice(dev));
+  return SPMESL_OK;
+}
+
+// Runs CD for [cb, ce) with automatic coefficient-list regrowth on overflow.
+int fit_columns_core(Workspace& W, const double* dX, int64_t n, int64_t p, int64_t cb, int64_t ce,
+                     double lambda0, double tol, int32_t max_iter, const spmesl_options& o,
+                     const FitOut& out, cudaStream_t s, spmesl_stats* st, Layout& L,
+                     int* nzcap_used) {
+  const int64_t m = ce - cb;
+  L.n = n;
+  L.p = p;
+  L.n_pad = (int)(((n + KC - 1) / KC) * KC);
+  L.nchunk = L.n_pad / KC;
+  L.nblk = (p + J - 1) / J;
+  const int T = choose_T(W, m, L.n_pad, o.tile_cols);
+  if (!T || cd_smem_bytes(T, L.n_pad) > (size_t)W.smem_optin)
+    return fail(SPMESL_ERR_UNSUPPORTED, "n = " + std::to_string(n) +
+                                            " does not fit the on-chip residual tile");
+  int nzcap = initial_nzcap(n, p);
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    int rc = alloc_core(W, L, m, nzcap);
+    if (rc) return rc;
+    int ctas = 0;
+    if ((rc = run_cd(W, dX, n, p, cb, ce, lambda0, tol, max_iter, o, nzcap, out, s, T, L, &ctas)))
+      return rc;
+    if ((rc = read_counters(W, s))) return rc;
+    if (W.host_counters->err) return std_error(W, st);
+    if (st) { st->tile_cols = T; st->num_ctas = ctas; }
+    if (!W.host_counters->overflow) { *nzcap_used = nzcap; return SPMESL_OK; }
+    if (nzcap >= p) break;
+    nzcap = (int)std::min<int64_t>(p, (int64_t)nzcap * 4);
+  }
+  return fail(SPMESL_ERR_OOM, "coefficient list overflow");
+}
+
+int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, double tol,
+                    int32_t max_iter, const spmesl_options& o, double* dTheta, double* dSigma,
+                    int32_t* dIters, int32_t* dSweeps, uint8_t* dConv, cudaStream_t s,
+                    spmesl_stats* st, Workspace& W) {
+  int rc;
+  if ((rc = ensure(W.sigma_std, (size_t)p * 8))) return rc;
+  if (!dSweeps) { if ((rc = ensure(W.sweeps, (size_t)p * 4))) return rc; dSweeps = (int32_t*)W.sweeps.ptr; }
+  if (!dConv) { if ((rc = ensure(W.conv, (size_t)p))) return rc; dConv = (uint8_t*)W.conv.ptr; }
+  FitOut out{0, p, (double*)W.sigma_std.ptr, dIters, dSweeps, dConv};
+  Layout L;
+  int nzcap = 0;
+  rc = fit_columns_core(W, dX, n, p, 0, p, lambda0, tol, max_iter, o, out, s, st, L, &nzcap);
+  if (rc) return rc;
+  const size_t cap = (size_t)p * (size_t)nzcap;
+  if ((rc = ensure(W.csc_rows, cap * 4))) return rc;
+  if ((rc = ensure(W.csc_vals, cap * 8))) return rc;
+  DevCounters* dc = (DevCounters*)W.counters.ptr;
+  CUDA_TRY(cudaEventRecord(W.ev[3], s));
+  CUDA_TRY(launch_csc_build((const int*)W.nz_count.ptr, (const int*)W.nz_cur.ptr,
+                            (const int*)W.nz_rows.ptr, (const double*)W.nz_vals.ptr, (int)p, nzcap,
+                            (int64_t*)W.col_ptr.ptr, (int32_t*)W.csc_rows.ptr,
+                            (double*)W.csc_vals.ptr, &dc->csc_total, s));
+  CUDA_TRY(launch_assemble(p, 0, p, (const int64_t*)W.col_ptr.ptr, (const int32_t*)W.csc_rows.ptr,
+                           (const double*)W.csc_vals.ptr, (const double*)W.sigma_std.ptr,
+                           o.standardize ? (const double*)W.scale.ptr : nullptr, o.symmetrize,
+                           dTheta, dSigma, s));
+  CUDA_TRY(cudaEventRecord(W.ev[4], s));
+  if ((rc = read_counters(W, s))) return rc;
+  int any_unconv = 0;
+  if ((rc = collect_stats(dIters, dSweeps, dConv, p, p, s, st, &any_unconv))) return rc;
+  if (st) {
+    st->nnz = W.host_counters->csc_total;
+    st->ms_standardize = ev_ms(W.ev[0], W.ev[1]);
+    st->ms_cd = ev_ms(W.ev[1], W.ev[2]);
+    st->ms_assemble = ev_ms(W.ev[3], W.ev[4]);
+    st->ms_total = ev_ms(W.ev[0], W.ev[4]);
+    st->kernel_launches = 7;   // standardize, gram, cd, csc_scan, csc_copy, assemble x2
+    st->bad_column = -1;
+  }
+  return any_unconv ? SPMESL_WARN_NOT_CONVERGED : SPMESL_OK;
+}
+
+void init_stats(spmesl_stats* st) {
+  if (st) { std::memset(st, 0, sizeof(*st)); st->bad_column = -1; }
+}
+
+}  // namespace
+
+extern "C" {
+
+void spmesl_default_options(spmesl_options* opt) {
+  if (!opt) return;
+  std::memset(opt, 0, sizeof(*opt));
+  opt->struct_size = sizeof(spmesl_options);
+  opt->max_inner = 10000;
+  opt->standardize = 1;
+  opt->symmetrize = 1;
+  opt->sigma_floor = 1e-8;
+  opt->mode = 0;
+  opt->tile_cols = 0;
+  opt->device = -1;
+}
+
+const char* spmesl_last_error(void) { return g_last_error.c_str(); }
+
+const char* spmesl_version(void) { return "spmesl-b200 0.1 (sm_100a)"; }
+
+int spmesl_release_workspace(void) {
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  int prev = -1;
+  cudaGetDevice(&prev);
+  for (auto*& w : g_ws) {
+    if (!w) continue;
+    std::lock_guard<std::mutex> lw(w->mu);
+    if (w->init) cudaSetDevice(w->device);
+    Buffer* bufs[] = {&w->xb, &w->gband, &w->mean, &w->scale, &w->counters, &w->queue,
+                      &w->sigma_std, &w->iters, &w->sweeps, &w->conv, &w->nz_count, &w->nz_cur,
+                      &w->nz_rows, &w->nz_vals, &w->col_ptr, &w->csc_rows, &w->csc_vals,
+                      &w->hx, &w->htheta, &w->hsigma, &w->hiters, &w->hsweeps, &w->hconv};
+    for (Buffer* b : bufs) { if (b->ptr) cudaFree(b->ptr); b->ptr = nullptr; b->bytes = 0; }
+    if (w->host_counters) cudaFreeHost(w->host_counters);
+    for (auto& e : w->ev) if (e) cudaEventDestroy(e);
+    w->init = false;
+  }
+  if (prev >= 0) cudaSetDevice(prev);
+  return SPMESL_OK;
+}
+
+int spmesl_fit_device(const double* dX, int64_t n, int64_t p, double lambda0, double tol,
+                      int32_t max_iter, const spmesl_options* opt, double* dTheta,
+                      double* dSigma, int32_t* dIters, int32_t* dSweeps, uint8_t* dConverged,
+                      void* cuda_stream, spmesl_stats* st) {
+  init_stats(st);
+  spmesl_options o = resolve(opt);
+  int rc = validate(dX, n, p, lambda0, tol, max_iter, o);
+  if (rc) return rc;
+  if (!dTheta || !dSigma || !dIters) return fail(SPMESL_ERR_ARG, "output pointer is NULL");
+  int dev;
+  if ((rc = current_device(-1, &dev))) return rc;
+  Workspace* W = workspace_for(dev);
+  std::lock_guard<std::mutex> lk(W->mu);
+  if ((rc = ws_init(*W, dev))) return rc;
+  if (W->cc_major < 10) return fail(SPMESL_ERR_UNSUPPORTED, "needs an sm_100 device");
+  return fit_device_impl(dX, n, p, lambda0, tol, max_iter, o, dTheta, dSigma, dIters, dSweeps,
+                         dConverged, (cudaStream_t)cuda_stream, st, *W);
+}
+
+int spmesl_fit_ex(const double* X, int64_t n, int64_t p, double lambda0, double tol,
+                  int32_t max_iter, const spmesl_options* opt, double* Theta, double* sigma,
+                  int32_t* iters, int32_t* sweeps, uint8_t* converged, spmesl_stats* st) {
+  init_stats(st);
+  spmesl_options o = resolve(opt);
+  int rc = validate(X, n, p, lambda0, tol, max_iter, o);
+  if (rc) return rc;
+  if (!Theta || !sigma || !iters) return fail(SPMESL_ERR_ARG, "output pointer is NULL");
+  int dev;
+  if ((rc = current_device(o.device, &dev))) return rc;
+  Workspace* W = workspace_for(dev);
+  std::lock_guard<std::mutex> lk(W->mu);
+  if ((rc = ws_init(*W, dev))) return rc;
+  if (W->cc_major < 10) return fail(SPMESL_ERR_UNSUPPORTED, "needs an sm_100 device");
+  const size_t np = (size_t)n * p, pp = (size_t)p * p;
+  if ((rc = ensure(W->hx, np * 8))) return rc;
+  if ((rc = ensure(W->htheta, pp * 8))) return rc;
+  if ((rc = ensure(W->hsigma, (size_t)p * 8))) return rc;
+  if ((rc = ensure(W->hiters, (size_t)p * 4))) return rc;
+  if ((rc = ensure(W->hsweeps, (size_t)p * 4))) return rc;
+  if ((rc = ensure(W->hconv, (size_t)p))) return rc;
+  cudaStream_t s = 0;
+  CUDA_TRY(cudaMemcpyAsync(W->hx.ptr, X, np * 8, cudaMemcpyHostToDevice, s));
+  rc = fit_device_impl((const double*)W->hx.ptr, n, p, lambda0, tol, max_iter, o,
+                       (double*)W->htheta.ptr, (double*)W->hsigma.ptr, (int32_t*)W->hiters.ptr,
+                       (int32_t*)W->hsweeps.ptr, (uint8_t*)W->hconv.ptr, s, st, *W);
+  if (rc < 0) return rc;
+  CUDA_TRY(cudaMemcpyAsync(Theta, W->htheta.ptr, pp * 8, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(sigma, W->hsigma.ptr, (size_t)p * 8, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(iters, W->hiters.ptr, (size_t)p * 4, cudaMemcpyDeviceToHost, s));
+  if (sweeps) CUDA_TRY(cudaMemcpyAsync(sweeps, W->hsweeps.ptr, (size_t)p * 4, cudaMemcpyDeviceToHost, s));
+  if (converged) CUDA_TRY(cudaMemcpyAsync(converged, W->hconv.ptr, (size_t)p, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return rc;
+}
+
+int spmesl_fit(const double* X, int64_t n, int64_t p, double lambda0, double tol,
+               int32_t max_iter, double* Theta, double* sigma, int32_t* iters) {
+  return spmesl_fit_ex(X, n, p, lambda0, tol, max_iter, nullptr, Theta, sigma, iters, nullptr,
+                       nullptr, nullptr);
+}
+
+int spmesl_fit_columns_device(const double* dX, int64_t n, int64_t p, int64_t col_begin,
+                              int64_t col_end, double lambda0, double tol, int32_t max_iter,
+                              const spmesl_options* opt, int32_t* dColCount, int32_t* dRows,
+                              double* dVals, int64_t cap, int64_t* nnz_out, double* dSigmaStd,
+                              double* dScale, int32_t* dIters, int32_t* dSweeps,
+                              uint8_t* dConverged, void* cuda_stream, spmesl_stats* st) {
+  init_stats(st);
+  spmesl_options o = resolve(opt);
+  int rc = validate(dX, n, p, lambda0, tol, max_iter, o);
+  if (rc) return rc;
+  if (col_begin < 0 || col_end > p || col_begin >= col_end)
+    return fail(SPMESL_ERR_ARG, "bad column range");
+  if (!dColCount || !dRows || !dVals || !nnz_out || !dSigmaStd || !dScale || !dIters)
+    return fail(SPMESL_ERR_ARG, "output pointer is NULL");
+  int dev;
+  if ((rc = current_device(-1, &dev))) return rc;
+  Workspace* W = workspace_for(dev);
+  std::lock_guard<std::mutex> lk(W->mu);
+  if ((rc = ws_init(*W, dev))) return rc;
+  if (W->cc_major < 10) return fail(SPMESL_ERR_UNSUPPORTED, "needs an sm_100 device");
+  const int64_t m = col_end - col_begin;
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  if (!dSweeps) { if ((rc = ensure(W->sweeps, (size_t)m * 4))) return rc; dSweeps = (int32_t*)W->sweeps.ptr; }
+  if (!dConverged) { if ((rc = ensure(W->conv, (size_t)m))) return rc; dConverged = (uint8_t*)W->conv.ptr; }
+  FitOut out{col_begin, col_end, dSigmaStd, dIters, dSweeps, dConverged};
+  Layout L;
+  int nzcap = 0;
+  rc = fit_columns_core(*W, dX, n, p, col_begin, col_end, lambda0, tol, max_iter, o, out, s, st, L,
+                        &nzcap);
+  if (rc) return rc;
+  DevCounters* dc = (DevCounters*)W->counters.ptr;
+  // scan only to learn the total, then copy straight into the caller's arrays
+  const size_t need_cap = (size_t)m * (size_t)nzcap;
+  if ((rc = ensure(W->csc_rows, need_cap * 4))) return rc;
+  if ((rc = ensure(W->csc_vals, need_cap * 8))) return rc;
+  CUDA_TRY(launch_csc_build((const int*)W->nz_count.ptr, (const int*)W->nz_cur.ptr,
+                            (const int*)W->nz_rows.ptr, (const double*)W->nz_vals.ptr, (int)m, nzcap,
+                            (int64_t*)W->col_ptr.ptr, (int32_t*)W->csc_rows.ptr,
+                            (double*)W->csc_vals.ptr, &dc->csc_total, s));
+  CUDA_TRY(launch_csc_counts((const int*)W->nz_count.ptr, (int)m, dColCount, s));
+  CUDA_TRY(cudaMemcpyAsync(dScale, W->scale.ptr, (size_t)p * 8, cudaMemcpyDeviceToDevice, s));
+  if ((rc = read_counters(*W, s))) return rc;
+  const int64_t total = W->host_counters->csc_total;
+  *nnz_out = total;
+  if (total > cap) return fail(SPMESL_ERR_ARG, "CSC capacity too small: need " + std::to_string(total));
+  if (total > 0) {
+    CUDA_TRY(cudaMemcpyAsync(dRows, W->csc_rows.ptr, (size_t)total * 4, cudaMemcpyDeviceToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(dVals, W->csc_vals.ptr, (size_t)total * 8, cudaMemcpyDeviceToDevice, s));
+  }
+  int any_unconv = 0;
+  if ((rc = collect_stats(dIters, dSweeps, dConverged, m, p, s, st, &any_unconv))) return rc;
+  if (st) {
+    st->nnz = total;
+    st->ms_standardize = ev_ms(W->ev[0], W->ev[1]);
+    st->ms_cd = ev_ms(W->ev[1], W->ev[2]);
+    st->kernel_launches = 6;
+  }
+  return any_unconv ? SPMESL_WARN_NOT_CONVERGED : SPMESL_OK;
+}
+
+int spmesl_assemble_device(int64_t p, int64_t col_begin, int64_t col_end, const int64_t* dColPtr,
+                           const int32_t* dRows, const double* dVals, const double* dSigmaStd,
+                           const double* dScale, const spmesl_options* opt, double* dTheta,
+                           double* dSigmaOut, void* cuda_stream) {
+  spmesl_options o = resolve(opt);
+  if (p < 2 || col_begin < 0 || col_end > p || col_begin >= col_end)
+    return fail(SPMESL_ERR_ARG, "bad column range");
+  if (!dColPtr || !dSigmaStd || !dTheta || (o.standardize && !dScale))
+    return fail(SPMESL_ERR_ARG, "NULL pointer");
+  CUDA_TRY(launch_assemble(p, col_begin, col_end, dColPtr, dRows, dVals, dSigmaStd,
+                           o.standardize ? dScale : nullptr, o.symmetrize, dTheta, dSigmaOut,
+                           (cudaStream_t)cuda_stream));
+  return SPMESL_OK;
+}
+
+}  // extern "C"

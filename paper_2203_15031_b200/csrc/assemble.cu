@@ -1,0 +1,183 @@
+// Coefficient export (CSC) and Theta assembly + symmetrization (steps a8-a10).
+//
+// csc_*      — each fitted column's final coefficient list (rows ascending, nonzeros only)
+//              is packed into one CSC array (col_ptr, rows, vals).  This is also the unit
+//              exchanged between GPUs (one all-gather of nonzeros instead of p^2 doubles).
+// assemble   — Alg. 2: omega_kk = 1/(sigma_k sigma_k), omega_jk = -b_jk omega_kk,
+//              Proposition 1 rescale omega_jk / (s_j s_k), and the
+//              minimum-magnitude symmetrization of Eq. (symm) (Alg. 2 P:709-719:
+//              for r < c keep Theta1[r,c] unless |Theta1[r,c]| > |Theta1[c,r]|).  Theta is
+//              zero-filled first (a cudaMemsetAsync, the only dense pass: 8 p^2 bytes
+//              written); then one thread per nonzero b_jk looks up its partner b_kj by binary
+//              search in column j and writes the chosen value into column k.  An entry whose
+//              partner is zero symmetrizes to zero (already there), so only mutual pairs and
+//              the diagonal are written.
+#include "spmesl_internal.cuh"
+
+namespace spmesl {
+
+// Exclusive scan of counts -> col_ptr[0..ncols], single CTA (ncols up to a few 1e5).
+__global__ void __launch_bounds__(1024) csc_scan_kernel(const int* __restrict__ cnt, int ncols,
+                                                        int64_t* __restrict__ col_ptr,
+                                                        int64_t* total) {
+  __shared__ int64_t warp_tot[32];
+  __shared__ int64_t carry;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < ncols; base += 1024) {
+    const int i = base + tid;
+    int64_t v = (i < ncols) ? (int64_t)cnt[i] : 0;
+    int64_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      int64_t s = warp_tot[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int64_t y = __shfl_up_sync(0xffffffffu, s, o);
+        if (lane >= o) s += y;
+      }
+      warp_tot[lane] = s;  // inclusive over warps
+    }
+    __syncthreads();
+    const int64_t excl = carry + (w ? warp_tot[w - 1] : 0) + x - v;
+    if (i < ncols) col_ptr[i] = excl;
+    __syncthreads();
+    if (tid == 1023) carry = excl + v;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    col_ptr[ncols] = carry;
+    *total = carry;
+  }
+}
+
+__global__ void csc_copy_kernel(const int* __restrict__ cnt, const int* __restrict__ cur,
+                                const int* __restrict__ nz_rows, const double* __restrict__ nz_vals,
+                                int ncols, int nzcap, const int64_t* __restrict__ col_ptr,
+                                int32_t* __restrict__ rows, double* __restrict__ vals) {
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (c >= ncols) return;
+  const int m = min(cnt[c], nzcap);
+  const size_t src = (size_t)c * 2 * nzcap + (size_t)cur[c] * nzcap;
+  const int64_t dst = col_ptr[c];
+  for (int e = lane; e < m; e += 32) {
+    rows[dst + e] = nz_rows[src + e];
+    vals[dst + e] = nz_vals[src + e];
+  }
+}
+
+__global__ void csc_counts_kernel(const int* __restrict__ cnt, int ncols, int32_t* out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < ncols) out[c] = cnt[c];
+}
+
+__device__ __forceinline__ double theta1(double b, double sigma_k, double s_j, double s_k,
+                                         bool rescale) {
+  const double wkk = 1.0 / (sigma_k * sigma_k);     // Alg. 2: omega_kk = sigma_k^-2
+  double w = -b * wkk;                              // omega_jk = -beta_jk omega_kk
+  if (rescale) w = w / (s_j * s_k);                 // Prop. 1
+  return w;
+}
+
+// Binary search for row r in the sorted rows[lo, hi); returns the value or 0.
+__device__ __forceinline__ double csc_lookup(const int32_t* __restrict__ rows,
+                                             const double* __restrict__ vals, int64_t lo,
+                                             int64_t hi, int32_t r) {
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    const int32_t v = rows[mid];
+    if (v == r) return vals[mid];
+    if (v < r) lo = mid + 1;
+    else hi = mid;
+  }
+  return 0.0;
+}
+
+__global__ void assemble_entries_kernel(int64_t p, int64_t col_begin, int64_t col_end,
+                                        const int64_t* __restrict__ col_ptr,
+                                        const int32_t* __restrict__ rows,
+                                        const double* __restrict__ vals,
+                                        const double* __restrict__ sigma_std,
+                                        const double* __restrict__ scale, int symmetrize,
+                                        int rescale, double* __restrict__ Theta) {
+  const int64_t e0 = col_ptr[col_begin], e1 = col_ptr[col_end];
+  for (int64_t e = e0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < e1;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    // column k of entry e: binary search in col_ptr[col_begin..col_end]
+    int64_t lo = col_begin, hi = col_end;   // find k with col_ptr[k] <= e < col_ptr[k+1]
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (col_ptr[mid] <= e) lo = mid;
+      else hi = mid;
+    }
+    const int64_t k = lo;
+    const int32_t j = rows[e];
+    const double sj = scale[j], sk = scale[k];
+    const double t_jk = theta1(vals[e], sigma_std[k], sj, sk, rescale != 0);
+    double out = t_jk;
+    if (symmetrize) {
+      const double b_kj = csc_lookup(rows, vals, col_ptr[j], col_ptr[j + 1], (int32_t)k);
+      if (b_kj == 0.0) continue;            // partner zero -> symmetrized value is zero
+      const double t_kj = theta1(b_kj, sigma_std[j], sk, sj, rescale != 0);
+      // pair (r, c), r < c: keep Theta1[r,c] unless |Theta1[r,c]| > |Theta1[c,r]|
+      const double u = (j < k) ? t_jk : t_kj;   // Theta1[min, max]
+      const double l = (j < k) ? t_kj : t_jk;   // Theta1[max, min]
+      out = (fabs(u) > fabs(l)) ? l : u;
+    }
+    Theta[(size_t)(k - col_begin) * (size_t)p + (size_t)j] = out;
+  }
+}
+
+__global__ void assemble_diag_kernel(int64_t p, int64_t col_begin, int64_t col_end,
+                                     const double* __restrict__ sigma_std,
+                                     const double* __restrict__ scale, int rescale,
+                                     double* __restrict__ Theta, double* __restrict__ sigma_out) {
+  const int64_t k = col_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= col_end) return;
+  const double sg = sigma_std[k];
+  double w = 1.0 / (sg * sg);
+  if (rescale) w = w / (scale[k] * scale[k]);
+  Theta[(size_t)(k - col_begin) * (size_t)p + (size_t)k] = w;
+  if (sigma_out) sigma_out[k - col_begin] = rescale ? scale[k] * sg : sg;
+}
+
+cudaError_t launch_csc_build(const int* nz_count, const int* nz_cur, const int* nz_rows,
+                             const double* nz_vals, int ncols, int nzcap, int64_t* col_ptr,
+                             int32_t* rows, double* vals, int64_t* total, cudaStream_t s) {
+  csc_scan_kernel<<<1, 1024, 0, s>>>(nz_count, ncols, col_ptr, total);
+  const int wpb = 8;
+  csc_copy_kernel<<<(ncols + wpb - 1) / wpb, wpb * 32, 0, s>>>(nz_count, nz_cur, nz_rows, nz_vals,
+                                                               ncols, nzcap, col_ptr, rows, vals);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_csc_counts(const int* nz_count, int ncols, int32_t* out, cudaStream_t s) {
+  csc_counts_kernel<<<(ncols + 255) / 256, 256, 0, s>>>(nz_count, ncols, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_assemble(int64_t p, int64_t col_begin, int64_t col_end, const int64_t* col_ptr,
+                            const int32_t* rows, const double* vals, const double* sigma_std,
+                            const double* scale, int symmetrize, double* Theta, double* sigma_out,
+                            cudaStream_t s) {
+  const int64_t m = col_end - col_begin;
+  cudaError_t e = cudaMemsetAsync(Theta, 0, sizeof(double) * (size_t)p * (size_t)m, s);
+  if (e != cudaSuccess) return e;
+  const int rescale = scale != nullptr;
+  assemble_entries_kernel<<<148 * 4, 256, 0, s>>>(p, col_begin, col_end, col_ptr, rows, vals,
+                                                  sigma_std, scale, symmetrize, rescale, Theta);
+  assemble_diag_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(p, col_begin, col_end,
+                                                                   sigma_std, scale, rescale,
+                                                                   Theta, sigma_out);
+  return cudaGetLastError();
+}
+
+}  // namespace spmesl

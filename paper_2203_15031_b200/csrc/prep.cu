@@ -1,0 +1,108 @@
+// Column standardization (step a2) and the Gram band used by the blocked CD walk (a4).
+//
+// standardize_kernel — P:305-307 ("centered and scaled to X_k^T X_k = n"): one warp per
+//   column; mu_k = sum_i x_ik / n, s_k = sqrt(sum_i (x_ik - mu_k)^2 / n) (divisor n, reading
+//   g14), x~_ik = (x_ik - mu_k) / s_k written straight into the tiled HBM layout Xb (see
+//   spmesl_internal.cuh).  Column k is an error if any x_ik is not finite or if
+//   s_k <= 1e-13 max_i |x_ik| (reading g15); the smallest offending column wins.
+//   HBM-bound: reads X twice (8np B each, the second from L2) and writes Xb (8np B).
+//
+// gram_kernel — G_b[jl][jm] = x~_{j0+jl}^T x~_{j0+jm} / n for each 32-row block b: the
+//   within-block couplings that let the CD walk of Proposition 2 process 32
+//   rows of a column with a single dot-product GEMM.  p*32*n FMAs, tiny.
+#include "spmesl_internal.cuh"
+
+namespace spmesl {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void standardize_kernel(const double* __restrict__ X, int64_t n, int64_t p, int nchunk,
+                                   int standardize, double* __restrict__ Xb, double* mu,
+                                   double* scale, int* err, unsigned long long* bad_key) {
+  const int lane = threadIdx.x & 31;
+  const int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (k >= p) return;
+  const double* x = X + k * n;
+  double sum = 0.0, mx = 0.0;
+  bool finite = true;
+  for (int64_t i = lane; i < n; i += 32) {
+    double v = x[i];
+    finite = finite && isfinite(v);
+    sum += v;
+    mx = fmax(mx, fabs(v));
+  }
+  finite = __all_sync(0xffffffffu, finite);
+  if (!finite) {
+    if (lane == 0) { atomicMin(bad_key, 2ull * (unsigned long long)k); atomicExch(err, 1); }
+    return;
+  }
+  sum = warp_sum(sum);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  double m = 0.0, s = 1.0;
+  if (standardize) {
+    m = sum / (double)n;
+    double ss = 0.0;
+    for (int64_t i = lane; i < n; i += 32) {
+      double c = x[i] - m;
+      ss = fma(c, c, ss);
+    }
+    ss = warp_sum(ss);
+    s = sqrt(ss / (double)n);
+    if (!(s > 1e-13 * mx)) {
+      if (lane == 0) { atomicMin(bad_key, 2ull * (unsigned long long)k + 1ull); atomicExch(err, 1); }
+      return;
+    }
+  }
+  if (lane == 0) { mu[k] = m; scale[k] = s; }
+  for (int64_t i = lane; i < n; i += 32) {
+    double v = standardize ? (x[i] - m) / s : x[i];
+    Xb[xb_index(i, k, nchunk)] = v;
+  }
+}
+
+__global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ Xb, int64_t n,
+                                                   int nchunk, double* __restrict__ G) {
+  __shared__ double t[J][KC + 1];
+  const int64_t blk = blockIdx.x;
+  const int tid = threadIdx.x;
+  // thread computes entries (r, c0..c0+3): r = tid / 8, c0 = (tid % 8) * 4
+  const int r = tid >> 3, c0 = (tid & 7) * 4;
+  double acc[4] = {0, 0, 0, 0};
+  for (int q = 0; q < nchunk; ++q) {
+    const double* src = Xb + ((size_t)blk * nchunk + q) * CHUNK_DOUBLES;
+    for (int e = tid; e < J * KC; e += 256) t[e / KC][e % KC] = src[(e / KC) * XS + (e % KC)];
+    __syncthreads();
+#pragma unroll 4
+    for (int kl = 0; kl < KC; ++kl) {
+      double a = t[r][kl];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u] = fma(a, t[c0 + u][kl], acc[u]);
+    }
+    __syncthreads();
+  }
+  double* g = G + (size_t)blk * J * J;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) g[r * J + c0 + u] = acc[u] / (double)n;
+}
+
+cudaError_t launch_standardize(const double* X, const Layout& L, int standardize, double* Xb,
+                               double* mu, double* scale, int* err, unsigned long long* bad_key,
+                               cudaStream_t s) {
+  const int wpb = 8;
+  dim3 grid((unsigned)((L.p + wpb - 1) / wpb));
+  standardize_kernel<<<grid, wpb * 32, 0, s>>>(X, L.n, L.p, L.nchunk, standardize, Xb, mu, scale,
+                                               err, bad_key);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gram(const double* Xb, const Layout& L, double* Gband, cudaStream_t s) {
+  gram_kernel<<<(unsigned)L.nblk, 256, 0, s>>>(Xb, L.n, L.nchunk, Gband);
+  return cudaGetLastError();
+}
+
+}  // namespace spmesl

@@ -1,0 +1,84 @@
+// Internal definitions shared by the SPMESL CUDA sources (product path only).
+//
+// HBM layout of the standardized predictors ("Xb", written by standardize_kernel):
+//   X~ (n x p) is stored in tiles of J = 32 predictor columns x KC = 32 samples, each tile
+//   row padded to XS = 36 doubles (36 = 4 mod 16 keeps the m8n8k4 fragment loads of
+//   8 rows x 4 consecutive k conflict-free in shared memory).  Tile (blk, q) holds
+//   x~_{blk*32 + jl}[q*32 + kl] at Xb[((blk*nchunk + q)*J + jl)*XS + kl] and is one
+//   contiguous 9216-byte block, so a single cp.async.bulk moves it into shared memory.
+//   Samples i >= n and predictors j >= p are zero.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace spmesl {
+
+constexpr int J = 32;                    // predictor rows per row block (CD visits rows block-wise)
+constexpr int KC = 32;                   // samples per staged X chunk
+constexpr int XS = KC + 4;               // padded chunk row stride (doubles)
+constexpr int CHUNK_DOUBLES = J * XS;    // 1152
+constexpr int CHUNK_BYTES = CHUNK_DOUBLES * 8;   // 9216
+constexpr int NCW = 8;                   // consumer warps in the CD kernel
+constexpr int KSPLIT = 4;                // k-split of every dot product (fixed => deterministic)
+constexpr int CD_THREADS = (NCW + 1) * 32;       // + 1 producer warp
+constexpr int MAX_T = 32;                // max resident columns (slots) per CTA
+
+struct Layout {
+  int64_t n, p;
+  int n_pad;      // n rounded up to KC
+  int nchunk;     // n_pad / KC
+  int64_t nblk;   // ceil(p / J)
+  size_t xb_doubles() const { return (size_t)nblk * nchunk * CHUNK_DOUBLES; }
+};
+
+__host__ __device__ inline size_t xb_index(int64_t i, int64_t j, int nchunk) {
+  int64_t blk = j / J, jl = j % J, q = i / KC, kl = i % KC;
+  return (size_t)(((blk * nchunk + q) * J + jl) * XS + kl);
+}
+
+// Error flags written by kernels (device int32[4]).
+enum : int { FLAG_CODE = 0, FLAG_OVERFLOW = 1 };
+
+struct CDParams {
+  const double* Xb;
+  const double* Gband;     // [nblk][J][J]  x~_j^T x~_j' / n within each row block
+  int n, n_pad, nchunk;
+  int p;
+  int nblk;
+  int64_t col_begin;       // global index of local column 0
+  int ncols;               // local columns (queue length)
+  double lambda0, tol, sigma_floor, sqrt_n;
+  int max_outer, max_inner;
+  int T;                   // resident columns per CTA (8, 16, 32)
+  int nzcap;               // per-column capacity of each coefficient list
+  int* queue;              // atomic head (local column index)
+  int* flags;              // FLAG_*
+  const int* err_in;       // standardization error code (CD exits early when nonzero)
+  int* nz_rows;            // [ncols][2][nzcap]
+  double* nz_vals;         // [ncols][2][nzcap]
+  int* nz_count;           // [ncols] entries of the final list
+  int* nz_cur;             // [ncols] which of the 2 lists is final
+  double* sigma_std;       // [ncols]
+  int* iters;              // [ncols]
+  int* sweeps;             // [ncols]
+  uint8_t* converged;      // [ncols]
+};
+
+size_t cd_smem_bytes(int T, int n_pad);
+
+// Launchers (stream-ordered, no host synchronisation).
+cudaError_t launch_standardize(const double* X, const Layout& L, int standardize, double* Xb,
+                               double* mu, double* scale, int* err, unsigned long long* bad_col,
+                               cudaStream_t s);
+cudaError_t launch_gram(const double* Xb, const Layout& L, double* Gband, cudaStream_t s);
+cudaError_t launch_cd(const CDParams& P, int num_ctas, cudaStream_t s);
+cudaError_t launch_csc_build(const int* nz_count, const int* nz_cur, const int* nz_rows,
+                             const double* nz_vals, int ncols, int nzcap, int64_t* col_ptr,
+                             int32_t* rows, double* vals, int64_t* total, cudaStream_t s);
+cudaError_t launch_csc_counts(const int* nz_count, int ncols, int32_t* out, cudaStream_t s);
+cudaError_t launch_assemble(int64_t p, int64_t col_begin, int64_t col_end, const int64_t* col_ptr,
+                            const int32_t* rows, const double* vals, const double* sigma_std,
+                            const double* scale, int symmetrize, double* Theta, double* sigma_out,
+                            cudaStream_t s);
+
+}  // namespace spmesl

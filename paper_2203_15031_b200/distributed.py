@@ -1,0 +1,86 @@
+"""Column-block sharding of SPMESL over the ranks of a torch.distributed process group
+(one process per GPU; BASELINE.json north_star (3) and SURVEY.md §8(e)).
+
+The p column problems are independent, so each rank solves the columns
+[c0, c1) of its contiguous block with X replicated and needs no communication during CD.
+The only exchange is ONE all-gather of the fitted coefficients in CSC form (counts, rows,
+values, sigma) — the nonzeros, not p x p doubles — after which every rank assembles and
+symmetrizes its own column block of Theta from the global CSC (the symmetrization of
+Eq. (symm), needs b_kj from column j, which may live on another rank).
+
+``gather_csc`` is backend-agnostic host logic (gloo on CPU tensors in the tests, NCCL on
+CUDA tensors in production); ``fit_distributed`` runs the CUDA path around it.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def column_range(p: int, rank: int, world: int):
+    """Contiguous, balanced block of columns for `rank` (first p % world ranks get one more)."""
+    base, rem = divmod(p, world)
+    c0 = rank * base + min(rank, rem)
+    return c0, c0 + base + (1 if rank < rem else 0)
+
+
+def _all_gather_padded(t: torch.Tensor, length: int, group=None):
+    """All-gather a 1-D tensor whose length differs per rank (padded to `length`)."""
+    world = dist.get_world_size(group)
+    buf = torch.zeros(length, dtype=t.dtype, device=t.device)
+    buf[: t.numel()] = t
+    out = torch.empty(world * length, dtype=t.dtype, device=t.device)
+    dist.all_gather_into_tensor(out, buf, group=group)
+    return out.view(world, length)
+
+
+def gather_csc(p: int, counts: torch.Tensor, rows: torch.Tensor, vals: torch.Tensor,
+               sigma_std: torch.Tensor, group=None):
+    """Concatenate every rank's column block (in rank = column order) into the global CSC.
+
+    counts[m_r] (int32), rows[nnz_r] (int32), vals[nnz_r] (float64), sigma_std[m_r] (float64)
+    -> (col_ptr[p+1] int64, rows[nnz] int32, vals[nnz] float64, sigma_std[p] float64)."""
+    world = dist.get_world_size(group)
+    dev = counts.device
+    m_max = -(-p // world)
+    meta = torch.tensor([counts.numel(), rows.numel()], dtype=torch.int64, device=dev)
+    metas = torch.empty(world * 2, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(metas, meta, group=group)
+    metas = metas.view(world, 2).cpu()
+    nnz_max = max(int(metas[:, 1].max()), 1)
+    cnt_all = _all_gather_padded(counts, m_max, group)
+    sig_all = _all_gather_padded(sigma_std, m_max, group)
+    rows_all = _all_gather_padded(rows, nnz_max, group)
+    vals_all = _all_gather_padded(vals, nnz_max, group)
+    cnt_list, sig_list, row_list, val_list = [], [], [], []
+    for r in range(world):
+        m_r, z_r = int(metas[r, 0]), int(metas[r, 1])
+        cnt_list.append(cnt_all[r, :m_r])
+        sig_list.append(sig_all[r, :m_r])
+        row_list.append(rows_all[r, :z_r])
+        val_list.append(vals_all[r, :z_r])
+    cnt = torch.cat(cnt_list).to(torch.int64)
+    if cnt.numel() != p:
+        raise ValueError("column blocks do not cover p columns")
+    col_ptr = torch.zeros(p + 1, dtype=torch.int64, device=dev)
+    col_ptr[1:] = torch.cumsum(cnt, 0)
+    return col_ptr, torch.cat(row_list), torch.cat(val_list), torch.cat(sig_list)
+
+
+def fit_distributed(X: torch.Tensor, lambda0: float, tol: float = 1e-4, max_iter: int = 100,
+                    group=None, stream=None, **options):
+    """Fit this rank's column block and return its block of Theta (p x m, column-major view).
+
+    X: (n, p) float64 CUDA tensor, identical on every rank."""
+    from . import assemble_device, fit_columns_device
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    n, p = X.shape
+    c0, c1 = column_range(p, rank, world)
+    part = fit_columns_device(X, c0, c1, lambda0, tol, max_iter, stream=stream, **options)
+    col_ptr, rows, vals, sig_all = gather_csc(p, part["counts"], part["rows"], part["vals"],
+                                              part["sigma_std"], group)
+    theta, sigma = assemble_device(p, c0, c1, col_ptr, rows, vals, sig_all, part["scale"],
+                                   stream=stream, **options)
+    return dict(theta=theta, sigma=sigma, iters=part["iters"], sweeps=part["sweeps"],
+                converged=part["converged"], col_range=(c0, c1), stats=part["stats"],
+                code=part["code"])

@@ -1,0 +1,183 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element,
+on the same seeded inputs.  Needs a B200 (marker gpu)."""
+import math
+
+import numpy as np
+import pytest
+
+from synth import generators as G
+from tests.parity import assert_parity, compare
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def S():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2203_15031_b200 as S
+    S.load()
+    return S
+
+
+def _lam(oracle, rule, n, p):
+    return {"univ": oracle.lambda_univ, "ub": oracle.lambda_ub}[rule](n, p)
+
+
+CASES = [
+    # (config, overrides, rule)
+    (1, {}, "univ"),
+    (1, {}, "ub"),
+    (2, {}, "univ"),
+    (2, {}, "ub"),
+    (3, {}, "ub"),
+    (3, {}, "univ"),
+    (4, dict(p=1000), "ub"),
+    (4, dict(p=1000, family="hub"), "ub"),
+    (4, dict(p=777, n=203), "univ"),          # ragged p and n (not multiples of 32)
+    (5, dict(p=1500), "ub"),
+]
+
+
+@pytest.mark.parametrize("cfg,over,rule", CASES)
+@pytest.mark.parametrize("delta", [1e-4, 1e-10])
+def test_parity_host_api(S, oracle, cfg, over, rule, delta):
+    X, gt, spec = G.make_config(cfg, **over)
+    n, p = X.shape
+    lam = _lam(oracle, rule, n, p)
+    ora = oracle.spmesl_fit(X, lam, delta=delta)
+    res = S.fit(X, lam, tol=delta, max_iter=100)
+    rep = compare(res.Theta, res.sigma, res.iters, res.sweeps, ora)
+    print(cfg, over, rule, delta, rep)
+    assert_parity(rep)
+    assert np.array_equal(res.converged, ora.converged)
+    assert np.array_equal(res.Theta, res.Theta.T)
+    st = res.stats
+    assert st["coord_updates"] == int(ora.sweeps.sum()) * (p - 1)
+
+
+@pytest.mark.parametrize("T", [8, 16, 32])
+def test_bit_identical_across_tile_sizes(S, oracle, T):
+    X, _, _ = G.make_config(4, p=600, family="hub")
+    lam = oracle.lambda_ub(*X.shape)
+    ref = S.fit(X, lam, tile_cols=8)
+    r = S.fit(X, lam, tile_cols=T)
+    assert np.array_equal(r.Theta, ref.Theta)
+    assert np.array_equal(r.sigma, ref.sigma)
+    assert np.array_equal(r.sweeps, ref.sweeps)
+
+
+def test_theta1_unsymmetrized_and_unstandardized(S, oracle):
+    X, _, _ = G.make_config(2)
+    n, p = X.shape
+    lam = oracle.lambda_univ(n, p)
+    ora = oracle.spmesl_fit(X, lam)
+    r = S.fit(X, lam, symmetrize=False)
+    d = np.abs(r.Theta - ora.Theta1)
+    assert np.all(d <= 1e-8 * np.abs(ora.Theta1) + 1e-12 * ora.Theta1.diagonal().max())
+    Xs, mu, s = oracle.standardize(X)
+    ora2 = oracle.spmesl_fit(Xs, lam, standardize=False)
+    r2 = S.fit(Xs, lam, standardize=False)
+    assert_parity(compare(r2.Theta, r2.sigma, r2.iters, r2.sweeps, ora2))
+
+
+def test_device_api_and_stream(S, oracle):
+    import torch
+    X, _, _ = G.make_config(3)
+    n, p = X.shape
+    lam = oracle.lambda_ub(n, p)
+    ora = oracle.spmesl_fit(X, lam)
+    Xd = torch.from_numpy(np.ascontiguousarray(X.T)).cuda().t()   # column-major (n, p)
+    s = torch.cuda.Stream()
+    r = S.fit_device(Xd, lam, stream=s)
+    rep = compare(r.Theta.cpu().numpy(), r.sigma.cpu().numpy(), r.iters.cpu().numpy(),
+                  r.sweeps.cpu().numpy(), ora)
+    assert_parity(rep)
+    # a row-major tensor is accepted too (copied to column-major)
+    r2 = S.fit_device(torch.from_numpy(np.ascontiguousarray(X)).cuda(), lam)
+    assert torch.equal(r2.Theta, r.Theta)
+
+
+def test_column_blocks_reproduce_full_fit(S, oracle):
+    """The multi-GPU building blocks: CSC of column blocks + assembly == single fit, bitwise."""
+    import torch
+    X, _, _ = G.make_config(4, p=900, family="hub")
+    n, p = X.shape
+    lam = oracle.lambda_ub(n, p)
+    full = S.fit(X, lam)
+    Xd = torch.from_numpy(np.ascontiguousarray(X)).cuda()
+    bounds = [0, 250, 251, 600, 900]
+    parts = [S.fit_columns_device(Xd, a, b, lam) for a, b in zip(bounds[:-1], bounds[1:])]
+    counts = torch.cat([q["counts"] for q in parts]).long()
+    col_ptr = torch.zeros(p + 1, dtype=torch.int64, device="cuda")
+    col_ptr[1:] = torch.cumsum(counts, 0)
+    rows = torch.cat([q["rows"] for q in parts])
+    vals = torch.cat([q["vals"] for q in parts])
+    sig = torch.cat([q["sigma_std"] for q in parts])
+    scale = parts[0]["scale"]
+    th, so = S.assemble_device(p, 0, p, col_ptr, rows, vals, sig, scale)
+    assert np.array_equal(th.cpu().numpy(), full.Theta)
+    assert np.array_equal(so.cpu().numpy(), full.sigma)
+    th2, so2 = S.assemble_device(p, 300, 700, col_ptr, rows, vals, sig, scale)
+    assert np.array_equal(th2.cpu().numpy(), full.Theta[:, 300:700])
+
+
+def test_null_case_and_small_p(S, oracle):
+    rng = np.random.default_rng(5)
+    for (n, p) in [(7, 2), (33, 3), (64, 31), (65, 33)]:
+        X = rng.standard_normal((n, p)) * rng.uniform(0.5, 2, p)
+        for lam in (0.05, 0.3, 5.0):
+            ora = oracle.spmesl_fit(X, lam)
+            r = S.fit(X, lam)
+            assert_parity(compare(r.Theta, r.sigma, r.iters, r.sweeps, ora))
+
+
+def test_errors(S):
+    X = np.random.default_rng(1).standard_normal((20, 40))
+    X[:, 17] = 2.5
+    with pytest.raises(S.SpmeslError) as e:
+        S.fit(X, 0.3)
+    assert e.value.code == -2 and e.value.bad_column == 17
+    X[:, 17] = np.arange(20)
+    X[3, 30] = np.inf
+    X[0, 35] = np.nan
+    with pytest.raises(S.SpmeslError) as e:
+        S.fit(X, 0.3)
+    assert e.value.code == -3 and e.value.bad_column == 30
+    # the library recovers after an error
+    X[3, 30] = 1.0
+    X[0, 35] = 1.0
+    S.fit(X, 0.3)
+
+
+def test_max_iter_cap_flags_columns(S, oracle):
+    X, _, _ = G.make_config(2)
+    lam = oracle.lambda_univ(*X.shape)
+    ora = oracle.spmesl_fit(X, lam, max_outer=2)
+    r = S.fit(X, lam, max_iter=2)
+    assert r.code == 1 and not r.converged.all()
+    assert np.array_equal(r.converged, ora.converged)
+    assert_parity(compare(r.Theta, r.sigma, r.iters, r.sweeps, ora))
+
+
+def test_full_size_config5_sampled_columns(S, oracle):
+    """BASELINE config 5 at full size (n=500, p=20000) in the bench's launch configuration;
+    the oracle solves a sample of columns one by one (each column is independent)."""
+    X, _, spec = G.make_config(5)
+    n, p = X.shape
+    lam = oracle.lambda_ub(n, p)
+    r = S.fit(X, lam, symmetrize=False)        # Theta1: column k depends on column k only
+    rng = np.random.default_rng(0)
+    cols = np.sort(rng.choice(p, 48, replace=False))
+    Xs, mu, s = oracle.standardize(X)
+    oc = oracle.spmesl_columns(Xs, cols, lam, want_margin=False)
+    assert np.array_equal(r.iters[cols], oc.outer) and np.array_equal(r.sweeps[cols], oc.sweeps)
+    np.testing.assert_allclose(r.sigma[cols], oc.sigma * s[cols], rtol=1e-10)
+    for c, k in enumerate(cols):
+        want = np.zeros(p)
+        want[:] = -oc.B[:, c] * (1.0 / (oc.sigma[c] * oc.sigma[c]))
+        want[k] = 1.0 / (oc.sigma[c] * oc.sigma[c])
+        want = want / (s * s[k])
+        got = r.Theta[:, k]
+        assert np.all(np.abs(got - want) <= 1e-8 * np.abs(want) + 1e-12 * abs(want[k])), k
