@@ -142,7 +142,7 @@ int choose_T(const Workspace& W, int64_t ncols, int n_pad, int requested) {
   int fallback = 0;
   for (int T : cands) {
     if (requested && T != requested) continue;
-    if (cd_smem_bytes(T, n_pad) > (size_t)W.smem_optin) continue;
+    if (cd_stages(T, n_pad, W.smem_optin) < 4) continue;
     if (!fallback) fallback = T;
     if (requested || (ncols + T - 1) / T >= W.sms || T == 8) return T;
   }
@@ -192,6 +192,7 @@ int run_cd(Workspace& W, const double* dX, int64_t n, int64_t p, int64_t cb, int
   P.max_outer = max_iter;
   P.max_inner = o.max_inner;
   P.T = T;
+  P.nst = cd_stages(T, L.n_pad, W.smem_optin);
   P.nzcap = nzcap;
   P.queue = (int*)W.queue.ptr;
   P.flags = &dc->err;   // FLAG_CODE (unused by CD), FLAG_OVERFLOW at +1
@@ -302,7 +303,7 @@ int fit_columns_core(Workspace& W, const double* dX, int64_t n, int64_t p, int64
   L.nchunk = L.n_pad / KC;
   L.nblk = (p + J - 1) / J;
   const int T = choose_T(W, m, L.n_pad, o.tile_cols);
-  if (!T || cd_smem_bytes(T, L.n_pad) > (size_t)W.smem_optin)
+  if (!T || cd_stages(T, L.n_pad, W.smem_optin) < 2)
     return fail(SPMESL_ERR_UNSUPPORTED, "n = " + std::to_string(n) +
                                             " does not fit the on-chip residual tile");
   int nzcap = initial_nzcap(n, p);

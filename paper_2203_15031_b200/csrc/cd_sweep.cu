@@ -27,6 +27,7 @@
 // Coefficients never live in a dense p x p array: each column keeps its nonzeros as a list
 // (rows ascending) rebuilt every sweep (double-buffered in HBM), read back with a cursor in
 // the next sweep and used for the residual refresh and the final CSC export.
+#include <algorithm>
 #include <cstdio>
 #include "spmesl_internal.cuh"
 
@@ -89,7 +90,8 @@ __device__ __forceinline__ double soft(double a, double lam) {
   return m > 0.0 ? copysign(m, a) : 0.0;
 }
 
-constexpr int NST = 4;  // X chunk pipeline depth
+constexpr int MAX_NST = 12; // max X chunk pipeline depth (runtime: as many as smem allows)
+constexpr int JP = J + 1;    // padded row-block stride of the per-column [c][row] tiles
 
 struct SlotState {
   int col[MAX_T];       // local column index, -1 = free
@@ -116,40 +118,113 @@ struct SlotState {
   int ld_dst[MAX_T];
 };
 
-size_t cd_smem_bytes(int T, int n_pad) {
-  size_t sr = (size_t)n_pad + 4;
+// Shared-memory carve-up (bytes), given T slots, padded n and the pipeline depth.
+static __host__ __device__ size_t smem_fixed_bytes(int T, int n_pad) {
   size_t b = 0;
-  b += (size_t)T * sr * 8;              // Rs
-  b += (size_t)NST * CHUNK_BYTES;       // Xs stages
-  b += (size_t)KSPLIT * J * T * 8;      // Zp
-  b += (size_t)J * T * 8;               // Bt
-  b += (size_t)T * J * 8;               // chg_d
-  b += (size_t)T * J;                   // chg_row
+  b += (size_t)T * (n_pad + RPAD) * 8;  // Rs   [T][n_pad+RPAD]
+  b += (size_t)KSPLIT * T * JP * 8;     // Zp   [KSPLIT][T][JP]
+  b += (size_t)T * JP * 8;              // Bt   [T][JP]
+  b += (size_t)J * T * 8;               // chg_d  [J][T]
+  b += (size_t)J * T;                   // chg_row[J][T]
   b = (b + 15) & ~(size_t)15;
   b += sizeof(SlotState);
   b = (b + 15) & ~(size_t)15;
-  b += 2 * NST * 8;                     // mbarriers
-  return b + 128;                       // alignment slack
+  b += 2 * MAX_NST * 8;                 // mbarriers
+  b = (b + 127) & ~(size_t)127;         // stage ring is 128-byte aligned
+  return b;
+}
+
+int cd_stages(int T, int n_pad, size_t smem_optin) {
+  const size_t fixed = smem_fixed_bytes(T, n_pad);
+  if (fixed + 2 * (size_t)CHUNK_BYTES > smem_optin) return 0;
+  return (int)std::min<size_t>(MAX_NST, (smem_optin - fixed) / CHUNK_BYTES);
+}
+
+size_t cd_smem_bytes(int T, int n_pad) {     // minimum (2 stages)
+  return smem_fixed_bytes(T, n_pad) + 2 * (size_t)CHUNK_BYTES;
+}
+
+// One row block's contraction Z(32 x 8NTa) = X_J^T R for the chunks q = grp (mod 2) of this
+// warp's parity group, for the warp's MT x NT subtile of 8x8 tiles starting at (m0, n0).
+// Paired-k fragments: for k-pair kp of a chunk, lane (g, t) loads the 2 consecutive samples
+// k = 8kp + 2t, 8kp + 2t + 1 of row g with one 128-bit LDS; the first DMMA takes the even
+// sample, the second the odd one (the same k mapping for A and B, so the sum is exact up to
+// its fixed association).  Each output's accumulation order depends only on k, never on the
+// subtile mapping, so results are independent of NTa and of the column's slot.
+template <int MT, int NT>
+__device__ __forceinline__ void gemm_block(const double* __restrict__ Xs, const double* __restrict__ Rs,
+                                           double* __restrict__ Zp, uint64_t* full, uint64_t* empty,
+                                           int grp, int m0, int n0, int nchunk, int NST, int s_base,
+                                           uint32_t ph_base, int SR, int T, int lane) {
+  const int g = lane >> 2, t4 = lane & 3;
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < NT; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+  int s = s_base + grp;
+  uint32_t ph = ph_base;
+  if (s >= NST) { s -= NST; ph ^= 1u; }
+  const double* rbase = Rs + (size_t)(n0 * 8 + g) * SR + 2 * t4;
+  for (int q = grp; q < nchunk; q += 2) {
+    mbar_wait(&full[s], ph);
+    const double* xs = Xs + (size_t)s * CHUNK_DOUBLES + (size_t)(m0 * 8 + g) * XS + 2 * t4;
+    const double* rs = rbase + q * KC;
+    const int sw = g & 1;                 // row parity of this lane's A rows (xswz)
+#pragma unroll
+    for (int kp = 0; kp < KC / 8; ++kp) {
+      double2 a[MT], bb[NT];
+#pragma unroll
+      for (int mi = 0; mi < MT; ++mi) a[mi] = *(const double2*)(xs + mi * 8 * XS + (kp ^ sw) * 8);
+#pragma unroll
+      for (int ni = 0; ni < NT; ++ni) bb[ni] = *(const double2*)(rs + (size_t)ni * 8 * SR + kp * 8);
+#pragma unroll
+      for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NT; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi].x, bb[ni].x);
+#pragma unroll
+      for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NT; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi].y, bb[ni].y);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    s += 2;
+    if (s >= NST) { s -= NST; ph ^= 1u; }
+  }
+  // partial sums: Zp[grp][col][row]
+#pragma unroll
+  for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < NT; ++ni) {
+      double* z = Zp + ((size_t)grp * T + (n0 + ni) * 8 + 2 * t4) * JP + (m0 + mi) * 8 + g;
+      z[0] = acc[mi][ni][0];
+      z[JP] = acc[mi][ni][1];
+    }
 }
 
 __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams P) {
-  extern __shared__ unsigned char smem_raw[];
-  unsigned char* base = (unsigned char*)(((uintptr_t)smem_raw + 127) & ~(uintptr_t)127);
+  // (pointer arithmetic only from the __shared__ array, so every access compiles to LDS/STS)
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int T = P.T;
-  const int SR = P.n_pad + 4;
-  double* Rs = (double*)base;                                   // [T][SR]
-  double* Xs = Rs + (size_t)T * SR;                             // [NST][J][XS]
-  double* Zp = Xs + (size_t)NST * CHUNK_DOUBLES;                // [KSPLIT][J][T]
-  double* Bt = Zp + (size_t)KSPLIT * J * T;                     // [J][T]
-  double* chg_d = Bt + (size_t)J * T;                           // [T][J]
-  unsigned char* chg_row = (unsigned char*)(chg_d + (size_t)T * J);  // [T][J]
-  size_t off = (size_t)((unsigned char*)(chg_row + T * J) - base);
+  const int SR = P.n_pad + RPAD;
+  const int NST = P.nst;
+  double* Rs = (double*)smem_raw;                               // [T][SR]
+  double* Zp = Rs + (size_t)T * SR;                             // [KSPLIT][T][JP]
+  double* Bt = Zp + (size_t)KSPLIT * T * JP;                    // [T][JP]
+  double* chg_d = Bt + (size_t)T * JP;                          // [J][T]
+  unsigned char* chg_row = (unsigned char*)(chg_d + (size_t)J * T);  // [J][T]
+  size_t off = (size_t)T * SR * 8 + (size_t)KSPLIT * T * JP * 8 + (size_t)T * JP * 8 +
+               (size_t)J * T * 8 + (size_t)J * T;
   off = (off + 15) & ~(size_t)15;
-  SlotState& S = *(SlotState*)(base + off);
+  SlotState& S = *(SlotState*)(smem_raw + off);
   off += sizeof(SlotState);
   off = (off + 15) & ~(size_t)15;
-  uint64_t* full = (uint64_t*)(base + off);
-  uint64_t* empty = full + NST;
+  uint64_t* full = (uint64_t*)(smem_raw + off);
+  uint64_t* empty = full + MAX_NST;
+  off += 2 * MAX_NST * 8;
+  off = (off + 127) & ~(size_t)127;
+  double* Xs = (double*)(smem_raw + off);                       // [NST][J][XS]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = P.n, n_pad = P.n_pad, nchunk = P.nchunk, p = P.p, nblk = P.nblk;
@@ -158,7 +233,7 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NCW);
+      mbar_init(&empty[s], NCW / KSPLIT);   // the 4 warps of the chunk's parity group
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -173,20 +248,20 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
 
   // ===================================================== producer warp: X tile stream
   if (warp == NCW) {
-    uint32_t it = 0;
+    int s = 0;
+    uint32_t ph = 0;
     for (;;) {
       named_bar_sync(2, CD_THREADS);
       int go = *(volatile int*)&S.go;
       if (!go) break;
       if (lane == 0) {
+        const double* src = P.Xb;
         for (int b = 0; b < nblk; ++b)
-          for (int q = 0; q < nchunk; ++q, ++it) {
-            const int s = it % NST;
-            const uint32_t ph = (it / NST) & 1u;
+          for (int q = 0; q < nchunk; ++q, src += CHUNK_DOUBLES) {
             mbar_wait(&empty[s], ph ^ 1u);
             mbar_arrive_expect_tx(&full[s], CHUNK_BYTES);
-            bulk_g2s(Xs + (size_t)s * CHUNK_DOUBLES,
-                     P.Xb + ((size_t)b * nchunk + q) * CHUNK_DOUBLES, CHUNK_BYTES, &full[s]);
+            bulk_g2s(Xs + (size_t)s * CHUNK_DOUBLES, src, CHUNK_BYTES, &full[s]);
+            if (++s == NST) { s = 0; ph ^= 1u; }
           }
       }
       __syncwarp();
@@ -196,7 +271,9 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
 
   // ===================================================== consumer warps
   const bool std_error = (*(volatile const int*)P.err_in) != 0;
-  uint32_t it = 0;
+  // ring position of the first chunk of the current block (identical sequence to the producer)
+  int s_base = 0;
+  uint32_t ph_base = 0;
   const int ncols = P.ncols;
   const int64_t cb = P.col_begin;
   const size_t list_stride = (size_t)2 * nzcap;   // per column: 2 lists
@@ -279,8 +356,12 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
       for (int c = 0; c < T_; ++c) nfree += (S.col[c] < 0);
       int got = 0, start = 0;
       if (nfree > 0 && !std_error) {
-        start = atomicAdd(P.queue, nfree);
-        got = max(0, min(nfree, ncols - start));
+        // take at most a fair share of what is left, so the last wave stays balanced
+        const int left = ncols - *(volatile int*)P.queue;
+        const int share = max(1, (left + (int)gridDim.x - 1) / (int)gridDim.x);
+        const int want = min(nfree, share);
+        start = atomicAdd(P.queue, want);
+        got = max(0, min(want, ncols - start));
       }
       int nl = 0;
       for (int c = 0; c < T_ && nl < got; ++c)
@@ -318,6 +399,7 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
       for (int c = 0; c < T_; ++c) if (S.col[c] >= 0) A = c + 1;
       S.A = A;
       S.go = A > 0;
+      S.anychg[0] = S.anychg[1] = 0;
     }
     consumer_sync();
     // execute moves (R columns) and loads (r = x~_c, e = x_c - X*0)
@@ -343,9 +425,8 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
 
     // ---------------------------------------------------------------- one sweep over all rows
     const int NTa = (A + 7) >> 3;          // active n-tiles of 8 columns
-    const int mp = warp & 1;               // m-pair: rows mp*16 .. mp*16+15 of the block
-    const int ks = warp >> 1;              // k-quarter of every chunk (fixed reduction order)
-    const int g = lane >> 2, t4 = lane & 3;
+    const int grp = warp >> 2;             // chunk parity group: consumes chunks q = grp (mod 2)
+    const int wg = warp & 3;               // warp within the group (its 8x8-tile subtile)
 
     for (int b = 0; b < nblk; ++b) {
       const int j0 = b * J;
@@ -367,55 +448,33 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
           }
         }
       }
-      // -- Z = X_J^T R over all chunks (DMMA), k-steps ks*2, ks*2+1 of each chunk
-      double acc[2][4][2];
-#pragma unroll
-      for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt) acc[mi][nt][0] = acc[mi][nt][1] = 0.0;
-
-      for (int q = 0; q < nchunk; ++q, ++it) {
-        const int s = it % NST;
-        mbar_wait(&full[s], (it / NST) & 1u);
-        const double* xs = Xs + (size_t)s * CHUNK_DOUBLES + (size_t)(mp * 16 + g) * XS;
-        const double* rs = Rs + (size_t)g * SR + q * KC;
-#pragma unroll
-        for (int st = 0; st < 2; ++st) {
-          const int kk = (ks * 2 + st) * 4 + t4;
-          const double a0 = xs[kk];
-          const double a1 = xs[8 * XS + kk];
-#pragma unroll
-          for (int nt = 0; nt < 4; ++nt) {
-            if (nt < NTa) {
-              const double bb = rs[(size_t)nt * 8 * SR + kk];
-              dmma(acc[0][nt][0], acc[0][nt][1], a0, bb);
-              dmma(acc[1][nt][0], acc[1][nt][1], a1, bb);
-            }
-          }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
+      // -- Z = X_J^T R over this group's chunks (DMMA), partial sums to Zp[grp]
+      switch (NTa) {
+        case 4: gemm_block<2, 2>(Xs, Rs, Zp, full, empty, grp, 2 * (wg & 1), 2 * (wg >> 1), nchunk,
+                                 NST, s_base, ph_base, SR, T, lane); break;
+        case 3:
+          if (wg < 2) gemm_block<2, 2>(Xs, Rs, Zp, full, empty, grp, 2 * (wg & 1), 0, nchunk, NST,
+                                       s_base, ph_base, SR, T, lane);
+          else gemm_block<2, 1>(Xs, Rs, Zp, full, empty, grp, 2 * (wg & 1), 2, nchunk, NST,
+                                s_base, ph_base, SR, T, lane);
+          break;
+        case 2: gemm_block<2, 1>(Xs, Rs, Zp, full, empty, grp, 2 * (wg & 1), wg >> 1, nchunk, NST,
+                                 s_base, ph_base, SR, T, lane); break;
+        default: gemm_block<1, 1>(Xs, Rs, Zp, full, empty, grp, wg, 0, nchunk, NST, s_base,
+                                  ph_base, SR, T, lane); break;
       }
-      // -- partial sums to smem: Zp[ks][row][col]
-#pragma unroll
-      for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
-          if (nt < NTa) {
-            double* z = Zp + ((size_t)ks * J + mp * 16 + mi * 8 + g) * T + nt * 8 + 2 * t4;
-            z[0] = acc[mi][nt][0];
-            z[1] = acc[mi][nt][1];
-          }
+      s_base += nchunk;
+      while (s_base >= NST) { s_base -= NST; ph_base ^= 1u; }
       // -- previous coefficients of this block into Bt (zero, then scatter list entries)
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int c = warp + NCW * u;
         if (c < A) {
-          Bt[lane * T + c] = 0.0;
+          Bt[c * JP + lane] = 0.0;
           __syncwarp();
           const bool in = pf_row[u] < j0 + J;
           const unsigned m = __ballot_sync(0xffffffffu, in);
-          if (in) Bt[(pf_row[u] - j0) * T + c] = pf_val[u];
+          if (in) Bt[c * JP + (pf_row[u] - j0)] = pf_val[u];
           if (lane == 0) S.cursor[c] += __popc(m);
         }
       }
@@ -430,13 +489,10 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
           const int c = warp + NCW * u;
           if (c < A) {
             const int gcol = (int)(cb + S.col[c]);
-            double zs = Zp[((size_t)0 * J + jl) * T + c];
-            zs += Zp[((size_t)1 * J + jl) * T + c];
-            zs += Zp[((size_t)2 * J + jl) * T + c];
-            zs += Zp[((size_t)3 * J + jl) * T + c];
+            const double zs = Zp[(size_t)c * JP + jl] + Zp[((size_t)T + c) * JP + jl];
             const double z = zs / (double)n;                   // x_j^T e / n
-            Zp[(size_t)jl * T + c] = z;
-            const double bo = Bt[jl * T + c];
+            Zp[(size_t)c * JP + jl] = z;
+            const double bo = Bt[c * JP + jl];
             const bool valid = (j < p) && (j != gcol);
             const double a = z + bo;
             const double bn = soft(a, S.lam[c]);
@@ -489,16 +545,16 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
             if (j == gcol) continue;                             // b_cc = 0 (reading g6)
             double corr = 0.0;
             for (int m = 0; m < nch; ++m)
-              corr = fma(G[jl * J + chg_row[c * J + m]], chg_d[c * J + m], corr);
-            const double bo = Bt[jl * T + c];
-            const double a = (Zp[(size_t)jl * T + c] + corr) + bo;
+              corr = fma(G[jl * J + chg_row[m * T + c]], chg_d[m * T + c], corr);
+            const double bo = Bt[c * JP + jl];
+            const double a = (Zp[(size_t)c * JP + jl] + corr) + bo;
             const double bn = soft(a, lam);
             const double d = bo - bn;                            // e += x_j d
             if (d != 0.0) {
-              chg_row[c * J + nch] = (unsigned char)jl;
-              chg_d[c * J + nch] = d;
+              chg_row[nch * T + c] = (unsigned char)jl;
+              chg_d[nch * T + c] = d;
               ++nch;
-              Bt[jl * T + c] = bn;
+              Bt[c * JP + jl] = bn;
               md = fmax(md, fabs(d));
             }
           }
@@ -509,7 +565,7 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
           int cnt = S.cnt_new[c];
           const size_t o = (size_t)col * list_stride + (size_t)(S.cur[c] ^ 1) * nzcap;
           for (int jl = 0; jl < J; ++jl) {
-            const double v = Bt[jl * T + c];
+            const double v = Bt[c * JP + jl];
             if (v != 0.0) {
               if (cnt < nzcap) { P.nz_rows[o + cnt] = j0 + jl; P.nz_vals[o + cnt] = v; }
               else atomicExch(&P.flags[FLAG_OVERFLOW], 1);
@@ -529,7 +585,7 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
           for (int i = tid; i < n_pad; i += NCW * 32) {
             double v = r[i];
             for (int m = 0; m < nch; ++m)
-              v = fma(P.Xb[xb_index(i, j0 + chg_row[c * J + m], nchunk)], chg_d[c * J + m], v);
+              v = fma(P.Xb[xb_index(i, j0 + chg_row[m * T + c], nchunk)], chg_d[m * T + c], v);
             r[i] = v;
           }
         }
@@ -540,7 +596,7 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
 }
 
 cudaError_t launch_cd(const CDParams& P, int num_ctas, cudaStream_t s) {
-  const size_t smem = cd_smem_bytes(P.T, P.n_pad);
+  const size_t smem = smem_fixed_bytes(P.T, P.n_pad) + (size_t)P.nst * CHUNK_BYTES;
   cudaError_t e = cudaFuncSetAttribute(cd_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;

@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ Xb
   double acc[4] = {0, 0, 0, 0};
   for (int q = 0; q < nchunk; ++q) {
     const double* src = Xb + ((size_t)blk * nchunk + q) * CHUNK_DOUBLES;
-    for (int e = tid; e < J * KC; e += 256) t[e / KC][e % KC] = src[(e / KC) * XS + (e % KC)];
+    for (int e = tid; e < J * KC; e += 256) t[e / KC][e % KC] = src[(e / KC) * XS + xswz(e / KC, e % KC)];
     __syncthreads();
 #pragma unroll 4
     for (int kl = 0; kl < KC; ++kl) {

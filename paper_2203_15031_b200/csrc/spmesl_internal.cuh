@@ -1,11 +1,12 @@
 // Internal definitions shared by the SPMESL CUDA sources (product path only).
 //
 // HBM layout of the standardized predictors ("Xb", written by standardize_kernel):
-//   X~ (n x p) is stored in tiles of J = 32 predictor columns x KC = 32 samples, each tile
-//   row padded to XS = 36 doubles (36 = 4 mod 16 keeps the m8n8k4 fragment loads of
-//   8 rows x 4 consecutive k conflict-free in shared memory).  Tile (blk, q) holds
-//   x~_{blk*32 + jl}[q*32 + kl] at Xb[((blk*nchunk + q)*J + jl)*XS + kl] and is one
-//   contiguous 9216-byte block, so a single cp.async.bulk moves it into shared memory.
+//   X~ (n x p) is stored in tiles of J = 32 predictor columns x KC = 32 samples.  Tile
+//   (blk, q) is one contiguous, unpadded 8192-byte block (so one cp.async.bulk moves it to
+//   shared memory verbatim) holding x~_{blk*32 + jl}[q*32 + kl] at row jl, position
+//   kl ^ (8 (jl & 1)): odd rows have their two 64-byte halves swapped.  That XOR swizzle makes
+//   the paired-k 128-bit DMMA fragment loads (8 lanes = rows g, g+1 x 4 lanes, 16 B each) hit
+//   8 distinct 16-byte bank groups per phase without any padding bytes in HBM, L2 or smem.
 //   Samples i >= n and predictors j >= p are zero.
 #pragma once
 #include <cstdint>
@@ -15,11 +16,12 @@ namespace spmesl {
 
 constexpr int J = 32;                    // predictor rows per row block (CD visits rows block-wise)
 constexpr int KC = 32;                   // samples per staged X chunk
-constexpr int XS = KC + 4;               // padded chunk row stride (doubles)
-constexpr int CHUNK_DOUBLES = J * XS;    // 1152
-constexpr int CHUNK_BYTES = CHUNK_DOUBLES * 8;   // 9216
+constexpr int XS = KC;                   // chunk row stride (doubles), swizzled not padded
+constexpr int CHUNK_DOUBLES = J * XS;    // 1024
+constexpr int CHUNK_BYTES = CHUNK_DOUBLES * 8;   // 8192
 constexpr int NCW = 8;                   // consumer warps in the CD kernel
-constexpr int KSPLIT = 4;                // k-split of every dot product (fixed => deterministic)
+constexpr int KSPLIT = 2;                // k-split by chunk parity (fixed => deterministic)
+constexpr int RPAD = 8;                  // residual row padding (n_pad + 8 = 8 mod 16)
 constexpr int CD_THREADS = (NCW + 1) * 32;       // + 1 producer warp
 constexpr int MAX_T = 32;                // max resident columns (slots) per CTA
 
@@ -31,9 +33,12 @@ struct Layout {
   size_t xb_doubles() const { return (size_t)nblk * nchunk * CHUNK_DOUBLES; }
 };
 
+// position of k within row jl of a tile (the XOR swizzle above)
+__host__ __device__ inline int xswz(int jl, int kl) { return kl ^ ((jl & 1) << 3); }
+
 __host__ __device__ inline size_t xb_index(int64_t i, int64_t j, int nchunk) {
   int64_t blk = j / J, jl = j % J, q = i / KC, kl = i % KC;
-  return (size_t)(((blk * nchunk + q) * J + jl) * XS + kl);
+  return (size_t)(((blk * nchunk + q) * J + jl) * XS + xswz((int)jl, (int)kl));
 }
 
 // Error flags written by kernels (device int32[4]).
@@ -50,6 +55,7 @@ struct CDParams {
   double lambda0, tol, sigma_floor, sqrt_n;
   int max_outer, max_inner;
   int T;                   // resident columns per CTA (8, 16, 32)
+  int nst;                 // X chunk pipeline stages
   int nzcap;               // per-column capacity of each coefficient list
   int* queue;              // atomic head (local column index)
   int* flags;              // FLAG_*
@@ -64,7 +70,8 @@ struct CDParams {
   uint8_t* converged;      // [ncols]
 };
 
-size_t cd_smem_bytes(int T, int n_pad);
+size_t cd_smem_bytes(int T, int n_pad);          // with the minimum 2 stages
+int cd_stages(int T, int n_pad, size_t smem_optin);  // stages that fit (0: does not fit)
 
 // Launchers (stream-ordered, no host synchronisation).
 cudaError_t launch_standardize(const double* X, const Layout& L, int standardize, double* Xb,
