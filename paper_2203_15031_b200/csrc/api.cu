@@ -7,6 +7,7 @@
 //   -> one 64-byte readback of flags/counters.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -194,6 +195,13 @@ int run_cd(Workspace& W, const double* dX, int64_t n, int64_t p, int64_t cb, int
   P.T = T;
   P.nst = cd_stages(T, L.n_pad, W.smem_optin);
   P.nzcap = nzcap;
+  { const char* d = getenv("SPMESL_CD_DEBUG"); P.debug = d ? atoi(d) : 0; }
+  static long long* dbg_buf = nullptr;
+  if (P.debug & 4) {
+    if (!dbg_buf) cudaMalloc(&dbg_buf, 16 * sizeof(long long));
+    cudaMemsetAsync(dbg_buf, 0, 16 * sizeof(long long), s);
+  }
+  P.dbg = dbg_buf;
   P.queue = (int*)W.queue.ptr;
   P.flags = &dc->err;   // FLAG_CODE (unused by CD), FLAG_OVERFLOW at +1
   P.err_in = &dc->err;
@@ -208,6 +216,16 @@ int run_cd(Workspace& W, const double* dX, int64_t n, int64_t p, int64_t cb, int
   const int ctas = (int)std::min<int64_t>(W.sms, (m + T - 1) / T);
   *num_ctas = ctas;
   CUDA_TRY(launch_cd(P, ctas, s));
+  if (P.debug & 4) {
+    long long h[16];
+    cudaMemcpyAsync(h, dbg_buf, sizeof(h), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    const char* nm[3] = {"mma-g0", "mma-g1", "epi"};
+    for (int w = 0; w < 3; ++w)
+      fprintf(stderr, "[cd phases] %-6s work %.3f ms  step-barrier %.3f ms  r-update %.3f ms (avg/CTA @1.965GHz)\n", nm[w],
+              h[w * 4 + 0] / (double)ctas / 1.965e6, h[w * 4 + 1] / (double)ctas / 1.965e6,
+              h[w * 4 + 2] / (double)ctas / 1.965e6);
+  }
   CUDA_TRY(cudaEventRecord(W.ev[2], s));
   return SPMESL_OK;
 }
@@ -215,7 +233,7 @@ int run_cd(Workspace& W, const double* dX, int64_t n, int64_t p, int64_t cb, int
 int alloc_core(Workspace& W, const Layout& L, int64_t m, int nzcap) {
   int rc;
   if ((rc = ensure(W.xb, L.xb_doubles() * 8))) return rc;
-  if ((rc = ensure(W.gband, (size_t)L.nblk * J * J * 8))) return rc;
+  if ((rc = ensure(W.gband, (size_t)L.nblk * J * 2 * J * 8))) return rc;
   if ((rc = ensure(W.mean, (size_t)L.p * 8))) return rc;
   if ((rc = ensure(W.scale, (size_t)L.p * 8))) return rc;
   if ((rc = ensure(W.counters, sizeof(DevCounters)))) return rc;

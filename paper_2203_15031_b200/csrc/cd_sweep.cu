@@ -11,18 +11,22 @@
 // generalised to dynamic refill).  Columns only join at row 0, so each column sees the
 // exact cyclic order j = 0..p-1 of Algorithm 1.
 //
-// How 32 rows are processed at once ("blocked walk"):
-//   1. Z = X_J^T R_T for the 32 rows j0..j0+31 of the block and the T resident residuals R_T
-//      (a dense fp64 contraction over n: mma.sync m8n8k4 DMMA, operands in shared memory;
-//      X tiles stream HBM/L2 -> smem by cp.async.bulk on an mbarrier ring driven by a
-//      producer warp).
-//   2. Parallel epilogue: a_jc = Z_jc/n + b_jc and Soft for all 32 x T visits at once.  Until
-//      the first row where b_jc changes, these are exactly Algorithm 1's values.
-//   3. Only for columns with a change: a one-lane-per-column walk from that first row on,
-//      correcting later rows with G_J (x_j^T x_j'/n): a_jc += sum_{j' changed} G_jj' d_j'c.
-//   4. R_c += x_j d_jc for the (rare) changed visits.
-// Every dot product is reduced in one fixed order (k-split of 4 warps, summed 0..3), so a
-// column's result does not depend on its slot, its CTA, the tile occupancy or the GPU count.
+// Rows are processed in blocks of J = 32 with a lag-1 software pipeline:
+//   step t:  MMA warps      Z_t = X_{B_t}^T R / n      (dense fp64 contraction over n,
+//                           mma.sync m8n8k4 DMMA; X tiles stream L2 -> smem by
+//                           cp.async.bulk into two mbarrier rings fed by a producer warp)
+//            epilogue warps finish block t-1:
+//              a_jc = Z_{t-1}[j,c] + sum_{j' in B_{t-2} changed} G^x_{jj'} d_j'c + b_jc
+//              (R used by Z_{t-1} lacked block t-2's updates; G^x = x_j^T x_j'/n folds them
+//              in exactly), Soft for all 32 rows at once; columns with a change are walked
+//              row by row from the first changed row, adding G^w_{jj'} d_j'c for the changes
+//              earlier in the same block.
+//   between steps: R_c += x_j d_jc for block t-1's changes (rare; skipped when none).
+// This is Proposition 2's row order j = 0..p-1 with the residual identity
+// x_j^T (e + x_j' d) / n = x_j^T e / n + (x_j^T x_j' / n) d, i.e. the same iterates as
+// Algorithm 1 up to rounding.  Every dot product is reduced in one fixed order (chunk-parity
+// partials p0 + p1), so a column's result does not depend on its slot, its CTA, the tile
+// occupancy or the GPU count.
 //
 // Coefficients never live in a dense p x p array: each column keeps its nonzeros as a list
 // (rows ascending) rebuilt every sweep (double-buffered in HBM), read back with a cursor in
@@ -67,13 +71,21 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// Named barriers in their NON-aligned form (barrier.sync / barrier.arrive): several call
+// sites follow lane-divergent code, and the .aligned form that bar.sync denotes requires the
+// whole warp to arrive converged.  The __syncwarp() reconverges the warp first.
 __device__ __forceinline__ void named_bar_sync(int id, int count) {
-  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+  __syncwarp();
+  asm volatile("barrier.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
 }
 __device__ __forceinline__ void named_bar_arrive(int id, int count) {
-  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+  __syncwarp();
+  asm volatile("barrier.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
 }
-__device__ __forceinline__ void consumer_sync() { named_bar_sync(1, NCW * 32); }
+// barrier ids: 0 __syncthreads, 1 work warps (MMA + epilogue), 2 producer handshake,
+// 3..6 MMA warp pairs (wg, wg + 4)
+constexpr int BAR_WORK = 1, BAR_PROD = 2, BAR_PAIR0 = 3;
+__device__ __forceinline__ void work_sync() { named_bar_sync(BAR_WORK, WORK_THREADS); }
 
 // D(8x8) += A(8x4, row) * B(4x8, col), fp64 tensor-core MMA.
 // Fragments (verified on B200, microbench/peaks.cu): lane = 4g + t;
@@ -90,7 +102,11 @@ __device__ __forceinline__ double soft(double a, double lam) {
   return m > 0.0 ? copysign(m, a) : 0.0;
 }
 
-constexpr int MAX_NST = 12; // max X chunk pipeline depth (runtime: as many as smem allows)
+constexpr int MAX_NST = 12;  // max X chunk pipeline depth (runtime: as many as smem allows)
+
+// development-only phase timers (P.debug & 4): per-CTA cycle totals in P.dbg[cta][16]
+#define PH_T0() long long _t0 = (P.debug & 4) ? clock64() : 0
+#define PH_ADD(slot) do { if (P.debug & 4) { long long _t1 = clock64(); if (lane == 0) dbg_acc[slot] += _t1 - _t0; _t0 = _t1; } } while (0)
 constexpr int JP = J + 1;    // padded row-block stride of the per-column [c][row] tiles
 
 struct SlotState {
@@ -103,8 +119,8 @@ struct SlotState {
   int cnt_old[MAX_T];
   int cnt_new[MAX_T];
   int cursor[MAX_T];
-  int first[MAX_T];     // first changed row in the current block (J = none)
-  int nchg[MAX_T];
+  int first[MAX_T];     // first changed row in the block being finished (J = none)
+  int nchg[2][MAX_T];   // changes per column in the block of parity x
   int retire[MAX_T];
   double sigma[MAX_T];
   double lam[MAX_T];
@@ -112,20 +128,18 @@ struct SlotState {
   // control
   int A;
   int go;
-  int anychg[2];
   int nmoves, nloads;
   int mv_dst[MAX_T], mv_src[MAX_T];
   int ld_dst[MAX_T];
 };
 
-// Shared-memory carve-up (bytes), given T slots, padded n and the pipeline depth.
+// Shared-memory carve-up (bytes) for T slots and padded n (plus the X ring).
 static __host__ __device__ size_t smem_fixed_bytes(int T, int n_pad) {
   size_t b = 0;
-  b += (size_t)T * (n_pad + RPAD) * 8;  // Rs   [T][n_pad+RPAD]
-  b += (size_t)KSPLIT * T * JP * 8;     // Zp   [KSPLIT][T][JP]
-  b += (size_t)T * JP * 8;              // Bt   [T][JP]
-  b += (size_t)J * T * 8;               // chg_d  [J][T]
-  b += (size_t)J * T;                   // chg_row[J][T]
+  b += (size_t)T * (n_pad + RPAD) * 8;  // Rs      [T][n_pad+RPAD]
+  b += (size_t)2 * T * JP * 8;          // Zp      [2 (block parity)][T][JP]
+  b += (size_t)2 * J * T * 8;           // chg_d   [2][J][T]
+  b += (size_t)2 * J * T;               // chg_row [2][J][T]
   b = (b + 15) & ~(size_t)15;
   b += sizeof(SlotState);
   b = (b + 15) & ~(size_t)15;
@@ -137,34 +151,33 @@ static __host__ __device__ size_t smem_fixed_bytes(int T, int n_pad) {
 int cd_stages(int T, int n_pad, size_t smem_optin) {
   const size_t fixed = smem_fixed_bytes(T, n_pad);
   if (fixed + 2 * (size_t)CHUNK_BYTES > smem_optin) return 0;
-  return (int)std::min<size_t>(MAX_NST, (smem_optin - fixed) / CHUNK_BYTES);
+  // even: the stages are split between the two parity-group rings
+  return (int)std::min<size_t>(MAX_NST, (smem_optin - fixed) / CHUNK_BYTES) & ~1;
 }
 
 size_t cd_smem_bytes(int T, int n_pad) {     // minimum (2 stages)
   return smem_fixed_bytes(T, n_pad) + 2 * (size_t)CHUNK_BYTES;
 }
 
-// One row block's contraction Z(32 x 8NTa) = X_J^T R for the chunks q = grp (mod 2) of this
-// warp's parity group, for the warp's MT x NT subtile of 8x8 tiles starting at (m0, n0).
+// One row block's contraction for the chunks q = grp (mod 2) of this warp's parity group,
+// for the warp's MT x NT subtile of 8x8 tiles starting at (m0, n0); the two parity partials
+// of a subtile (warps wg and wg+4) are combined as (p0 + p1) * (1/n) into Zb[col][row].
 // Paired-k fragments: for k-pair kp of a chunk, lane (g, t) loads the 2 consecutive samples
 // k = 8kp + 2t, 8kp + 2t + 1 of row g with one 128-bit LDS; the first DMMA takes the even
-// sample, the second the odd one (the same k mapping for A and B, so the sum is exact up to
-// its fixed association).  Each output's accumulation order depends only on k, never on the
-// subtile mapping, so results are independent of NTa and of the column's slot.
-template <int MT, int NT>
+// sample, the second the odd one (the same k mapping for A and B).  Each output's
+// accumulation order depends only on k, never on the subtile mapping, so results are
+// independent of NTa and of the column's slot.
+template <int MT, int NT, bool COMPUTE>
 __device__ __forceinline__ void gemm_block(const double* __restrict__ Xs, const double* __restrict__ Rs,
-                                           double* __restrict__ Zp, uint64_t* full, uint64_t* empty,
-                                           int grp, int m0, int n0, int nchunk, int NST, int s_base,
-                                           uint32_t ph_base, int SR, int T, int lane) {
+                                           double* __restrict__ Zb, uint64_t* full, uint64_t* empty,
+                                           int grp, int wg, int m0, int n0, int nchunk, int NSTG,
+                                           int& s, uint32_t& ph, int SR, double inv_n, int lane) {
   const int g = lane >> 2, t4 = lane & 3;
   double acc[MT][NT][2];
 #pragma unroll
   for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
     for (int ni = 0; ni < NT; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-  int s = s_base + grp;
-  uint32_t ph = ph_base;
-  if (s >= NST) { s -= NST; ph ^= 1u; }
   const double* rbase = Rs + (size_t)(n0 * 8 + g) * SR + 2 * t4;
   for (int q = grp; q < nchunk; q += 2) {
     mbar_wait(&full[s], ph);
@@ -172,7 +185,7 @@ __device__ __forceinline__ void gemm_block(const double* __restrict__ Xs, const 
     const double* rs = rbase + q * KC;
     const int sw = g & 1;                 // row parity of this lane's A rows (xswz)
 #pragma unroll
-    for (int kp = 0; kp < KC / 8; ++kp) {
+    for (int kp = 0; kp < (COMPUTE ? KC / 8 : 0); ++kp) {
       double2 a[MT], bb[NT];
 #pragma unroll
       for (int mi = 0; mi < MT; ++mi) a[mi] = *(const double2*)(xs + mi * 8 * XS + (kp ^ sw) * 8);
@@ -189,18 +202,60 @@ __device__ __forceinline__ void gemm_block(const double* __restrict__ Xs, const 
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
-    s += 2;
-    if (s >= NST) { s -= NST; ph ^= 1u; }
+    if (++s == NSTG) { s = 0; ph ^= 1u; }
   }
-  // partial sums: Zp[grp][col][row]
+  // parity-1 partial -> Zb, pair barrier, parity-0 warp adds its partial and scales by 1/n
+  if (grp == 1) {
 #pragma unroll
-  for (int mi = 0; mi < MT; ++mi)
+    for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
-    for (int ni = 0; ni < NT; ++ni) {
-      double* z = Zp + ((size_t)grp * T + (n0 + ni) * 8 + 2 * t4) * JP + (m0 + mi) * 8 + g;
-      z[0] = acc[mi][ni][0];
-      z[JP] = acc[mi][ni][1];
-    }
+      for (int ni = 0; ni < NT; ++ni) {
+        double* z = Zb + (size_t)((n0 + ni) * 8 + 2 * t4) * JP + (m0 + mi) * 8 + g;
+        z[0] = acc[mi][ni][0];
+        z[JP] = acc[mi][ni][1];
+      }
+  }
+  named_bar_sync(BAR_PAIR0 + wg, 64);
+  if (grp == 0) {
+#pragma unroll
+    for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < NT; ++ni) {
+        double* z = Zb + (size_t)((n0 + ni) * 8 + 2 * t4) * JP + (m0 + mi) * 8 + g;
+        z[0] = (acc[mi][ni][0] + z[0]) * inv_n;
+        z[JP] = (acc[mi][ni][1] + z[JP]) * inv_n;
+      }
+  }
+}
+
+// Subtile mapping of the 4 warps of a parity group for NTa active n-tiles.
+template <bool COMPUTE>
+__device__ __forceinline__ void run_gemm(int NTa, int grp, int wg, const double* Xs,
+                                         const double* Rs, double* Zb, uint64_t* full,
+                                         uint64_t* empty, int nchunk, int NSTG, int& s,
+                                         uint32_t& ph, int SR, double inv_n, int lane) {
+  switch (NTa) {
+    case 4:
+      gemm_block<2, 2, COMPUTE>(Xs, Rs, Zb, full, empty, grp, wg, 2 * (wg & 1), 2 * (wg >> 1),
+                                nchunk, NSTG, s, ph, SR, inv_n, lane);
+      break;
+    case 3:
+      if (wg < 2)
+        gemm_block<2, 2, COMPUTE>(Xs, Rs, Zb, full, empty, grp, wg, 2 * (wg & 1), 0, nchunk, NSTG,
+                                  s, ph, SR, inv_n, lane);
+      else
+        gemm_block<2, 1, COMPUTE>(Xs, Rs, Zb, full, empty, grp, wg, 2 * (wg & 1), 2, nchunk, NSTG,
+                                  s, ph, SR, inv_n, lane);
+      break;
+    case 2:
+      gemm_block<2, 1, COMPUTE>(Xs, Rs, Zb, full, empty, grp, wg, 2 * (wg & 1), wg >> 1, nchunk,
+                                NSTG, s, ph, SR, inv_n, lane);
+      break;
+    default:
+      gemm_block<1, 1, COMPUTE>(Xs, Rs, Zb, full, empty, grp, wg, wg, 0, nchunk, NSTG, s, ph, SR,
+                                inv_n, lane);
+      break;
+  }
 }
 
 __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams P) {
@@ -208,14 +263,13 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int T = P.T;
   const int SR = P.n_pad + RPAD;
-  const int NST = P.nst;
+  const int NSTG = P.nst / KSPLIT;   // stages per parity-group ring
   double* Rs = (double*)smem_raw;                               // [T][SR]
-  double* Zp = Rs + (size_t)T * SR;                             // [KSPLIT][T][JP]
-  double* Bt = Zp + (size_t)KSPLIT * T * JP;                    // [T][JP]
-  double* chg_d = Bt + (size_t)T * JP;                          // [J][T]
-  unsigned char* chg_row = (unsigned char*)(chg_d + (size_t)J * T);  // [J][T]
-  size_t off = (size_t)T * SR * 8 + (size_t)KSPLIT * T * JP * 8 + (size_t)T * JP * 8 +
-               (size_t)J * T * 8 + (size_t)J * T;
+  double* Zp = Rs + (size_t)T * SR;                             // [2][T][JP]
+  double* chg_d = Zp + (size_t)2 * T * JP;                      // [2][J][T]
+  unsigned char* chg_row = (unsigned char*)(chg_d + (size_t)2 * J * T);  // [2][J][T]
+  size_t off = (size_t)T * SR * 8 + (size_t)2 * T * JP * 8 + (size_t)2 * J * T * 8 +
+               (size_t)2 * J * T;
   off = (off + 15) & ~(size_t)15;
   SlotState& S = *(SlotState*)(smem_raw + off);
   off += sizeof(SlotState);
@@ -224,16 +278,20 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
   uint64_t* empty = full + MAX_NST;
   off += 2 * MAX_NST * 8;
   off = (off + 127) & ~(size_t)127;
-  double* Xs = (double*)(smem_raw + off);                       // [NST][J][XS]
+  double* Xs = (double*)(smem_raw + off);                       // [2 rings][NSTG][J][XS]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = P.n, n_pad = P.n_pad, nchunk = P.nchunk, p = P.p, nblk = P.nblk;
   const int nzcap = P.nzcap;
+  const double inv_n = 1.0 / (double)n;
+  long long dbg_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 
   if (tid == 0) {
-    for (int s = 0; s < NST; ++s) {
+    // one ring per parity group: every phase of a stage is consumed by the same 4 warps, so a
+    // parity wait can never alias a phase two rounds back
+    for (int s = 0; s < KSPLIT * NSTG; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NCW / KSPLIT);   // the 4 warps of the chunk's parity group
+      mbar_init(&empty[s], NMW / KSPLIT);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -241,27 +299,30 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
   for (int c = tid; c < MAX_T; c += blockDim.x) {
     S.col[c] = -1;
     S.retire[c] = 0;
+    S.nchg[0][c] = S.nchg[1][c] = 0;
   }
   for (size_t e = tid; e < (size_t)T * SR; e += blockDim.x) Rs[e] = 0.0;
-  if (tid == 0) { S.A = 0; S.anychg[0] = S.anychg[1] = 0; }
+  if (tid == 0) S.A = 0;
   __syncthreads();
 
   // ===================================================== producer warp: X tile stream
-  if (warp == NCW) {
-    int s = 0;
-    uint32_t ph = 0;
+  if (warp == PRODUCER_WARP) {
+    int sg[KSPLIT] = {0, 0};
+    uint32_t phg[KSPLIT] = {0u, 0u};
     for (;;) {
-      named_bar_sync(2, CD_THREADS);
+      named_bar_sync(BAR_PROD, CD_THREADS);
       int go = *(volatile int*)&S.go;
       if (!go) break;
       if (lane == 0) {
         const double* src = P.Xb;
         for (int b = 0; b < nblk; ++b)
           for (int q = 0; q < nchunk; ++q, src += CHUNK_DOUBLES) {
-            mbar_wait(&empty[s], ph ^ 1u);
-            mbar_arrive_expect_tx(&full[s], CHUNK_BYTES);
-            bulk_g2s(Xs + (size_t)s * CHUNK_DOUBLES, src, CHUNK_BYTES, &full[s]);
-            if (++s == NST) { s = 0; ph ^= 1u; }
+            const int g = q & 1;
+            const int st = g * NSTG + sg[g];
+            mbar_wait(&empty[st], phg[g] ^ 1u);
+            mbar_arrive_expect_tx(&full[st], CHUNK_BYTES);
+            bulk_g2s(Xs + (size_t)st * CHUNK_DOUBLES, src, CHUNK_BYTES, &full[st]);
+            if (++sg[g] == NSTG) { sg[g] = 0; phg[g] ^= 1u; }
           }
       }
       __syncwarp();
@@ -269,20 +330,25 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
     return;
   }
 
-  // ===================================================== consumer warps
+  // ===================================================== work warps (MMA 0..7, epilogue 8..9)
+  const bool is_mma = warp < NMW;
+  const int grp = (warp >> 2) & 1;       // MMA: chunk parity group (consumes chunks q = grp mod 2)
+  const int wg = warp & 3;               // MMA: warp within the group (its subtile)
   const bool std_error = (*(volatile const int*)P.err_in) != 0;
-  // ring position of the first chunk of the current block (identical sequence to the producer)
-  int s_base = 0;
-  uint32_t ph_base = 0;
+  int ring_s = 0;                        // MMA: position in this group's ring
+  uint32_t ring_ph = 0;
   const int ncols = P.ncols;
   const int64_t cb = P.col_begin;
   const size_t list_stride = (size_t)2 * nzcap;   // per column: 2 lists
+  const double* Xr = Xs + (size_t)grp * NSTG * CHUNK_DOUBLES;
+  uint64_t* fr = full + grp * NSTG;
+  uint64_t* er = empty + grp * NSTG;
 
   for (bool first_round = true;; first_round = false) {
     // ---------------------------------------------------------------- sweep boundary
     if (!first_round) {
-      // (a) per-slot end-of-sweep logic; warp w owns slots c = w (mod 8)
-      for (int c = warp; c < S.A; c += NCW) {
+      // (a) per-slot end-of-sweep logic; work warp w owns slots c = w (mod NWORK)
+      for (int c = warp; c < S.A; c += NWORK) {
         const int col = S.col[c];
         // the list built in this sweep becomes the current coefficients
         const int cur = S.cur[c] ^ 1;
@@ -345,11 +411,11 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
           }
         }
       }
-      consumer_sync();
+      work_sync();
     }
     // ---------------------------------------------------------------- refill / compaction plan
     if (tid == 0) {
-      int T_ = T;
+      const int T_ = T;
       for (int c = 0; c < S.A; ++c)
         if (S.retire[c]) { S.col[c] = -1; S.retire[c] = 0; }
       int nfree = 0;
@@ -376,7 +442,8 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
           S.maxd[c] = 0.0;
         }
       S.nloads = nl;
-      // compaction: move the highest active slots into the lowest holes
+      // compaction: move the highest active slots into the lowest holes (loads took the
+      // lowest holes, so a loaded slot never moves)
       int nm = 0;
       int lo = 0, hi = T_ - 1;
       for (;;) {
@@ -389,209 +456,171 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
         S.cnt_old[lo] = S.cnt_old[hi]; S.cnt_new[lo] = 0; S.cursor[lo] = 0;
         S.sigma[lo] = S.sigma[hi]; S.lam[lo] = S.lam[hi]; S.maxd[lo] = 0.0;
         S.col[hi] = -1;
-        // a slot loaded this round may move (only if holes remain below it, impossible since
-        // loads fill the lowest holes first) — keep the load target map consistent anyway
-        for (int l = 0; l < nl; ++l)
-          if (S.ld_dst[l] == hi) S.ld_dst[l] = lo;
       }
       S.nmoves = nm;
       int A = 0;
       for (int c = 0; c < T_; ++c) if (S.col[c] >= 0) A = c + 1;
       S.A = A;
       S.go = A > 0;
-      S.anychg[0] = S.anychg[1] = 0;
+      for (int c = 0; c < MAX_T; ++c) S.nchg[0][c] = S.nchg[1][c] = 0;
     }
-    consumer_sync();
+    work_sync();
     // execute moves (R columns) and loads (r = x~_c, e = x_c - X*0)
     {
       const int nm = S.nmoves, nl = S.nloads;
       for (int m = 0; m < nm; ++m) {
         const double* src = Rs + (size_t)S.mv_src[m] * SR;
         double* dst = Rs + (size_t)S.mv_dst[m] * SR;
-        for (int i = tid; i < n_pad; i += NCW * 32) dst[i] = src[i];
+        for (int i = tid; i < n_pad; i += WORK_THREADS) dst[i] = src[i];
       }
       for (int l = 0; l < nl; ++l) {
         const int c = S.ld_dst[l];
         const int64_t gcol = cb + S.col[c];
         double* dst = Rs + (size_t)c * SR;
-        for (int i = tid; i < n_pad; i += NCW * 32) dst[i] = P.Xb[xb_index(i, gcol, nchunk)];
+        for (int i = tid; i < n_pad; i += WORK_THREADS) dst[i] = P.Xb[xb_index(i, gcol, nchunk)];
       }
     }
     const int A = S.A;
     __threadfence_block();
-    consumer_sync();
-    named_bar_arrive(2, CD_THREADS);   // release the producer for this sweep (or exit)
+    work_sync();
+    named_bar_arrive(BAR_PROD, CD_THREADS);   // release the producer for this sweep (or exit)
     if (A == 0) break;
 
-    // ---------------------------------------------------------------- one sweep over all rows
+    // ---------------------------------------------------------------- one sweep, lag-1 pipeline
     const int NTa = (A + 7) >> 3;          // active n-tiles of 8 columns
-    const int grp = warp >> 2;             // chunk parity group: consumes chunks q = grp (mod 2)
-    const int wg = warp & 3;               // warp within the group (its 8x8-tile subtile)
-
-    for (int b = 0; b < nblk; ++b) {
-      const int j0 = b * J;
-      // -- prefetch this block's previous coefficients from each column's sorted list
-      int pf_row[4];
-      double pf_val[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int c = warp + NCW * u;
-        pf_row[u] = 0x7fffffff;
-        pf_val[u] = 0.0;
-        if (c < A) {
-          const int col = S.col[c];
-          const int idx = S.cursor[c] + lane;
-          if (idx < S.cnt_old[c] && idx < nzcap) {
-            const size_t o = (size_t)col * list_stride + (size_t)S.cur[c] * nzcap + idx;
-            pf_row[u] = P.nz_rows[o];
-            pf_val[u] = P.nz_vals[o];
-          }
-        }
-      }
-      // -- Z = X_J^T R over this group's chunks (DMMA), partial sums to Zp[grp]
-      switch (NTa) {
-        case 4: gemm_block<2, 2>(Xs, Rs, Zp, full, empty, grp, 2 * (wg & 1), 2 * (wg >> 1), nchunk,
-                                 NST, s_base, ph_base, SR, T, lane); break;
-        case 3:
-          if (wg < 2) gemm_block<2, 2>(Xs, Rs, Zp, full, empty, grp, 2 * (wg & 1), 0, nchunk, NST,
-                                       s_base, ph_base, SR, T, lane);
-          else gemm_block<2, 1>(Xs, Rs, Zp, full, empty, grp, 2 * (wg & 1), 2, nchunk, NST,
-                                s_base, ph_base, SR, T, lane);
-          break;
-        case 2: gemm_block<2, 1>(Xs, Rs, Zp, full, empty, grp, 2 * (wg & 1), wg >> 1, nchunk, NST,
-                                 s_base, ph_base, SR, T, lane); break;
-        default: gemm_block<1, 1>(Xs, Rs, Zp, full, empty, grp, wg, 0, nchunk, NST, s_base,
-                                  ph_base, SR, T, lane); break;
-      }
-      s_base += nchunk;
-      while (s_base >= NST) { s_base -= NST; ph_base ^= 1u; }
-      // -- previous coefficients of this block into Bt (zero, then scatter list entries)
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int c = warp + NCW * u;
-        if (c < A) {
-          Bt[c * JP + lane] = 0.0;
-          __syncwarp();
-          const bool in = pf_row[u] < j0 + J;
-          const unsigned m = __ballot_sync(0xffffffffu, in);
-          if (in) Bt[c * JP + (pf_row[u] - j0)] = pf_val[u];
-          if (lane == 0) S.cursor[c] += __popc(m);
-        }
-      }
-      consumer_sync();  // ---- #1: Z partials, Bt ready
-      if (tid == 0) S.anychg[(b + 1) & 1] = 0;
-      // -- parallel epilogue: warp w owns columns c = w (mod 8), lane = row jl
-      {
-        const int jl = lane;
-        const int j = j0 + jl;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int c = warp + NCW * u;
-          if (c < A) {
-            const int gcol = (int)(cb + S.col[c]);
-            const double zs = Zp[(size_t)c * JP + jl] + Zp[((size_t)T + c) * JP + jl];
-            const double z = zs / (double)n;                   // x_j^T e / n
-            Zp[(size_t)c * JP + jl] = z;
-            const double bo = Bt[c * JP + jl];
-            const bool valid = (j < p) && (j != gcol);
-            const double a = z + bo;
-            const double bn = soft(a, S.lam[c]);
-            const bool chg = valid && (bn != bo);
-            const unsigned mask = __ballot_sync(0xffffffffu, chg);
-            if (mask == 0u) {
-              // no change: the coefficients of this block are final; append nonzeros
-              const bool nz = bo != 0.0;
-              const unsigned nzm = __ballot_sync(0xffffffffu, nz);
-              if (nzm) {
-                const int basecnt = S.cnt_new[c];
-                if (nz) {
-                  const int pos = basecnt + __popc(nzm & ((1u << lane) - 1u));
-                  if (pos < nzcap) {
-                    const int col = S.col[c];
-                    const size_t o = (size_t)col * list_stride + (size_t)(S.cur[c] ^ 1) * nzcap + pos;
-                    P.nz_rows[o] = j;
-                    P.nz_vals[o] = bo;
-                  }
-                }
-                __syncwarp();
-                if (lane == 0) {
-                  S.cnt_new[c] = basecnt + __popc(nzm);
-                  if (basecnt + __popc(nzm) > nzcap) atomicExch(&P.flags[FLAG_OVERFLOW], 1);
-                }
-              }
-              if (lane == 0) S.first[c] = J;
-            } else {
-              if (lane == 0) {
-                S.first[c] = __ffs(mask) - 1;
-                S.anychg[b & 1] = 1;
-              }
-            }
-          }
-        }
-      }
-      consumer_sync();  // ---- #2
-      if (S.anychg[b & 1]) {
-        // -- sequential walk for columns with a change (one lane per column)
-        if (warp == 0 && lane < A && S.first[lane] < J) {
-          const int c = lane;
-          const int gcol = (int)(cb + S.col[c]);
-          const double lam = S.lam[c];
-          const double* G = P.Gband + (size_t)b * J * J;
-          double md = S.maxd[c];
-          int nch = 0;
-          for (int jl = S.first[c]; jl < J; ++jl) {
-            const int j = j0 + jl;
-            if (j >= p) break;
-            if (j == gcol) continue;                             // b_cc = 0 (reading g6)
-            double corr = 0.0;
-            for (int m = 0; m < nch; ++m)
-              corr = fma(G[jl * J + chg_row[m * T + c]], chg_d[m * T + c], corr);
-            const double bo = Bt[c * JP + jl];
-            const double a = (Zp[(size_t)c * JP + jl] + corr) + bo;
-            const double bn = soft(a, lam);
-            const double d = bo - bn;                            // e += x_j d
-            if (d != 0.0) {
-              chg_row[nch * T + c] = (unsigned char)jl;
-              chg_d[nch * T + c] = d;
-              ++nch;
-              Bt[c * JP + jl] = bn;
-              md = fmax(md, fabs(d));
-            }
-          }
-          S.maxd[c] = md;
-          S.nchg[c] = nch;
-          // append the block's final nonzeros in row order
-          const int col = S.col[c];
-          int cnt = S.cnt_new[c];
-          const size_t o = (size_t)col * list_stride + (size_t)(S.cur[c] ^ 1) * nzcap;
-          for (int jl = 0; jl < J; ++jl) {
-            const double v = Bt[c * JP + jl];
-            if (v != 0.0) {
-              if (cnt < nzcap) { P.nz_rows[o + cnt] = j0 + jl; P.nz_vals[o + cnt] = v; }
-              else atomicExch(&P.flags[FLAG_OVERFLOW], 1);
-              ++cnt;
-            }
-          }
-          S.cnt_new[c] = cnt;
-        } else if (warp == 0 && lane < A) {
-          S.nchg[lane] = 0;
-        }
-        consumer_sync();  // ---- #3
-        // -- residual updates e_c += x_j d for the changed visits (Prop. 2)
-        for (int c = 0; c < A; ++c) {
-          const int nch = S.nchg[c];
-          if (nch == 0) continue;
-          double* r = Rs + (size_t)c * SR;
-          for (int i = tid; i < n_pad; i += NCW * 32) {
-            double v = r[i];
-            for (int m = 0; m < nch; ++m)
-              v = fma(P.Xb[xb_index(i, j0 + chg_row[m * T + c], nchunk)], chg_d[m * T + c], v);
-            r[i] = v;
-          }
-        }
-        consumer_sync();  // ---- #4
-      }
+    // epilogue warp: lane = column; the column's state lives in registers for the sweep
+    const bool c_act = !is_mma && lane < A;
+    int gcol = 0, cnt_old = 0, cursor = 0, cnt_new = 0, nx_row = 0x7fffffff;
+    double lam = 0.0, maxd = 0.0, nx_val = 0.0;
+    const int* lst_old_r = nullptr;
+    const double* lst_old_v = nullptr;
+    int* lst_new_r = nullptr;
+    double* lst_new_v = nullptr;
+    if (c_act) {
+      const int col = S.col[lane];
+      gcol = (int)(cb + col);
+      lam = S.lam[lane];
+      cnt_old = S.cnt_old[lane];
+      const size_t base = (size_t)col * list_stride;
+      lst_old_r = P.nz_rows + base + (size_t)S.cur[lane] * nzcap;
+      lst_old_v = P.nz_vals + base + (size_t)S.cur[lane] * nzcap;
+      lst_new_r = P.nz_rows + base + (size_t)(S.cur[lane] ^ 1) * nzcap;
+      lst_new_v = P.nz_vals + base + (size_t)(S.cur[lane] ^ 1) * nzcap;
+      if (cnt_old > 0) { nx_row = lst_old_r[0]; nx_val = lst_old_v[0]; }
     }
+    for (int t = 0; t <= nblk; ++t) {
+      PH_T0();
+      if (is_mma) {
+        // ======== MMA warps: Z_t
+        if (t < nblk) {
+          double* Zb = Zp + (size_t)(t & 1) * T * JP;
+          if (P.debug & 1)
+            run_gemm<false>(NTa, grp, wg, Xr, Rs, Zb, fr, er, nchunk, NSTG, ring_s, ring_ph, SR,
+                            inv_n, lane);
+          else
+            run_gemm<true>(NTa, grp, wg, Xr, Rs, Zb, fr, er, nchunk, NSTG, ring_s, ring_ph, SR,
+                           inv_n, lane);
+        }
+      } else if (c_act) {
+        // ======== epilogue warp, lane = column c: finish block b = t-1 row by row
+        if (t >= 1 && !(P.debug & 2)) {
+          const int b = t - 1;
+          const int j0 = b * J;
+          const int xb = b & 1, xp = xb ^ 1;   // chg buffers: this block / previous block
+          const double* Zc = Zp + (size_t)xb * T * JP + (size_t)lane * JP;
+          const double* Gb = P.Gband + (size_t)b * J * (2 * J);   // [r][Gx(32) | Gw(32)]
+          const int np = (b >= 1) ? S.nchg[xp][lane] : 0;         // block b-1's changes
+          // fast path (almost every visit): b_old = 0 on all 32 rows, no correction from block
+          // b-1, and |z| <= lambda on every valid row => nothing changes, no nonzero to list.
+          // Soft(z, lam) != 0  <=>  |z| - lam > 0  <=>  |z| > lam for finite doubles.
+          // (branch-free: all 32 loads issue back to back, predicates combined bitwise)
+          double zv[J];
+#pragma unroll
+          for (int r = 0; r < J; ++r) zv[r] = Zc[r];
+          unsigned hit = 0u;
+#pragma unroll
+          for (int r = 0; r < J; ++r) hit |= (unsigned)(fabs(zv[r]) > lam) << r;
+          // rows that are valid predictors: j < p and j != this column's own index
+          unsigned valid = (j0 + J <= p) ? 0xffffffffu : ((1u << (p - j0)) - 1u);
+          if (gcol >= j0 && gcol < j0 + J) valid &= ~(1u << (gcol - j0));
+          hit &= valid;
+          int nch = 0;
+          if (hit != 0u || np != 0 || nx_row < j0 + J) {
+            // general path: the rows of this block in order (Algorithm 1's cyclic order)
+            for (int r = 0; r < J; ++r) {
+              const int j = j0 + r;
+              double z = Zc[r];
+              // R lacked block b-1's updates when Z_b was formed: add G^x_{jj'} d_j'
+              for (int m = 0; m < np; ++m)
+                z = fma(Gb[r * 2 * J + chg_row[(xp * J + m) * T + lane]],
+                        chg_d[(xp * J + m) * T + lane], z);
+              // and this block's earlier changes: G^w_{jj'} d_j'
+              for (int m = 0; m < nch; ++m)
+                z = fma(Gb[r * 2 * J + J + chg_row[(xb * J + m) * T + lane]],
+                        chg_d[(xb * J + m) * T + lane], z);
+              // previous coefficient b_jc: merge with the column's sorted list of the last sweep
+              double bo = 0.0;
+              if (nx_row == j) {
+                bo = nx_val;
+                ++cursor;
+                nx_row = 0x7fffffff;
+                if (cursor < cnt_old && cursor < nzcap) { nx_row = lst_old_r[cursor]; nx_val = lst_old_v[cursor]; }
+              }
+              if (j < p && j != gcol) {
+                const double bn = soft(z + bo, lam);
+                const double d = bo - bn;                        // e += x_j d
+                if (d != 0.0) {
+                  chg_row[(xb * J + nch) * T + lane] = (unsigned char)r;
+                  chg_d[(xb * J + nch) * T + lane] = d;
+                  ++nch;
+                  maxd = fmax(maxd, fabs(d));
+                }
+                if (bn != 0.0) {                                 // this sweep's list
+                  if (cnt_new < nzcap) { lst_new_r[cnt_new] = j; lst_new_v[cnt_new] = bn; }
+                  else atomicExch(&P.flags[FLAG_OVERFLOW], 1);
+                  ++cnt_new;
+                }
+              }
+            }
+          }
+          S.nchg[xb][lane] = nch;
+        }
+      }
+      PH_ADD(0);     // slot 0: this warp's own work in the step
+      work_sync();   // ---- end of step t
+      PH_ADD(1);     // slot 1: waiting at the step barrier
+      // -- residual updates e_c += x_j d for block t-1's changes (Prop. 2); rare
+      if (t >= 1) {
+        const int xb = (t - 1) & 1;
+        const bool any = __any_sync(0xffffffffu, lane < A && S.nchg[xb][lane] > 0);
+        if (any) {
+          const int j0 = (t - 1) * J;
+          for (int c = 0; c < A; ++c) {
+            const int nch = S.nchg[xb][c];
+            if (nch == 0) continue;
+            double* r = Rs + (size_t)c * SR;
+            for (int i = tid; i < n_pad; i += WORK_THREADS) {
+              double v = r[i];
+              for (int m = 0; m < nch; ++m)
+                v = fma(P.Xb[xb_index(i, j0 + chg_row[(xb * J + m) * T + c], nchunk)],
+                        chg_d[(xb * J + m) * T + c], v);
+              r[i] = v;
+            }
+          }
+          work_sync();
+        }
+      }
+      PH_ADD(2);     // slot 2: residual updates between steps
+    }
+    if (c_act) {
+      S.maxd[lane] = maxd;
+      S.cnt_new[lane] = cnt_new;
+    }
+    work_sync();
+  }
+  if ((P.debug & 4) && lane == 0 && (warp == 0 || warp == 4 || warp == NMW)) {
+    const int w = warp == 0 ? 0 : (warp == 4 ? 1 : 2);
+    for (int k = 0; k < 3; ++k) atomicAdd((unsigned long long*)&P.dbg[w * 4 + k], (unsigned long long)dbg_acc[k]);
   }
 }
 

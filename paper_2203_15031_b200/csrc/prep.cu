@@ -7,9 +7,9 @@
 //   s_k <= 1e-13 max_i |x_ik| (reading g15); the smallest offending column wins.
 //   HBM-bound: reads X twice (8np B each, the second from L2) and writes Xb (8np B).
 //
-// gram_kernel — G_b[jl][jm] = x~_{j0+jl}^T x~_{j0+jm} / n for each 32-row block b: the
-//   within-block couplings that let the CD walk of Proposition 2 process 32
-//   rows of a column with a single dot-product GEMM.  p*32*n FMAs, tiny.
+// gram_kernel — the couplings G_jj' = x~_j^T x~_j' / n between each row j of block b and the
+//   rows j' of blocks b-1 and b, which let the CD kernel process Proposition 2's row order
+//    32 rows at a time with a lag-1 pipeline.  2 p 32 n FMAs, tiny.
 #include "spmesl_internal.cuh"
 
 namespace spmesl {
@@ -67,27 +67,35 @@ __global__ void standardize_kernel(const double* __restrict__ X, int64_t n, int6
 
 __global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ Xb, int64_t n,
                                                    int nchunk, double* __restrict__ G) {
-  __shared__ double t[J][KC + 1];
+  // G[blk][jl][0..31]  = x~_{blk,jl}^T x~_{blk-1,jm} / n   (G^x; zero for blk = 0)
+  // G[blk][jl][32..63] = x~_{blk,jl}^T x~_{blk,jm} / n     (G^w)
+  __shared__ double t[2][J][KC + 1];
   const int64_t blk = blockIdx.x;
   const int tid = threadIdx.x;
-  // thread computes entries (r, c0..c0+3): r = tid / 8, c0 = (tid % 8) * 4
-  const int r = tid >> 3, c0 = (tid & 7) * 4;
-  double acc[4] = {0, 0, 0, 0};
+  // thread computes entries (r, c0..c0+7) of the 32 x 64 band: r = tid / 8, c0 = (tid % 8) * 8
+  const int r = tid >> 3, c0 = (tid & 7) * 8;
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int q = 0; q < nchunk; ++q) {
-    const double* src = Xb + ((size_t)blk * nchunk + q) * CHUNK_DOUBLES;
-    for (int e = tid; e < J * KC; e += 256) t[e / KC][e % KC] = src[(e / KC) * XS + xswz(e / KC, e % KC)];
+    const double* cur = Xb + ((size_t)blk * nchunk + q) * CHUNK_DOUBLES;
+    const double* prv = blk ? Xb + ((size_t)(blk - 1) * nchunk + q) * CHUNK_DOUBLES : nullptr;
+    for (int e = tid; e < J * KC; e += 256) {
+      const int jr = e / KC, kl = e % KC;
+      t[1][jr][kl] = cur[jr * XS + xswz(jr, kl)];
+      t[0][jr][kl] = prv ? prv[jr * XS + xswz(jr, kl)] : 0.0;
+    }
     __syncthreads();
+    const int half = c0 >> 5, cc = c0 & 31;
 #pragma unroll 4
     for (int kl = 0; kl < KC; ++kl) {
-      double a = t[r][kl];
+      const double a = t[1][r][kl];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) acc[u] = fma(a, t[c0 + u][kl], acc[u]);
+      for (int u = 0; u < 8; ++u) acc[u] = fma(a, t[half][cc + u][kl], acc[u]);
     }
     __syncthreads();
   }
-  double* g = G + (size_t)blk * J * J;
+  double* g = G + (size_t)blk * J * 2 * J;
 #pragma unroll
-  for (int u = 0; u < 4; ++u) g[r * J + c0 + u] = acc[u] / (double)n;
+  for (int u = 0; u < 8; ++u) g[r * 2 * J + c0 + u] = acc[u] / (double)n;
 }
 
 cudaError_t launch_standardize(const double* X, const Layout& L, int standardize, double* Xb,

@@ -19,10 +19,14 @@ constexpr int KC = 32;                   // samples per staged X chunk
 constexpr int XS = KC;                   // chunk row stride (doubles), swizzled not padded
 constexpr int CHUNK_DOUBLES = J * XS;    // 1024
 constexpr int CHUNK_BYTES = CHUNK_DOUBLES * 8;   // 8192
-constexpr int NCW = 8;                   // consumer warps in the CD kernel
+constexpr int NMW = 8;                   // CD kernel: MMA warps (2 chunk-parity groups x 4)
+constexpr int NEW = 1;                   // CD kernel: epilogue warp (lane = column)
+constexpr int NWORK = NMW + NEW;         // warps that take part in the per-step barrier
+constexpr int WORK_THREADS = NWORK * 32;
+constexpr int PRODUCER_WARP = NWORK;     // the X-tile producer warp
 constexpr int KSPLIT = 2;                // k-split by chunk parity (fixed => deterministic)
 constexpr int RPAD = 8;                  // residual row padding (n_pad + 8 = 8 mod 16)
-constexpr int CD_THREADS = (NCW + 1) * 32;       // + 1 producer warp
+constexpr int CD_THREADS = (NWORK + 1) * 32;     // + 1 producer warp
 constexpr int MAX_T = 32;                // max resident columns (slots) per CTA
 
 struct Layout {
@@ -46,7 +50,8 @@ enum : int { FLAG_CODE = 0, FLAG_OVERFLOW = 1 };
 
 struct CDParams {
   const double* Xb;
-  const double* Gband;     // [nblk][J][J]  x~_j^T x~_j' / n within each row block
+  const double* Gband;     // [nblk][J][2J]: x~_j^T x~_j' / n with j' in the previous block
+                           //   (G^x, columns 0..31) and in the same block (G^w, 32..63)
   int n, n_pad, nchunk;
   int p;
   int nblk;
@@ -57,6 +62,8 @@ struct CDParams {
   int T;                   // resident columns per CTA (8, 16, 32)
   int nst;                 // X chunk pipeline stages
   int nzcap;               // per-column capacity of each coefficient list
+  int debug;               // development timing switches (SPMESL_CD_DEBUG; 0 in production)
+  long long* dbg;          // development phase timers (debug & 4)
   int* queue;              // atomic head (local column index)
   int* flags;              // FLAG_*
   const int* err_in;       // standardization error code (CD exits early when nonzero)
