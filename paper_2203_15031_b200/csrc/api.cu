@@ -76,6 +76,8 @@ struct Workspace {
   Buffer hx, htheta, hsigma, hiters, hsweeps, hconv;
   DevCounters* host_counters = nullptr;   // pinned
   cudaEvent_t ev[6] = {};
+  cudaStream_t side = nullptr;            // Theta zero-fill overlapped with the CD kernel
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool init = false;
 };
 
@@ -99,6 +101,9 @@ int ws_init(Workspace& W, int dev) {
   W.cc_major = prop.major;
   CUDA_TRY(cudaMallocHost((void**)&W.host_counters, sizeof(DevCounters)));
   for (auto& e : W.ev) CUDA_TRY(cudaEventCreate(&e));
+  CUDA_TRY(cudaStreamCreateWithFlags(&W.side, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreateWithFlags(&W.ev_fork, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&W.ev_join, cudaEventDisableTiming));
   W.init = true;
   return SPMESL_OK;
 }
@@ -197,9 +202,9 @@ int run_cd(Workspace& W, const double* dX, int64_t n, int64_t p, int64_t cb, int
   P.nzcap = nzcap;
   { const char* d = getenv("SPMESL_CD_DEBUG"); P.debug = d ? atoi(d) : 0; }
   static long long* dbg_buf = nullptr;
-  if (P.debug & 4) {
-    if (!dbg_buf) cudaMalloc(&dbg_buf, 16 * sizeof(long long));
-    cudaMemsetAsync(dbg_buf, 0, 16 * sizeof(long long), s);
+  if (P.debug & 12) {
+    if (!dbg_buf) cudaMalloc(&dbg_buf, (16 + 4 * 1024) * sizeof(long long));
+    cudaMemsetAsync(dbg_buf, 0, (16 + 4 * 1024) * sizeof(long long), s);
   }
   P.dbg = dbg_buf;
   P.queue = (int*)W.queue.ptr;
@@ -216,6 +221,21 @@ int run_cd(Workspace& W, const double* dX, int64_t n, int64_t p, int64_t cb, int
   const int ctas = (int)std::min<int64_t>(W.sms, (m + T - 1) / T);
   *num_ctas = ctas;
   CUDA_TRY(launch_cd(P, ctas, s));
+  if (P.debug & 8) {
+    std::vector<long long> h(16 + 4 * ctas);
+    cudaMemcpyAsync(h.data(), dbg_buf, h.size() * 8, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    long long t0 = h[16 + 2], t1 = h[16 + 2];
+    for (int c = 0; c < ctas; ++c) { t0 = std::min(t0, h[16 + c * 4 + 2]); t1 = std::max(t1, h[16 + c * 4 + 2]); }
+    FILE* f = fopen("gpurun_out/cta_trace.csv", "w");
+    if (f) {
+      fprintf(f, "cta,tile_sweeps,columns,end_us_after_first,small_sweeps\n");
+      for (int c = 0; c < ctas; ++c)
+        fprintf(f, "%d,%lld,%lld,%.1f,%lld\n", c, h[16 + c * 4], h[16 + c * 4 + 1], (h[16 + c * 4 + 2] - t0) / 1e3, h[16 + c * 4 + 3]);
+      fclose(f);
+    }
+    fprintf(stderr, "[cd trace] CTA end-time spread %.3f ms\n", (t1 - t0) / 1e6);
+  }
   if (P.debug & 4) {
     long long h[16];
     cudaMemcpyAsync(h, dbg_buf, sizeof(h), cudaMemcpyDeviceToHost, s);
@@ -352,8 +372,14 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
   FitOut out{0, p, (double*)W.sigma_std.ptr, dIters, dSweeps, dConv};
   Layout L;
   int nzcap = 0;
+  // zero-fill Theta (8 p^2 bytes, the only dense pass) on a side stream while the CD kernel runs
+  CUDA_TRY(cudaEventRecord(W.ev_fork, s));
+  CUDA_TRY(cudaStreamWaitEvent(W.side, W.ev_fork, 0));
+  CUDA_TRY(cudaMemsetAsync(dTheta, 0, sizeof(double) * (size_t)p * (size_t)p, W.side));
+  CUDA_TRY(cudaEventRecord(W.ev_join, W.side));
   rc = fit_columns_core(W, dX, n, p, 0, p, lambda0, tol, max_iter, o, out, s, st, L, &nzcap);
-  if (rc) return rc;
+  if (rc) { cudaStreamWaitEvent(s, W.ev_join, 0); return rc; }
+  CUDA_TRY(cudaStreamWaitEvent(s, W.ev_join, 0));
   const size_t cap = (size_t)p * (size_t)nzcap;
   if ((rc = ensure(W.csc_rows, cap * 4))) return rc;
   if ((rc = ensure(W.csc_vals, cap * 8))) return rc;
@@ -366,7 +392,7 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
   CUDA_TRY(launch_assemble(p, 0, p, (const int64_t*)W.col_ptr.ptr, (const int32_t*)W.csc_rows.ptr,
                            (const double*)W.csc_vals.ptr, (const double*)W.sigma_std.ptr,
                            o.standardize ? (const double*)W.scale.ptr : nullptr, o.symmetrize,
-                           dTheta, dSigma, s));
+                           dTheta, dSigma, s, /*zero_fill=*/false));
   CUDA_TRY(cudaEventRecord(W.ev[4], s));
   if ((rc = read_counters(W, s))) return rc;
   int any_unconv = 0;
@@ -377,7 +403,7 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
     st->ms_cd = ev_ms(W.ev[1], W.ev[2]);
     st->ms_assemble = ev_ms(W.ev[3], W.ev[4]);
     st->ms_total = ev_ms(W.ev[0], W.ev[4]);
-    st->kernel_launches = 7;   // standardize, gram, cd, csc_scan, csc_copy, assemble x2
+    st->kernel_launches = 7;   // standardize, gram, cd, csc_scan, csc_copy, assemble x2 (+ memsets)
     st->bad_column = -1;
   }
   return any_unconv ? SPMESL_WARN_NOT_CONVERGED : SPMESL_OK;
@@ -423,6 +449,10 @@ int spmesl_release_workspace(void) {
     for (Buffer* b : bufs) { if (b->ptr) cudaFree(b->ptr); b->ptr = nullptr; b->bytes = 0; }
     if (w->host_counters) cudaFreeHost(w->host_counters);
     for (auto& e : w->ev) if (e) cudaEventDestroy(e);
+    if (w->side) cudaStreamDestroy(w->side);
+    if (w->ev_fork) cudaEventDestroy(w->ev_fork);
+    if (w->ev_join) cudaEventDestroy(w->ev_join);
+    w->side = nullptr; w->ev_fork = w->ev_join = nullptr;
     w->init = false;
   }
   if (prev >= 0) cudaSetDevice(prev);

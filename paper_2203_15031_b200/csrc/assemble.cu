@@ -167,10 +167,12 @@ cudaError_t launch_csc_counts(const int* nz_count, int ncols, int32_t* out, cuda
 cudaError_t launch_assemble(int64_t p, int64_t col_begin, int64_t col_end, const int64_t* col_ptr,
                             const int32_t* rows, const double* vals, const double* sigma_std,
                             const double* scale, int symmetrize, double* Theta, double* sigma_out,
-                            cudaStream_t s) {
+                            cudaStream_t s, bool zero_fill) {
   const int64_t m = col_end - col_begin;
-  cudaError_t e = cudaMemsetAsync(Theta, 0, sizeof(double) * (size_t)p * (size_t)m, s);
-  if (e != cudaSuccess) return e;
+  if (zero_fill) {
+    cudaError_t e = cudaMemsetAsync(Theta, 0, sizeof(double) * (size_t)p * (size_t)m, s);
+    if (e != cudaSuccess) return e;
+  }
   const int rescale = scale != nullptr;
   assemble_entries_kernel<<<148 * 4, 256, 0, s>>>(p, col_begin, col_end, col_ptr, rows, vals,
                                                   sigma_std, scale, symmetrize, rescale, Theta);

@@ -285,6 +285,7 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
   const int nzcap = P.nzcap;
   const double inv_n = 1.0 / (double)n;
   long long dbg_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long dbg_sweeps = 0, dbg_cols = 0, dbg_sweeps_small = 0;
 
   if (tid == 0) {
     // one ring per parity group: every phase of a stage is consumed by the same 4 warps, so a
@@ -481,6 +482,7 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
       }
     }
     const int A = S.A;
+    if (tid == 0 && A > 0) { dbg_sweeps++; dbg_cols += S.nloads; dbg_sweeps_small += (A <= 8); }
     __threadfence_block();
     work_sync();
     named_bar_arrive(BAR_PROD, CD_THREADS);   // release the producer for this sweep (or exit)
@@ -617,6 +619,14 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
       S.cnt_new[lane] = cnt_new;
     }
     work_sync();
+  }
+  if ((P.debug & 8) && tid == 0) {   // per-CTA trace: tile-sweeps, columns, end time
+    unsigned long long tnow;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+    P.dbg[16 + blockIdx.x * 4 + 0] = dbg_sweeps;
+    P.dbg[16 + blockIdx.x * 4 + 1] = dbg_cols;
+    P.dbg[16 + blockIdx.x * 4 + 2] = (long long)tnow;
+    P.dbg[16 + blockIdx.x * 4 + 3] = dbg_sweeps_small;
   }
   if ((P.debug & 4) && lane == 0 && (warp == 0 || warp == 4 || warp == NMW)) {
     const int w = warp == 0 ? 0 : (warp == 4 ? 1 : 2);

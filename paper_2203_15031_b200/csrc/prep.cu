@@ -65,37 +65,57 @@ __global__ void standardize_kernel(const double* __restrict__ X, int64_t n, int6
   }
 }
 
+// D(8x8) += A(8x4) B(4x8) in fp64 on the tensor cores (fragment layout: see cd_sweep.cu)
+__device__ __forceinline__ void dmma_g(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// G[blk][jl][0..31]  = x~_{blk,jl}^T x~_{blk-1,jm} / n   (G^x; zero for blk = 0)
+// G[blk][jl][32..63] = x~_{blk,jl}^T x~_{blk,jm} / n     (G^w)
+// One CTA per row block, 8 warps; warp w owns the m-tile (w & 3) and the 4 n-tiles of half
+// (w >> 2) of the 32 x 64 band.  The two tiles of each chunk pair are staged in shared memory
+// verbatim (so the swizzled layout and the paired-k fragment loads of the CD kernel apply).
 __global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ Xb, int64_t n,
                                                    int nchunk, double* __restrict__ G) {
-  // G[blk][jl][0..31]  = x~_{blk,jl}^T x~_{blk-1,jm} / n   (G^x; zero for blk = 0)
-  // G[blk][jl][32..63] = x~_{blk,jl}^T x~_{blk,jm} / n     (G^w)
-  __shared__ double t[2][J][KC + 1];
+  __shared__ __align__(128) double t[2][J * XS];     // [0]: block b-1, [1]: block b
   const int64_t blk = blockIdx.x;
-  const int tid = threadIdx.x;
-  // thread computes entries (r, c0..c0+7) of the 32 x 64 band: r = tid / 8, c0 = (tid % 8) * 8
-  const int r = tid >> 3, c0 = (tid & 7) * 8;
-  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t4 = lane & 3, sw = g & 1;
+  const int mt = warp & 3, half = warp >> 2;         // half 0: G^x (block b-1), 1: G^w (block b)
+  double acc[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
   for (int q = 0; q < nchunk; ++q) {
-    const double* cur = Xb + ((size_t)blk * nchunk + q) * CHUNK_DOUBLES;
-    const double* prv = blk ? Xb + ((size_t)(blk - 1) * nchunk + q) * CHUNK_DOUBLES : nullptr;
-    for (int e = tid; e < J * KC; e += 256) {
-      const int jr = e / KC, kl = e % KC;
-      t[1][jr][kl] = cur[jr * XS + xswz(jr, kl)];
-      t[0][jr][kl] = prv ? prv[jr * XS + xswz(jr, kl)] : 0.0;
+    const double2* cur = (const double2*)(Xb + ((size_t)blk * nchunk + q) * CHUNK_DOUBLES);
+    const double2* prv = blk ? (const double2*)(Xb + ((size_t)(blk - 1) * nchunk + q) * CHUNK_DOUBLES)
+                             : nullptr;
+    for (int e = tid; e < CHUNK_DOUBLES / 2; e += 256) {
+      ((double2*)t[1])[e] = cur[e];
+      ((double2*)t[0])[e] = prv ? prv[e] : make_double2(0.0, 0.0);
     }
     __syncthreads();
-    const int half = c0 >> 5, cc = c0 & 31;
-#pragma unroll 4
-    for (int kl = 0; kl < KC; ++kl) {
-      const double a = t[1][r][kl];
+    const double* xa = t[1] + (mt * 8 + g) * XS + 2 * t4;          // A = rows of block b
+    const double* xb = t[half] + g * XS + 2 * t4;                  // B = rows of block b-1 / b
 #pragma unroll
-      for (int u = 0; u < 8; ++u) acc[u] = fma(a, t[half][cc + u][kl], acc[u]);
+    for (int kp = 0; kp < KC / 8; ++kp) {
+      const double2 a = *(const double2*)(xa + (kp ^ sw) * 8);
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const double2 b = *(const double2*)(xb + nt * 8 * XS + (kp ^ sw) * 8);
+        dmma_g(acc[nt][0], acc[nt][1], a.x, b.x);
+        dmma_g(acc[nt][0], acc[nt][1], a.y, b.y);
+      }
     }
     __syncthreads();
   }
-  double* g = G + (size_t)blk * J * 2 * J;
+  double* gb = G + (size_t)blk * J * 2 * J;
+  const double inv_n = 1.0 / (double)n;
 #pragma unroll
-  for (int u = 0; u < 8; ++u) g[r * 2 * J + c0 + u] = acc[u] / (double)n;
+  for (int nt = 0; nt < 4; ++nt) {
+    const int row = mt * 8 + g, col = half * J + nt * 8 + 2 * t4;
+    gb[row * 2 * J + col] = acc[nt][0] * inv_n;
+    gb[row * 2 * J + col + 1] = acc[nt][1] * inv_n;
+  }
 }
 
 cudaError_t launch_standardize(const double* X, const Layout& L, int standardize, double* Xb,

@@ -93,6 +93,6 @@ cudaError_t launch_csc_counts(const int* nz_count, int ncols, int32_t* out, cuda
 cudaError_t launch_assemble(int64_t p, int64_t col_begin, int64_t col_end, const int64_t* col_ptr,
                             const int32_t* rows, const double* vals, const double* sigma_std,
                             const double* scale, int symmetrize, double* Theta, double* sigma_out,
-                            cudaStream_t s);
+                            cudaStream_t s, bool zero_fill = true);
 
 }  // namespace spmesl
