@@ -211,11 +211,19 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # SPMESL_BENCH_SHARE_GPU=1: all ranks on cuda:0 over gloo (functional test of the multi-rank
+    # path on a one-GPU box; not a performance configuration)
+    share = os.environ.get("SPMESL_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2203_15031_b200 as S
     from paper_2203_15031_b200 import distributed as D
     S.load()
@@ -271,11 +279,12 @@ def run_ours(args):
           file=sys.stderr, flush=True)
     tot_ms = sum(step_ms)
     cd_tot = sum(cd_ms)
+    cdev = torch.device("cpu") if share else dev
     if dist:
-        t = torch.tensor([tot_ms, cd_tot], dtype=torch.float64, device=dev)
+        t = torch.tensor([tot_ms, cd_tot], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms, cd_tot = float(t[0]), float(t[1])
-        u = torch.tensor([updates], dtype=torch.int64, device=dev)
+        u = torch.tensor([updates], dtype=torch.int64, device=cdev)
         dist.all_reduce(u)
         updates = int(u[0])
     value = updates / (tot_ms / 1000.0)
@@ -339,7 +348,7 @@ def run_ours(args):
             barrier()
         e_tot = float(np.mean(e_ms))
         if dist:
-            t = torch.tensor([e_tot], dtype=torch.float64, device=dev)
+            t = torch.tensor([e_tot], dtype=torch.float64, device=cdev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_tot = float(t[0])
         e2e = {"value": upd_per_step / (e_tot / 1000.0), "unit": UNIT,

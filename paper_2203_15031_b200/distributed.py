@@ -24,14 +24,22 @@ def column_range(p: int, rank: int, world: int):
     return c0, c0 + base + (1 if rank < rem else 0)
 
 
+def _comm_device(t: torch.Tensor, group=None) -> torch.device:
+    """gloo moves CPU tensors only: stage CUDA tensors through the host for it."""
+    if t.is_cuda and dist.get_backend(group) == "gloo":
+        return torch.device("cpu")
+    return t.device
+
+
 def _all_gather_padded(t: torch.Tensor, length: int, group=None):
     """All-gather a 1-D tensor whose length differs per rank (padded to `length`)."""
     world = dist.get_world_size(group)
-    buf = torch.zeros(length, dtype=t.dtype, device=t.device)
-    buf[: t.numel()] = t
-    out = torch.empty(world * length, dtype=t.dtype, device=t.device)
+    cdev = _comm_device(t, group)
+    buf = torch.zeros(length, dtype=t.dtype, device=cdev)
+    buf[: t.numel()] = t.to(cdev)
+    out = torch.empty(world * length, dtype=t.dtype, device=cdev)
     dist.all_gather_into_tensor(out, buf, group=group)
-    return out.view(world, length)
+    return out.to(t.device).view(world, length)
 
 
 def gather_csc(p: int, counts: torch.Tensor, rows: torch.Tensor, vals: torch.Tensor,
@@ -43,8 +51,9 @@ def gather_csc(p: int, counts: torch.Tensor, rows: torch.Tensor, vals: torch.Ten
     world = dist.get_world_size(group)
     dev = counts.device
     m_max = -(-p // world)
-    meta = torch.tensor([counts.numel(), rows.numel()], dtype=torch.int64, device=dev)
-    metas = torch.empty(world * 2, dtype=torch.int64, device=dev)
+    cdev = _comm_device(counts, group)
+    meta = torch.tensor([counts.numel(), rows.numel()], dtype=torch.int64, device=cdev)
+    metas = torch.empty(world * 2, dtype=torch.int64, device=cdev)
     dist.all_gather_into_tensor(metas, meta, group=group)
     metas = metas.view(world, 2).cpu()
     nnz_max = max(int(metas[:, 1].max()), 1)
@@ -81,6 +90,8 @@ def fit_distributed(X: torch.Tensor, lambda0: float, tol: float = 1e-4, max_iter
                                               part["sigma_std"], group)
     theta, sigma = assemble_device(p, c0, c1, col_ptr, rows, vals, sig_all, part["scale"],
                                    stream=stream, **options)
+    stats = dict(part["stats"])
+    stats["kernel_launches"] = stats.get("kernel_launches", 0) + 2   # assemble entries + diag
     return dict(theta=theta, sigma=sigma, iters=part["iters"], sweeps=part["sweeps"],
-                converged=part["converged"], col_range=(c0, c1), stats=part["stats"],
+                converged=part["converged"], col_range=(c0, c1), stats=stats,
                 code=part["code"])

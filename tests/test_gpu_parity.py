@@ -181,3 +181,45 @@ def test_full_size_config5_sampled_columns(S, oracle):
         want = want / (s * s[k])
         got = r.Theta[:, k]
         assert np.all(np.abs(got - want) <= 1e-8 * np.abs(want) + 1e-12 * abs(want[k])), k
+
+
+def _rank_worker(rank, world, port, X, lam, q):
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_2203_15031_b200.distributed import fit_distributed
+        Xd = torch.from_numpy(np.ascontiguousarray(X)).cuda()
+        r = fit_distributed(Xd, lam)
+        q.put((rank, r["col_range"], r["theta"].cpu().numpy(), r["sigma"].cpu().numpy(),
+               r["iters"].cpu().numpy(), r["sweeps"].cpu().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_ranks_sharing_one_gpu_match_single_fit(S, oracle):
+    """fit_distributed (column blocks + CSC all-gather + per-rank assembly) on 2 ranks that
+    share cuda:0 over gloo must reproduce the single-GPU fit bit for bit."""
+    import socket
+    import torch.multiprocessing as mp
+    X, _, _ = G.make_config(4, p=1200, family="hub")
+    lam = oracle.lambda_ub(*X.shape)
+    full = S.fit(X, lam)
+    sk = socket.socket(); sk.bind(("127.0.0.1", 0)); port = sk.getsockname()[1]; sk.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_rank_worker, args=(r, 2, port, X, lam, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=300) for _ in range(2)]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    for rank, (c0, c1), th, sg, it, sw in res:
+        assert np.array_equal(th, full.Theta[:, c0:c1])
+        assert np.array_equal(sg, full.sigma[c0:c1])
+        assert np.array_equal(it, full.iters[c0:c1]) and np.array_equal(sw, full.sweeps[c0:c1])
