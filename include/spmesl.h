@@ -63,7 +63,10 @@ typedef struct {
   int32_t mode;           /* 0: per-column stop (Alg. 1/2 semantics) — the only mode so far */
   int32_t tile_cols;      /* 0: auto; 8, 16 or 32 resident columns per SM (tests) */
   int32_t device;         /* host entry points: CUDA device ordinal (-1: current device) */
-  int32_t reserved[9];
+  int32_t tail_after;     /* columns still running after this many sweeps finish in the
+                             covariance-update tail solver (default 1; 0: never).  Same
+                             iterates up to rounding. */
+  int32_t reserved[8];
 } spmesl_options;
 
 typedef struct {
@@ -81,6 +84,9 @@ typedef struct {
   double  ms_cd;          /* device time of the persistent CD kernel */
   double  ms_assemble;    /* device time of assembly + symmetrization (incl. CSC build) */
   double  ms_total;       /* device time of the whole call on the stream */
+  double  ms_tail;        /* device time of the tail solver (0 if it did not run) */
+  int64_t tail_columns;   /* columns finished by the tail solver */
+  int64_t tail_gram_ondemand; /* Gram columns the tail solver computed on first use */
 } spmesl_stats;
 
 /* Fill *opt with the defaults listed above. */

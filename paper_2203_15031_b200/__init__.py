@@ -46,10 +46,11 @@ def _vp(a) -> ctypes.c_void_p:
 
 
 def _opts(max_inner=10000, standardize=True, symmetrize=True, sigma_floor=1e-8, tile_cols=0,
-          device=-1) -> _lib.Options:
+          device=-1, tail_after=1) -> _lib.Options:
     return default_options(max_inner=int(max_inner), standardize=int(bool(standardize)),
                            symmetrize=int(bool(symmetrize)), sigma_floor=float(sigma_floor),
-                           tile_cols=int(tile_cols), device=int(device))
+                           tile_cols=int(tile_cols), device=int(device),
+                           tail_after=int(tail_after))
 
 
 def fit(X, lambda0: float, tol: float = 1e-4, max_iter: int = 100, *, out_theta=None,

@@ -31,7 +31,8 @@ class Options(ctypes.Structure):
         ("mode", ctypes.c_int32),
         ("tile_cols", ctypes.c_int32),
         ("device", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 9),
+        ("tail_after", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 8),
     ]
 
 
@@ -51,6 +52,9 @@ class Stats(ctypes.Structure):
         ("ms_cd", ctypes.c_double),
         ("ms_assemble", ctypes.c_double),
         ("ms_total", ctypes.c_double),
+        ("ms_tail", ctypes.c_double),
+        ("tail_columns", ctypes.c_int64),
+        ("tail_gram_ondemand", ctypes.c_int64),
     ]
 
     def asdict(self):

@@ -39,7 +39,10 @@ int fail(int code, const std::string& msg) {
 struct DevCounters {
   int err;                      // standardization error seen
   int overflow;                 // a coefficient list exceeded nzcap
-  int pad[2];
+  int tail_count;               // columns handed to the tail solver
+  int tail_next;                // tail solver work counter
+  int gram_ondemand;            // Gram columns computed on first use by the tail solver
+  int pad2;
   unsigned long long bad_key;   // 2*col + (0 nonfinite | 1 constant)
   int64_t csc_total;
 };
@@ -72,10 +75,11 @@ struct Workspace {
   int cc_major = 0;
   Buffer xb, gband, mean, scale, counters, queue, sigma_std, iters, sweeps, conv, nz_count, nz_cur,
       nz_rows, nz_vals, col_ptr, csc_rows, csc_vals;
+  Buffer tail, umark, umap, uvars, tailV, zall, ondemand;   // tail solver
   // host-API staging
   Buffer hx, htheta, hsigma, hiters, hsweeps, hconv;
   DevCounters* host_counters = nullptr;   // pinned
-  cudaEvent_t ev[6] = {};
+  cudaEvent_t ev[8] = {};
   cudaStream_t side = nullptr;            // Theta zero-fill overlapped with the CD kernel
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool init = false;
@@ -163,6 +167,77 @@ struct FitOut {
   uint8_t* conv;
 };
 
+bool tail_enabled(const Workspace& W, const spmesl_options& o, const Layout& L, int nzcap) {
+  // (the fit-wide Gram table is p x p doubles: keep it under 16 GB)
+  return o.tail_after > 0 && tail_smem_bytes((int)L.p, L.n_pad, nzcap) <= (size_t)W.smem_optin &&
+         (double)L.p * (double)L.p * 8.0 <= 16e9;
+}
+
+// Tail solver for the columns the CD kernel handed over: fresh residuals, one
+// batched DMMA pass for z = X~^T r / n and the Gram columns of every active variable, then the
+// covariance-update sweeps.  Host work: the union of active variables (a p-flag readback).
+int run_tail(Workspace& W, const Layout& L, int64_t cb, double lambda0, double tol,
+             int32_t max_iter, const spmesl_options& o, int nzcap, const FitOut& out, int M,
+             cudaStream_t s, spmesl_stats* st) {
+  const int p = (int)L.p;
+  int rc;
+  // active variables of the handed-over columns (device marks, one readback)
+  if ((rc = ensure(W.umark, (size_t)p * 4))) return rc;
+  CUDA_TRY(cudaMemsetAsync(W.umark.ptr, 0, (size_t)p * 4, s));
+  CUDA_TRY(launch_tail_mark((const TailState*)W.tail.ptr, M, (const int*)W.nz_rows.ptr, nzcap,
+                            (int*)W.umark.ptr, s));
+  std::vector<int> mark(p);
+  CUDA_TRY(cudaMemcpyAsync(mark.data(), W.umark.ptr, (size_t)p * 4, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  // Gram columns to precompute: the active variables, or all p when the tail is large (the
+  // others are computed on first use by the tail kernel, once per fit)
+  std::vector<int> U;
+  const bool all = (int64_t)M * 16 > p;
+  for (int j = 0; j < p; ++j)
+    if (all || mark[j]) U.push_back(j);
+  const int nU = (int)U.size();
+  if ((rc = ensure(W.uvars, (size_t)std::max(nU, 1) * 4))) return rc;
+  if ((rc = ensure(W.umap, (size_t)p * 4))) return rc;             // gstate
+  if ((rc = ensure(W.tailV, (size_t)M * L.n_pad * 8))) return rc;
+  if ((rc = ensure(W.zall, (size_t)M * p * 8))) return rc;
+  if ((rc = ensure(W.ondemand, (size_t)p * p * 8))) return rc;     // Gtab
+  int grid = std::min(M, W.sms);
+  std::vector<int> gstate(p, 0);
+  for (int j : U) gstate[j] = 2;
+  CUDA_TRY(cudaMemcpyAsync(W.umap.ptr, gstate.data(), (size_t)p * 4, cudaMemcpyHostToDevice, s));
+  if (nU) CUDA_TRY(cudaMemcpyAsync(W.uvars.ptr, U.data(), (size_t)nU * 4, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaEventRecord(W.ev[5], s));
+  CUDA_TRY(launch_tail_residuals((const double*)W.xb.ptr, (const TailState*)W.tail.ptr, M,
+                                 (const int*)W.nz_rows.ptr, (const double*)W.nz_vals.ptr, nzcap, cb,
+                                 (int)L.n, L.n_pad, L.nchunk, (double*)W.tailV.ptr, s));
+  CUDA_TRY(launch_gram_pass((const double*)W.xb.ptr, (int)L.nblk, L.nchunk, (int)L.n, p,
+                            (const double*)W.tailV.ptr, M, (const int*)W.uvars.ptr, nU,
+                            (double*)W.zall.ptr, (double*)W.ondemand.ptr, s));
+  DevCounters* dc = (DevCounters*)W.counters.ptr;
+  TailParams T{};
+  T.Xb = (const double*)W.xb.ptr;
+  T.n = (int)L.n; T.n_pad = L.n_pad; T.nchunk = L.nchunk; T.p = p; T.nblk = (int)L.nblk;
+  T.col_begin = cb;
+  T.lambda0 = lambda0; T.tol = tol; T.sigma_floor = o.sigma_floor; T.sqrt_n = std::sqrt((double)L.n);
+  T.max_outer = max_iter; T.max_inner = o.max_inner;
+  T.nzcap = nzcap;
+  T.M = M;
+  T.tail = (const TailState*)W.tail.ptr;
+  T.Zz = (const double*)W.zall.ptr;
+  T.Gtab = (double*)W.ondemand.ptr;
+  T.gstate = (int*)W.umap.ptr;
+  T.next = &dc->tail_next;
+  T.ondemand_count = &dc->gram_ondemand;
+  T.flags = &dc->err;
+  T.nz_rows = (int*)W.nz_rows.ptr; T.nz_vals = (double*)W.nz_vals.ptr;
+  T.nz_count = (int*)W.nz_count.ptr; T.nz_cur = (int*)W.nz_cur.ptr;
+  T.sigma_std = out.sigma_std; T.iters = out.iters; T.sweeps = out.sweeps; T.converged = out.conv;
+  CUDA_TRY(launch_tail_sweeps(T, grid, s));
+  CUDA_TRY(cudaEventRecord(W.ev[6], s));   // end of the tail solver
+  if (st) { st->tail_columns = M; st->kernel_launches += 4; }
+  return SPMESL_OK;
+}
+
 // Core: standardize + gram + CD for columns [cb, ce) on stream s.  Leaves the coefficient
 // lists in the workspace (nz_*), per-column results in `out`.  Returns after enqueueing.
 int run_cd(Workspace& W, const double* dX, int64_t n, int64_t p, int64_t cb, int64_t ce,
@@ -200,6 +275,9 @@ int run_cd(Workspace& W, const double* dX, int64_t n, int64_t p, int64_t cb, int
   P.T = T;
   P.nst = cd_stages(T, L.n_pad, W.smem_optin);
   P.nzcap = nzcap;
+  P.evict_after = tail_enabled(W, o, L, nzcap) ? o.tail_after : 0;
+  P.tail_count = &dc->tail_count;
+  P.tail = (TailState*)W.tail.ptr;
   { const char* d = getenv("SPMESL_CD_DEBUG"); P.debug = d ? atoi(d) : 0; }
   static long long* dbg_buf = nullptr;
   if (P.debug & 12) {
@@ -263,6 +341,7 @@ int alloc_core(Workspace& W, const Layout& L, int64_t m, int nzcap) {
   if ((rc = ensure(W.nz_rows, (size_t)m * 2 * nzcap * 4))) return rc;
   if ((rc = ensure(W.nz_vals, (size_t)m * 2 * nzcap * 8))) return rc;
   if ((rc = ensure(W.col_ptr, (size_t)(m + 1) * 8))) return rc;
+  if ((rc = ensure(W.tail, (size_t)m * sizeof(TailState)))) return rc;
   return SPMESL_OK;
 }
 
@@ -354,6 +433,16 @@ int fit_columns_core(Workspace& W, const double* dX, int64_t n, int64_t p, int64
     if ((rc = read_counters(W, s))) return rc;
     if (W.host_counters->err) return std_error(W, st);
     if (st) { st->tile_cols = T; st->num_ctas = ctas; }
+    if (!W.host_counters->overflow && W.host_counters->tail_count > 0) {
+      if ((rc = run_tail(W, L, cb, lambda0, tol, max_iter, o, nzcap, out,
+                         W.host_counters->tail_count, s, st)))
+        return rc;
+      if ((rc = read_counters(W, s))) return rc;
+      if (st) {
+        st->ms_tail = ev_ms(W.ev[5], W.ev[6]);
+        st->tail_gram_ondemand = W.host_counters->gram_ondemand;
+      }
+    }
     if (!W.host_counters->overflow) { *nzcap_used = nzcap; return SPMESL_OK; }
     if (nzcap >= p) break;
     nzcap = (int)std::min<int64_t>(p, (int64_t)nzcap * 4);
@@ -428,6 +517,7 @@ void spmesl_default_options(spmesl_options* opt) {
   opt->mode = 0;
   opt->tile_cols = 0;
   opt->device = -1;
+  opt->tail_after = 1;
 }
 
 const char* spmesl_last_error(void) { return g_last_error.c_str(); }
@@ -442,7 +532,8 @@ int spmesl_release_workspace(void) {
     if (!w) continue;
     std::lock_guard<std::mutex> lw(w->mu);
     if (w->init) cudaSetDevice(w->device);
-    Buffer* bufs[] = {&w->xb, &w->gband, &w->mean, &w->scale, &w->counters, &w->queue,
+    Buffer* bufs[] = {&w->tail, &w->umark, &w->umap, &w->uvars, &w->tailV, &w->zall, &w->ondemand,
+                      &w->xb, &w->gband, &w->mean, &w->scale, &w->counters, &w->queue,
                       &w->sigma_std, &w->iters, &w->sweeps, &w->conv, &w->nz_count, &w->nz_cur,
                       &w->nz_rows, &w->nz_vals, &w->col_ptr, &w->csc_rows, &w->csc_vals,
                       &w->hx, &w->htheta, &w->hsigma, &w->hiters, &w->hsweeps, &w->hconv};

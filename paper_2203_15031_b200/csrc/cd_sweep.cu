@@ -401,8 +401,16 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
           S.sigma[c] = sigma;
           S.lam[c] = sigma * P.lambda0;
           S.maxd[c] = 0.0;
-          S.retire[c] = retire;
-          if (retire) {
+          if (!retire && P.evict_after > 0 && S.sweeps[c] >= P.evict_after) {
+            // hand the column to the covariance-update tail solver (tail.cu): a decision that
+            // depends only on the column, so results stay independent of scheduling
+            const int k = atomicAdd(P.tail_count, 1);
+            TailState ts;
+            ts.col = col; ts.outer = outer; ts.sweeps = S.sweeps[c]; ts.inner = inner;
+            ts.flags = flags; ts.cur = cur; ts.cnt = cnt; ts.sigma = sigma;
+            P.tail[k] = ts;
+            retire = 1;
+          } else if (retire) {
             P.sigma_std[col] = sigma;
             P.iters[col] = outer;
             P.sweeps[col] = S.sweeps[c];
@@ -410,6 +418,7 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
             P.nz_count[col] = cnt;
             P.nz_cur[col] = cur;
           }
+          S.retire[c] = retire;
         }
       }
       work_sync();

@@ -48,6 +48,19 @@ __host__ __device__ inline size_t xb_index(int64_t i, int64_t j, int nchunk) {
 // Error flags written by kernels (device int32[4]).
 enum : int { FLAG_CODE = 0, FLAG_OVERFLOW = 1 };
 
+// State of a column handed from the CD kernel to the tail solver at a sweep boundary
+// (coefficients stay in the column's list `cur` with `cnt` entries).
+struct TailState {
+  int col;        // local column index
+  int outer;      // outer iterations completed
+  int sweeps;     // sweeps completed
+  int inner;      // sweeps completed in the current outer iteration
+  int flags;      // bit1: an inner loop hit max_inner
+  int cur, cnt;   // current coefficient list
+  int pad;
+  double sigma;   // current sigma (lambda = sigma lambda0)
+};
+
 struct CDParams {
   const double* Xb;
   const double* Gband;     // [nblk][J][2J]: x~_j^T x~_j' / n with j' in the previous block
@@ -62,6 +75,10 @@ struct CDParams {
   int T;                   // resident columns per CTA (8, 16, 32)
   int nst;                 // X chunk pipeline stages
   int nzcap;               // per-column capacity of each coefficient list
+  int evict_after;         // hand columns that continue after this many sweeps to the tail
+                           //   solver (0: never)
+  int* tail_count;         // number of columns handed over
+  TailState* tail;         // [ncols]
   int debug;               // development timing switches (SPMESL_CD_DEBUG; 0 in production)
   long long* dbg;          // development phase timers (debug & 4)
   int* queue;              // atomic head (local column index)
@@ -76,6 +93,42 @@ struct CDParams {
   int* sweeps;             // [ncols]
   uint8_t* converged;      // [ncols]
 };
+
+struct TailParams {
+  const double* Xb;
+  int n, n_pad, nchunk, p, nblk;
+  int64_t col_begin;
+  double lambda0, tol, sigma_floor, sqrt_n;
+  int max_outer, max_inner;
+  int nzcap;
+  int M;                   // tail columns
+  const TailState* tail;   // [M]
+  const double* Zz;        // [M][p]: z_k = X~^T r_k / n for tail column k
+  double* Gtab;            // [p][p]: Gram column G[:, j] = X~^T x~_j / n of variable j
+  int* gstate;             // [p]: 0 absent, 1 being computed, 2 ready
+  int* next;               // atomic work counter
+  int* ondemand_count;     // Gram columns computed on first use
+  int* flags;
+  int* nz_rows;            // column coefficient lists (as in CDParams)
+  double* nz_vals;
+  int* nz_count;
+  int* nz_cur;
+  double* sigma_std;
+  int* iters;
+  int* sweeps;
+  uint8_t* converged;
+};
+constexpr int TAIL_THREADS = 256;
+constexpr int TAIL_ODC = 8;          // on-demand Gram column cache entries per CTA
+size_t tail_smem_bytes(int p, int n_pad, int nzcap);
+cudaError_t launch_tail_residuals(const double* Xb, const TailState* tail, int M, const int* nz_rows,
+                                  const double* nz_vals, int nzcap, int64_t col_begin, int n,
+                                  int n_pad, int nchunk, double* V, cudaStream_t s);
+cudaError_t launch_gram_pass(const double* Xb, int nblk, int nchunk, int n, int p, const double* V,
+                             int M, const int* U, int nU, double* Zz, double* Gtab, cudaStream_t s);
+cudaError_t launch_tail_mark(const TailState* tail, int M, const int* nz_rows, int nzcap, int* umark,
+                             cudaStream_t s);
+cudaError_t launch_tail_sweeps(const TailParams& P, int grid, cudaStream_t s);
 
 size_t cd_smem_bytes(int T, int n_pad);          // with the minimum 2 stages
 int cd_stages(int T, int n_pad, size_t smem_optin);  // stages that fit (0: does not fit)

@@ -1,0 +1,342 @@
+// Covariance-update tail solver (SURVEY.md §8(f) f2 applied to the columns that need more than
+// one sweep).
+//
+// The CD kernel performs every column's first sweep — the dense screening pass, z = X~^T x~_c / n
+// for all rows, on the tensor cores.  A column that does not retire after it is handed over
+// here.  For such a column Algorithm 1 continues in the SAME cyclic row order, but
+// instead of forming x_j^T e / n by a length-n dot product at every visit, it keeps
+//     z_j = x~_j^T e / n   for all rows j  (shared memory)
+// and, whenever b_j changes by -d (e += x~_j d, Prop. 2), updates z += d G[:, j] with the
+// Gram column G[:, j] = X~^T x~_j / n.  A visit to a row with b_j = 0 and |z_j| <= lambda cannot
+// change anything (Soft returns 0, d = 0), so a sweep only visits the rows with b_j != 0 or
+// |z_j| > lambda, found in row order by a block-wide search: O(p (1 + changes)) work per sweep
+// instead of O(p n).  The iterates are Algorithm 1's up to rounding; every operation is a fixed
+// function of the column (the Gram columns come from one DMMA routine, whether precomputed in
+// the batched pass or computed on demand), so results do not depend on scheduling.
+#include <cstdio>
+#include "spmesl_internal.cuh"
+
+namespace spmesl {
+
+__device__ __forceinline__ void dmma_t(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ double soft_t(double a, double lam) {
+  double m = fabs(a) - lam;
+  return m > 0.0 ? copysign(m, a) : 0.0;
+}
+
+// ------------------------------------------------------------------ fresh residuals
+// V[k] = x~_c - sum_{b_j != 0, ascending} x~_j b_j for tail column k (one warp per column;
+// the same per-element order as the CD kernel's refresh).
+__global__ void tail_residuals_kernel(const double* __restrict__ Xb, const TailState* __restrict__ tail,
+                                      int M, const int* __restrict__ nz_rows,
+                                      const double* __restrict__ nz_vals, int nzcap,
+                                      int64_t col_begin, int n_pad, int nchunk, double* __restrict__ V) {
+  const int lane = threadIdx.x & 31;
+  const int k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (k >= M) return;
+  const TailState ts = tail[k];
+  const int64_t gc = col_begin + ts.col;
+  const size_t lo = (size_t)ts.col * 2 * nzcap + (size_t)ts.cur * nzcap;
+  double* r = V + (size_t)k * n_pad;
+  for (int i = lane; i < n_pad; i += 32) r[i] = Xb[xb_index(i, gc, nchunk)];
+  const int m_end = min(ts.cnt, nzcap);
+  for (int m = 0; m < m_end; ++m) {
+    const int j = nz_rows[lo + m];
+    const double bj = nz_vals[lo + m];
+    for (int i = lane; i < n_pad; i += 32) r[i] = fma(-Xb[xb_index(i, j, nchunk)], bj, r[i]);
+  }
+}
+
+// ------------------------------------------------------------------ Gram / z columns (DMMA)
+// Loads chunk q of vector `vid` (row `vr` of a 32 x 32 smem tile, stored swizzled like Xb).
+// vid < M: residual V[vid]; vid - M < nU: variable U[vid - M] (a row of Xb); else zero.
+__device__ __forceinline__ void load_vec_chunk(double* tile, int vr, int vid, int q, int lane,
+                                               const double* Xb, int nchunk, const double* V,
+                                               int M, const int* U, int nU, int n_pad) {
+  double v = 0.0;
+  if (vid < M) {
+    v = V[(size_t)vid * n_pad + q * KC + lane];
+  } else if (vid - M < nU) {
+    v = Xb[xb_index((int64_t)q * KC + lane, U[vid - M], nchunk)];
+  }
+  tile[vr * XS + xswz(vr, lane)] = v;
+}
+
+// One 32-row block x one 32-vector tile of Z = X~_b^T W / n on 8 warps (warp w: m-tile w & 3,
+// n-tiles 2 (w >> 2), +1).  Per output the chain is: chunks q ascending, k-pairs 0..3, even
+// then odd sample — identical for every caller.
+__device__ __forceinline__ void gram_tile(const double* Xb, int b, int nchunk, int n, int p,
+                                          const double* V, int M, const int* U, int nU, int n_pad,
+                                          int vt, int nvec_valid, double* tx, double* tv,
+                                          double* Zz, double* Gtab) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t4 = lane & 3, sw = g & 1;
+  const int mt = warp & 3, nt0 = (warp >> 2) * 2;
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  for (int q = 0; q < nchunk; ++q) {
+    const double2* src = (const double2*)(Xb + ((size_t)b * nchunk + q) * CHUNK_DOUBLES);
+    for (int e = tid; e < CHUNK_DOUBLES / 2; e += blockDim.x) ((double2*)tx)[e] = src[e];
+    for (int vr = warp; vr < 32; vr += blockDim.x >> 5)
+      load_vec_chunk(tv, vr, vt * 32 + vr, q, lane, Xb, nchunk, V, M, U, nU, n_pad);
+    __syncthreads();
+    const double* xa = tx + (mt * 8 + g) * XS + 2 * t4;
+#pragma unroll
+    for (int kp = 0; kp < KC / 8; ++kp) {
+      const double2 a = *(const double2*)(xa + (kp ^ sw) * 8);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const double2 bb = *(const double2*)(tv + ((nt0 + u) * 8 + g) * XS + 2 * t4 + (kp ^ sw) * 8);
+        dmma_t(acc[u][0], acc[u][1], a.x, bb.x);
+        dmma_t(acc[u][0], acc[u][1], a.y, bb.y);
+      }
+    }
+    __syncthreads();
+  }
+  const double inv_n = 1.0 / (double)n;
+  const int row = b * J + mt * 8 + g;
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int v = (nt0 + u) * 8 + 2 * t4 + e;
+      if (row < p && v < nvec_valid) {
+        const int vid = vt * 32 + v;
+        double* col = vid < M ? Zz + (size_t)vid * p : Gtab + (size_t)U[vid - M] * p;
+        col[row] = acc[u][e] * inv_n;
+      }
+    }
+}
+
+__global__ void __launch_bounds__(256) gram_pass_kernel(const double* __restrict__ Xb, int nchunk,
+                                                        int n, int p, const double* __restrict__ V,
+                                                        int M, const int* __restrict__ U, int nU,
+                                                        int n_pad, double* __restrict__ Zz,
+                                                        double* __restrict__ Gtab) {
+  __shared__ __align__(128) double tx[J * XS];
+  __shared__ __align__(128) double tv[J * XS];
+  const int b = blockIdx.x, vt = blockIdx.y;
+  const int total = M + nU;
+  gram_tile(Xb, b, nchunk, n, p, V, M, U, nU, n_pad, vt, total - vt * 32, tx, tv, Zz, Gtab);
+}
+
+// mark the active variables of the handed-over columns (umark[j] = 1)
+__global__ void tail_mark_kernel(const TailState* __restrict__ tail, int M, const int* __restrict__ nz_rows,
+                                 int nzcap, int* __restrict__ umark) {
+  const int lane = threadIdx.x & 31;
+  const int k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (k >= M) return;
+  const TailState ts = tail[k];
+  const size_t lo = (size_t)ts.col * 2 * nzcap + (size_t)ts.cur * nzcap;
+  for (int m = lane; m < min(ts.cnt, nzcap); m += 32) umark[nz_rows[lo + m]] = 1;
+}
+
+// ------------------------------------------------------------------ per-column sweeps
+struct TailShared {
+  double red[TAIL_THREADS / 32];
+  int wmin[TAIL_THREADS / 32];
+  int oc_var[TAIL_ODC];
+  int oc_next;
+  int k;
+  int k2;
+};
+
+// doubles: tiles [2][J*XS], z [p], r [n_pad], old/new list values [2][nzcap];
+// ints: old/new list rows [2][nzcap]; then TailShared (8-aligned)
+size_t tail_smem_bytes(int p, int n_pad, int nzcap) {
+  size_t b = ((size_t)2 * J * XS + p + n_pad + 2 * (size_t)nzcap) * 8;
+  b += (size_t)2 * nzcap * 4;
+  b = (b + 15) & ~(size_t)15;
+  b += sizeof(TailShared);
+  return (b + 127) & ~(size_t)127;
+}
+
+__global__ void __launch_bounds__(TAIL_THREADS, 1) tail_sweep_kernel(const TailParams P) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  const int p = P.p, n = P.n, n_pad = P.n_pad, nchunk = P.nchunk, nzcap = P.nzcap;
+  double* tx = (double*)sm;                                  // [J*XS]
+  double* tvv = tx + J * XS;                                 // [J*XS]
+  double* z = tvv + J * XS;                                  // [p]
+  double* r = z + p;                                         // [n_pad]
+  double* ov = r + n_pad;                                    // [nzcap] old list values
+  double* nv = ov + nzcap;                                   // [nzcap] new list values
+  int* orow = (int*)(nv + nzcap);                            // [nzcap]
+  int* nrow = orow + nzcap;                                  // [nzcap]
+  size_t ts_off = ((size_t)2 * J * XS + p + n_pad + 2 * (size_t)nzcap) * 8 + (size_t)2 * nzcap * 4;
+  ts_off = (ts_off + 15) & ~(size_t)15;
+  TailShared& TS = *(TailShared*)(sm + ts_off);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const size_t list_stride = (size_t)2 * nzcap;
+  if (tid < TAIL_ODC) TS.oc_var[tid] = -1;
+  if (tid == 0) TS.oc_next = 0;
+
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) TS.k = atomicAdd(P.next, 1);
+    __syncthreads();
+    const int k = TS.k;
+    if (k >= P.M) break;
+    const TailState ts = P.tail[k];
+    const int col = ts.col;
+    const int gc = (int)(P.col_begin + col);
+    double sigma = ts.sigma;
+    int outer = ts.outer, sweeps = ts.sweeps, inner = ts.inner, flags = ts.flags;
+    int cur = ts.cur;
+    int ocnt = min(ts.cnt, nzcap);
+    bool overflow = ts.cnt > nzcap;
+    for (int j = tid; j < p; j += TAIL_THREADS) z[j] = P.Zz[(size_t)k * p + j];
+    {
+      const size_t lo = (size_t)col * list_stride + (size_t)cur * nzcap;
+      for (int m = tid; m < ocnt; m += TAIL_THREADS) { orow[m] = P.nz_rows[lo + m]; ov[m] = P.nz_vals[lo + m]; }
+    }
+    __syncthreads();
+    bool retire = false;
+    while (!retire) {
+      // ------------------------------------------------ one sweep, rows in cyclic order
+      const double lam = sigma * P.lambda0;
+      double maxd = 0.0;
+      int pos = 0, cursor = 0, ncnt = 0;
+      for (;;) {
+        const int na = cursor < ocnt ? orow[cursor] : p;     // next row with b_j != 0
+        // first row in [pos, na) with |z_j| > lambda (j != this column)
+        int j = na;
+        for (int base = pos; base < na; base += TAIL_THREADS) {
+          const int jj = base + tid;
+          const bool hit = jj < na && jj != gc && fabs(z[jj]) > lam;
+          const unsigned m = __ballot_sync(0xffffffffu, hit);
+          if (lane == 0) TS.wmin[warp] = m ? base + warp * 32 + __ffs(m) - 1 : 0x7fffffff;
+          __syncthreads();
+          int best = 0x7fffffff;
+#pragma unroll
+          for (int w = 0; w < TAIL_THREADS / 32; ++w) best = min(best, TS.wmin[w]);
+          __syncthreads();
+          if (best != 0x7fffffff) { j = best; break; }
+        }
+        if (j >= p) break;
+        double bo = 0.0;
+        if (j == na) { bo = ov[cursor]; ++cursor; }
+        const double a = z[j] + bo;
+        const double bn = soft_t(a, lam);
+        const double d = bo - bn;                             // e += x_j d
+        if (bn != 0.0) {
+          if (ncnt < nzcap) { if (tid == 0) { nrow[ncnt] = j; nv[ncnt] = bn; } }
+          else overflow = true;
+          ++ncnt;
+        }
+        if (d != 0.0) {
+          maxd = fmax(maxd, fabs(d));
+          // Gram column G[:, j]: precomputed, cached, or computed now (same DMMA routine)
+          // Gram column G[:, j] from the fit-wide table: precomputed, or computed here once
+          // (claim 0 -> 1, write, publish 2); every CTA is resident, so waiting is safe
+          const double* gcol = P.Gtab + (size_t)j * p;
+          if (*(volatile int*)&P.gstate[j] != 2) {
+            if (tid == 0) { TS.oc_var[0] = j; TS.k2 = atomicCAS(&P.gstate[j], 0, 1); }
+            __syncthreads();
+            if (TS.k2 == 0) {
+              for (int b = 0; b < P.nblk; ++b)     // vector j alone in a tile: same DMMA chain
+                gram_tile(P.Xb, b, nchunk, n, p, nullptr, 0, &TS.oc_var[0], 1, n_pad, 0, 1,
+                          tx, tvv, nullptr, P.Gtab);
+              __threadfence();
+              __syncthreads();
+              if (tid == 0) { atomicExch(&P.gstate[j], 2); atomicAdd(P.ondemand_count, 1); }
+            } else if (tid == 0) {
+              while (*(volatile int*)&P.gstate[j] != 2) __nanosleep(200);
+            }
+            __threadfence();
+            __syncthreads();
+          }
+          for (int t = tid; t < p; t += TAIL_THREADS) z[t] = fma(d, __ldcg(gcol + t), z[t]);
+        }
+        __syncthreads();
+        pos = j + 1;
+      }
+      ++sweeps;
+      ++inner;
+      // the new list becomes the current one
+      for (int m = tid; m < min(ncnt, nzcap); m += TAIL_THREADS) { orow[m] = nrow[m]; ov[m] = nv[m]; }
+      ocnt = min(ncnt, nzcap);
+      __syncthreads();
+      if (maxd < P.tol || inner >= P.max_inner) {
+        if (!(maxd < P.tol)) flags |= 2;
+        // fresh residual and sigma (reading g4), warp 0 in the CD kernel's order
+        if (warp == 0) {
+          for (int i = lane; i < n_pad; i += 32) r[i] = P.Xb[xb_index(i, gc, nchunk)];
+          for (int m = 0; m < ocnt; ++m) {
+            const int jj = orow[m];
+            const double bj = ov[m];
+            for (int i = lane; i < n_pad; i += 32) r[i] = fma(-P.Xb[xb_index(i, jj, nchunk)], bj, r[i]);
+          }
+          double ss = 0.0;
+          for (int i = lane; i < n; i += 32) ss = fma(r[i], r[i], ss);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+          if (lane == 0) TS.red[0] = ss;
+        }
+        __syncthreads();
+        double sn = sqrt(TS.red[0]) / P.sqrt_n;
+        if (sn < P.sigma_floor) sn = P.sigma_floor;
+        ++outer;
+        if (fabs(sn - sigma) < P.tol) { flags |= 1; retire = true; }
+        else if (outer >= P.max_outer) retire = true;
+        sigma = sn;
+        inner = 0;
+        __syncthreads();
+      }
+    }
+    // outputs: coefficients into the column's other list, per-column results
+    const int dst = cur ^ 1;
+    const size_t lo = (size_t)col * list_stride + (size_t)dst * nzcap;
+    for (int m = tid; m < ocnt; m += TAIL_THREADS) { P.nz_rows[lo + m] = orow[m]; P.nz_vals[lo + m] = ov[m]; }
+    if (tid == 0) {
+      P.nz_count[col] = ocnt;
+      P.nz_cur[col] = dst;
+      P.sigma_std[col] = sigma;
+      P.iters[col] = outer;
+      P.sweeps[col] = sweeps;
+      P.converged[col] = (uint8_t)((flags & 1) && !(flags & 2));
+      if (overflow) atomicExch(&P.flags[FLAG_OVERFLOW], 1);
+    }
+  }
+}
+
+cudaError_t launch_tail_residuals(const double* Xb, const TailState* tail, int M, const int* nz_rows,
+                                  const double* nz_vals, int nzcap, int64_t col_begin, int n,
+                                  int n_pad, int nchunk, double* V, cudaStream_t s) {
+  (void)n;
+  const int wpb = 8;
+  tail_residuals_kernel<<<(M + wpb - 1) / wpb, wpb * 32, 0, s>>>(Xb, tail, M, nz_rows, nz_vals, nzcap,
+                                                                col_begin, n_pad, nchunk, V);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gram_pass(const double* Xb, int nblk, int nchunk, int n, int p, const double* V,
+                             int M, const int* U, int nU, double* Zz, double* Gtab, cudaStream_t s) {
+  const int ntile = (M + nU + 31) / 32;
+  if (ntile == 0) return cudaSuccess;
+  dim3 grid((unsigned)nblk, (unsigned)ntile);
+  // n_pad is implied by nchunk
+  gram_pass_kernel<<<grid, 256, 0, s>>>(Xb, nchunk, n, p, V, M, U, nU, nchunk * KC, Zz, Gtab);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tail_mark(const TailState* tail, int M, const int* nz_rows, int nzcap, int* umark,
+                             cudaStream_t s) {
+  const int wpb = 8;
+  tail_mark_kernel<<<(M + wpb - 1) / wpb, wpb * 32, 0, s>>>(tail, M, nz_rows, nzcap, umark);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tail_sweeps(const TailParams& P, int grid, cudaStream_t s) {
+  const size_t smem = tail_smem_bytes(P.p, P.n_pad, P.nzcap);
+  cudaError_t e = cudaFuncSetAttribute(tail_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  tail_sweep_kernel<<<grid, TAIL_THREADS, smem, s>>>(P);
+  return cudaGetLastError();
+}
+
+}  // namespace spmesl

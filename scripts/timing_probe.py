@@ -18,4 +18,4 @@ for it in range(5):
     r = S.fit_device(Xd, lam)
     e1.record(); torch.cuda.synchronize(); t1 = time.perf_counter()
     st = r.stats
-    print(f"it{it} host {1e3*(t1-t0):.2f} ms  dev {e0.elapsed_time(e1):.2f} ms  std {st['ms_standardize']:.2f} cd {st['ms_cd']:.2f} asm {st['ms_assemble']:.2f} total {st['ms_total']:.2f} sweeps {st['total_sweeps']} max {st['max_sweeps']} nnz {st['nnz']} T {st['tile_cols']}", flush=True)
+    print(f"it{it} host {1e3*(t1-t0):.2f} ms  dev {e0.elapsed_time(e1):.2f} ms  std {st['ms_standardize']:.2f} cd {st['ms_cd']:.2f} asm {st['ms_assemble']:.2f} total {st['ms_total']:.2f} sweeps {st["total_sweeps"]} max {st["max_sweeps"]} nnz {st["nnz"]} T {st["tile_cols"]} tail {st["tail_columns"]} cols {st["ms_tail"]:.2f} ms", flush=True)

@@ -223,3 +223,44 @@ def test_two_ranks_sharing_one_gpu_match_single_fit(S, oracle):
         assert np.array_equal(th, full.Theta[:, c0:c1])
         assert np.array_equal(sg, full.sigma[c0:c1])
         assert np.array_equal(it, full.iters[c0:c1]) and np.array_equal(sw, full.sweeps[c0:c1])
+
+
+@pytest.mark.parametrize("tail_after", [0, 1, 3])
+def test_tail_solver_handoff_points(S, oracle, tail_after):
+    """Columns needing several sweeps are finished by the covariance-update tail solver after
+    `tail_after` sweeps (0: never); every hand-off point must reproduce the oracle."""
+    X, _, _ = G.make_config(4, p=700, n=300, family="hub")
+    lam = oracle.lambda_ub(*X.shape)
+    ora = oracle.spmesl_fit(X, lam)
+    r = S.fit(X, lam, tail_after=tail_after)
+    assert_parity(compare(r.Theta, r.sigma, r.iters, r.sweeps, ora))
+    if tail_after == 0:
+        assert r.stats["tail_columns"] == 0
+    else:
+        assert r.stats["tail_columns"] > 0
+
+
+def test_tail_solver_on_demand_gram_columns(S, oracle):
+    """Few handed-over columns -> only their active variables get precomputed Gram columns;
+    a variable entering later is computed on first use (same DMMA routine).  Config 5 family at
+    p = 8000: the columns that needed more than one sweep (the tail) are checked one by one
+    against the oracle."""
+    X, _, _ = G.make_config(5, p=8000)
+    n, p = X.shape
+    lam = oracle.lambda_ub(n, p)
+    r = S.fit(X, lam, symmetrize=False)
+    assert r.stats["tail_columns"] > 0 and r.stats["tail_gram_ondemand"] > 0
+    cols = np.nonzero(r.sweeps > 1)[0]
+    assert len(cols) == r.stats["tail_columns"]
+    Xs, mu, s = oracle.standardize(X)
+    oc = oracle.spmesl_columns(Xs, cols, lam, want_margin=False)
+    assert np.array_equal(r.iters[cols], oc.outer) and np.array_equal(r.sweeps[cols], oc.sweeps)
+    np.testing.assert_allclose(r.sigma[cols], oc.sigma * s[cols], rtol=1e-10)
+    for c, k in enumerate(cols):
+        w = 1.0 / (oc.sigma[c] * oc.sigma[c])
+        want = -oc.B[:, c] * w
+        want[k] = w
+        want = want / (s * s[k])
+        got = r.Theta[:, k]
+        assert np.array_equal(got != 0, want != 0), k
+        assert np.all(np.abs(got - want) <= 1e-8 * np.abs(want) + 1e-12 * abs(want[k])), k
