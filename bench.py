@@ -319,7 +319,9 @@ def run_ours(args):
                                      ctypes.c_void_p(sh.data_ptr()),
                                      ctypes.c_void_p(ih.data_ptr()), None, None, None)
                 assert rc >= 0, L.spmesl_last_error()
-            h2d, d2h = 8 * n * p, 8 * p * p + 8 * p + 4 * p
+            # bytes that cross PCIe per step: X in; Theta's nonzeros (COO: 4+4+8 B each) +
+            # diagonal + sigma + iters out (the dense zero-fill of Theta runs on host threads)
+            h2d, d2h = 8 * n * p, None
         else:
             m = c1 - c0
             Th = torch.empty((m, p), dtype=torch.float64).pin_memory()
@@ -351,6 +353,9 @@ def run_ours(args):
             t = torch.tensor([e_tot], dtype=torch.float64, device=cdev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_tot = float(t[0])
+        if d2h is None:
+            nnz_sym = int(np.count_nonzero(Th.numpy())) - p      # off-diagonal nonzeros of Theta
+            d2h = 16 * nnz_sym + 8 * p + 8 * p + 4 * p
         e2e = {"value": upd_per_step / (e_tot / 1000.0), "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e_tot,
                "api": "spmesl_fit_ex (host pointers)" if world == 1 else

@@ -27,7 +27,7 @@
  *     allocates its device scratch per device and reuses it across calls
  *     (spmesl_release_workspace frees it).  Calls on one device are serialised.
  *   - Return codes below.  On a negative code the contents of output buffers are
- *     unspecified (the host entry points leave host outputs untouched); the message is
+ *     unspecified (the host entry points may have zero-filled Theta); the message is
  *     available from spmesl_last_error() (thread-local).
  *   - Paper-silent points follow the readings listed in DESIGN.md §3 (tolerances are
  *     absolute; the residual is recomputed at each outer boundary; sigma floor; the
@@ -95,8 +95,9 @@ void spmesl_default_options(spmesl_options* opt);
 /*
  * Host-memory entry point (BASELINE.json: spmesl_fit(X, n, p, lambda0, tol, max_iter ->
  * Theta, sigma, iters)).  X: host n x p; Theta: host p x p; sigma: host [p]; iters: host [p].
- * Copies X to the current device, runs the whole path there and copies the results back.
- * Host buffers may be pageable or pinned (pinned is faster).  Blocking.
+ * Copies X to the current device and runs the whole path there.  Theta is zero-filled by host
+ * threads while the device computes; only its nonzero entries (and the diagonal) are copied
+ * back and scattered.  Host buffers may be pageable or pinned.  Blocking.
  */
 int spmesl_fit(const double* X, int64_t n, int64_t p, double lambda0, double tol,
                int32_t max_iter, double* Theta, double* sigma, int32_t* iters);

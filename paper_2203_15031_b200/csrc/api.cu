@@ -9,8 +9,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "spmesl.h"
@@ -42,7 +44,7 @@ struct DevCounters {
   int tail_count;               // columns handed to the tail solver
   int tail_next;                // tail solver work counter
   int gram_ondemand;            // Gram columns computed on first use by the tail solver
-  int pad2;
+  int coo_count;                // host API: nonzero entries of Theta emitted as COO
   unsigned long long bad_key;   // 2*col + (0 nonfinite | 1 constant)
   int64_t csc_total;
 };
@@ -77,7 +79,7 @@ struct Workspace {
       nz_rows, nz_vals, col_ptr, csc_rows, csc_vals;
   Buffer tail, umark, umap, uvars, tailV, zall, ondemand;   // tail solver
   // host-API staging
-  Buffer hx, htheta, hsigma, hiters, hsweeps, hconv;
+  Buffer hx, htheta, hsigma, hiters, hsweeps, hconv, coo_r, coo_c, coo_v, hdiag, zeros;
   DevCounters* host_counters = nullptr;   // pinned
   cudaEvent_t ev[8] = {};
   cudaStream_t side = nullptr;            // Theta zero-fill overlapped with the CD kernel
@@ -492,7 +494,7 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
     st->ms_cd = ev_ms(W.ev[1], W.ev[2]);
     st->ms_assemble = ev_ms(W.ev[3], W.ev[4]);
     st->ms_total = ev_ms(W.ev[0], W.ev[4]);
-    st->kernel_launches = 7;   // standardize, gram, cd, csc_scan, csc_copy, assemble x2 (+ memsets)
+    st->kernel_launches += 7;  // standardize, gram, cd, csc_scan, csc_copy, assemble x2 (+ memsets)
     st->bad_column = -1;
   }
   return any_unconv ? SPMESL_WARN_NOT_CONVERGED : SPMESL_OK;
@@ -536,7 +538,8 @@ int spmesl_release_workspace(void) {
                       &w->xb, &w->gband, &w->mean, &w->scale, &w->counters, &w->queue,
                       &w->sigma_std, &w->iters, &w->sweeps, &w->conv, &w->nz_count, &w->nz_cur,
                       &w->nz_rows, &w->nz_vals, &w->col_ptr, &w->csc_rows, &w->csc_vals,
-                      &w->hx, &w->htheta, &w->hsigma, &w->hiters, &w->hsweeps, &w->hconv};
+                      &w->hx, &w->htheta, &w->hsigma, &w->hiters, &w->hsweeps, &w->hconv,
+                      &w->coo_r, &w->coo_c, &w->coo_v, &w->hdiag, &w->zeros};
     for (Buffer* b : bufs) { if (b->ptr) cudaFree(b->ptr); b->ptr = nullptr; b->bytes = 0; }
     if (w->host_counters) cudaFreeHost(w->host_counters);
     for (auto& e : w->ev) if (e) cudaEventDestroy(e);
@@ -584,25 +587,131 @@ int spmesl_fit_ex(const double* X, int64_t n, int64_t p, double lambda0, double 
   if ((rc = ws_init(*W, dev))) return rc;
   if (W->cc_major < 10) return fail(SPMESL_ERR_UNSUPPORTED, "needs an sm_100 device");
   const size_t np = (size_t)n * p, pp = (size_t)p * p;
-  if ((rc = ensure(W->hx, np * 8))) return rc;
-  if ((rc = ensure(W->htheta, pp * 8))) return rc;
-  if ((rc = ensure(W->hsigma, (size_t)p * 8))) return rc;
-  if ((rc = ensure(W->hiters, (size_t)p * 4))) return rc;
-  if ((rc = ensure(W->hsweeps, (size_t)p * 4))) return rc;
-  if ((rc = ensure(W->hconv, (size_t)p))) return rc;
+  // Theta is dense on the host but sparse in content: it is zero-filled while the device
+  // computes — by the copy engine (D2H of a device zero buffer, when Theta is pinned) and by host
+  // threads, in parallel; only the nonzero entries (COO) and the diagonal cross PCIe afterwards.
+  size_t dma_elems = 0;
+  {
+    cudaPointerAttributes pa;
+    const bool pinned = cudaPointerGetAttributes(&pa, Theta) == cudaSuccess &&
+                        pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    const size_t zbytes = (size_t)64 << 20;
+    if (pinned && pp * 8 >= ((size_t)256 << 20) && ensure(W->zeros, zbytes) == SPMESL_OK) {
+      if (cudaMemsetAsync(W->zeros.ptr, 0, zbytes, W->side) == cudaSuccess) {
+        dma_elems = (size_t)(0.3 * (double)pp);
+        for (size_t off = 0; off < dma_elems; off += zbytes / 8) {
+          const size_t cnt = std::min(zbytes / 8, dma_elems - off);
+          if (cudaMemcpyAsync(Theta + off, W->zeros.ptr, cnt * 8, cudaMemcpyDeviceToHost, W->side) !=
+              cudaSuccess) {
+            dma_elems = off;
+            break;
+          }
+        }
+      }
+      cudaGetLastError();
+    }
+  }
+  std::vector<std::thread> zero;
+  {
+    const size_t rest = pp - dma_elems;
+    const unsigned hc = std::max(1u, std::thread::hardware_concurrency());
+    const size_t nth = std::min<size_t>(std::min(16u, hc), std::max<size_t>(1, rest >> 20));
+    const size_t per = (rest + nth - 1) / nth;
+    for (size_t t = 0; t < nth; ++t) {
+      const size_t lo = dma_elems + t * per, hi = std::min(pp, lo + per);
+      if (lo < hi) zero.emplace_back([=] { std::memset(Theta + lo, 0, (hi - lo) * sizeof(double)); });
+    }
+  }
+  auto join = [&] {
+    for (auto& th : zero) if (th.joinable()) th.join();
+    if (dma_elems) cudaStreamSynchronize(W->side);
+  };
+  auto bail = [&](int code) { join(); return code; };
+  if ((rc = ensure(W->hx, np * 8))) return bail(rc);
+  if ((rc = ensure(W->sigma_std, (size_t)p * 8))) return bail(rc);
+  if ((rc = ensure(W->hsigma, (size_t)p * 8))) return bail(rc);
+  if ((rc = ensure(W->hiters, (size_t)p * 4))) return bail(rc);
+  if ((rc = ensure(W->hsweeps, (size_t)p * 4))) return bail(rc);
+  if ((rc = ensure(W->hconv, (size_t)p))) return bail(rc);
+  if ((rc = ensure(W->hdiag, (size_t)p * 8))) return bail(rc);
   cudaStream_t s = 0;
-  CUDA_TRY(cudaMemcpyAsync(W->hx.ptr, X, np * 8, cudaMemcpyHostToDevice, s));
-  rc = fit_device_impl((const double*)W->hx.ptr, n, p, lambda0, tol, max_iter, o,
-                       (double*)W->htheta.ptr, (double*)W->hsigma.ptr, (int32_t*)W->hiters.ptr,
-                       (int32_t*)W->hsweeps.ptr, (uint8_t*)W->hconv.ptr, s, st, *W);
-  if (rc < 0) return rc;
-  CUDA_TRY(cudaMemcpyAsync(Theta, W->htheta.ptr, pp * 8, cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaMemcpyAsync(sigma, W->hsigma.ptr, (size_t)p * 8, cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaMemcpyAsync(iters, W->hiters.ptr, (size_t)p * 4, cudaMemcpyDeviceToHost, s));
-  if (sweeps) CUDA_TRY(cudaMemcpyAsync(sweeps, W->hsweeps.ptr, (size_t)p * 4, cudaMemcpyDeviceToHost, s));
-  if (converged) CUDA_TRY(cudaMemcpyAsync(converged, W->hconv.ptr, (size_t)p, cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaStreamSynchronize(s));
-  return rc;
+  {
+    cudaError_t e = cudaMemcpyAsync(W->hx.ptr, X, np * 8, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return bail(fail(SPMESL_ERR_CUDA, cudaGetErrorString(e)));
+  }
+  FitOut out{0, p, (double*)W->sigma_std.ptr, (int32_t*)W->hiters.ptr, (int32_t*)W->hsweeps.ptr,
+             (uint8_t*)W->hconv.ptr};
+  Layout L;
+  int nzcap = 0;
+  rc = fit_columns_core(*W, (const double*)W->hx.ptr, n, p, 0, p, lambda0, tol, max_iter, o, out, s,
+                        st, L, &nzcap);
+  if (rc) return bail(rc);
+  const size_t cap = (size_t)p * (size_t)nzcap;
+  if ((rc = ensure(W->csc_rows, cap * 4))) return bail(rc);
+  if ((rc = ensure(W->csc_vals, cap * 8))) return bail(rc);
+  DevCounters* dc = (DevCounters*)W->counters.ptr;
+  std::vector<int32_t> cr, cc;
+  std::vector<double> cv;
+  int ncoo = 0;
+  {
+    auto step = [&]() -> int {
+      CUDA_TRY(cudaEventRecord(W->ev[3], s));
+      CUDA_TRY(launch_csc_build((const int*)W->nz_count.ptr, (const int*)W->nz_cur.ptr,
+                                (const int*)W->nz_rows.ptr, (const double*)W->nz_vals.ptr, (int)p,
+                                nzcap, (int64_t*)W->col_ptr.ptr, (int32_t*)W->csc_rows.ptr,
+                                (double*)W->csc_vals.ptr, &dc->csc_total, s));
+      if ((rc = read_counters(*W, s))) return rc;
+      const int64_t nnz = W->host_counters->csc_total;
+      if ((rc = ensure(W->coo_r, (size_t)std::max<int64_t>(nnz, 1) * 4))) return rc;
+      if ((rc = ensure(W->coo_c, (size_t)std::max<int64_t>(nnz, 1) * 4))) return rc;
+      if ((rc = ensure(W->coo_v, (size_t)std::max<int64_t>(nnz, 1) * 8))) return rc;
+      CUDA_TRY(launch_assemble_coo(p, (const int64_t*)W->col_ptr.ptr, (const int32_t*)W->csc_rows.ptr,
+                                   (const double*)W->csc_vals.ptr, (const double*)W->sigma_std.ptr,
+                                   o.standardize ? (const double*)W->scale.ptr : nullptr,
+                                   o.symmetrize, (int32_t*)W->coo_r.ptr, (int32_t*)W->coo_c.ptr,
+                                   (double*)W->coo_v.ptr, &dc->coo_count, (double*)W->hdiag.ptr,
+                                   (double*)W->hsigma.ptr, s));
+      CUDA_TRY(cudaEventRecord(W->ev[4], s));
+      if ((rc = read_counters(*W, s))) return rc;
+      ncoo = W->host_counters->coo_count;
+      cr.resize(ncoo); cc.resize(ncoo); cv.resize(ncoo);
+      if (ncoo) {
+        CUDA_TRY(cudaMemcpyAsync(cr.data(), W->coo_r.ptr, (size_t)ncoo * 4, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(cc.data(), W->coo_c.ptr, (size_t)ncoo * 4, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(cv.data(), W->coo_v.ptr, (size_t)ncoo * 8, cudaMemcpyDeviceToHost, s));
+      }
+      CUDA_TRY(cudaMemcpyAsync(sigma, W->hsigma.ptr, (size_t)p * 8, cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaMemcpyAsync(iters, W->hiters.ptr, (size_t)p * 4, cudaMemcpyDeviceToHost, s));
+      if (sweeps) CUDA_TRY(cudaMemcpyAsync(sweeps, W->hsweeps.ptr, (size_t)p * 4, cudaMemcpyDeviceToHost, s));
+      if (converged) CUDA_TRY(cudaMemcpyAsync(converged, W->hconv.ptr, (size_t)p, cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaStreamSynchronize(s));
+      return SPMESL_OK;
+    };
+    if ((rc = step())) return bail(rc);
+  }
+  std::vector<double> diag(p);
+  {
+    cudaError_t e = cudaMemcpy(diag.data(), W->hdiag.ptr, (size_t)p * 8, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return bail(fail(SPMESL_ERR_CUDA, cudaGetErrorString(e)));
+  }
+  int any_unconv = 0;
+  if ((rc = collect_stats((const int32_t*)W->hiters.ptr, (const int32_t*)W->hsweeps.ptr,
+                          (const uint8_t*)W->hconv.ptr, p, p, s, st, &any_unconv)))
+    return bail(rc);
+  join();
+  for (int e = 0; e < ncoo; ++e) Theta[(size_t)cc[e] * p + cr[e]] = cv[e];
+  for (int64_t k = 0; k < p; ++k) Theta[(size_t)k * p + k] = diag[k];
+  if (st) {
+    st->nnz = W->host_counters->csc_total;
+    st->ms_standardize = ev_ms(W->ev[0], W->ev[1]);
+    st->ms_cd = ev_ms(W->ev[1], W->ev[2]);
+    st->ms_assemble = ev_ms(W->ev[3], W->ev[4]);
+    st->ms_total = ev_ms(W->ev[0], W->ev[4]);
+    st->kernel_launches += 7;
+    st->bad_column = -1;
+  }
+  return any_unconv ? SPMESL_WARN_NOT_CONVERGED : SPMESL_OK;
 }
 
 int spmesl_fit(const double* X, int64_t n, int64_t p, double lambda0, double tol,
@@ -666,7 +775,7 @@ int spmesl_fit_columns_device(const double* dX, int64_t n, int64_t p, int64_t co
     st->nnz = total;
     st->ms_standardize = ev_ms(W->ev[0], W->ev[1]);
     st->ms_cd = ev_ms(W->ev[1], W->ev[2]);
-    st->kernel_launches = 6;
+    st->kernel_launches += 6;
   }
   return any_unconv ? SPMESL_WARN_NOT_CONVERGED : SPMESL_OK;
 }

@@ -149,6 +149,59 @@ __global__ void assemble_diag_kernel(int64_t p, int64_t col_begin, int64_t col_e
   if (sigma_out) sigma_out[k - col_begin] = rescale ? scale[k] * sg : sg;
 }
 
+// Host-API variant: the nonzero entries of Theta (symmetrized or Theta1) as COO triplets plus
+// the diagonal and sigma, so that only these cross PCIe (the dense zero-fill happens on the
+// host while the device computes).  Entry order is arbitrary; positions are distinct.
+__global__ void assemble_coo_kernel(int64_t p, const int64_t* __restrict__ col_ptr,
+                                    const int32_t* __restrict__ rows, const double* __restrict__ vals,
+                                    const double* __restrict__ sigma_std,
+                                    const double* __restrict__ scale, int symmetrize, int rescale,
+                                    int32_t* __restrict__ coo_row, int32_t* __restrict__ coo_col,
+                                    double* __restrict__ coo_val, int* __restrict__ coo_count) {
+  const int64_t e1 = col_ptr[p];
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < e1;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = p;
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (col_ptr[mid] <= e) lo = mid;
+      else hi = mid;
+    }
+    const int64_t k = lo;
+    const int32_t j = rows[e];
+    const double sj = scale ? scale[j] : 1.0, sk = scale ? scale[k] : 1.0;
+    const double t_jk = theta1(vals[e], sigma_std[k], sj, sk, rescale != 0);
+    double out = t_jk;
+    if (symmetrize) {
+      const double b_kj = csc_lookup(rows, vals, col_ptr[j], col_ptr[j + 1], (int32_t)k);
+      if (b_kj == 0.0) continue;
+      const double t_kj = theta1(b_kj, sigma_std[j], sk, sj, rescale != 0);
+      const double u = (j < k) ? t_jk : t_kj;
+      const double l = (j < k) ? t_kj : t_jk;
+      out = (fabs(u) > fabs(l)) ? l : u;
+    }
+    const int slot = atomicAdd(coo_count, 1);
+    coo_row[slot] = j;
+    coo_col[slot] = (int32_t)k;
+    coo_val[slot] = out;
+  }
+}
+
+cudaError_t launch_assemble_coo(int64_t p, const int64_t* col_ptr, const int32_t* rows,
+                                const double* vals, const double* sigma_std, const double* scale,
+                                int symmetrize, int32_t* coo_row, int32_t* coo_col, double* coo_val,
+                                int* coo_count, double* diag, double* sigma_out, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(coo_count, 0, sizeof(int), s);
+  if (e != cudaSuccess) return e;
+  const int rescale = scale != nullptr;
+  assemble_coo_kernel<<<148 * 4, 256, 0, s>>>(p, col_ptr, rows, vals, sigma_std, scale, symmetrize,
+                                              rescale, coo_row, coo_col, coo_val, coo_count);
+  // diagonal written as a 1-row "Theta" of stride 0: reuse the diag kernel on a p-vector
+  assemble_diag_kernel<<<(unsigned)((p + 255) / 256), 256, 0, s>>>(0, 0, p, sigma_std, scale,
+                                                                   rescale, diag, sigma_out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_csc_build(const int* nz_count, const int* nz_cur, const int* nz_rows,
                              const double* nz_vals, int ncols, int nzcap, int64_t* col_ptr,
                              int32_t* rows, double* vals, int64_t* total, cudaStream_t s) {

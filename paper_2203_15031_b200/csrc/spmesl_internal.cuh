@@ -142,6 +142,10 @@ cudaError_t launch_cd(const CDParams& P, int num_ctas, cudaStream_t s);
 cudaError_t launch_csc_build(const int* nz_count, const int* nz_cur, const int* nz_rows,
                              const double* nz_vals, int ncols, int nzcap, int64_t* col_ptr,
                              int32_t* rows, double* vals, int64_t* total, cudaStream_t s);
+cudaError_t launch_assemble_coo(int64_t p, const int64_t* col_ptr, const int32_t* rows,
+                                const double* vals, const double* sigma_std, const double* scale,
+                                int symmetrize, int32_t* coo_row, int32_t* coo_col, double* coo_val,
+                                int* coo_count, double* diag, double* sigma_out, cudaStream_t s);
 cudaError_t launch_csc_counts(const int* nz_count, int ncols, int32_t* out, cudaStream_t s);
 cudaError_t launch_assemble(int64_t p, int64_t col_begin, int64_t col_end, const int64_t* col_ptr,
                             const int32_t* rows, const double* vals, const double* sigma_std,
