@@ -87,6 +87,7 @@ typedef struct {
   double  ms_tail;        /* device time of the tail solver (0 if it did not run) */
   int64_t tail_columns;   /* columns finished by the tail solver */
   int64_t tail_gram_ondemand; /* Gram columns the tail solver computed on first use */
+  int64_t tail_sweeps;    /* sweeps performed by the tail solver (the CD kernel did the rest) */
 } spmesl_stats;
 
 /* Fill *opt with the defaults listed above. */

@@ -55,6 +55,7 @@ class Stats(ctypes.Structure):
         ("ms_tail", ctypes.c_double),
         ("tail_columns", ctypes.c_int64),
         ("tail_gram_ondemand", ctypes.c_int64),
+        ("tail_sweeps", ctypes.c_int64),
     ]
 
     def asdict(self):

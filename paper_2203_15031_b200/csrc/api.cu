@@ -45,6 +45,8 @@ struct DevCounters {
   int tail_next;                // tail solver work counter
   int gram_ondemand;            // Gram columns computed on first use by the tail solver
   int coo_count;                // host API: nonzero entries of Theta emitted as COO
+  int tail_sweeps;              // sweeps performed by the tail solver
+  int pad3;
   unsigned long long bad_key;   // 2*col + (0 nonfinite | 1 constant)
   int64_t csc_total;
 };
@@ -230,6 +232,7 @@ int run_tail(Workspace& W, const Layout& L, int64_t cb, double lambda0, double t
   T.gstate = (int*)W.umap.ptr;
   T.next = &dc->tail_next;
   T.ondemand_count = &dc->gram_ondemand;
+  T.sweeps_count = &dc->tail_sweeps;
   T.flags = &dc->err;
   T.nz_rows = (int*)W.nz_rows.ptr; T.nz_vals = (double*)W.nz_vals.ptr;
   T.nz_count = (int*)W.nz_count.ptr; T.nz_cur = (int*)W.nz_cur.ptr;
@@ -443,6 +446,7 @@ int fit_columns_core(Workspace& W, const double* dX, int64_t n, int64_t p, int64
       if (st) {
         st->ms_tail = ev_ms(W.ev[5], W.ev[6]);
         st->tail_gram_ondemand = W.host_counters->gram_ondemand;
+        st->tail_sweeps = W.host_counters->tail_sweeps;
       }
     }
     if (!W.host_counters->overflow) { *nzcap_used = nzcap; return SPMESL_OK; }

@@ -108,6 +108,7 @@ struct TailParams {
   int* gstate;             // [p]: 0 absent, 1 being computed, 2 ready
   int* next;               // atomic work counter
   int* ondemand_count;     // Gram columns computed on first use
+  int* sweeps_count;       // sweeps performed here
   int* flags;
   int* nz_rows;            // column coefficient lists (as in CDParams)
   double* nz_vals;

@@ -299,6 +299,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) tail_sweep_kernel(const TailP
       P.sweeps[col] = sweeps;
       P.converged[col] = (uint8_t)((flags & 1) && !(flags & 2));
       if (overflow) atomicExch(&P.flags[FLAG_OVERFLOW], 1);
+      atomicAdd(P.sweeps_count, sweeps - ts.sweeps);
     }
   }
 }
