@@ -67,6 +67,10 @@ def lib():
                                         ctypes.c_double, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp,
                                         vp]
         L.oracle_num_threads.restype = ctypes.c_int
+        L.oracle_joint_columns.argtypes = [vp, i64, i64, vp, i64, ctypes.c_double, ctypes.c_double,
+                                           i32, i32, ctypes.c_double, vp, vp, vp, vp, vp]
+        L.oracle_spmesl_fit_joint.argtypes = [vp, i64, i64, ctypes.c_double, ctypes.c_double, i32,
+                                              i32, ctypes.c_double, i32, vp, vp, vp, vp, vp, vp, vp]
         del dp
         _lib = L
     return _lib
@@ -237,6 +241,46 @@ def spmesl_fit(X, lambda0, delta=1e-4, max_outer=100, max_inner=10000, sigma_flo
     if rc < 0:
         raise OracleError(rc, int(bad[0]))
     return FitResult(rc, T, sig, outer, sweeps, conv.astype(bool), B, T1, margin)
+
+
+def joint_columns(Xs, cols, lambda0, delta=1e-4, max_outer=100, max_inner=10000,
+                  sigma_floor=1e-8):
+    """Algorithm 3 (joint stop) for a subset of columns of standardized Xs."""
+    Xs = _colmajor(Xs)
+    n, p = Xs.shape
+    cols = np.ascontiguousarray(cols, dtype=np.int64)
+    m = len(cols)
+    B = np.zeros((p, m), order="F")
+    sig = np.zeros(m)
+    outer = np.zeros(m, np.int32)
+    sweeps = np.zeros(m, np.int32)
+    conv = np.zeros(m, np.uint8)
+    rc = lib().oracle_joint_columns(_p(Xs), n, p, _p(cols), m, lambda0, delta, max_outer,
+                                    max_inner, sigma_floor, _p(B), _p(sig), _p(outer),
+                                    _p(sweeps), _p(conv))
+    if rc < 0:
+        raise OracleError(rc)
+    return ColumnsResult(B, sig, outer, sweeps, conv.astype(bool), None)
+
+
+def spmesl_fit_joint(X, lambda0, delta=1e-4, max_outer=100, max_inner=10000, sigma_floor=1e-8,
+                     standardize=True):
+    """Algorithm 3 end to end with Prop. 1 rescaling and Eq. (symm)."""
+    X = _colmajor(X)
+    n, p = X.shape
+    T = np.zeros((p, p), order="F")
+    B = np.zeros((p, p), order="F")
+    sig = np.zeros(p)
+    outer = np.zeros(p, np.int32)
+    sweeps = np.zeros(p, np.int32)
+    conv = np.zeros(p, np.uint8)
+    bad = np.zeros(1, np.int64)
+    rc = lib().oracle_spmesl_fit_joint(_p(X), n, p, lambda0, delta, max_outer, max_inner,
+                                       sigma_floor, 1 if standardize else 0, _p(T), _p(sig),
+                                       _p(outer), _p(sweeps), _p(conv), _p(B), _p(bad))
+    if rc < 0:
+        raise OracleError(rc, int(bad[0]))
+    return FitResult(rc, T, sig, outer, sweeps, conv.astype(bool), B, None, None)
 
 
 def num_threads() -> int:

@@ -340,3 +340,140 @@ int oracle_num_threads(void) {
   return 1;
 #endif
 }
+
+/*
+ * Algorithm 3, the paper-literal joint ("PCD") mode, for the columns cols[0..m-1] of
+ * the standardized Xs (reading g8: the compaction keeps I_l <- I_j; g9: the residual update uses
+ * x_j).  Outer loop r: lambda_c = sigma_c lambda0; E = x_{I} - X B (fresh);
+ * inner repeat: for j = 1..p: for every active column c: a = x_j^T e_c / n + b_jc,
+ * a_cc <- 0, b_jc <- Soft(a), e_c += x_j (b_old - b_new); until
+ * max_{active c, j} |db_jc| < delta (the joint criterion) or max_inner sweeps; then
+ * sigma_c = ||e_c||/sqrt(n) from a fresh residual, F_c = |dsigma_c| >= delta
+ * and the active set keeps the columns with F_c = 1 in order.  Stops when no column
+ * is active or after max_outer outer iterations.  Outputs as oracle_spmesl_columns.
+ */
+int oracle_joint_columns(const double* Xs, int64_t n, int64_t p, const int64_t* cols, int64_t m,
+                         double lambda0, double delta, int32_t max_outer, int32_t max_inner,
+                         double sigma_floor, double* B, double* sigma, int32_t* outer,
+                         int32_t* sweeps, uint8_t* converged) {
+  int rc = check_args(n, p, lambda0, delta, max_outer, max_inner);
+  if (rc) return rc;
+  for (int64_t c = 0; c < m; ++c)
+    if (cols[c] < 0 || cols[c] >= p) return ORACLE_ERR_ARG;
+  double* E = (double*)malloc(sizeof(double) * (size_t)n * (size_t)(m > 0 ? m : 1));
+  double* lam = (double*)malloc(sizeof(double) * (size_t)(m > 0 ? m : 1));
+  int64_t* I = (int64_t*)malloc(sizeof(int64_t) * (size_t)(m > 0 ? m : 1));   /* active set */
+  uint8_t* capped = (uint8_t*)calloc((size_t)(m > 0 ? m : 1), 1);
+  if (!E || !lam || !I || !capped) { free(E); free(lam); free(I); free(capped); return ORACLE_ERR_OOM; }
+  for (int64_t c = 0; c < m; ++c) {                 /* Require line P:941-943 */
+    for (int64_t j = 0; j < p; ++j) B[j + c * p] = 0.0;
+    sigma[c] = 1.0;
+    outer[c] = 0;
+    sweeps[c] = 0;
+    converged[c] = 0;
+    I[c] = c;
+  }
+  int64_t nc = m;
+  for (int32_t r = 0; nc > 0 && r < max_outer; ++r) {
+    for (int64_t a = 0; a < nc; ++a) lam[a] = sigma[I[a]] * lambda0;
+    for (int64_t a = 0; a < nc; ++a) {
+      const int64_t c = I[a], k = cols[c];
+      double* e = E + a * n;
+      for (int64_t i = 0; i < n; ++i) e[i] = Xs[i + k * n];
+      for (int64_t j = 0; j < p; ++j) {
+        const double b = B[j + c * p];
+        if (j == k || b == 0.0) continue;
+        for (int64_t i = 0; i < n; ++i) e[i] = e[i] - Xs[i + j * n] * b;
+      }
+    }
+    int32_t inner = 0;
+    double maxd;
+    do {
+      maxd = 0.0;
+      for (int64_t j = 0; j < p; ++j) {
+        const double* xj = Xs + j * n;
+        for (int64_t a = 0; a < nc; ++a) {
+          const int64_t c = I[a], k = cols[c];
+          if (j == k) continue;                                                   /* a_jj <- 0 */
+          double* e = E + a * n;
+          double dot = 0.0;
+          for (int64_t i = 0; i < n; ++i) dot = dot + xj[i] * e[i];
+          const double av = dot / (double)n + B[j + c * p];
+          const double bn = oracle_soft_threshold(av, lam[a]);
+          const double d = B[j + c * p] - bn;
+          if (d != 0.0)
+            for (int64_t i = 0; i < n; ++i) e[i] = e[i] + xj[i] * d;
+          B[j + c * p] = bn;
+          if (fabs(d) > maxd) maxd = fabs(d);
+        }
+      }
+      for (int64_t a = 0; a < nc; ++a) sweeps[I[a]] += 1;
+      ++inner;
+    } while (!(maxd < delta) && inner < max_inner);
+    if (!(maxd < delta))
+      for (int64_t a = 0; a < nc; ++a) capped[I[a]] = 1;
+    int64_t l = 0;
+    for (int64_t a = 0; a < nc; ++a) {
+      const int64_t c = I[a], k = cols[c];
+      double* e = E + a * n;                         /* fresh residual (reading g4) */
+      for (int64_t i = 0; i < n; ++i) e[i] = Xs[i + k * n];
+      for (int64_t j = 0; j < p; ++j) {
+        const double b = B[j + c * p];
+        if (j == k || b == 0.0) continue;
+        for (int64_t i = 0; i < n; ++i) e[i] = e[i] - Xs[i + j * n] * b;
+      }
+      double ss = 0.0;
+      for (int64_t i = 0; i < n; ++i) ss = ss + e[i] * e[i];
+      double sn = sqrt(ss) / sqrt((double)n);
+      if (sn < sigma_floor) sn = sigma_floor;
+      const int keep = !(fabs(sn - sigma[c]) < delta);                           /* F_c */
+      sigma[c] = sn;
+      outer[c] += 1;
+      if (keep) I[l++] = c;
+      else converged[c] = 1;
+    }
+    nc = l;
+  }
+  for (int64_t c = 0; c < m; ++c)
+    if (capped[c]) converged[c] = 0;
+  free(E); free(lam); free(I); free(capped);
+  return ORACLE_OK;
+}
+
+/* Algorithm 3 end to end (standardize, joint CD, assemble + rescale, symmetrize). */
+int oracle_spmesl_fit_joint(const double* X, int64_t n, int64_t p, double lambda0, double delta,
+                            int32_t max_outer, int32_t max_inner, double sigma_floor,
+                            int32_t standardize, double* Theta, double* sigma_out, int32_t* outer,
+                            int32_t* sweeps, uint8_t* converged, double* B_out, int64_t* bad_col) {
+  int rc = check_args(n, p, lambda0, delta, max_outer, max_inner);
+  if (rc) return rc;
+  if (n < 2 || p < 2) return ORACLE_ERR_ARG;
+  size_t np = (size_t)n * (size_t)p, pp = (size_t)p * (size_t)p;
+  double* Xs = (double*)malloc(sizeof(double) * np);
+  double* mu = (double*)malloc(sizeof(double) * (size_t)p);
+  double* s = (double*)malloc(sizeof(double) * (size_t)p);
+  double* B = B_out ? B_out : (double*)malloc(sizeof(double) * pp);
+  int64_t* cols = (int64_t*)malloc(sizeof(int64_t) * (size_t)p);
+  if (!Xs || !mu || !s || !B || !cols) { rc = ORACLE_ERR_OOM; goto done; }
+  if (standardize) {
+    rc = oracle_standardize(X, n, p, Xs, mu, s, bad_col);
+    if (rc) goto done;
+  } else {
+    for (size_t t = 0; t < np; ++t) Xs[t] = X[t];
+  }
+  for (int64_t k = 0; k < p; ++k) cols[k] = k;
+  rc = oracle_joint_columns(Xs, n, p, cols, p, lambda0, delta, max_outer, max_inner, sigma_floor,
+                            B, sigma_out, outer, sweeps, converged);
+  if (rc) goto done;
+  oracle_assemble(B, sigma_out, standardize ? s : NULL, p, Theta);
+  oracle_symmetrize(Theta, p);
+  if (standardize)
+    for (int64_t k = 0; k < p; ++k) sigma_out[k] = s[k] * sigma_out[k];
+  rc = ORACLE_OK;
+  for (int64_t k = 0; k < p; ++k)
+    if (!converged[k]) rc = ORACLE_WARN_NOT_CONVERGED;
+done:
+  free(Xs); free(mu); free(s); free(cols);
+  if (!B_out) free(B);
+  return rc;
+}
