@@ -60,7 +60,14 @@ typedef struct {
                              sigma on the input scale (Prop. 1); 0: X is used as given */
   int32_t symmetrize;     /* 1 (default): Eq. (symm); 0: return Theta1 */
   double  sigma_floor;    /* sigma_k >= sigma_floor (default 1e-8; reading g5) */
-  int32_t mode;           /* 0: per-column stop (Alg. 1/2 semantics) — the only mode so far */
+  int32_t mode;           /* 0 (default): per-column stop — each column runs Algorithm 1 with
+                             its own inner stop and leaves when its sigma settles.
+                             1: Algorithm 3 — all active columns sweep together
+                             until max over them of ||B_next - B_cur||_inf < tol, then
+                             sigma is refit for all and settled columns leave the
+                             active set.  Mode 1 ignores tail_after and, in
+                             spmesl_fit_columns_device, needs the whole range [0, p)
+                             (else SPMESL_ERR_UNSUPPORTED). */
   int32_t tile_cols;      /* 0: auto; 8, 16 or 32 resident columns per SM (tests) */
   int32_t device;         /* host entry points: CUDA device ordinal (-1: current device) */
   int32_t tail_after;     /* columns still running after this many sweeps finish in the

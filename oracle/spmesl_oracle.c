@@ -363,7 +363,7 @@ int oracle_joint_columns(const double* Xs, int64_t n, int64_t p, const int64_t* 
   double* E = (double*)malloc(sizeof(double) * (size_t)n * (size_t)(m > 0 ? m : 1));
   double* lam = (double*)malloc(sizeof(double) * (size_t)(m > 0 ? m : 1));
   int64_t* I = (int64_t*)malloc(sizeof(int64_t) * (size_t)(m > 0 ? m : 1));   /* active set */
-  uint8_t* capped = (uint8_t*)calloc((size_t)(m > 0 ? m : 1), 1);
+  uint8_t* capped = (uint8_t*)calloc((size_t)(m > 0 ? 2 * m : 1), 1);
   if (!E || !lam || !I || !capped) { free(E); free(lam); free(I); free(capped); return ORACLE_ERR_OOM; }
   for (int64_t c = 0; c < m; ++c) {                 /* Require line P:941-943 */
     for (int64_t j = 0; j < p; ++j) B[j + c * p] = 0.0;
@@ -376,6 +376,7 @@ int oracle_joint_columns(const double* Xs, int64_t n, int64_t p, const int64_t* 
   int64_t nc = m;                                   /* P:944 */
   for (int32_t r = 0; nc > 0 && r < max_outer; ++r) {
     for (int64_t a = 0; a < nc; ++a) lam[a] = sigma[I[a]] * lambda0;             /* P:946 */
+#pragma omp parallel for schedule(dynamic)
     for (int64_t a = 0; a < nc; ++a) {                                           /* P:949 */
       const int64_t c = I[a], k = cols[c];
       double* e = E + a * n;
@@ -392,6 +393,9 @@ int oracle_joint_columns(const double* Xs, int64_t n, int64_t p, const int64_t* 
       maxd = 0.0;
       for (int64_t j = 0; j < p; ++j) {                                           /* P:954 */
         const double* xj = Xs + j * n;
+        /* the active columns are independent: threads split them, each column's arithmetic
+           is unchanged */
+#pragma omp parallel for reduction(max : maxd) schedule(static) if (nc >= 64)
         for (int64_t a = 0; a < nc; ++a) {
           const int64_t c = I[a], k = cols[c];
           if (j == k) continue;                                                   /* a_jj <- 0 */
@@ -412,8 +416,9 @@ int oracle_joint_columns(const double* Xs, int64_t n, int64_t p, const int64_t* 
     } while (!(maxd < delta) && inner < max_inner);                              /* P:964 */
     if (!(maxd < delta))
       for (int64_t a = 0; a < nc; ++a) capped[I[a]] = 1;
-    int64_t l = 0;
-    for (int64_t a = 0; a < nc; ++a) {                                            /* P:968-976 */
+    uint8_t* F = capped + m;  /* scratch F_c flags */
+#pragma omp parallel for schedule(dynamic)
+    for (int64_t a = 0; a < nc; ++a) {                                            /* P:968-969 */
       const int64_t c = I[a], k = cols[c];
       double* e = E + a * n;                         /* fresh residual (reading g4) */
       for (int64_t i = 0; i < n; ++i) e[i] = Xs[i + k * n];
@@ -426,11 +431,14 @@ int oracle_joint_columns(const double* Xs, int64_t n, int64_t p, const int64_t* 
       for (int64_t i = 0; i < n; ++i) ss = ss + e[i] * e[i];
       double sn = sqrt(ss) / sqrt((double)n);
       if (sn < sigma_floor) sn = sigma_floor;
-      const int keep = !(fabs(sn - sigma[c]) < delta);                           /* F_c */
+      F[a] = (uint8_t)!(fabs(sn - sigma[c]) < delta);                            /* F_c */
       sigma[c] = sn;
       outer[c] += 1;
-      if (keep) I[l++] = c;
-      else converged[c] = 1;
+    }
+    int64_t l = 0;
+    for (int64_t a = 0; a < nc; ++a) {
+      if (F[a]) I[l++] = I[a];
+      else converged[I[a]] = 1;
     }
     nc = l;
   }

@@ -46,9 +46,10 @@ struct DevCounters {
   int gram_ondemand;            // Gram columns computed on first use by the tail solver
   int coo_count;                // host API: nonzero entries of Theta emitted as COO
   int tail_sweeps;              // sweeps performed by the tail solver
-  int pad3;
+  int joint_nact;               // mode 1: active columns after the last compaction
   unsigned long long bad_key;   // 2*col + (0 nonfinite | 1 constant)
   int64_t csc_total;
+  unsigned long long joint_maxd;   // mode 1: max |db| of the last sweep (double bits)
 };
 
 struct Buffer {
@@ -80,6 +81,7 @@ struct Workspace {
   Buffer xb, gband, mean, scale, counters, queue, sigma_std, iters, sweeps, conv, nz_count, nz_cur,
       nz_rows, nz_vals, col_ptr, csc_rows, csc_vals;
   Buffer tail, umark, umap, uvars, tailV, zall, ondemand;   // tail solver
+  Buffer ej, act0, act1, keep, jflags;                      // mode 1 (Algorithm 3)
   // host-API staging
   Buffer hx, htheta, hsigma, hiters, hsweeps, hconv, coo_r, coo_c, coo_v, hdiag, zeros;
   DevCounters* host_counters = nullptr;   // pinned
@@ -127,7 +129,7 @@ int validate(const void* X, int64_t n, int64_t p, double lambda0, double tol, in
   if (max_iter < 1) return fail(SPMESL_ERR_ARG, "max_iter must be >= 1");
   if (o.max_inner < 1) return fail(SPMESL_ERR_ARG, "max_inner must be >= 1");
   if (!(o.sigma_floor > 0.0)) return fail(SPMESL_ERR_ARG, "sigma_floor must be > 0");
-  if (o.mode != 0) return fail(SPMESL_ERR_ARG, "only mode 0 (per-column stop) is implemented");
+  if (o.mode != 0 && o.mode != 1) return fail(SPMESL_ERR_ARG, "mode must be 0 (per-column stop) or 1 (Algorithm 3 joint stop)");
   if (o.tile_cols != 0 && o.tile_cols != 8 && o.tile_cols != 16 && o.tile_cols != 32)
     return fail(SPMESL_ERR_ARG, "tile_cols must be 0, 8, 16 or 32");
   const double pp = (double)p * (double)p * 8.0;
@@ -243,12 +245,9 @@ int run_tail(Workspace& W, const Layout& L, int64_t cb, double lambda0, double t
   return SPMESL_OK;
 }
 
-// Core: standardize + gram + CD for columns [cb, ce) on stream s.  Leaves the coefficient
-// lists in the workspace (nz_*), per-column results in `out`.  Returns after enqueueing.
-int run_cd(Workspace& W, const double* dX, int64_t n, int64_t p, int64_t cb, int64_t ce,
-           double lambda0, double tol, int32_t max_iter, const spmesl_options& o, int nzcap,
-           const FitOut& out, cudaStream_t s, int T, Layout& L, int* num_ctas) {
-  const int64_t m = ce - cb;
+// Scratch reset + standardize (a2) + Gram band for columns [cb, cb + m) on stream s.
+int run_prep(Workspace& W, const double* dX, int64_t m, const spmesl_options& o, const Layout& L,
+             cudaStream_t s) {
   CUDA_TRY(cudaMemsetAsync(W.xb.ptr, 0, L.xb_doubles() * 8, s));
   CUDA_TRY(cudaMemsetAsync(W.counters.ptr, 0, sizeof(DevCounters), s));
   CUDA_TRY(cudaMemsetAsync((char*)W.counters.ptr + offsetof(DevCounters, bad_key), 0xff, 8, s));
@@ -261,20 +260,27 @@ int run_cd(Workspace& W, const double* dX, int64_t n, int64_t p, int64_t cb, int
                               (double*)W.scale.ptr, &dc->err, &dc->bad_key, s));
   CUDA_TRY(launch_gram((const double*)W.xb.ptr, L, (double*)W.gband.ptr, s));
   CUDA_TRY(cudaEventRecord(W.ev[1], s));
+  return SPMESL_OK;
+}
+
+CDParams cd_params(Workspace& W, const Layout& L, int64_t cb, int64_t m, double lambda0,
+                   double tol, int32_t max_iter, const spmesl_options& o, int nzcap,
+                   const FitOut& out, int T) {
+  DevCounters* dc = (DevCounters*)W.counters.ptr;
   CDParams P{};
   P.Xb = (const double*)W.xb.ptr;
   P.Gband = (const double*)W.gband.ptr;
-  P.n = (int)n;
+  P.n = (int)L.n;
   P.n_pad = L.n_pad;
   P.nchunk = L.nchunk;
-  P.p = (int)p;
+  P.p = (int)L.p;
   P.nblk = (int)L.nblk;
   P.col_begin = cb;
   P.ncols = (int)m;
   P.lambda0 = lambda0;
   P.tol = tol;
   P.sigma_floor = o.sigma_floor;
-  P.sqrt_n = std::sqrt((double)n);
+  P.sqrt_n = std::sqrt((double)L.n);
   P.max_outer = max_iter;
   P.max_inner = o.max_inner;
   P.T = T;
@@ -283,13 +289,6 @@ int run_cd(Workspace& W, const double* dX, int64_t n, int64_t p, int64_t cb, int
   P.evict_after = tail_enabled(W, o, L, nzcap) ? o.tail_after : 0;
   P.tail_count = &dc->tail_count;
   P.tail = (TailState*)W.tail.ptr;
-  { const char* d = getenv("SPMESL_CD_DEBUG"); P.debug = d ? atoi(d) : 0; }
-  static long long* dbg_buf = nullptr;
-  if (P.debug & 12) {
-    if (!dbg_buf) cudaMalloc(&dbg_buf, (16 + 4 * 1024) * sizeof(long long));
-    cudaMemsetAsync(dbg_buf, 0, (16 + 4 * 1024) * sizeof(long long), s);
-  }
-  P.dbg = dbg_buf;
   P.queue = (int*)W.queue.ptr;
   P.flags = &dc->err;   // FLAG_CODE (unused by CD), FLAG_OVERFLOW at +1
   P.err_in = &dc->err;
@@ -301,6 +300,25 @@ int run_cd(Workspace& W, const double* dX, int64_t n, int64_t p, int64_t cb, int
   P.iters = out.iters;
   P.sweeps = out.sweeps;
   P.converged = out.conv;
+  return P;
+}
+
+// Core: standardize + gram + CD for columns [cb, ce) on stream s.  Leaves the coefficient
+// lists in the workspace (nz_*), per-column results in `out`.  Returns after enqueueing.
+int run_cd(Workspace& W, const double* dX, int64_t n, int64_t p, int64_t cb, int64_t ce,
+           double lambda0, double tol, int32_t max_iter, const spmesl_options& o, int nzcap,
+           const FitOut& out, cudaStream_t s, int T, Layout& L, int* num_ctas) {
+  const int64_t m = ce - cb;
+  int rc;
+  if ((rc = run_prep(W, dX, m, o, L, s))) return rc;
+  CDParams P = cd_params(W, L, cb, m, lambda0, tol, max_iter, o, nzcap, out, T);
+  { const char* d = getenv("SPMESL_CD_DEBUG"); P.debug = d ? atoi(d) : 0; }
+  static long long* dbg_buf = nullptr;
+  if (P.debug & 12) {
+    if (!dbg_buf) cudaMalloc(&dbg_buf, (16 + 4 * 1024) * sizeof(long long));
+    cudaMemsetAsync(dbg_buf, 0, (16 + 4 * 1024) * sizeof(long long), s);
+  }
+  P.dbg = dbg_buf;
   const int ctas = (int)std::min<int64_t>(W.sms, (m + T - 1) / T);
   *num_ctas = ctas;
   CUDA_TRY(launch_cd(P, ctas, s));
@@ -413,17 +431,110 @@ int current_device(int requested, int* dev) {
   return SPMESL_OK;
 }
 
+void set_layout(Layout& L, int64_t n, int64_t p) {
+  L.n = n;
+  L.p = p;
+  L.n_pad = (int)(((n + KC - 1) / KC) * KC);
+  L.nchunk = L.n_pad / KC;
+  L.nblk = (p + J - 1) / J;
+}
+
+// Mode 1: Algorithm 3 for columns [cb, ce).  Host loop: one CD-kernel launch per
+// joint sweep (every active column sweeps once at lambda_c = sigma_c lambda0, residuals carried
+// in Ej), then the joint stop on max |db| (one 8-byte readback); at the outer boundary
+// the sigma kernel (fresh residuals) and the order-preserving compaction of the
+// active set.  Coefficient lists regrow on overflow like mode 0.
+int fit_joint_core(Workspace& W, const double* dX, int64_t n, int64_t p, int64_t cb, int64_t ce,
+                   double lambda0, double tol, int32_t max_iter, const spmesl_options& o,
+                   const FitOut& out, cudaStream_t s, spmesl_stats* st, Layout& L,
+                   int* nzcap_used) {
+  const int64_t m = ce - cb;
+  set_layout(L, n, p);
+  if (!choose_T(W, m, L.n_pad, o.tile_cols))
+    return fail(SPMESL_ERR_UNSUPPORTED, "n = " + std::to_string(n) +
+                                            " does not fit the on-chip residual tile");
+  DevCounters* dc = (DevCounters*)W.counters.ptr;
+  int nzcap = initial_nzcap(n, p);
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    int rc = alloc_core(W, L, m, nzcap);
+    if (rc) return rc;
+    if ((rc = ensure(W.ej, (size_t)m * L.n_pad * 8))) return rc;
+    if ((rc = ensure(W.act0, (size_t)m * 4))) return rc;
+    if ((rc = ensure(W.act1, (size_t)m * 4))) return rc;
+    if ((rc = ensure(W.keep, (size_t)m))) return rc;
+    if ((rc = ensure(W.jflags, (size_t)m))) return rc;
+    dc = (DevCounters*)W.counters.ptr;
+    if ((rc = run_prep(W, dX, m, o, L, s))) return rc;
+    CUDA_TRY(cudaMemsetAsync(out.iters, 0, 4 * (size_t)m, s));
+    CUDA_TRY(cudaMemsetAsync(out.sweeps, 0, 4 * (size_t)m, s));
+    CUDA_TRY(cudaMemsetAsync(out.conv, 0, (size_t)m, s));
+    CUDA_TRY(cudaMemsetAsync(W.jflags.ptr, 0, (size_t)m, s));
+    CUDA_TRY(launch_joint_init((const double*)W.xb.ptr, cb, (int)m, L.n_pad, L.nchunk,
+                               (int*)W.act0.ptr, out.sigma_std, (double*)W.ej.ptr, s));
+    if ((rc = read_counters(W, s))) return rc;
+    if (W.host_counters->err) return std_error(W, st);
+    int* act = (int*)W.act0.ptr;
+    int* act_next = (int*)W.act1.ptr;
+    int nact = (int)m, launches = 3, T0 = 0, ctas0 = 0;
+    bool overflow = false;
+    for (int r = 0; r < max_iter && nact > 0 && !overflow; ++r) {
+      int inner = 0;
+      double jm = 0.0;
+      do {
+        CUDA_TRY(cudaMemsetAsync(&dc->joint_maxd, 0, 8, s));
+        CUDA_TRY(cudaMemsetAsync(W.queue.ptr, 0, 16, s));
+        const int T = choose_T(W, nact, L.n_pad, o.tile_cols);
+        CDParams P = cd_params(W, L, cb, nact, lambda0, tol, max_iter, o, nzcap, out, T);
+        P.evict_after = 0;
+        P.joint = 1;
+        P.act = act;
+        P.Ej = (double*)W.ej.ptr;
+        P.joint_maxd = &dc->joint_maxd;
+        const int ctas = (int)std::min<int64_t>(W.sms, (nact + T - 1) / T);
+        if (!T0) { T0 = T; ctas0 = ctas; }
+        CUDA_TRY(launch_cd(P, ctas, s));
+        ++launches;
+        if ((rc = read_counters(W, s))) return rc;
+        if (W.host_counters->overflow) { overflow = true; break; }
+        std::memcpy(&jm, &W.host_counters->joint_maxd, 8);
+        ++inner;
+      } while (!(jm < tol) && inner < o.max_inner);
+      if (overflow) break;
+      CUDA_TRY(launch_joint_sigma((const double*)W.xb.ptr, cb, act, nact, (const int*)W.nz_rows.ptr,
+                                  (const double*)W.nz_vals.ptr, (const int*)W.nz_count.ptr,
+                                  (const int*)W.nz_cur.ptr, nzcap, (int)n, L.n_pad, L.nchunk,
+                                  std::sqrt((double)n), o.sigma_floor, tol, !(jm < tol),
+                                  out.sigma_std, out.iters, (uint8_t*)W.jflags.ptr, out.conv,
+                                  (double*)W.ej.ptr, (uint8_t*)W.keep.ptr, s));
+      CUDA_TRY(launch_joint_compact(act, (const uint8_t*)W.keep.ptr, nact, act_next,
+                                    &dc->joint_nact, s));
+      launches += 2;
+      if ((rc = read_counters(W, s))) return rc;
+      nact = W.host_counters->joint_nact;
+      std::swap(act, act_next);
+    }
+    if (!overflow) {
+      CUDA_TRY(cudaEventRecord(W.ev[2], s));
+      if (st) { st->tile_cols = T0; st->num_ctas = ctas0; st->kernel_launches += launches; }
+      *nzcap_used = nzcap;
+      return SPMESL_OK;
+    }
+    if (nzcap >= p) break;
+    nzcap = (int)std::min<int64_t>(p, (int64_t)nzcap * 4);
+  }
+  return fail(SPMESL_ERR_OOM, "coefficient list overflow");
+}
+
 // Runs CD for [cb, ce) with automatic coefficient-list regrowth on overflow.
 int fit_columns_core(Workspace& W, const double* dX, int64_t n, int64_t p, int64_t cb, int64_t ce,
                      double lambda0, double tol, int32_t max_iter, const spmesl_options& o,
                      const FitOut& out, cudaStream_t s, spmesl_stats* st, Layout& L,
                      int* nzcap_used) {
   const int64_t m = ce - cb;
-  L.n = n;
-  L.p = p;
-  L.n_pad = (int)(((n + KC - 1) / KC) * KC);
-  L.nchunk = L.n_pad / KC;
-  L.nblk = (p + J - 1) / J;
+  if (o.mode == 1)
+    return fit_joint_core(W, dX, n, p, cb, ce, lambda0, tol, max_iter, o, out, s, st, L,
+                          nzcap_used);
+  set_layout(L, n, p);
   const int T = choose_T(W, m, L.n_pad, o.tile_cols);
   if (!T || cd_stages(T, L.n_pad, W.smem_optin) < 2)
     return fail(SPMESL_ERR_UNSUPPORTED, "n = " + std::to_string(n) +
@@ -736,6 +847,9 @@ int spmesl_fit_columns_device(const double* dX, int64_t n, int64_t p, int64_t co
   if (rc) return rc;
   if (col_begin < 0 || col_end > p || col_begin >= col_end)
     return fail(SPMESL_ERR_ARG, "bad column range");
+  if (o.mode == 1 && (col_begin != 0 || col_end != p))
+    return fail(SPMESL_ERR_UNSUPPORTED, "mode 1 (joint stop over all columns) needs the whole "
+                                        "column range on one device");
   if (!dColCount || !dRows || !dVals || !nnz_out || !dSigmaStd || !dScale || !dIters)
     return fail(SPMESL_ERR_ARG, "output pointer is NULL");
   int dev;

@@ -355,6 +355,22 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
         const int cur = S.cur[c] ^ 1;
         const int cnt = S.cnt_new[c];
         const double maxd = S.maxd[c];
+        if (P.joint) {
+          // Algorithm 3: one sweep per launch; the host applies the joint stop.  Carry
+          // the residual (not recomputed inside the inner loop) and the list.
+          const double* r = Rs + (size_t)c * SR;
+          double* e = P.Ej + (size_t)col * n_pad;
+          for (int i = lane; i < n_pad; i += 32) e[i] = r[i];
+          __syncwarp();
+          if (lane == 0) {
+            P.nz_count[col] = cnt;
+            P.nz_cur[col] = cur;
+            P.sweeps[col] = S.sweeps[c] + 1;
+            atomicMax(P.joint_maxd, (unsigned long long)__double_as_longlong(maxd));
+            S.retire[c] = 1;
+          }
+          continue;
+        }
         int inner = S.inner[c] + 1;
         int flags = S.flags[c];
         bool done_inner = (maxd < P.tol) || inner >= P.max_inner;
@@ -442,7 +458,7 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
       int nl = 0;
       for (int c = 0; c < T_ && nl < got; ++c)
         if (S.col[c] < 0) {
-          const int col = start + nl;
+          const int col = P.joint ? P.act[start + nl] : start + nl;
           S.col[c] = col;
           S.ld_dst[nl++] = c;
           S.outer[c] = 0; S.sweeps[c] = 0; S.inner[c] = 0; S.flags[c] = 0;
@@ -450,6 +466,13 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
           S.sigma[c] = 1.0;                                     // P:608 sigma^(0) = 1
           S.lam[c] = P.lambda0;
           S.maxd[c] = 0.0;
+          if (P.joint) {                                        // resume the column (Alg. 3)
+            S.sweeps[c] = P.sweeps[col];
+            S.cur[c] = P.nz_cur[col];
+            S.cnt_old[c] = P.nz_count[col];
+            S.sigma[c] = P.sigma_std[col];
+            S.lam[c] = S.sigma[c] * P.lambda0;
+          }
         }
       S.nloads = nl;
       // compaction: move the highest active slots into the lowest holes (loads took the
@@ -487,7 +510,12 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
         const int c = S.ld_dst[l];
         const int64_t gcol = cb + S.col[c];
         double* dst = Rs + (size_t)c * SR;
-        for (int i = tid; i < n_pad; i += WORK_THREADS) dst[i] = P.Xb[xb_index(i, gcol, nchunk)];
+        if (P.joint) {
+          const double* e = P.Ej + (size_t)S.col[c] * n_pad;
+          for (int i = tid; i < n_pad; i += WORK_THREADS) dst[i] = e[i];
+        } else {
+          for (int i = tid; i < n_pad; i += WORK_THREADS) dst[i] = P.Xb[xb_index(i, gcol, nchunk)];
+        }
       }
     }
     const int A = S.A;

@@ -92,6 +92,12 @@ struct CDParams {
   int* iters;              // [ncols]
   int* sweeps;             // [ncols]
   uint8_t* converged;      // [ncols]
+  // Algorithm 3 joint mode (mode 1): every queued column does exactly one sweep at its current
+  // sigma and lambda, starting from its carried residual, then hands its state back
+  int joint;
+  const int* act;          // [ncols] local column index of each queue entry (active set I)
+  double* Ej;              // [m][n_pad] residual e_c carried between launches
+  unsigned long long* joint_maxd;   // max over columns of max_j |db_jc| (bits of a double >= 0)
 };
 
 struct TailParams {
@@ -130,6 +136,18 @@ cudaError_t launch_gram_pass(const double* Xb, int nblk, int nchunk, int n, int 
 cudaError_t launch_tail_mark(const TailState* tail, int M, const int* nz_rows, int nzcap, int* umark,
                              cudaStream_t s);
 cudaError_t launch_tail_sweeps(const TailParams& P, int grid, cudaStream_t s);
+
+// Algorithm 3 joint mode helpers (joint.cu)
+cudaError_t launch_joint_init(const double* Xb, int64_t col_begin, int m, int n_pad, int nchunk,
+                              int* act, double* sigma, double* Ej, cudaStream_t s);
+cudaError_t launch_joint_sigma(const double* Xb, int64_t col_begin, const int* act, int nact,
+                               const int* nz_rows, const double* nz_vals, const int* nz_count,
+                               const int* nz_cur, int nzcap, int n, int n_pad, int nchunk,
+                               double sqrt_n, double sigma_floor, double tol, int capped,
+                               double* sigma, int* iters, uint8_t* jflags, uint8_t* converged,
+                               double* Ej, uint8_t* keep, cudaStream_t s);
+cudaError_t launch_joint_compact(const int* act, const uint8_t* keep, int nact, int* act_out,
+                                 int* nact_out, cudaStream_t s);
 
 size_t cd_smem_bytes(int T, int n_pad);          // with the minimum 2 stages
 int cd_stages(int T, int n_pad, size_t smem_optin);  // stages that fit (0: does not fit)

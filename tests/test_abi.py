@@ -84,7 +84,7 @@ def test_argument_validation_before_any_cuda_call(S):
     assert _call(S, X, 10, 5, max_iter=0) == -1
     assert _call(S, X, 10, 5, max_inner=0) == -1
     assert _call(S, X, 10, 5, tile_cols=12) == -1
-    assert _call(S, X, 10, 5, mode=1) == -1
+    assert _call(S, X, 10, 5, mode=2) == -1
     assert b"mode" in S.load().spmesl_last_error()
 
 
