@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--mode", default="per_column", choices=["per_column", "joint"],
+                    help="per_column (default; Alg. 1/2 stop) or joint (Algorithm 3, P:938-990)")
     return ap.parse_args()
 
 
@@ -218,6 +220,8 @@ def run_ours(args):
         local = 0
     torch.cuda.set_device(local)
     dist = None
+    if world > 1 and args.mode != "per_column":
+        raise SystemExit("--mode joint runs on one GPU (its stop is a max over all columns)")
     if world > 1:
         import torch.distributed as dist
         if share:
@@ -249,7 +253,7 @@ def run_ours(args):
 
     def step():
         if world == 1:
-            r = S.fit_device(Xd, lam, TOL, MAX_ITER, stream=stream, out=outbuf)
+            r = S.fit_device(Xd, lam, TOL, MAX_ITER, stream=stream, out=outbuf, mode=args.mode)
             return r.stats, r
         r = D.fit_distributed(Xd, lam, TOL, MAX_ITER, stream=stream)
         return r["stats"], r
@@ -316,7 +320,7 @@ def run_ours(args):
             ih = torch.empty(p, dtype=torch.int32).pin_memory()
             import ctypes
             L = S.load()
-            o = S.default_options()
+            o = S.default_options(mode=S.MODES[args.mode])
 
             def e2e_step():
                 rc = L.spmesl_fit_ex(ctypes.c_void_p(Xh.data_ptr()), n, p, lam, TOL, MAX_ITER,
@@ -366,7 +370,7 @@ def run_ours(args):
                "api": "spmesl_fit_ex (host pointers)" if world == 1 else
                       "fit_distributed with host pinned H2D/D2H"}
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.mode == "per_column":
         cpu = cpu_baseline(X, lam, args.cpu_seconds)
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -377,7 +381,7 @@ def run_ours(args):
                     "sweeps_total": stats_last["total_sweeps"],
                     "max_sweeps": stats_last["max_sweeps"], "max_outer": stats_last["max_outer"],
                     "nnz": stats_last["nnz"], "tile_cols": stats_last["tile_cols"],
-                    "num_ctas": stats_last["num_ctas"]}),
+                    "num_ctas": stats_last["num_ctas"], "mode": args.mode}),
                 "roofline": roof, "clocks": clk.summary(), "e2e": e2e,
                 "gpu_launches": int(stats_last["kernel_launches"]) * args.steps,
                 "ms_breakdown": {"standardize": stats_last["ms_standardize"],
