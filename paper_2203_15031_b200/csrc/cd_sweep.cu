@@ -128,6 +128,7 @@ struct SlotState {
   // control
   int A;
   int go;
+  int taken;            // columns this CTA has taken from the queue
   int nmoves, nloads;
   int mv_dst[MAX_T], mv_src[MAX_T];
   int ld_dst[MAX_T];
@@ -173,11 +174,15 @@ __device__ __forceinline__ void gemm_block(const double* __restrict__ Xs, const 
                                            int grp, int wg, int m0, int n0, int nchunk, int NSTG,
                                            int& s, uint32_t& ph, int SR, double inv_n, int lane) {
   const int g = lane >> 2, t4 = lane & 3;
-  double acc[MT][NT][2];
+  // two accumulators per 8x8 tile: even samples (h = 0) and odd samples (h = 1) of each pair,
+  // so consecutive DMMAs never depend on each other; summed as (even + odd) at the end
+  double acc[MT][NT][2][2];
 #pragma unroll
   for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
-    for (int ni = 0; ni < NT; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+    for (int ni = 0; ni < NT; ++ni)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) acc[mi][ni][h][0] = acc[mi][ni][h][1] = 0.0;
   const double* rbase = Rs + (size_t)(n0 * 8 + g) * SR + 2 * t4;
   for (int q = grp; q < nchunk; q += 2) {
     mbar_wait(&full[s], ph);
@@ -194,11 +199,11 @@ __device__ __forceinline__ void gemm_block(const double* __restrict__ Xs, const 
 #pragma unroll
       for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < NT; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi].x, bb[ni].x);
+        for (int ni = 0; ni < NT; ++ni) dmma(acc[mi][ni][0][0], acc[mi][ni][0][1], a[mi].x, bb[ni].x);
 #pragma unroll
       for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < NT; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi].y, bb[ni].y);
+        for (int ni = 0; ni < NT; ++ni) dmma(acc[mi][ni][1][0], acc[mi][ni][1][1], a[mi].y, bb[ni].y);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -211,8 +216,8 @@ __device__ __forceinline__ void gemm_block(const double* __restrict__ Xs, const 
 #pragma unroll
       for (int ni = 0; ni < NT; ++ni) {
         double* z = Zb + (size_t)((n0 + ni) * 8 + 2 * t4) * JP + (m0 + mi) * 8 + g;
-        z[0] = acc[mi][ni][0];
-        z[JP] = acc[mi][ni][1];
+        z[0] = acc[mi][ni][0][0] + acc[mi][ni][1][0];
+        z[JP] = acc[mi][ni][0][1] + acc[mi][ni][1][1];
       }
   }
   named_bar_sync(BAR_PAIR0 + wg, 64);
@@ -222,8 +227,8 @@ __device__ __forceinline__ void gemm_block(const double* __restrict__ Xs, const 
 #pragma unroll
       for (int ni = 0; ni < NT; ++ni) {
         double* z = Zb + (size_t)((n0 + ni) * 8 + 2 * t4) * JP + (m0 + mi) * 8 + g;
-        z[0] = (acc[mi][ni][0] + z[0]) * inv_n;
-        z[JP] = (acc[mi][ni][1] + z[JP]) * inv_n;
+        z[0] = ((acc[mi][ni][0][0] + acc[mi][ni][1][0]) + z[0]) * inv_n;
+        z[JP] = ((acc[mi][ni][0][1] + acc[mi][ni][1][1]) + z[JP]) * inv_n;
       }
   }
 }
@@ -303,7 +308,7 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
     S.nchg[0][c] = S.nchg[1][c] = 0;
   }
   for (size_t e = tid; e < (size_t)T * SR; e += blockDim.x) Rs[e] = 0.0;
-  if (tid == 0) S.A = 0;
+  if (tid == 0) { S.A = 0; S.taken = 0; }
   __syncthreads();
 
   // ===================================================== producer warp: X tile stream
@@ -448,12 +453,21 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
       for (int c = 0; c < T_; ++c) nfree += (S.col[c] < 0);
       int got = 0, start = 0;
       if (nfree > 0 && !std_error) {
-        // take at most a fair share of what is left, so the last wave stays balanced
-        const int left = ncols - *(volatile int*)P.queue;
-        const int share = max(1, (left + (int)gridDim.x - 1) / (int)gridDim.x);
+        // each CTA first takes its quota (an equal split of the queue, so when every column
+        // needs the same number of sweeps all CTAs finish together); past its quota it takes
+        // at most a fair share of what is left (work stealing from slower CTAs)
+        const int quota = ncols / (int)gridDim.x + ((int)blockIdx.x < ncols % (int)gridDim.x);
+        int share;
+        if (S.taken < quota) {
+          share = quota - S.taken;
+        } else {
+          const int left = ncols - *(volatile int*)P.queue;
+          share = max(1, (left + (int)gridDim.x - 1) / (int)gridDim.x);
+        }
         const int want = min(nfree, share);
         start = atomicAdd(P.queue, want);
         got = max(0, min(want, ncols - start));
+        S.taken += got;
       }
       int nl = 0;
       for (int c = 0; c < T_ && nl < got; ++c)

@@ -81,7 +81,7 @@ struct CDParams {
   TailState* tail;         // [ncols]
   int debug;               // development timing switches (SPMESL_CD_DEBUG; 0 in production)
   long long* dbg;          // development phase timers (debug & 4)
-  int* queue;              // atomic head (local column index)
+  int* queue;              // atomic head (queue index)
   int* flags;              // FLAG_*
   const int* err_in;       // standardization error code (CD exits early when nonzero)
   int* nz_rows;            // [ncols][2][nzcap]
