@@ -73,7 +73,15 @@ typedef struct {
   int32_t tail_after;     /* columns still running after this many sweeps finish in the
                              covariance-update tail solver (default 1; 0: never).  Same
                              iterates up to rounding. */
-  int32_t reserved[8];
+  int32_t solver;         /* 0 (default): auto — the Gram solver when mode = 0, the whole
+                             column range is fitted on one device, p is at most ~26000 (the
+                             sweep kernel keeps z[p] on chip) and 8 p^2 bytes fit in device
+                             memory; else the residual solver.  1: residual solver (persistent
+                             CD kernel on X~ streamed through shared memory).  2: Gram solver
+                             (S = X~^T X~ / n by a symmetric DMMA contraction with fused
+                             first-sweep screening, then covariance updates; SPMESL_ERR_UNSUPPORTED
+                             where it does not apply).  Same iterates up to rounding. */
+  int32_t reserved[7];
 } spmesl_options;
 
 typedef struct {
@@ -95,6 +103,9 @@ typedef struct {
   int64_t tail_columns;   /* columns finished by the tail solver */
   int64_t tail_gram_ondemand; /* Gram columns the tail solver computed on first use */
   int64_t tail_sweeps;    /* sweeps performed by the tail solver (the CD kernel did the rest) */
+  int32_t solver;         /* solver used: 1 residual, 2 Gram */
+  int32_t pad0;
+  double  ms_gram;        /* Gram solver: device time of the symmetric Gram + screening kernel */
 } spmesl_stats;
 
 /* Fill *opt with the defaults listed above. */

@@ -46,16 +46,19 @@ def _vp(a) -> ctypes.c_void_p:
 
 
 MODES = {"per_column": 0, "joint": 1}
+SOLVERS = {"auto": 0, "residual": 1, "gram": 2}
 
 
 def _opts(max_inner=10000, standardize=True, symmetrize=True, sigma_floor=1e-8, tile_cols=0,
-          device=-1, tail_after=1, mode="per_column") -> _lib.Options:
-    """mode: "per_column" (Algorithm 1 stop per column) or "joint" (Algorithm 3)."""
+          device=-1, tail_after=1, mode="per_column", solver="auto") -> _lib.Options:
+    """mode: "per_column" (Algorithm 1 stop per column) or "joint" (Algorithm 3).
+    solver: "auto", "residual" (CD on X~) or "gram" (covariance updates on X~^T X~ / n)."""
     return default_options(max_inner=int(max_inner), standardize=int(bool(standardize)),
                            symmetrize=int(bool(symmetrize)), sigma_floor=float(sigma_floor),
                            tile_cols=int(tile_cols), device=int(device),
-                           tail_after=int(tail_after), mode=MODES[mode] if isinstance(mode, str)
-                           else int(mode))
+                           tail_after=int(tail_after),
+                           mode=MODES[mode] if isinstance(mode, str) else int(mode),
+                           solver=SOLVERS[solver] if isinstance(solver, str) else int(solver))
 
 
 def fit(X, lambda0: float, tol: float = 1e-4, max_iter: int = 100, *, out_theta=None,

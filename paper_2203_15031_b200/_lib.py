@@ -32,7 +32,8 @@ class Options(ctypes.Structure):
         ("tile_cols", ctypes.c_int32),
         ("device", ctypes.c_int32),
         ("tail_after", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 8),
+        ("solver", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 7),
     ]
 
 
@@ -56,6 +57,9 @@ class Stats(ctypes.Structure):
         ("tail_columns", ctypes.c_int64),
         ("tail_gram_ondemand", ctypes.c_int64),
         ("tail_sweeps", ctypes.c_int64),
+        ("solver", ctypes.c_int32),
+        ("pad0", ctypes.c_int32),
+        ("ms_gram", ctypes.c_double),
     ]
 
     def asdict(self):

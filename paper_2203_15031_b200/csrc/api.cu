@@ -82,6 +82,7 @@ struct Workspace {
       nz_rows, nz_vals, col_ptr, csc_rows, csc_vals;
   Buffer tail, umark, umap, uvars, tailV, zall, ondemand;   // tail solver
   Buffer ej, act0, act1, keep, jflags;                      // mode 1 (Algorithm 3)
+  Buffer hit;                                               // Gram solver screening flags
   // host-API staging
   Buffer hx, htheta, hsigma, hiters, hsweeps, hconv, coo_r, coo_c, coo_v, hdiag, zeros;
   DevCounters* host_counters = nullptr;   // pinned
@@ -130,6 +131,7 @@ int validate(const void* X, int64_t n, int64_t p, double lambda0, double tol, in
   if (o.max_inner < 1) return fail(SPMESL_ERR_ARG, "max_inner must be >= 1");
   if (!(o.sigma_floor > 0.0)) return fail(SPMESL_ERR_ARG, "sigma_floor must be > 0");
   if (o.mode != 0 && o.mode != 1) return fail(SPMESL_ERR_ARG, "mode must be 0 (per-column stop) or 1 (Algorithm 3 joint stop)");
+  if (o.solver < 0 || o.solver > 2) return fail(SPMESL_ERR_ARG, "solver must be 0, 1 or 2");
   if (o.tile_cols != 0 && o.tile_cols != 8 && o.tile_cols != 16 && o.tile_cols != 32)
     return fail(SPMESL_ERR_ARG, "tile_cols must be 0, 8, 16 or 32");
   const double pp = (double)p * (double)p * 8.0;
@@ -247,7 +249,7 @@ int run_tail(Workspace& W, const Layout& L, int64_t cb, double lambda0, double t
 
 // Scratch reset + standardize (a2) + Gram band for columns [cb, cb + m) on stream s.
 int run_prep(Workspace& W, const double* dX, int64_t m, const spmesl_options& o, const Layout& L,
-             cudaStream_t s) {
+             cudaStream_t s, bool band = true) {
   CUDA_TRY(cudaMemsetAsync(W.xb.ptr, 0, L.xb_doubles() * 8, s));
   CUDA_TRY(cudaMemsetAsync(W.counters.ptr, 0, sizeof(DevCounters), s));
   CUDA_TRY(cudaMemsetAsync((char*)W.counters.ptr + offsetof(DevCounters, bad_key), 0xff, 8, s));
@@ -258,7 +260,7 @@ int run_prep(Workspace& W, const double* dX, int64_t m, const spmesl_options& o,
   DevCounters* dc = (DevCounters*)W.counters.ptr;
   CUDA_TRY(launch_standardize(dX, L, o.standardize, (double*)W.xb.ptr, (double*)W.mean.ptr,
                               (double*)W.scale.ptr, &dc->err, &dc->bad_key, s));
-  CUDA_TRY(launch_gram((const double*)W.xb.ptr, L, (double*)W.gband.ptr, s));
+  if (band) CUDA_TRY(launch_gram((const double*)W.xb.ptr, L, (double*)W.gband.ptr, s));
   CUDA_TRY(cudaEventRecord(W.ev[1], s));
   return SPMESL_OK;
 }
@@ -285,6 +287,10 @@ CDParams cd_params(Workspace& W, const Layout& L, int64_t cb, int64_t m, double 
   P.max_inner = o.max_inner;
   P.T = T;
   P.nst = cd_stages(T, L.n_pad, W.smem_optin);
+  if (const char* e = getenv("SPMESL_CD_NST")) {   // development: cap the X ring depth
+    const int v = atoi(e) & ~1;
+    if (v >= 2 && v < P.nst) P.nst = v;
+  }
   P.nzcap = nzcap;
   P.evict_after = tail_enabled(W, o, L, nzcap) ? o.tail_after : 0;
   P.tail_count = &dc->tail_count;
@@ -525,6 +531,113 @@ int fit_joint_core(Workspace& W, const double* dX, int64_t n, int64_t p, int64_t
   return fail(SPMESL_ERR_OOM, "coefficient list overflow");
 }
 
+// Whether the Gram solver applies (see spmesl_options.solver).
+bool gram_applicable(const Workspace& W, const spmesl_options& o, int64_t n, int64_t p, int64_t cb,
+                     int64_t ce, std::string* why) {
+  if (o.mode != 0) { if (why) *why = "the Gram solver implements mode 0"; return false; }
+  if (cb != 0 || ce != p) { if (why) *why = "the Gram solver fits the whole column range"; return false; }
+  const int n_pad = (int)(((n + KC - 1) / KC) * KC);
+  if (tail_smem_bytes((int)p, n_pad, initial_nzcap(n, p)) > (size_t)W.smem_optin) {
+    if (why) *why = "p too large for the on-chip gradient vector";
+    return false;
+  }
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) { cudaGetLastError(); free_b = 0; }
+  const double need = (double)p * (double)p * 8.0;
+  const double have = (double)free_b + (double)W.ondemand.bytes;
+  if (need > 0.6 * have) { if (why) *why = "8 p^2 bytes do not fit in device memory"; return false; }
+  return true;
+}
+
+// Gram solver for [0, p): standardize, S = X~^T X~ / n with fused
+// screening, retire the columns whose first sweep changes nothing, covariance-update sweeps for
+// the rest (tail.cu with z = S[:, c]).  Coefficient lists regrow on overflow.
+int fit_gram_core(Workspace& W, const double* dX, int64_t n, int64_t p, double lambda0, double tol,
+                  int32_t max_iter, const spmesl_options& o, const FitOut& out, cudaStream_t s,
+                  spmesl_stats* st, Layout& L, int* nzcap_used) {
+  const int64_t m = p;
+  set_layout(L, n, p);
+  int nzcap = initial_nzcap(n, p);
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    int rc = alloc_core(W, L, m, nzcap);
+    if (rc) return rc;
+    if (tail_smem_bytes((int)p, L.n_pad, nzcap) > (size_t)W.smem_optin)
+      return fail(SPMESL_ERR_UNSUPPORTED, "Gram solver: sweep state does not fit on chip");
+    if ((rc = ensure(W.ondemand, (size_t)p * p * 8))) return rc;
+    if ((rc = ensure(W.hit, (size_t)p))) return rc;
+    DevCounters* dc = (DevCounters*)W.counters.ptr;
+    if ((rc = run_prep(W, dX, m, o, L, s, /*band=*/false))) return rc;
+    CUDA_TRY(cudaMemsetAsync(W.hit.ptr, 0, (size_t)p, s));
+    GramParams G{};
+    G.Xb = (const double*)W.xb.ptr;
+    G.n = (int)n; G.n_pad = L.n_pad; G.nchunk = L.nchunk; G.p = (int)p; G.nblk = (int)L.nblk;
+    G.col_begin = 0;
+    G.ncols = (int)m;
+    G.lambda0 = lambda0; G.tol = tol; G.sigma_floor = o.sigma_floor; G.sqrt_n = std::sqrt((double)n);
+    G.max_outer = max_iter;
+    G.G = (double*)W.ondemand.ptr;
+    G.hit = (uint8_t*)W.hit.ptr;
+    G.tail = (TailState*)W.tail.ptr;
+    G.tail_count = &dc->tail_count;
+    G.sigma_std = out.sigma_std; G.iters = out.iters; G.sweeps = out.sweeps;
+    G.converged = out.conv;
+    G.nz_count = (int*)W.nz_count.ptr; G.nz_cur = (int*)W.nz_cur.ptr;
+    const int nT = (int)((L.nblk + 3) / 4);
+    const int ntiles = nT * (nT + 1) / 2;
+    CUDA_TRY(launch_syrk_screen(G, std::min(W.sms, ntiles), s));
+    CUDA_TRY(cudaEventRecord(W.ev[7], s));
+    CUDA_TRY(launch_gram_init(G, s));
+    if ((rc = read_counters(W, s))) return rc;
+    if (W.host_counters->err) return std_error(W, st);
+    const int M = W.host_counters->tail_count;
+    CUDA_TRY(cudaEventRecord(W.ev[5], s));
+    if (M > 0) {
+      TailParams T{};
+      T.Xb = (const double*)W.xb.ptr;
+      T.n = (int)n; T.n_pad = L.n_pad; T.nchunk = L.nchunk; T.p = (int)p; T.nblk = (int)L.nblk;
+      T.col_begin = 0;
+      T.lambda0 = lambda0; T.tol = tol; T.sigma_floor = o.sigma_floor; T.sqrt_n = std::sqrt((double)n);
+      T.max_outer = max_iter; T.max_inner = o.max_inner;
+      T.nzcap = nzcap;
+      T.M = M;
+      T.tail = (const TailState*)W.tail.ptr;
+      T.Zz = nullptr;
+      T.Gtab = (double*)W.ondemand.ptr;
+      T.gstate = nullptr;
+      T.z_from_gtab = 1;
+      T.gtab_full = 1;
+      T.next = &dc->tail_next;
+      T.ondemand_count = &dc->gram_ondemand;
+      T.sweeps_count = &dc->tail_sweeps;
+      T.flags = &dc->err;
+      T.nz_rows = (int*)W.nz_rows.ptr; T.nz_vals = (double*)W.nz_vals.ptr;
+      T.nz_count = (int*)W.nz_count.ptr; T.nz_cur = (int*)W.nz_cur.ptr;
+      T.sigma_std = out.sigma_std; T.iters = out.iters; T.sweeps = out.sweeps; T.converged = out.conv;
+      CUDA_TRY(launch_tail_sweeps(T, std::min(M, W.sms), s));
+    }
+    CUDA_TRY(cudaEventRecord(W.ev[6], s));
+    CUDA_TRY(cudaEventRecord(W.ev[2], s));
+    if ((rc = read_counters(W, s))) return rc;
+    if (!W.host_counters->overflow) {
+      if (st) {
+        st->solver = 2;
+        st->tile_cols = 0;
+        st->num_ctas = std::min(W.sms, ntiles);
+        st->kernel_launches += 2 + (M > 0 ? 1 : 0);
+        st->ms_gram = ev_ms(W.ev[1], W.ev[7]);
+        st->ms_tail = ev_ms(W.ev[5], W.ev[6]);
+        st->tail_columns = M;
+        st->tail_sweeps = W.host_counters->tail_sweeps;
+      }
+      *nzcap_used = nzcap;
+      return SPMESL_OK;
+    }
+    if (nzcap >= p) break;
+    nzcap = (int)std::min<int64_t>(p, (int64_t)nzcap * 4);
+  }
+  return fail(SPMESL_ERR_OOM, "coefficient list overflow");
+}
+
 // Runs CD for [cb, ce) with automatic coefficient-list regrowth on overflow.
 int fit_columns_core(Workspace& W, const double* dX, int64_t n, int64_t p, int64_t cb, int64_t ce,
                      double lambda0, double tol, int32_t max_iter, const spmesl_options& o,
@@ -534,6 +647,14 @@ int fit_columns_core(Workspace& W, const double* dX, int64_t n, int64_t p, int64
   if (o.mode == 1)
     return fit_joint_core(W, dX, n, p, cb, ce, lambda0, tol, max_iter, o, out, s, st, L,
                           nzcap_used);
+  {
+    std::string why;
+    const bool ok = gram_applicable(W, o, n, p, cb, ce, &why);
+    if (o.solver == 2 && !ok) return fail(SPMESL_ERR_UNSUPPORTED, "solver = 2: " + why);
+    if (ok && o.solver != 1)
+      return fit_gram_core(W, dX, n, p, lambda0, tol, max_iter, o, out, s, st, L, nzcap_used);
+  }
+  if (st) st->solver = 1;
   set_layout(L, n, p);
   const int T = choose_T(W, m, L.n_pad, o.tile_cols);
   if (!T || cd_stages(T, L.n_pad, W.smem_optin) < 2)

@@ -1,0 +1,253 @@
+// Gram solver: S = X~^T X~ / n once, by a symmetric DMMA
+// contraction (only the upper triangle of 128 x 128 tiles is computed; each tile is written
+// to both G[I, J] and G[J, I]), then covariance-update coordinate descent on it.
+//
+// Why: for b_c = 0 the residual of column c is x~_c, so the first sweep of every column of
+// Algorithm 1 visits z_j = x~_j^T x~_c / n = G_jc — the first sweeps of all p
+// columns together ARE the Gram matrix (2 n p^2 flops); computing it once with symmetry costs
+// n p (p + 1).  The screening test of that first sweep (b_j = 0 stays 0 unless |G_jc| >
+// lambda0, since sigma^(0) = 1) is fused into the tile epilogue: a column with no
+// hit finishes its first sweep with no change, and its outer iteration ends right there
+// (gram_init_kernel); the others continue in the covariance-update sweep kernel (tail.cu) from
+// z = G[:, c].  Iterates are Algorithm 1's up to rounding (the residual identity of Prop. 2).
+#include "spmesl_internal.cuh"
+
+namespace spmesl {
+
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32g(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init_g(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32g(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_g(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32g(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_g(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32g(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_g(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32g(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_g(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32g(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32g(bar))
+      : "memory");
+}
+__device__ __forceinline__ void dmma_g(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+constexpr int GB = 4;                  // 32-row blocks per tile side (tile = 128 x 128)
+constexpr int G_MMA_WARPS = 8;
+constexpr int G_THREADS = (G_MMA_WARPS + 1) * 32;
+constexpr int G_STAGE_DOUBLES = 2 * GB * CHUNK_DOUBLES;     // 8 Xb tiles = 64 KB
+constexpr int G_MAX_NST = 3;
+
+// tile index t of the upper triangle (I <= J) of an nT x nT tile grid, row-major by I
+__device__ __forceinline__ void tri_tile(int t, int nT, int& I, int& Jt) {
+  int i = 0, rowlen = nT;
+  while (t >= rowlen) { t -= rowlen; ++i; --rowlen; }
+  I = i;
+  Jt = i + t;
+}
+
+__global__ void __launch_bounds__(G_THREADS, 1) syrk_screen_kernel(const GramParams P) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  uint64_t* full = (uint64_t*)smem_raw;
+  uint64_t* empty = full + G_MAX_NST;
+  double* Xs = (double*)(smem_raw + 128);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nst = P.nst;
+  const int nchunk = P.nchunk, nblk = P.nblk, p = P.p;
+  const int nT = (nblk + GB - 1) / GB;
+  const int ntiles = nT * (nT + 1) / 2;
+  if (tid == 0) {
+    for (int s = 0; s < nst; ++s) {
+      mbar_init_g(&full[s], 1);
+      mbar_init_g(&empty[s], G_MMA_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == G_MMA_WARPS) {
+    // ---------------------------------------------------------------- producer
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int I, Jt;
+        tri_tile(t, nT, I, Jt);
+        for (int q = 0; q < nchunk; ++q) {
+          mbar_wait_g(&empty[s], ph ^ 1u);
+          double* st = Xs + (size_t)s * G_STAGE_DOUBLES;
+          int cnt = 0;
+          for (int u = 0; u < 2 * GB; ++u) {
+            const int blk = (u < GB ? I * GB + u : Jt * GB + (u - GB));
+            if (blk < nblk) ++cnt;
+          }
+          mbar_expect_g(&full[s], (uint32_t)cnt * CHUNK_BYTES);
+          for (int u = 0; u < 2 * GB; ++u) {
+            const int blk = (u < GB ? I * GB + u : Jt * GB + (u - GB));
+            if (blk < nblk)
+              bulk_g2s_g(st + (size_t)u * CHUNK_DOUBLES,
+                         P.Xb + ((size_t)blk * nchunk + q) * CHUNK_DOUBLES, CHUNK_BYTES, &full[s]);
+          }
+          if (++s == nst) { s = 0; ph ^= 1u; }
+        }
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------ MMA warps
+  const int g = lane >> 2, t4 = lane & 3, sw = g & 1;
+  const int mh = warp & 1;          // rows [64 mh, 64 mh + 64) of the tile
+  const int nq = warp >> 1;         // cols [32 nq, 32 nq + 32)
+  const double inv_n = 1.0 / (double)P.n;
+  const double lam0 = P.lambda0;
+  int s = 0;
+  uint32_t ph = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    int I, Jt;
+    tri_tile(t, nT, I, Jt);
+    double acc[8][4][2];
+#pragma unroll
+    for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+    for (int q = 0; q < nchunk; ++q) {
+      mbar_wait_g(&full[s], ph);
+      const double* st = Xs + (size_t)s * G_STAGE_DOUBLES;
+      const double* abase = st + (size_t)(2 * mh) * CHUNK_DOUBLES + (size_t)g * XS + 2 * t4;
+      const double* bbase = st + (size_t)(GB + nq) * CHUNK_DOUBLES + (size_t)g * XS + 2 * t4;
+#pragma unroll
+      for (int kp = 0; kp < KC / 8; ++kp) {
+        const int ko = (kp ^ sw) * 8;
+        double2 b[4];
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) b[ni] = *(const double2*)(bbase + ni * 8 * XS + ko);
+#pragma unroll
+        for (int mi = 0; mi < 8; ++mi) {
+          // (one A fragment live at a time: 9 warps leave 168 registers per thread)
+          const double2 a = *(const double2*)(abase + (size_t)(mi >> 2) * CHUNK_DOUBLES +
+                                              (mi & 3) * 8 * XS + ko);
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) dmma_g(acc[mi][ni][0], acc[mi][ni][1], a.x, b[ni].x);
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) dmma_g(acc[mi][ni][0], acc[mi][ni][1], a.y, b[ni].y);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_g(&empty[s]);
+      if (++s == nst) { s = 0; ph ^= 1u; }
+    }
+    // epilogue: G = acc / n to both triangles; screening hits |G_jc| > lambda0 (j != c)
+    const bool diag_tile = (I == Jt);
+    const int row0 = I * GB * J + 64 * mh;
+    const int col0 = Jt * GB * J + 32 * nq;
+#pragma unroll
+    for (int mi = 0; mi < 8; ++mi) {
+      const int row = row0 + mi * 8 + g;
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = col0 + ni * 8 + 2 * t4 + e;
+          if (row < p && col < p) {
+            const double v = acc[mi][ni][e] * inv_n;
+            __stcs(P.G + (size_t)col * p + row, v);
+            if (!diag_tile) __stcs(P.G + (size_t)row * p + col, v);
+            if (row != col && fabs(v) > lam0) {
+              P.hit[col] = 1;
+              if (!diag_tile) P.hit[row] = 1;
+            }
+          }
+        }
+    }
+  }
+}
+
+// Columns without a screening hit: the first sweep changes nothing (b stays 0, max|db| = 0),
+// so outer iteration 1 ends with the fresh residual x~_c (reading g4).  Retire it or,
+// if sigma moved by >= tol (possible only without standardization), hand it to the sweep
+// kernel like every column with a hit.
+__global__ void gram_init_kernel(const GramParams P) {
+  const int lane = threadIdx.x & 31;
+  const int c = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
+  if (c >= P.ncols) return;
+  const int64_t gc = P.col_begin + c;
+  TailState ts;
+  ts.col = c; ts.outer = 0; ts.sweeps = 0; ts.inner = 0; ts.flags = 0; ts.cur = 0; ts.cnt = 0;
+  ts.pad = 0; ts.sigma = 1.0;
+  if (!P.hit[gc]) {
+    double ss = 0.0;
+    for (int i = lane; i < P.n; i += 32) {
+      const double r = P.Xb[xb_index(i, gc, P.nchunk)];
+      ss = fma(r, r, ss);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    double sn = sqrt(ss) / P.sqrt_n;
+    if (sn < P.sigma_floor) sn = P.sigma_floor;                  // reading g5
+    if (lane == 0) {
+      const bool conv = fabs(sn - 1.0) < P.tol;
+      if (conv || P.max_outer <= 1) {
+        P.sigma_std[c] = sn;
+        P.iters[c] = 1;
+        P.sweeps[c] = 1;
+        P.converged[c] = (uint8_t)conv;
+        P.nz_count[c] = 0;
+        P.nz_cur[c] = 0;
+        return;
+      }
+      ts.outer = 1; ts.sweeps = 1; ts.sigma = sn;
+    } else {
+      return;
+    }
+  }
+  if (lane == 0) P.tail[atomicAdd(P.tail_count, 1)] = ts;
+}
+
+}  // namespace
+
+size_t syrk_smem_bytes(int nst) { return 128 + (size_t)nst * G_STAGE_DOUBLES * 8; }
+
+cudaError_t launch_syrk_screen(const GramParams& P, int grid, cudaStream_t s) {
+  GramParams Q = P;
+  Q.nst = G_MAX_NST;
+  const size_t smem = syrk_smem_bytes(Q.nst);
+  cudaError_t e = cudaFuncSetAttribute(syrk_screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  syrk_screen_kernel<<<grid, G_THREADS, smem, s>>>(Q);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gram_init(const GramParams& P, cudaStream_t s) {
+  if (P.ncols <= 0) return cudaSuccess;
+  const int wpb = 8;
+  gram_init_kernel<<<(P.ncols + wpb - 1) / wpb, wpb * 32, 0, s>>>(P);
+  return cudaGetLastError();
+}
+
+}  // namespace spmesl

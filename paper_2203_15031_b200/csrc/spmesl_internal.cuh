@@ -115,6 +115,8 @@ struct TailParams {
   int* next;               // atomic work counter
   int* ondemand_count;     // Gram columns computed on first use
   int* sweeps_count;       // sweeps performed here
+  int z_from_gtab;         // 1: z starts as Gtab[:, col] (Gram solver: b = 0, r = x~_c)
+  int gtab_full;           // 1: every Gram column is present (no on-demand path)
   int* flags;
   int* nz_rows;            // column coefficient lists (as in CDParams)
   double* nz_vals;
@@ -125,6 +127,30 @@ struct TailParams {
   int* sweeps;
   uint8_t* converged;
 };
+// Gram solver (gram_full.cu): symmetric S = X~^T X~ / n with fused first-sweep screening.
+struct GramParams {
+  const double* Xb;
+  int n, n_pad, nchunk, p, nblk;
+  int64_t col_begin;
+  int ncols;
+  double lambda0, tol, sigma_floor, sqrt_n;
+  int max_outer;
+  int nst;
+  double* G;               // [p][p] column-major
+  uint8_t* hit;            // [p] column has some |G_jc| > lambda0, j != c
+  TailState* tail;         // columns for the sweep kernel
+  int* tail_count;
+  double* sigma_std;
+  int* iters;
+  int* sweeps;
+  uint8_t* converged;
+  int* nz_count;
+  int* nz_cur;
+};
+size_t syrk_smem_bytes(int nst);
+cudaError_t launch_syrk_screen(const GramParams& P, int grid, cudaStream_t s);
+cudaError_t launch_gram_init(const GramParams& P, cudaStream_t s);
+
 constexpr int TAIL_THREADS = 256;
 constexpr int TAIL_ODC = 8;          // on-demand Gram column cache entries per CTA
 size_t tail_smem_bytes(int p, int n_pad, int nzcap);

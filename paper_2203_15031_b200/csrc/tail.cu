@@ -188,7 +188,12 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) tail_sweep_kernel(const TailP
     int cur = ts.cur;
     int ocnt = min(ts.cnt, nzcap);
     bool overflow = ts.cnt > nzcap;
-    for (int j = tid; j < p; j += TAIL_THREADS) z[j] = P.Zz[(size_t)k * p + j];
+    if (P.z_from_gtab) {
+      const double* gz = P.Gtab + (size_t)gc * p;
+      for (int j = tid; j < p; j += TAIL_THREADS) z[j] = __ldcs(gz + j);
+    } else {
+      for (int j = tid; j < p; j += TAIL_THREADS) z[j] = P.Zz[(size_t)k * p + j];
+    }
     {
       const size_t lo = (size_t)col * list_stride + (size_t)cur * nzcap;
       for (int m = tid; m < ocnt; m += TAIL_THREADS) { orow[m] = P.nz_rows[lo + m]; ov[m] = P.nz_vals[lo + m]; }
@@ -233,7 +238,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) tail_sweep_kernel(const TailP
           // Gram column G[:, j] from the fit-wide table: precomputed, or computed here once
           // (claim 0 -> 1, write, publish 2); every CTA is resident, so waiting is safe
           const double* gcol = P.Gtab + (size_t)j * p;
-          if (*(volatile int*)&P.gstate[j] != 2) {
+          if (!P.gtab_full && *(volatile int*)&P.gstate[j] != 2) {
             if (tid == 0) { TS.oc_var[0] = j; TS.k2 = atomicCAS(&P.gstate[j], 0, 1); }
             __syncthreads();
             if (TS.k2 == 0) {

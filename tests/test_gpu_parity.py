@@ -42,12 +42,14 @@ CASES = [
 
 @pytest.mark.parametrize("cfg,over,rule", CASES)
 @pytest.mark.parametrize("delta", [1e-4, 1e-10])
-def test_parity_host_api(S, oracle, cfg, over, rule, delta):
+@pytest.mark.parametrize("solver", ["residual", "gram"])
+def test_parity_host_api(S, oracle, cfg, over, rule, delta, solver):
     X, gt, spec = G.make_config(cfg, **over)
     n, p = X.shape
     lam = _lam(oracle, rule, n, p)
     ora = oracle.spmesl_fit(X, lam, delta=delta)
-    res = S.fit(X, lam, tol=delta, max_iter=100)
+    res = S.fit(X, lam, tol=delta, max_iter=100, solver=solver)
+    assert res.stats["solver"] == {"residual": 1, "gram": 2}[solver]
     rep = compare(res.Theta, res.sigma, res.iters, res.sweeps, ora)
     print(cfg, over, rule, delta, rep)
     assert_parity(rep)
@@ -61,24 +63,25 @@ def test_parity_host_api(S, oracle, cfg, over, rule, delta):
 def test_bit_identical_across_tile_sizes(S, oracle, T):
     X, _, _ = G.make_config(4, p=600, family="hub")
     lam = oracle.lambda_ub(*X.shape)
-    ref = S.fit(X, lam, tile_cols=8)
-    r = S.fit(X, lam, tile_cols=T)
+    ref = S.fit(X, lam, tile_cols=8, solver="residual")
+    r = S.fit(X, lam, tile_cols=T, solver="residual")
     assert np.array_equal(r.Theta, ref.Theta)
     assert np.array_equal(r.sigma, ref.sigma)
     assert np.array_equal(r.sweeps, ref.sweeps)
 
 
-def test_theta1_unsymmetrized_and_unstandardized(S, oracle):
+@pytest.mark.parametrize("solver", ["residual", "gram"])
+def test_theta1_unsymmetrized_and_unstandardized(S, oracle, solver):
     X, _, _ = G.make_config(2)
     n, p = X.shape
     lam = oracle.lambda_univ(n, p)
     ora = oracle.spmesl_fit(X, lam)
-    r = S.fit(X, lam, symmetrize=False)
+    r = S.fit(X, lam, symmetrize=False, solver=solver)
     d = np.abs(r.Theta - ora.Theta1)
     assert np.all(d <= 1e-8 * np.abs(ora.Theta1) + 1e-12 * ora.Theta1.diagonal().max())
     Xs, mu, s = oracle.standardize(X)
     ora2 = oracle.spmesl_fit(Xs, lam, standardize=False)
-    r2 = S.fit(Xs, lam, standardize=False)
+    r2 = S.fit(Xs, lam, standardize=False, solver=solver)
     assert_parity(compare(r2.Theta, r2.sigma, r2.iters, r2.sweeps, ora2))
 
 
@@ -105,7 +108,7 @@ def test_column_blocks_reproduce_full_fit(S, oracle):
     X, _, _ = G.make_config(4, p=900, family="hub")
     n, p = X.shape
     lam = oracle.lambda_ub(n, p)
-    full = S.fit(X, lam)
+    full = S.fit(X, lam, solver="residual")
     Xd = torch.from_numpy(np.ascontiguousarray(X)).cuda()
     bounds = [0, 250, 251, 600, 900]
     parts = [S.fit_columns_device(Xd, a, b, lam) for a, b in zip(bounds[:-1], bounds[1:])]
@@ -123,53 +126,59 @@ def test_column_blocks_reproduce_full_fit(S, oracle):
     assert np.array_equal(th2.cpu().numpy(), full.Theta[:, 300:700])
 
 
-def test_null_case_and_small_p(S, oracle):
+@pytest.mark.parametrize("solver", ["residual", "gram"])
+def test_null_case_and_small_p(S, oracle, solver):
     rng = np.random.default_rng(5)
-    for (n, p) in [(7, 2), (33, 3), (64, 31), (65, 33)]:
+    for (n, p) in [(7, 2), (33, 3), (64, 31), (65, 33), (40, 129)]:
         X = rng.standard_normal((n, p)) * rng.uniform(0.5, 2, p)
         for lam in (0.05, 0.3, 5.0):
             ora = oracle.spmesl_fit(X, lam)
-            r = S.fit(X, lam)
+            r = S.fit(X, lam, solver=solver)
             assert_parity(compare(r.Theta, r.sigma, r.iters, r.sweeps, ora))
 
 
-def test_errors(S):
+@pytest.mark.parametrize("solver", ["residual", "gram"])
+def test_errors(S, solver):
     X = np.random.default_rng(1).standard_normal((20, 40))
     X[:, 17] = 2.5
     with pytest.raises(S.SpmeslError) as e:
-        S.fit(X, 0.3)
+        S.fit(X, 0.3, solver=solver)
     assert e.value.code == -2 and e.value.bad_column == 17
     X[:, 17] = np.arange(20)
     X[3, 30] = np.inf
     X[0, 35] = np.nan
     with pytest.raises(S.SpmeslError) as e:
-        S.fit(X, 0.3)
+        S.fit(X, 0.3, solver=solver)
     assert e.value.code == -3 and e.value.bad_column == 30
     # the library recovers after an error
     X[3, 30] = 1.0
     X[0, 35] = 1.0
-    S.fit(X, 0.3)
+    S.fit(X, 0.3, solver=solver)
 
 
-def test_max_iter_cap_flags_columns(S, oracle):
+@pytest.mark.parametrize("solver", ["residual", "gram"])
+def test_max_iter_cap_flags_columns(S, oracle, solver):
     X, _, _ = G.make_config(2)
     lam = oracle.lambda_univ(*X.shape)
     ora = oracle.spmesl_fit(X, lam, max_outer=2)
-    r = S.fit(X, lam, max_iter=2)
+    r = S.fit(X, lam, max_iter=2, solver=solver)
     assert r.code == 1 and not r.converged.all()
     assert np.array_equal(r.converged, ora.converged)
     assert_parity(compare(r.Theta, r.sigma, r.iters, r.sweeps, ora))
 
 
-def test_full_size_config5_sampled_columns(S, oracle):
+@pytest.mark.parametrize("solver", ["residual", "gram"])
+def test_full_size_config5_sampled_columns(S, oracle, solver):
     """BASELINE config 5 at full size (n=500, p=20000) in the bench's launch configuration;
-    the oracle solves a sample of columns one by one (each column is independent)."""
+    the oracle solves a sample of columns one by one (each column is independent): random
+    columns plus every column that needed more than one sweep (at most 40 of them)."""
     X, _, spec = G.make_config(5)
     n, p = X.shape
     lam = oracle.lambda_ub(n, p)
-    r = S.fit(X, lam, symmetrize=False)        # Theta1: column k depends on column k only
+    r = S.fit(X, lam, symmetrize=False, solver=solver)   # Theta1: column k depends on k only
     rng = np.random.default_rng(0)
-    cols = np.sort(rng.choice(p, 48, replace=False))
+    multi = np.nonzero(r.sweeps > 1)[0][:40]
+    cols = np.unique(np.concatenate([rng.choice(p, 48, replace=False), multi]))
     Xs, mu, s = oracle.standardize(X)
     oc = oracle.spmesl_columns(Xs, cols, lam, want_margin=False)
     assert np.array_equal(r.iters[cols], oc.outer) and np.array_equal(r.sweeps[cols], oc.sweeps)
@@ -208,7 +217,7 @@ def test_two_ranks_sharing_one_gpu_match_single_fit(S, oracle):
     import torch.multiprocessing as mp
     X, _, _ = G.make_config(4, p=1200, family="hub")
     lam = oracle.lambda_ub(*X.shape)
-    full = S.fit(X, lam)
+    full = S.fit(X, lam, solver="residual")
     sk = socket.socket(); sk.bind(("127.0.0.1", 0)); port = sk.getsockname()[1]; sk.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -232,7 +241,7 @@ def test_tail_solver_handoff_points(S, oracle, tail_after):
     X, _, _ = G.make_config(4, p=700, n=300, family="hub")
     lam = oracle.lambda_ub(*X.shape)
     ora = oracle.spmesl_fit(X, lam)
-    r = S.fit(X, lam, tail_after=tail_after)
+    r = S.fit(X, lam, tail_after=tail_after, solver="residual")
     assert_parity(compare(r.Theta, r.sigma, r.iters, r.sweeps, ora))
     if tail_after == 0:
         assert r.stats["tail_columns"] == 0
@@ -248,7 +257,7 @@ def test_tail_solver_on_demand_gram_columns(S, oracle):
     X, _, _ = G.make_config(5, p=8000)
     n, p = X.shape
     lam = oracle.lambda_ub(n, p)
-    r = S.fit(X, lam, symmetrize=False)
+    r = S.fit(X, lam, symmetrize=False, solver="residual")
     assert r.stats["tail_columns"] > 0 and r.stats["tail_gram_ondemand"] > 0
     cols = np.nonzero(r.sweeps > 1)[0]
     assert len(cols) == r.stats["tail_columns"]
@@ -264,3 +273,23 @@ def test_tail_solver_on_demand_gram_columns(S, oracle):
         got = r.Theta[:, k]
         assert np.array_equal(got != 0, want != 0), k
         assert np.all(np.abs(got - want) <= 1e-8 * np.abs(want) + 1e-12 * abs(want[k])), k
+
+
+@pytest.mark.parametrize("solver", ["residual", "gram"])
+@pytest.mark.parametrize("mi", [1, 100])
+def test_unstandardized_scaled_columns_and_caps(S, oracle, solver, mi):
+    # standardize = 0 with column norms ||x_k||^2 / n in [0.64, 1.44] (sigma of a column whose
+    # first sweep changes nothing is then not 1, so it continues) and max_iter = 1.  (Unit-step
+    # CD assumes x_j^T x_j = n; norms far from that make both sides diverge alike.)
+    X, gt, spec = G.make_config(2)
+    n, p = X.shape
+    Xs, _, _ = oracle.standardize(X)
+    Xs = Xs * np.linspace(0.8, 1.2, p)[None, :]
+    lam = oracle.lambda_univ(n, p)
+    if True:
+        ora = oracle.spmesl_fit(Xs, lam, delta=1e-4, max_outer=mi, standardize=False)
+        res = S.fit(Xs, lam, tol=1e-4, max_iter=mi, standardize=False, solver=solver)
+        rep = compare(res.Theta, res.sigma, res.iters, res.sweeps, ora)
+        print(solver, mi, rep)
+        assert_parity(rep)
+        assert np.array_equal(res.converged, ora.converged)
