@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--mode", default="per_column", choices=["per_column", "joint"],
                     help="per_column (default; Alg. 1/2 stop) or joint (Algorithm 3, P:938-990)")
+    ap.add_argument("--solver", default="auto", choices=["auto", "residual", "gram"])
     return ap.parse_args()
 
 
@@ -253,7 +254,8 @@ def run_ours(args):
 
     def step():
         if world == 1:
-            r = S.fit_device(Xd, lam, TOL, MAX_ITER, stream=stream, out=outbuf, mode=args.mode)
+            r = S.fit_device(Xd, lam, TOL, MAX_ITER, stream=stream, out=outbuf, mode=args.mode,
+                             solver=args.solver)
             return r.stats, r
         r = D.fit_distributed(Xd, lam, TOL, MAX_ITER, stream=stream)
         return r["stats"], r
@@ -293,22 +295,36 @@ def run_ours(args):
         updates = int(u[0])
     value = updates / (tot_ms / 1000.0)
     upd_per_step = updates / args.steps
-    # roofline of the dominant kernel (CD sweep): 2n flops per coordinate update (§8(d))
+    # roofline of the dominant kernel (DESIGN.md §5/§7)
     peak, peak_src = fp64_peak()
-    # the CD kernel's own updates (the tail solver's sweeps are not DMMA work)
-    cd_updates = (stats_last["total_sweeps"] - stats_last["tail_sweeps"]) * (p - 1)
-    flops_per_step_rank = 2.0 * n * cd_updates
-    achieved = flops_per_step_rank / (float(np.mean(cd_ms)) / 1000.0) / 1e12
     traffic = cd_traffic()
-    roof = {"kernel": "cd_sweep_kernel", "bound": "tensor", "achieved": achieved, "peak": peak,
-            "unit": "TFLOP/s", "frac": achieved / peak,
-            "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
-            "peak_source": peak_src, "dtype": "fp64 (DMMA m8n8k4)",
-            "cd_share_of_step": float(np.mean(cd_ms)) / (tot_ms / args.steps),
-            "algorithmic": "2n flops per coordinate update of the CD kernel "
-                           "(sweeps done in the tail solver excluded)",
-            "tail_solver_ms": stats_last.get("ms_tail", 0.0),
-            "tail_columns": stats_last.get("tail_columns", 0)}
+    step_ms_mean = tot_ms / args.steps
+    if stats_last.get("solver") == 2:
+        # Gram solver: the symmetric Gram kernel; algorithmic work n p (p + 1) flops (each of
+        # the p (p + 1) / 2 distinct entries of X~^T X~ is a length-n dot product)
+        gram_ms = float(stats_last["ms_gram"])
+        achieved = n * p * (p + 1) / (gram_ms / 1000.0) / 1e12
+        roof = {"kernel": "syrk_screen_kernel", "bound": "tensor", "achieved": achieved,
+                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": (traffic or {}).get("syrk_dram_bytes_per_launch"),
+                "peak_source": peak_src, "dtype": "fp64 (DMMA m8n8k4)",
+                "kernel_ms": gram_ms, "kernel_share_of_step": gram_ms / step_ms_mean,
+                "algorithmic": "n p (p+1) flops: the distinct entries of X~^T X~ (symmetric)",
+                "sweep_kernel_ms": stats_last.get("ms_tail", 0.0),
+                "sweep_columns": stats_last.get("tail_columns", 0)}
+    else:
+        # residual solver: the persistent CD kernel; 2n flops per coordinate update (§8(d))
+        cd_updates = (stats_last["total_sweeps"] - stats_last["tail_sweeps"]) * (p - 1)
+        achieved = 2.0 * n * cd_updates / (float(np.mean(cd_ms)) / 1000.0) / 1e12
+        roof = {"kernel": "cd_sweep_kernel", "bound": "tensor", "achieved": achieved, "peak": peak,
+                "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": (traffic or {}).get("dram_bytes_per_launch"),
+                "peak_source": peak_src, "dtype": "fp64 (DMMA m8n8k4)",
+                "kernel_share_of_step": float(np.mean(cd_ms)) / step_ms_mean,
+                "algorithmic": "2n flops per coordinate update of the CD kernel "
+                               "(sweeps done in the tail solver excluded)",
+                "tail_solver_ms": stats_last.get("ms_tail", 0.0),
+                "tail_columns": stats_last.get("tail_columns", 0)}
     # e2e through the host C-ABI entry point (pinned host buffers)
     e2e = None
     if not args.no_e2e:
@@ -320,7 +336,7 @@ def run_ours(args):
             ih = torch.empty(p, dtype=torch.int32).pin_memory()
             import ctypes
             L = S.load()
-            o = S.default_options(mode=S.MODES[args.mode])
+            o = S.default_options(mode=S.MODES[args.mode], solver=S.SOLVERS[args.solver])
 
             def e2e_step():
                 rc = L.spmesl_fit_ex(ctypes.c_void_p(Xh.data_ptr()), n, p, lam, TOL, MAX_ITER,
@@ -381,11 +397,14 @@ def run_ours(args):
                     "sweeps_total": stats_last["total_sweeps"],
                     "max_sweeps": stats_last["max_sweeps"], "max_outer": stats_last["max_outer"],
                     "nnz": stats_last["nnz"], "tile_cols": stats_last["tile_cols"],
-                    "num_ctas": stats_last["num_ctas"], "mode": args.mode}),
+                    "num_ctas": stats_last["num_ctas"], "mode": args.mode,
+                    "solver": {1: "residual", 2: "gram"}.get(stats_last.get("solver"), "?")}),
                 "roofline": roof, "clocks": clk.summary(), "e2e": e2e,
                 "gpu_launches": int(stats_last["kernel_launches"]) * args.steps,
                 "ms_breakdown": {"standardize": stats_last["ms_standardize"],
-                                 "cd": stats_last["ms_cd"], "assemble": stats_last["ms_assemble"]}}
+                                 "solve": stats_last["ms_cd"], "gram": stats_last.get("ms_gram", 0.0),
+                                 "sweeps": stats_last.get("ms_tail", 0.0),
+                                 "assemble": stats_last["ms_assemble"]}}
         if cpu:
             line["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
         print(json.dumps(line), flush=True)
