@@ -91,7 +91,7 @@ class ClockSampler:
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "10"],
                                          stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -107,12 +107,25 @@ class ClockSampler:
                 self.proc.kill()
             self.f.close()
 
+    def mark(self):
+        """Samples before this call (warm-up) are excluded from the summary."""
+        try:
+            self.f.flush()
+            self.skip = sum(1 for _ in open(self.path))
+        except Exception:
+            self.skip = 0
+
     def summary(self):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
+        lines = open(self.path).readlines()
+        skip = getattr(self, "skip", 0)
+        window = "timed steps"
+        if len(lines) - skip < 1:          # timed region shorter than one sample interval
+            skip, window = max(0, skip - 3), "last warm-up samples + timed steps"
+        for line in lines[skip:]:
             f = [x.strip() for x in line.split(",")]
             if len(f) < 9:
                 continue
@@ -128,7 +141,7 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": sorted(reasons)}
         load = [x for x in sm if x > 500] or sm
         return {"sm_mhz": statistics.median(load), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "window": window}
 
 
 # ----------------------------------------------------------------------------- peaks
@@ -260,13 +273,16 @@ def run_ours(args):
         r = D.fit_distributed(Xd, lam, TOL, MAX_ITER, stream=stream)
         return r["stats"], r
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     cd_ms, updates, stats_last = [], 0, None
+    # the clock sampler starts before the warm-up (its first nvidia-smi queries can stall the
+    # GPU briefly) and its summary covers the timed steps
     with ClockSampler(local) as clk:
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        clk.mark()
         for k in range(args.steps):
             flush.fill_(k & 0xff)
             torch.cuda.synchronize()

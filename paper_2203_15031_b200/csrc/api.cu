@@ -50,6 +50,8 @@ struct DevCounters {
   unsigned long long bad_key;   // 2*col + (0 nonfinite | 1 constant)
   int64_t csc_total;
   unsigned long long joint_maxd;   // mode 1: max |db| of the last sweep (double bits)
+  unsigned long long st_sweeps;    // column statistics (column_stats_kernel)
+  int st_max_sweeps, st_max_outer, st_unconv, pad4;
 };
 
 struct Buffer {
@@ -397,6 +399,27 @@ int initial_nzcap(int64_t n, int64_t p) {
   return (int)c;
 }
 
+// Per-column statistics computed on the device into the counters (read with them).
+int device_stats(Workspace& W, const int32_t* dIters, const int32_t* dSweeps, const uint8_t* dConv,
+                 int64_t m, cudaStream_t s) {
+  DevCounters* dc = (DevCounters*)W.counters.ptr;
+  CUDA_TRY(cudaMemsetAsync(&dc->st_sweeps, 0, 24, s));
+  CUDA_TRY(launch_column_stats(dIters, dSweeps, dConv, m, &dc->st_sweeps, &dc->st_max_sweeps,
+                               &dc->st_max_outer, &dc->st_unconv, s));
+  return SPMESL_OK;
+}
+
+void stats_from_counters(const DevCounters& c, int64_t p, spmesl_stats* st, int* any_unconv) {
+  *any_unconv = c.st_unconv > 0;
+  if (st) {
+    st->total_sweeps = (int64_t)c.st_sweeps;
+    st->coord_updates = (int64_t)c.st_sweeps * (p - 1);
+    st->max_sweeps = c.st_max_sweeps;
+    st->max_outer = c.st_max_outer;
+    st->n_unconverged = c.st_unconv;
+  }
+}
+
 // Per-column statistics (host side) from device arrays.
 int collect_stats(const int32_t* dIters, const int32_t* dSweeps, const uint8_t* dConv, int64_t m,
                   int64_t p, cudaStream_t s, spmesl_stats* st, int* any_unconv) {
@@ -541,9 +564,10 @@ bool gram_applicable(const Workspace& W, const spmesl_options& o, int64_t n, int
     if (why) *why = "p too large for the on-chip gradient vector";
     return false;
   }
+  const double need = (double)p * (double)p * 8.0;
+  if ((double)W.ondemand.bytes >= need) return true;   // (no driver query on repeat calls)
   size_t free_b = 0, total_b = 0;
   if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) { cudaGetLastError(); free_b = 0; }
-  const double need = (double)p * (double)p * 8.0;
   const double have = (double)free_b + (double)W.ondemand.bytes;
   if (need > 0.6 * have) { if (why) *why = "8 p^2 bytes do not fit in device memory"; return false; }
   return true;
@@ -551,84 +575,99 @@ bool gram_applicable(const Workspace& W, const spmesl_options& o, int64_t n, int
 
 // Gram solver for [0, p): standardize, S = X~^T X~ / n with fused
 // screening, retire the columns whose first sweep changes nothing, covariance-update sweeps for
-// the rest (tail.cu with z = S[:, c]).  Coefficient lists regrow on overflow.
+// the rest (tail.cu with z = S[:, c]).  Enqueue only (no host synchronisation): the caller reads
+// the counters afterwards and checks err / overflow.
+int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, double lambda0,
+                     double tol, int32_t max_iter, const spmesl_options& o, const FitOut& out,
+                     cudaStream_t s, Layout& L, int nzcap) {
+  const int64_t m = p;
+  set_layout(L, n, p);
+  int rc = alloc_core(W, L, m, nzcap);
+  if (rc) return rc;
+  if (tail_smem_bytes((int)p, L.n_pad, nzcap) > (size_t)W.smem_optin)
+    return fail(SPMESL_ERR_UNSUPPORTED, "Gram solver: sweep state does not fit on chip");
+  if ((rc = ensure(W.ondemand, (size_t)p * p * 8))) return rc;
+  if ((rc = ensure(W.hit, (size_t)p))) return rc;
+  DevCounters* dc = (DevCounters*)W.counters.ptr;
+  if ((rc = run_prep(W, dX, m, o, L, s, /*band=*/false))) return rc;
+  CUDA_TRY(cudaMemsetAsync(W.hit.ptr, 0, (size_t)p, s));
+  GramParams G{};
+  G.Xb = (const double*)W.xb.ptr;
+  G.n = (int)n; G.n_pad = L.n_pad; G.nchunk = L.nchunk; G.p = (int)p; G.nblk = (int)L.nblk;
+  G.col_begin = 0;
+  G.ncols = (int)m;
+  G.lambda0 = lambda0; G.tol = tol; G.sigma_floor = o.sigma_floor; G.sqrt_n = std::sqrt((double)n);
+  G.max_outer = max_iter;
+  G.G = (double*)W.ondemand.ptr;
+  G.hit = (uint8_t*)W.hit.ptr;
+  G.tail = (TailState*)W.tail.ptr;
+  G.tail_count = &dc->tail_count;
+  G.sigma_std = out.sigma_std; G.iters = out.iters; G.sweeps = out.sweeps;
+  G.converged = out.conv;
+  G.nz_count = (int*)W.nz_count.ptr; G.nz_cur = (int*)W.nz_cur.ptr;
+  const int nT = (int)((L.nblk + 3) / 4);
+  const int ntiles = nT * (nT + 1) / 2;
+  CUDA_TRY(launch_syrk_screen(G, std::min(W.sms, ntiles), s));
+  CUDA_TRY(cudaEventRecord(W.ev[7], s));
+  CUDA_TRY(launch_gram_init(G, s));
+  CUDA_TRY(cudaEventRecord(W.ev[5], s));
+  // the sweep kernel reads the number of columns with hits from the device counter (no host
+  // round trip); one CTA per SM, each takes columns from the shared work counter
+  TailParams T{};
+  T.Xb = (const double*)W.xb.ptr;
+  T.n = (int)n; T.n_pad = L.n_pad; T.nchunk = L.nchunk; T.p = (int)p; T.nblk = (int)L.nblk;
+  T.col_begin = 0;
+  T.lambda0 = lambda0; T.tol = tol; T.sigma_floor = o.sigma_floor; T.sqrt_n = std::sqrt((double)n);
+  T.max_outer = max_iter; T.max_inner = o.max_inner;
+  T.nzcap = nzcap;
+  T.M = 0;
+  T.M_dev = &dc->tail_count;
+  T.tail = (const TailState*)W.tail.ptr;
+  T.Zz = nullptr;
+  T.Gtab = (double*)W.ondemand.ptr;
+  T.gstate = nullptr;
+  T.z_from_gtab = 1;
+  T.gtab_full = 1;
+  T.next = &dc->tail_next;
+  T.ondemand_count = &dc->gram_ondemand;
+  T.sweeps_count = &dc->tail_sweeps;
+  T.flags = &dc->err;
+  T.nz_rows = (int*)W.nz_rows.ptr; T.nz_vals = (double*)W.nz_vals.ptr;
+  T.nz_count = (int*)W.nz_count.ptr; T.nz_cur = (int*)W.nz_cur.ptr;
+  T.sigma_std = out.sigma_std; T.iters = out.iters; T.sweeps = out.sweeps; T.converged = out.conv;
+  CUDA_TRY(launch_tail_sweeps(T, (int)std::min<int64_t>(W.sms, p), s));
+  CUDA_TRY(cudaEventRecord(W.ev[6], s));
+  CUDA_TRY(cudaEventRecord(W.ev[2], s));
+  return SPMESL_OK;
+}
+
+void gram_stats(Workspace& W, int64_t p, int nzcap, spmesl_stats* st) {
+  (void)nzcap;
+  if (!st) return;
+  const int nT = (int)((((p + J - 1) / J) + 3) / 4);
+  st->solver = 2;
+  st->tile_cols = 0;
+  st->num_ctas = std::min(W.sms, nT * (nT + 1) / 2);
+  st->kernel_launches += 3;
+  st->ms_gram = ev_ms(W.ev[1], W.ev[7]);
+  st->ms_tail = ev_ms(W.ev[5], W.ev[6]);
+  st->tail_columns = W.host_counters->tail_count;
+  st->tail_sweeps = W.host_counters->tail_sweeps;
+}
+
+// The Gram solver with its own synchronisation and coefficient-list regrowth (for callers that
+// continue on the host).
 int fit_gram_core(Workspace& W, const double* dX, int64_t n, int64_t p, double lambda0, double tol,
                   int32_t max_iter, const spmesl_options& o, const FitOut& out, cudaStream_t s,
                   spmesl_stats* st, Layout& L, int* nzcap_used) {
-  const int64_t m = p;
-  set_layout(L, n, p);
   int nzcap = initial_nzcap(n, p);
   for (int attempt = 0; attempt < 4; ++attempt) {
-    int rc = alloc_core(W, L, m, nzcap);
+    int rc = fit_gram_enqueue(W, dX, n, p, lambda0, tol, max_iter, o, out, s, L, nzcap);
     if (rc) return rc;
-    if (tail_smem_bytes((int)p, L.n_pad, nzcap) > (size_t)W.smem_optin)
-      return fail(SPMESL_ERR_UNSUPPORTED, "Gram solver: sweep state does not fit on chip");
-    if ((rc = ensure(W.ondemand, (size_t)p * p * 8))) return rc;
-    if ((rc = ensure(W.hit, (size_t)p))) return rc;
-    DevCounters* dc = (DevCounters*)W.counters.ptr;
-    if ((rc = run_prep(W, dX, m, o, L, s, /*band=*/false))) return rc;
-    CUDA_TRY(cudaMemsetAsync(W.hit.ptr, 0, (size_t)p, s));
-    GramParams G{};
-    G.Xb = (const double*)W.xb.ptr;
-    G.n = (int)n; G.n_pad = L.n_pad; G.nchunk = L.nchunk; G.p = (int)p; G.nblk = (int)L.nblk;
-    G.col_begin = 0;
-    G.ncols = (int)m;
-    G.lambda0 = lambda0; G.tol = tol; G.sigma_floor = o.sigma_floor; G.sqrt_n = std::sqrt((double)n);
-    G.max_outer = max_iter;
-    G.G = (double*)W.ondemand.ptr;
-    G.hit = (uint8_t*)W.hit.ptr;
-    G.tail = (TailState*)W.tail.ptr;
-    G.tail_count = &dc->tail_count;
-    G.sigma_std = out.sigma_std; G.iters = out.iters; G.sweeps = out.sweeps;
-    G.converged = out.conv;
-    G.nz_count = (int*)W.nz_count.ptr; G.nz_cur = (int*)W.nz_cur.ptr;
-    const int nT = (int)((L.nblk + 3) / 4);
-    const int ntiles = nT * (nT + 1) / 2;
-    CUDA_TRY(launch_syrk_screen(G, std::min(W.sms, ntiles), s));
-    CUDA_TRY(cudaEventRecord(W.ev[7], s));
-    CUDA_TRY(launch_gram_init(G, s));
     if ((rc = read_counters(W, s))) return rc;
     if (W.host_counters->err) return std_error(W, st);
-    const int M = W.host_counters->tail_count;
-    CUDA_TRY(cudaEventRecord(W.ev[5], s));
-    if (M > 0) {
-      TailParams T{};
-      T.Xb = (const double*)W.xb.ptr;
-      T.n = (int)n; T.n_pad = L.n_pad; T.nchunk = L.nchunk; T.p = (int)p; T.nblk = (int)L.nblk;
-      T.col_begin = 0;
-      T.lambda0 = lambda0; T.tol = tol; T.sigma_floor = o.sigma_floor; T.sqrt_n = std::sqrt((double)n);
-      T.max_outer = max_iter; T.max_inner = o.max_inner;
-      T.nzcap = nzcap;
-      T.M = M;
-      T.tail = (const TailState*)W.tail.ptr;
-      T.Zz = nullptr;
-      T.Gtab = (double*)W.ondemand.ptr;
-      T.gstate = nullptr;
-      T.z_from_gtab = 1;
-      T.gtab_full = 1;
-      T.next = &dc->tail_next;
-      T.ondemand_count = &dc->gram_ondemand;
-      T.sweeps_count = &dc->tail_sweeps;
-      T.flags = &dc->err;
-      T.nz_rows = (int*)W.nz_rows.ptr; T.nz_vals = (double*)W.nz_vals.ptr;
-      T.nz_count = (int*)W.nz_count.ptr; T.nz_cur = (int*)W.nz_cur.ptr;
-      T.sigma_std = out.sigma_std; T.iters = out.iters; T.sweeps = out.sweeps; T.converged = out.conv;
-      CUDA_TRY(launch_tail_sweeps(T, std::min(M, W.sms), s));
-    }
-    CUDA_TRY(cudaEventRecord(W.ev[6], s));
-    CUDA_TRY(cudaEventRecord(W.ev[2], s));
-    if ((rc = read_counters(W, s))) return rc;
     if (!W.host_counters->overflow) {
-      if (st) {
-        st->solver = 2;
-        st->tile_cols = 0;
-        st->num_ctas = std::min(W.sms, ntiles);
-        st->kernel_launches += 2 + (M > 0 ? 1 : 0);
-        st->ms_gram = ev_ms(W.ev[1], W.ev[7]);
-        st->ms_tail = ev_ms(W.ev[5], W.ev[6]);
-        st->tail_columns = M;
-        st->tail_sweeps = W.host_counters->tail_sweeps;
-      }
+      gram_stats(W, p, nzcap, st);
       *nzcap_used = nzcap;
       return SPMESL_OK;
     }
@@ -699,38 +738,63 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
   FitOut out{0, p, (double*)W.sigma_std.ptr, dIters, dSweeps, dConv};
   Layout L;
   int nzcap = 0;
-  // zero-fill Theta (8 p^2 bytes, the only dense pass) on a side stream while the CD kernel runs
+  std::string why;
+  const bool gram_ok = gram_applicable(W, o, n, p, 0, p, &why);
+  if (o.solver == 2 && !gram_ok) return fail(SPMESL_ERR_UNSUPPORTED, "solver = 2: " + why);
+  const bool gram = gram_ok && o.solver != 1 && o.mode == 0;
+  // zero-fill Theta (8 p^2 bytes, the only dense pass) on a side stream while the solver runs
   CUDA_TRY(cudaEventRecord(W.ev_fork, s));
   CUDA_TRY(cudaStreamWaitEvent(W.side, W.ev_fork, 0));
   CUDA_TRY(cudaMemsetAsync(dTheta, 0, sizeof(double) * (size_t)p * (size_t)p, W.side));
   CUDA_TRY(cudaEventRecord(W.ev_join, W.side));
-  rc = fit_columns_core(W, dX, n, p, 0, p, lambda0, tol, max_iter, o, out, s, st, L, &nzcap);
-  if (rc) { cudaStreamWaitEvent(s, W.ev_join, 0); return rc; }
-  CUDA_TRY(cudaStreamWaitEvent(s, W.ev_join, 0));
-  const size_t cap = (size_t)p * (size_t)nzcap;
-  if ((rc = ensure(W.csc_rows, cap * 4))) return rc;
-  if ((rc = ensure(W.csc_vals, cap * 8))) return rc;
-  DevCounters* dc = (DevCounters*)W.counters.ptr;
-  CUDA_TRY(cudaEventRecord(W.ev[3], s));
-  CUDA_TRY(launch_csc_build((const int*)W.nz_count.ptr, (const int*)W.nz_cur.ptr,
-                            (const int*)W.nz_rows.ptr, (const double*)W.nz_vals.ptr, (int)p, nzcap,
-                            (int64_t*)W.col_ptr.ptr, (int32_t*)W.csc_rows.ptr,
-                            (double*)W.csc_vals.ptr, &dc->csc_total, s));
-  CUDA_TRY(launch_assemble(p, 0, p, (const int64_t*)W.col_ptr.ptr, (const int32_t*)W.csc_rows.ptr,
-                           (const double*)W.csc_vals.ptr, (const double*)W.sigma_std.ptr,
-                           o.standardize ? (const double*)W.scale.ptr : nullptr, o.symmetrize,
-                           dTheta, dSigma, s, /*zero_fill=*/false));
-  CUDA_TRY(cudaEventRecord(W.ev[4], s));
-  if ((rc = read_counters(W, s))) return rc;
+  DevCounters* dc = nullptr;
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    if (gram) {
+      // everything is enqueued; the one host synchronisation is the counter read at the end
+      if (!nzcap) nzcap = initial_nzcap(n, p);
+      rc = fit_gram_enqueue(W, dX, n, p, lambda0, tol, max_iter, o, out, s, L, nzcap);
+    } else {
+      rc = fit_columns_core(W, dX, n, p, 0, p, lambda0, tol, max_iter, o, out, s, st, L, &nzcap);
+    }
+    if (rc) { cudaStreamWaitEvent(s, W.ev_join, 0); return rc; }
+    CUDA_TRY(cudaStreamWaitEvent(s, W.ev_join, 0));
+    const size_t cap = (size_t)p * (size_t)nzcap;
+    if ((rc = ensure(W.csc_rows, cap * 4))) return rc;
+    if ((rc = ensure(W.csc_vals, cap * 8))) return rc;
+    dc = (DevCounters*)W.counters.ptr;
+    CUDA_TRY(cudaEventRecord(W.ev[3], s));
+    CUDA_TRY(launch_csc_build((const int*)W.nz_count.ptr, (const int*)W.nz_cur.ptr,
+                              (const int*)W.nz_rows.ptr, (const double*)W.nz_vals.ptr, (int)p,
+                              nzcap, (int64_t*)W.col_ptr.ptr, (int32_t*)W.csc_rows.ptr,
+                              (double*)W.csc_vals.ptr, &dc->csc_total, s));
+    CUDA_TRY(launch_assemble(p, 0, p, (const int64_t*)W.col_ptr.ptr,
+                             (const int32_t*)W.csc_rows.ptr, (const double*)W.csc_vals.ptr,
+                             (const double*)W.sigma_std.ptr,
+                             o.standardize ? (const double*)W.scale.ptr : nullptr, o.symmetrize,
+                             dTheta, dSigma, s, /*zero_fill=*/false));
+    CUDA_TRY(cudaEventRecord(W.ev[4], s));
+    if ((rc = device_stats(W, dIters, dSweeps, dConv, p, s))) return rc;
+    if ((rc = read_counters(W, s))) return rc;
+    if (!gram) break;
+    if (W.host_counters->err) return std_error(W, st);
+    if (!W.host_counters->overflow) { gram_stats(W, p, nzcap, st); break; }
+    if (nzcap >= p) return fail(SPMESL_ERR_OOM, "coefficient list overflow");
+    nzcap = (int)std::min<int64_t>(p, (int64_t)nzcap * 4);
+    // (Theta's zero fill is redone: the assembly above wrote into it)
+    CUDA_TRY(cudaEventRecord(W.ev_fork, s));
+    CUDA_TRY(cudaStreamWaitEvent(W.side, W.ev_fork, 0));
+    CUDA_TRY(cudaMemsetAsync(dTheta, 0, sizeof(double) * (size_t)p * (size_t)p, W.side));
+    CUDA_TRY(cudaEventRecord(W.ev_join, W.side));
+  }
   int any_unconv = 0;
-  if ((rc = collect_stats(dIters, dSweeps, dConv, p, p, s, st, &any_unconv))) return rc;
+  stats_from_counters(*W.host_counters, p, st, &any_unconv);
   if (st) {
     st->nnz = W.host_counters->csc_total;
     st->ms_standardize = ev_ms(W.ev[0], W.ev[1]);
     st->ms_cd = ev_ms(W.ev[1], W.ev[2]);
     st->ms_assemble = ev_ms(W.ev[3], W.ev[4]);
     st->ms_total = ev_ms(W.ev[0], W.ev[4]);
-    st->kernel_launches += 7;  // standardize, gram, cd, csc_scan, csc_copy, assemble x2 (+ memsets)
+    st->kernel_launches += 5;  // standardize, csc_scan, csc_copy, assemble x2 (+ solver kernels)
     st->bad_column = -1;
   }
   return any_unconv ? SPMESL_WARN_NOT_CONVERGED : SPMESL_OK;
@@ -932,9 +996,11 @@ int spmesl_fit_ex(const double* X, int64_t n, int64_t p, double lambda0, double 
     if (e != cudaSuccess) return bail(fail(SPMESL_ERR_CUDA, cudaGetErrorString(e)));
   }
   int any_unconv = 0;
-  if ((rc = collect_stats((const int32_t*)W->hiters.ptr, (const int32_t*)W->hsweeps.ptr,
-                          (const uint8_t*)W->hconv.ptr, p, p, s, st, &any_unconv)))
+  if ((rc = device_stats(*W, (const int32_t*)W->hiters.ptr, (const int32_t*)W->hsweeps.ptr,
+                         (const uint8_t*)W->hconv.ptr, p, s)))
     return bail(rc);
+  if ((rc = read_counters(*W, s))) return bail(rc);
+  stats_from_counters(*W->host_counters, p, st, &any_unconv);
   join();
   for (int e = 0; e < ncoo; ++e) Theta[(size_t)cc[e] * p + cr[e]] = cv[e];
   for (int64_t k = 0; k < p; ++k) Theta[(size_t)k * p + k] = diag[k];

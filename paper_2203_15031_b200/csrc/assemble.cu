@@ -1,3 +1,4 @@
+#include <algorithm>
 // Coefficient export (CSC) and Theta assembly + symmetrization (steps a8-a10).
 //
 // csc_*      — each fitted column's final coefficient list (rows ascending, nonzeros only)
@@ -232,6 +233,43 @@ cudaError_t launch_assemble(int64_t p, int64_t col_begin, int64_t col_end, const
   assemble_diag_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(p, col_begin, col_end,
                                                                    sigma_std, scale, rescale,
                                                                    Theta, sigma_out);
+  return cudaGetLastError();
+}
+
+// Per-column statistics on the device (no host copy of iters/sweeps/converged):
+// out[0] += sum sweeps (64-bit), out[2] = max sweeps, out[3] = max iters, out[4] += unconverged.
+__global__ void column_stats_kernel(const int32_t* __restrict__ iters, const int32_t* __restrict__ sweeps,
+                                    const uint8_t* __restrict__ conv, int64_t m,
+                                    unsigned long long* tot, int* mx_sweeps, int* mx_outer, int* nunc) {
+  unsigned long long t = 0;
+  int ms = 0, mo = 0, nu = 0;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    t += (unsigned long long)sweeps[k];
+    ms = max(ms, sweeps[k]);
+    mo = max(mo, iters[k]);
+    nu += conv[k] ? 0 : 1;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    t += __shfl_xor_sync(0xffffffffu, t, o);
+    ms = max(ms, __shfl_xor_sync(0xffffffffu, ms, o));
+    mo = max(mo, __shfl_xor_sync(0xffffffffu, mo, o));
+    nu += __shfl_xor_sync(0xffffffffu, nu, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (t) atomicAdd(tot, t);
+    atomicMax(mx_sweeps, ms);
+    atomicMax(mx_outer, mo);
+    if (nu) atomicAdd(nunc, nu);
+  }
+}
+
+cudaError_t launch_column_stats(const int32_t* iters, const int32_t* sweeps, const uint8_t* conv,
+                                int64_t m, unsigned long long* tot, int* mx_sweeps, int* mx_outer,
+                                int* nunc, cudaStream_t s) {
+  if (m <= 0) return cudaSuccess;
+  const int blocks = (int)std::min<int64_t>(64, (m + 255) / 256);
+  column_stats_kernel<<<blocks, 256, 0, s>>>(iters, sweeps, conv, m, tot, mx_sweeps, mx_outer, nunc);
   return cudaGetLastError();
 }
 

@@ -107,7 +107,8 @@ struct TailParams {
   double lambda0, tol, sigma_floor, sqrt_n;
   int max_outer, max_inner;
   int nzcap;
-  int M;                   // tail columns
+  int M;                   // tail columns (or, if M_dev != nullptr, *M_dev at kernel start)
+  const int* M_dev;
   const TailState* tail;   // [M]
   const double* Zz;        // [M][p]: z_k = X~^T r_k / n for tail column k
   double* Gtab;            // [p][p]: Gram column G[:, j] = X~^T x~_j / n of variable j
@@ -191,6 +192,9 @@ cudaError_t launch_assemble_coo(int64_t p, const int64_t* col_ptr, const int32_t
                                 const double* vals, const double* sigma_std, const double* scale,
                                 int symmetrize, int32_t* coo_row, int32_t* coo_col, double* coo_val,
                                 int* coo_count, double* diag, double* sigma_out, cudaStream_t s);
+cudaError_t launch_column_stats(const int32_t* iters, const int32_t* sweeps, const uint8_t* conv,
+                                int64_t m, unsigned long long* tot, int* mx_sweeps, int* mx_outer,
+                                int* nunc, cudaStream_t s);
 cudaError_t launch_csc_counts(const int* nz_count, int ncols, int32_t* out, cudaStream_t s);
 cudaError_t launch_assemble(int64_t p, int64_t col_begin, int64_t col_end, const int64_t* col_ptr,
                             const int32_t* rows, const double* vals, const double* sigma_std,

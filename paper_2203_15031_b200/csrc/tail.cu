@@ -171,6 +171,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) tail_sweep_kernel(const TailP
   TailShared& TS = *(TailShared*)(sm + ts_off);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const size_t list_stride = (size_t)2 * nzcap;
+  const int M = P.M_dev ? *(volatile const int*)P.M_dev : P.M;
   if (tid < TAIL_ODC) TS.oc_var[tid] = -1;
   if (tid == 0) TS.oc_next = 0;
 
@@ -179,7 +180,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) tail_sweep_kernel(const TailP
     if (tid == 0) TS.k = atomicAdd(P.next, 1);
     __syncthreads();
     const int k = TS.k;
-    if (k >= P.M) break;
+    if (k >= M) break;
     const TailState ts = P.tail[k];
     const int col = ts.col;
     const int gc = (int)(P.col_begin + col);
