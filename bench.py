@@ -319,7 +319,12 @@ def run_ours(args):
         # Gram solver: the symmetric Gram kernel; algorithmic work n p (p + 1) flops (each of
         # the p (p + 1) / 2 distinct entries of X~^T X~ is a length-n dot product)
         gram_ms = float(stats_last["ms_gram"])
-        achieved = n * p * (p + 1) / (gram_ms / 1000.0) / 1e12
+        share = 1.0
+        if world > 1:      # this rank screened tiles [t0, t1) of the triangle
+            nt = S.gram_tile_count(p)
+            t0, t1 = D.tile_range(nt, rank, world)
+            share = (t1 - t0) / nt
+        achieved = n * p * (p + 1) * share / (gram_ms / 1000.0) / 1e12
         roof = {"kernel": "syrk_screen_kernel", "bound": "tensor", "achieved": achieved,
                 "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "traffic": (traffic or {}).get("syrk_dram_bytes_per_launch"),

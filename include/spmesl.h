@@ -163,6 +163,37 @@ int spmesl_fit_columns_device(const double* dX, int64_t n, int64_t p, int64_t co
                               double* dScale, int32_t* dIters, int32_t* dSweeps,
                               uint8_t* dConverged, void* cuda_stream, spmesl_stats* st);
 
+/*
+ * Multi-GPU building blocks of the Gram solver (SURVEY.md §8(f) f2 + §8(e)).
+ * The first sweep of column c with b_c = 0 changes coefficient j iff |x~_j^T x~_c / n| > lambda0
+ * (sigma^(0) = 1); "screening" evaluates that test for all pairs (j, c) from the
+ * tiles of the symmetric S = X~^T X~ / n.
+ *
+ * spmesl_gram_tile_count: number of 128 x 128 upper-triangle tiles of S (-1 if p is invalid);
+ *   ranks split [0, count) into contiguous shares.
+ * spmesl_gram_screen_device: standardize dX (n x p, column-major, device) and evaluate tiles
+ *   [tile_begin, tile_end): dHit[c] = 1 (never cleared; the caller zero-fills dHit[p] once) for
+ *   every column c with some |S_jc| > lambda0, j != c, in those tiles.  The OR (max) of dHit
+ *   over all ranks is the global screening result.  Blocking; errors as spmesl_fit.
+ * spmesl_fit_columns_gram_device: as spmesl_fit_columns_device, for the Gram solver, given the
+ *   global dHit[p]: columns without a hit finish after one sweep; the others run covariance-
+ *   update sweeps.  mode must be 0.  Same outputs and iterates as the single-device Gram solver
+ *   up to rounding.  Blocking.
+ */
+int64_t spmesl_gram_tile_count(int64_t p);
+/* 1 if the Gram solver's sweep state fits on chip for (n, p) on the current device, else 0. */
+int spmesl_gram_supported(int64_t n, int64_t p);
+int spmesl_gram_screen_device(const double* dX, int64_t n, int64_t p, double lambda0,
+                              int64_t tile_begin, int64_t tile_end, const spmesl_options* opt,
+                              uint8_t* dHit, void* cuda_stream, spmesl_stats* st);
+int spmesl_fit_columns_gram_device(const double* dX, int64_t n, int64_t p, int64_t col_begin,
+                                   int64_t col_end, double lambda0, double tol, int32_t max_iter,
+                                   const spmesl_options* opt, const uint8_t* dHit,
+                                   int32_t* dColCount, int32_t* dRows, double* dVals, int64_t cap,
+                                   int64_t* nnz_out, double* dSigmaStd, double* dScale,
+                                   int32_t* dIters, int32_t* dSweeps, uint8_t* dConverged,
+                                   void* cuda_stream, spmesl_stats* st);
+
 int spmesl_assemble_device(int64_t p, int64_t col_begin, int64_t col_end, const int64_t* dColPtr,
                            const int32_t* dRows, const double* dVals, const double* dSigmaStd,
                            const double* dScale, const spmesl_options* opt, double* dTheta,

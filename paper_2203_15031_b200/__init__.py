@@ -21,7 +21,8 @@ import numpy as np
 from . import _lib
 from ._lib import SpmeslError, Stats, default_options, load  # noqa: F401
 
-__all__ = ["fit", "fit_device", "fit_columns_device", "assemble_device", "lambda_univ",
+__all__ = ["fit", "fit_device", "fit_columns_device", "assemble_device", "gram_tile_count",
+           "gram_screen_device", "fit_columns_gram_device", "gram_supported", "lambda_univ",
            "lambda_ub", "lambda_pb", "solve_k", "FitResult", "SpmeslError", "load",
            "release_workspace", "version"]
 
@@ -117,6 +118,79 @@ def fit_device(X, lambda0: float, tol: float = 1e-4, max_iter: int = 100, *, str
     # the buffer holds Theta column-major: element (j, k) at j + k p -> view as its transpose
     return FitResult(rc, out["theta"].t(), out["sigma"], out["iters"], out["sweeps"],
                      out["conv"].bool(), st.asdict())
+
+
+def gram_supported(n: int, p: int) -> bool:
+    """spmesl_gram_supported: the Gram solver's sweep state fits on chip for (n, p)."""
+    return bool(load().spmesl_gram_supported(int(n), int(p)))
+
+
+def gram_tile_count(p: int) -> int:
+    """spmesl_gram_tile_count: upper-triangle tiles of S = X~^T X~ / n."""
+    return int(load().spmesl_gram_tile_count(int(p)))
+
+
+def gram_screen_device(X, lambda0: float, tile_begin: int, tile_end: int, hit, *, stream=None,
+                       **options) -> dict:
+    """spmesl_gram_screen_device: OR the screening hits of tiles [tile_begin, tile_end) into
+    `hit` (uint8 CUDA tensor [p], zero-filled by the caller)."""
+    import torch
+    X = as_colmajor(X)
+    n, p = X.shape
+    if hit.dtype != torch.uint8 or hit.numel() != p or not hit.is_cuda:
+        raise TypeError("hit must be a uint8 CUDA tensor of length p")
+    s = stream if stream is not None else torch.cuda.current_stream(X.device)
+    st = Stats()
+    o = _opts(**options)
+    with torch.cuda.device(X.device):
+        rc = load().spmesl_gram_screen_device(_vp(X), n, p, float(lambda0), int(tile_begin),
+                                              int(tile_end), ctypes.byref(o), _vp(hit),
+                                              ctypes.c_void_p(s.cuda_stream), ctypes.byref(st))
+    _lib.check(rc, st)
+    return st.asdict()
+
+
+def _columns_outputs(X, m, p, cap):
+    import torch
+    dev = X.device
+    n = X.shape[0]
+    if cap is None:
+        cap = m * min(p, ((n + 31) // 32) * 32 + 64)
+    return dict(counts=torch.empty(m, dtype=torch.int32, device=dev),
+                rows=torch.empty(max(cap, 1), dtype=torch.int32, device=dev),
+                vals=torch.empty(max(cap, 1), dtype=torch.float64, device=dev),
+                sigma_std=torch.empty(m, dtype=torch.float64, device=dev),
+                scale=torch.empty(p, dtype=torch.float64, device=dev),
+                iters=torch.empty(m, dtype=torch.int32, device=dev),
+                sweeps=torch.empty(m, dtype=torch.int32, device=dev),
+                conv=torch.empty(m, dtype=torch.uint8, device=dev)), cap
+
+
+def fit_columns_gram_device(X, col_begin: int, col_end: int, lambda0: float, hit,
+                            tol: float = 1e-4, max_iter: int = 100, *, stream=None, cap=None,
+                            **options):
+    """spmesl_fit_columns_gram_device: Gram-solver CSC coefficients of columns
+    [col_begin, col_end) given the global screening flags `hit` (uint8 CUDA tensor [p])."""
+    import torch
+    X = as_colmajor(X)
+    n, p = X.shape
+    m = col_end - col_begin
+    b, cap = _columns_outputs(X, m, p, cap)
+    nnz = ctypes.c_int64(0)
+    s = stream if stream is not None else torch.cuda.current_stream(X.device)
+    st = Stats()
+    o = _opts(**options)
+    with torch.cuda.device(X.device):
+        rc = load().spmesl_fit_columns_gram_device(
+            _vp(X), n, p, col_begin, col_end, float(lambda0), float(tol), int(max_iter),
+            ctypes.byref(o), _vp(hit), _vp(b["counts"]), _vp(b["rows"]), _vp(b["vals"]), cap,
+            ctypes.byref(nnz), _vp(b["sigma_std"]), _vp(b["scale"]), _vp(b["iters"]),
+            _vp(b["sweeps"]), _vp(b["conv"]), ctypes.c_void_p(s.cuda_stream), ctypes.byref(st))
+    _lib.check(rc, st)
+    k = nnz.value
+    return dict(code=rc, counts=b["counts"], rows=b["rows"][:k], vals=b["vals"][:k],
+                sigma_std=b["sigma_std"], scale=b["scale"], iters=b["iters"],
+                sweeps=b["sweeps"], converged=b["conv"].bool(), stats=st.asdict())
 
 
 def fit_columns_device(X, col_begin: int, col_end: int, lambda0: float, tol: float = 1e-4,

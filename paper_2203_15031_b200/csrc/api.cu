@@ -600,6 +600,8 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   G.max_outer = max_iter;
   G.G = (double*)W.ondemand.ptr;
   G.hit = (uint8_t*)W.hit.ptr;
+  G.tile_begin = 0;
+  G.tile_end = gram_tile_count(p);
   G.tail = (TailState*)W.tail.ptr;
   G.tail_count = &dc->tail_count;
   G.sigma_std = out.sigma_std; G.iters = out.iters; G.sweeps = out.sweeps;
@@ -798,6 +800,142 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
     st->bad_column = -1;
   }
   return any_unconv ? SPMESL_WARN_NOT_CONVERGED : SPMESL_OK;
+}
+
+// CSC export of the fitted columns into the caller's device arrays (columns API).
+int export_columns(Workspace& W, int64_t m, int64_t p, int nzcap, int32_t* dColCount,
+                   int32_t* dRows, double* dVals, int64_t cap, int64_t* nnz_out, double* dScale,
+                   const int32_t* dIters, const int32_t* dSweeps, const uint8_t* dConverged,
+                   cudaStream_t s, spmesl_stats* st) {
+  int rc;
+  DevCounters* dc = (DevCounters*)W.counters.ptr;
+  // scan only to learn the total, then copy straight into the caller's arrays
+  const size_t need_cap = (size_t)m * (size_t)nzcap;
+  if ((rc = ensure(W.csc_rows, need_cap * 4))) return rc;
+  if ((rc = ensure(W.csc_vals, need_cap * 8))) return rc;
+  dc = (DevCounters*)W.counters.ptr;
+  CUDA_TRY(launch_csc_build((const int*)W.nz_count.ptr, (const int*)W.nz_cur.ptr,
+                            (const int*)W.nz_rows.ptr, (const double*)W.nz_vals.ptr, (int)m, nzcap,
+                            (int64_t*)W.col_ptr.ptr, (int32_t*)W.csc_rows.ptr,
+                            (double*)W.csc_vals.ptr, &dc->csc_total, s));
+  CUDA_TRY(launch_csc_counts((const int*)W.nz_count.ptr, (int)m, dColCount, s));
+  CUDA_TRY(cudaMemcpyAsync(dScale, W.scale.ptr, (size_t)p * 8, cudaMemcpyDeviceToDevice, s));
+  if ((rc = device_stats(W, dIters, dSweeps, dConverged, m, s))) return rc;
+  if ((rc = read_counters(W, s))) return rc;
+  const int64_t total = W.host_counters->csc_total;
+  *nnz_out = total;
+  if (total > cap) return fail(SPMESL_ERR_ARG, "CSC capacity too small: need " + std::to_string(total));
+  if (total > 0) {
+    CUDA_TRY(cudaMemcpyAsync(dRows, W.csc_rows.ptr, (size_t)total * 4, cudaMemcpyDeviceToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(dVals, W.csc_vals.ptr, (size_t)total * 8, cudaMemcpyDeviceToDevice, s));
+  }
+  int any_unconv = 0;
+  stats_from_counters(*W.host_counters, p, st, &any_unconv);
+  if (st) {
+    st->nnz = total;
+    st->ms_standardize = ev_ms(W.ev[0], W.ev[1]);
+    st->ms_cd = ev_ms(W.ev[1], W.ev[2]);
+    st->kernel_launches += 6;
+  }
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return any_unconv ? SPMESL_WARN_NOT_CONVERGED : SPMESL_OK;
+}
+
+// Multi-GPU Gram solver, part 2: columns [cb, ce) given the global screening flags.  Gram
+// columns of the hit columns of the range come from one batched DMMA pass; any other column a
+// sweep needs is computed on first use.
+int fit_gram_columns_core(Workspace& W, const double* dX, int64_t n, int64_t p, int64_t cb,
+                          int64_t ce, double lambda0, double tol, int32_t max_iter,
+                          const spmesl_options& o, const uint8_t* dHit, const FitOut& out,
+                          cudaStream_t s, spmesl_stats* st, Layout& L, int* nzcap_used) {
+  const int64_t m = ce - cb;
+  set_layout(L, n, p);
+  int nzcap = initial_nzcap(n, p);
+  std::vector<uint8_t> hh(m);
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    int rc = alloc_core(W, L, m, nzcap);
+    if (rc) return rc;
+    if (tail_smem_bytes((int)p, L.n_pad, nzcap) > (size_t)W.smem_optin)
+      return fail(SPMESL_ERR_UNSUPPORTED, "Gram solver: sweep state does not fit on chip");
+    if ((rc = ensure(W.ondemand, (size_t)p * p * 8))) return rc;
+    if ((rc = ensure(W.umap, (size_t)p * 4))) return rc;             // gstate
+    if ((rc = ensure(W.uvars, (size_t)std::max<int64_t>(m, 1) * 4))) return rc;
+    DevCounters* dc = (DevCounters*)W.counters.ptr;
+    if ((rc = run_prep(W, dX, m, o, L, s, /*band=*/false))) return rc;
+    CUDA_TRY(cudaMemcpyAsync(hh.data(), dHit + cb, (size_t)m, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    std::vector<int> U;
+    for (int64_t c = 0; c < m; ++c)
+      if (hh[c]) U.push_back((int)(cb + c));
+    const int nU = (int)U.size();
+    std::vector<int> gstate(p, 0);
+    for (int j : U) gstate[j] = 2;
+    CUDA_TRY(cudaMemcpyAsync(W.umap.ptr, gstate.data(), (size_t)p * 4, cudaMemcpyHostToDevice, s));
+    if (nU) CUDA_TRY(cudaMemcpyAsync(W.uvars.ptr, U.data(), (size_t)nU * 4, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(launch_gram_pass((const double*)W.xb.ptr, (int)L.nblk, L.nchunk, (int)n, (int)p,
+                              nullptr, 0, (const int*)W.uvars.ptr, nU, nullptr,
+                              (double*)W.ondemand.ptr, s));
+    CUDA_TRY(cudaEventRecord(W.ev[7], s));
+    GramParams G{};
+    G.Xb = (const double*)W.xb.ptr;
+    G.n = (int)n; G.n_pad = L.n_pad; G.nchunk = L.nchunk; G.p = (int)p; G.nblk = (int)L.nblk;
+    G.col_begin = cb;
+    G.ncols = (int)m;
+    G.lambda0 = lambda0; G.tol = tol; G.sigma_floor = o.sigma_floor; G.sqrt_n = std::sqrt((double)n);
+    G.max_outer = max_iter;
+    G.G = nullptr;
+    G.hit = const_cast<uint8_t*>(dHit);
+    G.tail = (TailState*)W.tail.ptr;
+    G.tail_count = &dc->tail_count;
+    G.sigma_std = out.sigma_std; G.iters = out.iters; G.sweeps = out.sweeps;
+    G.converged = out.conv;
+    G.nz_count = (int*)W.nz_count.ptr; G.nz_cur = (int*)W.nz_cur.ptr;
+    CUDA_TRY(launch_gram_init(G, s));
+    CUDA_TRY(cudaEventRecord(W.ev[5], s));
+    TailParams T{};
+    T.Xb = (const double*)W.xb.ptr;
+    T.n = (int)n; T.n_pad = L.n_pad; T.nchunk = L.nchunk; T.p = (int)p; T.nblk = (int)L.nblk;
+    T.col_begin = cb;
+    T.lambda0 = lambda0; T.tol = tol; T.sigma_floor = o.sigma_floor; T.sqrt_n = std::sqrt((double)n);
+    T.max_outer = max_iter; T.max_inner = o.max_inner;
+    T.nzcap = nzcap;
+    T.M = 0;
+    T.M_dev = &dc->tail_count;
+    T.tail = (const TailState*)W.tail.ptr;
+    T.Zz = nullptr;
+    T.Gtab = (double*)W.ondemand.ptr;
+    T.gstate = (int*)W.umap.ptr;
+    T.z_from_gtab = 1;
+    T.gtab_full = 0;
+    T.next = &dc->tail_next;
+    T.ondemand_count = &dc->gram_ondemand;
+    T.sweeps_count = &dc->tail_sweeps;
+    T.flags = &dc->err;
+    T.nz_rows = (int*)W.nz_rows.ptr; T.nz_vals = (double*)W.nz_vals.ptr;
+    T.nz_count = (int*)W.nz_count.ptr; T.nz_cur = (int*)W.nz_cur.ptr;
+    T.sigma_std = out.sigma_std; T.iters = out.iters; T.sweeps = out.sweeps; T.converged = out.conv;
+    CUDA_TRY(launch_tail_sweeps(T, (int)std::min<int64_t>(W.sms, m), s));
+    CUDA_TRY(cudaEventRecord(W.ev[6], s));
+    CUDA_TRY(cudaEventRecord(W.ev[2], s));
+    if ((rc = read_counters(W, s))) return rc;
+    if (W.host_counters->err) return std_error(W, st);
+    if (!W.host_counters->overflow) {
+      if (st) {
+        st->solver = 2;
+        st->kernel_launches += 4;
+        st->ms_gram = ev_ms(W.ev[1], W.ev[7]);
+        st->ms_tail = ev_ms(W.ev[5], W.ev[6]);
+        st->tail_columns = W.host_counters->tail_count;
+        st->tail_sweeps = W.host_counters->tail_sweeps;
+        st->tail_gram_ondemand = W.host_counters->gram_ondemand;
+      }
+      *nzcap_used = nzcap;
+      return SPMESL_OK;
+    }
+    if (nzcap >= p) break;
+    nzcap = (int)std::min<int64_t>(p, (int64_t)nzcap * 4);
+  }
+  return fail(SPMESL_ERR_OOM, "coefficient list overflow");
 }
 
 void init_stats(spmesl_stats* st) {
@@ -1055,34 +1193,106 @@ int spmesl_fit_columns_device(const double* dX, int64_t n, int64_t p, int64_t co
   rc = fit_columns_core(*W, dX, n, p, col_begin, col_end, lambda0, tol, max_iter, o, out, s, st, L,
                         &nzcap);
   if (rc) return rc;
-  DevCounters* dc = (DevCounters*)W->counters.ptr;
-  // scan only to learn the total, then copy straight into the caller's arrays
-  const size_t need_cap = (size_t)m * (size_t)nzcap;
-  if ((rc = ensure(W->csc_rows, need_cap * 4))) return rc;
-  if ((rc = ensure(W->csc_vals, need_cap * 8))) return rc;
-  CUDA_TRY(launch_csc_build((const int*)W->nz_count.ptr, (const int*)W->nz_cur.ptr,
-                            (const int*)W->nz_rows.ptr, (const double*)W->nz_vals.ptr, (int)m, nzcap,
-                            (int64_t*)W->col_ptr.ptr, (int32_t*)W->csc_rows.ptr,
-                            (double*)W->csc_vals.ptr, &dc->csc_total, s));
-  CUDA_TRY(launch_csc_counts((const int*)W->nz_count.ptr, (int)m, dColCount, s));
-  CUDA_TRY(cudaMemcpyAsync(dScale, W->scale.ptr, (size_t)p * 8, cudaMemcpyDeviceToDevice, s));
+  return export_columns(*W, m, p, nzcap, dColCount, dRows, dVals, cap, nnz_out, dScale, dIters,
+                        dSweeps, dConverged, s, st);
+}
+
+int spmesl_gram_supported(int64_t n, int64_t p) {
+  if (n < 2 || p < 2 || p > (int64_t)0x7fffffff) return 0;
+  int dev;
+  if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return 0; }
+  int optin = 0;
+  if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  const int n_pad = (int)(((n + KC - 1) / KC) * KC);
+  return tail_smem_bytes((int)p, n_pad, initial_nzcap(n, p)) <= (size_t)optin ? 1 : 0;
+}
+
+int64_t spmesl_gram_tile_count(int64_t p) {
+  if (p < 1 || p > (int64_t)0x7fffffff) return -1;
+  return gram_tile_count(p);
+}
+
+int spmesl_gram_screen_device(const double* dX, int64_t n, int64_t p, double lambda0,
+                              int64_t tile_begin, int64_t tile_end, const spmesl_options* opt,
+                              uint8_t* dHit, void* cuda_stream, spmesl_stats* st) {
+  init_stats(st);
+  spmesl_options o = resolve(opt);
+  int rc = validate(dX, n, p, lambda0, 1.0, 1, o);
+  if (rc) return rc;
+  if (!dHit) return fail(SPMESL_ERR_ARG, "dHit is NULL");
+  const int64_t nt = gram_tile_count(p);
+  if (tile_begin < 0 || tile_end > nt || tile_begin > tile_end)
+    return fail(SPMESL_ERR_ARG, "bad tile range");
+  int dev;
+  if ((rc = current_device(-1, &dev))) return rc;
+  Workspace* W = workspace_for(dev);
+  std::lock_guard<std::mutex> lk(W->mu);
+  if ((rc = ws_init(*W, dev))) return rc;
+  if (W->cc_major < 10) return fail(SPMESL_ERR_UNSUPPORTED, "needs an sm_100 device");
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  Layout L;
+  set_layout(L, n, p);
+  if ((rc = alloc_core(*W, L, 1, 8))) return rc;
+  if ((rc = run_prep(*W, dX, 1, o, L, s, /*band=*/false))) return rc;
+  GramParams G{};
+  G.Xb = (const double*)W->xb.ptr;
+  G.n = (int)n; G.n_pad = L.n_pad; G.nchunk = L.nchunk; G.p = (int)p; G.nblk = (int)L.nblk;
+  G.lambda0 = lambda0;
+  G.G = nullptr;
+  G.hit = dHit;
+  G.tile_begin = (int)tile_begin;
+  G.tile_end = (int)tile_end;
+  CUDA_TRY(launch_syrk_screen(G, (int)std::min<int64_t>(W->sms, std::max<int64_t>(1, tile_end - tile_begin)), s));
+  CUDA_TRY(cudaEventRecord(W->ev[7], s));
   if ((rc = read_counters(*W, s))) return rc;
-  const int64_t total = W->host_counters->csc_total;
-  *nnz_out = total;
-  if (total > cap) return fail(SPMESL_ERR_ARG, "CSC capacity too small: need " + std::to_string(total));
-  if (total > 0) {
-    CUDA_TRY(cudaMemcpyAsync(dRows, W->csc_rows.ptr, (size_t)total * 4, cudaMemcpyDeviceToDevice, s));
-    CUDA_TRY(cudaMemcpyAsync(dVals, W->csc_vals.ptr, (size_t)total * 8, cudaMemcpyDeviceToDevice, s));
-  }
-  int any_unconv = 0;
-  if ((rc = collect_stats(dIters, dSweeps, dConverged, m, p, s, st, &any_unconv))) return rc;
+  if (W->host_counters->err) return std_error(*W, st);
   if (st) {
-    st->nnz = total;
+    st->solver = 2;
     st->ms_standardize = ev_ms(W->ev[0], W->ev[1]);
-    st->ms_cd = ev_ms(W->ev[1], W->ev[2]);
-    st->kernel_launches += 6;
+    st->ms_gram = ev_ms(W->ev[1], W->ev[7]);
+    st->kernel_launches = 2;
+    st->bad_column = -1;
   }
-  return any_unconv ? SPMESL_WARN_NOT_CONVERGED : SPMESL_OK;
+  return SPMESL_OK;
+}
+
+int spmesl_fit_columns_gram_device(const double* dX, int64_t n, int64_t p, int64_t col_begin,
+                                   int64_t col_end, double lambda0, double tol, int32_t max_iter,
+                                   const spmesl_options* opt, const uint8_t* dHit,
+                                   int32_t* dColCount, int32_t* dRows, double* dVals, int64_t cap,
+                                   int64_t* nnz_out, double* dSigmaStd, double* dScale,
+                                   int32_t* dIters, int32_t* dSweeps, uint8_t* dConverged,
+                                   void* cuda_stream, spmesl_stats* st) {
+  init_stats(st);
+  spmesl_options o = resolve(opt);
+  int rc = validate(dX, n, p, lambda0, tol, max_iter, o);
+  if (rc) return rc;
+  if (col_begin < 0 || col_end > p || col_begin >= col_end)
+    return fail(SPMESL_ERR_ARG, "bad column range");
+  if (o.mode != 0) return fail(SPMESL_ERR_UNSUPPORTED, "the Gram solver implements mode 0");
+  if (!dHit || !dColCount || !dRows || !dVals || !nnz_out || !dSigmaStd || !dScale || !dIters)
+    return fail(SPMESL_ERR_ARG, "pointer argument is NULL");
+  int dev;
+  if ((rc = current_device(-1, &dev))) return rc;
+  Workspace* W = workspace_for(dev);
+  std::lock_guard<std::mutex> lk(W->mu);
+  if ((rc = ws_init(*W, dev))) return rc;
+  if (W->cc_major < 10) return fail(SPMESL_ERR_UNSUPPORTED, "needs an sm_100 device");
+  const int64_t m = col_end - col_begin;
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  if (!dSweeps) { if ((rc = ensure(W->sweeps, (size_t)m * 4))) return rc; dSweeps = (int32_t*)W->sweeps.ptr; }
+  if (!dConverged) { if ((rc = ensure(W->conv, (size_t)m))) return rc; dConverged = (uint8_t*)W->conv.ptr; }
+  FitOut out{col_begin, col_end, dSigmaStd, dIters, dSweeps, dConverged};
+  Layout L;
+  int nzcap = 0;
+  rc = fit_gram_columns_core(*W, dX, n, p, col_begin, col_end, lambda0, tol, max_iter, o, dHit, out,
+                             s, st, L, &nzcap);
+  if (rc) return rc;
+  return export_columns(*W, m, p, nzcap, dColCount, dRows, dVals, cap, nnz_out, dScale, dIters,
+                        dSweeps, dConverged, s, st);
 }
 
 int spmesl_assemble_device(int64_t p, int64_t col_begin, int64_t col_end, const int64_t* dColPtr,

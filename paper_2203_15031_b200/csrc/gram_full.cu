@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) syrk_screen_kernel(const GramPar
   const int nst = P.nst;
   const int nchunk = P.nchunk, nblk = P.nblk, p = P.p;
   const int nT = (nblk + GB - 1) / GB;
-  const int ntiles = nT * (nT + 1) / 2;
+  const int t_begin = P.tile_begin, t_end = P.tile_end;
   if (tid == 0) {
     for (int s = 0; s < nst; ++s) {
       mbar_init_g(&full[s], 1);
@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) syrk_screen_kernel(const GramPar
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int t = t_begin + blockIdx.x; t < t_end; t += gridDim.x) {
         int I, Jt;
         tri_tile(t, nT, I, Jt);
         for (int q = 0; q < nchunk; ++q) {
@@ -127,7 +127,8 @@ __global__ void __launch_bounds__(G_THREADS, 1) syrk_screen_kernel(const GramPar
   const double lam0 = P.lambda0;
   int s = 0;
   uint32_t ph = 0;
-  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  double* const Gout = P.G;
+  for (int t = t_begin + blockIdx.x; t < t_end; t += gridDim.x) {
     int I, Jt;
     tri_tile(t, nT, I, Jt);
     double acc[8][4][2];
@@ -175,8 +176,10 @@ __global__ void __launch_bounds__(G_THREADS, 1) syrk_screen_kernel(const GramPar
           const int col = col0 + ni * 8 + 2 * t4 + e;
           if (row < p && col < p) {
             const double v = acc[mi][ni][e] * inv_n;
-            __stcs(P.G + (size_t)col * p + row, v);
-            if (!diag_tile) __stcs(P.G + (size_t)row * p + col, v);
+            if (Gout) {
+              __stcs(Gout + (size_t)col * p + row, v);
+              if (!diag_tile) __stcs(Gout + (size_t)row * p + col, v);
+            }
             if (row != col && fabs(v) > lam0) {
               P.hit[col] = 1;
               if (!diag_tile) P.hit[row] = 1;
@@ -232,9 +235,15 @@ __global__ void gram_init_kernel(const GramParams P) {
 
 size_t syrk_smem_bytes(int nst) { return 128 + (size_t)nst * G_STAGE_DOUBLES * 8; }
 
+int gram_tile_count(int64_t p) {
+  const int64_t nT = (((p + J - 1) / J) + GB - 1) / GB;
+  return (int)(nT * (nT + 1) / 2);
+}
+
 cudaError_t launch_syrk_screen(const GramParams& P, int grid, cudaStream_t s) {
   GramParams Q = P;
   Q.nst = G_MAX_NST;
+  if (Q.tile_end <= Q.tile_begin) return cudaSuccess;
   const size_t smem = syrk_smem_bytes(Q.nst);
   cudaError_t e = cudaFuncSetAttribute(syrk_screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);

@@ -137,8 +137,9 @@ struct GramParams {
   double lambda0, tol, sigma_floor, sqrt_n;
   int max_outer;
   int nst;
-  double* G;               // [p][p] column-major
+  double* G;               // [p][p] column-major (nullptr: screening only)
   uint8_t* hit;            // [p] column has some |G_jc| > lambda0, j != c
+  int tile_begin, tile_end;   // upper-triangle tiles to process (multi-GPU share)
   TailState* tail;         // columns for the sweep kernel
   int* tail_count;
   double* sigma_std;
@@ -151,6 +152,7 @@ struct GramParams {
 size_t syrk_smem_bytes(int nst);
 cudaError_t launch_syrk_screen(const GramParams& P, int grid, cudaStream_t s);
 cudaError_t launch_gram_init(const GramParams& P, cudaStream_t s);
+int gram_tile_count(int64_t p);
 
 constexpr int TAIL_THREADS = 256;
 constexpr int TAIL_ODC = 8;          // on-demand Gram column cache entries per CTA

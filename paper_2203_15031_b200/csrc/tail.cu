@@ -155,6 +155,30 @@ size_t tail_smem_bytes(int p, int n_pad, int nzcap) {
   return (b + 127) & ~(size_t)127;
 }
 
+// Gram column G[:, j] of the fit-wide table: precomputed, or computed here once (claim 0 -> 1,
+// write, publish 2) by the same DMMA routine as the batched pass; every CTA is resident, so
+// waiting for another CTA's claim is safe.  Called by all threads of the block.
+__device__ void ensure_gram_column(const TailParams& P, int j, TailShared& TS, double* tx,
+                                   double* tvv) {
+  if (P.gtab_full || *(volatile int*)&P.gstate[j] == 2) return;
+  const int tid = threadIdx.x;
+  __syncthreads();
+  if (tid == 0) { TS.oc_var[0] = j; TS.k2 = atomicCAS(&P.gstate[j], 0, 1); }
+  __syncthreads();
+  if (TS.k2 == 0) {
+    for (int b = 0; b < P.nblk; ++b)     // vector j alone in a tile: same DMMA chain
+      gram_tile(P.Xb, b, P.nchunk, P.n, P.p, nullptr, 0, &TS.oc_var[0], 1, P.n_pad, 0, 1, tx,
+                tvv, nullptr, P.Gtab);
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) { atomicExch(&P.gstate[j], 2); atomicAdd(P.ondemand_count, 1); }
+  } else if (tid == 0) {
+    while (*(volatile int*)&P.gstate[j] != 2) __nanosleep(200);
+  }
+  __threadfence();
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(TAIL_THREADS, 1) tail_sweep_kernel(const TailParams P) {
   extern __shared__ __align__(128) unsigned char sm[];
   const int p = P.p, n = P.n, n_pad = P.n_pad, nchunk = P.nchunk, nzcap = P.nzcap;
@@ -190,6 +214,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) tail_sweep_kernel(const TailP
     int ocnt = min(ts.cnt, nzcap);
     bool overflow = ts.cnt > nzcap;
     if (P.z_from_gtab) {
+      ensure_gram_column(P, gc, TS, tx, tvv);
       const double* gz = P.Gtab + (size_t)gc * p;
       for (int j = tid; j < p; j += TAIL_THREADS) z[j] = __ldcs(gz + j);
     } else {
@@ -235,26 +260,8 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) tail_sweep_kernel(const TailP
         }
         if (d != 0.0) {
           maxd = fmax(maxd, fabs(d));
-          // Gram column G[:, j]: precomputed, cached, or computed now (same DMMA routine)
-          // Gram column G[:, j] from the fit-wide table: precomputed, or computed here once
-          // (claim 0 -> 1, write, publish 2); every CTA is resident, so waiting is safe
           const double* gcol = P.Gtab + (size_t)j * p;
-          if (!P.gtab_full && *(volatile int*)&P.gstate[j] != 2) {
-            if (tid == 0) { TS.oc_var[0] = j; TS.k2 = atomicCAS(&P.gstate[j], 0, 1); }
-            __syncthreads();
-            if (TS.k2 == 0) {
-              for (int b = 0; b < P.nblk; ++b)     // vector j alone in a tile: same DMMA chain
-                gram_tile(P.Xb, b, nchunk, n, p, nullptr, 0, &TS.oc_var[0], 1, n_pad, 0, 1,
-                          tx, tvv, nullptr, P.Gtab);
-              __threadfence();
-              __syncthreads();
-              if (tid == 0) { atomicExch(&P.gstate[j], 2); atomicAdd(P.ondemand_count, 1); }
-            } else if (tid == 0) {
-              while (*(volatile int*)&P.gstate[j] != 2) __nanosleep(200);
-            }
-            __threadfence();
-            __syncthreads();
-          }
+          ensure_gram_column(P, j, TS, tx, tvv);
           for (int t = tid; t < p; t += TAIL_THREADS) z[t] = fma(d, __ldcg(gcol + t), z[t]);
         }
         __syncthreads();

@@ -8,8 +8,14 @@ values, sigma) — the nonzeros, not p x p doubles — after which every rank as
 symmetrizes its own column block of Theta from the global CSC (the symmetrization of
 Eq. (symm), needs b_kj from column j, which may live on another rank).
 
-``gather_csc`` is backend-agnostic host logic (gloo on CPU tensors in the tests, NCCL on
-CUDA tensors in production); ``fit_distributed`` runs the CUDA path around it.
+With the Gram solver (default when it applies) there is one more, tiny exchange before the
+fit: every rank screens an equal share of the upper-triangle tiles of S = X~^T X~ / n (the
+first sweeps of all columns) and the p screening flags are max-all-reduced, so
+each rank knows which of its columns need more than one sweep.
+
+``gather_csc`` / ``allreduce_hits`` are backend-agnostic host logic (gloo on CPU tensors in
+the tests, NCCL on CUDA tensors in production); ``fit_distributed`` runs the CUDA path around
+them.
 """
 from __future__ import annotations
 
@@ -22,6 +28,11 @@ def column_range(p: int, rank: int, world: int):
     base, rem = divmod(p, world)
     c0 = rank * base + min(rank, rem)
     return c0, c0 + base + (1 if rank < rem else 0)
+
+
+def tile_range(ntiles: int, rank: int, world: int):
+    """Contiguous, balanced share of the Gram tiles for `rank` (same rule as column_range)."""
+    return column_range(ntiles, rank, world)
 
 
 def _comm_device(t: torch.Tensor, group=None) -> torch.device:
@@ -76,22 +87,51 @@ def gather_csc(p: int, counts: torch.Tensor, rows: torch.Tensor, vals: torch.Ten
     return col_ptr, torch.cat(row_list), torch.cat(val_list), torch.cat(sig_list)
 
 
+def allreduce_hits(hit: torch.Tensor, group=None) -> torch.Tensor:
+    """Elementwise max (= OR of 0/1 flags) of the uint8 screening flags over all ranks."""
+    cdev = _comm_device(hit, group)
+    buf = hit.to(cdev)
+    dist.all_reduce(buf, op=dist.ReduceOp.MAX, group=group)
+    if buf is not hit:
+        hit.copy_(buf.to(hit.device))
+    return hit
+
+
 def fit_distributed(X: torch.Tensor, lambda0: float, tol: float = 1e-4, max_iter: int = 100,
-                    group=None, stream=None, **options):
+                    group=None, stream=None, solver: str = "auto", **options):
     """Fit this rank's column block and return its block of Theta (p x m, column-major view).
 
-    X: (n, p) float64 CUDA tensor, identical on every rank."""
-    from . import assemble_device, fit_columns_device
+    X: (n, p) float64 CUDA tensor, identical on every rank.  solver: "auto" (Gram when it
+    applies), "gram" or "residual"."""
+    from . import (as_colmajor, assemble_device, fit_columns_device, fit_columns_gram_device,
+                   gram_screen_device, gram_supported, gram_tile_count)
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     n, p = X.shape
     c0, c1 = column_range(p, rank, world)
-    part = fit_columns_device(X, c0, c1, lambda0, tol, max_iter, stream=stream, **options)
+    mode = options.get("mode", "per_column")
+    use_gram = solver == "gram" or (solver == "auto" and mode in ("per_column", 0)
+                                    and gram_supported(n, p))
+    screen_stats = None
+    if use_gram:
+        X = as_colmajor(X)
+        t0, t1 = tile_range(gram_tile_count(p), rank, world)
+        hit = torch.zeros(p, dtype=torch.uint8, device=X.device)
+        screen_stats = gram_screen_device(X, lambda0, t0, t1, hit, stream=stream, **options)
+        allreduce_hits(hit, group)
+        part = fit_columns_gram_device(X, c0, c1, lambda0, hit, tol, max_iter, stream=stream,
+                                       **options)
+    else:
+        part = fit_columns_device(X, c0, c1, lambda0, tol, max_iter, stream=stream,
+                                  solver="residual" if solver == "auto" else solver, **options)
     col_ptr, rows, vals, sig_all = gather_csc(p, part["counts"], part["rows"], part["vals"],
                                               part["sigma_std"], group)
     theta, sigma = assemble_device(p, c0, c1, col_ptr, rows, vals, sig_all, part["scale"],
                                    stream=stream, **options)
     stats = dict(part["stats"])
     stats["kernel_launches"] = stats.get("kernel_launches", 0) + 2   # assemble entries + diag
+    if screen_stats is not None:
+        stats["ms_gram"] = screen_stats["ms_gram"]
+        stats["kernel_launches"] += screen_stats["kernel_launches"]
     return dict(theta=theta, sigma=sigma, iters=part["iters"], sweeps=part["sweeps"],
                 converged=part["converged"], col_range=(c0, c1), stats=stats,
                 code=part["code"])

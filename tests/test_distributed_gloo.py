@@ -89,3 +89,51 @@ def test_gather_csc_matches_single_fit(oracle, world):
         np.testing.assert_array_equal(grows, rows)
         np.testing.assert_array_equal(gvals, vals)
         np.testing.assert_array_equal(gsig, full.sigma)
+
+
+def _hits_worker(rank, world, port, Xs, lam, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2203_15031_b200.distributed import allreduce_hits, tile_range
+        n, p = Xs.shape
+        S = Xs.T @ Xs / n
+        np.fill_diagonal(S, 0.0)
+        # this rank's share of the (column-pair) work: a contiguous block of rows of S
+        r0, r1 = tile_range(p, rank, world)
+        hit = np.zeros(p, np.uint8)
+        blk = np.abs(S[r0:r1, :]) > lam          # (j in share, c): S is symmetric
+        hit[np.any(blk, axis=0)] = 1              # column c hit through row j
+        hit[r0:r1][np.any(blk, axis=1)] = 1       # the mirror entries (c, j)
+        t = torch.from_numpy(hit)
+        allreduce_hits(t, None)
+        out_q.put((rank, t.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_allreduce_hits_is_the_global_screen(oracle, world):
+    """The max-all-reduce of per-rank screening flags equals the screening of the full S."""
+    from synth import generators as G
+    X, _, _ = G.make_config(3, p=300, n=150)
+    Xs, mu, s = oracle.standardize(X)
+    lam = oracle.lambda_univ(*X.shape)
+    S = Xs.T @ Xs / X.shape[0]
+    np.fill_diagonal(S, 0.0)
+    want = np.any(np.abs(S) > lam, axis=0).astype(np.uint8)
+    assert 0 < want.sum() < want.size
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_hits_worker, args=(r, world, port, Xs, lam, q))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    for rank, hit in res:
+        np.testing.assert_array_equal(hit, want)

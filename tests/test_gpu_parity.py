@@ -192,7 +192,7 @@ def test_full_size_config5_sampled_columns(S, oracle, solver):
         assert np.all(np.abs(got - want) <= 1e-8 * np.abs(want) + 1e-12 * abs(want[k])), k
 
 
-def _rank_worker(rank, world, port, X, lam, q):
+def _rank_worker(rank, world, port, X, lam, q, solver):
     import os
     import torch
     import torch.distributed as dist
@@ -203,25 +203,28 @@ def _rank_worker(rank, world, port, X, lam, q):
         torch.cuda.set_device(0)
         from paper_2203_15031_b200.distributed import fit_distributed
         Xd = torch.from_numpy(np.ascontiguousarray(X)).cuda()
-        r = fit_distributed(Xd, lam)
+        r = fit_distributed(Xd, lam, solver=solver)
         q.put((rank, r["col_range"], r["theta"].cpu().numpy(), r["sigma"].cpu().numpy(),
                r["iters"].cpu().numpy(), r["sweeps"].cpu().numpy()))
     finally:
         dist.destroy_process_group()
 
 
-def test_two_ranks_sharing_one_gpu_match_single_fit(S, oracle):
-    """fit_distributed (column blocks + CSC all-gather + per-rank assembly) on 2 ranks that
-    share cuda:0 over gloo must reproduce the single-GPU fit bit for bit."""
+@pytest.mark.parametrize("solver", ["residual", "gram"])
+def test_two_ranks_sharing_one_gpu_match_single_fit(S, oracle, solver):
+    """fit_distributed (column blocks + CSC all-gather + per-rank assembly; for the Gram solver
+    also the tile-share screening + flag all-reduce) on 2 ranks that share cuda:0 over gloo
+    must reproduce the single-GPU fit bit for bit."""
     import socket
     import torch.multiprocessing as mp
     X, _, _ = G.make_config(4, p=1200, family="hub")
     lam = oracle.lambda_ub(*X.shape)
-    full = S.fit(X, lam, solver="residual")
+    full = S.fit(X, lam, solver=solver)
     sk = socket.socket(); sk.bind(("127.0.0.1", 0)); port = sk.getsockname()[1]; sk.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_rank_worker, args=(r, 2, port, X, lam, q)) for r in range(2)]
+    procs = [ctx.Process(target=_rank_worker, args=(r, 2, port, X, lam, q, solver))
+             for r in range(2)]
     for pr in procs:
         pr.start()
     res = [q.get(timeout=300) for _ in range(2)]
@@ -293,3 +296,31 @@ def test_unstandardized_scaled_columns_and_caps(S, oracle, solver, mi):
         print(solver, mi, rep)
         assert_parity(rep)
         assert np.array_equal(res.converged, ora.converged)
+
+
+def test_gram_building_blocks_reproduce_full_fit(S, oracle):
+    """Screening in tile shares + Gram column blocks + assembly == the single Gram fit."""
+    import torch
+    X, _, _ = G.make_config(4, p=900, family="hub")
+    n, p = X.shape
+    lam = oracle.lambda_ub(n, p)
+    full = S.fit(X, lam, solver="gram")
+    Xd = torch.from_numpy(np.ascontiguousarray(X)).cuda()
+    nt = S.gram_tile_count(p)
+    hit = torch.zeros(p, dtype=torch.uint8, device="cuda")
+    for a, b in [(0, nt // 3), (nt // 3, nt // 3), (nt // 3, nt)]:
+        S.gram_screen_device(Xd, lam, a, b, hit)
+    bounds = [0, 250, 251, 600, 900]
+    parts = [S.fit_columns_gram_device(Xd, a, b, lam, hit) for a, b in zip(bounds[:-1], bounds[1:])]
+    counts = torch.cat([q["counts"] for q in parts]).long()
+    col_ptr = torch.zeros(p + 1, dtype=torch.int64, device="cuda")
+    col_ptr[1:] = torch.cumsum(counts, 0)
+    rows = torch.cat([q["rows"] for q in parts])
+    vals = torch.cat([q["vals"] for q in parts])
+    sig = torch.cat([q["sigma_std"] for q in parts])
+    th, so = S.assemble_device(p, 0, p, col_ptr, rows, vals, sig, parts[0]["scale"])
+    it = torch.cat([q["iters"] for q in parts]).cpu().numpy()
+    sw = torch.cat([q["sweeps"] for q in parts]).cpu().numpy()
+    assert np.array_equal(it, full.iters) and np.array_equal(sw, full.sweeps)
+    assert np.array_equal(so.cpu().numpy(), full.sigma)
+    assert np.array_equal(th.cpu().numpy(), full.Theta)
