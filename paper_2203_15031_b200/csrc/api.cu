@@ -91,6 +91,10 @@ struct Workspace {
   cudaEvent_t ev[8] = {};
   cudaStream_t side = nullptr;            // Theta zero-fill overlapped with the CD kernel
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  double* pending_zero = nullptr;         // Theta to zero-fill once standardization is done
+  size_t pending_count = 0;
+  double* take_zero = nullptr;            // Theta the Gram kernel may zero-fill itself
+  size_t take_count = 0;
   bool init = false;
 };
 
@@ -264,6 +268,13 @@ int run_prep(Workspace& W, const double* dX, int64_t m, const spmesl_options& o,
                               (double*)W.scale.ptr, &dc->err, &dc->bad_key, s));
   if (band) CUDA_TRY(launch_gram((const double*)W.xb.ptr, L, (double*)W.gband.ptr, s));
   CUDA_TRY(cudaEventRecord(W.ev[1], s));
+  if (W.pending_zero) {
+    // Theta's zero fill (HBM-bound) overlaps the solver (compute-bound), not standardization
+    CUDA_TRY(cudaStreamWaitEvent(W.side, W.ev[1], 0));
+    CUDA_TRY(launch_zero_fill(W.pending_zero, W.pending_count, W.sms, W.side));
+    CUDA_TRY(cudaEventRecord(W.ev_join, W.side));
+    W.pending_zero = nullptr;
+  }
   return SPMESL_OK;
 }
 
@@ -602,6 +613,12 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   G.hit = (uint8_t*)W.hit.ptr;
   G.tile_begin = 0;
   G.tile_end = gram_tile_count(p);
+  if (W.pending_zero == nullptr && W.take_zero && (((uintptr_t)W.take_zero & 15) == 0) &&
+      (W.take_count & 1) == 0) {
+    // the Gram kernel's producer zero-fills Theta with bulk stores while it computes
+    G.zero_ptr = W.take_zero;
+    G.zero_count = W.take_count;
+  }
   G.tail = (TailState*)W.tail.ptr;
   G.tail_count = &dc->tail_count;
   G.sigma_std = out.sigma_std; G.iters = out.iters; G.sweeps = out.sweeps;
@@ -745,12 +762,15 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
   if (o.solver == 2 && !gram_ok) return fail(SPMESL_ERR_UNSUPPORTED, "solver = 2: " + why);
   const bool gram = gram_ok && o.solver != 1 && o.mode == 0;
   // zero-fill Theta (8 p^2 bytes, the only dense pass) on a side stream while the solver runs
-  CUDA_TRY(cudaEventRecord(W.ev_fork, s));
-  CUDA_TRY(cudaStreamWaitEvent(W.side, W.ev_fork, 0));
-  CUDA_TRY(cudaMemsetAsync(dTheta, 0, sizeof(double) * (size_t)p * (size_t)p, W.side));
-  CUDA_TRY(cudaEventRecord(W.ev_join, W.side));
+  // (launched by run_prep right after standardization; joined before the assembly)
   DevCounters* dc = nullptr;
   for (int attempt = 0; attempt < 4; ++attempt) {
+    const size_t pp = (size_t)p * (size_t)p;
+    // the Gram kernel zero-fills Theta itself (bulk stores from its producer warp) when the
+    // buffer allows 16-byte pieces; otherwise a side-stream kernel does, after standardization
+    const bool take = gram && (((uintptr_t)dTheta & 15) == 0) && (pp & 1) == 0;
+    if (take) { W.take_zero = dTheta; W.take_count = pp; }
+    else { W.pending_zero = dTheta; W.pending_count = pp; }
     if (gram) {
       // everything is enqueued; the one host synchronisation is the counter read at the end
       if (!nzcap) nzcap = initial_nzcap(n, p);
@@ -758,8 +778,13 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
     } else {
       rc = fit_columns_core(W, dX, n, p, 0, p, lambda0, tol, max_iter, o, out, s, st, L, &nzcap);
     }
-    if (rc) { cudaStreamWaitEvent(s, W.ev_join, 0); return rc; }
-    CUDA_TRY(cudaStreamWaitEvent(s, W.ev_join, 0));
+    W.take_zero = nullptr;
+    if (W.pending_zero) {    // (the solver failed before standardization)
+      W.pending_zero = nullptr;
+      if (!rc) rc = fail(SPMESL_ERR_CUDA, "internal: Theta zero fill was not launched");
+    }
+    if (rc) { if (!take) cudaStreamWaitEvent(s, W.ev_join, 0); return rc; }
+    if (!take) CUDA_TRY(cudaStreamWaitEvent(s, W.ev_join, 0));
     const size_t cap = (size_t)p * (size_t)nzcap;
     if ((rc = ensure(W.csc_rows, cap * 4))) return rc;
     if ((rc = ensure(W.csc_vals, cap * 8))) return rc;
@@ -782,11 +807,7 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
     if (!W.host_counters->overflow) { gram_stats(W, p, nzcap, st); break; }
     if (nzcap >= p) return fail(SPMESL_ERR_OOM, "coefficient list overflow");
     nzcap = (int)std::min<int64_t>(p, (int64_t)nzcap * 4);
-    // (Theta's zero fill is redone: the assembly above wrote into it)
-    CUDA_TRY(cudaEventRecord(W.ev_fork, s));
-    CUDA_TRY(cudaStreamWaitEvent(W.side, W.ev_fork, 0));
-    CUDA_TRY(cudaMemsetAsync(dTheta, 0, sizeof(double) * (size_t)p * (size_t)p, W.side));
-    CUDA_TRY(cudaEventRecord(W.ev_join, W.side));
+    // (Theta's zero fill is redone at the top of the loop: the assembly above wrote into it)
   }
   int any_unconv = 0;
   stats_from_counters(*W.host_counters, p, st, &any_unconv);

@@ -273,4 +273,29 @@ cudaError_t launch_column_stats(const int32_t* iters, const int32_t* sweeps, con
   return cudaGetLastError();
 }
 
+// Zero-fill of Theta on a side stream with a grid of one 256-thread block per SM: small enough
+// to stay co-resident with the solver kernel (one CTA per SM), so the 8 p^2-byte write really
+// overlaps the solve instead of occupying every SM first as a library memset would.
+__global__ void __launch_bounds__(256) zero_fill_kernel(double2* __restrict__ a, size_t n2) {
+  const double2 z = make_double2(0.0, 0.0);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n2;
+       i += (size_t)gridDim.x * blockDim.x)
+    __stcs(a + i, z);
+}
+
+cudaError_t launch_zero_fill(double* a, size_t count, int sms, cudaStream_t s) {
+  if (count == 0) return cudaSuccess;
+  if (((uintptr_t)a & 15) != 0 || (count & 1)) return cudaMemsetAsync(a, 0, count * 8, s);
+  // same shared-memory carve-out as the solver kernels, so an SM running this kernel can take a
+  // solver CTA without being reconfigured (which would serialize the two)
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(zero_fill_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    attr = true;
+  }
+  zero_fill_kernel<<<sms, 256, 0, s>>>((double2*)a, count / 2);
+  return cudaGetLastError();
+}
+
 }  // namespace spmesl

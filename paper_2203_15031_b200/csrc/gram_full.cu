@@ -42,12 +42,29 @@ __device__ __forceinline__ void mbar_wait_g(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void bulk_g2s_g(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+// (X~ is re-read by every tile row/column: keep it in L2 ahead of the streaming G stores)
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t pol) {
   asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
           smem_u32g(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32g(bar))
+      "l"(src), "r"(bytes), "r"(smem_u32g(bar)), "l"(pol)
       : "memory");
+}
+// bulk store shared -> global (async proxy), grouped for a final wait
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst),
+               "r"(smem_u32g(src)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 __device__ __forceinline__ void dmma_g(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -60,6 +77,7 @@ constexpr int G_MMA_WARPS = 8;
 constexpr int G_THREADS = (G_MMA_WARPS + 1) * 32;
 constexpr int G_STAGE_DOUBLES = 2 * GB * CHUNK_DOUBLES;     // 8 Xb tiles = 64 KB
 constexpr int G_MAX_NST = 3;
+constexpr int G_ZPIECE = 2048;         // doubles per zero-fill bulk store (16 KB)
 
 // tile index t of the upper triangle (I <= J) of an nT x nT tile grid, row-major by I
 __device__ __forceinline__ void tri_tile(int t, int nT, int& I, int& Jt) {
@@ -74,11 +92,14 @@ __global__ void __launch_bounds__(G_THREADS, 1) syrk_screen_kernel(const GramPar
   uint64_t* full = (uint64_t*)smem_raw;
   uint64_t* empty = full + G_MAX_NST;
   double* Xs = (double*)(smem_raw + 128);
+  double* zbuf = Xs + (size_t)P.nst * G_STAGE_DOUBLES;        // [G_ZPIECE] zeros
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nst = P.nst;
   const int nchunk = P.nchunk, nblk = P.nblk, p = P.p;
   const int nT = (nblk + GB - 1) / GB;
   const int t_begin = P.tile_begin, t_end = P.tile_end;
+  if (P.zero_ptr)
+    for (int e = tid; e < G_ZPIECE; e += blockDim.x) zbuf[e] = 0.0;
   if (tid == 0) {
     for (int s = 0; s < nst; ++s) {
       mbar_init_g(&full[s], 1);
@@ -94,6 +115,19 @@ __global__ void __launch_bounds__(G_THREADS, 1) syrk_screen_kernel(const GramPar
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
+      const uint64_t pol = l2_evict_last_policy();
+      // Theta's zero fill rides along: one 16 KB bulk store of zeros per X chunk issued
+      // (pieces b, b + G, ... of the output), the rest after the last tile
+      const size_t npieces = P.zero_ptr ? (P.zero_count + G_ZPIECE - 1) / G_ZPIECE : 0;
+      size_t zp = blockIdx.x;
+      auto zero_piece = [&]() {
+        if (zp < npieces) {
+          const size_t off = zp * G_ZPIECE;
+          const size_t cnt = min((size_t)G_ZPIECE, P.zero_count - off);
+          bulk_s2g(P.zero_ptr + off, zbuf, (uint32_t)(cnt * 8));
+          zp += gridDim.x;
+        }
+      };
       for (int t = t_begin + blockIdx.x; t < t_end; t += gridDim.x) {
         int I, Jt;
         tri_tile(t, nT, I, Jt);
@@ -109,12 +143,16 @@ __global__ void __launch_bounds__(G_THREADS, 1) syrk_screen_kernel(const GramPar
           for (int u = 0; u < 2 * GB; ++u) {
             const int blk = (u < GB ? I * GB + u : Jt * GB + (u - GB));
             if (blk < nblk)
-              bulk_g2s_g(st + (size_t)u * CHUNK_DOUBLES,
-                         P.Xb + ((size_t)blk * nchunk + q) * CHUNK_DOUBLES, CHUNK_BYTES, &full[s]);
+              bulk_g2s_hint(st + (size_t)u * CHUNK_DOUBLES,
+                            P.Xb + ((size_t)blk * nchunk + q) * CHUNK_DOUBLES, CHUNK_BYTES, &full[s],
+                            pol);
           }
+          zero_piece();
           if (++s == nst) { s = 0; ph ^= 1u; }
         }
       }
+      while (zp < npieces) zero_piece();
+      bulk_wait_all();
     }
     return;
   }
@@ -166,26 +204,43 @@ __global__ void __launch_bounds__(G_THREADS, 1) syrk_screen_kernel(const GramPar
     const bool diag_tile = (I == Jt);
     const int row0 = I * GB * J + 64 * mh;
     const int col0 = Jt * GB * J + 32 * nq;
+    // stores are whole 32-byte sectors when p % 4 == 0 (8 lanes x 8 B down a column of G, or
+    // 4 lanes x 16 B along a row for the mirror), so L2 never reads back partial sectors
+    const bool vec = (p & 3) == 0;
 #pragma unroll
     for (int mi = 0; mi < 8; ++mi) {
       const int row = row0 + mi * 8 + g;
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni)
+      for (int ni = 0; ni < 4; ++ni) {
+        const int colp = col0 + ni * 8 + 2 * t4;         // this lane's column pair
+        const double v0 = acc[mi][ni][0] * inv_n, v1 = acc[mi][ni][1] * inv_n;
+        if (Gout) {
+          if (vec && row < p && colp + 1 < p) {
+            __stcs(Gout + (size_t)colp * p + row, v0);
+            __stcs(Gout + (size_t)(colp + 1) * p + row, v1);
+            if (!diag_tile) __stcs((double2*)(Gout + (size_t)row * p + colp), make_double2(v0, v1));
+          } else {
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int col = col0 + ni * 8 + 2 * t4 + e;
-          if (row < p && col < p) {
-            const double v = acc[mi][ni][e] * inv_n;
-            if (Gout) {
-              __stcs(Gout + (size_t)col * p + row, v);
-              if (!diag_tile) __stcs(Gout + (size_t)row * p + col, v);
-            }
-            if (row != col && fabs(v) > lam0) {
-              P.hit[col] = 1;
-              if (!diag_tile) P.hit[row] = 1;
+            for (int e = 0; e < 2; ++e) {
+              const int col = colp + e;
+              if (row < p && col < p) {
+                const double v = e ? v1 : v0;
+                __stcs(Gout + (size_t)col * p + row, v);
+                if (!diag_tile) __stcs(Gout + (size_t)row * p + col, v);
+              }
             }
           }
         }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = colp + e;
+          const double v = e ? v1 : v0;
+          if (row < p && col < p && row != col && fabs(v) > lam0) {
+            P.hit[col] = 1;
+            if (!diag_tile) P.hit[row] = 1;
+          }
+        }
+      }
     }
   }
 }
@@ -233,7 +288,7 @@ __global__ void gram_init_kernel(const GramParams P) {
 
 }  // namespace
 
-size_t syrk_smem_bytes(int nst) { return 128 + (size_t)nst * G_STAGE_DOUBLES * 8; }
+size_t syrk_smem_bytes(int nst) { return 128 + ((size_t)nst * G_STAGE_DOUBLES + G_ZPIECE) * 8; }
 
 int gram_tile_count(int64_t p) {
   const int64_t nT = (((p + J - 1) / J) + GB - 1) / GB;

@@ -140,6 +140,8 @@ struct GramParams {
   double* G;               // [p][p] column-major (nullptr: screening only)
   uint8_t* hit;            // [p] column has some |G_jc| > lambda0, j != c
   int tile_begin, tile_end;   // upper-triangle tiles to process (multi-GPU share)
+  double* zero_ptr;        // optional: zero-filled by the producer's bulk stores (Theta)
+  size_t zero_count;       // doubles (even; zero_ptr 16-byte aligned)
   TailState* tail;         // columns for the sweep kernel
   int* tail_count;
   double* sigma_std;
@@ -197,6 +199,7 @@ cudaError_t launch_assemble_coo(int64_t p, const int64_t* col_ptr, const int32_t
 cudaError_t launch_column_stats(const int32_t* iters, const int32_t* sweeps, const uint8_t* conv,
                                 int64_t m, unsigned long long* tot, int* mx_sweeps, int* mx_outer,
                                 int* nunc, cudaStream_t s);
+cudaError_t launch_zero_fill(double* a, size_t count, int sms, cudaStream_t s);
 cudaError_t launch_csc_counts(const int* nz_count, int ncols, int32_t* out, cudaStream_t s);
 cudaError_t launch_assemble(int64_t p, int64_t col_begin, int64_t col_end, const int64_t* col_ptr,
                             const int32_t* rows, const double* vals, const double* sigma_std,
