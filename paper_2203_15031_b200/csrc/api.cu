@@ -181,6 +181,15 @@ struct FitOut {
   uint8_t* conv;
 };
 
+// Gram-column prefetch in the sweep kernel when two p-vectors fit in shared memory and the
+// columns are 16-byte aligned (p even); SPMESL_TAIL_NOPREFETCH=1 disables it (development).
+void set_prefetch(const Workspace& W, TailParams& T) {
+  static const bool off = getenv("SPMESL_TAIL_NOPREFETCH") && atoi(getenv("SPMESL_TAIL_NOPREFETCH"));
+  T.prefetch = !off && (T.p % 2 == 0) &&
+               tail_smem_bytes(T.p, T.n_pad, T.nzcap) + tail_prefetch_bytes(T.p) <=
+                   (size_t)W.smem_optin;
+}
+
 bool tail_enabled(const Workspace& W, const spmesl_options& o, const Layout& L, int nzcap) {
   // (the fit-wide Gram table is p x p doubles: keep it under 16 GB)
   return o.tail_after > 0 && tail_smem_bytes((int)L.p, L.n_pad, nzcap) <= (size_t)W.smem_optin &&
@@ -247,6 +256,7 @@ int run_tail(Workspace& W, const Layout& L, int64_t cb, double lambda0, double t
   T.nz_rows = (int*)W.nz_rows.ptr; T.nz_vals = (double*)W.nz_vals.ptr;
   T.nz_count = (int*)W.nz_count.ptr; T.nz_cur = (int*)W.nz_cur.ptr;
   T.sigma_std = out.sigma_std; T.iters = out.iters; T.sweeps = out.sweeps; T.converged = out.conv;
+  set_prefetch(W, T);
   CUDA_TRY(launch_tail_sweeps(T, grid, s));
   CUDA_TRY(cudaEventRecord(W.ev[6], s));   // end of the tail solver
   if (st) { st->tail_columns = M; st->kernel_launches += 4; }
@@ -429,34 +439,6 @@ void stats_from_counters(const DevCounters& c, int64_t p, spmesl_stats* st, int*
     st->max_outer = c.st_max_outer;
     st->n_unconverged = c.st_unconv;
   }
-}
-
-// Per-column statistics (host side) from device arrays.
-int collect_stats(const int32_t* dIters, const int32_t* dSweeps, const uint8_t* dConv, int64_t m,
-                  int64_t p, cudaStream_t s, spmesl_stats* st, int* any_unconv) {
-  std::vector<int32_t> it(m), sw(m);
-  std::vector<uint8_t> cv(m);
-  CUDA_TRY(cudaMemcpyAsync(it.data(), dIters, 4 * m, cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaMemcpyAsync(sw.data(), dSweeps, 4 * m, cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaMemcpyAsync(cv.data(), dConv, m, cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaStreamSynchronize(s));
-  int64_t tot = 0;
-  int mx = 0, mo = 0, nu = 0;
-  for (int64_t k = 0; k < m; ++k) {
-    tot += sw[k];
-    mx = std::max(mx, sw[k]);
-    mo = std::max(mo, it[k]);
-    nu += cv[k] ? 0 : 1;
-  }
-  *any_unconv = nu > 0;
-  if (st) {
-    st->total_sweeps = tot;
-    st->coord_updates = tot * (p - 1);
-    st->max_sweeps = mx;
-    st->max_outer = mo;
-    st->n_unconverged = nu;
-  }
-  return SPMESL_OK;
 }
 
 float ev_ms(cudaEvent_t a, cudaEvent_t b) {
@@ -654,6 +636,7 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   T.nz_rows = (int*)W.nz_rows.ptr; T.nz_vals = (double*)W.nz_vals.ptr;
   T.nz_count = (int*)W.nz_count.ptr; T.nz_cur = (int*)W.nz_cur.ptr;
   T.sigma_std = out.sigma_std; T.iters = out.iters; T.sweeps = out.sweeps; T.converged = out.conv;
+  set_prefetch(W, T);
   CUDA_TRY(launch_tail_sweeps(T, (int)std::min<int64_t>(W.sms, p), s));
   CUDA_TRY(cudaEventRecord(W.ev[6], s));
   CUDA_TRY(cudaEventRecord(W.ev[2], s));
@@ -935,6 +918,7 @@ int fit_gram_columns_core(Workspace& W, const double* dX, int64_t n, int64_t p, 
     T.nz_rows = (int*)W.nz_rows.ptr; T.nz_vals = (double*)W.nz_vals.ptr;
     T.nz_count = (int*)W.nz_count.ptr; T.nz_cur = (int*)W.nz_cur.ptr;
     T.sigma_std = out.sigma_std; T.iters = out.iters; T.sweeps = out.sweeps; T.converged = out.conv;
+    set_prefetch(W, T);
     CUDA_TRY(launch_tail_sweeps(T, (int)std::min<int64_t>(W.sms, m), s));
     CUDA_TRY(cudaEventRecord(W.ev[6], s));
     CUDA_TRY(cudaEventRecord(W.ev[2], s));

@@ -79,6 +79,7 @@ __global__ void joint_compact_kernel(const int* __restrict__ act, const uint8_t*
   __shared__ int base_s;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   if (tid == 0) base_s = 0;
+  __syncwarp();
   __syncthreads();
   for (int off = 0; off < nact; off += blockDim.x) {
     const int q = off + tid;
@@ -91,12 +92,14 @@ __global__ void joint_compact_kernel(const int* __restrict__ act, const uint8_t*
     for (int w = 0; w < warp; ++w) wbase += wsum[w];
     const int base = base_s;
     if (f) act_out[base + wbase + pre] = act[q];
+    __syncwarp();
     __syncthreads();
     if (tid == 0) {
       int t = 0;
       for (int w = 0; w < nw; ++w) t += wsum[w];
       base_s = base + t;
     }
+    __syncwarp();
     __syncthreads();
   }
   if (tid == 0) *nact_out = base_s;

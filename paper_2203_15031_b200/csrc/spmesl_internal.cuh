@@ -118,6 +118,8 @@ struct TailParams {
   int* sweeps_count;       // sweeps performed here
   int z_from_gtab;         // 1: z starts as Gtab[:, col] (Gram solver: b = 0, r = x~_c)
   int gtab_full;           // 1: every Gram column is present (no on-demand path)
+  int prefetch;            // 1: stream the Gram columns of the current nonzeros into shared
+                           //    memory ahead of their visits (needs tail_prefetch_bytes more)
   int* flags;
   int* nz_rows;            // column coefficient lists (as in CDParams)
   double* nz_vals;
@@ -157,8 +159,10 @@ cudaError_t launch_gram_init(const GramParams& P, cudaStream_t s);
 int gram_tile_count(int64_t p);
 
 constexpr int TAIL_THREADS = 256;
+constexpr int TAIL_SCAN = 4 * TAIL_THREADS;   // rows tested per search round
 constexpr int TAIL_ODC = 8;          // on-demand Gram column cache entries per CTA
-size_t tail_smem_bytes(int p, int n_pad, int nzcap);
+__host__ __device__ size_t tail_smem_bytes(int p, int n_pad, int nzcap);
+size_t tail_prefetch_bytes(int p);
 cudaError_t launch_tail_residuals(const double* Xb, const TailState* tail, int M, const int* nz_rows,
                                   const double* nz_vals, int nzcap, int64_t col_begin, int n,
                                   int n_pad, int nchunk, double* V, cudaStream_t s);

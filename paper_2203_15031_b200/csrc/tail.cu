@@ -13,6 +13,13 @@
 // instead of O(p n).  The iterates are Algorithm 1's up to rounding; every operation is a fixed
 // function of the column (the Gram columns come from one DMMA routine, whether precomputed in
 // the batched pass or computed on demand), so results do not depend on scheduling.
+//
+// Gram-column prefetch (TailParams::prefetch, when two p-vectors fit in shared memory): the rows
+// of the column's current nonzeros are visited in order every sweep and almost every visit
+// changes b_j, so the Gram columns of the next two such rows are streamed L2 -> shared memory
+// by cp.async.bulk while the sweep proceeds; the z update then reads shared memory instead of
+// paying an L2 round trip per change (the straggler columns of hub graphs make hundreds of
+// sweeps with ~10 changes each).
 #include <cstdio>
 #include "spmesl_internal.cuh"
 
@@ -22,6 +29,45 @@ __device__ __forceinline__ void dmma_t(double& d0, double& d1, double a, double 
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
+}
+
+// Block barrier after reconverging the warp: __syncthreads() is the aligned bar.sync, which
+// needs all lanes of a warp to arrive together, and several call sites follow a block executed
+// by thread 0 alone (lanes 1-31 could otherwise reach the barrier first and release it early).
+__device__ __forceinline__ void bsync() {
+  __syncwarp();
+  __syncthreads();
+}
+
+__device__ __forceinline__ uint32_t smem_u32t(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init_t(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32t(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32t(bar)),
+      "r"(parity)
+      : "memory");
+}
+// (issued by one thread) Gram column j -> shared buffer, completion on bar
+__device__ __forceinline__ void prefetch_col(double* dst, const double* src, uint32_t bytes,
+                                             uint64_t* bar) {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32t(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32t(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32t(bar))
+      : "memory");
 }
 
 __device__ __forceinline__ double soft_t(double a, double lam) {
@@ -83,7 +129,7 @@ __device__ __forceinline__ void gram_tile(const double* Xb, int b, int nchunk, i
     for (int e = tid; e < CHUNK_DOUBLES / 2; e += blockDim.x) ((double2*)tx)[e] = src[e];
     for (int vr = warp; vr < 32; vr += blockDim.x >> 5)
       load_vec_chunk(tv, vr, vt * 32 + vr, q, lane, Xb, nchunk, V, M, U, nU, n_pad);
-    __syncthreads();
+    bsync();
     const double* xa = tx + (mt * 8 + g) * XS + 2 * t4;
 #pragma unroll
     for (int kp = 0; kp < KC / 8; ++kp) {
@@ -95,7 +141,7 @@ __device__ __forceinline__ void gram_tile(const double* Xb, int b, int nchunk, i
         dmma_t(acc[u][0], acc[u][1], a.y, bb.y);
       }
     }
-    __syncthreads();
+    bsync();
   }
   const double inv_n = 1.0 / (double)n;
   const int row = b * J + mt * 8 + g;
@@ -137,23 +183,27 @@ __global__ void tail_mark_kernel(const TailState* __restrict__ tail, int M, cons
 
 // ------------------------------------------------------------------ per-column sweeps
 struct TailShared {
+  uint64_t pf_bar[2];    // prefetch buffers' mbarriers
   double red[TAIL_THREADS / 32];
   int wmin[TAIL_THREADS / 32];
   int oc_var[TAIL_ODC];
   int oc_next;
   int k;
   int k2;
+  int pf_row[2];         // variable whose Gram column is (being) loaded into each buffer, or -1
 };
 
 // doubles: tiles [2][J*XS], z [p], r [n_pad], old/new list values [2][nzcap];
 // ints: old/new list rows [2][nzcap]; then TailShared (8-aligned)
-size_t tail_smem_bytes(int p, int n_pad, int nzcap) {
+__host__ __device__ size_t tail_smem_bytes(int p, int n_pad, int nzcap) {
   size_t b = ((size_t)2 * J * XS + p + n_pad + 2 * (size_t)nzcap) * 8;
   b += (size_t)2 * nzcap * 4;
   b = (b + 15) & ~(size_t)15;
   b += sizeof(TailShared);
   return (b + 127) & ~(size_t)127;
 }
+
+size_t tail_prefetch_bytes(int p) { return (((size_t)2 * p * 8) + 127) & ~(size_t)127; }
 
 // Gram column G[:, j] of the fit-wide table: precomputed, or computed here once (claim 0 -> 1,
 // write, publish 2) by the same DMMA routine as the batched pass; every CTA is resident, so
@@ -162,21 +212,21 @@ __device__ void ensure_gram_column(const TailParams& P, int j, TailShared& TS, d
                                    double* tvv) {
   if (P.gtab_full || *(volatile int*)&P.gstate[j] == 2) return;
   const int tid = threadIdx.x;
-  __syncthreads();
+  bsync();
   if (tid == 0) { TS.oc_var[0] = j; TS.k2 = atomicCAS(&P.gstate[j], 0, 1); }
-  __syncthreads();
+  bsync();
   if (TS.k2 == 0) {
     for (int b = 0; b < P.nblk; ++b)     // vector j alone in a tile: same DMMA chain
       gram_tile(P.Xb, b, P.nchunk, P.n, P.p, nullptr, 0, &TS.oc_var[0], 1, P.n_pad, 0, 1, tx,
                 tvv, nullptr, P.Gtab);
     __threadfence();
-    __syncthreads();
+    bsync();
     if (tid == 0) { atomicExch(&P.gstate[j], 2); atomicAdd(P.ondemand_count, 1); }
   } else if (tid == 0) {
     while (*(volatile int*)&P.gstate[j] != 2) __nanosleep(200);
   }
   __threadfence();
-  __syncthreads();
+  bsync();
 }
 
 __global__ void __launch_bounds__(TAIL_THREADS, 1) tail_sweep_kernel(const TailParams P) {
@@ -196,13 +246,38 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) tail_sweep_kernel(const TailP
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const size_t list_stride = (size_t)2 * nzcap;
   const int M = P.M_dev ? *(volatile const int*)P.M_dev : P.M;
+  // prefetch buffers [2][p] after the base layout (128-byte aligned)
+  double* gbuf = (double*)(sm + tail_smem_bytes(p, n_pad, nzcap));
+  const bool pf = P.prefetch != 0;
+  uint32_t pf_ph[2] = {0u, 0u};
   if (tid < TAIL_ODC) TS.oc_var[tid] = -1;
-  if (tid == 0) TS.oc_next = 0;
+  if (tid == 0) {
+    TS.oc_next = 0;
+    TS.pf_row[0] = TS.pf_row[1] = -1;
+    if (pf) {
+      mbar_init_t(&TS.pf_bar[0], 1);
+      mbar_init_t(&TS.pf_bar[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+  }
+  // (one thread) start loading the Gram column of old-list entry c into buffer c & 1
+  auto pf_issue = [&](int c, int cnt) {
+    if (c < cnt) {
+      const int jv = orow[c];
+      if (P.gtab_full || *(volatile int*)&P.gstate[jv] == 2) {
+        prefetch_col(gbuf + (size_t)(c & 1) * p, P.Gtab + (size_t)jv * p, (uint32_t)p * 8,
+                     &TS.pf_bar[c & 1]);
+        TS.pf_row[c & 1] = jv;
+        return;
+      }
+    }
+    TS.pf_row[c & 1] = -1;
+  };
 
   for (;;) {
-    __syncthreads();
+    bsync();
     if (tid == 0) TS.k = atomicAdd(P.next, 1);
-    __syncthreads();
+    bsync();
     const int k = TS.k;
     if (k >= M) break;
     const TailState ts = P.tail[k];
@@ -224,32 +299,59 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) tail_sweep_kernel(const TailP
       const size_t lo = (size_t)col * list_stride + (size_t)cur * nzcap;
       for (int m = tid; m < ocnt; m += TAIL_THREADS) { orow[m] = P.nz_rows[lo + m]; ov[m] = P.nz_vals[lo + m]; }
     }
-    __syncthreads();
+    bsync();
     bool retire = false;
     while (!retire) {
       // ------------------------------------------------ one sweep, rows in cyclic order
       const double lam = sigma * P.lambda0;
       double maxd = 0.0;
       int pos = 0, cursor = 0, ncnt = 0;
+      if (pf) {
+        if (tid == 0) { pf_issue(0, ocnt); pf_issue(1, ocnt); }
+        bsync();
+      }
       for (;;) {
         const int na = cursor < ocnt ? orow[cursor] : p;     // next row with b_j != 0
         // first row in [pos, na) with |z_j| > lambda (j != this column)
+        // (rounds of TAIL_SCAN rows: thread t tests rows base + t + TAIL_THREADS r, r < 4;
+        // the first hit is the block-wide minimum of the hit rows)
         int j = na;
-        for (int base = pos; base < na; base += TAIL_THREADS) {
-          const int jj = base + tid;
-          const bool hit = jj < na && jj != gc && fabs(z[jj]) > lam;
-          const unsigned m = __ballot_sync(0xffffffffu, hit);
-          if (lane == 0) TS.wmin[warp] = m ? base + warp * 32 + __ffs(m) - 1 : 0x7fffffff;
-          __syncthreads();
+        for (int base = pos; base < na; base += TAIL_SCAN) {
+          int my = 0x7fffffff;
+#pragma unroll
+          for (int r = 3; r >= 0; --r) {
+            const int jj = base + tid + r * TAIL_THREADS;
+            if (jj < na && jj != gc && fabs(z[jj]) > lam) my = jj;
+          }
+          my = __reduce_min_sync(0xffffffffu, my);
+          if (lane == 0) TS.wmin[warp] = my;
+          bsync();
           int best = 0x7fffffff;
 #pragma unroll
           for (int w = 0; w < TAIL_THREADS / 32; ++w) best = min(best, TS.wmin[w]);
-          __syncthreads();
+          bsync();
           if (best != 0x7fffffff) { j = best; break; }
         }
         if (j >= p) break;
         double bo = 0.0;
-        if (j == na) { bo = ov[cursor]; ++cursor; }
+        int pfb = -1;                 // prefetch buffer holding G[:, j], if any
+        int pf_next = -1;             // old-list entry to prefetch after this visit
+        if (j == na) {
+          bo = ov[cursor];
+          if (pf) {
+            const int b = cursor & 1;
+            if (TS.pf_row[b] == j) {   // consume the load (wait even if b_j does not change):
+              if (tid == 0) {          // the issuing thread waits, the barrier publishes it
+                mbar_wait_t(&TS.pf_bar[b], pf_ph[b]);
+                pf_ph[b] ^= 1u;
+              }
+              bsync();
+              pfb = b;
+            }
+            pf_next = cursor + 2;
+          }
+          ++cursor;
+        }
         const double a = z[j] + bo;
         const double bn = soft_t(a, lam);
         const double d = bo - bn;                             // e += x_j d
@@ -258,13 +360,32 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) tail_sweep_kernel(const TailP
           else overflow = true;
           ++ncnt;
         }
-        if (d != 0.0) {
+        if (d != 0.0 && pfb >= 0) {
+          maxd = fmax(maxd, fabs(d));
+          const double* gs = gbuf + (size_t)pfb * p;          // G[:, j] in shared memory
+          for (int t = tid; t < p; t += TAIL_THREADS) z[t] = fma(d, gs[t], z[t]);
+        } else if (d != 0.0) {
           maxd = fmax(maxd, fabs(d));
           const double* gcol = P.Gtab + (size_t)j * p;
           ensure_gram_column(P, j, TS, tx, tvv);
-          for (int t = tid; t < p; t += TAIL_THREADS) z[t] = fma(d, __ldcg(gcol + t), z[t]);
+          // (up to 16 independent L2 loads in flight per thread: one round trip per 4096 rows)
+          constexpr int UB = 16;
+          for (int t0 = 0; t0 < p; t0 += UB * TAIL_THREADS) {
+            double gv[UB];
+#pragma unroll
+            for (int u = 0; u < UB; ++u) {
+              const int t = t0 + u * TAIL_THREADS + tid;
+              gv[u] = t < p ? __ldcg(gcol + t) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < UB; ++u) {
+              const int t = t0 + u * TAIL_THREADS + tid;
+              if (t < p) z[t] = fma(d, gv[u], z[t]);
+            }
+          }
         }
-        __syncthreads();
+        bsync();
+        if (pf_next >= 0 && tid == 0) pf_issue(pf_next, ocnt);   // (buffer just released)
         pos = j + 1;
       }
       ++sweeps;
@@ -272,7 +393,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) tail_sweep_kernel(const TailP
       // the new list becomes the current one
       for (int m = tid; m < min(ncnt, nzcap); m += TAIL_THREADS) { orow[m] = nrow[m]; ov[m] = nv[m]; }
       ocnt = min(ncnt, nzcap);
-      __syncthreads();
+      bsync();
       if (maxd < P.tol || inner >= P.max_inner) {
         if (!(maxd < P.tol)) flags |= 2;
         // fresh residual and sigma (reading g4), warp 0 in the CD kernel's order
@@ -289,7 +410,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) tail_sweep_kernel(const TailP
           for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
           if (lane == 0) TS.red[0] = ss;
         }
-        __syncthreads();
+        bsync();
         double sn = sqrt(TS.red[0]) / P.sqrt_n;
         if (sn < P.sigma_floor) sn = P.sigma_floor;
         ++outer;
@@ -297,7 +418,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) tail_sweep_kernel(const TailP
         else if (outer >= P.max_outer) retire = true;
         sigma = sn;
         inner = 0;
-        __syncthreads();
+        bsync();
       }
     }
     // outputs: coefficients into the column's other list, per-column results
@@ -345,7 +466,8 @@ cudaError_t launch_tail_mark(const TailState* tail, int M, const int* nz_rows, i
 }
 
 cudaError_t launch_tail_sweeps(const TailParams& P, int grid, cudaStream_t s) {
-  const size_t smem = tail_smem_bytes(P.p, P.n_pad, P.nzcap);
+  size_t smem = tail_smem_bytes(P.p, P.n_pad, P.nzcap);
+  if (P.prefetch) smem += tail_prefetch_bytes(P.p);
   cudaError_t e = cudaFuncSetAttribute(tail_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
