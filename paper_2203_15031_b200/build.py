@@ -21,6 +21,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+# (development: extra -D switches for kernel variants, e.g. SPMESL_NVCC_EXTRA="-DSPMESL_SYRK_MIG=4")
+FLAGS += os.environ.get("SPMESL_NVCC_EXTRA", "").split()
 
 
 def _stale(out: str, deps) -> bool:

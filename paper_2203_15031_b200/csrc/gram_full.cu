@@ -73,11 +73,27 @@ __device__ __forceinline__ void dmma_g(double& d0, double& d1, double a, double 
 }
 
 constexpr int GB = 4;                  // 32-row blocks per tile side (tile = 128 x 128)
-constexpr int G_MMA_WARPS = 8;
-constexpr int G_THREADS = (G_MMA_WARPS + 1) * 32;
+#ifndef SPMESL_SYRK_WM
+#define SPMESL_SYRK_WM 8
+#endif
+constexpr int WM = SPMESL_SYRK_WM;     // 8-row m-tiles per warp (warp tile WM*8 x 32)
+constexpr int MR = 128 / (8 * WM);     // warp row groups per tile
+constexpr int G_MMA_WARPS = MR * 4;
+#ifndef SPMESL_SYRK_SMNR
+#define SPMESL_SYRK_SMNR 1
+#endif
+// With SMNR the producer is a whole warpgroup (warps G_MMA_WARPS .. +3, one lane working) that
+// gives registers back (setmaxnreg.dec) so the MMA warpgroups can hold their 64 accumulators,
+// fragments and addresses without spilling (setmaxnreg.inc): 8 x 232 + 4 x 40 registers.
+constexpr int G_PROD_WARPS = SPMESL_SYRK_SMNR ? 4 : 1;
+constexpr int G_THREADS = (G_MMA_WARPS + G_PROD_WARPS) * 32;
 constexpr int G_STAGE_DOUBLES = 2 * GB * CHUNK_DOUBLES;     // 8 Xb tiles = 64 KB
 constexpr int G_MAX_NST = 3;
-constexpr int G_ZPIECE = 2048;         // doubles per zero-fill bulk store (16 KB)
+constexpr int G_ZPIECE = 2048;
+#ifndef SPMESL_SYRK_MIG
+#define SPMESL_SYRK_MIG 2
+#endif
+constexpr int MI_G = SPMESL_SYRK_MIG;     // A fragments per DMMA group         // doubles per zero-fill bulk store (16 KB)
 
 // tile index t of the upper triangle (I <= J) of an nT x nT tile grid, row-major by I
 __device__ __forceinline__ void tri_tile(int t, int nT, int& I, int& Jt) {
@@ -110,9 +126,12 @@ __global__ void __launch_bounds__(G_THREADS, 1) syrk_screen_kernel(const GramPar
   }
   __syncthreads();
 
-  if (warp == G_MMA_WARPS) {
+  if (warp >= G_MMA_WARPS) {
     // ---------------------------------------------------------------- producer
-    if (lane == 0) {
+#if SPMESL_SYRK_SMNR
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+#endif
+    if (warp == G_MMA_WARPS && lane == 0) {
       int s = 0;
       uint32_t ph = 0;
       const uint64_t pol = l2_evict_last_policy();
@@ -158,9 +177,12 @@ __global__ void __launch_bounds__(G_THREADS, 1) syrk_screen_kernel(const GramPar
   }
 
   // ------------------------------------------------------------------ MMA warps
+#if SPMESL_SYRK_SMNR
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+#endif
   const int g = lane >> 2, t4 = lane & 3, sw = g & 1;
-  const int mh = warp & 1;          // rows [64 mh, 64 mh + 64) of the tile
-  const int nq = warp >> 1;         // cols [32 nq, 32 nq + 32)
+  const int mq = warp % MR;         // rows [8 WM mq, 8 WM (mq + 1)) of the tile
+  const int nq = warp / MR;         // cols [32 nq, 32 nq + 32)
   const double inv_n = 1.0 / (double)P.n;
   const double lam0 = P.lambda0;
   int s = 0;
@@ -169,15 +191,15 @@ __global__ void __launch_bounds__(G_THREADS, 1) syrk_screen_kernel(const GramPar
   for (int t = t_begin + blockIdx.x; t < t_end; t += gridDim.x) {
     int I, Jt;
     tri_tile(t, nT, I, Jt);
-    double acc[8][4][2];
+    double acc[WM][4][2];
 #pragma unroll
-    for (int mi = 0; mi < 8; ++mi)
+    for (int mi = 0; mi < WM; ++mi)
 #pragma unroll
       for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
     for (int q = 0; q < nchunk; ++q) {
       mbar_wait_g(&full[s], ph);
       const double* st = Xs + (size_t)s * G_STAGE_DOUBLES;
-      const double* abase = st + (size_t)(2 * mh) * CHUNK_DOUBLES + (size_t)g * XS + 2 * t4;
+      const double* abase = st + (size_t)g * XS + 2 * t4;
       const double* bbase = st + (size_t)(GB + nq) * CHUNK_DOUBLES + (size_t)g * XS + 2 * t4;
 #pragma unroll
       for (int kp = 0; kp < KC / 8; ++kp) {
@@ -186,14 +208,25 @@ __global__ void __launch_bounds__(G_THREADS, 1) syrk_screen_kernel(const GramPar
 #pragma unroll
         for (int ni = 0; ni < 4; ++ni) b[ni] = *(const double2*)(bbase + ni * 8 * XS + ko);
 #pragma unroll
-        for (int mi = 0; mi < 8; ++mi) {
-          // (one A fragment live at a time: 9 warps leave 168 registers per thread)
-          const double2 a = *(const double2*)(abase + (size_t)(mi >> 2) * CHUNK_DOUBLES +
-                                              (mi & 3) * 8 * XS + ko);
+        for (int m2 = 0; m2 < WM; m2 += MI_G) {
+          // (MI_G A fragments live at a time — 9 warps leave 168 registers per thread — and
+          // 4 MI_G DMMAs between two updates of the same accumulator)
+          double2 a[MI_G];
 #pragma unroll
-          for (int ni = 0; ni < 4; ++ni) dmma_g(acc[mi][ni][0], acc[mi][ni][1], a.x, b[ni].x);
+          for (int u = 0; u < MI_G; ++u) {
+            const int mt = mq * WM + m2 + u;          // m-tile within the 128-row tile
+            a[u] = *(const double2*)(abase + (size_t)(mt >> 2) * CHUNK_DOUBLES + (mt & 3) * 8 * XS + ko);
+          }
 #pragma unroll
-          for (int ni = 0; ni < 4; ++ni) dmma_g(acc[mi][ni][0], acc[mi][ni][1], a.y, b[ni].y);
+          for (int u = 0; u < MI_G; ++u)
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni)
+              dmma_g(acc[m2 + u][ni][0], acc[m2 + u][ni][1], a[u].x, b[ni].x);
+#pragma unroll
+          for (int u = 0; u < MI_G; ++u)
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni)
+              dmma_g(acc[m2 + u][ni][0], acc[m2 + u][ni][1], a[u].y, b[ni].y);
         }
       }
       __syncwarp();
@@ -202,13 +235,13 @@ __global__ void __launch_bounds__(G_THREADS, 1) syrk_screen_kernel(const GramPar
     }
     // epilogue: G = acc / n to both triangles; screening hits |G_jc| > lambda0 (j != c)
     const bool diag_tile = (I == Jt);
-    const int row0 = I * GB * J + 64 * mh;
+    const int row0 = I * GB * J + 8 * WM * mq;
     const int col0 = Jt * GB * J + 32 * nq;
     // stores are whole 32-byte sectors when p % 4 == 0 (8 lanes x 8 B down a column of G, or
     // 4 lanes x 16 B along a row for the mirror), so L2 never reads back partial sectors
     const bool vec = (p & 3) == 0;
 #pragma unroll
-    for (int mi = 0; mi < 8; ++mi) {
+    for (int mi = 0; mi < WM; ++mi) {
       const int row = row0 + mi * 8 + g;
 #pragma unroll
       for (int ni = 0; ni < 4; ++ni) {
