@@ -164,6 +164,22 @@ int spmesl_fit_columns_device(const double* dX, int64_t n, int64_t p, int64_t co
                               uint8_t* dConverged, void* cuda_stream, spmesl_stats* st);
 
 /*
+ * Several penalty levels in one call (a regularization path; SURVEY.md §8(f) f4's "batch the
+ * three lambda0 in one launch"), e.g. lambda_pb, lambda_univ, lambda_ub (SPMESL-P, -2,
+ * -4).  lambdas: HOST array of nlam (1..8) penalty levels.  Outputs are device arrays laid out
+ * level by level: dTheta[nlam][p x p] (each column-major), dSigma[nlam][p], dIters[nlam][p],
+ * dSweeps / dConverged (nullable) [nlam][p].  Level l's results are those of spmesl_fit_device
+ * with lambda0 = lambdas[l] (same iterates; with the Gram solver bit-identical): X~, S and the
+ * screening pass are computed once and shared by all levels.  Enqueued on cuda_stream; returns
+ * after one synchronisation.  Errors as spmesl_fit_device; SPMESL_ERR_ARG for nlam outside
+ * 1..8.
+ */
+int spmesl_fit_path_device(const double* dX, int64_t n, int64_t p, const double* lambdas,
+                           int32_t nlam, double tol, int32_t max_iter, const spmesl_options* opt,
+                           double* dTheta, double* dSigma, int32_t* dIters, int32_t* dSweeps,
+                           uint8_t* dConverged, void* cuda_stream, spmesl_stats* st);
+
+/*
  * Multi-GPU building blocks of the Gram solver (SURVEY.md §8(f) f2 + §8(e)).
  * The first sweep of column c with b_c = 0 changes coefficient j iff |x~_j^T x~_c / n| > lambda0
  * (sigma^(0) = 1); "screening" evaluates that test for all pairs (j, c) from the

@@ -22,7 +22,8 @@ from . import _lib
 from ._lib import SpmeslError, Stats, default_options, load  # noqa: F401
 
 __all__ = ["fit", "fit_device", "fit_columns_device", "assemble_device", "gram_tile_count",
-           "gram_screen_device", "fit_columns_gram_device", "gram_supported", "lambda_univ",
+           "gram_screen_device", "fit_columns_gram_device", "gram_supported", "fit_path_device",
+           "lambda_univ",
            "lambda_ub", "lambda_pb", "solve_k", "FitResult", "SpmeslError", "load",
            "release_workspace", "version"]
 
@@ -191,6 +192,37 @@ def fit_columns_gram_device(X, col_begin: int, col_end: int, lambda0: float, hit
     return dict(code=rc, counts=b["counts"], rows=b["rows"][:k], vals=b["vals"][:k],
                 sigma_std=b["sigma_std"], scale=b["scale"], iters=b["iters"],
                 sweeps=b["sweeps"], converged=b["conv"].bool(), stats=st.asdict())
+
+
+def fit_path_device(X, lambdas, tol: float = 1e-4, max_iter: int = 100, *, stream=None,
+                    **options) -> list:
+    """spmesl_fit_path_device: one fit per penalty level in `lambdas` (1..8 levels) sharing
+    X~, S = X~^T X~ / n and the screening pass.  Returns a list of FitResult (device tensors)."""
+    import torch
+    if not X.is_cuda or X.dtype != torch.float64:
+        raise TypeError("X must be a float64 CUDA tensor")
+    X = as_colmajor(X)
+    n, p = X.shape
+    lam = np.ascontiguousarray(np.asarray(lambdas, dtype=np.float64).ravel())
+    L = lam.size
+    dev = X.device
+    theta = torch.empty((L, p, p), dtype=torch.float64, device=dev)
+    sigma = torch.empty((L, p), dtype=torch.float64, device=dev)
+    iters = torch.empty((L, p), dtype=torch.int32, device=dev)
+    sweeps = torch.empty((L, p), dtype=torch.int32, device=dev)
+    conv = torch.empty((L, p), dtype=torch.uint8, device=dev)
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    st = Stats()
+    o = _opts(**options)
+    with torch.cuda.device(dev):
+        rc = load().spmesl_fit_path_device(_vp(X), n, p, _vp(lam), L, float(tol), int(max_iter),
+                                           ctypes.byref(o), _vp(theta), _vp(sigma), _vp(iters),
+                                           _vp(sweeps), _vp(conv), ctypes.c_void_p(s.cuda_stream),
+                                           ctypes.byref(st))
+    _lib.check(rc, st)
+    stats = st.asdict()
+    return [FitResult(rc, theta[l].t(), sigma[l], iters[l], sweeps[l], conv[l].bool(), stats)
+            for l in range(L)]
 
 
 def fit_columns_device(X, col_begin: int, col_end: int, lambda0: float, tol: float = 1e-4,

@@ -85,6 +85,7 @@ struct Workspace {
   Buffer tail, umark, umap, uvars, tailV, zall, ondemand;   // tail solver
   Buffer ej, act0, act1, keep, jflags;                      // mode 1 (Algorithm 3)
   Buffer hit;                                               // Gram solver screening flags
+  Buffer lam_dev;                                           // multi-lambda: penalty levels
   // host-API staging
   Buffer hx, htheta, hsigma, hiters, hsweeps, hconv, coo_r, coo_c, coo_v, hdiag, zeros;
   DevCounters* host_counters = nullptr;   // pinned
@@ -572,24 +573,32 @@ bool gram_applicable(const Workspace& W, const spmesl_options& o, int64_t n, int
 // the counters afterwards and checks err / overflow.
 int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, double lambda0,
                      double tol, int32_t max_iter, const spmesl_options& o, const FitOut& out,
-                     cudaStream_t s, Layout& L, int nzcap) {
+                     cudaStream_t s, Layout& L, int nzcap, const double* lams = nullptr,
+                     int nlam = 1) {
+  // nlam > 1: several penalty levels share X~, S and its screening pass (regularization path);
+  // the outputs of level l, column c sit at l p + c
   const int64_t m = p;
   set_layout(L, n, p);
-  int rc = alloc_core(W, L, m, nzcap);
+  int rc = alloc_core(W, L, m * nlam, nzcap);
   if (rc) return rc;
   if (tail_smem_bytes((int)p, L.n_pad, nzcap) > (size_t)W.smem_optin)
     return fail(SPMESL_ERR_UNSUPPORTED, "Gram solver: sweep state does not fit on chip");
   if ((rc = ensure(W.ondemand, (size_t)p * p * 8))) return rc;
-  if ((rc = ensure(W.hit, (size_t)p))) return rc;
+  if ((rc = ensure(W.hit, (size_t)p * nlam))) return rc;
+  if ((rc = ensure(W.lam_dev, (size_t)SPMESL_MAX_LAM * 8))) return rc;
   DevCounters* dc = (DevCounters*)W.counters.ptr;
-  if ((rc = run_prep(W, dX, m, o, L, s, /*band=*/false))) return rc;
-  CUDA_TRY(cudaMemsetAsync(W.hit.ptr, 0, (size_t)p, s));
+  if ((rc = run_prep(W, dX, m * nlam, o, L, s, /*band=*/false))) return rc;
+  CUDA_TRY(cudaMemsetAsync(W.hit.ptr, 0, (size_t)p * nlam, s));
+  if (nlam > 1)
+    CUDA_TRY(cudaMemcpyAsync(W.lam_dev.ptr, lams, (size_t)nlam * 8, cudaMemcpyHostToDevice, s));
   GramParams G{};
   G.Xb = (const double*)W.xb.ptr;
   G.n = (int)n; G.n_pad = L.n_pad; G.nchunk = L.nchunk; G.p = (int)p; G.nblk = (int)L.nblk;
   G.col_begin = 0;
   G.ncols = (int)m;
   G.lambda0 = lambda0; G.tol = tol; G.sigma_floor = o.sigma_floor; G.sqrt_n = std::sqrt((double)n);
+  G.nlam = nlam;
+  for (int l = 0; l < nlam; ++l) G.lams[l] = nlam > 1 ? lams[l] : lambda0;
   G.max_outer = max_iter;
   G.G = (double*)W.ondemand.ptr;
   G.hit = (uint8_t*)W.hit.ptr;
@@ -636,8 +645,9 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   T.nz_rows = (int*)W.nz_rows.ptr; T.nz_vals = (double*)W.nz_vals.ptr;
   T.nz_count = (int*)W.nz_count.ptr; T.nz_cur = (int*)W.nz_cur.ptr;
   T.sigma_std = out.sigma_std; T.iters = out.iters; T.sweeps = out.sweeps; T.converged = out.conv;
+  if (nlam > 1) { T.lambdas = (const double*)W.lam_dev.ptr; T.slot_stride = (int)p; }
   set_prefetch(W, T);
-  CUDA_TRY(launch_tail_sweeps(T, (int)std::min<int64_t>(W.sms, p), s));
+  CUDA_TRY(launch_tail_sweeps(T, (int)std::min<int64_t>(W.sms, p * nlam), s));
   CUDA_TRY(cudaEventRecord(W.ev[6], s));
   CUDA_TRY(cudaEventRecord(W.ev[2], s));
   return SPMESL_OK;
@@ -886,6 +896,8 @@ int fit_gram_columns_core(Workspace& W, const double* dX, int64_t n, int64_t p, 
     G.col_begin = cb;
     G.ncols = (int)m;
     G.lambda0 = lambda0; G.tol = tol; G.sigma_floor = o.sigma_floor; G.sqrt_n = std::sqrt((double)n);
+    G.nlam = 1;
+    G.lams[0] = lambda0;
     G.max_outer = max_iter;
     G.G = nullptr;
     G.hit = const_cast<uint8_t*>(dHit);
@@ -1013,6 +1025,102 @@ int spmesl_fit_device(const double* dX, int64_t n, int64_t p, double lambda0, do
   if (W->cc_major < 10) return fail(SPMESL_ERR_UNSUPPORTED, "needs an sm_100 device");
   return fit_device_impl(dX, n, p, lambda0, tol, max_iter, o, dTheta, dSigma, dIters, dSweeps,
                          dConverged, (cudaStream_t)cuda_stream, st, *W);
+}
+
+int spmesl_fit_path_device(const double* dX, int64_t n, int64_t p, const double* lambdas,
+                           int32_t nlam, double tol, int32_t max_iter, const spmesl_options* opt,
+                           double* dTheta, double* dSigma, int32_t* dIters, int32_t* dSweeps,
+                           uint8_t* dConverged, void* cuda_stream, spmesl_stats* st) {
+  init_stats(st);
+  spmesl_options o = resolve(opt);
+  if (!lambdas || nlam < 1 || nlam > SPMESL_MAX_LAM)
+    return fail(SPMESL_ERR_ARG, "nlam must be 1..8 and lambdas non-NULL");
+  int rc;
+  for (int l = 0; l < nlam; ++l)
+    if ((rc = validate(dX, n, p, lambdas[l], tol, max_iter, o))) return rc;
+  if (!dTheta || !dSigma || !dIters) return fail(SPMESL_ERR_ARG, "output pointer is NULL");
+  int dev;
+  if ((rc = current_device(-1, &dev))) return rc;
+  Workspace* W = workspace_for(dev);
+  std::lock_guard<std::mutex> lk(W->mu);
+  if ((rc = ws_init(*W, dev))) return rc;
+  if (W->cc_major < 10) return fail(SPMESL_ERR_UNSUPPORTED, "needs an sm_100 device");
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  const size_t pp = (size_t)p * (size_t)p;
+  std::string why;
+  const bool gram = o.mode == 0 && o.solver != 1 && gram_applicable(*W, o, n, p, 0, p, &why);
+  if (!gram) {
+    // (no shared pass to exploit: one fit per level)
+    int worst = SPMESL_OK;
+    for (int l = 0; l < nlam; ++l) {
+      spmesl_stats sl;
+      init_stats(&sl);
+      rc = fit_device_impl(dX, n, p, lambdas[l], tol, max_iter, o, dTheta + l * pp, dSigma + l * p,
+                           dIters + l * p, dSweeps ? dSweeps + l * p : nullptr,
+                           dConverged ? dConverged + l * p : nullptr, s, &sl, *W);
+      if (rc < 0) return rc;
+      worst = std::max(worst, rc);
+      if (st) { st->coord_updates += sl.coord_updates; st->total_sweeps += sl.total_sweeps;
+                st->ms_total += sl.ms_total; st->solver = sl.solver; }
+    }
+    return worst;
+  }
+  const int64_t m = p * nlam;
+  if ((rc = ensure(W->sigma_std, (size_t)m * 8))) return rc;
+  if (!dSweeps) { if ((rc = ensure(W->sweeps, (size_t)m * 4))) return rc; dSweeps = (int32_t*)W->sweeps.ptr; }
+  if (!dConverged) { if ((rc = ensure(W->conv, (size_t)m))) return rc; dConverged = (uint8_t*)W->conv.ptr; }
+  FitOut out{0, p, (double*)W->sigma_std.ptr, dIters, dSweeps, dConverged};
+  Layout L;
+  int nzcap = initial_nzcap(n, p);
+  DevCounters* dc = nullptr;
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    const bool take = (((uintptr_t)dTheta & 15) == 0) && ((pp * nlam) & 1) == 0;
+    if (take) { W->take_zero = dTheta; W->take_count = pp * nlam; }
+    else { W->pending_zero = dTheta; W->pending_count = pp * nlam; }
+    rc = fit_gram_enqueue(*W, dX, n, p, lambdas[0], tol, max_iter, o, out, s, L, nzcap, lambdas,
+                          nlam);
+    W->take_zero = nullptr;
+    if (W->pending_zero) { W->pending_zero = nullptr; if (!rc) rc = fail(SPMESL_ERR_CUDA, "internal"); }
+    if (rc) { if (!take) cudaStreamWaitEvent(s, W->ev_join, 0); return rc; }
+    if (!take) CUDA_TRY(cudaStreamWaitEvent(s, W->ev_join, 0));
+    const size_t cap = (size_t)p * (size_t)nzcap;
+    if ((rc = ensure(W->csc_rows, cap * 4))) return rc;
+    if ((rc = ensure(W->csc_vals, cap * 8))) return rc;
+    dc = (DevCounters*)W->counters.ptr;
+    CUDA_TRY(cudaEventRecord(W->ev[3], s));
+    for (int l = 0; l < nlam; ++l) {   // CSC + assembly of each level (stream-ordered reuse)
+      const size_t lo = (size_t)l * p;
+      CUDA_TRY(launch_csc_build((const int*)W->nz_count.ptr + lo, (const int*)W->nz_cur.ptr + lo,
+                                (const int*)W->nz_rows.ptr + lo * 2 * nzcap,
+                                (const double*)W->nz_vals.ptr + lo * 2 * nzcap, (int)p, nzcap,
+                                (int64_t*)W->col_ptr.ptr, (int32_t*)W->csc_rows.ptr,
+                                (double*)W->csc_vals.ptr, &dc->csc_total, s));
+      CUDA_TRY(launch_assemble(p, 0, p, (const int64_t*)W->col_ptr.ptr,
+                               (const int32_t*)W->csc_rows.ptr, (const double*)W->csc_vals.ptr,
+                               (const double*)W->sigma_std.ptr + lo,
+                               o.standardize ? (const double*)W->scale.ptr : nullptr, o.symmetrize,
+                               dTheta + l * pp, dSigma + lo, s, /*zero_fill=*/false));
+    }
+    CUDA_TRY(cudaEventRecord(W->ev[4], s));
+    if ((rc = device_stats(*W, dIters, dSweeps, dConverged, m, s))) return rc;
+    if ((rc = read_counters(*W, s))) return rc;
+    if (W->host_counters->err) return std_error(*W, st);
+    if (!W->host_counters->overflow) break;
+    if (nzcap >= p) return fail(SPMESL_ERR_OOM, "coefficient list overflow");
+    nzcap = (int)std::min<int64_t>(p, (int64_t)nzcap * 4);
+  }
+  int any_unconv = 0;
+  stats_from_counters(*W->host_counters, p, st, &any_unconv);
+  if (st) {
+    gram_stats(*W, p, nzcap, st);
+    st->ms_standardize = ev_ms(W->ev[0], W->ev[1]);
+    st->ms_cd = ev_ms(W->ev[1], W->ev[2]);
+    st->ms_assemble = ev_ms(W->ev[3], W->ev[4]);
+    st->ms_total = ev_ms(W->ev[0], W->ev[4]);
+    st->kernel_launches += 2 + 3 * nlam;
+    st->bad_column = -1;
+  }
+  return any_unconv ? SPMESL_WARN_NOT_CONVERGED : SPMESL_OK;
 }
 
 int spmesl_fit_ex(const double* X, int64_t n, int64_t p, double lambda0, double tol,
@@ -1246,6 +1354,8 @@ int spmesl_gram_screen_device(const double* dX, int64_t n, int64_t p, double lam
   G.Xb = (const double*)W->xb.ptr;
   G.n = (int)n; G.n_pad = L.n_pad; G.nchunk = L.nchunk; G.p = (int)p; G.nblk = (int)L.nblk;
   G.lambda0 = lambda0;
+  G.nlam = 1;
+  G.lams[0] = lambda0;
   G.G = nullptr;
   G.hit = dHit;
   G.tile_begin = (int)tile_begin;

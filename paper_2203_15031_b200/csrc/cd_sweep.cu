@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
             const int k = atomicAdd(P.tail_count, 1);
             TailState ts;
             ts.col = col; ts.outer = outer; ts.sweeps = S.sweeps[c]; ts.inner = inner;
-            ts.flags = flags; ts.cur = cur; ts.cnt = cnt; ts.sigma = sigma;
+            ts.flags = flags; ts.cur = cur; ts.cnt = cnt; ts.lam = 0; ts.sigma = sigma;
             P.tail[k] = ts;
             retire = 1;
           } else if (retire) {

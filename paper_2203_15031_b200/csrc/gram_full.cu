@@ -184,7 +184,8 @@ __global__ void __launch_bounds__(G_THREADS, 1) syrk_screen_kernel(const GramPar
   const int mq = warp % MR;         // rows [8 WM mq, 8 WM (mq + 1)) of the tile
   const int nq = warp / MR;         // cols [32 nq, 32 nq + 32)
   const double inv_n = 1.0 / (double)P.n;
-  const double lam0 = P.lambda0;
+  double lam0 = P.lams[0];
+  for (int l = 1; l < P.nlam; ++l) lam0 = fmin(lam0, P.lams[l]);
   int s = 0;
   uint32_t ph = 0;
   double* const Gout = P.G;
@@ -269,8 +270,12 @@ __global__ void __launch_bounds__(G_THREADS, 1) syrk_screen_kernel(const GramPar
           const int col = colp + e;
           const double v = e ? v1 : v0;
           if (row < p && col < p && row != col && fabs(v) > lam0) {
-            P.hit[col] = 1;
-            if (!diag_tile) P.hit[row] = 1;
+            // (lam0 = the smallest level: no other level can hit where it does not)
+            for (int l = 0; l < P.nlam; ++l)
+              if (fabs(v) > P.lams[l]) {
+                P.hit[(size_t)l * p + col] = 1;
+                if (!diag_tile) P.hit[(size_t)l * p + row] = 1;
+              }
           }
         }
       }
@@ -284,13 +289,15 @@ __global__ void __launch_bounds__(G_THREADS, 1) syrk_screen_kernel(const GramPar
 // kernel like every column with a hit.
 __global__ void gram_init_kernel(const GramParams P) {
   const int lane = threadIdx.x & 31;
-  const int c = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
-  if (c >= P.ncols) return;
+  const int q = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
+  if (q >= P.ncols * P.nlam) return;
+  const int l = q / P.ncols, c = q - l * P.ncols;                // penalty level, column
+  const int slot = l * P.ncols + c;                              // output index
   const int64_t gc = P.col_begin + c;
   TailState ts;
   ts.col = c; ts.outer = 0; ts.sweeps = 0; ts.inner = 0; ts.flags = 0; ts.cur = 0; ts.cnt = 0;
-  ts.pad = 0; ts.sigma = 1.0;
-  if (!P.hit[gc]) {
+  ts.lam = l; ts.sigma = 1.0;
+  if (!P.hit[(size_t)l * P.p + gc]) {
     double ss = 0.0;
     for (int i = lane; i < P.n; i += 32) {
       const double r = P.Xb[xb_index(i, gc, P.nchunk)];
@@ -303,12 +310,12 @@ __global__ void gram_init_kernel(const GramParams P) {
     if (lane == 0) {
       const bool conv = fabs(sn - 1.0) < P.tol;
       if (conv || P.max_outer <= 1) {
-        P.sigma_std[c] = sn;
-        P.iters[c] = 1;
-        P.sweeps[c] = 1;
-        P.converged[c] = (uint8_t)conv;
-        P.nz_count[c] = 0;
-        P.nz_cur[c] = 0;
+        P.sigma_std[slot] = sn;
+        P.iters[slot] = 1;
+        P.sweeps[slot] = 1;
+        P.converged[slot] = (uint8_t)conv;
+        P.nz_count[slot] = 0;
+        P.nz_cur[slot] = 0;
         return;
       }
       ts.outer = 1; ts.sweeps = 1; ts.sigma = sn;
@@ -343,7 +350,8 @@ cudaError_t launch_syrk_screen(const GramParams& P, int grid, cudaStream_t s) {
 cudaError_t launch_gram_init(const GramParams& P, cudaStream_t s) {
   if (P.ncols <= 0) return cudaSuccess;
   const int wpb = 8;
-  gram_init_kernel<<<(P.ncols + wpb - 1) / wpb, wpb * 32, 0, s>>>(P);
+  const int w = P.ncols * P.nlam;
+  gram_init_kernel<<<(w + wpb - 1) / wpb, wpb * 32, 0, s>>>(P);
   return cudaGetLastError();
 }
 

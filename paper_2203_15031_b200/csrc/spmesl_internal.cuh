@@ -50,6 +50,8 @@ enum : int { FLAG_CODE = 0, FLAG_OVERFLOW = 1 };
 
 // State of a column handed from the CD kernel to the tail solver at a sweep boundary
 // (coefficients stay in the column's list `cur` with `cnt` entries).
+constexpr int SPMESL_MAX_LAM = 8;
+
 struct TailState {
   int col;        // local column index
   int outer;      // outer iterations completed
@@ -57,7 +59,7 @@ struct TailState {
   int inner;      // sweeps completed in the current outer iteration
   int flags;      // bit1: an inner loop hit max_inner
   int cur, cnt;   // current coefficient list
-  int pad;
+  int lam;        // penalty index (multi-lambda fits; 0 otherwise)
   double sigma;   // current sigma (lambda = sigma lambda0)
 };
 
@@ -107,6 +109,8 @@ struct TailParams {
   double lambda0, tol, sigma_floor, sqrt_n;
   int max_outer, max_inner;
   int nzcap;
+  const double* lambdas;   // multi-lambda fits: lambda0 of TailState::lam (nullptr: lambda0)
+  int slot_stride;         // multi-lambda fits: outputs of (lam, col) at lam * slot_stride + col
   int M;                   // tail columns (or, if M_dev != nullptr, *M_dev at kernel start)
   const int* M_dev;
   const TailState* tail;   // [M]
@@ -140,7 +144,9 @@ struct GramParams {
   int max_outer;
   int nst;
   double* G;               // [p][p] column-major (nullptr: screening only)
-  uint8_t* hit;            // [p] column has some |G_jc| > lambda0, j != c
+  uint8_t* hit;            // [nlam][p] column has some |G_jc| > lambda0_l, j != c
+  int nlam;                // penalty levels screened / fitted together (1..SPMESL_MAX_LAM)
+  double lams[8];          // their lambda0 values
   int tile_begin, tile_end;   // upper-triangle tiles to process (multi-GPU share)
   double* zero_ptr;        // optional: zero-filled by the producer's bulk stores (Theta)
   size_t zero_count;       // doubles (even; zero_ptr 16-byte aligned)

@@ -281,8 +281,9 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) tail_sweep_kernel(const TailP
     const int k = TS.k;
     if (k >= M) break;
     const TailState ts = P.tail[k];
-    const int col = ts.col;
-    const int gc = (int)(P.col_begin + col);
+    const int col = ts.lam * P.slot_stride + ts.col;         // lists / outputs index
+    const int gc = (int)(P.col_begin + ts.col);              // the variable itself
+    const double lambda0 = P.lambdas ? P.lambdas[ts.lam] : P.lambda0;
     double sigma = ts.sigma;
     int outer = ts.outer, sweeps = ts.sweeps, inner = ts.inner, flags = ts.flags;
     int cur = ts.cur;
@@ -303,7 +304,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) tail_sweep_kernel(const TailP
     bool retire = false;
     while (!retire) {
       // ------------------------------------------------ one sweep, rows in cyclic order
-      const double lam = sigma * P.lambda0;
+      const double lam = sigma * lambda0;
       double maxd = 0.0;
       int pos = 0, cursor = 0, ncnt = 0;
       if (pf) {

@@ -324,3 +324,27 @@ def test_gram_building_blocks_reproduce_full_fit(S, oracle):
     assert np.array_equal(it, full.iters) and np.array_equal(sw, full.sweeps)
     assert np.array_equal(so.cpu().numpy(), full.sigma)
     assert np.array_equal(th.cpu().numpy(), full.Theta)
+
+
+@pytest.mark.parametrize("solver", ["gram", "residual"])
+def test_penalty_path_equals_single_fits(S, oracle, solver):
+    """spmesl_fit_path_device: lambda_pb, lambda_univ, lambda_ub (SPMESL-P/-2/-4, P:1133) in
+    one call; every level equals its own single fit (bit for bit with the Gram solver) and the
+    oracle."""
+    import torch
+    X, _, _ = G.make_config(2, p=300, n=150)
+    n, p = X.shape
+    lams = [oracle.lambda_pb(n, p), oracle.lambda_univ(n, p), oracle.lambda_ub(n, p)]
+    Xd = torch.from_numpy(np.ascontiguousarray(X.T)).cuda().t()
+    res = S.fit_path_device(Xd, lams, solver=solver)
+    for lam, r in zip(lams, res):
+        one = S.fit_device(Xd, lam, solver=solver)
+        assert torch.equal(r.Theta, one.Theta) and torch.equal(r.sigma, one.sigma)
+        assert torch.equal(r.sweeps, one.sweeps) and torch.equal(r.iters, one.iters)
+        ora = oracle.spmesl_fit(X, lam)
+        assert_parity(compare(r.Theta.cpu().numpy(), r.sigma.cpu().numpy(),
+                              r.iters.cpu().numpy(), r.sweeps.cpu().numpy(), ora))
+    # levels are independent of their order in the call
+    rev = S.fit_path_device(Xd, lams[::-1], solver=solver)
+    for a, b in zip(res, rev[::-1]):
+        assert torch.equal(a.Theta, b.Theta)
