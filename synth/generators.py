@@ -147,6 +147,29 @@ def _hub_edges(m: int, rng, n_hubs: int = 10) -> np.ndarray:
     return e
 
 
+def _sf_edges(m: int, rng, alpha: float = 2.3, kmax: int = 8) -> np.ndarray:
+    """Scale-free block: Barabasi-Albert growth, one edge per new node (a tree:
+    m - 1 edges, so |E| = 495 at p = 500 as in the paper's Table 4), attachment probability
+    proportional to k + a with a = alpha - 3 (linear preferential attachment with offset gives
+    P(k) ~ k^-(3 + a), i.e. the paper's alpha = 2.3).  Reading i3: degrees are
+    capped at kmax = 8 — with the weights of P:1045-1062 a node of degree d whose neighbours
+    are leaves gets couplings ~1/3, and the block stays positive definite only while d / 9 < 1
+    (the paper does not say how it obtained positive-definite scale-free matrices)."""
+    a = alpha - 3.0
+    deg = np.zeros(m, dtype=np.float64)
+    edges = []
+    if m >= 2:
+        edges.append((0, 1))
+        deg[0] = deg[1] = 1.0
+    for v in range(2, m):
+        w = np.where(deg[:v] < kmax, deg[:v] + a, 0.0)
+        u = int(rng.choice(v, p=w / w.sum()))
+        edges.append((min(u, v), max(u, v)))
+        deg[u] += 1.0
+        deg[v] += 1.0
+    return np.array(edges, dtype=np.int64).reshape(-1, 2)
+
+
 def _block_family(p: int, kind: str, seed: int, floor: float, block: int, edge_fn) -> GroundTruth:
     blocks = []
     off = 0
@@ -170,6 +193,10 @@ def _block_family(p: int, kind: str, seed: int, floor: float, block: int, edge_f
 
 def er(p: int, d: float = 10.0, seed: int = 0, floor: float = 0.1, block: int = 100) -> GroundTruth:
     return _block_family(p, f"er{d:g}", seed, floor, block, lambda m, rng: _er_edges(m, d, rng))
+
+
+def scale_free(p: int, seed: int = 0, floor: float = 0.1, block: int = 100) -> GroundTruth:
+    return _block_family(p, "sf", seed, floor, block, lambda m, rng: _sf_edges(m, rng))
 
 
 def hub(p: int, seed: int = 0, floor: float = 0.1, block: int = 100) -> GroundTruth:
@@ -227,6 +254,8 @@ def make_truth(family: str, p: int, seed: int) -> GroundTruth:
         return band(p, 4)
     if family == "hub":
         return hub(p, seed=seed)
+    if family == "sf":
+        return scale_free(p, seed=seed)
     if family == "er":
         return er(p, 10.0, seed=seed)
     raise ValueError(family)

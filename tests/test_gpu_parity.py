@@ -348,3 +348,14 @@ def test_penalty_path_equals_single_fits(S, oracle, solver):
     rev = S.fit_path_device(Xd, lams[::-1], solver=solver)
     for a, b in zip(res, rev[::-1]):
         assert torch.equal(a.Theta, b.Theta)
+
+
+def test_estimation_workload_ar1_matches_paper_band(S):
+    """f4: the estimation workload (one penalty-path fit per dataset, three levels) on the
+    paper's AR(1) setting (p = 500, n = 250): SPMESL-4 recovers every edge with FDR near the
+    paper's 1.07 % (Table 3); SPMESL-P has the most false discoveries."""
+    from workloads.estimation import run
+    r = run(reps=2, networks=["ar1_paper"])["ar1_paper"]
+    assert r["SPMESL-4"]["SEN"] == 100.0 and r["SPMESL-4"]["FDR"] <= 4.0
+    assert r["SPMESL-P"]["FDR"] > r["SPMESL-2"]["FDR"] > r["SPMESL-4"]["FDR"]
+    assert r["SPMESL-P"]["Frob"] < r["SPMESL-4"]["Frob"]
