@@ -5,6 +5,7 @@
 //   memset scratch -> standardize_kernel (a2) -> gram_kernel -> cd_sweep_kernel (a3-a7)
 //   -> csc_scan + csc_copy -> memset Theta + assemble_entries + assemble_diag (a8, a10)
 //   -> one 64-byte readback of flags/counters.
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1142,6 +1143,12 @@ int spmesl_fit_ex(const double* X, int64_t n, int64_t p, double lambda0, double 
   // computes — by the copy engine (D2H of a device zero buffer, when Theta is pinned) and by host
   // threads, in parallel; only the nonzero entries (COO) and the diagonal cross PCIe afterwards.
   size_t dma_elems = 0;
+  const bool e2e_dbg = getenv("SPMESL_E2E_DEBUG") != nullptr;
+  auto now_ms = [] {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
+  const double t_start = now_ms();
+  const double dma_frac = getenv("SPMESL_E2E_DMA") ? atof(getenv("SPMESL_E2E_DMA")) : 0.3;
   {
     cudaPointerAttributes pa;
     const bool pinned = cudaPointerGetAttributes(&pa, Theta) == cudaSuccess &&
@@ -1150,7 +1157,7 @@ int spmesl_fit_ex(const double* X, int64_t n, int64_t p, double lambda0, double 
     const size_t zbytes = (size_t)64 << 20;
     if (pinned && pp * 8 >= ((size_t)256 << 20) && ensure(W->zeros, zbytes) == SPMESL_OK) {
       if (cudaMemsetAsync(W->zeros.ptr, 0, zbytes, W->side) == cudaSuccess) {
-        dma_elems = (size_t)(0.3 * (double)pp);
+        dma_elems = (size_t)(dma_frac * (double)pp);
         for (size_t off = 0; off < dma_elems; off += zbytes / 8) {
           const size_t cnt = std::min(zbytes / 8, dma_elems - off);
           if (cudaMemcpyAsync(Theta + off, W->zeros.ptr, cnt * 8, cudaMemcpyDeviceToHost, W->side) !=
@@ -1167,16 +1174,20 @@ int spmesl_fit_ex(const double* X, int64_t n, int64_t p, double lambda0, double 
   {
     const size_t rest = pp - dma_elems;
     const unsigned hc = std::max(1u, std::thread::hardware_concurrency());
-    const size_t nth = std::min<size_t>(std::min(16u, hc), std::max<size_t>(1, rest >> 20));
+    const unsigned cap_th = getenv("SPMESL_E2E_THREADS") ? (unsigned)atoi(getenv("SPMESL_E2E_THREADS")) : 16u;
+    const size_t nth = std::min<size_t>(std::min(cap_th, hc), std::max<size_t>(1, rest >> 20));
     const size_t per = (rest + nth - 1) / nth;
     for (size_t t = 0; t < nth; ++t) {
       const size_t lo = dma_elems + t * per, hi = std::min(pp, lo + per);
       if (lo < hi) zero.emplace_back([=] { std::memset(Theta + lo, 0, (hi - lo) * sizeof(double)); });
     }
   }
+  double t_threads = 0, t_dma = 0;
   auto join = [&] {
     for (auto& th : zero) if (th.joinable()) th.join();
+    t_threads = now_ms();
     if (dma_elems) cudaStreamSynchronize(W->side);
+    t_dma = now_ms();
   };
   auto bail = [&](int code) { join(); return code; };
   if ((rc = ensure(W->hx, np * 8))) return bail(rc);
@@ -1252,9 +1263,13 @@ int spmesl_fit_ex(const double* X, int64_t n, int64_t p, double lambda0, double 
     return bail(rc);
   if ((rc = read_counters(*W, s))) return bail(rc);
   stats_from_counters(*W->host_counters, p, st, &any_unconv);
+  const double t_dev = now_ms();
   join();
   for (int e = 0; e < ncoo; ++e) Theta[(size_t)cc[e] * p + cr[e]] = cv[e];
   for (int64_t k = 0; k < p; ++k) Theta[(size_t)k * p + k] = diag[k];
+  if (e2e_dbg)
+    fprintf(stderr, "[e2e] device done %.2f ms, zero threads %.2f ms, dma %.2f ms, end %.2f ms\n",
+            t_dev - t_start, t_threads - t_start, t_dma - t_start, now_ms() - t_start);
   if (st) {
     st->nnz = W->host_counters->csc_total;
     st->ms_standardize = ev_ms(W->ev[0], W->ev[1]);
