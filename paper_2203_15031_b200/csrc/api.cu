@@ -600,6 +600,10 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   G.lambda0 = lambda0; G.tol = tol; G.sigma_floor = o.sigma_floor; G.sqrt_n = std::sqrt((double)n);
   G.nlam = nlam;
   for (int l = 0; l < nlam; ++l) G.lams[l] = nlam > 1 ? lams[l] : lambda0;
+  if (nlam > 1) {   // the Gram kernel screens at the smallest level (a superset of all hits)
+    G.lambda0 = G.lams[0];
+    for (int l = 1; l < nlam; ++l) G.lambda0 = std::min(G.lambda0, G.lams[l]);
+  }
   G.max_outer = max_iter;
   G.G = (double*)W.ondemand.ptr;
   G.hit = (uint8_t*)W.hit.ptr;
@@ -620,6 +624,7 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   const int ntiles = nT * (nT + 1) / 2;
   CUDA_TRY(launch_syrk_screen(G, std::min(W.sms, ntiles), s));
   CUDA_TRY(cudaEventRecord(W.ev[7], s));
+  if (nlam > 1) CUDA_TRY(launch_level_flags(G, s));
   CUDA_TRY(launch_gram_init(G, s));
   CUDA_TRY(cudaEventRecord(W.ev[5], s));
   // the sweep kernel reads the number of columns with hits from the device counter (no host

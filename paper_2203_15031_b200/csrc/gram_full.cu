@@ -184,8 +184,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) syrk_screen_kernel(const GramPar
   const int mq = warp % MR;         // rows [8 WM mq, 8 WM (mq + 1)) of the tile
   const int nq = warp / MR;         // cols [32 nq, 32 nq + 32)
   const double inv_n = 1.0 / (double)P.n;
-  double lam0 = P.lams[0];
-  for (int l = 1; l < P.nlam; ++l) lam0 = fmin(lam0, P.lams[l]);
+  const double lam0 = P.lambda0;   // (multi-level fits: the smallest level; see level_flags)
   int s = 0;
   uint32_t ph = 0;
   double* const Gout = P.G;
@@ -270,17 +269,30 @@ __global__ void __launch_bounds__(G_THREADS, 1) syrk_screen_kernel(const GramPar
           const int col = colp + e;
           const double v = e ? v1 : v0;
           if (row < p && col < p && row != col && fabs(v) > lam0) {
-            // (lam0 = the smallest level: no other level can hit where it does not)
-            for (int l = 0; l < P.nlam; ++l)
-              if (fabs(v) > P.lams[l]) {
-                P.hit[(size_t)l * p + col] = 1;
-                if (!diag_tile) P.hit[(size_t)l * p + row] = 1;
-              }
+            P.hit[col] = 1;
+            if (!diag_tile) P.hit[row] = 1;
           }
         }
       }
     }
   }
+}
+
+// Multi-level fits: the screening flags of every level (hit[l][c] = max_{j != c} |S_jc| >
+// lambda_l), from the stored S (one warp per column, coalesced); the Gram kernel's epilogue
+// screens at the smallest level only.
+__global__ void level_flags_kernel(const GramParams P) {
+  const int lane = threadIdx.x & 31;
+  const int c = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
+  if (c >= P.p) return;
+  const double* col = P.G + (size_t)c * P.p;
+  double m = 0.0;
+  for (int j = lane; j < P.p; j += 32)
+    if (j != c) m = fmax(m, fabs(col[j]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0)
+    for (int l = 0; l < P.nlam; ++l) P.hit[(size_t)l * P.p + c] = (uint8_t)(m > P.lams[l]);
 }
 
 // Columns without a screening hit: the first sweep changes nothing (b stays 0, max|db| = 0),
@@ -344,6 +356,12 @@ cudaError_t launch_syrk_screen(const GramParams& P, int grid, cudaStream_t s) {
                                        (int)smem);
   if (e != cudaSuccess) return e;
   syrk_screen_kernel<<<grid, G_THREADS, smem, s>>>(Q);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_level_flags(const GramParams& P, cudaStream_t s) {
+  const int wpb = 8;
+  level_flags_kernel<<<(P.p + wpb - 1) / wpb, wpb * 32, 0, s>>>(P);
   return cudaGetLastError();
 }
 

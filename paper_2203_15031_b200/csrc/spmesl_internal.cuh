@@ -162,6 +162,7 @@ struct GramParams {
 size_t syrk_smem_bytes(int nst);
 cudaError_t launch_syrk_screen(const GramParams& P, int grid, cudaStream_t s);
 cudaError_t launch_gram_init(const GramParams& P, cudaStream_t s);
+cudaError_t launch_level_flags(const GramParams& P, cudaStream_t s);
 int gram_tile_count(int64_t p);
 
 constexpr int TAIL_THREADS = 256;
