@@ -359,3 +359,29 @@ def test_estimation_workload_ar1_matches_paper_band(S):
     assert r["SPMESL-4"]["SEN"] == 100.0 and r["SPMESL-4"]["FDR"] <= 4.0
     assert r["SPMESL-P"]["FDR"] > r["SPMESL-2"]["FDR"] > r["SPMESL-4"]["FDR"]
     assert r["SPMESL-P"]["Frob"] < r["SPMESL-4"]["Frob"]
+
+
+@pytest.mark.parametrize("family", ["band3", "hub"])
+def test_full_size_config4_slowest_columns(S, oracle, family):
+    """BASELINE config 4 at full size (n = 400, p = 5000; band(3) and hub): the 6 columns that
+    needed the most sweeps (the stragglers, up to ~490 sweeps for hub graphs) and 10 random ones
+    are solved one by one by the oracle; counts identical, sigma and Theta_1 within tolerance."""
+    X, _, spec = G.make_config(4, family=family)
+    n, p = X.shape
+    lam = oracle.lambda_ub(n, p)
+    r = S.fit(X, lam, symmetrize=False)
+    rng = np.random.default_rng(1)
+    slow = np.argsort(-r.sweeps)[:6]
+    cols = np.unique(np.concatenate([slow, rng.choice(p, 10, replace=False)]))
+    Xs, mu, s = oracle.standardize(X)
+    oc = oracle.spmesl_columns(Xs, cols, lam, want_margin=False)
+    assert r.sweeps[slow].max() == oc.sweeps.max() and r.sweeps[slow].min() > 10
+    assert np.array_equal(r.iters[cols], oc.outer) and np.array_equal(r.sweeps[cols], oc.sweeps)
+    np.testing.assert_allclose(r.sigma[cols], oc.sigma * s[cols], rtol=1e-10)
+    for c, k in enumerate(cols):
+        w = 1.0 / (oc.sigma[c] * oc.sigma[c])
+        want = -oc.B[:, c] * w
+        want[k] = w
+        want = want / (s * s[k])
+        got = r.Theta[:, k]
+        assert np.all(np.abs(got - want) <= 1e-8 * np.abs(want) + 1e-12 * abs(want[k])), k
