@@ -73,14 +73,19 @@ typedef struct {
   int32_t tail_after;     /* columns still running after this many sweeps finish in the
                              covariance-update tail solver (default 1; 0: never).  Same
                              iterates up to rounding. */
-  int32_t solver;         /* 0 (default): auto — the Gram solver when mode = 0, the whole
-                             column range is fitted on one device, p is at most ~26000 (the
-                             sweep kernel keeps z[p] on chip) and 8 p^2 bytes fit in device
-                             memory; else the residual solver.  1: residual solver (persistent
-                             CD kernel on X~ streamed through shared memory).  2: Gram solver
-                             (S = X~^T X~ / n by a symmetric DMMA contraction with fused
-                             first-sweep screening, then covariance updates; SPMESL_ERR_UNSUPPORTED
-                             where it does not apply).  Same iterates up to rounding. */
+  int32_t solver;         /* 0 (default): auto — solver 3 when mode = 0, the whole column range
+                             is fitted on one device, p is at most ~26000 (the sweep kernel
+                             keeps z[p] on chip) and 8 p^2 bytes fit in device memory; else
+                             the residual solver.  1: residual solver (persistent CD kernel on
+                             X~ streamed through shared memory).  2: Gram solver with the full
+                             S = X~^T X~ / n (symmetric FP64 DMMA contraction, first-sweep
+                             screening fused in), then covariance updates.  3: Gram solver with
+                             certified f16 screening: the first-sweep test |S_jc| > lambda0 is
+                             decided on the f16 tensor cores with a rigorous error bound; only
+                             the columns it cannot certify get exact FP64 Gram columns (and
+                             their exact test), the others are known to stop after one sweep.
+                             2 and 3: SPMESL_ERR_UNSUPPORTED where they do not apply.  All
+                             solvers: same iterates up to FP64 rounding. */
   int32_t reserved[7];
 } spmesl_options;
 
@@ -105,7 +110,10 @@ typedef struct {
   int64_t tail_sweeps;    /* sweeps performed by the tail solver (the CD kernel did the rest) */
   int32_t solver;         /* solver used: 1 residual, 2 Gram */
   int32_t pad0;
-  double  ms_gram;        /* Gram solver: device time of the symmetric Gram + screening kernel */
+  double  ms_gram;        /* Gram solver: device time of the screening pass (solver 2: the FP64
+                             Gram kernel; solver 3: f16 screening + exact Gram columns of the
+                             candidates) */
+  int64_t screen_candidates; /* solver 3: columns the f16 screening could not certify hit-free */
 } spmesl_stats;
 
 /* Fill *opt with the defaults listed above. */

@@ -48,7 +48,7 @@ def _vp(a) -> ctypes.c_void_p:
 
 
 MODES = {"per_column": 0, "joint": 1}
-SOLVERS = {"auto": 0, "residual": 1, "gram": 2}
+SOLVERS = {"auto": 0, "residual": 1, "gram": 2, "gram16": 3}
 
 
 def _opts(max_inner=10000, standardize=True, symmetrize=True, sigma_floor=1e-8, tile_cols=0,

@@ -60,6 +60,7 @@ class Stats(ctypes.Structure):
         ("solver", ctypes.c_int32),
         ("pad0", ctypes.c_int32),
         ("ms_gram", ctypes.c_double),
+        ("screen_candidates", ctypes.c_int64),
     ]
 
     def asdict(self):

@@ -14,7 +14,7 @@ CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libspmesl.so")
 
-SOURCES = ["prep.cu", "cd_sweep.cu", "tail.cu", "joint.cu", "gram_full.cu", "assemble.cu", "api.cu", "penalty.cpp"]
+SOURCES = ["prep.cu", "cd_sweep.cu", "tail.cu", "joint.cu", "gram_full.cu", "screen16.cu", "assemble.cu", "api.cu", "penalty.cpp"]
 HEADERS = [os.path.join(CSRC, "spmesl_internal.cuh"), os.path.join(ROOT, "include", "spmesl.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -87,6 +87,7 @@ struct Workspace {
   Buffer ej, act0, act1, keep, jflags;                      // mode 1 (Algorithm 3)
   Buffer hit;                                               // Gram solver screening flags
   Buffer lam_dev;                                           // multi-lambda: penalty levels
+  Buffer nrm, sq, y16, cand;                                // certified f16 screening
   // host-API staging
   Buffer hx, htheta, hsigma, hiters, hsweeps, hconv, coo_r, coo_c, coo_v, hdiag, zeros;
   DevCounters* host_counters = nullptr;   // pinned
@@ -97,6 +98,9 @@ struct Workspace {
   size_t pending_count = 0;
   double* take_zero = nullptr;            // Theta the Gram kernel may zero-fill itself
   size_t take_count = 0;
+  std::vector<double> lam_host;           // (pinned-free staging of the penalty levels)
+  std::vector<uint8_t> cand_host;         // certified screening: candidate flags
+  int last_candidates = 0;
   bool init = false;
 };
 
@@ -139,7 +143,7 @@ int validate(const void* X, int64_t n, int64_t p, double lambda0, double tol, in
   if (o.max_inner < 1) return fail(SPMESL_ERR_ARG, "max_inner must be >= 1");
   if (!(o.sigma_floor > 0.0)) return fail(SPMESL_ERR_ARG, "sigma_floor must be > 0");
   if (o.mode != 0 && o.mode != 1) return fail(SPMESL_ERR_ARG, "mode must be 0 (per-column stop) or 1 (Algorithm 3 joint stop)");
-  if (o.solver < 0 || o.solver > 2) return fail(SPMESL_ERR_ARG, "solver must be 0, 1 or 2");
+  if (o.solver < 0 || o.solver > 3) return fail(SPMESL_ERR_ARG, "solver must be 0, 1, 2 or 3");
   if (o.tile_cols != 0 && o.tile_cols != 8 && o.tile_cols != 16 && o.tile_cols != 32)
     return fail(SPMESL_ERR_ARG, "tile_cols must be 0, 8, 16 or 32");
   const double pp = (double)p * (double)p * 8.0;
@@ -277,7 +281,8 @@ int run_prep(Workspace& W, const double* dX, int64_t m, const spmesl_options& o,
   CUDA_TRY(cudaEventRecord(W.ev[0], s));
   DevCounters* dc = (DevCounters*)W.counters.ptr;
   CUDA_TRY(launch_standardize(dX, L, o.standardize, (double*)W.xb.ptr, (double*)W.mean.ptr,
-                              (double*)W.scale.ptr, &dc->err, &dc->bad_key, s));
+                              (double*)W.scale.ptr, &dc->err, &dc->bad_key, s,
+                              W.nrm.bytes >= (size_t)L.p * 8 ? (double*)W.nrm.ptr : nullptr));
   if (band) CUDA_TRY(launch_gram((const double*)W.xb.ptr, L, (double*)W.gband.ptr, s));
   CUDA_TRY(cudaEventRecord(W.ev[1], s));
   if (W.pending_zero) {
@@ -575,7 +580,7 @@ bool gram_applicable(const Workspace& W, const spmesl_options& o, int64_t n, int
 int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, double lambda0,
                      double tol, int32_t max_iter, const spmesl_options& o, const FitOut& out,
                      cudaStream_t s, Layout& L, int nzcap, const double* lams = nullptr,
-                     int nlam = 1) {
+                     int nlam = 1, bool screen16 = false) {
   // nlam > 1: several penalty levels share X~, S and its screening pass (regularization path);
   // the outputs of level l, column c sit at l p + c
   const int64_t m = p;
@@ -587,11 +592,24 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   if ((rc = ensure(W.ondemand, (size_t)p * p * 8))) return rc;
   if ((rc = ensure(W.hit, (size_t)p * nlam))) return rc;
   if ((rc = ensure(W.lam_dev, (size_t)SPMESL_MAX_LAM * 8))) return rc;
+  if (screen16) {
+    if ((rc = ensure(W.nrm, (size_t)p * 8))) return rc;
+    if ((rc = ensure(W.sq, (size_t)p * 8))) return rc;
+    if ((rc = ensure(W.y16, screen16_y_halves(p, L.n_pad) * 2))) return rc;
+    if ((rc = ensure(W.cand, (size_t)p))) return rc;
+    if ((rc = ensure(W.umap, (size_t)p * 4))) return rc;
+    if ((rc = ensure(W.uvars, (size_t)p * 4))) return rc;
+  }
   DevCounters* dc = (DevCounters*)W.counters.ptr;
   if ((rc = run_prep(W, dX, m * nlam, o, L, s, /*band=*/false))) return rc;
   CUDA_TRY(cudaMemsetAsync(W.hit.ptr, 0, (size_t)p * nlam, s));
-  if (nlam > 1)
-    CUDA_TRY(cudaMemcpyAsync(W.lam_dev.ptr, lams, (size_t)nlam * 8, cudaMemcpyHostToDevice, s));
+  {
+    double lv[SPMESL_MAX_LAM];
+    for (int l = 0; l < nlam; ++l) lv[l] = nlam > 1 ? lams[l] : lambda0;
+    W.lam_host.assign(lv, lv + nlam);
+    CUDA_TRY(cudaMemcpyAsync(W.lam_dev.ptr, W.lam_host.data(), (size_t)nlam * 8,
+                             cudaMemcpyHostToDevice, s));
+  }
   GramParams G{};
   G.Xb = (const double*)W.xb.ptr;
   G.n = (int)n; G.n_pad = L.n_pad; G.nchunk = L.nchunk; G.p = (int)p; G.nblk = (int)L.nblk;
@@ -620,11 +638,63 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   G.sigma_std = out.sigma_std; G.iters = out.iters; G.sweeps = out.sweeps;
   G.converged = out.conv;
   G.nz_count = (int*)W.nz_count.ptr; G.nz_cur = (int*)W.nz_cur.ptr;
-  const int nT = (int)((L.nblk + 3) / 4);
-  const int ntiles = nT * (nT + 1) / 2;
-  CUDA_TRY(launch_syrk_screen(G, std::min(W.sms, ntiles), s));
-  CUDA_TRY(cudaEventRecord(W.ev[7], s));
-  if (nlam > 1) CUDA_TRY(launch_level_flags(G, s));
+  bool full_gram = !screen16;
+  if (screen16) {
+    // certified f16 screening (screen16.cu): candidate columns, then their exact FP64 Gram
+    // columns and the exact decision; one host round trip for the candidate list
+    CUDA_TRY(launch_sqrt((const double*)W.nrm.ptr, (double*)W.sq.ptr, (int)p, s));
+    CUDA_TRY(launch_to_f16((const double*)W.xb.ptr, (const double*)W.nrm.ptr, (int)p, L.n_pad,
+                           L.nchunk, (__half*)W.y16.ptr, s));
+    CUDA_TRY(cudaMemsetAsync(W.cand.ptr, 0, (size_t)p, s));
+    Screen16Params Q{};
+    Q.Y16 = (const __half*)W.y16.ptr;
+    Q.sq = (const double*)W.sq.ptr;
+    Q.p = (int)p; Q.n = (int)n;
+    Q.ntb = (int)((p + 127) / 128);
+    Q.nchunk64 = (L.n_pad + 63) / 64;
+    Q.tile_begin = 0;
+    Q.tile_end = screen16_tile_count(p);
+    Q.lambda0 = G.lambda0;
+    Q.eps = screen16_eps(L.n_pad);
+    Q.cand = (uint8_t*)W.cand.ptr;
+    Q.zero_ptr = G.zero_ptr;
+    Q.zero_count = G.zero_count;
+    CUDA_TRY(launch_screen16(Q, std::min(W.sms, Q.tile_end), s));
+    W.cand_host.resize(p);
+    CUDA_TRY(cudaMemcpyAsync(W.cand_host.data(), W.cand.ptr, (size_t)p, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    std::vector<int> U;
+    std::vector<int> gstate(p, 0);
+    for (int64_t c = 0; c < p; ++c)
+      if (W.cand_host[c]) { U.push_back((int)c); gstate[c] = 2; }
+    const int nU = (int)U.size();
+    W.last_candidates = nU;
+    if (2 * (int64_t)nU > p) {
+      // most columns are candidates (multi-sweep workloads): the symmetric FP64 Gram kernel
+      // (n p (p+1) flops) is cheaper than nU exact columns (2 n p nU); it decides exactly
+      full_gram = true;
+      G.zero_ptr = nullptr;            // (Theta was zero-filled by the screening pass)
+      const int nT = (int)((L.nblk + 3) / 4);
+      const int ntiles = nT * (nT + 1) / 2;
+      CUDA_TRY(launch_syrk_screen(G, std::min(W.sms, ntiles), s));
+      if (nlam > 1) CUDA_TRY(launch_level_flags(G, s));
+    } else {
+      CUDA_TRY(cudaMemcpyAsync(W.umap.ptr, gstate.data(), (size_t)p * 4, cudaMemcpyHostToDevice, s));
+      if (nU) CUDA_TRY(cudaMemcpyAsync(W.uvars.ptr, U.data(), (size_t)nU * 4, cudaMemcpyHostToDevice, s));
+      CUDA_TRY(launch_gram_pass((const double*)W.xb.ptr, (int)L.nblk, L.nchunk, (int)n, (int)p,
+                                nullptr, 0, (const int*)W.uvars.ptr, nU, nullptr,
+                                (double*)W.ondemand.ptr, s));
+      CUDA_TRY(launch_exact_hits((const double*)W.ondemand.ptr, (int)p, (const int*)W.uvars.ptr,
+                                 nU, (const double*)W.lam_dev.ptr, nlam, (uint8_t*)W.hit.ptr, s));
+    }
+    CUDA_TRY(cudaEventRecord(W.ev[7], s));
+  } else {
+    const int nT = (int)((L.nblk + 3) / 4);
+    const int ntiles = nT * (nT + 1) / 2;
+    CUDA_TRY(launch_syrk_screen(G, std::min(W.sms, ntiles), s));
+    CUDA_TRY(cudaEventRecord(W.ev[7], s));
+    if (nlam > 1) CUDA_TRY(launch_level_flags(G, s));
+  }
   CUDA_TRY(launch_gram_init(G, s));
   CUDA_TRY(cudaEventRecord(W.ev[5], s));
   // the sweep kernel reads the number of columns with hits from the device counter (no host
@@ -641,9 +711,9 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   T.tail = (const TailState*)W.tail.ptr;
   T.Zz = nullptr;
   T.Gtab = (double*)W.ondemand.ptr;
-  T.gstate = nullptr;
+  T.gstate = full_gram ? nullptr : (int*)W.umap.ptr;
   T.z_from_gtab = 1;
-  T.gtab_full = 1;
+  T.gtab_full = full_gram ? 1 : 0;
   T.next = &dc->tail_next;
   T.ondemand_count = &dc->gram_ondemand;
   T.sweeps_count = &dc->tail_sweeps;
@@ -659,11 +729,12 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   return SPMESL_OK;
 }
 
-void gram_stats(Workspace& W, int64_t p, int nzcap, spmesl_stats* st) {
+void gram_stats(Workspace& W, int64_t p, int nzcap, spmesl_stats* st, bool screen16 = false) {
   (void)nzcap;
   if (!st) return;
   const int nT = (int)((((p + J - 1) / J) + 3) / 4);
-  st->solver = 2;
+  st->solver = screen16 ? 3 : 2;
+  if (screen16) st->screen_candidates = W.last_candidates;
   st->tile_cols = 0;
   st->num_ctas = std::min(W.sms, nT * (nT + 1) / 2);
   st->kernel_launches += 3;
@@ -680,12 +751,13 @@ int fit_gram_core(Workspace& W, const double* dX, int64_t n, int64_t p, double l
                   spmesl_stats* st, Layout& L, int* nzcap_used) {
   int nzcap = initial_nzcap(n, p);
   for (int attempt = 0; attempt < 4; ++attempt) {
-    int rc = fit_gram_enqueue(W, dX, n, p, lambda0, tol, max_iter, o, out, s, L, nzcap);
+    int rc = fit_gram_enqueue(W, dX, n, p, lambda0, tol, max_iter, o, out, s, L, nzcap, nullptr, 1,
+                              o.solver != 2);
     if (rc) return rc;
     if ((rc = read_counters(W, s))) return rc;
     if (W.host_counters->err) return std_error(W, st);
     if (!W.host_counters->overflow) {
-      gram_stats(W, p, nzcap, st);
+      gram_stats(W, p, nzcap, st, o.solver != 2);
       *nzcap_used = nzcap;
       return SPMESL_OK;
     }
@@ -707,7 +779,7 @@ int fit_columns_core(Workspace& W, const double* dX, int64_t n, int64_t p, int64
   {
     std::string why;
     const bool ok = gram_applicable(W, o, n, p, cb, ce, &why);
-    if (o.solver == 2 && !ok) return fail(SPMESL_ERR_UNSUPPORTED, "solver = 2: " + why);
+    if ((o.solver == 2 || o.solver == 3) && !ok) return fail(SPMESL_ERR_UNSUPPORTED, "Gram solver: " + why);
     if (ok && o.solver != 1)
       return fit_gram_core(W, dX, n, p, lambda0, tol, max_iter, o, out, s, st, L, nzcap_used);
   }
@@ -758,7 +830,8 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
   int nzcap = 0;
   std::string why;
   const bool gram_ok = gram_applicable(W, o, n, p, 0, p, &why);
-  if (o.solver == 2 && !gram_ok) return fail(SPMESL_ERR_UNSUPPORTED, "solver = 2: " + why);
+  if ((o.solver == 2 || o.solver == 3) && !gram_ok)
+    return fail(SPMESL_ERR_UNSUPPORTED, "Gram solver: " + why);
   const bool gram = gram_ok && o.solver != 1 && o.mode == 0;
   // zero-fill Theta (8 p^2 bytes, the only dense pass) on a side stream while the solver runs
   // (launched by run_prep right after standardization; joined before the assembly)
@@ -773,7 +846,8 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
     if (gram) {
       // everything is enqueued; the one host synchronisation is the counter read at the end
       if (!nzcap) nzcap = initial_nzcap(n, p);
-      rc = fit_gram_enqueue(W, dX, n, p, lambda0, tol, max_iter, o, out, s, L, nzcap);
+      rc = fit_gram_enqueue(W, dX, n, p, lambda0, tol, max_iter, o, out, s, L, nzcap, nullptr, 1,
+                            o.solver != 2);
     } else {
       rc = fit_columns_core(W, dX, n, p, 0, p, lambda0, tol, max_iter, o, out, s, st, L, &nzcap);
     }
@@ -803,7 +877,7 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
     if ((rc = read_counters(W, s))) return rc;
     if (!gram) break;
     if (W.host_counters->err) return std_error(W, st);
-    if (!W.host_counters->overflow) { gram_stats(W, p, nzcap, st); break; }
+    if (!W.host_counters->overflow) { gram_stats(W, p, nzcap, st, o.solver != 2); break; }
     if (nzcap >= p) return fail(SPMESL_ERR_OOM, "coefficient list overflow");
     nzcap = (int)std::min<int64_t>(p, (int64_t)nzcap * 4);
     // (Theta's zero fill is redone at the top of the loop: the assembly above wrote into it)
@@ -1084,7 +1158,7 @@ int spmesl_fit_path_device(const double* dX, int64_t n, int64_t p, const double*
     if (take) { W->take_zero = dTheta; W->take_count = pp * nlam; }
     else { W->pending_zero = dTheta; W->pending_count = pp * nlam; }
     rc = fit_gram_enqueue(*W, dX, n, p, lambdas[0], tol, max_iter, o, out, s, L, nzcap, lambdas,
-                          nlam);
+                          nlam, o.solver != 2);
     W->take_zero = nullptr;
     if (W->pending_zero) { W->pending_zero = nullptr; if (!rc) rc = fail(SPMESL_ERR_CUDA, "internal"); }
     if (rc) { if (!take) cudaStreamWaitEvent(s, W->ev_join, 0); return rc; }
@@ -1118,7 +1192,7 @@ int spmesl_fit_path_device(const double* dX, int64_t n, int64_t p, const double*
   int any_unconv = 0;
   stats_from_counters(*W->host_counters, p, st, &any_unconv);
   if (st) {
-    gram_stats(*W, p, nzcap, st);
+    gram_stats(*W, p, nzcap, st, o.solver != 2);
     st->ms_standardize = ev_ms(W->ev[0], W->ev[1]);
     st->ms_cd = ev_ms(W->ev[1], W->ev[2]);
     st->ms_assemble = ev_ms(W->ev[3], W->ev[4]);

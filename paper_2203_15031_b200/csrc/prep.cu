@@ -22,7 +22,8 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 __global__ void standardize_kernel(const double* __restrict__ X, int64_t n, int64_t p, int nchunk,
                                    int standardize, double* __restrict__ Xb, double* mu,
-                                   double* scale, int* err, unsigned long long* bad_key) {
+                                   double* scale, int* err, unsigned long long* bad_key,
+                                   double* nrm) {
   const int lane = threadIdx.x & 31;
   const int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (k >= p) return;
@@ -59,10 +60,14 @@ __global__ void standardize_kernel(const double* __restrict__ X, int64_t n, int6
     }
   }
   if (lane == 0) { mu[k] = m; scale[k] = s; }
+  double g = 0.0;
   for (int64_t i = lane; i < n; i += 32) {
     double v = standardize ? (x[i] - m) / s : x[i];
     Xb[xb_index(i, k, nchunk)] = v;
+    g = fma(v, v, g);
   }
+  g = warp_sum(g);
+  if (lane == 0 && nrm) nrm[k] = g / (double)n;     // N_k = x~_k^T x~_k / n (= S_kk)
 }
 
 // D(8x8) += A(8x4) B(4x8) in fp64 on the tensor cores (fragment layout: see cd_sweep.cu)
@@ -120,11 +125,11 @@ __global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ Xb
 
 cudaError_t launch_standardize(const double* X, const Layout& L, int standardize, double* Xb,
                                double* mu, double* scale, int* err, unsigned long long* bad_key,
-                               cudaStream_t s) {
+                               cudaStream_t s, double* nrm) {
   const int wpb = 8;
   dim3 grid((unsigned)((L.p + wpb - 1) / wpb));
   standardize_kernel<<<grid, wpb * 32, 0, s>>>(X, L.n, L.p, L.nchunk, standardize, Xb, mu, scale,
-                                               err, bad_key);
+                                               err, bad_key, nrm);
   return cudaGetLastError();
 }
 

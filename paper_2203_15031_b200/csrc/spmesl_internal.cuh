@@ -11,6 +11,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
 
 namespace spmesl {
 
@@ -160,6 +161,27 @@ struct GramParams {
   int* nz_cur;
 };
 size_t syrk_smem_bytes(int nst);
+
+// Certified f16 screening (screen16.cu)
+struct Screen16Params {
+  const __half* Y16;       // normalized f16 tiles
+  const double* sq;        // [p] sqrt(N_k)
+  int p, n, ntb, nchunk64;
+  int tile_begin, tile_end;
+  double lambda0, eps;
+  uint8_t* cand;           // [p] column may have a hit (must be checked exactly)
+  double* zero_ptr;        // optional Theta zero fill (as GramParams)
+  size_t zero_count;
+};
+size_t screen16_y_halves(int64_t p, int n_pad);
+int screen16_tile_count(int64_t p);
+double screen16_eps(int n_pad);
+cudaError_t launch_to_f16(const double* Xb, const double* nrm, int p, int n_pad, int nchunk32,
+                          __half* Y16, cudaStream_t s);
+cudaError_t launch_screen16(const Screen16Params& P, int grid, cudaStream_t s);
+cudaError_t launch_exact_hits(const double* Gtab, int p, const int* U, int nU, const double* lams,
+                              int nlam, uint8_t* hit, cudaStream_t s);
+cudaError_t launch_sqrt(const double* in, double* out, int p, cudaStream_t s);
 cudaError_t launch_syrk_screen(const GramParams& P, int grid, cudaStream_t s);
 cudaError_t launch_gram_init(const GramParams& P, cudaStream_t s);
 cudaError_t launch_level_flags(const GramParams& P, cudaStream_t s);
@@ -197,7 +219,7 @@ int cd_stages(int T, int n_pad, size_t smem_optin);  // stages that fit (0: does
 // Launchers (stream-ordered, no host synchronisation).
 cudaError_t launch_standardize(const double* X, const Layout& L, int standardize, double* Xb,
                                double* mu, double* scale, int* err, unsigned long long* bad_col,
-                               cudaStream_t s);
+                               cudaStream_t s, double* nrm = nullptr);
 cudaError_t launch_gram(const double* Xb, const Layout& L, double* Gband, cudaStream_t s);
 cudaError_t launch_cd(const CDParams& P, int num_ctas, cudaStream_t s);
 cudaError_t launch_csc_build(const int* nz_count, const int* nz_cur, const int* nz_rows,

@@ -42,14 +42,14 @@ CASES = [
 
 @pytest.mark.parametrize("cfg,over,rule", CASES)
 @pytest.mark.parametrize("delta", [1e-4, 1e-10])
-@pytest.mark.parametrize("solver", ["residual", "gram"])
+@pytest.mark.parametrize("solver", ["residual", "gram", "gram16"])
 def test_parity_host_api(S, oracle, cfg, over, rule, delta, solver):
     X, gt, spec = G.make_config(cfg, **over)
     n, p = X.shape
     lam = _lam(oracle, rule, n, p)
     ora = oracle.spmesl_fit(X, lam, delta=delta)
     res = S.fit(X, lam, tol=delta, max_iter=100, solver=solver)
-    assert res.stats["solver"] == {"residual": 1, "gram": 2}[solver]
+    assert res.stats["solver"] == {"residual": 1, "gram": 2, "gram16": 3}[solver]
     rep = compare(res.Theta, res.sigma, res.iters, res.sweeps, ora)
     print(cfg, over, rule, delta, rep)
     assert_parity(rep)
@@ -167,7 +167,7 @@ def test_max_iter_cap_flags_columns(S, oracle, solver):
     assert_parity(compare(r.Theta, r.sigma, r.iters, r.sweeps, ora))
 
 
-@pytest.mark.parametrize("solver", ["residual", "gram"])
+@pytest.mark.parametrize("solver", ["residual", "gram", "gram16"])
 def test_full_size_config5_sampled_columns(S, oracle, solver):
     """BASELINE config 5 at full size (n=500, p=20000) in the bench's launch configuration;
     the oracle solves a sample of columns one by one (each column is independent): random
@@ -385,3 +385,26 @@ def test_full_size_config4_slowest_columns(S, oracle, family):
         want = want / (s * s[k])
         got = r.Theta[:, k]
         assert np.all(np.abs(got - want) <= 1e-8 * np.abs(want) + 1e-12 * abs(want[k])), k
+
+
+def test_certified_screening_equals_full_gram(S):
+    """solver 3 (f16 screening certified by an error bound + exact FP64 Gram columns of the
+    candidates) gives bit-identical results to solver 2 (the full FP64 S) — the low-precision
+    pass only decides which columns need no exact work — on screening-dominated (ER) and
+    multi-sweep (band, hub) workloads, including the penalty path."""
+    import torch
+    for cfg, over in [(5, dict(p=6000)), (4, dict(p=1500)), (4, dict(p=1500, family="hub")),
+                      (3, {})]:
+        X, _, spec = G.make_config(cfg, **over)
+        n, p = X.shape
+        Xd = torch.from_numpy(np.ascontiguousarray(X.T)).cuda().t()
+        lam = S.lambda_ub(n, p)
+        a = S.fit_device(Xd, lam, solver="gram")
+        b = S.fit_device(Xd, lam, solver="gram16")
+        assert b.stats["solver"] == 3 and b.stats["screen_candidates"] >= b.stats["tail_columns"] - 0
+        assert torch.equal(a.Theta, b.Theta) and torch.equal(a.sweeps, b.sweeps)
+        lams = [S.lambda_pb(n, p), S.lambda_univ(n, p), lam]
+        pa = S.fit_path_device(Xd, lams, solver="gram")
+        pb = S.fit_path_device(Xd, lams, solver="gram16")
+        for x, y in zip(pa, pb):
+            assert torch.equal(x.Theta, y.Theta) and torch.equal(x.sweeps, y.sweeps)
