@@ -594,7 +594,7 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   if ((rc = ensure(W.lam_dev, (size_t)SPMESL_MAX_LAM * 8))) return rc;
   if (screen16) {
     if ((rc = ensure(W.nrm, (size_t)p * 8))) return rc;
-    if ((rc = ensure(W.sq, (size_t)p * 8))) return rc;
+    if ((rc = ensure(W.sq, (size_t)p * 16))) return rc;   // sq (f64) + inv_sq, lam_sq (f32)
     if ((rc = ensure(W.y16, screen16_y_halves(p, L.n_pad) * 2))) return rc;
     if ((rc = ensure(W.cand, (size_t)p))) return rc;
     if ((rc = ensure(W.umap, (size_t)p * 4))) return rc;
@@ -642,13 +642,17 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   if (screen16) {
     // certified f16 screening (screen16.cu): candidate columns, then their exact FP64 Gram
     // columns and the exact decision; one host round trip for the candidate list
-    CUDA_TRY(launch_sqrt((const double*)W.nrm.ptr, (double*)W.sq.ptr, (int)p, s));
+    CUDA_TRY(launch_sqrt((const double*)W.nrm.ptr, (double*)W.sq.ptr,
+                         (float*)((double*)W.sq.ptr + p), (float*)((double*)W.sq.ptr + p) + p,
+                         G.lambda0, (int)p, s));
     CUDA_TRY(launch_to_f16((const double*)W.xb.ptr, (const double*)W.nrm.ptr, (int)p, L.n_pad,
                            L.nchunk, (__half*)W.y16.ptr, s));
     CUDA_TRY(cudaMemsetAsync(W.cand.ptr, 0, (size_t)p, s));
     Screen16Params Q{};
     Q.Y16 = (const __half*)W.y16.ptr;
     Q.sq = (const double*)W.sq.ptr;
+    Q.inv_sq = (const float*)((const double*)W.sq.ptr + p);
+    Q.lam_sq = (const float*)((const double*)W.sq.ptr + p) + p;
     Q.p = (int)p; Q.n = (int)n;
     Q.ntb = (int)((p + 127) / 128);
     Q.nchunk64 = (L.n_pad + 63) / 64;
@@ -656,9 +660,12 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
     Q.tile_end = screen16_tile_count(p);
     Q.lambda0 = G.lambda0;
     Q.eps = screen16_eps(L.n_pad);
+    Q.eps_f = std::nextafter((float)Q.eps, 1.0f);     // (>= eps)
+    Q.n_f = (float)n;
     Q.cand = (uint8_t*)W.cand.ptr;
     Q.zero_ptr = G.zero_ptr;
     Q.zero_count = G.zero_count;
+    if (getenv("SPMESL_DEV_S16_NOZERO")) { Q.zero_ptr = nullptr; Q.zero_count = 0; }   // (dev)
     CUDA_TRY(launch_screen16(Q, std::min(W.sms, Q.tile_end), s));
     W.cand_host.resize(p);
     CUDA_TRY(cudaMemcpyAsync(W.cand_host.data(), W.cand.ptr, (size_t)p, cudaMemcpyDeviceToHost, s));

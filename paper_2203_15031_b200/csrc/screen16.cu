@@ -31,7 +31,10 @@ constexpr int S16_KC = 64;                  // samples per chunk
 constexpr int S16_TILE_HALVES = S16_TB * S16_KC;     // 8192 halves = 16 KB
 constexpr int S16_MMA_WARPS = 8;
 constexpr int S16_THREADS = (S16_MMA_WARPS + 1) * 32;
-constexpr int S16_NST = 4;                  // ring stages (2 tiles = 32 KB each)
+#ifndef SPMESL_S16_NST
+#define SPMESL_S16_NST 4
+#endif
+constexpr int S16_NST = SPMESL_S16_NST;     // ring stages (2 tiles = 32 KB each)
 constexpr int S16_ZPIECE = 2048;            // doubles per Theta zero-fill bulk store
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -183,45 +186,49 @@ __global__ void __launch_bounds__(S16_THREADS, 1) screen16_kernel(const Screen16
       mbar_wait_s(&full[s], ph);
       const __half* tA = ring + (size_t)s * 2 * S16_TILE_HALVES;
       const __half* tB = tA + S16_TILE_HALVES;
+      // fragments of k-step kk + 1 are loaded while the MMAs of k-step kk issue
+      uint32_t a[2][4][4], b[2][4][2];
+      auto load_frags = [&](int kk, int buf) {
 #pragma unroll
-      for (int kk = 0; kk < S16_KC / 16; ++kk) {
-        // A: rows mq*64 + mi*16 + (lane & 15), 16-byte chunk 2 kk + (lane >> 4)
-        uint32_t a[4][4];
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi) {
+        for (int mi = 0; mi < 4; ++mi) {   // A: rows mq*64 + mi*16 + (lane & 15), chunk 2kk + lane/16
           const int r = mq * 64 + mi * 16 + (lane & 15);
           const int ch = 2 * kk + (lane >> 4);
-          ldsm_x4(a[mi][0], a[mi][1], a[mi][2], a[mi][3], tA + r * S16_KC + ((ch ^ (r & 7)) << 3));
+          ldsm_x4(a[buf][mi][0], a[buf][mi][1], a[buf][mi][2], a[buf][mi][3],
+                  tA + r * S16_KC + ((ch ^ (r & 7)) << 3));
         }
-        // B: for n-tile pair (2 x 8 columns): matrices (cols 0-7, k lo), (cols 0-7, k hi),
-        // (cols 8-15, k lo), (cols 8-15, k hi)
-        uint32_t b[4][2];
 #pragma unroll
-        for (int np = 0; np < 2; ++np) {
+        for (int np = 0; np < 2; ++np) {   // B: (cols 0-7, k lo/hi), (cols 8-15, k lo/hi)
           const int r = nq * 32 + np * 16 + (lane & 7) + ((lane >> 4) << 3);
           const int ch = 2 * kk + ((lane >> 3) & 1);
-          ldsm_x4(b[2 * np][0], b[2 * np][1], b[2 * np + 1][0], b[2 * np + 1][1],
+          ldsm_x4(b[buf][2 * np][0], b[buf][2 * np][1], b[buf][2 * np + 1][0], b[buf][2 * np + 1][1],
                   tB + r * S16_KC + ((ch ^ (r & 7)) << 3));
         }
+      };
+      load_frags(0, 0);
+#pragma unroll
+      for (int kk = 0; kk < S16_KC / 16; ++kk) {
+        if (kk + 1 < S16_KC / 16) load_frags(kk + 1, (kk + 1) & 1);
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-          for (int ni = 0; ni < 4; ++ni) hmma(acc[mi][ni], a[mi], b[ni][0], b[ni][1]);
+          for (int ni = 0; ni < 4; ++ni) hmma(acc[mi][ni], a[kk & 1][mi], b[kk & 1][ni][0], b[kk & 1][ni][1]);
       }
       __syncwarp();
       if (lane == 0)
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(&empty[s])) : "memory");
       if (++s == S16_NST) { s = 0; ph ^= 1u; }
     }
-    // epilogue: certify or flag (both orientations of an off-diagonal tile)
+    // epilogue: certify or flag (both orientations of an off-diagonal tile).  The pair is
+    // certified when |acc| <= n (lambda0 / (sq_j sq_c) - eps); that threshold is evaluated in
+    // f32 with every rounding directed downwards (a smaller threshold only adds candidates).
     const bool diag_tile = (I == Jt);
-    double sqc[4][2];
+    float cB[4][2];
 #pragma unroll
     for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int c = Jt * S16_TB + nq * 32 + ni * 8 + 2 * t4 + e;
-        sqc[ni][e] = c < P.p ? P.sq[c] : 0.0;
+        cB[ni][e] = c < P.p ? P.inv_sq[c] : 0.f;
       }
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
@@ -229,15 +236,14 @@ __global__ void __launch_bounds__(S16_THREADS, 1) screen16_kernel(const Screen16
       for (int h = 0; h < 2; ++h) {
         const int j = I * S16_TB + mq * 64 + mi * 16 + g + 8 * h;
         if (j >= P.p) continue;
-        const double sqj = P.sq[j];
+        const float rA = P.lam_sq[j];
 #pragma unroll
         for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int c = Jt * S16_TB + nq * 32 + ni * 8 + 2 * t4 + e;
-            if (c >= P.p || c == j) continue;
-            const double rv = fabs((double)acc[mi][ni][2 * h + e]) * inv_n;
-            if ((rv + P.eps) * (1.0 + 0x1p-40) * sqj * sqc[ni][e] > P.lambda0) {
+            const float thr = __fmul_rd(__fsub_rd(__fmul_rd(rA, cB[ni][e]), P.eps_f), P.n_f);
+            if (fabsf(acc[mi][ni][2 * h + e]) > thr && c < P.p && c != j) {
               P.cand[c] = 1;
               if (!diag_tile) P.cand[j] = 1;
             }
@@ -264,15 +270,24 @@ __global__ void exact_hits_kernel(const double* __restrict__ Gtab, int p, const 
     for (int l = 0; l < nlam; ++l) hit[(size_t)l * p + c] = (uint8_t)(m > lams[l]);
 }
 
-__global__ void sqrt_kernel(const double* __restrict__ in, double* __restrict__ out, int p) {
+__global__ void sqrt_kernel(const double* __restrict__ in, double* __restrict__ out,
+                            float* __restrict__ inv_sq, float* __restrict__ lam_sq, double lambda0,
+                            int p) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < p) out[k] = sqrt(in[k]);
+  if (k < p) {
+    const double q = sqrt(in[k]);
+    out[k] = q;
+    // directed roundings: the epilogue's f32 threshold may only come out smaller
+    inv_sq[k] = __double2float_rd(1.0 / q * (1.0 - 0x1p-40));
+    lam_sq[k] = __double2float_rd(lambda0 / q * (1.0 - 0x1p-40));
+  }
 }
 
 }  // namespace
 
-cudaError_t launch_sqrt(const double* in, double* out, int p, cudaStream_t s) {
-  sqrt_kernel<<<(p + 255) / 256, 256, 0, s>>>(in, out, p);
+cudaError_t launch_sqrt(const double* in, double* out, float* inv_sq, float* lam_sq,
+                        double lambda0, int p, cudaStream_t s) {
+  sqrt_kernel<<<(p + 255) / 256, 256, 0, s>>>(in, out, inv_sq, lam_sq, lambda0, p);
   return cudaGetLastError();
 }
 

@@ -166,9 +166,12 @@ size_t syrk_smem_bytes(int nst);
 struct Screen16Params {
   const __half* Y16;       // normalized f16 tiles
   const double* sq;        // [p] sqrt(N_k)
+  const float* inv_sq;     // [p] 1 / sqrt(N_k), rounded down
+  const float* lam_sq;     // [p] lambda0 / sqrt(N_k), rounded down
   int p, n, ntb, nchunk64;
   int tile_begin, tile_end;
   double lambda0, eps;
+  float eps_f, n_f;        // eps rounded up, n (exact) for the f32 epilogue
   uint8_t* cand;           // [p] column may have a hit (must be checked exactly)
   double* zero_ptr;        // optional Theta zero fill (as GramParams)
   size_t zero_count;
@@ -181,7 +184,8 @@ cudaError_t launch_to_f16(const double* Xb, const double* nrm, int p, int n_pad,
 cudaError_t launch_screen16(const Screen16Params& P, int grid, cudaStream_t s);
 cudaError_t launch_exact_hits(const double* Gtab, int p, const int* U, int nU, const double* lams,
                               int nlam, uint8_t* hit, cudaStream_t s);
-cudaError_t launch_sqrt(const double* in, double* out, int p, cudaStream_t s);
+cudaError_t launch_sqrt(const double* in, double* out, float* inv_sq, float* lam_sq,
+                        double lambda0, int p, cudaStream_t s);
 cudaError_t launch_syrk_screen(const GramParams& P, int grid, cudaStream_t s);
 cudaError_t launch_gram_init(const GramParams& P, cudaStream_t s);
 cudaError_t launch_level_flags(const GramParams& P, cudaStream_t s);
