@@ -594,7 +594,8 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   if ((rc = ensure(W.lam_dev, (size_t)SPMESL_MAX_LAM * 8))) return rc;
   if (screen16) {
     if ((rc = ensure(W.nrm, (size_t)p * 8))) return rc;
-    if ((rc = ensure(W.sq, (size_t)p * 16))) return rc;   // sq (f64) + inv_sq, lam_sq (f32)
+    // inv_sq, lam_n (f32, padded to the 128-column tiles; 16-byte aligned) + sq (f64, p)
+    if ((rc = ensure(W.sq, (size_t)screen16_pad(p) * 8 + (size_t)p * 8))) return rc;
     if ((rc = ensure(W.y16, screen16_y_halves(p, L.n_pad) * 2))) return rc;
     if ((rc = ensure(W.cand, (size_t)p))) return rc;
     if ((rc = ensure(W.umap, (size_t)p * 4))) return rc;
@@ -642,17 +643,20 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   if (screen16) {
     // certified f16 screening (screen16.cu): candidate columns, then their exact FP64 Gram
     // columns and the exact decision; one host round trip for the candidate list
-    CUDA_TRY(launch_sqrt((const double*)W.nrm.ptr, (double*)W.sq.ptr,
-                         (float*)((double*)W.sq.ptr + p), (float*)((double*)W.sq.ptr + p) + p,
-                         G.lambda0, (int)p, s));
+    const int64_t p_pad = screen16_pad(p);
+    float* inv_sq = (float*)W.sq.ptr;
+    float* lam_n = inv_sq + p_pad;
+    double* sqv = (double*)(lam_n + p_pad);
+    CUDA_TRY(launch_sqrt((const double*)W.nrm.ptr, sqv, inv_sq, lam_n, G.lambda0,
+                         (int)n, (int)p, (int)p_pad, s));
     CUDA_TRY(launch_to_f16((const double*)W.xb.ptr, (const double*)W.nrm.ptr, (int)p, L.n_pad,
                            L.nchunk, (__half*)W.y16.ptr, s));
     CUDA_TRY(cudaMemsetAsync(W.cand.ptr, 0, (size_t)p, s));
     Screen16Params Q{};
     Q.Y16 = (const __half*)W.y16.ptr;
-    Q.sq = (const double*)W.sq.ptr;
-    Q.inv_sq = (const float*)((const double*)W.sq.ptr + p);
-    Q.lam_sq = (const float*)((const double*)W.sq.ptr + p) + p;
+    Q.sq = sqv;
+    Q.inv_sq = inv_sq;
+    Q.lam_n = lam_n;
     Q.p = (int)p; Q.n = (int)n;
     Q.ntb = (int)((p + 127) / 128);
     Q.nchunk64 = (L.n_pad + 63) / 64;
@@ -660,8 +664,13 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
     Q.tile_end = screen16_tile_count(p);
     Q.lambda0 = G.lambda0;
     Q.eps = screen16_eps(L.n_pad);
-    Q.eps_f = std::nextafter((float)Q.eps, 1.0f);     // (>= eps)
-    Q.n_f = (float)n;
+    {   // n eps rounded upwards to f32 (the product of the two doubles is rounded first; the
+        // margin 2^-40 relative covers that rounding)
+      const double ne = (double)n * Q.eps * (1.0 + 0x1p-40);
+      float f = (float)ne;
+      if ((double)f < ne) f = std::nextafter(f, INFINITY);
+      Q.epsn = f;
+    }
     Q.cand = (uint8_t*)W.cand.ptr;
     Q.zero_ptr = G.zero_ptr;
     Q.zero_count = G.zero_count;

@@ -19,6 +19,7 @@
 // Layout of Y16: tiles of 128 variables x 64 samples, one contiguous 16 KB block per tile
 // ([nblk128][nchunk64][128][64] halves), each 128-byte row's 16-byte chunks XOR-swizzled by
 // (row & 7) so the ldmatrix row fetches hit distinct bank groups.
+#include <cstdlib>
 #include <cuda_fp16.h>
 #include "spmesl_internal.cuh"
 
@@ -47,6 +48,28 @@ __device__ __forceinline__ void mbar_wait_s(uint64_t* bar, uint32_t parity) {
 }
 
 // Xb (FP64 tiles) -> Y16 (normalized f16 tiles).  One CTA per (128-block, 64-chunk) tile.
+// Theta's zero fill is spread over the producer's chunks in proportion, so the 8 p^2-byte write
+// (the kernel's HBM floor at large p) overlaps the whole contraction instead of trailing it.
+__device__ __forceinline__ size_t zero_quota(const Screen16Params& P, size_t npieces, int nchunk) {
+  const int bid = blockIdx.x, G = gridDim.x;
+  const int ntiles = P.tile_end - P.tile_begin;
+  const size_t my_chunks = (size_t)(ntiles > bid ? (ntiles - bid + G - 1) / G : 0) * nchunk;
+  const size_t my_pieces = npieces > (size_t)bid ? (npieces - bid + G - 1) / G : 0;
+  return my_chunks ? (my_pieces + my_chunks - 1) / my_chunks : 0;
+}
+__device__ __forceinline__ void zero_pieces(const Screen16Params& P, const double* zbuf, size_t& zp,
+                                            size_t npieces, size_t k) {
+  for (; k > 0 && zp < npieces; --k) {
+    const size_t off = zp * S16_ZPIECE;
+    const size_t cnt = min((size_t)S16_ZPIECE, P.zero_count - off);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(P.zero_ptr + off),
+                 "r"(su32(zbuf)), "r"((uint32_t)(cnt * 8))
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    zp += gridDim.x;
+  }
+}
+
 __global__ void to_f16_kernel(const double* __restrict__ Xb, const double* __restrict__ nrm,
                               int p, int nchunk32, int nchunk64, __half* __restrict__ Y16) {
   const int blk = blockIdx.x, q = blockIdx.y;
@@ -120,6 +143,7 @@ __global__ void __launch_bounds__(S16_THREADS, 1) screen16_kernel(const Screen16
       uint32_t ph = 0;
       const size_t npieces = P.zero_ptr ? (P.zero_count + S16_ZPIECE - 1) / S16_ZPIECE : 0;
       size_t zp = blockIdx.x;
+      const size_t zquota = zero_quota(P, npieces, nchunk);
       for (int t = P.tile_begin + blockIdx.x; t < P.tile_end; t += gridDim.x) {
         int I, Jt;
         tri_tile16(t, nT, I, Jt);
@@ -141,28 +165,11 @@ __global__ void __launch_bounds__(S16_THREADS, 1) screen16_kernel(const Screen16
                   su32(dst + S16_TILE_HALVES)),
               "l"(srcB), "r"((uint32_t)S16_TILE_HALVES * 2u), "r"(su32(&full[s]))
               : "memory");
-          if (zp < npieces) {   // Theta's zero fill rides along (16 KB per chunk issued)
-            const size_t off = zp * S16_ZPIECE;
-            const size_t cnt = min((size_t)S16_ZPIECE, P.zero_count - off);
-            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(
-                             P.zero_ptr + off),
-                         "r"(su32(zbuf)), "r"((uint32_t)(cnt * 8))
-                         : "memory");
-            asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-            zp += gridDim.x;
-          }
+          zero_pieces(P, zbuf, zp, npieces, zquota);   // Theta's zero fill rides along
           if (++s == S16_NST) { s = 0; ph ^= 1u; }
         }
       }
-      while (zp < npieces) {
-        const size_t off = zp * S16_ZPIECE;
-        const size_t cnt = min((size_t)S16_ZPIECE, P.zero_count - off);
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(P.zero_ptr + off),
-                     "r"(su32(zbuf)), "r"((uint32_t)(cnt * 8))
-                     : "memory");
-        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-        zp += gridDim.x;
-      }
+      zero_pieces(P, zbuf, zp, npieces, npieces);
       asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
     }
     return;
@@ -219,37 +226,238 @@ __global__ void __launch_bounds__(S16_THREADS, 1) screen16_kernel(const Screen16
       if (++s == S16_NST) { s = 0; ph ^= 1u; }
     }
     // epilogue: certify or flag (both orientations of an off-diagonal tile).  The pair is
-    // certified when |acc| <= n (lambda0 / (sq_j sq_c) - eps); that threshold is evaluated in
-    // f32 with every rounding directed downwards (a smaller threshold only adds candidates).
+    // certified when |acc| <= n lambda0 / (sq_j sq_c) - n eps; that threshold is evaluated as
+    // one f32 fma rounded downwards from factors rounded downwards (n eps rounded upwards), so
+    // it can only come out smaller (a smaller threshold only adds candidates).  Padding
+    // columns carry inv_sq = +inf (never flag).
     const bool diag_tile = (I == Jt);
     float cB[4][2];
 #pragma unroll
     for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int c = Jt * S16_TB + nq * 32 + ni * 8 + 2 * t4 + e;
-        cB[ni][e] = c < P.p ? P.inv_sq[c] : 0.f;
-      }
+      for (int e = 0; e < 2; ++e) cB[ni][e] = P.inv_sq[Jt * S16_TB + nq * 32 + ni * 8 + 2 * t4 + e];
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int j = I * S16_TB + mq * 64 + mi * 16 + g + 8 * h;
         if (j >= P.p) continue;
-        const float rA = P.lam_sq[j];
+        const float rA = P.lam_n[j];
 #pragma unroll
         for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int c = Jt * S16_TB + nq * 32 + ni * 8 + 2 * t4 + e;
-            const float thr = __fmul_rd(__fsub_rd(__fmul_rd(rA, cB[ni][e]), P.eps_f), P.n_f);
-            if (fabsf(acc[mi][ni][2 * h + e]) > thr && c < P.p && c != j) {
+            const float thr = __fmaf_rd(rA, cB[ni][e], -P.epsn);
+            if (fabsf(acc[mi][ni][2 * h + e]) > thr && c != j) {
               P.cand[c] = 1;
               if (!diag_tile) P.cand[j] = 1;
             }
           }
       }
   }
+}
+
+
+// ------------------------------------------------------------------ tcgen05 version
+// The same screening contraction on the 5th-generation tensor cores: the 128 x 64 f16 tiles of
+// Y16 are already the canonical K-major SWIZZLE_128B layout (128-byte rows, 16-byte chunks
+// XOR-ed with row & 7, 1024-byte aligned), so one thread issues tcgen05.mma (M = N = 128,
+// K = 16) straight from the TMA-filled ring into a TMEM accumulator (two 128-column buffers:
+// the epilogue of tile t overlaps the MMAs of tile t + 1), and four epilogue warps read it
+// back with tcgen05.ld.  Roles: warp 0 TMA producer (+ Theta zero fill), warp 1 MMA issuer
+// and TMEM owner, warps 2-9 epilogue (two per TMEM lane quarter, each half of the columns).
+constexpr int T5_EPI_WARPS = 8;
+constexpr int T5_THREADS = (2 + T5_EPI_WARPS) * 32;
+constexpr int T5_NST = 4;
+
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu)      // start address
+         | ((uint64_t)1 << 16)                    // leading byte offset (16 B; unused for SW128 K)
+         | ((uint64_t)(1024 >> 4) << 32)          // stride byte offset: 8 rows x 128 B
+         | ((uint64_t)1 << 46)                    // descriptor version (sm_100)
+         | ((uint64_t)2 << 61);                   // SWIZZLE_128B
+}
+
+__global__ void __launch_bounds__(T5_THREADS, 1) screen16_tc_kernel(const Screen16Params P) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // [0, 1024): barriers + TMEM address; ring at 1024 (1024-aligned tiles); zero piece after it
+  uint64_t* full = (uint64_t*)smem_raw;
+  uint64_t* empty = full + T5_NST;
+  uint64_t* tfull = empty + T5_NST;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  __half* ring = (__half*)(smem_raw + 1024);
+  double* zbuf = (double*)(ring + (size_t)T5_NST * 2 * S16_TILE_HALVES);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nT = P.ntb, nchunk = P.nchunk64;
+  if (P.zero_ptr)
+    for (int e = tid; e < S16_ZPIECE; e += blockDim.x) zbuf[e] = 0.0;
+  if (tid == 0) {
+    for (int s = 0; s < T5_NST; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(&full[s])), "r"(1));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(&empty[s])), "r"(1));
+    }
+    for (int b = 0; b < 2; ++b) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(&tfull[b])), "r"(1));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(&tempty[b])), "r"(T5_EPI_WARPS));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
+  if (warp == 1) {   // TMEM: 2 accumulators x 128 columns (f32), 128 lanes
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
+                 "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *(volatile uint32_t*)tmem_slot;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      const size_t npieces = P.zero_ptr ? (P.zero_count + S16_ZPIECE - 1) / S16_ZPIECE : 0;
+      size_t zp = blockIdx.x;
+      const size_t zquota = zero_quota(P, npieces, nchunk);
+      for (int t = P.tile_begin + blockIdx.x; t < P.tile_end; t += gridDim.x) {
+        int I, Jt;
+        tri_tile16(t, nT, I, Jt);
+        for (int q = 0; q < nchunk; ++q) {
+          mbar_wait_s(&empty[s], ph ^ 1u);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(&full[s])),
+                       "r"(2u * S16_TILE_HALVES * 2u)
+                       : "memory");
+          const __half* srcA = P.Y16 + ((size_t)I * nchunk + q) * S16_TILE_HALVES;
+          const __half* srcB = P.Y16 + ((size_t)Jt * nchunk + q) * S16_TILE_HALVES;
+          __half* dst = ring + (size_t)s * 2 * S16_TILE_HALVES;
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                  su32(dst)),
+              "l"(srcA), "r"((uint32_t)S16_TILE_HALVES * 2u), "r"(su32(&full[s]))
+              : "memory");
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                  su32(dst + S16_TILE_HALVES)),
+              "l"(srcB), "r"((uint32_t)S16_TILE_HALVES * 2u), "r"(su32(&full[s]))
+              : "memory");
+          zero_pieces(P, zbuf, zp, npieces, zquota);   // Theta's zero fill rides along
+          if (++s == T5_NST) { s = 0; ph ^= 1u; }
+        }
+      }
+      zero_pieces(P, zbuf, zp, npieces, npieces);
+      asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    // instruction descriptor: D f32, A = B = f16, both K-major, N = 128, M = 128
+    const uint32_t idesc = (1u << 4) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+    int s = 0, it = 0;
+    uint32_t ph = 0;
+    uint32_t ph_te[2] = {0u, 0u};
+    for (int t = P.tile_begin + blockIdx.x; t < P.tile_end; t += gridDim.x, ++it) {
+      const int ab = it & 1;
+      mbar_wait_s(&tempty[ab], ph_te[ab] ^ 1u);     // the epilogue has drained this buffer
+      ph_te[ab] ^= 1u;
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const uint32_t dtm = tmem + (uint32_t)(ab * 128);
+      for (int q = 0; q < nchunk; ++q) {
+        mbar_wait_s(&full[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        if (lane == 0) {
+          const uint32_t sa = su32(ring + (size_t)s * 2 * S16_TILE_HALVES);
+          const uint32_t sb = sa + S16_TILE_HALVES * 2;
+#pragma unroll
+          for (int kk = 0; kk < S16_KC / 16; ++kk) {
+            const uint64_t da = umma_desc_sw128(sa + kk * 32);
+            const uint64_t db = umma_desc_sw128(sb + kk * 32);
+            const uint32_t acc = (q > 0 || kk > 0) ? 1u : 0u;
+            asm volatile(
+                "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(dtm),
+                "l"(da), "l"(db), "r"(idesc), "r"(acc));
+          }
+          // the stage is free once these MMAs have read it
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                           su32(&empty[s]))
+                       : "memory");
+        }
+        __syncwarp();
+        if (++s == T5_NST) { s = 0; ph ^= 1u; }
+      }
+      if (lane == 0)   // accumulator complete
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                         su32(&tfull[ab]))
+                     : "memory");
+      __syncwarp();
+    }
+  } else {
+    // ---------------------------------------------------------------- epilogue (warps 2-9)
+    const int qd = warp & 3;                     // TMEM lane quarter this warp may access
+    const int half = (warp - 2) >> 2;            // column half of the tile
+    int it = 0;
+    uint32_t ph_tf[2] = {0u, 0u};
+    for (int t = P.tile_begin + blockIdx.x; t < P.tile_end; t += gridDim.x, ++it) {
+      int I, Jt;
+      tri_tile16(t, nT, I, Jt);
+      const int ab = it & 1;
+      mbar_wait_s(&tfull[ab], ph_tf[ab]);
+      ph_tf[ab] ^= 1u;
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const bool diag_tile = (I == Jt);
+      const int j = I * S16_TB + 32 * qd + lane;          // this thread's row of the tile
+      const bool jok = j < P.p;
+      const float rA = jok ? P.lam_n[j] : 0.f;
+#pragma unroll 1
+      for (int cg = 2 * half; cg < 2 * half + 2; ++cg) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem + ((uint32_t)(32 * qd) << 16) + (uint32_t)(ab * 128 + 32 * cg);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+            "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+              "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+              "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+              "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        if (jok) {
+          // thresholds as in screen16_kernel; the 32 columns' factors are warp-uniform loads
+          const int c0 = Jt * S16_TB + 32 * cg;
+          const float4* iv = reinterpret_cast<const float4*>(P.inv_sq + c0);
+          uint32_t hits = 0;
+#pragma unroll
+          for (int k4 = 0; k4 < 8; ++k4) {
+            const float4 f = __ldg(iv + k4);
+            hits |= (uint32_t)(fabsf(__uint_as_float(v[4 * k4 + 0])) > __fmaf_rd(rA, f.x, -P.epsn)) << (4 * k4 + 0);
+            hits |= (uint32_t)(fabsf(__uint_as_float(v[4 * k4 + 1])) > __fmaf_rd(rA, f.y, -P.epsn)) << (4 * k4 + 1);
+            hits |= (uint32_t)(fabsf(__uint_as_float(v[4 * k4 + 2])) > __fmaf_rd(rA, f.z, -P.epsn)) << (4 * k4 + 2);
+            hits |= (uint32_t)(fabsf(__uint_as_float(v[4 * k4 + 3])) > __fmaf_rd(rA, f.w, -P.epsn)) << (4 * k4 + 3);
+          }
+          if (diag_tile && (unsigned)(j - c0) < 32u) hits &= ~(1u << (j - c0));   // c == j
+          while (hits) {   // rare
+            const int i = __ffs(hits) - 1;
+            hits &= hits - 1;
+            P.cand[c0 + i] = 1;
+            if (!diag_tile) P.cand[j] = 1;
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(&tempty[ab])) : "memory");
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(256));
 }
 
 // exact decision for the candidate columns from their FP64 Gram columns (one warp each)
@@ -271,23 +479,26 @@ __global__ void exact_hits_kernel(const double* __restrict__ Gtab, int p, const 
 }
 
 __global__ void sqrt_kernel(const double* __restrict__ in, double* __restrict__ out,
-                            float* __restrict__ inv_sq, float* __restrict__ lam_sq, double lambda0,
-                            int p) {
+                            float* __restrict__ inv_sq, float* __restrict__ lam_n, double lambda0,
+                            int n, int p, int p_pad) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k < p) {
     const double q = sqrt(in[k]);
     out[k] = q;
     // directed roundings: the epilogue's f32 threshold may only come out smaller
     inv_sq[k] = __double2float_rd(1.0 / q * (1.0 - 0x1p-40));
-    lam_sq[k] = __double2float_rd(lambda0 / q * (1.0 - 0x1p-40));
+    lam_n[k] = __double2float_rd((double)n * lambda0 / q * (1.0 - 0x1p-40));
+  } else if (k < p_pad) {   // padding columns never flag (threshold +inf), padding rows are skipped
+    inv_sq[k] = __int_as_float(0x7f800000);
+    lam_n[k] = 0.f;
   }
 }
 
 }  // namespace
 
-cudaError_t launch_sqrt(const double* in, double* out, float* inv_sq, float* lam_sq,
-                        double lambda0, int p, cudaStream_t s) {
-  sqrt_kernel<<<(p + 255) / 256, 256, 0, s>>>(in, out, inv_sq, lam_sq, lambda0, p);
+cudaError_t launch_sqrt(const double* in, double* out, float* inv_sq, float* lam_n,
+                        double lambda0, int n, int p, int p_pad, cudaStream_t s) {
+  sqrt_kernel<<<(p_pad + 255) / 256, 256, 0, s>>>(in, out, inv_sq, lam_n, lambda0, n, p, p_pad);
   return cudaGetLastError();
 }
 
@@ -296,6 +507,8 @@ size_t screen16_y_halves(int64_t p, int n_pad) {
   const int64_t nc = (n_pad + S16_KC - 1) / S16_KC;
   return (size_t)(nb * nc * S16_TILE_HALVES);
 }
+
+int64_t screen16_pad(int64_t p) { return (p + S16_TB - 1) / S16_TB * S16_TB; }
 
 int screen16_tile_count(int64_t p) {
   const int64_t nT = (p + S16_TB - 1) / S16_TB;
@@ -317,6 +530,16 @@ cudaError_t launch_to_f16(const double* Xb, const double* nrm, int p, int n_pad,
 
 cudaError_t launch_screen16(const Screen16Params& P, int grid, cudaStream_t s) {
   if (P.tile_end <= P.tile_begin) return cudaSuccess;
+  static const bool mma_sync = getenv("SPMESL_S16_MMA_SYNC") && atoi(getenv("SPMESL_S16_MMA_SYNC"));
+  if (!mma_sync) {   // tcgen05 (default)
+    const size_t smem = 1024 + (size_t)T5_NST * 2 * S16_TILE_HALVES * 2 + (size_t)S16_ZPIECE * 8;
+    static_assert(T5_EPI_WARPS == 8, "epilogue: two warps per TMEM lane quarter");
+    cudaError_t e = cudaFuncSetAttribute(screen16_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    screen16_tc_kernel<<<grid, T5_THREADS, smem, s>>>(P);
+    return cudaGetLastError();
+  }
   const size_t smem = 128 + (size_t)S16_NST * 2 * S16_TILE_HALVES * 2 + (size_t)S16_ZPIECE * 8;
   cudaError_t e = cudaFuncSetAttribute(screen16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);

@@ -166,26 +166,27 @@ size_t syrk_smem_bytes(int nst);
 struct Screen16Params {
   const __half* Y16;       // normalized f16 tiles
   const double* sq;        // [p] sqrt(N_k)
-  const float* inv_sq;     // [p] 1 / sqrt(N_k), rounded down
-  const float* lam_sq;     // [p] lambda0 / sqrt(N_k), rounded down
+  const float* inv_sq;     // [ntb*128] 1 / sqrt(N_k) rounded down; +inf past p
+  const float* lam_n;      // [ntb*128] n lambda0 / sqrt(N_k) rounded down; 0 past p
   int p, n, ntb, nchunk64;
   int tile_begin, tile_end;
   double lambda0, eps;
-  float eps_f, n_f;        // eps rounded up, n (exact) for the f32 epilogue
+  float epsn;              // n eps rounded up (f32 epilogue)
   uint8_t* cand;           // [p] column may have a hit (must be checked exactly)
   double* zero_ptr;        // optional Theta zero fill (as GramParams)
   size_t zero_count;
 };
 size_t screen16_y_halves(int64_t p, int n_pad);
 int screen16_tile_count(int64_t p);
+int64_t screen16_pad(int64_t p);   // p rounded up to the 128-column tiles
 double screen16_eps(int n_pad);
 cudaError_t launch_to_f16(const double* Xb, const double* nrm, int p, int n_pad, int nchunk32,
                           __half* Y16, cudaStream_t s);
 cudaError_t launch_screen16(const Screen16Params& P, int grid, cudaStream_t s);
 cudaError_t launch_exact_hits(const double* Gtab, int p, const int* U, int nU, const double* lams,
                               int nlam, uint8_t* hit, cudaStream_t s);
-cudaError_t launch_sqrt(const double* in, double* out, float* inv_sq, float* lam_sq,
-                        double lambda0, int p, cudaStream_t s);
+cudaError_t launch_sqrt(const double* in, double* out, float* inv_sq, float* lam_n,
+                        double lambda0, int n, int p, int p_pad, cudaStream_t s);
 cudaError_t launch_syrk_screen(const GramParams& P, int grid, cudaStream_t s);
 cudaError_t launch_gram_init(const GramParams& P, cudaStream_t s);
 cudaError_t launch_level_flags(const GramParams& P, cudaStream_t s);
