@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--mode", default="per_column", choices=["per_column", "joint"],
                     help="per_column (default; Alg. 1/2 stop) or joint (Algorithm 3, P:938-990)")
-    ap.add_argument("--solver", default="auto", choices=["auto", "residual", "gram"])
+    ap.add_argument("--solver", default="auto", choices=["auto", "residual", "gram", "gram16"])
     return ap.parse_args()
 
 
@@ -154,6 +154,15 @@ def fp64_peak():
         return max(d[k] for k in keys), "profiles/r01_peaks_microbench.json (DMMA f64, measured)"
     except Exception:
         return 36.8, "fallback 36.8 TFLOP/s (microbench value)"
+
+
+def hbm_peak_gbs():
+    """Measured HBM copy bandwidth of this pool's B200s (driver-written MEASURED_PEAKS.json)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)"
+    except Exception:
+        return 6650.0, "of fallback 6650 GB/s (B200_PROFILING.md)"
 
 
 def cd_traffic():
@@ -315,10 +324,31 @@ def run_ours(args):
     peak, peak_src = fp64_peak()
     traffic = cd_traffic()
     step_ms_mean = tot_ms / args.steps
-    if stats_last.get("solver") == 2:
+    if stats_last.get("solver") == 3 and not stats_last.get("gram_fallback"):
+        # default solver: the certified f16 screening kernel (tcgen05) is the longest kernel of
+        # the step; it also writes Theta's p^2 zeros, which makes it HBM-bound: algorithmic
+        # bytes = 8 p^2 (Theta zero fill) + the f16 operand tiles read once (2 p_pad n_pad64)
+        scr_ms = float(stats_last["ms_screen"])
+        p_pad, n_pad64 = -(-p // 128) * 128, -(-n // 64) * 64
+        nbytes = 8.0 * p * p + 2.0 * p_pad * n_pad64 + p
+        achieved = nbytes / (scr_ms / 1000.0) / 1e9
+        hbm_peak = hbm_peak_gbs()
+        flops = float(n_pad64) * p_pad * (p_pad + 128)   # the triangle of 128 x 128 tiles
+        roof = {"kernel": "screen16_tc_kernel", "bound": "hbm", "achieved": achieved,
+                "peak": hbm_peak[0], "unit": "GB/s", "frac": achieved / hbm_peak[0],
+                "traffic": (traffic or {}).get("screen16_dram_bytes_per_launch"),
+                "peak_source": hbm_peak[1], "dtype": "f16 x f16 -> f32 (tcgen05.mma kind::f16)",
+                "kernel_ms": scr_ms, "kernel_share_of_step": scr_ms / step_ms_mean,
+                "algorithmic": "8 p^2 bytes (Theta zero fill) + 2 p_pad n_pad bytes (f16 tiles) + p",
+                "tensor_tflops": flops / (scr_ms / 1000.0) / 1e12,
+                "screen_candidates": stats_last.get("screen_candidates"),
+                "exact_and_sweeps_ms": stats_last.get("ms_gram", 0.0) - scr_ms,
+                "sweep_kernel_ms": stats_last.get("ms_tail", 0.0),
+                "sweep_columns": stats_last.get("tail_columns", 0)}
+    elif stats_last.get("solver") in (2, 3):
         # Gram solver: the symmetric Gram kernel; algorithmic work n p (p + 1) flops (each of
         # the p (p + 1) / 2 distinct entries of X~^T X~ is a length-n dot product)
-        gram_ms = float(stats_last["ms_gram"])
+        gram_ms = float(stats_last.get("ms_screen") or stats_last["ms_gram"])
         share = 1.0
         if world > 1:      # this rank screened tiles [t0, t1) of the triangle
             nt = S.gram_tile_count(p)
@@ -419,7 +449,7 @@ def run_ours(args):
                     "max_sweeps": stats_last["max_sweeps"], "max_outer": stats_last["max_outer"],
                     "nnz": stats_last["nnz"], "tile_cols": stats_last["tile_cols"],
                     "num_ctas": stats_last["num_ctas"], "mode": args.mode,
-                    "solver": {1: "residual", 2: "gram"}.get(stats_last.get("solver"), "?")}),
+                    "solver": {1: "residual", 2: "gram", 3: "gram16"}.get(stats_last.get("solver"), "?")}),
                 "roofline": roof, "clocks": clk.summary(), "e2e": e2e,
                 "gpu_launches": int(stats_last["kernel_launches"]) * args.steps,
                 "ms_breakdown": {"standardize": stats_last["ms_standardize"],

@@ -108,12 +108,16 @@ typedef struct {
   int64_t tail_columns;   /* columns finished by the tail solver */
   int64_t tail_gram_ondemand; /* Gram columns the tail solver computed on first use */
   int64_t tail_sweeps;    /* sweeps performed by the tail solver (the CD kernel did the rest) */
-  int32_t solver;         /* solver used: 1 residual, 2 Gram */
-  int32_t pad0;
+  int32_t solver;         /* solver used: 1 residual, 2 Gram (FP64 S), 3 Gram (certified f16
+                             screening) */
+  int32_t gram_fallback;  /* solver 3: 1 if most columns were candidates and the full FP64 Gram
+                             kernel decided them instead */
   double  ms_gram;        /* Gram solver: device time of the screening pass (solver 2: the FP64
                              Gram kernel; solver 3: f16 screening + exact Gram columns of the
                              candidates) */
   int64_t screen_candidates; /* solver 3: columns the f16 screening could not certify hit-free */
+  double  ms_screen;      /* device time of the screening kernel alone (solver 2: the FP64 Gram
+                             kernel; solver 3: the f16 screening kernel incl. Theta's zero fill) */
 } spmesl_stats;
 
 /* Fill *opt with the defaults listed above. */

@@ -58,9 +58,10 @@ class Stats(ctypes.Structure):
         ("tail_gram_ondemand", ctypes.c_int64),
         ("tail_sweeps", ctypes.c_int64),
         ("solver", ctypes.c_int32),
-        ("pad0", ctypes.c_int32),
+        ("gram_fallback", ctypes.c_int32),
         ("ms_gram", ctypes.c_double),
         ("screen_candidates", ctypes.c_int64),
+        ("ms_screen", ctypes.c_double),
     ]
 
     def asdict(self):

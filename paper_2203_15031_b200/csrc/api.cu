@@ -91,7 +91,7 @@ struct Workspace {
   // host-API staging
   Buffer hx, htheta, hsigma, hiters, hsweeps, hconv, coo_r, coo_c, coo_v, hdiag, zeros;
   DevCounters* host_counters = nullptr;   // pinned
-  cudaEvent_t ev[8] = {};
+  cudaEvent_t ev[10] = {};   // [8], [9]: around the screening kernel
   cudaStream_t side = nullptr;            // Theta zero-fill overlapped with the CD kernel
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   double* pending_zero = nullptr;         // Theta to zero-fill once standardization is done
@@ -101,6 +101,9 @@ struct Workspace {
   std::vector<double> lam_host;           // (pinned-free staging of the penalty levels)
   std::vector<uint8_t> cand_host;         // certified screening: candidate flags
   int last_candidates = 0;
+  int gram_fallback = 0;      // solver 3 fell back to the full FP64 Gram kernel (last fit)
+  bool zero_join = false;     // part of Theta's zero fill runs on `side` (join ev_join)
+  int gram_launches = 0;      // kernels fit_gram_enqueue launched (last fit)
   bool init = false;
 };
 
@@ -640,6 +643,8 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   G.converged = out.conv;
   G.nz_count = (int*)W.nz_count.ptr; G.nz_cur = (int*)W.nz_cur.ptr;
   bool full_gram = !screen16;
+  int launches = 0;
+  W.gram_fallback = 0;
   if (screen16) {
     // certified f16 screening (screen16.cu): candidate columns, then their exact FP64 Gram
     // columns and the exact decision; one host round trip for the candidate list
@@ -672,10 +677,31 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
       Q.epsn = f;
     }
     Q.cand = (uint8_t*)W.cand.ptr;
-    Q.zero_ptr = G.zero_ptr;
-    Q.zero_count = G.zero_count;
+    // Theta's zero fill is split: the screening kernel writes the first part under its
+    // contraction, a side-stream kernel the rest while the exact Gram columns and the sweeps
+    // (latency-bound, little HBM traffic) run; the caller joins it before the assembly
+    // (measured on config 5: all fused 1.13 ms per fit, half and half 1.02 ms)
+    static const double zfrac = getenv("SPMESL_S16_ZFRAC") ? atof(getenv("SPMESL_S16_ZFRAC")) : 0.5;
+    size_t zfused = (size_t)(zfrac * (double)G.zero_count) & ~(size_t)1;
+    if (zfused > G.zero_count) zfused = G.zero_count;
+    Q.zero_ptr = zfused ? G.zero_ptr : nullptr;
+    Q.zero_count = zfused;
     if (getenv("SPMESL_DEV_S16_NOZERO")) { Q.zero_ptr = nullptr; Q.zero_count = 0; }   // (dev)
+    CUDA_TRY(cudaEventRecord(W.ev[8], s));
     CUDA_TRY(launch_screen16(Q, std::min(W.sms, Q.tile_end), s));
+    CUDA_TRY(cudaEventRecord(W.ev[9], s));
+    if (G.zero_ptr && zfused < G.zero_count) {
+      CUDA_TRY(cudaStreamWaitEvent(W.side, W.ev[9], 0));
+      static const int zgrid = getenv("SPMESL_ZB_GRID") ? atoi(getenv("SPMESL_ZB_GRID")) : W.sms;
+      if (zgrid > 0)
+        CUDA_TRY(launch_zero_fill_bulk(G.zero_ptr + zfused, G.zero_count - zfused, zgrid, W.side));
+      else
+        CUDA_TRY(launch_zero_fill(G.zero_ptr + zfused, G.zero_count - zfused, W.sms, W.side));
+      CUDA_TRY(cudaEventRecord(W.ev_join, W.side));
+      W.zero_join = true;
+      ++launches;
+    }
+    launches += 3;   // sqrt, to_f16, screen16
     W.cand_host.resize(p);
     CUDA_TRY(cudaMemcpyAsync(W.cand_host.data(), W.cand.ptr, (size_t)p, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
@@ -694,22 +720,27 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
       const int ntiles = nT * (nT + 1) / 2;
       CUDA_TRY(launch_syrk_screen(G, std::min(W.sms, ntiles), s));
       if (nlam > 1) CUDA_TRY(launch_level_flags(G, s));
+      launches += 1 + (nlam > 1);
+      W.gram_fallback = 1;
     } else {
       CUDA_TRY(cudaMemcpyAsync(W.umap.ptr, gstate.data(), (size_t)p * 4, cudaMemcpyHostToDevice, s));
       if (nU) CUDA_TRY(cudaMemcpyAsync(W.uvars.ptr, U.data(), (size_t)nU * 4, cudaMemcpyHostToDevice, s));
       CUDA_TRY(launch_gram_pass((const double*)W.xb.ptr, (int)L.nblk, L.nchunk, (int)n, (int)p,
                                 nullptr, 0, (const int*)W.uvars.ptr, nU, nullptr,
-                                (double*)W.ondemand.ptr, s));
-      CUDA_TRY(launch_exact_hits((const double*)W.ondemand.ptr, (int)p, (const int*)W.uvars.ptr,
-                                 nU, (const double*)W.lam_dev.ptr, nlam, (uint8_t*)W.hit.ptr, s));
+                                (double*)W.ondemand.ptr, s, (uint8_t*)W.hit.ptr,
+                                (const double*)W.lam_dev.ptr, nlam));
+      launches += 1;
     }
     CUDA_TRY(cudaEventRecord(W.ev[7], s));
   } else {
     const int nT = (int)((L.nblk + 3) / 4);
     const int ntiles = nT * (nT + 1) / 2;
+    CUDA_TRY(cudaEventRecord(W.ev[8], s));
     CUDA_TRY(launch_syrk_screen(G, std::min(W.sms, ntiles), s));
+    CUDA_TRY(cudaEventRecord(W.ev[9], s));
     CUDA_TRY(cudaEventRecord(W.ev[7], s));
     if (nlam > 1) CUDA_TRY(launch_level_flags(G, s));
+    launches += 1 + (nlam > 1);
   }
   CUDA_TRY(launch_gram_init(G, s));
   CUDA_TRY(cudaEventRecord(W.ev[5], s));
@@ -742,6 +773,7 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   CUDA_TRY(launch_tail_sweeps(T, (int)std::min<int64_t>(W.sms, p * nlam), s));
   CUDA_TRY(cudaEventRecord(W.ev[6], s));
   CUDA_TRY(cudaEventRecord(W.ev[2], s));
+  W.gram_launches = launches + 2;   // + gram_init, tail
   return SPMESL_OK;
 }
 
@@ -751,10 +783,12 @@ void gram_stats(Workspace& W, int64_t p, int nzcap, spmesl_stats* st, bool scree
   const int nT = (int)((((p + J - 1) / J) + 3) / 4);
   st->solver = screen16 ? 3 : 2;
   if (screen16) st->screen_candidates = W.last_candidates;
+  st->gram_fallback = W.gram_fallback;
   st->tile_cols = 0;
   st->num_ctas = std::min(W.sms, nT * (nT + 1) / 2);
-  st->kernel_launches += 3;
+  st->kernel_launches += W.gram_launches;
   st->ms_gram = ev_ms(W.ev[1], W.ev[7]);
+  st->ms_screen = ev_ms(W.ev[8], W.ev[9]);
   st->ms_tail = ev_ms(W.ev[5], W.ev[6]);
   st->tail_columns = W.host_counters->tail_count;
   st->tail_sweeps = W.host_counters->tail_sweeps;
@@ -856,7 +890,8 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
     const size_t pp = (size_t)p * (size_t)p;
     // the Gram kernel zero-fills Theta itself (bulk stores from its producer warp) when the
     // buffer allows 16-byte pieces; otherwise a side-stream kernel does, after standardization
-    const bool take = gram && (((uintptr_t)dTheta & 15) == 0) && (pp & 1) == 0;
+    static const bool side_zero = getenv("SPMESL_DEV_SIDE_ZERO") != nullptr;   // (dev)
+    const bool take = gram && !side_zero && (((uintptr_t)dTheta & 15) == 0) && (pp & 1) == 0;
     if (take) { W.take_zero = dTheta; W.take_count = pp; }
     else { W.pending_zero = dTheta; W.pending_count = pp; }
     if (gram) {
@@ -872,8 +907,10 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
       W.pending_zero = nullptr;
       if (!rc) rc = fail(SPMESL_ERR_CUDA, "internal: Theta zero fill was not launched");
     }
-    if (rc) { if (!take) cudaStreamWaitEvent(s, W.ev_join, 0); return rc; }
-    if (!take) CUDA_TRY(cudaStreamWaitEvent(s, W.ev_join, 0));
+    const bool join = !take || W.zero_join;
+    W.zero_join = false;
+    if (rc) { if (join) cudaStreamWaitEvent(s, W.ev_join, 0); return rc; }
+    if (join) CUDA_TRY(cudaStreamWaitEvent(s, W.ev_join, 0));
     const size_t cap = (size_t)p * (size_t)nzcap;
     if ((rc = ensure(W.csc_rows, cap * 4))) return rc;
     if ((rc = ensure(W.csc_vals, cap * 8))) return rc;
@@ -1177,8 +1214,10 @@ int spmesl_fit_path_device(const double* dX, int64_t n, int64_t p, const double*
                           nlam, o.solver != 2);
     W->take_zero = nullptr;
     if (W->pending_zero) { W->pending_zero = nullptr; if (!rc) rc = fail(SPMESL_ERR_CUDA, "internal"); }
-    if (rc) { if (!take) cudaStreamWaitEvent(s, W->ev_join, 0); return rc; }
-    if (!take) CUDA_TRY(cudaStreamWaitEvent(s, W->ev_join, 0));
+    const bool join = !take || W->zero_join;
+    W->zero_join = false;
+    if (rc) { if (join) cudaStreamWaitEvent(s, W->ev_join, 0); return rc; }
+    if (join) CUDA_TRY(cudaStreamWaitEvent(s, W->ev_join, 0));
     const size_t cap = (size_t)p * (size_t)nzcap;
     if ((rc = ensure(W->csc_rows, cap * 4))) return rc;
     if ((rc = ensure(W->csc_vals, cap * 8))) return rc;

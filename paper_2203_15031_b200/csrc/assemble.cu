@@ -283,6 +283,39 @@ __global__ void __launch_bounds__(256) zero_fill_kernel(double2* __restrict__ a,
     __stcs(a + i, z);
 }
 
+// The same fill with bulk (TMA) stores from one elected thread per 32-thread CTA: almost no SM
+// footprint (it runs beside the exact Gram-column and sweep kernels), and the stores carry an
+// L2 evict-first hint so the 8 p^2 bytes streaming through L2 do not push out X~.
+constexpr int ZB_PIECE = 2048;   // doubles per bulk store (16 KB)
+__global__ void __launch_bounds__(32) zero_fill_bulk_kernel(double* __restrict__ a, size_t count) {
+  __shared__ __align__(128) double zb[ZB_PIECE];
+  for (int e = threadIdx.x; e < ZB_PIECE; e += 32) zb[e] = 0.0;
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  __syncwarp();
+  if (threadIdx.x != 0) return;
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  const uint32_t src = (uint32_t)__cvta_generic_to_shared(zb);
+  const size_t npieces = (count + ZB_PIECE - 1) / ZB_PIECE;
+  for (size_t k = blockIdx.x; k < npieces; k += gridDim.x) {
+    const size_t off = k * ZB_PIECE;
+    const size_t cnt = min((size_t)ZB_PIECE, count - off);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;\n" ::"l"(
+                     a + off),
+                 "r"(src), "r"((uint32_t)(cnt * 8)), "l"(pol)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+  }
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+
+cudaError_t launch_zero_fill_bulk(double* a, size_t count, int grid, cudaStream_t s) {
+  if (count == 0) return cudaSuccess;
+  if (((uintptr_t)a & 15) != 0 || (count & 1)) return cudaMemsetAsync(a, 0, count * 8, s);
+  zero_fill_bulk_kernel<<<grid, 32, 0, s>>>(a, count);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_zero_fill(double* a, size_t count, int sms, cudaStream_t s) {
   if (count == 0) return cudaSuccess;
   if (((uintptr_t)a & 15) != 0 || (count & 1)) return cudaMemsetAsync(a, 0, count * 8, s);

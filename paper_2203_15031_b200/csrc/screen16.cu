@@ -2,10 +2,11 @@
 //
 // The first sweep of column c changes some b_jc iff |S_jc| > lambda0 for some j != c
 // (sigma^(0) = 1), S = X~^T X~ / n.  Deciding that needs S only to the extent of a
-// comparison, so it is done on the f16 tensor cores (mma.sync m16n8k16, f32 accumulate; ~15x
-// the FP64 DMMA rate on B200) with a rigorous error bound, and only the columns that cannot be
-// certified hit-free get their exact FP64 Gram column (DMMA, gram_pass in tail.cu), from which
-// the exact decision is taken.  No low-precision value ever enters the iterates.
+// comparison, so it is done on the f16 tensor cores (tcgen05.mma kind::f16 with the f32
+// accumulator in TMEM — default — or mma.sync m16n8k16 with SPMESL_S16_MMA_SYNC=1) with a
+// rigorous error bound, and only the columns that cannot be certified hit-free get their exact
+// FP64 Gram column (DMMA, gram_pass in tail.cu, which also takes the exact decision).  No
+// low-precision value ever enters the iterates.
 //
 // Bound.  y_k = x~_k / sqrt(N_k) with N_k = x~_k^T x~_k / n, so y_k^T y_k = n and
 // R = Y^T Y / n is the correlation-scaled S: S_jc = R_jc sqrt(N_j N_c), |R_jc| <= 1.
@@ -15,6 +16,10 @@
 // (Cauchy-Schwarz):
 //   |R_hat_jc - R_jc| <= 2.1 u + n_pad 2^-22 + 2^-23 + 2^-20 =: eps      (n_pad <= 2^16)
 // The pair is certified hit-free when (|R_hat_jc| + eps)(1 + 2^-40) sqrt(N_j N_c) <= lambda0.
+// In terms of the raw accumulator acc = n R_hat_jc the epilogue tests
+//   |acc| <= fma_rd(lam_n_j, inv_c, -epsn),  lam_n_j = rd(n lambda0 / sqrt(N_j)),
+//   inv_c = rd(1 / sqrt(N_c)), epsn = ru(n eps)
+// (every factor rounded so the f32 threshold can only come out smaller).
 //
 // Layout of Y16: tiles of 128 variables x 64 samples, one contiguous 16 KB block per tile
 // ([nblk128][nchunk64][128][64] halves), each 128-byte row's 16-byte chunks XOR-swizzled by
@@ -62,9 +67,19 @@ __device__ __forceinline__ void zero_pieces(const Screen16Params& P, const doubl
   for (; k > 0 && zp < npieces; --k) {
     const size_t off = zp * S16_ZPIECE;
     const size_t cnt = min((size_t)S16_ZPIECE, P.zero_count - off);
+#ifndef SPMESL_S16_NO_EVICT_FIRST
+    // evict-first: the 8 p^2 bytes streaming through L2 should not push out the f16 tiles
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;\n" ::"l"(
+                     P.zero_ptr + off),
+                 "r"(su32(zbuf)), "r"((uint32_t)(cnt * 8)), "l"(pol)
+                 : "memory");
+#else
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(P.zero_ptr + off),
                  "r"(su32(zbuf)), "r"((uint32_t)(cnt * 8))
                  : "memory");
+#endif
     asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
     zp += gridDim.x;
   }
@@ -460,24 +475,6 @@ __global__ void __launch_bounds__(T5_THREADS, 1) screen16_tc_kernel(const Screen
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(256));
 }
 
-// exact decision for the candidate columns from their FP64 Gram columns (one warp each)
-__global__ void exact_hits_kernel(const double* __restrict__ Gtab, int p, const int* __restrict__ U,
-                                  int nU, const double* __restrict__ lams, int nlam,
-                                  uint8_t* __restrict__ hit) {
-  const int lane = threadIdx.x & 31;
-  const int w = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
-  if (w >= nU) return;
-  const int c = U[w];
-  const double* col = Gtab + (size_t)c * p;
-  double m = 0.0;
-  for (int j = lane; j < p; j += 32)
-    if (j != c) m = fmax(m, fabs(col[j]));
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if (lane == 0)
-    for (int l = 0; l < nlam; ++l) hit[(size_t)l * p + c] = (uint8_t)(m > lams[l]);
-}
-
 __global__ void sqrt_kernel(const double* __restrict__ in, double* __restrict__ out,
                             float* __restrict__ inv_sq, float* __restrict__ lam_n, double lambda0,
                             int n, int p, int p_pad) {
@@ -548,12 +545,5 @@ cudaError_t launch_screen16(const Screen16Params& P, int grid, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_exact_hits(const double* Gtab, int p, const int* U, int nU, const double* lams,
-                              int nlam, uint8_t* hit, cudaStream_t s) {
-  if (nU <= 0) return cudaSuccess;
-  const int wpb = 8;
-  exact_hits_kernel<<<(nU + wpb - 1) / wpb, wpb * 32, 0, s>>>(Gtab, p, U, nU, lams, nlam, hit);
-  return cudaGetLastError();
-}
 
 }  // namespace spmesl

@@ -183,8 +183,6 @@ double screen16_eps(int n_pad);
 cudaError_t launch_to_f16(const double* Xb, const double* nrm, int p, int n_pad, int nchunk32,
                           __half* Y16, cudaStream_t s);
 cudaError_t launch_screen16(const Screen16Params& P, int grid, cudaStream_t s);
-cudaError_t launch_exact_hits(const double* Gtab, int p, const int* U, int nU, const double* lams,
-                              int nlam, uint8_t* hit, cudaStream_t s);
 cudaError_t launch_sqrt(const double* in, double* out, float* inv_sq, float* lam_n,
                         double lambda0, int n, int p, int p_pad, cudaStream_t s);
 cudaError_t launch_syrk_screen(const GramParams& P, int grid, cudaStream_t s);
@@ -200,8 +198,11 @@ size_t tail_prefetch_bytes(int p);
 cudaError_t launch_tail_residuals(const double* Xb, const TailState* tail, int M, const int* nz_rows,
                                   const double* nz_vals, int nzcap, int64_t col_begin, int n,
                                   int n_pad, int nchunk, double* V, cudaStream_t s);
+// hit (optional): hit[l p + c] = 1 for every candidate c = U[.] with some |G_jc| > lams[l], j != c
+// (hit must be zeroed first; only ones are written)
 cudaError_t launch_gram_pass(const double* Xb, int nblk, int nchunk, int n, int p, const double* V,
-                             int M, const int* U, int nU, double* Zz, double* Gtab, cudaStream_t s);
+                             int M, const int* U, int nU, double* Zz, double* Gtab, cudaStream_t s,
+                             uint8_t* hit = nullptr, const double* lams = nullptr, int nlam = 0);
 cudaError_t launch_tail_mark(const TailState* tail, int M, const int* nz_rows, int nzcap, int* umark,
                              cudaStream_t s);
 cudaError_t launch_tail_sweeps(const TailParams& P, int grid, cudaStream_t s);
@@ -238,6 +239,7 @@ cudaError_t launch_column_stats(const int32_t* iters, const int32_t* sweeps, con
                                 int64_t m, unsigned long long* tot, int* mx_sweeps, int* mx_outer,
                                 int* nunc, cudaStream_t s);
 cudaError_t launch_zero_fill(double* a, size_t count, int sms, cudaStream_t s);
+cudaError_t launch_zero_fill_bulk(double* a, size_t count, int grid, cudaStream_t s);
 cudaError_t launch_csc_counts(const int* nz_count, int ncols, int32_t* out, cudaStream_t s);
 cudaError_t launch_assemble(int64_t p, int64_t col_begin, int64_t col_end, const int64_t* col_ptr,
                             const int32_t* rows, const double* vals, const double* sigma_std,
