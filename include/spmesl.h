@@ -117,7 +117,10 @@ typedef struct {
                              candidates) */
   int64_t screen_candidates; /* solver 3: columns the f16 screening could not certify hit-free */
   double  ms_screen;      /* device time of the screening kernel alone (solver 2: the FP64 Gram
-                             kernel; solver 3: the f16 screening kernel incl. Theta's zero fill) */
+                             kernel; solver 3: the f16 screening kernel incl. its share of
+                             Theta's zero fill) */
+  int64_t screen_fill_bytes; /* bytes of Theta the screening kernel zero-filled (the rest of the
+                             fill, if any, ran on a side stream beside the later kernels) */
 } spmesl_stats;
 
 /* Fill *opt with the defaults listed above. */

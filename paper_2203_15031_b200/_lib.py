@@ -62,6 +62,7 @@ class Stats(ctypes.Structure):
         ("ms_gram", ctypes.c_double),
         ("screen_candidates", ctypes.c_int64),
         ("ms_screen", ctypes.c_double),
+        ("screen_fill_bytes", ctypes.c_int64),
     ]
 
     def asdict(self):

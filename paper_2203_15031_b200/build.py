@@ -52,6 +52,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
+        # every symbol must resolve (no GPU needed to load the library)
+        r = subprocess.run(["python3", "-c", f"import ctypes; ctypes.CDLL({LIB!r})"],
+                           capture_output=True, text=True)
+        if r.returncode != 0:
+            os.remove(LIB)
+            raise RuntimeError(f"{LIB} does not load:\n{r.stderr}")
     if verbose:
         print("\n".join(x for x in log if x))
     return LIB

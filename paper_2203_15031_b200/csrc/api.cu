@@ -53,6 +53,7 @@ struct DevCounters {
   unsigned long long joint_maxd;   // mode 1: max |db| of the last sweep (double bits)
   unsigned long long st_sweeps;    // column statistics (column_stats_kernel)
   int st_max_sweeps, st_max_outer, st_unconv, pad4;
+  int s16_nU, pad5;                // solver 3: candidate columns of the certified screening
 };
 
 struct Buffer {
@@ -99,10 +100,8 @@ struct Workspace {
   double* take_zero = nullptr;            // Theta the Gram kernel may zero-fill itself
   size_t take_count = 0;
   std::vector<double> lam_host;           // (pinned-free staging of the penalty levels)
-  std::vector<uint8_t> cand_host;         // certified screening: candidate flags
-  int last_candidates = 0;
-  int gram_fallback = 0;      // solver 3 fell back to the full FP64 Gram kernel (last fit)
   bool zero_join = false;     // part of Theta's zero fill runs on `side` (join ev_join)
+  int64_t screen_fill = 0;    // doubles of Theta the screening kernel zero-filled (last fit)
   int gram_launches = 0;      // kernels fit_gram_enqueue launched (last fit)
   bool init = false;
 };
@@ -642,9 +641,9 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   G.sigma_std = out.sigma_std; G.iters = out.iters; G.sweeps = out.sweeps;
   G.converged = out.conv;
   G.nz_count = (int*)W.nz_count.ptr; G.nz_cur = (int*)W.nz_cur.ptr;
-  bool full_gram = !screen16;
+  const bool full_gram = !screen16;
+  W.screen_fill = screen16 ? 0 : (int64_t)G.zero_count;
   int launches = 0;
-  W.gram_fallback = 0;
   if (screen16) {
     // certified f16 screening (screen16.cu): candidate columns, then their exact FP64 Gram
     // columns and the exact decision; one host round trip for the candidate list
@@ -680,13 +679,16 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
     // Theta's zero fill is split: the screening kernel writes the first part under its
     // contraction, a side-stream kernel the rest while the exact Gram columns and the sweeps
     // (latency-bound, little HBM traffic) run; the caller joins it before the assembly
-    // (measured on config 5: all fused 1.13 ms per fit, half and half 1.02 ms)
-    static const double zfrac = getenv("SPMESL_S16_ZFRAC") ? atof(getenv("SPMESL_S16_ZFRAC")) : 0.5;
+    // (measured on config 5 with the 128 x 256 tiles: all fused 1.04 ms per fit, half and half
+    // 1.03 ms — within noise, so the simpler schedule: the screening kernel writes all of it
+    // at 0.95 of the HBM copy bandwidth)
+    static const double zfrac = getenv("SPMESL_S16_ZFRAC") ? atof(getenv("SPMESL_S16_ZFRAC")) : 1.0;
     size_t zfused = (size_t)(zfrac * (double)G.zero_count) & ~(size_t)1;
     if (zfused > G.zero_count) zfused = G.zero_count;
     Q.zero_ptr = zfused ? G.zero_ptr : nullptr;
     Q.zero_count = zfused;
     if (getenv("SPMESL_DEV_S16_NOZERO")) { Q.zero_ptr = nullptr; Q.zero_count = 0; }   // (dev)
+    W.screen_fill = (int64_t)Q.zero_count;
     CUDA_TRY(cudaEventRecord(W.ev[8], s));
     CUDA_TRY(launch_screen16(Q, std::min(W.sms, Q.tile_end), s));
     CUDA_TRY(cudaEventRecord(W.ev[9], s));
@@ -702,35 +704,26 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
       ++launches;
     }
     launches += 3;   // sqrt, to_f16, screen16
-    W.cand_host.resize(p);
-    CUDA_TRY(cudaMemcpyAsync(W.cand_host.data(), W.cand.ptr, (size_t)p, cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
-    std::vector<int> U;
-    std::vector<int> gstate(p, 0);
-    for (int64_t c = 0; c < p; ++c)
-      if (W.cand_host[c]) { U.push_back((int)c); gstate[c] = 2; }
-    const int nU = (int)U.size();
-    W.last_candidates = nU;
-    if (2 * (int64_t)nU > p) {
-      // most columns are candidates (multi-sweep workloads): the symmetric FP64 Gram kernel
-      // (n p (p+1) flops) is cheaper than nU exact columns (2 n p nU); it decides exactly
-      full_gram = true;
-      G.zero_ptr = nullptr;            // (Theta was zero-filled by the screening pass)
+    // candidate list on the device; then, by its count (read on the device), either the exact
+    // Gram columns of the candidates (2 n p nU flops) or — when most columns are candidates
+    // (multi-sweep workloads) — the symmetric FP64 Gram kernel (n p (p+1) flops) decides
+    // exactly; the kernel not needed exits at once.  No host round trip.
+    int* nU_dev = &dc->s16_nU;
+    CUDA_TRY(launch_cand_compact((const uint8_t*)W.cand.ptr, (int)p, (int*)W.uvars.ptr, nU_dev,
+                                 (int*)W.umap.ptr, s));
+    G.zero_ptr = nullptr;              // (Theta's zero fill is already under way)
+    G.cond_nU = nU_dev;
+    {
       const int nT = (int)((L.nblk + 3) / 4);
       const int ntiles = nT * (nT + 1) / 2;
       CUDA_TRY(launch_syrk_screen(G, std::min(W.sms, ntiles), s));
       if (nlam > 1) CUDA_TRY(launch_level_flags(G, s));
-      launches += 1 + (nlam > 1);
-      W.gram_fallback = 1;
-    } else {
-      CUDA_TRY(cudaMemcpyAsync(W.umap.ptr, gstate.data(), (size_t)p * 4, cudaMemcpyHostToDevice, s));
-      if (nU) CUDA_TRY(cudaMemcpyAsync(W.uvars.ptr, U.data(), (size_t)nU * 4, cudaMemcpyHostToDevice, s));
-      CUDA_TRY(launch_gram_pass((const double*)W.xb.ptr, (int)L.nblk, L.nchunk, (int)n, (int)p,
-                                nullptr, 0, (const int*)W.uvars.ptr, nU, nullptr,
-                                (double*)W.ondemand.ptr, s, (uint8_t*)W.hit.ptr,
-                                (const double*)W.lam_dev.ptr, nlam));
-      launches += 1;
     }
+    CUDA_TRY(launch_gram_cols((const double*)W.xb.ptr, (int)L.nblk, L.nchunk, (int)n, (int)p,
+                              (const int*)W.uvars.ptr, 0, nU_dev, W.sms, (double*)W.ondemand.ptr,
+                              (uint8_t*)W.hit.ptr, (const double*)W.lam_dev.ptr, nlam,
+                              (int*)W.umap.ptr, s));
+    launches += 3 + (nlam > 1);
     CUDA_TRY(cudaEventRecord(W.ev[7], s));
   } else {
     const int nT = (int)((L.nblk + 3) / 4);
@@ -782,13 +775,16 @@ void gram_stats(Workspace& W, int64_t p, int nzcap, spmesl_stats* st, bool scree
   if (!st) return;
   const int nT = (int)((((p + J - 1) / J) + 3) / 4);
   st->solver = screen16 ? 3 : 2;
-  if (screen16) st->screen_candidates = W.last_candidates;
-  st->gram_fallback = W.gram_fallback;
+  if (screen16) {
+    st->screen_candidates = W.host_counters->s16_nU;
+    st->gram_fallback = 2 * (int64_t)W.host_counters->s16_nU > p;
+  }
   st->tile_cols = 0;
   st->num_ctas = std::min(W.sms, nT * (nT + 1) / 2);
   st->kernel_launches += W.gram_launches;
   st->ms_gram = ev_ms(W.ev[1], W.ev[7]);
   st->ms_screen = ev_ms(W.ev[8], W.ev[9]);
+  st->screen_fill_bytes = W.screen_fill * 8;
   st->ms_tail = ev_ms(W.ev[5], W.ev[6]);
   st->tail_columns = W.host_counters->tail_count;
   st->tail_sweeps = W.host_counters->tail_sweeps;

@@ -24,6 +24,7 @@
 // Layout of Y16: tiles of 128 variables x 64 samples, one contiguous 16 KB block per tile
 // ([nblk128][nchunk64][128][64] halves), each 128-byte row's 16-byte chunks XOR-swizzled by
 // (row & 7) so the ldmatrix row fetches hit distinct bank groups.
+#include <algorithm>
 #include <cstdlib>
 #include <cuda_fp16.h>
 #include "spmesl_internal.cuh"
@@ -277,14 +278,26 @@ __global__ void __launch_bounds__(S16_THREADS, 1) screen16_kernel(const Screen16
 // ------------------------------------------------------------------ tcgen05 version
 // The same screening contraction on the 5th-generation tensor cores: the 128 x 64 f16 tiles of
 // Y16 are already the canonical K-major SWIZZLE_128B layout (128-byte rows, 16-byte chunks
-// XOR-ed with row & 7, 1024-byte aligned), so one thread issues tcgen05.mma (M = N = 128,
-// K = 16) straight from the TMA-filled ring into a TMEM accumulator (two 128-column buffers:
-// the epilogue of tile t overlaps the MMAs of tile t + 1), and four epilogue warps read it
-// back with tcgen05.ld.  Roles: warp 0 TMA producer (+ Theta zero fill), warp 1 MMA issuer
-// and TMEM owner, warps 2-9 epilogue (two per TMEM lane quarter, each half of the columns).
+// XOR-ed with row & 7, 1024-byte aligned; two consecutive tiles form the 256-row layout), so
+// one thread issues tcgen05.mma (M = 128, N = BN, K = 16) straight from the TMA-filled ring
+// into a TMEM accumulator (two BN-column buffers: the epilogue of tile t overlaps the MMAs of
+// tile t + 1), and eight epilogue warps read it back with tcgen05.ld.  Roles: warp 0 TMA
+// producer (+ Theta zero fill), warp 1 MMA issuer and TMEM owner, warps 2-9 epilogue (two per
+// TMEM lane quarter, each half of the columns).
+// BN = 256 (default): tiles of 128 rows x 256 columns, 1.5 B of operand traffic per output
+// instead of 2 (the kernel is bound by L2 -> SM operand traffic, not by the tensor cores).
+// Tile set: column block Jb (256 wide) pairs with row blocks I = 0 .. min(2 Jb + 1, ntb - 1),
+// which covers every pair of the upper triangle (plus one redundant 128 x 128 sub-block below
+// the diagonal per column block).
 constexpr int T5_EPI_WARPS = 8;
 constexpr int T5_THREADS = (2 + T5_EPI_WARPS) * 32;
-constexpr int T5_NST = 4;
+
+template <int BN>
+__host__ __device__ constexpr int t5_nst() { return BN == 256 ? 4 : 4; }
+template <int BN>
+__host__ __device__ constexpr size_t t5_smem() {
+  return 1024 + (size_t)t5_nst<BN>() * (1 + BN / 128) * S16_TILE_HALVES * 2 + (size_t)S16_ZPIECE * 8;
+}
 
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
   return (uint64_t)((saddr >> 4) & 0x3FFFu)      // start address
@@ -294,22 +307,42 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
          | ((uint64_t)2 << 61);                   // SWIZZLE_128B
 }
 
+// wide tile t -> (row block I, 256-column block Jb); column block Jb holds min(2 Jb + 2, ntb)
+// tiles, so tiles before block Jb number Jb (Jb + 1) (only the last block can be capped)
+__device__ __forceinline__ void wide_tile(int t, int& I, int& Jb) {
+  int jb = (int)((sqrt(4.0 * (double)t + 1.0) - 1.0) * 0.5);
+  while ((jb + 1) * (jb + 2) <= t) ++jb;
+  while (jb * (jb + 1) > t) --jb;
+  Jb = jb;
+  I = t - jb * (jb + 1);
+}
+
+template <int BN>
+__device__ __forceinline__ void t5_tile(int t, int nT, int& I, int& Jb) {
+  if (BN == 256) wide_tile(t, I, Jb);
+  else tri_tile16(t, nT, I, Jb);
+}
+
+template <int BN>
 __global__ void __launch_bounds__(T5_THREADS, 1) screen16_tc_kernel(const Screen16Params P) {
+  constexpr int NBT = BN / 128;                    // B sub-tiles per stage
+  constexpr int NST = t5_nst<BN>();
+  constexpr int STAGE_HALVES = (1 + NBT) * S16_TILE_HALVES;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // [0, 1024): barriers + TMEM address; ring at 1024 (1024-aligned tiles); zero piece after it
   uint64_t* full = (uint64_t*)smem_raw;
-  uint64_t* empty = full + T5_NST;
-  uint64_t* tfull = empty + T5_NST;
+  uint64_t* empty = full + NST;
+  uint64_t* tfull = empty + NST;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
   __half* ring = (__half*)(smem_raw + 1024);
-  double* zbuf = (double*)(ring + (size_t)T5_NST * 2 * S16_TILE_HALVES);
+  double* zbuf = (double*)(ring + (size_t)NST * STAGE_HALVES);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nT = P.ntb, nchunk = P.nchunk64;
   if (P.zero_ptr)
     for (int e = tid; e < S16_ZPIECE; e += blockDim.x) zbuf[e] = 0.0;
   if (tid == 0) {
-    for (int s = 0; s < T5_NST; ++s) {
+    for (int s = 0; s < NST; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(&full[s])), "r"(1));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(&empty[s])), "r"(1));
     }
@@ -320,9 +353,9 @@ __global__ void __launch_bounds__(T5_THREADS, 1) screen16_tc_kernel(const Screen
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   }
-  if (warp == 1) {   // TMEM: 2 accumulators x 128 columns (f32), 128 lanes
+  if (warp == 1) {   // TMEM: 2 accumulators x BN columns (f32), 128 lanes
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
-                 "r"(256));
+                 "r"(2 * BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -339,28 +372,26 @@ __global__ void __launch_bounds__(T5_THREADS, 1) screen16_tc_kernel(const Screen
       size_t zp = blockIdx.x;
       const size_t zquota = zero_quota(P, npieces, nchunk);
       for (int t = P.tile_begin + blockIdx.x; t < P.tile_end; t += gridDim.x) {
-        int I, Jt;
-        tri_tile16(t, nT, I, Jt);
+        int I, Jb;
+        t5_tile<BN>(t, nT, I, Jb);
         for (int q = 0; q < nchunk; ++q) {
           mbar_wait_s(&empty[s], ph ^ 1u);
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(&full[s])),
-                       "r"(2u * S16_TILE_HALVES * 2u)
+                       "r"((uint32_t)STAGE_HALVES * 2u)
                        : "memory");
-          const __half* srcA = P.Y16 + ((size_t)I * nchunk + q) * S16_TILE_HALVES;
-          const __half* srcB = P.Y16 + ((size_t)Jt * nchunk + q) * S16_TILE_HALVES;
-          __half* dst = ring + (size_t)s * 2 * S16_TILE_HALVES;
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                  su32(dst)),
-              "l"(srcA), "r"((uint32_t)S16_TILE_HALVES * 2u), "r"(su32(&full[s]))
-              : "memory");
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                  su32(dst + S16_TILE_HALVES)),
-              "l"(srcB), "r"((uint32_t)S16_TILE_HALVES * 2u), "r"(su32(&full[s]))
-              : "memory");
+          __half* dst = ring + (size_t)s * STAGE_HALVES;
+#pragma unroll
+          for (int u = 0; u <= NBT; ++u) {   // A tile, then the NBT tiles of the column block
+            const int blk = u == 0 ? I : Jb * NBT + (u - 1);
+            const __half* src = P.Y16 + ((size_t)blk * nchunk + q) * S16_TILE_HALVES;
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                    su32(dst + (size_t)u * S16_TILE_HALVES)),
+                "l"(src), "r"((uint32_t)S16_TILE_HALVES * 2u), "r"(su32(&full[s]))
+                : "memory");
+          }
           zero_pieces(P, zbuf, zp, npieces, zquota);   // Theta's zero fill rides along
-          if (++s == T5_NST) { s = 0; ph ^= 1u; }
+          if (++s == NST) { s = 0; ph ^= 1u; }
         }
       }
       zero_pieces(P, zbuf, zp, npieces, npieces);
@@ -368,8 +399,8 @@ __global__ void __launch_bounds__(T5_THREADS, 1) screen16_tc_kernel(const Screen
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
-    // instruction descriptor: D f32, A = B = f16, both K-major, N = 128, M = 128
-    const uint32_t idesc = (1u << 4) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+    // instruction descriptor: D f32, A = B = f16, both K-major, N = BN, M = 128
+    const uint32_t idesc = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((128u >> 4) << 24);
     int s = 0, it = 0;
     uint32_t ph = 0;
     uint32_t ph_te[2] = {0u, 0u};
@@ -378,12 +409,12 @@ __global__ void __launch_bounds__(T5_THREADS, 1) screen16_tc_kernel(const Screen
       mbar_wait_s(&tempty[ab], ph_te[ab] ^ 1u);     // the epilogue has drained this buffer
       ph_te[ab] ^= 1u;
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      const uint32_t dtm = tmem + (uint32_t)(ab * 128);
+      const uint32_t dtm = tmem + (uint32_t)(ab * BN);
       for (int q = 0; q < nchunk; ++q) {
         mbar_wait_s(&full[s], ph);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         if (lane == 0) {
-          const uint32_t sa = su32(ring + (size_t)s * 2 * S16_TILE_HALVES);
+          const uint32_t sa = su32(ring + (size_t)s * STAGE_HALVES);
           const uint32_t sb = sa + S16_TILE_HALVES * 2;
 #pragma unroll
           for (int kk = 0; kk < S16_KC / 16; ++kk) {
@@ -401,7 +432,7 @@ __global__ void __launch_bounds__(T5_THREADS, 1) screen16_tc_kernel(const Screen
                        : "memory");
         }
         __syncwarp();
-        if (++s == T5_NST) { s = 0; ph ^= 1u; }
+        if (++s == NST) { s = 0; ph ^= 1u; }
       }
       if (lane == 0)   // accumulator complete
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
@@ -413,23 +444,23 @@ __global__ void __launch_bounds__(T5_THREADS, 1) screen16_tc_kernel(const Screen
     // ---------------------------------------------------------------- epilogue (warps 2-9)
     const int qd = warp & 3;                     // TMEM lane quarter this warp may access
     const int half = (warp - 2) >> 2;            // column half of the tile
+    constexpr int GPW = BN / 64;                 // 32-column groups per warp
     int it = 0;
     uint32_t ph_tf[2] = {0u, 0u};
     for (int t = P.tile_begin + blockIdx.x; t < P.tile_end; t += gridDim.x, ++it) {
-      int I, Jt;
-      tri_tile16(t, nT, I, Jt);
+      int I, Jb;
+      t5_tile<BN>(t, nT, I, Jb);
       const int ab = it & 1;
       mbar_wait_s(&tfull[ab], ph_tf[ab]);
       ph_tf[ab] ^= 1u;
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      const bool diag_tile = (I == Jt);
       const int j = I * S16_TB + 32 * qd + lane;          // this thread's row of the tile
       const bool jok = j < P.p;
       const float rA = jok ? P.lam_n[j] : 0.f;
 #pragma unroll 1
-      for (int cg = 2 * half; cg < 2 * half + 2; ++cg) {
+      for (int cg = GPW * half; cg < GPW * half + GPW; ++cg) {
         uint32_t v[32];
-        const uint32_t taddr = tmem + ((uint32_t)(32 * qd) << 16) + (uint32_t)(ab * 128 + 32 * cg);
+        const uint32_t taddr = tmem + ((uint32_t)(32 * qd) << 16) + (uint32_t)(ab * BN + 32 * cg);
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
             "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
@@ -442,7 +473,8 @@ __global__ void __launch_bounds__(T5_THREADS, 1) screen16_tc_kernel(const Screen
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
         if (jok) {
           // thresholds as in screen16_kernel; the 32 columns' factors are warp-uniform loads
-          const int c0 = Jt * S16_TB + 32 * cg;
+          const int c0 = Jb * BN + 32 * cg;
+          const bool diag_sub = (c0 >> 7) == I;           // the 128 x 128 diagonal sub-block
           const float4* iv = reinterpret_cast<const float4*>(P.inv_sq + c0);
           uint32_t hits = 0;
 #pragma unroll
@@ -453,12 +485,12 @@ __global__ void __launch_bounds__(T5_THREADS, 1) screen16_tc_kernel(const Screen
             hits |= (uint32_t)(fabsf(__uint_as_float(v[4 * k4 + 2])) > __fmaf_rd(rA, f.z, -P.epsn)) << (4 * k4 + 2);
             hits |= (uint32_t)(fabsf(__uint_as_float(v[4 * k4 + 3])) > __fmaf_rd(rA, f.w, -P.epsn)) << (4 * k4 + 3);
           }
-          if (diag_tile && (unsigned)(j - c0) < 32u) hits &= ~(1u << (j - c0));   // c == j
+          if (diag_sub && (unsigned)(j - c0) < 32u) hits &= ~(1u << (j - c0));   // c == j
           while (hits) {   // rare
             const int i = __ffs(hits) - 1;
             hits &= hits - 1;
             P.cand[c0 + i] = 1;
-            if (!diag_tile) P.cand[j] = 1;
+            if (!diag_sub) P.cand[j] = 1;
           }
         }
       }
@@ -472,7 +504,25 @@ __global__ void __launch_bounds__(T5_THREADS, 1) screen16_tc_kernel(const Screen
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   if (warp == 1)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(256));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(2 * BN));
+}
+
+// Candidate list on the device (no host round trip): U[0..nU) = {c : cand[c]} in any order
+// (every consumer indexes its results by c), gstate[c] = 2 for candidates (their Gram column
+// will be present), 0 otherwise.
+__global__ void cand_compact_kernel(const uint8_t* __restrict__ cand, int p, int* __restrict__ U,
+                                    int* __restrict__ nU, int* __restrict__ gstate) {
+  const int lane = threadIdx.x & 31;
+  for (int base = blockIdx.x * blockDim.x; base < p; base += gridDim.x * blockDim.x) {
+    const int c = base + threadIdx.x;
+    const bool f = c < p && cand[c];
+    if (c < p) gstate[c] = f ? 2 : 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, f);
+    int first = 0;
+    if (lane == 0 && bal) first = atomicAdd(nU, __popc(bal));
+    first = __shfl_sync(0xffffffffu, first, 0);
+    if (f) U[first + __popc(bal & ((1u << lane) - 1u))] = c;
+  }
 }
 
 __global__ void sqrt_kernel(const double* __restrict__ in, double* __restrict__ out,
@@ -493,32 +543,55 @@ __global__ void sqrt_kernel(const double* __restrict__ in, double* __restrict__ 
 
 }  // namespace
 
+cudaError_t launch_cand_compact(const uint8_t* cand, int p, int* U, int* nU, int* gstate,
+                                cudaStream_t s) {
+  const int blocks = std::max(1, std::min(296, (p + 255) / 256));
+  cand_compact_kernel<<<blocks, 256, 0, s>>>(cand, p, U, nU, gstate);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_sqrt(const double* in, double* out, float* inv_sq, float* lam_n,
                         double lambda0, int n, int p, int p_pad, cudaStream_t s) {
   sqrt_kernel<<<(p_pad + 255) / 256, 256, 0, s>>>(in, out, inv_sq, lam_n, lambda0, n, p, p_pad);
   return cudaGetLastError();
 }
 
-size_t screen16_y_halves(int64_t p, int n_pad) {
-  const int64_t nb = (p + S16_TB - 1) / S16_TB;
-  const int64_t nc = (n_pad + S16_KC - 1) / S16_KC;
-  return (size_t)(nb * nc * S16_TILE_HALVES);
+// which tcgen05 tile width runs (256 default; SPMESL_S16_BN=128 for the square-tile variant)
+static int s16_bn() {
+  static const int bn = getenv("SPMESL_S16_BN") ? atoi(getenv("SPMESL_S16_BN")) : 256;
+  return bn == 128 ? 128 : 256;
+}
+static bool s16_mma_sync() {
+  static const bool v = getenv("SPMESL_S16_MMA_SYNC") && atoi(getenv("SPMESL_S16_MMA_SYNC"));
+  return v;
 }
 
-int64_t screen16_pad(int64_t p) { return (p + S16_TB - 1) / S16_TB * S16_TB; }
-
-int screen16_tile_count(int64_t p) {
-  const int64_t nT = (p + S16_TB - 1) / S16_TB;
-  return (int)(nT * (nT + 1) / 2);
+// Y16 holds an even number of 128-row tiles (the 256-column blocks read two; the padding
+// tiles are zero)
+size_t screen16_y_halves(int64_t p, int n_pad) {
+  const int64_t nb = (p + 2 * S16_TB - 1) / (2 * S16_TB) * 2;
+  const int64_t nc = (n_pad + S16_KC - 1) / S16_KC;
+  return (size_t)(nb * nc * S16_TILE_HALVES);
 }
 
 double screen16_eps(int n_pad) {
   return 2.1 * 0x1p-11 + (double)n_pad * 0x1p-22 + 0x1p-23 + 0x1p-20;
 }
 
+int64_t screen16_pad(int64_t p) { return (p + 2 * S16_TB - 1) / (2 * S16_TB) * (2 * S16_TB); }
+
+int screen16_tile_count(int64_t p) {
+  const int64_t nT = (p + S16_TB - 1) / S16_TB;
+  if (s16_mma_sync() || s16_bn() == 128) return (int)(nT * (nT + 1) / 2);
+  const int64_t ncb = (nT + 1) / 2;
+  int64_t tot = 0;
+  for (int64_t jb = 0; jb < ncb; ++jb) tot += std::min<int64_t>(2 * jb + 2, nT);
+  return (int)tot;
+}
+
 cudaError_t launch_to_f16(const double* Xb, const double* nrm, int p, int n_pad, int nchunk32,
                           __half* Y16, cudaStream_t s) {
-  const int nb = (p + S16_TB - 1) / S16_TB;
+  const int nb = (p + 2 * S16_TB - 1) / (2 * S16_TB) * 2;
   const int nc = (n_pad + S16_KC - 1) / S16_KC;
   dim3 grid((unsigned)nb, (unsigned)nc);
   to_f16_kernel<<<grid, 256, 0, s>>>(Xb, nrm, p, nchunk32, nc, Y16);
@@ -527,14 +600,21 @@ cudaError_t launch_to_f16(const double* Xb, const double* nrm, int p, int n_pad,
 
 cudaError_t launch_screen16(const Screen16Params& P, int grid, cudaStream_t s) {
   if (P.tile_end <= P.tile_begin) return cudaSuccess;
-  static const bool mma_sync = getenv("SPMESL_S16_MMA_SYNC") && atoi(getenv("SPMESL_S16_MMA_SYNC"));
-  if (!mma_sync) {   // tcgen05 (default)
-    const size_t smem = 1024 + (size_t)T5_NST * 2 * S16_TILE_HALVES * 2 + (size_t)S16_ZPIECE * 8;
+  if (!s16_mma_sync()) {   // tcgen05 (default)
     static_assert(T5_EPI_WARPS == 8, "epilogue: two warps per TMEM lane quarter");
-    cudaError_t e = cudaFuncSetAttribute(screen16_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-    screen16_tc_kernel<<<grid, T5_THREADS, smem, s>>>(P);
+    if (s16_bn() == 256) {
+      cudaError_t e = cudaFuncSetAttribute(screen16_tc_kernel<256>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)t5_smem<256>());
+      if (e != cudaSuccess) return e;
+      screen16_tc_kernel<256><<<grid, T5_THREADS, t5_smem<256>(), s>>>(P);
+    } else {
+      cudaError_t e = cudaFuncSetAttribute(screen16_tc_kernel<128>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)t5_smem<128>());
+      if (e != cudaSuccess) return e;
+      screen16_tc_kernel<128><<<grid, T5_THREADS, t5_smem<128>(), s>>>(P);
+    }
     return cudaGetLastError();
   }
   const size_t smem = 128 + (size_t)S16_NST * 2 * S16_TILE_HALVES * 2 + (size_t)S16_ZPIECE * 8;

@@ -151,6 +151,7 @@ struct GramParams {
   int tile_begin, tile_end;   // upper-triangle tiles to process (multi-GPU share)
   double* zero_ptr;        // optional: zero-filled by the producer's bulk stores (Theta)
   size_t zero_count;       // doubles (even; zero_ptr 16-byte aligned)
+  const int* cond_nU;      // optional: run only if 2 * *cond_nU > p (solver 3 fallback)
   TailState* tail;         // columns for the sweep kernel
   int* tail_count;
   double* sigma_std;
@@ -183,6 +184,8 @@ double screen16_eps(int n_pad);
 cudaError_t launch_to_f16(const double* Xb, const double* nrm, int p, int n_pad, int nchunk32,
                           __half* Y16, cudaStream_t s);
 cudaError_t launch_screen16(const Screen16Params& P, int grid, cudaStream_t s);
+cudaError_t launch_cand_compact(const uint8_t* cand, int p, int* U, int* nU, int* gstate,
+                                cudaStream_t s);
 cudaError_t launch_sqrt(const double* in, double* out, float* inv_sq, float* lam_n,
                         double lambda0, int n, int p, int p_pad, cudaStream_t s);
 cudaError_t launch_syrk_screen(const GramParams& P, int grid, cudaStream_t s);
@@ -198,6 +201,11 @@ size_t tail_prefetch_bytes(int p);
 cudaError_t launch_tail_residuals(const double* Xb, const TailState* tail, int M, const int* nz_rows,
                                   const double* nz_vals, int nzcap, int64_t col_begin, int n,
                                   int n_pad, int nchunk, double* V, cudaStream_t s);
+// Exact Gram columns of a candidate list U (count nU, or *nU_dev read on the device; with a
+// device count and 2 nU > p the kernel only sets gstate[:] = 2 — the full Gram kernel decides)
+cudaError_t launch_gram_cols(const double* Xb, int nblk, int nchunk, int n, int p, const int* U,
+                             int nU, const int* nU_dev, int sms, double* Gtab, uint8_t* hit,
+                             const double* lams, int nlam, int* gstate, cudaStream_t s);
 // hit (optional): hit[l p + c] = 1 for every candidate c = U[.] with some |G_jc| > lams[l], j != c
 // (hit must be zeroed first; only ones are written)
 cudaError_t launch_gram_pass(const double* Xb, int nblk, int nchunk, int n, int p, const double* V,

@@ -189,8 +189,8 @@ __global__ void __launch_bounds__(256) gram_pass_kernel(const double* __restrict
 // per output the same DMMA chain as gram_tile (chunks ascending, k-pairs 0..3, even then odd
 // sample), so every caller sees bit-identical columns.  Optional exact screening decision as
 // in gram_tile.
-constexpr int GC_NTMAX = 16;            // n-tiles of 8 vectors per CTA
-constexpr int GC_STAGES = 3;
+constexpr int GC_NTMAX = 16;            // n-tiles of 8 vectors per vector group (128 columns)
+constexpr int GC_STAGES = 2;            // 2 x 48 KB: two CTAs per SM
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
@@ -199,83 +199,98 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
                : "memory");
 }
 
+// nU_dev (optional): the candidate count is read on the device; when 2 nU > p the full Gram
+// kernel decides instead (solver 3 fallback): this kernel then only marks every column of its
+// rows present (gstate = 2) and exits.
 __global__ void __launch_bounds__(256, 2) gram_cols_kernel(const double* __restrict__ Xb, int nchunk,
                                                            int n, int p, int nblk,
-                                                           const int* __restrict__ U, int nU,
+                                                           const int* __restrict__ U, int nU_host,
+                                                           const int* __restrict__ nU_dev,
                                                            double* __restrict__ Gtab,
                                                            uint8_t* __restrict__ hit,
-                                                           const double* __restrict__ lams, int nlam) {
+                                                           const double* __restrict__ lams, int nlam,
+                                                           int* __restrict__ gstate) {
   extern __shared__ __align__(128) double gsm[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t4 = lane & 3, sw = g & 1;
   const int b0 = blockIdx.x * 2;
-  const int v0 = blockIdx.y * (GC_NTMAX * 8);
-  const int nvec = min(nU - v0, GC_NTMAX * 8);
-  const int ntc = (nvec + 7) >> 3;
-  const int stage_d = 2 * CHUNK_DOUBLES + ntc * 8 * XS;
-  auto load = [&](int q, int st) {
-    double* sx = gsm + (size_t)st * stage_d;
-    double* sv = sx + 2 * CHUNK_DOUBLES;
-    for (int e = tid; e < CHUNK_DOUBLES; e += 256) {       // 2 blocks x 512 pieces of 16 B
-      const int bb = e >> 9, r = e & 511;
-      if (b0 + bb < nblk)
-        cp_async16(sx + bb * CHUNK_DOUBLES + 2 * r,
-                   Xb + ((size_t)(b0 + bb) * nchunk + q) * CHUNK_DOUBLES + 2 * r);
-    }
-    for (int e = tid; e < nvec * 16; e += 256) {           // candidate rows, 16 pieces each
-      const int v = e >> 4, pos = 2 * (e & 15);
-      const int u = U[v0 + v];
-      const double* src = Xb + (((size_t)(u / J) * nchunk + q) * J + (u % J)) * XS;
-      cp_async16(sv + v * XS + (pos ^ (((u ^ v) & 1) << 3)), src + pos);
-    }
-  };
-  double acc[GC_NTMAX][2];
-#pragma unroll
-  for (int t = 0; t < GC_NTMAX; ++t) acc[t][0] = acc[t][1] = 0.0;
+  const int nU = nU_dev ? *(volatile const int*)nU_dev : nU_host;
+  if (nU_dev && 2 * (int64_t)nU > p) {
+    if (gstate && blockIdx.y == 0)
+      for (int r = b0 * J + tid; r < min(p, (b0 + 2) * J); r += blockDim.x) gstate[r] = 2;
+    return;
+  }
+  const int stage_d = 2 * CHUNK_DOUBLES + GC_NTMAX * 8 * XS;
   const int bb = warp >> 2, mt = warp & 3;
-#pragma unroll
-  for (int q = 0; q < GC_STAGES - 1; ++q) {
-    if (q < nchunk) load(q, q);
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-  }
-  for (int q = 0; q < nchunk; ++q) {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(GC_STAGES - 2) : "memory");
-    __syncthreads();
-    if (q + GC_STAGES - 1 < nchunk) load(q + GC_STAGES - 1, (q + GC_STAGES - 1) % GC_STAGES);
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-    const double* sx = gsm + (size_t)(q % GC_STAGES) * stage_d;
-    const double* sv = sx + 2 * CHUNK_DOUBLES;
-    const double* xa = sx + bb * CHUNK_DOUBLES + (mt * 8 + g) * XS + 2 * t4;
-#pragma unroll
-    for (int kp = 0; kp < KC / 8; ++kp) {
-      const double2 a = *(const double2*)(xa + (kp ^ sw) * 8);
-#pragma unroll
-      for (int t = 0; t < GC_NTMAX; ++t) {
-        if (t < ntc) {
-          const double2 b2 = *(const double2*)(sv + (t * 8 + g) * XS + 2 * t4 + (kp ^ sw) * 8);
-          dmma_t(acc[t][0], acc[t][1], a.x, b2.x);
-          dmma_t(acc[t][0], acc[t][1], a.y, b2.y);
-        }
-      }
-    }
-  }
   const double inv_n = 1.0 / (double)n;
   const int row = (b0 + bb) * J + mt * 8 + g;
-  if (row >= p) return;
-#pragma unroll
-  for (int t = 0; t < GC_NTMAX; ++t)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int v = t * 8 + 2 * t4 + e;
-      if (t < ntc && v < nvec) {
-        const int c = U[v0 + v];
-        const double g_rc = acc[t][e] * inv_n;
-        Gtab[(size_t)c * p + row] = g_rc;
-        if (hit && row != c)   // exact screening decision: some |S_jc| > lambda, j != c
-          for (int l = 0; l < nlam; ++l)
-            if (fabs(g_rc) > lams[l]) hit[(size_t)l * p + c] = 1;
+  for (int v0 = blockIdx.y * GC_NTMAX * 8; v0 < nU; v0 += gridDim.y * GC_NTMAX * 8) {
+    const int nvec = min(nU - v0, GC_NTMAX * 8);
+    const int ntc = (nvec + 7) >> 3;
+    auto load = [&](int q, int st) {
+      double* sx = gsm + (size_t)st * stage_d;
+      double* sv = sx + 2 * CHUNK_DOUBLES;
+      for (int e = tid; e < CHUNK_DOUBLES; e += 256) {       // 2 blocks x 512 pieces of 16 B
+        const int bq = e >> 9, r = e & 511;
+        if (b0 + bq < nblk)
+          cp_async16(sx + bq * CHUNK_DOUBLES + 2 * r,
+                     Xb + ((size_t)(b0 + bq) * nchunk + q) * CHUNK_DOUBLES + 2 * r);
       }
+      for (int e = tid; e < nvec * 16; e += 256) {           // candidate rows, 16 pieces each
+        const int v = e >> 4, pos = 2 * (e & 15);
+        const int u = U[v0 + v];
+        const double* src = Xb + (((size_t)(u / J) * nchunk + q) * J + (u % J)) * XS;
+        cp_async16(sv + v * XS + (pos ^ (((u ^ v) & 1) << 3)), src + pos);
+      }
+    };
+    double acc[GC_NTMAX][2];
+#pragma unroll
+    for (int t = 0; t < GC_NTMAX; ++t) acc[t][0] = acc[t][1] = 0.0;
+    __syncthreads();   // the previous group's last stage has been read
+#pragma unroll
+    for (int q = 0; q < GC_STAGES - 1; ++q) {
+      if (q < nchunk) load(q, q);
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
+    for (int q = 0; q < nchunk; ++q) {
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(GC_STAGES - 2) : "memory");
+      __syncthreads();
+      if (q + GC_STAGES - 1 < nchunk) load(q + GC_STAGES - 1, (q + GC_STAGES - 1) % GC_STAGES);
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+      const double* sx = gsm + (size_t)(q % GC_STAGES) * stage_d;
+      const double* sv = sx + 2 * CHUNK_DOUBLES;
+      const double* xa = sx + bb * CHUNK_DOUBLES + (mt * 8 + g) * XS + 2 * t4;
+#pragma unroll
+      for (int kp = 0; kp < KC / 8; ++kp) {
+        const double2 a = *(const double2*)(xa + (kp ^ sw) * 8);
+#pragma unroll
+        for (int t = 0; t < GC_NTMAX; ++t) {
+          if (t < ntc) {
+            const double2 b2 = *(const double2*)(sv + (t * 8 + g) * XS + 2 * t4 + (kp ^ sw) * 8);
+            dmma_t(acc[t][0], acc[t][1], a.x, b2.x);
+            dmma_t(acc[t][0], acc[t][1], a.y, b2.y);
+          }
+        }
+      }
+      if (GC_STAGES == 2) __syncthreads();   // stage q % 2 is reloaded next iteration
+    }
+    if (row < p) {
+#pragma unroll
+      for (int t = 0; t < GC_NTMAX; ++t)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int v = t * 8 + 2 * t4 + e;
+          if (t < ntc && v < nvec) {
+            const int c = U[v0 + v];
+            const double g_rc = acc[t][e] * inv_n;
+            Gtab[(size_t)c * p + row] = g_rc;
+            if (hit && row != c)   // exact screening decision: some |S_jc| > lambda, j != c
+              for (int l = 0; l < nlam; ++l)
+                if (fabs(g_rc) > lams[l]) hit[(size_t)l * p + c] = 1;
+          }
+        }
+    }
+  }
 }
 
 // mark the active variables of the handed-over columns (umark[j] = 1)
@@ -557,22 +572,38 @@ cudaError_t launch_tail_residuals(const double* Xb, const TailState* tail, int M
   return cudaGetLastError();
 }
 
+cudaError_t launch_gram_cols(const double* Xb, int nblk, int nchunk, int n, int p, const int* U,
+                             int nU, const int* nU_dev, int sms, double* Gtab, uint8_t* hit,
+                             const double* lams, int nlam, int* gstate, cudaStream_t s) {
+  if (!nU_dev && nU <= 0) return cudaSuccess;
+  const size_t smem = (size_t)GC_STAGES * (2 * CHUNK_DOUBLES + GC_NTMAX * 8 * XS) * 8;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gram_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int gx = (nblk + 1) / 2;
+  // vector groups: all of them for a host count; for a device count, enough CTAs to fill the
+  // GPU twice over (each loops over its groups)
+  int gy = nU_dev ? std::max(1, std::min((p + GC_NTMAX * 8 - 1) / (GC_NTMAX * 8), 2 * std::max(sms, 1) / gx))
+                  : (nU + GC_NTMAX * 8 - 1) / (GC_NTMAX * 8);
+  dim3 g2((unsigned)gx, (unsigned)gy);
+  gram_cols_kernel<<<g2, 256, smem, s>>>(Xb, nchunk, n, p, nblk, U, nU, nU_dev, Gtab, hit, lams,
+                                         nlam, gstate);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_gram_pass(const double* Xb, int nblk, int nchunk, int n, int p, const double* V,
                              int M, const int* U, int nU, double* Zz, double* Gtab, cudaStream_t s,
                              uint8_t* hit, const double* lams, int nlam) {
   const int ntile = (M + nU + 31) / 32;
   if (ntile == 0) return cudaSuccess;
   static const bool old_pass = getenv("SPMESL_DEV_OLD_GRAM_PASS") != nullptr;   // (dev)
-  if (M == 0 && !old_pass) {
-    const int ntc = (std::min(nU, GC_NTMAX * 8) + 7) / 8;
-    const size_t smem = (size_t)GC_STAGES * (2 * CHUNK_DOUBLES + ntc * 8 * XS) * 8;
-    cudaError_t e = cudaFuncSetAttribute(gram_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-    dim3 g2((unsigned)((nblk + 1) / 2), (unsigned)((nU + GC_NTMAX * 8 - 1) / (GC_NTMAX * 8)));
-    gram_cols_kernel<<<g2, 256, smem, s>>>(Xb, nchunk, n, p, nblk, U, nU, Gtab, hit, lams, nlam);
-    return cudaGetLastError();
-  }
+  if (M == 0 && !old_pass)
+    return launch_gram_cols(Xb, nblk, nchunk, n, p, U, nU, nullptr, 0, Gtab, hit, lams, nlam,
+                            nullptr, s);
   dim3 grid((unsigned)nblk, (unsigned)ntile);
   // n_pad is implied by nchunk
   gram_pass_kernel<<<grid, 256, 0, s>>>(Xb, nchunk, n, p, V, M, U, nU, nchunk * KC, Zz, Gtab, hit,
