@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(256) gram_pass_kernel(const double* __restrict
 // sample), so every caller sees bit-identical columns.  Optional exact screening decision as
 // in gram_tile.
 constexpr int GC_NTMAX = 16;            // n-tiles of 8 vectors per vector group (128 columns)
-constexpr int GC_STAGES = 2;            // 2 x 48 KB: two CTAs per SM
+constexpr int GC_STAGES = 3;            // 3 x (34 + 32) KB at 17 warps
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
@@ -202,93 +202,115 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 // nU_dev (optional): the candidate count is read on the device; when 2 nU > p the full Gram
 // kernel decides instead (solver 3 fallback): this kernel then only marks every column of its
 // rows present (gstate = 2) and exits.
-__global__ void __launch_bounds__(256, 2) gram_cols_kernel(const double* __restrict__ Xb, int nchunk,
-                                                           int n, int p, int nblk,
-                                                           const int* __restrict__ U, int nU_host,
-                                                           const int* __restrict__ nU_dev,
-                                                           double* __restrict__ Gtab,
-                                                           uint8_t* __restrict__ hit,
-                                                           const double* __restrict__ lams, int nlam,
-                                                           int* __restrict__ gstate) {
+// Work split: one CTA per SM with T <= 17 warps, one 8-row m-tile per warp; CTA i owns a
+// balanced contiguous range of m-tiles and walks it in rounds of T (one round when
+// p <= 8 T #SMs: 17 warps x 148 SMs cover p = 20000 in one round, so no SM runs a second wave).
+constexpr int GC_MAXW = 17;
+__global__ void __launch_bounds__(GC_MAXW * 32, 1) gram_cols_kernel(const double* __restrict__ Xb,
+                                                                 int nchunk, int n, int p,
+                                                                 const int* __restrict__ U, int nU_host,
+                                                                 const int* __restrict__ nU_dev,
+                                                                 double* __restrict__ Gtab,
+                                                                 uint8_t* __restrict__ hit,
+                                                                 const double* __restrict__ lams,
+                                                                 int nlam, int* __restrict__ gstate) {
   extern __shared__ __align__(128) double gsm[];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nthr = blockDim.x;
+  const int T = nthr >> 5;
   const int g = lane >> 2, t4 = lane & 3, sw = g & 1;
-  const int b0 = blockIdx.x * 2;
+  const int nmt = (p + 7) / 8;
+  const int m0 = (int)((int64_t)blockIdx.x * nmt / gridDim.x);
+  const int m1 = (int)((int64_t)(blockIdx.x + 1) * nmt / gridDim.x);
   const int nU = nU_dev ? *(volatile const int*)nU_dev : nU_host;
   if (nU_dev && 2 * (int64_t)nU > p) {
-    if (gstate && blockIdx.y == 0)
-      for (int r = b0 * J + tid; r < min(p, (b0 + 2) * J); r += blockDim.x) gstate[r] = 2;
+    if (gstate)
+      for (int r = m0 * 8 + tid; r < min(p, m1 * 8); r += nthr) gstate[r] = 2;
     return;
   }
-  const int stage_d = 2 * CHUNK_DOUBLES + GC_NTMAX * 8 * XS;
-  const int bb = warp >> 2, mt = warp & 3;
+  const int xrows = T * 8;
+  const int stage_d = xrows * XS + GC_NTMAX * 8 * XS;
   const double inv_n = 1.0 / (double)n;
-  const int row = (b0 + bb) * J + mt * 8 + g;
-  for (int v0 = blockIdx.y * GC_NTMAX * 8; v0 < nU; v0 += gridDim.y * GC_NTMAX * 8) {
+  for (int v0 = 0; v0 < nU; v0 += GC_NTMAX * 8) {
     const int nvec = min(nU - v0, GC_NTMAX * 8);
     const int ntc = (nvec + 7) >> 3;
-    auto load = [&](int q, int st) {
-      double* sx = gsm + (size_t)st * stage_d;
-      double* sv = sx + 2 * CHUNK_DOUBLES;
-      for (int e = tid; e < CHUNK_DOUBLES; e += 256) {       // 2 blocks x 512 pieces of 16 B
-        const int bq = e >> 9, r = e & 511;
-        if (b0 + bq < nblk)
-          cp_async16(sx + bq * CHUNK_DOUBLES + 2 * r,
-                     Xb + ((size_t)(b0 + bq) * nchunk + q) * CHUNK_DOUBLES + 2 * r);
+    for (int r0 = m0; r0 < m1; r0 += T) {
+      const int mcnt = min(T, m1 - r0);
+      const bool active = warp < mcnt;
+      auto load = [&](int q, int st) {
+        double* sx = gsm + (size_t)st * stage_d;
+        double* sv = sx + xrows * XS;
+        for (int e = tid; e < mcnt * 128; e += nthr) {     // m-tile rows: 2 KB contiguous each
+          const int lm = e >> 7, r = e & 127;
+          const int mt = r0 + lm;
+          const double* src = Xb + (((size_t)(mt >> 2) * nchunk + q) * J + (mt & 3) * 8) * XS;
+          cp_async16(sx + lm * 8 * XS + 2 * r, src + 2 * r);
+        }
+        for (int e = tid; e < nvec * 16; e += nthr) {      // candidate rows, 16 pieces each
+          const int v = e >> 4, pos = 2 * (e & 15);
+          const int u = U[v0 + v];
+          const double* src = Xb + (((size_t)(u / J) * nchunk + q) * J + (u % J)) * XS;
+          cp_async16(sv + v * XS + (pos ^ (((u ^ v) & 1) << 3)), src + pos);
+        }
+      };
+      double acc[GC_NTMAX][2];
+#pragma unroll
+      for (int t = 0; t < GC_NTMAX; ++t) acc[t][0] = acc[t][1] = 0.0;
+      __syncthreads();   // the previous round's stages have been read
+#pragma unroll
+      for (int q = 0; q < GC_STAGES - 1; ++q) {
+        if (q < nchunk) load(q, q);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
       }
-      for (int e = tid; e < nvec * 16; e += 256) {           // candidate rows, 16 pieces each
-        const int v = e >> 4, pos = 2 * (e & 15);
-        const int u = U[v0 + v];
-        const double* src = Xb + (((size_t)(u / J) * nchunk + q) * J + (u % J)) * XS;
-        cp_async16(sv + v * XS + (pos ^ (((u ^ v) & 1) << 3)), src + pos);
-      }
-    };
-    double acc[GC_NTMAX][2];
+      for (int q = 0; q < nchunk; ++q) {
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(GC_STAGES - 2) : "memory");
+        __syncthreads();
+        if (q + GC_STAGES - 1 < nchunk) load(q + GC_STAGES - 1, (q + GC_STAGES - 1) % GC_STAGES);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        if (active) {
+          const double* sx = gsm + (size_t)(q % GC_STAGES) * stage_d;
+          const double* sv = sx + xrows * XS;
+          const double* xa = sx + (warp * 8 + g) * XS + 2 * t4;
 #pragma unroll
-    for (int t = 0; t < GC_NTMAX; ++t) acc[t][0] = acc[t][1] = 0.0;
-    __syncthreads();   // the previous group's last stage has been read
+          for (int kp = 0; kp < KC / 8; ++kp) {
+            const double2 a = *(const double2*)(xa + (kp ^ sw) * 8);
+            // groups of 4 n-tiles: the even samples of the group, then the odd ones — per
+            // output the chain is unchanged (even then odd), consecutive DMMAs are independent
 #pragma unroll
-    for (int q = 0; q < GC_STAGES - 1; ++q) {
-      if (q < nchunk) load(q, q);
-      asm volatile("cp.async.commit_group;\n" ::: "memory");
-    }
-    for (int q = 0; q < nchunk; ++q) {
-      asm volatile("cp.async.wait_group %0;\n" ::"n"(GC_STAGES - 2) : "memory");
-      __syncthreads();
-      if (q + GC_STAGES - 1 < nchunk) load(q + GC_STAGES - 1, (q + GC_STAGES - 1) % GC_STAGES);
-      asm volatile("cp.async.commit_group;\n" ::: "memory");
-      const double* sx = gsm + (size_t)(q % GC_STAGES) * stage_d;
-      const double* sv = sx + 2 * CHUNK_DOUBLES;
-      const double* xa = sx + bb * CHUNK_DOUBLES + (mt * 8 + g) * XS + 2 * t4;
+            for (int t0 = 0; t0 < GC_NTMAX; t0 += 4) {
+              if (t0 < ntc) {
+                double2 b2[4];
 #pragma unroll
-      for (int kp = 0; kp < KC / 8; ++kp) {
-        const double2 a = *(const double2*)(xa + (kp ^ sw) * 8);
+                for (int u = 0; u < 4; ++u)
+                  if (t0 + u < ntc)
+                    b2[u] = *(const double2*)(sv + ((t0 + u) * 8 + g) * XS + 2 * t4 + (kp ^ sw) * 8);
 #pragma unroll
-        for (int t = 0; t < GC_NTMAX; ++t) {
-          if (t < ntc) {
-            const double2 b2 = *(const double2*)(sv + (t * 8 + g) * XS + 2 * t4 + (kp ^ sw) * 8);
-            dmma_t(acc[t][0], acc[t][1], a.x, b2.x);
-            dmma_t(acc[t][0], acc[t][1], a.y, b2.y);
+                for (int u = 0; u < 4; ++u)
+                  if (t0 + u < ntc) dmma_t(acc[t0 + u][0], acc[t0 + u][1], a.x, b2[u].x);
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                  if (t0 + u < ntc) dmma_t(acc[t0 + u][0], acc[t0 + u][1], a.y, b2[u].y);
+              }
+            }
           }
         }
       }
-      if (GC_STAGES == 2) __syncthreads();   // stage q % 2 is reloaded next iteration
-    }
-    if (row < p) {
+      const int row = (r0 + warp) * 8 + g;
+      if (active && row < p) {
 #pragma unroll
-      for (int t = 0; t < GC_NTMAX; ++t)
+        for (int t = 0; t < GC_NTMAX; ++t)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int v = t * 8 + 2 * t4 + e;
-          if (t < ntc && v < nvec) {
-            const int c = U[v0 + v];
-            const double g_rc = acc[t][e] * inv_n;
-            Gtab[(size_t)c * p + row] = g_rc;
-            if (hit && row != c)   // exact screening decision: some |S_jc| > lambda, j != c
-              for (int l = 0; l < nlam; ++l)
-                if (fabs(g_rc) > lams[l]) hit[(size_t)l * p + c] = 1;
+          for (int e = 0; e < 2; ++e) {
+            const int v = t * 8 + 2 * t4 + e;
+            if (t < ntc && v < nvec) {
+              const int c = U[v0 + v];
+              const double g_rc = acc[t][e] * inv_n;
+              Gtab[(size_t)c * p + row] = g_rc;
+              if (hit && row != c)   // exact screening decision: some |S_jc| > lambda, j != c
+                for (int l = 0; l < nlam; ++l)
+                  if (fabs(g_rc) > lams[l]) hit[(size_t)l * p + c] = 1;
+            }
           }
-        }
+      }
     }
   }
 }
@@ -576,22 +598,33 @@ cudaError_t launch_gram_cols(const double* Xb, int nblk, int nchunk, int n, int 
                              int nU, const int* nU_dev, int sms, double* Gtab, uint8_t* hit,
                              const double* lams, int nlam, int* gstate, cudaStream_t s) {
   if (!nU_dev && nU <= 0) return cudaSuccess;
-  const size_t smem = (size_t)GC_STAGES * (2 * CHUNK_DOUBLES + GC_NTMAX * 8 * XS) * 8;
+  if (sms <= 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 1;
+  }
+  static int max_warps = 0;
+  if (!max_warps) {
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, gram_cols_kernel) != cudaSuccess) return cudaGetLastError();
+    max_warps = std::max(1, std::min(GC_MAXW, fa.maxThreadsPerBlock / 32));
+    if (getenv("SPMESL_DEV_GC_DEBUG"))
+      fprintf(stderr, "gram_cols: maxThreadsPerBlock %d numRegs %d\n", fa.maxThreadsPerBlock, fa.numRegs);
+  }
+  const int nmt = (p + 7) / 8;
+  const int T = std::max(1, std::min(max_warps, (nmt + sms - 1) / sms));
+  const int grid = std::max(1, std::min(sms, (nmt + T - 1) / T));
+  const size_t smem = (size_t)GC_STAGES * (T * 8 * XS + GC_NTMAX * 8 * XS) * 8;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(gram_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+                                         (int)((size_t)GC_STAGES * (GC_MAXW * 8 * XS + GC_NTMAX * 8 * XS) * 8));
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int gx = (nblk + 1) / 2;
-  // vector groups: all of them for a host count; for a device count, enough CTAs to fill the
-  // GPU twice over (each loops over its groups)
-  int gy = nU_dev ? std::max(1, std::min((p + GC_NTMAX * 8 - 1) / (GC_NTMAX * 8), 2 * std::max(sms, 1) / gx))
-                  : (nU + GC_NTMAX * 8 - 1) / (GC_NTMAX * 8);
-  dim3 g2((unsigned)gx, (unsigned)gy);
-  gram_cols_kernel<<<g2, 256, smem, s>>>(Xb, nchunk, n, p, nblk, U, nU, nU_dev, Gtab, hit, lams,
-                                         nlam, gstate);
+  gram_cols_kernel<<<grid, T * 32, smem, s>>>(Xb, nchunk, n, p, U, nU, nU_dev, Gtab, hit, lams,
+                                             nlam, gstate);
   return cudaGetLastError();
 }
 
