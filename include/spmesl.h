@@ -201,17 +201,25 @@ int spmesl_fit_path_device(const double* dX, int64_t n, int64_t p, const double*
  * tiles of the symmetric S = X~^T X~ / n.
  *
  * spmesl_gram_tile_count: number of 128 x 128 upper-triangle tiles of S (-1 if p is invalid);
- *   ranks split [0, count) into contiguous shares.
+ *   ranks split [0, count) into contiguous shares (solver 2 screening).
+ * spmesl_screen_tile_count: the tile count of the screening pass opt selects: solver 2 as
+ *   spmesl_gram_tile_count; solvers 0 / 3 the 128 x 256 tiles of the certified f16 screening.
  * spmesl_gram_screen_device: standardize dX (n x p, column-major, device) and evaluate tiles
- *   [tile_begin, tile_end): dHit[c] = 1 (never cleared; the caller zero-fills dHit[p] once) for
- *   every column c with some |S_jc| > lambda0, j != c, in those tiles.  The OR (max) of dHit
- *   over all ranks is the global screening result.  Blocking; errors as spmesl_fit.
+ *   [tile_begin, tile_end) of the screening pass opt selects; dHit[c] = 1 (never cleared; the
+ *   caller zero-fills dHit[p] once) for
+ *     solver 2: every column c with some |S_jc| > lambda0, j != c, in those tiles (exact);
+ *     solvers 0 / 3: every column c of a pair (j, c) in those tiles that the certified f16
+ *       bound cannot clear (candidates: a superset of the columns with a hit).
+ *   The OR (max) of dHit over all ranks is the global screening result.  Blocking; errors as
+ *   spmesl_fit.
  * spmesl_fit_columns_gram_device: as spmesl_fit_columns_device, for the Gram solver, given the
- *   global dHit[p]: columns without a hit finish after one sweep; the others run covariance-
- *   update sweeps.  mode must be 0.  Same outputs and iterates as the single-device Gram solver
- *   up to rounding.  Blocking.
+ *   global dHit[p] of spmesl_gram_screen_device with the same solver (for solvers 0 / 3 the
+ *   candidates of the block get their exact FP64 Gram columns, which decide): columns without
+ *   a hit finish after one sweep; the others run covariance-update sweeps.  mode must be 0.
+ *   Same outputs and iterates as the single-device Gram solver (bit for bit).  Blocking.
  */
 int64_t spmesl_gram_tile_count(int64_t p);
+int64_t spmesl_screen_tile_count(int64_t p, const spmesl_options* opt);
 /* 1 if the Gram solver's sweep state fits on chip for (n, p) on the current device, else 0. */
 int spmesl_gram_supported(int64_t n, int64_t p);
 int spmesl_gram_screen_device(const double* dX, int64_t n, int64_t p, double lambda0,

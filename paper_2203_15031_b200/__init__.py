@@ -126,15 +126,22 @@ def gram_supported(n: int, p: int) -> bool:
     return bool(load().spmesl_gram_supported(int(n), int(p)))
 
 
-def gram_tile_count(p: int) -> int:
-    """spmesl_gram_tile_count: upper-triangle tiles of S = X~^T X~ / n."""
-    return int(load().spmesl_gram_tile_count(int(p)))
+def gram_tile_count(p: int, solver=None) -> int:
+    """Tiles of the screening pass: spmesl_gram_tile_count (the 128 x 128 upper-triangle tiles
+    of S = X~^T X~ / n, solver "gram") or, with `solver`, spmesl_screen_tile_count for that
+    solver ("auto"/"gram16": the 128 x 256 tiles of the certified f16 screening)."""
+    if solver is None:
+        return int(load().spmesl_gram_tile_count(int(p)))
+    o = _opts(solver=solver)
+    return int(load().spmesl_screen_tile_count(int(p), ctypes.byref(o)))
 
 
 def gram_screen_device(X, lambda0: float, tile_begin: int, tile_end: int, hit, *, stream=None,
                        **options) -> dict:
-    """spmesl_gram_screen_device: OR the screening hits of tiles [tile_begin, tile_end) into
-    `hit` (uint8 CUDA tensor [p], zero-filled by the caller)."""
+    """spmesl_gram_screen_device: OR the screening flags of tiles [tile_begin, tile_end) into
+    `hit` (uint8 CUDA tensor [p], zero-filled by the caller).  solver "gram": exact hits of the
+    FP64 Gram tiles; "auto"/"gram16" (default): candidates of the certified f16 screening
+    (a superset of the hits; fit_columns_gram_device with the same solver decides them)."""
     import torch
     X = as_colmajor(X)
     n, p = X.shape
@@ -171,7 +178,8 @@ def fit_columns_gram_device(X, col_begin: int, col_end: int, lambda0: float, hit
                             tol: float = 1e-4, max_iter: int = 100, *, stream=None, cap=None,
                             **options):
     """spmesl_fit_columns_gram_device: Gram-solver CSC coefficients of columns
-    [col_begin, col_end) given the global screening flags `hit` (uint8 CUDA tensor [p])."""
+    [col_begin, col_end) given the global screening flags `hit` (uint8 CUDA tensor [p]) of
+    gram_screen_device with the same solver."""
     import torch
     X = as_colmajor(X)
     n, p = X.shape

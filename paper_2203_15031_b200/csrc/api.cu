@@ -290,7 +290,11 @@ int run_prep(Workspace& W, const double* dX, int64_t m, const spmesl_options& o,
   if (W.pending_zero) {
     // Theta's zero fill (HBM-bound) overlaps the solver (compute-bound), not standardization
     CUDA_TRY(cudaStreamWaitEvent(W.side, W.ev[1], 0));
-    CUDA_TRY(launch_zero_fill(W.pending_zero, W.pending_count, W.sms, W.side));
+    static const int pz_bulk = getenv("SPMESL_DEV_PZ_BULK") ? atoi(getenv("SPMESL_DEV_PZ_BULK")) : 0;
+    if (pz_bulk > 0)
+      CUDA_TRY(launch_zero_fill_bulk(W.pending_zero, W.pending_count, pz_bulk, W.side));
+    else
+      CUDA_TRY(launch_zero_fill(W.pending_zero, W.pending_count, W.sms, W.side));
     CUDA_TRY(cudaEventRecord(W.ev_join, W.side));
     W.pending_zero = nullptr;
   }
@@ -448,6 +452,15 @@ void stats_from_counters(const DevCounters& c, int64_t p, spmesl_stats* st, int*
     st->max_outer = c.st_max_outer;
     st->n_unconverged = c.st_unconv;
   }
+}
+
+// n eps rounded upwards to f32 (the product of the two doubles is rounded first; the margin
+// 2^-40 relative covers that rounding)
+float screen16_epsn(int64_t n, double eps) {
+  const double ne = (double)n * eps * (1.0 + 0x1p-40);
+  float f = (float)ne;
+  if ((double)f < ne) f = std::nextafter(f, INFINITY);
+  return f;
 }
 
 float ev_ms(cudaEvent_t a, cudaEvent_t b) {
@@ -668,13 +681,7 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
     Q.tile_end = screen16_tile_count(p);
     Q.lambda0 = G.lambda0;
     Q.eps = screen16_eps(L.n_pad);
-    {   // n eps rounded upwards to f32 (the product of the two doubles is rounded first; the
-        // margin 2^-40 relative covers that rounding)
-      const double ne = (double)n * Q.eps * (1.0 + 0x1p-40);
-      float f = (float)ne;
-      if ((double)f < ne) f = std::nextafter(f, INFINITY);
-      Q.epsn = f;
-    }
+    Q.epsn = screen16_epsn(n, Q.eps);
     Q.cand = (uint8_t*)W.cand.ptr;
     // Theta's zero fill is split: the screening kernel writes the first part under its
     // contraction, a side-stream kernel the rest while the exact Gram columns and the sweeps
@@ -992,6 +999,7 @@ int fit_gram_columns_core(Workspace& W, const double* dX, int64_t n, int64_t p, 
                           const spmesl_options& o, const uint8_t* dHit, const FitOut& out,
                           cudaStream_t s, spmesl_stats* st, Layout& L, int* nzcap_used) {
   const int64_t m = ce - cb;
+  const bool cand = o.solver != 2;   // dHit: candidates of the certified screening (solver 0/3)
   set_layout(L, n, p);
   int nzcap = initial_nzcap(n, p);
   std::vector<uint8_t> hh(m);
@@ -1015,9 +1023,23 @@ int fit_gram_columns_core(Workspace& W, const double* dX, int64_t n, int64_t p, 
     for (int j : U) gstate[j] = 2;
     CUDA_TRY(cudaMemcpyAsync(W.umap.ptr, gstate.data(), (size_t)p * 4, cudaMemcpyHostToDevice, s));
     if (nU) CUDA_TRY(cudaMemcpyAsync(W.uvars.ptr, U.data(), (size_t)nU * 4, cudaMemcpyHostToDevice, s));
-    CUDA_TRY(launch_gram_pass((const double*)W.xb.ptr, (int)L.nblk, L.nchunk, (int)n, (int)p,
-                              nullptr, 0, (const int*)W.uvars.ptr, nU, nullptr,
-                              (double*)W.ondemand.ptr, s));
+    const uint8_t* hit = dHit;
+    if (cand) {
+      // dHit holds candidates (certified screening): their exact Gram columns decide
+      if ((rc = ensure(W.hit, (size_t)p))) return rc;
+      if ((rc = ensure(W.lam_dev, (size_t)SPMESL_MAX_LAM * 8))) return rc;
+      W.lam_host.assign(1, lambda0);
+      CUDA_TRY(cudaMemcpyAsync(W.lam_dev.ptr, W.lam_host.data(), 8, cudaMemcpyHostToDevice, s));
+      CUDA_TRY(cudaMemsetAsync(W.hit.ptr, 0, (size_t)p, s));
+      CUDA_TRY(launch_gram_cols((const double*)W.xb.ptr, (int)L.nblk, L.nchunk, (int)n, (int)p,
+                                (const int*)W.uvars.ptr, nU, nullptr, W.sms, (double*)W.ondemand.ptr,
+                                (uint8_t*)W.hit.ptr, (const double*)W.lam_dev.ptr, 1, nullptr, s));
+      hit = (const uint8_t*)W.hit.ptr;
+    } else {
+      CUDA_TRY(launch_gram_pass((const double*)W.xb.ptr, (int)L.nblk, L.nchunk, (int)n, (int)p,
+                                nullptr, 0, (const int*)W.uvars.ptr, nU, nullptr,
+                                (double*)W.ondemand.ptr, s));
+    }
     CUDA_TRY(cudaEventRecord(W.ev[7], s));
     GramParams G{};
     G.Xb = (const double*)W.xb.ptr;
@@ -1029,7 +1051,7 @@ int fit_gram_columns_core(Workspace& W, const double* dX, int64_t n, int64_t p, 
     G.lams[0] = lambda0;
     G.max_outer = max_iter;
     G.G = nullptr;
-    G.hit = const_cast<uint8_t*>(dHit);
+    G.hit = const_cast<uint8_t*>(hit);
     G.tail = (TailState*)W.tail.ptr;
     G.tail_count = &dc->tail_count;
     G.sigma_std = out.sigma_std; G.iters = out.iters; G.sweeps = out.sweeps;
@@ -1067,8 +1089,9 @@ int fit_gram_columns_core(Workspace& W, const double* dX, int64_t n, int64_t p, 
     if (W.host_counters->err) return std_error(W, st);
     if (!W.host_counters->overflow) {
       if (st) {
-        st->solver = 2;
+        st->solver = cand ? 3 : 2;
         st->kernel_launches += 4;
+        if (cand) st->screen_candidates = nU;
         st->ms_gram = ev_ms(W.ev[1], W.ev[7]);
         st->ms_tail = ev_ms(W.ev[5], W.ev[6]);
         st->tail_columns = W.host_counters->tail_count;
@@ -1473,6 +1496,12 @@ int64_t spmesl_gram_tile_count(int64_t p) {
   return gram_tile_count(p);
 }
 
+int64_t spmesl_screen_tile_count(int64_t p, const spmesl_options* opt) {
+  if (p < 1 || p > (int64_t)0x7fffffff) return -1;
+  const spmesl_options o = resolve(opt);
+  return o.solver == 2 ? gram_tile_count(p) : screen16_tile_count(p);
+}
+
 int spmesl_gram_screen_device(const double* dX, int64_t n, int64_t p, double lambda0,
                               int64_t tile_begin, int64_t tile_end, const spmesl_options* opt,
                               uint8_t* dHit, void* cuda_stream, spmesl_stats* st) {
@@ -1481,7 +1510,8 @@ int spmesl_gram_screen_device(const double* dX, int64_t n, int64_t p, double lam
   int rc = validate(dX, n, p, lambda0, 1.0, 1, o);
   if (rc) return rc;
   if (!dHit) return fail(SPMESL_ERR_ARG, "dHit is NULL");
-  const int64_t nt = gram_tile_count(p);
+  const bool s16 = o.solver != 2;     // certified f16 screening (solvers 0 / 3)
+  const int64_t nt = s16 ? screen16_tile_count(p) : gram_tile_count(p);
   if (tile_begin < 0 || tile_end > nt || tile_begin > tile_end)
     return fail(SPMESL_ERR_ARG, "bad tile range");
   int dev;
@@ -1494,7 +1524,53 @@ int spmesl_gram_screen_device(const double* dX, int64_t n, int64_t p, double lam
   Layout L;
   set_layout(L, n, p);
   if ((rc = alloc_core(*W, L, 1, 8))) return rc;
+  if (s16) {
+    if ((rc = ensure(W->nrm, (size_t)p * 8))) return rc;
+    if ((rc = ensure(W->sq, (size_t)screen16_pad(p) * 8 + (size_t)p * 8))) return rc;
+    if ((rc = ensure(W->y16, screen16_y_halves(p, L.n_pad) * 2))) return rc;
+  }
   if ((rc = run_prep(*W, dX, 1, o, L, s, /*band=*/false))) return rc;
+  if (s16) {
+    // dHit[c] = 1 for the columns the certified f16 screening of these tiles cannot clear
+    // (candidates: a superset of the columns with a hit there)
+    const int64_t p_pad = screen16_pad(p);
+    float* inv_sq = (float*)W->sq.ptr;
+    float* lam_n = inv_sq + p_pad;
+    double* sqv = (double*)(lam_n + p_pad);
+    CUDA_TRY(launch_sqrt((const double*)W->nrm.ptr, sqv, inv_sq, lam_n, lambda0, (int)n, (int)p,
+                         (int)p_pad, s));
+    CUDA_TRY(launch_to_f16((const double*)W->xb.ptr, (const double*)W->nrm.ptr, (int)p, L.n_pad,
+                           L.nchunk, (__half*)W->y16.ptr, s));
+    Screen16Params Q{};
+    Q.Y16 = (const __half*)W->y16.ptr;
+    Q.sq = sqv;
+    Q.inv_sq = inv_sq;
+    Q.lam_n = lam_n;
+    Q.p = (int)p; Q.n = (int)n;
+    Q.ntb = (int)((p + 127) / 128);
+    Q.nchunk64 = (L.n_pad + 63) / 64;
+    Q.tile_begin = (int)tile_begin;
+    Q.tile_end = (int)tile_end;
+    Q.lambda0 = lambda0;
+    Q.eps = screen16_eps(L.n_pad);
+    Q.epsn = screen16_epsn(n, Q.eps);
+    Q.cand = dHit;
+    CUDA_TRY(cudaEventRecord(W->ev[8], s));
+    CUDA_TRY(launch_screen16(Q, (int)std::min<int64_t>(W->sms, std::max<int64_t>(1, tile_end - tile_begin)), s));
+    CUDA_TRY(cudaEventRecord(W->ev[9], s));
+    CUDA_TRY(cudaEventRecord(W->ev[7], s));
+    if ((rc = read_counters(*W, s))) return rc;
+    if (W->host_counters->err) return std_error(*W, st);
+    if (st) {
+      st->solver = 3;
+      st->ms_standardize = ev_ms(W->ev[0], W->ev[1]);
+      st->ms_gram = ev_ms(W->ev[1], W->ev[7]);
+      st->ms_screen = ev_ms(W->ev[8], W->ev[9]);
+      st->kernel_launches = 4;
+      st->bad_column = -1;
+    }
+    return SPMESL_OK;
+  }
   GramParams G{};
   G.Xb = (const double*)W->xb.ptr;
   G.n = (int)n; G.n_pad = L.n_pad; G.nchunk = L.nchunk; G.p = (int)p; G.nblk = (int)L.nblk;

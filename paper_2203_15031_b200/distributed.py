@@ -9,9 +9,10 @@ symmetrizes its own column block of Theta from the global CSC (the symmetrizatio
 Eq. (symm), needs b_kj from column j, which may live on another rank).
 
 With the Gram solver (default when it applies) there is one more, tiny exchange before the
-fit: every rank screens an equal share of the upper-triangle tiles of S = X~^T X~ / n (the
-first sweeps of all columns) and the p screening flags are max-all-reduced, so
-each rank knows which of its columns need more than one sweep.
+fit: every rank screens an equal share of the tiles of S = X~^T X~ / n (the first sweeps of all
+columns; by default the certified f16 screening) and the p screening flags are
+max-all-reduced, so each rank knows which of its columns may need more than one sweep (their
+exact FP64 Gram columns then decide, on the rank that owns the column).
 
 ``gather_csc`` / ``allreduce_hits`` are backend-agnostic host logic (gloo on CPU tensors in
 the tests, NCCL on CUDA tensors in production); ``fit_distributed`` runs the CUDA path around
@@ -101,25 +102,27 @@ def fit_distributed(X: torch.Tensor, lambda0: float, tol: float = 1e-4, max_iter
                     group=None, stream=None, solver: str = "auto", **options):
     """Fit this rank's column block and return its block of Theta (p x m, column-major view).
 
-    X: (n, p) float64 CUDA tensor, identical on every rank.  solver: "auto" (Gram when it
-    applies), "gram" or "residual"."""
+    X: (n, p) float64 CUDA tensor, identical on every rank.  solver: "auto" (the Gram solver
+    with certified f16 screening when it applies), "gram16", "gram" (FP64 Gram screening) or
+    "residual"."""
     from . import (as_colmajor, assemble_device, fit_columns_device, fit_columns_gram_device,
                    gram_screen_device, gram_supported, gram_tile_count)
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     n, p = X.shape
     c0, c1 = column_range(p, rank, world)
     mode = options.get("mode", "per_column")
-    use_gram = solver == "gram" or (solver == "auto" and mode in ("per_column", 0)
-                                    and gram_supported(n, p))
+    use_gram = solver in ("gram", "gram16") or (solver == "auto" and mode in ("per_column", 0)
+                                                and gram_supported(n, p))
     screen_stats = None
     if use_gram:
         X = as_colmajor(X)
-        t0, t1 = tile_range(gram_tile_count(p), rank, world)
+        t0, t1 = tile_range(gram_tile_count(p, solver=solver), rank, world)
         hit = torch.zeros(p, dtype=torch.uint8, device=X.device)
-        screen_stats = gram_screen_device(X, lambda0, t0, t1, hit, stream=stream, **options)
+        screen_stats = gram_screen_device(X, lambda0, t0, t1, hit, stream=stream, solver=solver,
+                                          **options)
         allreduce_hits(hit, group)
         part = fit_columns_gram_device(X, c0, c1, lambda0, hit, tol, max_iter, stream=stream,
-                                       **options)
+                                       solver=solver, **options)
     else:
         part = fit_columns_device(X, c0, c1, lambda0, tol, max_iter, stream=stream,
                                   solver="residual" if solver == "auto" else solver, **options)
@@ -131,6 +134,9 @@ def fit_distributed(X: torch.Tensor, lambda0: float, tol: float = 1e-4, max_iter
     stats["kernel_launches"] = stats.get("kernel_launches", 0) + 2   # assemble entries + diag
     if screen_stats is not None:
         stats["ms_gram"] = screen_stats["ms_gram"]
+        stats["ms_screen"] = screen_stats.get("ms_screen", 0.0)
+        stats["screen_fill_bytes"] = 0
+        stats["screen_tiles"] = (t0, t1)
         stats["kernel_launches"] += screen_stats["kernel_launches"]
     return dict(theta=theta, sigma=sigma, iters=part["iters"], sweeps=part["sweeps"],
                 converged=part["converged"], col_range=(c0, c1), stats=stats,

@@ -210,7 +210,7 @@ def _rank_worker(rank, world, port, X, lam, q, solver):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("solver", ["residual", "gram"])
+@pytest.mark.parametrize("solver", ["residual", "gram", "auto"])
 def test_two_ranks_sharing_one_gpu_match_single_fit(S, oracle, solver):
     """fit_distributed (column blocks + CSC all-gather + per-rank assembly; for the Gram solver
     also the tile-share screening + flag all-reduce) on 2 ranks that share cuda:0 over gloo
@@ -298,20 +298,27 @@ def test_unstandardized_scaled_columns_and_caps(S, oracle, solver, mi):
         assert np.array_equal(res.converged, ora.converged)
 
 
-def test_gram_building_blocks_reproduce_full_fit(S, oracle):
-    """Screening in tile shares + Gram column blocks + assembly == the single Gram fit."""
+@pytest.mark.parametrize("solver", ["gram", "gram16"])
+def test_gram_building_blocks_reproduce_full_fit(S, oracle, solver):
+    """Screening in tile shares + Gram column blocks + assembly == the single Gram fit (gram16:
+    the shares flag candidates, each column block decides its own exactly)."""
     import torch
     X, _, _ = G.make_config(4, p=900, family="hub")
     n, p = X.shape
     lam = oracle.lambda_ub(n, p)
     full = S.fit(X, lam, solver="gram")
     Xd = torch.from_numpy(np.ascontiguousarray(X)).cuda()
-    nt = S.gram_tile_count(p)
+    nt = S.gram_tile_count(p, solver=solver)
     hit = torch.zeros(p, dtype=torch.uint8, device="cuda")
     for a, b in [(0, nt // 3), (nt // 3, nt // 3), (nt // 3, nt)]:
-        S.gram_screen_device(Xd, lam, a, b, hit)
+        S.gram_screen_device(Xd, lam, a, b, hit, solver=solver)
+    if solver == "gram16":   # candidates: a superset of the exact hits of the FP64 screening
+        exact = torch.zeros(p, dtype=torch.uint8, device="cuda")
+        S.gram_screen_device(Xd, lam, 0, S.gram_tile_count(p), exact, solver="gram")
+        assert bool(((exact == 1) <= (hit == 1)).all())
     bounds = [0, 250, 251, 600, 900]
-    parts = [S.fit_columns_gram_device(Xd, a, b, lam, hit) for a, b in zip(bounds[:-1], bounds[1:])]
+    parts = [S.fit_columns_gram_device(Xd, a, b, lam, hit, solver=solver)
+             for a, b in zip(bounds[:-1], bounds[1:])]
     counts = torch.cat([q["counts"] for q in parts]).long()
     col_ptr = torch.zeros(p + 1, dtype=torch.int64, device="cuda")
     col_ptr[1:] = torch.cumsum(counts, 0)
