@@ -371,7 +371,7 @@ def run_ours(args):
                 "screen_fill_bytes": fill,
                 "tensor_tflops": flops / (scr_ms / 1000.0) / 1e12,
                 "screen_candidates": stats_last.get("screen_candidates"),
-                "exact_and_sweeps_ms": stats_last.get("ms_gram", 0.0) - scr_ms,
+                "rest_of_step_ms": step_ms_mean - scr_ms,
                 "sweep_kernel_ms": stats_last.get("ms_tail", 0.0),
                 "sweep_columns": stats_last.get("tail_columns", 0)}
     elif stats_last.get("solver") in (2, 3):
@@ -481,10 +481,12 @@ def run_ours(args):
                     "solver": {1: "residual", 2: "gram", 3: "gram16"}.get(stats_last.get("solver"), "?")}),
                 "roofline": roof, "clocks": clk.summary(), "e2e": e2e,
                 "gpu_launches": int(stats_last["kernel_launches"]) * args.steps,
-                "ms_breakdown": {"standardize": stats_last["ms_standardize"],
-                                 "solve": stats_last["ms_cd"], "gram": stats_last.get("ms_gram", 0.0),
-                                 "sweeps": stats_last.get("ms_tail", 0.0),
-                                 "assemble": stats_last["ms_assemble"]}}
+                "ms_breakdown": {k: (v if v is None or v >= 0 else None) for k, v in {
+                    "standardize": stats_last["ms_standardize"], "solve": stats_last["ms_cd"],
+                    "gram": stats_last.get("ms_gram", 0.0), "sweeps": stats_last.get("ms_tail", 0.0),
+                    "assemble": stats_last["ms_assemble"], "screen": stats_last.get("ms_screen"),
+                    "total_device": stats_last.get("ms_total")}.items()},
+                "graph_replay": bool(stats_last.get("graph_replay", 0))}
         if cpu:
             line["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
         print(json.dumps(line), flush=True)

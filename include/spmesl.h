@@ -86,7 +86,11 @@ typedef struct {
                              their exact test), the others are known to stop after one sweep.
                              2 and 3: SPMESL_ERR_UNSUPPORTED where they do not apply.  All
                              solvers: same iterates up to FP64 rounding. */
-  int32_t reserved[7];
+  int32_t eager;          /* spmesl_fit_device, Gram solvers: 0 (default) captures the whole
+                             enqueued fit as a CUDA graph the second time the same arguments
+                             (pointers included) arrive and replays it from then on (one launch
+                             per fit); 1: enqueue every operation on each call.  Same results. */
+  int32_t reserved[6];
 } spmesl_options;
 
 typedef struct {
@@ -121,6 +125,9 @@ typedef struct {
                              Theta's zero fill) */
   int64_t screen_fill_bytes; /* bytes of Theta the screening kernel zero-filled (the rest of the
                              fill, if any, ran on a side stream beside the later kernels) */
+  int32_t graph_replay;   /* 1 if this call ran as one CUDA-graph launch (options.eager); then
+                             only ms_total and ms_screen are measured, the other ms_* read -1 */
+  int32_t pad1;
 } spmesl_stats;
 
 /* Fill *opt with the defaults listed above. */

@@ -51,8 +51,21 @@ MODES = {"per_column": 0, "joint": 1}
 SOLVERS = {"auto": 0, "residual": 1, "gram": 2, "gram16": 3}
 
 
-def _opts(max_inner=10000, standardize=True, symmetrize=True, sigma_floor=1e-8, tile_cols=0,
-          device=-1, tail_after=1, mode="per_column", solver="auto") -> _lib.Options:
+_OPTS_CACHE = {}
+
+
+def _opts(**kw) -> _lib.Options:
+    """Options for these keyword arguments (cached: the device path is called per fit)."""
+    key = tuple(sorted(kw.items()))
+    o = _OPTS_CACHE.get(key)
+    if o is None:
+        o = _OPTS_CACHE[key] = _make_opts(**kw)
+    return o
+
+
+def _make_opts(max_inner=10000, standardize=True, symmetrize=True, sigma_floor=1e-8, tile_cols=0,
+               device=-1, tail_after=1, mode="per_column", solver="auto",
+               eager=False) -> _lib.Options:
     """mode: "per_column" (Algorithm 1 stop per column) or "joint" (Algorithm 3).
     solver: "auto", "residual" (CD on X~) or "gram" (covariance updates on X~^T X~ / n)."""
     return default_options(max_inner=int(max_inner), standardize=int(bool(standardize)),
@@ -60,7 +73,8 @@ def _opts(max_inner=10000, standardize=True, symmetrize=True, sigma_floor=1e-8, 
                            tile_cols=int(tile_cols), device=int(device),
                            tail_after=int(tail_after),
                            mode=MODES[mode] if isinstance(mode, str) else int(mode),
-                           solver=SOLVERS[solver] if isinstance(solver, str) else int(solver))
+                           solver=SOLVERS[solver] if isinstance(solver, str) else int(solver),
+                           eager=int(bool(eager)))
 
 
 def fit(X, lambda0: float, tol: float = 1e-4, max_iter: int = 100, *, out_theta=None,
@@ -117,8 +131,9 @@ def fit_device(X, lambda0: float, tol: float = 1e-4, max_iter: int = 100, *, str
                                       ctypes.c_void_p(s.cuda_stream), ctypes.byref(st))
     _lib.check(rc, st)
     # the buffer holds Theta column-major: element (j, k) at j + k p -> view as its transpose
+    # (uint8 0/1 reinterpreted as bool: a view, no conversion kernel)
     return FitResult(rc, out["theta"].t(), out["sigma"], out["iters"], out["sweeps"],
-                     out["conv"].bool(), st.asdict())
+                     out["conv"].view(torch.bool), st.asdict())
 
 
 def gram_supported(n: int, p: int) -> bool:

@@ -33,7 +33,8 @@ class Options(ctypes.Structure):
         ("device", ctypes.c_int32),
         ("tail_after", ctypes.c_int32),
         ("solver", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 7),
+        ("eager", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 6),
     ]
 
 
@@ -63,6 +64,8 @@ class Stats(ctypes.Structure):
         ("screen_candidates", ctypes.c_int64),
         ("ms_screen", ctypes.c_double),
         ("screen_fill_bytes", ctypes.c_int64),
+        ("graph_replay", ctypes.c_int32),
+        ("pad1", ctypes.c_int32),
     ]
 
     def asdict(self):

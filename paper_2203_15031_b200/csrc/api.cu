@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <algorithm>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -61,9 +62,13 @@ struct Buffer {
   size_t bytes = 0;
 };
 
+// bumped on every (re)allocation: a captured CUDA graph is only valid while no buffer moved
+std::atomic<uint64_t> g_alloc_gen{0};
+
 int ensure(Buffer& b, size_t bytes) {
   if (bytes == 0) bytes = 16;
   if (b.bytes >= bytes) return SPMESL_OK;
+  g_alloc_gen.fetch_add(1);
   if (b.ptr) cudaFree(b.ptr);
   b.ptr = nullptr;
   b.bytes = 0;
@@ -99,12 +104,31 @@ struct Workspace {
   size_t pending_count = 0;
   double* take_zero = nullptr;            // Theta the Gram kernel may zero-fill itself
   size_t take_count = 0;
-  std::vector<double> lam_host;           // (pinned-free staging of the penalty levels)
+  double* lam_pinned = nullptr;           // staging of the penalty levels (pinned, H2D)
+  // CUDA-graph replay of the device-path fit: the whole enqueue is captured
+  // once per argument set and replayed with one launch
+  cudaStream_t cap = nullptr;             // capture stream
+  bool capturing = false;                 // timing events become external record nodes
+  cudaGraphExec_t gexec = nullptr;
+  std::vector<unsigned char> gkey;        // arguments of the captured graph
+  std::vector<unsigned char> last_key;    // arguments of the previous eager device-path fit
+  int graph_nzcap = 0;                    // coefficient-list capacity the graph was built for
   bool zero_join = false;     // part of Theta's zero fill runs on `side` (join ev_join)
   int64_t screen_fill = 0;    // doubles of Theta the screening kernel zero-filled (last fit)
   int gram_launches = 0;      // kernels fit_gram_enqueue launched (last fit)
   bool init = false;
 };
+
+// Timing events: inside a graph capture they must be external record nodes (recorded at every
+// replay), not the intra-graph dependency a plain record becomes.
+// Each external record node costs a few microseconds of idle GPU between its neighbours, so
+// a captured fit keeps only the events of ms_total (ev[0], ev[4]) and of the screening kernel
+// (ev[8], ev[9], the roofline's denominator); the other phase times read -1 after a replay.
+cudaError_t ev_record(const Workspace& W, cudaEvent_t e, cudaStream_t s) {
+  if (!W.capturing) return cudaEventRecord(e, s);
+  if (e != W.ev[0] && e != W.ev[4] && e != W.ev[8] && e != W.ev[9]) return cudaSuccess;
+  return cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+}
 
 std::mutex g_ws_mu;
 std::vector<Workspace*> g_ws;
@@ -125,6 +149,8 @@ int ws_init(Workspace& W, int dev) {
   W.smem_optin = (int)prop.sharedMemPerBlockOptin;
   W.cc_major = prop.major;
   CUDA_TRY(cudaMallocHost((void**)&W.host_counters, sizeof(DevCounters)));
+  CUDA_TRY(cudaMallocHost((void**)&W.lam_pinned, sizeof(double) * SPMESL_MAX_LAM));
+  CUDA_TRY(cudaStreamCreateWithFlags(&W.cap, cudaStreamNonBlocking));
   for (auto& e : W.ev) CUDA_TRY(cudaEventCreate(&e));
   CUDA_TRY(cudaStreamCreateWithFlags(&W.side, cudaStreamNonBlocking));
   CUDA_TRY(cudaEventCreateWithFlags(&W.ev_fork, cudaEventDisableTiming));
@@ -237,7 +263,7 @@ int run_tail(Workspace& W, const Layout& L, int64_t cb, double lambda0, double t
   for (int j : U) gstate[j] = 2;
   CUDA_TRY(cudaMemcpyAsync(W.umap.ptr, gstate.data(), (size_t)p * 4, cudaMemcpyHostToDevice, s));
   if (nU) CUDA_TRY(cudaMemcpyAsync(W.uvars.ptr, U.data(), (size_t)nU * 4, cudaMemcpyHostToDevice, s));
-  CUDA_TRY(cudaEventRecord(W.ev[5], s));
+  CUDA_TRY(ev_record(W, W.ev[5], s));
   CUDA_TRY(launch_tail_residuals((const double*)W.xb.ptr, (const TailState*)W.tail.ptr, M,
                                  (const int*)W.nz_rows.ptr, (const double*)W.nz_vals.ptr, nzcap, cb,
                                  (int)L.n, L.n_pad, L.nchunk, (double*)W.tailV.ptr, s));
@@ -266,7 +292,7 @@ int run_tail(Workspace& W, const Layout& L, int64_t cb, double lambda0, double t
   T.sigma_std = out.sigma_std; T.iters = out.iters; T.sweeps = out.sweeps; T.converged = out.conv;
   set_prefetch(W, T);
   CUDA_TRY(launch_tail_sweeps(T, grid, s));
-  CUDA_TRY(cudaEventRecord(W.ev[6], s));   // end of the tail solver
+  CUDA_TRY(ev_record(W, W.ev[6], s));   // end of the tail solver
   if (st) { st->tail_columns = M; st->kernel_launches += 4; }
   return SPMESL_OK;
 }
@@ -280,13 +306,13 @@ int run_prep(Workspace& W, const double* dX, int64_t m, const spmesl_options& o,
   CUDA_TRY(cudaMemsetAsync(W.queue.ptr, 0, 16, s));
   CUDA_TRY(cudaMemsetAsync(W.nz_count.ptr, 0, sizeof(int) * (size_t)m, s));
   CUDA_TRY(cudaMemsetAsync(W.nz_cur.ptr, 0, sizeof(int) * (size_t)m, s));
-  CUDA_TRY(cudaEventRecord(W.ev[0], s));
+  CUDA_TRY(ev_record(W, W.ev[0], s));
   DevCounters* dc = (DevCounters*)W.counters.ptr;
   CUDA_TRY(launch_standardize(dX, L, o.standardize, (double*)W.xb.ptr, (double*)W.mean.ptr,
                               (double*)W.scale.ptr, &dc->err, &dc->bad_key, s,
                               W.nrm.bytes >= (size_t)L.p * 8 ? (double*)W.nrm.ptr : nullptr));
   if (band) CUDA_TRY(launch_gram((const double*)W.xb.ptr, L, (double*)W.gband.ptr, s));
-  CUDA_TRY(cudaEventRecord(W.ev[1], s));
+  CUDA_TRY(ev_record(W, W.ev[1], s));
   if (W.pending_zero) {
     // Theta's zero fill (HBM-bound) overlaps the solver (compute-bound), not standardization
     CUDA_TRY(cudaStreamWaitEvent(W.side, W.ev[1], 0));
@@ -389,7 +415,7 @@ int run_cd(Workspace& W, const double* dX, int64_t n, int64_t p, int64_t cb, int
               h[w * 4 + 0] / (double)ctas / 1.965e6, h[w * 4 + 1] / (double)ctas / 1.965e6,
               h[w * 4 + 2] / (double)ctas / 1.965e6);
   }
-  CUDA_TRY(cudaEventRecord(W.ev[2], s));
+  CUDA_TRY(ev_record(W, W.ev[2], s));
   return SPMESL_OK;
 }
 
@@ -558,7 +584,7 @@ int fit_joint_core(Workspace& W, const double* dX, int64_t n, int64_t p, int64_t
       std::swap(act, act_next);
     }
     if (!overflow) {
-      CUDA_TRY(cudaEventRecord(W.ev[2], s));
+      CUDA_TRY(ev_record(W, W.ev[2], s));
       if (st) { st->tile_cols = T0; st->num_ctas = ctas0; st->kernel_launches += launches; }
       *nzcap_used = nzcap;
       return SPMESL_OK;
@@ -622,8 +648,8 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   {
     double lv[SPMESL_MAX_LAM];
     for (int l = 0; l < nlam; ++l) lv[l] = nlam > 1 ? lams[l] : lambda0;
-    W.lam_host.assign(lv, lv + nlam);
-    CUDA_TRY(cudaMemcpyAsync(W.lam_dev.ptr, W.lam_host.data(), (size_t)nlam * 8,
+    std::memcpy(W.lam_pinned, lv, (size_t)nlam * 8);
+    CUDA_TRY(cudaMemcpyAsync(W.lam_dev.ptr, W.lam_pinned, (size_t)nlam * 8,
                              cudaMemcpyHostToDevice, s));
   }
   GramParams G{};
@@ -696,9 +722,9 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
     Q.zero_count = zfused;
     if (getenv("SPMESL_DEV_S16_NOZERO")) { Q.zero_ptr = nullptr; Q.zero_count = 0; }   // (dev)
     W.screen_fill = (int64_t)Q.zero_count;
-    CUDA_TRY(cudaEventRecord(W.ev[8], s));
+    CUDA_TRY(ev_record(W, W.ev[8], s));
     CUDA_TRY(launch_screen16(Q, std::min(W.sms, Q.tile_end), s));
-    CUDA_TRY(cudaEventRecord(W.ev[9], s));
+    CUDA_TRY(ev_record(W, W.ev[9], s));
     if (G.zero_ptr && zfused < G.zero_count) {
       CUDA_TRY(cudaStreamWaitEvent(W.side, W.ev[9], 0));
       static const int zgrid = getenv("SPMESL_ZB_GRID") ? atoi(getenv("SPMESL_ZB_GRID")) : W.sms;
@@ -731,19 +757,19 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
                               (uint8_t*)W.hit.ptr, (const double*)W.lam_dev.ptr, nlam,
                               (int*)W.umap.ptr, s));
     launches += 3 + (nlam > 1);
-    CUDA_TRY(cudaEventRecord(W.ev[7], s));
+    CUDA_TRY(ev_record(W, W.ev[7], s));
   } else {
     const int nT = (int)((L.nblk + 3) / 4);
     const int ntiles = nT * (nT + 1) / 2;
-    CUDA_TRY(cudaEventRecord(W.ev[8], s));
+    CUDA_TRY(ev_record(W, W.ev[8], s));
     CUDA_TRY(launch_syrk_screen(G, std::min(W.sms, ntiles), s));
-    CUDA_TRY(cudaEventRecord(W.ev[9], s));
-    CUDA_TRY(cudaEventRecord(W.ev[7], s));
+    CUDA_TRY(ev_record(W, W.ev[9], s));
+    CUDA_TRY(ev_record(W, W.ev[7], s));
     if (nlam > 1) CUDA_TRY(launch_level_flags(G, s));
     launches += 1 + (nlam > 1);
   }
   CUDA_TRY(launch_gram_init(G, s));
-  CUDA_TRY(cudaEventRecord(W.ev[5], s));
+  CUDA_TRY(ev_record(W, W.ev[5], s));
   // the sweep kernel reads the number of columns with hits from the device counter (no host
   // round trip); one CTA per SM, each takes columns from the shared work counter
   TailParams T{};
@@ -771,8 +797,8 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   if (nlam > 1) { T.lambdas = (const double*)W.lam_dev.ptr; T.slot_stride = (int)p; }
   set_prefetch(W, T);
   CUDA_TRY(launch_tail_sweeps(T, (int)std::min<int64_t>(W.sms, p * nlam), s));
-  CUDA_TRY(cudaEventRecord(W.ev[6], s));
-  CUDA_TRY(cudaEventRecord(W.ev[2], s));
+  CUDA_TRY(ev_record(W, W.ev[6], s));
+  CUDA_TRY(ev_record(W, W.ev[2], s));
   W.gram_launches = launches + 2;   // + gram_init, tail
   return SPMESL_OK;
 }
@@ -870,6 +896,92 @@ int fit_columns_core(Workspace& W, const double* dX, int64_t n, int64_t p, int64
   return fail(SPMESL_ERR_OOM, "coefficient list overflow");
 }
 
+// One attempt of the device-path Gram fit, enqueued on `cs` up to and including the read of
+// the counter block into pinned host memory (no synchronisation): the eager path runs it on
+// the caller's stream; the graph path captures it once and replays it.
+int gram_fit_enqueue_all(Workspace& W, const double* dX, int64_t n, int64_t p, double lambda0,
+                         double tol, int32_t max_iter, const spmesl_options& o, double* dTheta,
+                         double* dSigma, int32_t* dIters, int32_t* dSweeps, uint8_t* dConv,
+                         const FitOut& out, cudaStream_t cs, Layout& L, int nzcap) {
+  int rc;
+  const size_t pp = (size_t)p * (size_t)p;
+  // the screening kernel zero-fills Theta itself (bulk stores from its producer warp) when the
+  // buffer allows 16-byte pieces; otherwise a side-stream kernel does, after standardization
+  static const bool side_zero = getenv("SPMESL_DEV_SIDE_ZERO") != nullptr;   // (dev)
+  const bool take = !side_zero && (((uintptr_t)dTheta & 15) == 0) && (pp & 1) == 0;
+  if (take) { W.take_zero = dTheta; W.take_count = pp; }
+  else { W.pending_zero = dTheta; W.pending_count = pp; }
+  rc = fit_gram_enqueue(W, dX, n, p, lambda0, tol, max_iter, o, out, cs, L, nzcap, nullptr, 1,
+                        o.solver != 2);
+  W.take_zero = nullptr;
+  if (W.pending_zero) {    // (the solver failed before standardization)
+    W.pending_zero = nullptr;
+    if (!rc) rc = fail(SPMESL_ERR_CUDA, "internal: Theta zero fill was not launched");
+  }
+  const bool join = !take || W.zero_join;
+  W.zero_join = false;
+  if (rc) { if (join) cudaStreamWaitEvent(cs, W.ev_join, 0); return rc; }
+  if (join) CUDA_TRY(cudaStreamWaitEvent(cs, W.ev_join, 0));
+  const size_t cap = (size_t)p * (size_t)nzcap;
+  if ((rc = ensure(W.csc_rows, cap * 4))) return rc;
+  if ((rc = ensure(W.csc_vals, cap * 8))) return rc;
+  DevCounters* dc = (DevCounters*)W.counters.ptr;
+  CUDA_TRY(ev_record(W, W.ev[3], cs));
+  CUDA_TRY(launch_csc_build((const int*)W.nz_count.ptr, (const int*)W.nz_cur.ptr,
+                            (const int*)W.nz_rows.ptr, (const double*)W.nz_vals.ptr, (int)p,
+                            nzcap, (int64_t*)W.col_ptr.ptr, (int32_t*)W.csc_rows.ptr,
+                            (double*)W.csc_vals.ptr, &dc->csc_total, cs));
+  CUDA_TRY(launch_assemble(p, 0, p, (const int64_t*)W.col_ptr.ptr,
+                           (const int32_t*)W.csc_rows.ptr, (const double*)W.csc_vals.ptr,
+                           (const double*)W.sigma_std.ptr,
+                           o.standardize ? (const double*)W.scale.ptr : nullptr, o.symmetrize,
+                           dTheta, dSigma, cs, /*zero_fill=*/false));
+  CUDA_TRY(ev_record(W, W.ev[4], cs));
+  if ((rc = device_stats(W, dIters, dSweeps, dConv, p, cs))) return rc;
+  CUDA_TRY(cudaMemcpyAsync(W.host_counters, W.counters.ptr, sizeof(DevCounters),
+                           cudaMemcpyDeviceToHost, cs));
+  return SPMESL_OK;
+}
+
+void finish_stats(Workspace& W, int64_t p, spmesl_stats* st, int* any_unconv) {
+  stats_from_counters(*W.host_counters, p, st, any_unconv);
+  if (st) {
+    st->nnz = W.host_counters->csc_total;
+    st->ms_standardize = ev_ms(W.ev[0], W.ev[1]);
+    st->ms_cd = ev_ms(W.ev[1], W.ev[2]);
+    st->ms_assemble = ev_ms(W.ev[3], W.ev[4]);
+    st->ms_total = ev_ms(W.ev[0], W.ev[4]);
+    st->kernel_launches += 5;  // standardize, csc_scan, csc_copy, assemble x2 (+ solver kernels)
+    st->bad_column = -1;
+  }
+}
+
+// The arguments a captured fit depends on (pointers included: the graph bakes them in) plus the
+// allocation generation (no workspace buffer may have moved since the capture).
+std::vector<unsigned char> graph_key(const double* dX, int64_t n, int64_t p, double lambda0,
+                                     double tol, int32_t max_iter, const spmesl_options& o,
+                                     const void* dTheta, const void* dSigma, const void* dIters,
+                                     const void* dSweeps, const void* dConv, int nzcap,
+                                     cudaStream_t s) {
+  struct K {
+    const void* x; int64_t n, p; double lam, tol; int32_t mi, nzcap; spmesl_options o;
+    const void *th, *sg, *it, *sw, *cv; uint64_t gen; int dev;
+  } k;
+  std::memset(&k, 0, sizeof(k));
+  k.x = dX; k.n = n; k.p = p; k.lam = lambda0; k.tol = tol; k.mi = max_iter; k.nzcap = nzcap;
+  k.o = o; k.th = dTheta; k.sg = dSigma; k.it = dIters; k.sw = dSweeps; k.cv = dConv;
+  k.gen = g_alloc_gen.load();
+  cudaGetDevice(&k.dev);
+  (void)s;
+  const unsigned char* b = (const unsigned char*)&k;
+  return std::vector<unsigned char>(b, b + sizeof(k));
+}
+
+void drop_graph(Workspace& W) {
+  if (W.gexec) { cudaGraphExecDestroy(W.gexec); W.gexec = nullptr; }
+  W.gkey.clear();
+}
+
 int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, double tol,
                     int32_t max_iter, const spmesl_options& o, double* dTheta, double* dSigma,
                     int32_t* dIters, int32_t* dSweeps, uint8_t* dConv, cudaStream_t s,
@@ -886,39 +998,93 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
   if ((o.solver == 2 || o.solver == 3) && !gram_ok)
     return fail(SPMESL_ERR_UNSUPPORTED, "Gram solver: " + why);
   const bool gram = gram_ok && o.solver != 1 && o.mode == 0;
-  // zero-fill Theta (8 p^2 bytes, the only dense pass) on a side stream while the solver runs
-  // (launched by run_prep right after standardization; joined before the assembly)
-  DevCounters* dc = nullptr;
-  for (int attempt = 0; attempt < 4; ++attempt) {
-    const size_t pp = (size_t)p * (size_t)p;
-    // the Gram kernel zero-fills Theta itself (bulk stores from its producer warp) when the
-    // buffer allows 16-byte pieces; otherwise a side-stream kernel does, after standardization
-    static const bool side_zero = getenv("SPMESL_DEV_SIDE_ZERO") != nullptr;   // (dev)
-    const bool take = gram && !side_zero && (((uintptr_t)dTheta & 15) == 0) && (pp & 1) == 0;
-    if (take) { W.take_zero = dTheta; W.take_count = pp; }
-    else { W.pending_zero = dTheta; W.pending_count = pp; }
-    if (gram) {
-      // everything is enqueued; the one host synchronisation is the counter read at the end
-      if (!nzcap) nzcap = initial_nzcap(n, p);
-      rc = fit_gram_enqueue(W, dX, n, p, lambda0, tol, max_iter, o, out, s, L, nzcap, nullptr, 1,
-                            o.solver != 2);
-    } else {
-      rc = fit_columns_core(W, dX, n, p, 0, p, lambda0, tol, max_iter, o, out, s, st, L, &nzcap);
+  if (gram) {
+    static const bool no_graph = getenv("SPMESL_NO_GRAPH") != nullptr;
+    // (no side-stream work may be captured: the fill must be the screening kernel's own)
+    const bool use_graph = !no_graph && !o.eager && getenv("SPMESL_DEV_SIDE_ZERO") == nullptr &&
+                           getenv("SPMESL_S16_ZFRAC") == nullptr && o.solver != 2 &&
+                           (((uintptr_t)dTheta & 15) == 0) && (((size_t)p * (size_t)p) & 1) == 0;
+    nzcap = (W.graph_nzcap > 0 && !W.gkey.empty()) ? W.graph_nzcap : initial_nzcap(n, p);
+    for (int attempt = 0; attempt < 4; ++attempt) {
+      std::vector<unsigned char> key = graph_key(dX, n, p, lambda0, tol, max_iter, o, dTheta,
+                                                 dSigma, dIters, dSweeps, dConv, nzcap, s);
+      bool launched = false;
+      if (use_graph && W.gexec && key == W.gkey) {
+        // replay: one launch for the whole fit (the penalty level is re-staged first)
+        W.lam_pinned[0] = lambda0;
+        CUDA_TRY(cudaGraphLaunch(W.gexec, s));
+        launched = true;
+      } else if (use_graph && key == W.last_key) {
+        // the same arguments twice in a row and nothing reallocated since: capture them
+        drop_graph(W);
+        const uint64_t gen0 = g_alloc_gen.load();
+        W.capturing = true;
+        cudaError_t e = cudaStreamBeginCapture(W.cap, cudaStreamCaptureModeRelaxed);
+        if (e == cudaSuccess) {
+          rc = gram_fit_enqueue_all(W, dX, n, p, lambda0, tol, max_iter, o, dTheta, dSigma,
+                                    dIters, dSweeps, dConv, out, W.cap, L, nzcap);
+          cudaGraph_t g = nullptr;
+          e = cudaStreamEndCapture(W.cap, &g);
+          W.capturing = false;
+          if (rc == SPMESL_OK && e == cudaSuccess && g &&
+              g_alloc_gen.load() == gen0 &&
+              cudaGraphInstantiate(&W.gexec, g, 0) == cudaSuccess) {
+            W.gkey = key;
+            W.graph_nzcap = nzcap;
+          } else {
+            W.gexec = nullptr;
+          }
+          if (g) cudaGraphDestroy(g);
+          cudaGetLastError();
+          if (rc) return rc;
+        }
+        W.capturing = false;
+        if (W.gexec) {
+          W.lam_pinned[0] = lambda0;
+          CUDA_TRY(cudaGraphLaunch(W.gexec, s));
+          launched = true;
+        }
+      }
+      if (!launched) {
+        rc = gram_fit_enqueue_all(W, dX, n, p, lambda0, tol, max_iter, o, dTheta, dSigma,
+                                  dIters, dSweeps, dConv, out, s, L, nzcap);
+        if (rc) return rc;
+        W.last_key = key;
+      }
+      CUDA_TRY(cudaStreamSynchronize(s));
+      if (W.host_counters->err) return std_error(W, st);
+      if (!W.host_counters->overflow) {
+        gram_stats(W, p, nzcap, st, o.solver != 2);
+        if (st) st->graph_replay = launched ? 1 : 0;
+        break;
+      }
+      if (nzcap >= p) return fail(SPMESL_ERR_OOM, "coefficient list overflow");
+      nzcap = (int)std::min<int64_t>(p, (int64_t)nzcap * 4);
+      drop_graph(W);
+      // (Theta's zero fill is redone by the next attempt: the assembly above wrote into it)
     }
-    W.take_zero = nullptr;
+    int any_unconv = 0;
+    finish_stats(W, p, st, &any_unconv);
+    if (st && st->graph_replay) {   // phase events not recorded by the replay (ev_record)
+      st->ms_standardize = st->ms_cd = st->ms_assemble = st->ms_tail = st->ms_gram = -1.0;
+    }
+    return any_unconv ? SPMESL_WARN_NOT_CONVERGED : SPMESL_OK;
+  }
+  // residual solver / joint mode: enqueue per call
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    W.pending_zero = dTheta; W.pending_count = (size_t)p * (size_t)p;
+    rc = fit_columns_core(W, dX, n, p, 0, p, lambda0, tol, max_iter, o, out, s, st, L, &nzcap);
     if (W.pending_zero) {    // (the solver failed before standardization)
       W.pending_zero = nullptr;
       if (!rc) rc = fail(SPMESL_ERR_CUDA, "internal: Theta zero fill was not launched");
     }
-    const bool join = !take || W.zero_join;
-    W.zero_join = false;
-    if (rc) { if (join) cudaStreamWaitEvent(s, W.ev_join, 0); return rc; }
-    if (join) CUDA_TRY(cudaStreamWaitEvent(s, W.ev_join, 0));
+    if (rc) { cudaStreamWaitEvent(s, W.ev_join, 0); return rc; }
+    CUDA_TRY(cudaStreamWaitEvent(s, W.ev_join, 0));
     const size_t cap = (size_t)p * (size_t)nzcap;
     if ((rc = ensure(W.csc_rows, cap * 4))) return rc;
     if ((rc = ensure(W.csc_vals, cap * 8))) return rc;
-    dc = (DevCounters*)W.counters.ptr;
-    CUDA_TRY(cudaEventRecord(W.ev[3], s));
+    DevCounters* dc = (DevCounters*)W.counters.ptr;
+    CUDA_TRY(ev_record(W, W.ev[3], s));
     CUDA_TRY(launch_csc_build((const int*)W.nz_count.ptr, (const int*)W.nz_cur.ptr,
                               (const int*)W.nz_rows.ptr, (const double*)W.nz_vals.ptr, (int)p,
                               nzcap, (int64_t*)W.col_ptr.ptr, (int32_t*)W.csc_rows.ptr,
@@ -928,27 +1094,13 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
                              (const double*)W.sigma_std.ptr,
                              o.standardize ? (const double*)W.scale.ptr : nullptr, o.symmetrize,
                              dTheta, dSigma, s, /*zero_fill=*/false));
-    CUDA_TRY(cudaEventRecord(W.ev[4], s));
+    CUDA_TRY(ev_record(W, W.ev[4], s));
     if ((rc = device_stats(W, dIters, dSweeps, dConv, p, s))) return rc;
     if ((rc = read_counters(W, s))) return rc;
-    if (!gram) break;
-    if (W.host_counters->err) return std_error(W, st);
-    if (!W.host_counters->overflow) { gram_stats(W, p, nzcap, st, o.solver != 2); break; }
-    if (nzcap >= p) return fail(SPMESL_ERR_OOM, "coefficient list overflow");
-    nzcap = (int)std::min<int64_t>(p, (int64_t)nzcap * 4);
-    // (Theta's zero fill is redone at the top of the loop: the assembly above wrote into it)
+    break;
   }
   int any_unconv = 0;
-  stats_from_counters(*W.host_counters, p, st, &any_unconv);
-  if (st) {
-    st->nnz = W.host_counters->csc_total;
-    st->ms_standardize = ev_ms(W.ev[0], W.ev[1]);
-    st->ms_cd = ev_ms(W.ev[1], W.ev[2]);
-    st->ms_assemble = ev_ms(W.ev[3], W.ev[4]);
-    st->ms_total = ev_ms(W.ev[0], W.ev[4]);
-    st->kernel_launches += 5;  // standardize, csc_scan, csc_copy, assemble x2 (+ solver kernels)
-    st->bad_column = -1;
-  }
+  finish_stats(W, p, st, &any_unconv);
   return any_unconv ? SPMESL_WARN_NOT_CONVERGED : SPMESL_OK;
 }
 
@@ -1028,8 +1180,8 @@ int fit_gram_columns_core(Workspace& W, const double* dX, int64_t n, int64_t p, 
       // dHit holds candidates (certified screening): their exact Gram columns decide
       if ((rc = ensure(W.hit, (size_t)p))) return rc;
       if ((rc = ensure(W.lam_dev, (size_t)SPMESL_MAX_LAM * 8))) return rc;
-      W.lam_host.assign(1, lambda0);
-      CUDA_TRY(cudaMemcpyAsync(W.lam_dev.ptr, W.lam_host.data(), 8, cudaMemcpyHostToDevice, s));
+      W.lam_pinned[0] = lambda0;
+      CUDA_TRY(cudaMemcpyAsync(W.lam_dev.ptr, W.lam_pinned, 8, cudaMemcpyHostToDevice, s));
       CUDA_TRY(cudaMemsetAsync(W.hit.ptr, 0, (size_t)p, s));
       CUDA_TRY(launch_gram_cols((const double*)W.xb.ptr, (int)L.nblk, L.nchunk, (int)n, (int)p,
                                 (const int*)W.uvars.ptr, nU, nullptr, W.sms, (double*)W.ondemand.ptr,
@@ -1040,7 +1192,7 @@ int fit_gram_columns_core(Workspace& W, const double* dX, int64_t n, int64_t p, 
                                 nullptr, 0, (const int*)W.uvars.ptr, nU, nullptr,
                                 (double*)W.ondemand.ptr, s));
     }
-    CUDA_TRY(cudaEventRecord(W.ev[7], s));
+    CUDA_TRY(ev_record(W, W.ev[7], s));
     GramParams G{};
     G.Xb = (const double*)W.xb.ptr;
     G.n = (int)n; G.n_pad = L.n_pad; G.nchunk = L.nchunk; G.p = (int)p; G.nblk = (int)L.nblk;
@@ -1058,7 +1210,7 @@ int fit_gram_columns_core(Workspace& W, const double* dX, int64_t n, int64_t p, 
     G.converged = out.conv;
     G.nz_count = (int*)W.nz_count.ptr; G.nz_cur = (int*)W.nz_cur.ptr;
     CUDA_TRY(launch_gram_init(G, s));
-    CUDA_TRY(cudaEventRecord(W.ev[5], s));
+    CUDA_TRY(ev_record(W, W.ev[5], s));
     TailParams T{};
     T.Xb = (const double*)W.xb.ptr;
     T.n = (int)n; T.n_pad = L.n_pad; T.nchunk = L.nchunk; T.p = (int)p; T.nblk = (int)L.nblk;
@@ -1083,8 +1235,8 @@ int fit_gram_columns_core(Workspace& W, const double* dX, int64_t n, int64_t p, 
     T.sigma_std = out.sigma_std; T.iters = out.iters; T.sweeps = out.sweeps; T.converged = out.conv;
     set_prefetch(W, T);
     CUDA_TRY(launch_tail_sweeps(T, (int)std::min<int64_t>(W.sms, m), s));
-    CUDA_TRY(cudaEventRecord(W.ev[6], s));
-    CUDA_TRY(cudaEventRecord(W.ev[2], s));
+    CUDA_TRY(ev_record(W, W.ev[6], s));
+    CUDA_TRY(ev_record(W, W.ev[2], s));
     if ((rc = read_counters(W, s))) return rc;
     if (W.host_counters->err) return std_error(W, st);
     if (!W.host_counters->overflow) {
@@ -1146,11 +1298,21 @@ int spmesl_release_workspace(void) {
                       &w->sigma_std, &w->iters, &w->sweeps, &w->conv, &w->nz_count, &w->nz_cur,
                       &w->nz_rows, &w->nz_vals, &w->col_ptr, &w->csc_rows, &w->csc_vals,
                       &w->hx, &w->htheta, &w->hsigma, &w->hiters, &w->hsweeps, &w->hconv,
-                      &w->coo_r, &w->coo_c, &w->coo_v, &w->hdiag, &w->zeros};
+                      &w->coo_r, &w->coo_c, &w->coo_v, &w->hdiag, &w->zeros, &w->ej, &w->act0,
+                      &w->act1, &w->keep, &w->jflags, &w->hit, &w->lam_dev, &w->nrm, &w->sq,
+                      &w->y16, &w->cand};
+    drop_graph(*w);
+    w->last_key.clear();
+    g_alloc_gen.fetch_add(1);
     for (Buffer* b : bufs) { if (b->ptr) cudaFree(b->ptr); b->ptr = nullptr; b->bytes = 0; }
     if (w->host_counters) cudaFreeHost(w->host_counters);
+    if (w->lam_pinned) cudaFreeHost(w->lam_pinned);
+    w->host_counters = nullptr;
+    w->lam_pinned = nullptr;
     for (auto& e : w->ev) if (e) cudaEventDestroy(e);
     if (w->side) cudaStreamDestroy(w->side);
+    if (w->cap) cudaStreamDestroy(w->cap);
+    w->cap = nullptr;
     if (w->ev_fork) cudaEventDestroy(w->ev_fork);
     if (w->ev_join) cudaEventDestroy(w->ev_join);
     w->side = nullptr; w->ev_fork = w->ev_join = nullptr;
@@ -1241,7 +1403,7 @@ int spmesl_fit_path_device(const double* dX, int64_t n, int64_t p, const double*
     if ((rc = ensure(W->csc_rows, cap * 4))) return rc;
     if ((rc = ensure(W->csc_vals, cap * 8))) return rc;
     dc = (DevCounters*)W->counters.ptr;
-    CUDA_TRY(cudaEventRecord(W->ev[3], s));
+    CUDA_TRY(ev_record(*W, W->ev[3], s));
     for (int l = 0; l < nlam; ++l) {   // CSC + assembly of each level (stream-ordered reuse)
       const size_t lo = (size_t)l * p;
       CUDA_TRY(launch_csc_build((const int*)W->nz_count.ptr + lo, (const int*)W->nz_cur.ptr + lo,
@@ -1255,7 +1417,7 @@ int spmesl_fit_path_device(const double* dX, int64_t n, int64_t p, const double*
                                o.standardize ? (const double*)W->scale.ptr : nullptr, o.symmetrize,
                                dTheta + l * pp, dSigma + lo, s, /*zero_fill=*/false));
     }
-    CUDA_TRY(cudaEventRecord(W->ev[4], s));
+    CUDA_TRY(ev_record(*W, W->ev[4], s));
     if ((rc = device_stats(*W, dIters, dSweeps, dConverged, m, s))) return rc;
     if ((rc = read_counters(*W, s))) return rc;
     if (W->host_counters->err) return std_error(*W, st);
@@ -1371,7 +1533,7 @@ int spmesl_fit_ex(const double* X, int64_t n, int64_t p, double lambda0, double 
   int ncoo = 0;
   {
     auto step = [&]() -> int {
-      CUDA_TRY(cudaEventRecord(W->ev[3], s));
+      CUDA_TRY(ev_record(*W, W->ev[3], s));
       CUDA_TRY(launch_csc_build((const int*)W->nz_count.ptr, (const int*)W->nz_cur.ptr,
                                 (const int*)W->nz_rows.ptr, (const double*)W->nz_vals.ptr, (int)p,
                                 nzcap, (int64_t*)W->col_ptr.ptr, (int32_t*)W->csc_rows.ptr,
@@ -1387,7 +1549,7 @@ int spmesl_fit_ex(const double* X, int64_t n, int64_t p, double lambda0, double 
                                    o.symmetrize, (int32_t*)W->coo_r.ptr, (int32_t*)W->coo_c.ptr,
                                    (double*)W->coo_v.ptr, &dc->coo_count, (double*)W->hdiag.ptr,
                                    (double*)W->hsigma.ptr, s));
-      CUDA_TRY(cudaEventRecord(W->ev[4], s));
+      CUDA_TRY(ev_record(*W, W->ev[4], s));
       if ((rc = read_counters(*W, s))) return rc;
       ncoo = W->host_counters->coo_count;
       cr.resize(ncoo); cc.resize(ncoo); cv.resize(ncoo);
@@ -1555,10 +1717,10 @@ int spmesl_gram_screen_device(const double* dX, int64_t n, int64_t p, double lam
     Q.eps = screen16_eps(L.n_pad);
     Q.epsn = screen16_epsn(n, Q.eps);
     Q.cand = dHit;
-    CUDA_TRY(cudaEventRecord(W->ev[8], s));
+    CUDA_TRY(ev_record(*W, W->ev[8], s));
     CUDA_TRY(launch_screen16(Q, (int)std::min<int64_t>(W->sms, std::max<int64_t>(1, tile_end - tile_begin)), s));
-    CUDA_TRY(cudaEventRecord(W->ev[9], s));
-    CUDA_TRY(cudaEventRecord(W->ev[7], s));
+    CUDA_TRY(ev_record(*W, W->ev[9], s));
+    CUDA_TRY(ev_record(*W, W->ev[7], s));
     if ((rc = read_counters(*W, s))) return rc;
     if (W->host_counters->err) return std_error(*W, st);
     if (st) {
@@ -1582,7 +1744,7 @@ int spmesl_gram_screen_device(const double* dX, int64_t n, int64_t p, double lam
   G.tile_begin = (int)tile_begin;
   G.tile_end = (int)tile_end;
   CUDA_TRY(launch_syrk_screen(G, (int)std::min<int64_t>(W->sms, std::max<int64_t>(1, tile_end - tile_begin)), s));
-  CUDA_TRY(cudaEventRecord(W->ev[7], s));
+  CUDA_TRY(ev_record(*W, W->ev[7], s));
   if ((rc = read_counters(*W, s))) return rc;
   if (W->host_counters->err) return std_error(*W, st);
   if (st) {

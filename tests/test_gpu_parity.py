@@ -419,3 +419,40 @@ def test_certified_screening_equals_full_gram(S):
         pb = S.fit_path_device(Xd, lams, solver="gram16")
         for x, y in zip(pa, pb):
             assert torch.equal(x.Theta, y.Theta) and torch.equal(x.sweeps, y.sweeps)
+
+
+def test_graph_replay_matches_eager(S, oracle):
+    """spmesl_fit_device with the same arguments: the second call captures the enqueued fit as
+    a CUDA graph and later calls replay it; every replay equals the eager fit bit for bit, and
+    a replay reads the current contents of X (new data at the same address -> new result)."""
+    import torch
+    X, _, _ = G.make_config(5, p=3000)
+    n, p = X.shape
+    lam = oracle.lambda_ub(n, p)
+    Xd = torch.from_numpy(np.ascontiguousarray(X.T)).cuda().t()
+
+    def outs():
+        return dict(theta=torch.empty((p, p), dtype=torch.float64, device="cuda"),
+                    sigma=torch.empty(p, dtype=torch.float64, device="cuda"),
+                    iters=torch.empty(p, dtype=torch.int32, device="cuda"),
+                    sweeps=torch.empty(p, dtype=torch.int32, device="cuda"),
+                    conv=torch.empty(p, dtype=torch.uint8, device="cuda"))
+
+    ref = S.fit_device(Xd, lam, out=outs(), eager=True)
+    ref = [t.clone() for t in (ref.Theta, ref.sigma, ref.iters, ref.sweeps)]
+    out = outs()
+    flags = []
+    for _ in range(4):
+        r = S.fit_device(Xd, lam, out=out)
+        flags.append(r.stats["graph_replay"])
+        got = (r.Theta, r.sigma, r.iters, r.sweeps)
+        assert all(torch.equal(a, b) for a, b in zip(got, ref))
+        assert r.stats["ms_total"] > 0 and r.stats["ms_screen"] > 0
+    assert flags == [0, 1, 1, 1]
+    # new data in the same buffer: the replay must see it
+    X2, _, _ = G.make_config(5, p=3000, seed=7)
+    Xd.copy_(torch.from_numpy(np.ascontiguousarray(X2.T)).cuda().t())
+    r = S.fit_device(Xd, lam, out=out)
+    assert r.stats["graph_replay"] == 1
+    e = S.fit_device(Xd, lam, out=outs(), eager=True)
+    assert torch.equal(r.Theta, e.Theta) and torch.equal(r.sweeps, e.sweeps)
