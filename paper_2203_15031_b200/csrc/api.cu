@@ -298,9 +298,10 @@ int run_tail(Workspace& W, const Layout& L, int64_t cb, double lambda0, double t
 }
 
 // Scratch reset + standardize (a2) + Gram band for columns [cb, cb + m) on stream s.
+// (Xb's padding is written by the standardization itself; y16: the certified screening's
+// operands, written by the same kernel)
 int run_prep(Workspace& W, const double* dX, int64_t m, const spmesl_options& o, const Layout& L,
-             cudaStream_t s, bool band = true) {
-  CUDA_TRY(cudaMemsetAsync(W.xb.ptr, 0, L.xb_doubles() * 8, s));
+             cudaStream_t s, bool band = true, const S16Prep* y16 = nullptr) {
   CUDA_TRY(cudaMemsetAsync(W.counters.ptr, 0, sizeof(DevCounters), s));
   CUDA_TRY(cudaMemsetAsync((char*)W.counters.ptr + offsetof(DevCounters, bad_key), 0xff, 8, s));
   CUDA_TRY(cudaMemsetAsync(W.queue.ptr, 0, 16, s));
@@ -310,7 +311,8 @@ int run_prep(Workspace& W, const double* dX, int64_t m, const spmesl_options& o,
   DevCounters* dc = (DevCounters*)W.counters.ptr;
   CUDA_TRY(launch_standardize(dX, L, o.standardize, (double*)W.xb.ptr, (double*)W.mean.ptr,
                               (double*)W.scale.ptr, &dc->err, &dc->bad_key, s,
-                              W.nrm.bytes >= (size_t)L.p * 8 ? (double*)W.nrm.ptr : nullptr));
+                              W.nrm.bytes >= (size_t)L.p * 8 ? (double*)W.nrm.ptr : nullptr,
+                              y16));
   if (band) CUDA_TRY(launch_gram((const double*)W.xb.ptr, L, (double*)W.gband.ptr, s));
   CUDA_TRY(ev_record(W, W.ev[1], s));
   if (W.pending_zero) {
@@ -643,7 +645,22 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
     if ((rc = ensure(W.uvars, (size_t)p * 4))) return rc;
   }
   DevCounters* dc = (DevCounters*)W.counters.ptr;
-  if ((rc = run_prep(W, dX, m * nlam, o, L, s, /*band=*/false))) return rc;
+  // the screening level: the smallest penalty (a superset of every level's hits)
+  double lam_screen = lambda0;
+  if (nlam > 1) { lam_screen = lams[0]; for (int l = 1; l < nlam; ++l) lam_screen = std::min(lam_screen, lams[l]); }
+  const int64_t p_pad16 = screen16 ? screen16_pad(p) : 0;
+  float* inv_sq = screen16 ? (float*)W.sq.ptr : nullptr;
+  float* lam_n = screen16 ? inv_sq + p_pad16 : nullptr;
+  double* sqv = screen16 ? (double*)(lam_n + p_pad16) : nullptr;
+  S16Prep yprep{};
+  if (screen16) {
+    yprep.Y16 = (__half*)W.y16.ptr;
+    yprep.nchunk64 = (L.n_pad + 63) / 64;
+    yprep.p_pad = p_pad16;
+    yprep.sq = sqv; yprep.inv_sq = inv_sq; yprep.lam_n = lam_n;
+    yprep.lambda0 = lam_screen;
+  }
+  if ((rc = run_prep(W, dX, m * nlam, o, L, s, /*band=*/false, screen16 ? &yprep : nullptr))) return rc;
   CUDA_TRY(cudaMemsetAsync(W.hit.ptr, 0, (size_t)p * nlam, s));
   {
     double lv[SPMESL_MAX_LAM];
@@ -686,14 +703,7 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   if (screen16) {
     // certified f16 screening (screen16.cu): candidate columns, then their exact FP64 Gram
     // columns and the exact decision; one host round trip for the candidate list
-    const int64_t p_pad = screen16_pad(p);
-    float* inv_sq = (float*)W.sq.ptr;
-    float* lam_n = inv_sq + p_pad;
-    double* sqv = (double*)(lam_n + p_pad);
-    CUDA_TRY(launch_sqrt((const double*)W.nrm.ptr, sqv, inv_sq, lam_n, G.lambda0,
-                         (int)n, (int)p, (int)p_pad, s));
-    CUDA_TRY(launch_to_f16((const double*)W.xb.ptr, (const double*)W.nrm.ptr, (int)p, L.n_pad,
-                           L.nchunk, (__half*)W.y16.ptr, s));
+    // (y16 operands and threshold factors were written by the standardization)
     CUDA_TRY(cudaMemsetAsync(W.cand.ptr, 0, (size_t)p, s));
     Screen16Params Q{};
     Q.Y16 = (const __half*)W.y16.ptr;
@@ -736,7 +746,7 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
       W.zero_join = true;
       ++launches;
     }
-    launches += 3;   // sqrt, to_f16, screen16
+    launches += 1;   // screen16
     // candidate list on the device; then, by its count (read on the device), either the exact
     // Gram columns of the candidates (2 n p nU flops) or — when most columns are candidates
     // (multi-sweep workloads) — the symmetric FP64 Gram kernel (n p (p+1) flops) decides

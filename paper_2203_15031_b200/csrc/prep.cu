@@ -5,11 +5,14 @@
 //   g14), x~_ik = (x_ik - mu_k) / s_k written straight into the tiled HBM layout Xb (see
 //   spmesl_internal.cuh).  Column k is an error if any x_ik is not finite or if
 //   s_k <= 1e-13 max_i |x_ik| (reading g15); the smallest offending column wins.
-//   HBM-bound: reads X twice (8np B each, the second from L2) and writes Xb (8np B).
+//   HBM-bound: reads X twice (8np B each, the second from L2) and writes Xb (8np B) including
+//   its zero padding (samples n..n_pad, rows p..nblk*32: no separate memset).  With S16Prep it
+//   also writes the certified screening's f16 operand y = x~/sqrt(N_k) and threshold factors.
 //
 // gram_kernel — the couplings G_jj' = x~_j^T x~_j' / n between each row j of block b and the
 //   rows j' of blocks b-1 and b, which let the CD kernel process Proposition 2's row order
 //    32 rows at a time with a lag-1 pipeline.  2 p 32 n FMAs, tiny.
+#include <algorithm>
 #include "spmesl_internal.cuh"
 
 namespace spmesl {
@@ -20,13 +23,32 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// y_k (f16) of sample i in the Y16 tile layout of screen16.cu: tiles of 128 variables x 64
+// samples, 128-byte rows whose 16-byte chunks are XOR-swizzled by (row & 7)
+__device__ __forceinline__ size_t y16_index(int64_t k, int64_t i, int nchunk64) {
+  const int64_t blk = k >> 7, r = k & 127, q = i >> 6, pos = i & 63;
+  return (size_t)((blk * nchunk64 + q) * 8192 + r * 64 + ((((pos >> 3) ^ (r & 7))) << 3) + (pos & 7));
+}
+
 __global__ void standardize_kernel(const double* __restrict__ X, int64_t n, int64_t p, int nchunk,
-                                   int standardize, double* __restrict__ Xb, double* mu,
-                                   double* scale, int* err, unsigned long long* bad_key,
-                                   double* nrm) {
+                                   int64_t nrows, int standardize, double* __restrict__ Xb,
+                                   double* mu, double* scale, int* err, unsigned long long* bad_key,
+                                   double* nrm, S16Prep y) {
   const int lane = threadIdx.x & 31;
   const int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (k >= p) return;
+  const int64_t n_pad = (int64_t)nchunk * KC;
+  const int64_t n64 = (int64_t)y.nchunk64 * 64;
+  if (k >= p) {
+    // padding rows: zeros in Xb and Y16, threshold factors that never flag
+    if (k < nrows)
+      for (int64_t i = lane; i < n_pad; i += 32) Xb[xb_index(i, k, nchunk)] = 0.0;
+    if (y.Y16 && k < y.p_pad) {
+      for (int64_t i0 = 8 * lane; i0 < n64; i0 += 256)
+        *(uint4*)(y.Y16 + y16_index(k, i0, y.nchunk64)) = make_uint4(0u, 0u, 0u, 0u);
+      if (lane == 0) { y.inv_sq[k] = __int_as_float(0x7f800000); y.lam_n[k] = 0.f; }
+    }
+    return;
+  }
   const double* x = X + k * n;
   double sum = 0.0, mx = 0.0;
   bool finite = true;
@@ -61,13 +83,35 @@ __global__ void standardize_kernel(const double* __restrict__ X, int64_t n, int6
   }
   if (lane == 0) { mu[k] = m; scale[k] = s; }
   double g = 0.0;
-  for (int64_t i = lane; i < n; i += 32) {
-    double v = standardize ? (x[i] - m) / s : x[i];
+  for (int64_t i = lane; i < n_pad; i += 32) {
+    const double v = i < n ? (standardize ? (x[i] - m) / s : x[i]) : 0.0;
     Xb[xb_index(i, k, nchunk)] = v;
     g = fma(v, v, g);
   }
   g = warp_sum(g);
-  if (lane == 0 && nrm) nrm[k] = g / (double)n;     // N_k = x~_k^T x~_k / n (= S_kk)
+  const double Nk = g / (double)n;                   // N_k = x~_k^T x~_k / n (= S_kk)
+  if (lane == 0 && nrm) nrm[k] = Nk;
+  if (y.Y16) {
+    // y = x~ / sqrt(N_k) in f16 (the same double product to_f16_kernel forms), and the
+    // epilogue's threshold factors (as sqrt_kernel: directed roundings)
+    const double sc = rsqrt(Nk);
+    for (int64_t i0 = 8 * lane; i0 < n64; i0 += 256) {   // 8 samples = one 16-byte chunk
+      __align__(16) __half h[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int64_t i = i0 + t;
+        const double v = i < n ? (standardize ? (x[i] - m) / s : x[i]) : 0.0;
+        h[t] = __double2half(v * sc);
+      }
+      *(uint4*)(y.Y16 + y16_index(k, i0, y.nchunk64)) = *(const uint4*)h;
+    }
+    if (lane == 0) {
+      const double q = sqrt(Nk);
+      y.sq[k] = q;
+      y.inv_sq[k] = __double2float_rd(1.0 / q * (1.0 - 0x1p-40));
+      y.lam_n[k] = __double2float_rd((double)n * y.lambda0 / q * (1.0 - 0x1p-40));
+    }
+  }
 }
 
 // D(8x8) += A(8x4) B(4x8) in fp64 on the tensor cores (fragment layout: see cd_sweep.cu)
@@ -125,11 +169,15 @@ __global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ Xb
 
 cudaError_t launch_standardize(const double* X, const Layout& L, int standardize, double* Xb,
                                double* mu, double* scale, int* err, unsigned long long* bad_key,
-                               cudaStream_t s, double* nrm) {
+                               cudaStream_t s, double* nrm, const S16Prep* y) {
   const int wpb = 8;
-  dim3 grid((unsigned)((L.p + wpb - 1) / wpb));
-  standardize_kernel<<<grid, wpb * 32, 0, s>>>(X, L.n, L.p, L.nchunk, standardize, Xb, mu, scale,
-                                               err, bad_key, nrm);
+  S16Prep yy{};
+  if (y) yy = *y;
+  const int64_t nrows = L.nblk * J;                 // Xb rows incl. padding
+  const int64_t cols = std::max<int64_t>(nrows, yy.Y16 ? yy.p_pad : 0);
+  dim3 grid((unsigned)((cols + wpb - 1) / wpb));
+  standardize_kernel<<<grid, wpb * 32, 0, s>>>(X, L.n, L.p, L.nchunk, nrows, standardize, Xb, mu,
+                                               scale, err, bad_key, nrm, yy);
   return cudaGetLastError();
 }
 

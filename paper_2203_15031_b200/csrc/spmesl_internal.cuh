@@ -231,9 +231,21 @@ size_t cd_smem_bytes(int T, int n_pad);          // with the minimum 2 stages
 int cd_stages(int T, int n_pad, size_t smem_optin);  // stages that fit (0: does not fit)
 
 // Launchers (stream-ordered, no host synchronisation).
+// Optional outputs of the standardization for the certified f16 screening (screen16.cu):
+// y_k = x~_k / sqrt(N_k) as f16 tiles, sq_k = sqrt(N_k), inv_sq / lam_n (directed roundings),
+// including the zero / +inf padding up to p_pad.  Replaces to_f16 + sqrt kernels.
+struct S16Prep {
+  __half* Y16;
+  int nchunk64;
+  int64_t p_pad;
+  double* sq;
+  float* inv_sq;
+  float* lam_n;
+  double lambda0;
+};
 cudaError_t launch_standardize(const double* X, const Layout& L, int standardize, double* Xb,
-                               double* mu, double* scale, int* err, unsigned long long* bad_col,
-                               cudaStream_t s, double* nrm = nullptr);
+                               double* mu, double* scale, int* err, unsigned long long* bad_key,
+                               cudaStream_t s, double* nrm = nullptr, const S16Prep* y = nullptr);
 cudaError_t launch_gram(const double* Xb, const Layout& L, double* Gband, cudaStream_t s);
 cudaError_t launch_cd(const CDParams& P, int num_ctas, cudaStream_t s);
 cudaError_t launch_csc_build(const int* nz_count, const int* nz_cur, const int* nz_rows,

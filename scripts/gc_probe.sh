@@ -6,5 +6,5 @@ run() {
 for l in sys.stdin:
   if l.startswith('{'): d=json.loads(l); print(round(d['ms_per_step'],4), round(d['roofline']['kernel_ms'],4), d['roofline']['frac'], d['gpu_launches'], d['ms_breakdown'], d['graph_replay'])"
 }
-run SPMESL_NO_GRAPH=1
 run A=1
+SPMESL_NO_GRAPH=1 timeout 180 python scripts/timeline_probe.py 5 2>&1 | tail -22 | cut -c1-110
