@@ -94,6 +94,7 @@ struct Workspace {
   Buffer hit;                                               // Gram solver screening flags
   Buffer lam_dev;                                           // multi-lambda: penalty levels
   Buffer nrm, sq, y16, cand;                                // certified f16 screening
+  Buffer ssq;                                               // x~_c^T x~_c (Gram solvers)
   // host-API staging
   Buffer hx, htheta, hsigma, hiters, hsweeps, hconv, coo_r, coo_c, coo_v, hdiag, zeros;
   DevCounters* host_counters = nullptr;   // pinned
@@ -312,7 +313,7 @@ int run_prep(Workspace& W, const double* dX, int64_t m, const spmesl_options& o,
   CUDA_TRY(launch_standardize(dX, L, o.standardize, (double*)W.xb.ptr, (double*)W.mean.ptr,
                               (double*)W.scale.ptr, &dc->err, &dc->bad_key, s,
                               W.nrm.bytes >= (size_t)L.p * 8 ? (double*)W.nrm.ptr : nullptr,
-                              y16));
+                              y16, W.ssq.bytes >= (size_t)L.p * 8 ? (double*)W.ssq.ptr : nullptr));
   if (band) CUDA_TRY(launch_gram((const double*)W.xb.ptr, L, (double*)W.gband.ptr, s));
   CUDA_TRY(ev_record(W, W.ev[1], s));
   if (W.pending_zero) {
@@ -635,6 +636,7 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   if ((rc = ensure(W.ondemand, (size_t)p * p * 8))) return rc;
   if ((rc = ensure(W.hit, (size_t)p * nlam))) return rc;
   if ((rc = ensure(W.lam_dev, (size_t)SPMESL_MAX_LAM * 8))) return rc;
+  if ((rc = ensure(W.ssq, (size_t)p * 8))) return rc;
   if (screen16) {
     if ((rc = ensure(W.nrm, (size_t)p * 8))) return rc;
     // inv_sq, lam_n (f32, padded to the 128-column tiles; 16-byte aligned) + sq (f64, p)
@@ -684,6 +686,7 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   G.max_outer = max_iter;
   G.G = (double*)W.ondemand.ptr;
   G.hit = (uint8_t*)W.hit.ptr;
+  G.ssq = (const double*)W.ssq.ptr;
   G.tile_begin = 0;
   G.tile_end = gram_tile_count(p);
   if (W.pending_zero == nullptr && W.take_zero && (((uintptr_t)W.take_zero & 15) == 0) &&
@@ -932,20 +935,14 @@ int gram_fit_enqueue_all(Workspace& W, const double* dX, int64_t n, int64_t p, d
   W.zero_join = false;
   if (rc) { if (join) cudaStreamWaitEvent(cs, W.ev_join, 0); return rc; }
   if (join) CUDA_TRY(cudaStreamWaitEvent(cs, W.ev_join, 0));
-  const size_t cap = (size_t)p * (size_t)nzcap;
-  if ((rc = ensure(W.csc_rows, cap * 4))) return rc;
-  if ((rc = ensure(W.csc_vals, cap * 8))) return rc;
   DevCounters* dc = (DevCounters*)W.counters.ptr;
   CUDA_TRY(ev_record(W, W.ev[3], cs));
-  CUDA_TRY(launch_csc_build((const int*)W.nz_count.ptr, (const int*)W.nz_cur.ptr,
-                            (const int*)W.nz_rows.ptr, (const double*)W.nz_vals.ptr, (int)p,
-                            nzcap, (int64_t*)W.col_ptr.ptr, (int32_t*)W.csc_rows.ptr,
-                            (double*)W.csc_vals.ptr, &dc->csc_total, cs));
-  CUDA_TRY(launch_assemble(p, 0, p, (const int64_t*)W.col_ptr.ptr,
-                           (const int32_t*)W.csc_rows.ptr, (const double*)W.csc_vals.ptr,
-                           (const double*)W.sigma_std.ptr,
-                           o.standardize ? (const double*)W.scale.ptr : nullptr, o.symmetrize,
-                           dTheta, dSigma, cs, /*zero_fill=*/false));
+  // assembly + symmetrization straight from the coefficient lists (no CSC packing)
+  CUDA_TRY(launch_assemble_lists(p, (const int*)W.nz_count.ptr, (const int*)W.nz_cur.ptr,
+                                 (const int*)W.nz_rows.ptr, (const double*)W.nz_vals.ptr, nzcap,
+                                 (const double*)W.sigma_std.ptr,
+                                 o.standardize ? (const double*)W.scale.ptr : nullptr,
+                                 o.symmetrize, dTheta, dSigma, &dc->csc_total, cs));
   CUDA_TRY(ev_record(W, W.ev[4], cs));
   if ((rc = device_stats(W, dIters, dSweeps, dConv, p, cs))) return rc;
   CUDA_TRY(cudaMemcpyAsync(W.host_counters, W.counters.ptr, sizeof(DevCounters),
@@ -953,7 +950,7 @@ int gram_fit_enqueue_all(Workspace& W, const double* dX, int64_t n, int64_t p, d
   return SPMESL_OK;
 }
 
-void finish_stats(Workspace& W, int64_t p, spmesl_stats* st, int* any_unconv) {
+void finish_stats(Workspace& W, int64_t p, spmesl_stats* st, int* any_unconv, int launches) {
   stats_from_counters(*W.host_counters, p, st, any_unconv);
   if (st) {
     st->nnz = W.host_counters->csc_total;
@@ -961,7 +958,7 @@ void finish_stats(Workspace& W, int64_t p, spmesl_stats* st, int* any_unconv) {
     st->ms_cd = ev_ms(W.ev[1], W.ev[2]);
     st->ms_assemble = ev_ms(W.ev[3], W.ev[4]);
     st->ms_total = ev_ms(W.ev[0], W.ev[4]);
-    st->kernel_launches += 5;  // standardize, csc_scan, csc_copy, assemble x2 (+ solver kernels)
+    st->kernel_launches += launches;   // (+ the solver kernels, counted by the solver)
     st->bad_column = -1;
   }
 }
@@ -1074,7 +1071,7 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
       // (Theta's zero fill is redone by the next attempt: the assembly above wrote into it)
     }
     int any_unconv = 0;
-    finish_stats(W, p, st, &any_unconv);
+    finish_stats(W, p, st, &any_unconv, 3);   // standardize, assemble_lists, column_stats
     if (st && st->graph_replay) {   // phase events not recorded by the replay (ev_record)
       st->ms_standardize = st->ms_cd = st->ms_assemble = st->ms_tail = st->ms_gram = -1.0;
     }
@@ -1110,7 +1107,7 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
     break;
   }
   int any_unconv = 0;
-  finish_stats(W, p, st, &any_unconv);
+  finish_stats(W, p, st, &any_unconv, 5);   // standardize, csc_scan, csc_copy, assemble x2
   return any_unconv ? SPMESL_WARN_NOT_CONVERGED : SPMESL_OK;
 }
 
@@ -1173,6 +1170,7 @@ int fit_gram_columns_core(Workspace& W, const double* dX, int64_t n, int64_t p, 
     if ((rc = ensure(W.ondemand, (size_t)p * p * 8))) return rc;
     if ((rc = ensure(W.umap, (size_t)p * 4))) return rc;             // gstate
     if ((rc = ensure(W.uvars, (size_t)std::max<int64_t>(m, 1) * 4))) return rc;
+    if ((rc = ensure(W.ssq, (size_t)p * 8))) return rc;
     DevCounters* dc = (DevCounters*)W.counters.ptr;
     if ((rc = run_prep(W, dX, m, o, L, s, /*band=*/false))) return rc;
     CUDA_TRY(cudaMemcpyAsync(hh.data(), dHit + cb, (size_t)m, cudaMemcpyDeviceToHost, s));
@@ -1214,6 +1212,7 @@ int fit_gram_columns_core(Workspace& W, const double* dX, int64_t n, int64_t p, 
     G.max_outer = max_iter;
     G.G = nullptr;
     G.hit = const_cast<uint8_t*>(hit);
+    G.ssq = (const double*)W.ssq.ptr;
     G.tail = (TailState*)W.tail.ptr;
     G.tail_count = &dc->tail_count;
     G.sigma_std = out.sigma_std; G.iters = out.iters; G.sweeps = out.sweeps;
@@ -1310,7 +1309,7 @@ int spmesl_release_workspace(void) {
                       &w->hx, &w->htheta, &w->hsigma, &w->hiters, &w->hsweeps, &w->hconv,
                       &w->coo_r, &w->coo_c, &w->coo_v, &w->hdiag, &w->zeros, &w->ej, &w->act0,
                       &w->act1, &w->keep, &w->jflags, &w->hit, &w->lam_dev, &w->nrm, &w->sq,
-                      &w->y16, &w->cand};
+                      &w->y16, &w->cand, &w->ssq};
     drop_graph(*w);
     w->last_key.clear();
     g_alloc_gen.fetch_add(1);

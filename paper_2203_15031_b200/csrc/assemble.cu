@@ -17,45 +17,60 @@
 
 namespace spmesl {
 
-// Exclusive scan of counts -> col_ptr[0..ncols], single CTA (ncols up to a few 1e5).
-__global__ void __launch_bounds__(1024) csc_scan_kernel(const int* __restrict__ cnt, int ncols,
+// Exclusive scan of counts -> col_ptr[0..ncols], single CTA: thread t sums its contiguous
+// segment of ceil(ncols / 1024) counts, one block-wide scan of the 1024 partial sums, then each
+// thread writes its segment (one barrier round instead of one per 1024 columns).
+__global__ void __launch_bounds__(1024) csc_scan_kernel(const int* __restrict__ cnt_g, int ncols,
                                                         int64_t* __restrict__ col_ptr,
-                                                        int64_t* total) {
+                                                        int64_t* total, int staged) {
   __shared__ int64_t warp_tot[32];
-  __shared__ int64_t carry;
+  extern __shared__ int cnt_s[];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  if (tid == 0) carry = 0;
+  // counts staged in shared memory by coalesced loads when they fit (the segments below are
+  // strided across threads)
+  const int* cnt = cnt_g;
+  if (staged) {
+    for (int i0 = tid; i0 < ncols; i0 += 8 * 1024) {   // 8 loads in flight per thread
+      int v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = (i0 + u * 1024 < ncols) ? __ldg(cnt_g + i0 + u * 1024) : 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (i0 + u * 1024 < ncols) cnt_s[i0 + u * 1024] = v[u];
+    }
+    __syncthreads();
+    cnt = cnt_s;
+  }
+  const int seg = (ncols + 1023) / 1024;
+  const int lo = min(ncols, tid * seg), hi = min(ncols, lo + seg);
+  int64_t v = 0;
+  for (int i = lo; i < hi; ++i) v += cnt[i];
+  int64_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[w] = x;
   __syncthreads();
-  for (int base = 0; base < ncols; base += 1024) {
-    const int i = base + tid;
-    int64_t v = (i < ncols) ? (int64_t)cnt[i] : 0;
-    int64_t x = v;
+  if (w == 0) {
+    int64_t t = warp_tot[lane];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      int64_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
+      const int64_t y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
     }
-    if (lane == 31) warp_tot[w] = x;
-    __syncthreads();
-    if (w == 0) {
-      int64_t s = warp_tot[lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int64_t y = __shfl_up_sync(0xffffffffu, s, o);
-        if (lane >= o) s += y;
-      }
-      warp_tot[lane] = s;  // inclusive over warps
-    }
-    __syncthreads();
-    const int64_t excl = carry + (w ? warp_tot[w - 1] : 0) + x - v;
-    if (i < ncols) col_ptr[i] = excl;
-    __syncthreads();
-    if (tid == 1023) carry = excl + v;
-    __syncthreads();
+    warp_tot[lane] = t;  // inclusive over warps
   }
-  if (tid == 0) {
-    col_ptr[ncols] = carry;
-    *total = carry;
+  __syncthreads();
+  int64_t run = (w ? warp_tot[w - 1] : 0) + x - v;   // exclusive prefix of this segment
+  for (int i = lo; i < hi; ++i) {
+    col_ptr[i] = run;
+    run += cnt[i];
+  }
+  if (tid == 1023) {
+    col_ptr[ncols] = warp_tot[31];
+    *total = warp_tot[31];
   }
 }
 
@@ -137,6 +152,61 @@ __global__ void assemble_entries_kernel(int64_t p, int64_t col_begin, int64_t co
   }
 }
 
+// Device-path assembly straight from the per-column coefficient lists (rows ascending; no CSC
+// packing): one warp per column k writes its off-diagonal entries (a8 + a10: the partner b_kj
+// is found by binary search in column j's list, exactly as in the CSC variant) and lane 0 the
+// diagonal and sigma; the column's entry count is added to
+// *nnz_total.  Bit-identical to csc_build + assemble_entries + assemble_diag.
+__global__ void assemble_lists_kernel(int64_t p, const int* __restrict__ cnt,
+                                      const int* __restrict__ cur,
+                                      const int* __restrict__ nz_rows,
+                                      const double* __restrict__ nz_vals, int nzcap,
+                                      const double* __restrict__ sigma_std,
+                                      const double* __restrict__ scale, int symmetrize,
+                                      int rescale, double* __restrict__ Theta,
+                                      double* __restrict__ sigma_out,
+                                      unsigned long long* __restrict__ nnz_total) {
+  const int lane = threadIdx.x & 31;
+  const int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (k >= p) return;
+  const int m = min(cnt[k], nzcap);
+  const double sk = rescale ? scale[k] : 1.0;
+  if (lane == 0) {
+    const double sg = sigma_std[k];
+    double w = 1.0 / (sg * sg);
+    if (rescale) w = w / (sk * sk);
+    Theta[(size_t)k * (size_t)p + (size_t)k] = w;
+    if (sigma_out) sigma_out[k] = rescale ? sk * sg : sg;
+    if (m) atomicAdd(nnz_total, (unsigned long long)m);
+  }
+  const size_t base = (size_t)k * 2 * nzcap + (size_t)cur[k] * nzcap;
+  for (int e = lane; e < m; e += 32) {
+    const int j = nz_rows[base + e];
+    const double sj = rescale ? scale[j] : 1.0;
+    const double t_jk = theta1(nz_vals[base + e], sigma_std[k], sj, sk, rescale != 0);
+    double out = t_jk;
+    if (symmetrize) {
+      const size_t bj = (size_t)j * 2 * nzcap + (size_t)cur[j] * nzcap;
+      const int mj = min(cnt[j], nzcap);
+      int lo = 0, hi = mj;
+      double b_kj = 0.0;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        const int v = nz_rows[bj + mid];
+        if (v == (int)k) { b_kj = nz_vals[bj + mid]; break; }
+        if (v < (int)k) lo = mid + 1;
+        else hi = mid;
+      }
+      if (b_kj == 0.0) continue;            // partner zero -> symmetrized value is zero
+      const double t_kj = theta1(b_kj, sigma_std[j], sk, sj, rescale != 0);
+      const double u = (j < k) ? t_jk : t_kj;   // Theta1[min, max]
+      const double l = (j < k) ? t_kj : t_jk;   // Theta1[max, min]
+      out = (fabs(u) > fabs(l)) ? l : u;
+    }
+    Theta[(size_t)k * (size_t)p + (size_t)j] = out;
+  }
+}
+
 __global__ void assemble_diag_kernel(int64_t p, int64_t col_begin, int64_t col_end,
                                      const double* __restrict__ sigma_std,
                                      const double* __restrict__ scale, int rescale,
@@ -206,7 +276,16 @@ cudaError_t launch_assemble_coo(int64_t p, const int64_t* col_ptr, const int32_t
 cudaError_t launch_csc_build(const int* nz_count, const int* nz_cur, const int* nz_rows,
                              const double* nz_vals, int ncols, int nzcap, int64_t* col_ptr,
                              int32_t* rows, double* vals, int64_t* total, cudaStream_t s) {
-  csc_scan_kernel<<<1, 1024, 0, s>>>(nz_count, ncols, col_ptr, total);
+  const bool staged = (size_t)ncols * 4 <= 160 * 1024;
+  if (staged) {
+    static int attr = 0;
+    if (!attr) {
+      cudaFuncSetAttribute(csc_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      attr = 1;
+    }
+  }
+  csc_scan_kernel<<<1, 1024, staged ? (size_t)ncols * 4 : 0, s>>>(nz_count, ncols, col_ptr, total,
+                                                                 staged ? 1 : 0);
   const int wpb = 8;
   csc_copy_kernel<<<(ncols + wpb - 1) / wpb, wpb * 32, 0, s>>>(nz_count, nz_cur, nz_rows, nz_vals,
                                                                ncols, nzcap, col_ptr, rows, vals);
@@ -233,6 +312,18 @@ cudaError_t launch_assemble(int64_t p, int64_t col_begin, int64_t col_end, const
   assemble_diag_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(p, col_begin, col_end,
                                                                    sigma_std, scale, rescale,
                                                                    Theta, sigma_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_assemble_lists(int64_t p, const int* nz_count, const int* nz_cur,
+                                  const int* nz_rows, const double* nz_vals, int nzcap,
+                                  const double* sigma_std, const double* scale, int symmetrize,
+                                  double* Theta, double* sigma_out, int64_t* nnz_total,
+                                  cudaStream_t s) {
+  const int wpb = 8;
+  assemble_lists_kernel<<<(unsigned)((p + wpb - 1) / wpb), wpb * 32, 0, s>>>(
+      p, nz_count, nz_cur, nz_rows, nz_vals, nzcap, sigma_std, scale, symmetrize,
+      scale != nullptr, Theta, sigma_out, (unsigned long long*)nnz_total);
   return cudaGetLastError();
 }
 

@@ -313,12 +313,16 @@ __global__ void gram_init_kernel(const GramParams P) {
   ts.lam = l; ts.sigma = 1.0;
   if (!P.hit[(size_t)l * P.p + gc]) {
     double ss = 0.0;
-    for (int i = lane; i < P.n; i += 32) {
-      const double r = P.Xb[xb_index(i, gc, P.nchunk)];
-      ss = fma(r, r, ss);
-    }
+    if (P.ssq) {
+      ss = P.ssq[gc];   // (summed by the standardization in this very order)
+    } else {
+      for (int i = lane; i < P.n; i += 32) {
+        const double r = P.Xb[xb_index(i, gc, P.nchunk)];
+        ss = fma(r, r, ss);
+      }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    }
     double sn = sqrt(ss) / P.sqrt_n;
     if (sn < P.sigma_floor) sn = P.sigma_floor;                  // reading g5
     if (lane == 0) {

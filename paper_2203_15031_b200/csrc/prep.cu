@@ -33,7 +33,7 @@ __device__ __forceinline__ size_t y16_index(int64_t k, int64_t i, int nchunk64) 
 __global__ void standardize_kernel(const double* __restrict__ X, int64_t n, int64_t p, int nchunk,
                                    int64_t nrows, int standardize, double* __restrict__ Xb,
                                    double* mu, double* scale, int* err, unsigned long long* bad_key,
-                                   double* nrm, S16Prep y) {
+                                   double* nrm, S16Prep y, double* ssq) {
   const int lane = threadIdx.x & 31;
   const int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int64_t n_pad = (int64_t)nchunk * KC;
@@ -91,6 +91,9 @@ __global__ void standardize_kernel(const double* __restrict__ X, int64_t n, int6
   g = warp_sum(g);
   const double Nk = g / (double)n;                   // N_k = x~_k^T x~_k / n (= S_kk)
   if (lane == 0 && nrm) nrm[k] = Nk;
+  // (the same lane-strided fma chain and xor reduction as gram_init_kernel's ||x~_c||^2, so
+  // that kernel can take the value instead of re-reading X~: bit-identical)
+  if (lane == 0 && ssq) ssq[k] = g;
   if (y.Y16) {
     // y = x~ / sqrt(N_k) in f16 (the same double product to_f16_kernel forms), and the
     // epilogue's threshold factors (as sqrt_kernel: directed roundings)
@@ -169,7 +172,7 @@ __global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ Xb
 
 cudaError_t launch_standardize(const double* X, const Layout& L, int standardize, double* Xb,
                                double* mu, double* scale, int* err, unsigned long long* bad_key,
-                               cudaStream_t s, double* nrm, const S16Prep* y) {
+                               cudaStream_t s, double* nrm, const S16Prep* y, double* ssq) {
   const int wpb = 8;
   S16Prep yy{};
   if (y) yy = *y;
@@ -177,7 +180,7 @@ cudaError_t launch_standardize(const double* X, const Layout& L, int standardize
   const int64_t cols = std::max<int64_t>(nrows, yy.Y16 ? yy.p_pad : 0);
   dim3 grid((unsigned)((cols + wpb - 1) / wpb));
   standardize_kernel<<<grid, wpb * 32, 0, s>>>(X, L.n, L.p, L.nchunk, nrows, standardize, Xb, mu,
-                                               scale, err, bad_key, nrm, yy);
+                                               scale, err, bad_key, nrm, yy, ssq);
   return cudaGetLastError();
 }
 

@@ -146,6 +146,7 @@ struct GramParams {
   int nst;
   double* G;               // [p][p] column-major (nullptr: screening only)
   uint8_t* hit;            // [nlam][p] column has some |G_jc| > lambda0_l, j != c
+  const double* ssq;       // optional [p]: x~_c^T x~_c as the standardization summed it
   int nlam;                // penalty levels screened / fitted together (1..SPMESL_MAX_LAM)
   double lams[8];          // their lambda0 values
   int tile_begin, tile_end;   // upper-triangle tiles to process (multi-GPU share)
@@ -245,7 +246,8 @@ struct S16Prep {
 };
 cudaError_t launch_standardize(const double* X, const Layout& L, int standardize, double* Xb,
                                double* mu, double* scale, int* err, unsigned long long* bad_key,
-                               cudaStream_t s, double* nrm = nullptr, const S16Prep* y = nullptr);
+                               cudaStream_t s, double* nrm = nullptr, const S16Prep* y = nullptr,
+                               double* ssq = nullptr);
 cudaError_t launch_gram(const double* Xb, const Layout& L, double* Gband, cudaStream_t s);
 cudaError_t launch_cd(const CDParams& P, int num_ctas, cudaStream_t s);
 cudaError_t launch_csc_build(const int* nz_count, const int* nz_cur, const int* nz_rows,
@@ -261,6 +263,11 @@ cudaError_t launch_column_stats(const int32_t* iters, const int32_t* sweeps, con
 cudaError_t launch_zero_fill(double* a, size_t count, int sms, cudaStream_t s);
 cudaError_t launch_zero_fill_bulk(double* a, size_t count, int grid, cudaStream_t s);
 cudaError_t launch_csc_counts(const int* nz_count, int ncols, int32_t* out, cudaStream_t s);
+cudaError_t launch_assemble_lists(int64_t p, const int* nz_count, const int* nz_cur,
+                                  const int* nz_rows, const double* nz_vals, int nzcap,
+                                  const double* sigma_std, const double* scale, int symmetrize,
+                                  double* Theta, double* sigma_out, int64_t* nnz_total,
+                                  cudaStream_t s);
 cudaError_t launch_assemble(int64_t p, int64_t col_begin, int64_t col_end, const int64_t* col_ptr,
                             const int32_t* rows, const double* vals, const double* sigma_std,
                             const double* scale, int symmetrize, double* Theta, double* sigma_out,
