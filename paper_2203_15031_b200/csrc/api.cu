@@ -303,11 +303,8 @@ int run_tail(Workspace& W, const Layout& L, int64_t cb, double lambda0, double t
 // operands, written by the same kernel)
 int run_prep(Workspace& W, const double* dX, int64_t m, const spmesl_options& o, const Layout& L,
              cudaStream_t s, bool band = true, const S16Prep* y16 = nullptr) {
-  CUDA_TRY(cudaMemsetAsync(W.counters.ptr, 0, sizeof(DevCounters), s));
-  CUDA_TRY(cudaMemsetAsync((char*)W.counters.ptr + offsetof(DevCounters, bad_key), 0xff, 8, s));
-  CUDA_TRY(cudaMemsetAsync(W.queue.ptr, 0, 16, s));
-  CUDA_TRY(cudaMemsetAsync(W.nz_count.ptr, 0, sizeof(int) * (size_t)m, s));
-  CUDA_TRY(cudaMemsetAsync(W.nz_cur.ptr, 0, sizeof(int) * (size_t)m, s));
+  CUDA_TRY(launch_reset(W.counters.ptr, (int)sizeof(DevCounters), (int)offsetof(DevCounters, bad_key),
+                        (int*)W.queue.ptr, (int*)W.nz_count.ptr, (int*)W.nz_cur.ptr, m, s));
   CUDA_TRY(ev_record(W, W.ev[0], s));
   DevCounters* dc = (DevCounters*)W.counters.ptr;
   CUDA_TRY(launch_standardize(dX, L, o.standardize, (double*)W.xb.ptr, (double*)W.mean.ptr,
@@ -466,7 +463,7 @@ int initial_nzcap(int64_t n, int64_t p) {
 int device_stats(Workspace& W, const int32_t* dIters, const int32_t* dSweeps, const uint8_t* dConv,
                  int64_t m, cudaStream_t s) {
   DevCounters* dc = (DevCounters*)W.counters.ptr;
-  CUDA_TRY(cudaMemsetAsync(&dc->st_sweeps, 0, 24, s));
+  // (st_* start at zero: every fit resets the whole counter block in run_prep)
   CUDA_TRY(launch_column_stats(dIters, dSweeps, dConv, m, &dc->st_sweeps, &dc->st_max_sweeps,
                                &dc->st_max_outer, &dc->st_unconv, s));
   return SPMESL_OK;

@@ -400,6 +400,28 @@ __global__ void __launch_bounds__(32) zero_fill_bulk_kernel(double* __restrict__
   asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
+// Per-fit scratch reset in one launch (instead of five memsets): the counter block (zeros,
+// with the 8-byte bad-column key at key_off set to all ones), the 16-byte work queue and the
+// per-slot list counters nz_count / nz_cur.
+__global__ void reset_kernel(unsigned char* counters, int counters_bytes, int key_off, int* queue,
+                             int* nz_count, int* nz_cur, int64_t m) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = t; i < counters_bytes; i += stride)
+    counters[i] = (i >= key_off && i < key_off + 8) ? 0xff : 0;
+  if (t < 4) queue[t] = 0;
+  for (int64_t i = t; i < m; i += stride) { nz_count[i] = 0; nz_cur[i] = 0; }
+}
+
+cudaError_t launch_reset(void* counters, int counters_bytes, int key_off, int* queue, int* nz_count,
+                         int* nz_cur, int64_t m, cudaStream_t s) {
+  const int64_t work = std::max<int64_t>(m, counters_bytes);
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(296, (work + 255) / 256));
+  reset_kernel<<<blocks, 256, 0, s>>>((unsigned char*)counters, counters_bytes, key_off, queue,
+                                      nz_count, nz_cur, m);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_zero_fill_bulk(double* a, size_t count, int grid, cudaStream_t s) {
   if (count == 0) return cudaSuccess;
   if (((uintptr_t)a & 15) != 0 || (count & 1)) return cudaMemsetAsync(a, 0, count * 8, s);

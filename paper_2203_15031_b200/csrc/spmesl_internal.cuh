@@ -262,6 +262,8 @@ cudaError_t launch_column_stats(const int32_t* iters, const int32_t* sweeps, con
                                 int* nunc, cudaStream_t s);
 cudaError_t launch_zero_fill(double* a, size_t count, int sms, cudaStream_t s);
 cudaError_t launch_zero_fill_bulk(double* a, size_t count, int grid, cudaStream_t s);
+cudaError_t launch_reset(void* counters, int counters_bytes, int key_off, int* queue, int* nz_count,
+                         int* nz_cur, int64_t m, cudaStream_t s);
 cudaError_t launch_csc_counts(const int* nz_count, int ncols, int32_t* out, cudaStream_t s);
 cudaError_t launch_assemble_lists(int64_t p, const int* nz_count, const int* nz_cur,
                                   const int* nz_rows, const double* nz_vals, int nzcap,
