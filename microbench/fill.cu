@@ -57,6 +57,36 @@ __global__ void bulk_contig(double* a, size_t count) {
   }
   asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
+// S contiguous streams per CTA issued round-robin by ONE thread (as a producer warp would)
+template <int PIECE>
+__global__ void bulk_streams(double* a, size_t count, int S) {
+  extern __shared__ __align__(128) double zb[];
+  for (int e = threadIdx.x; e < PIECE; e += blockDim.x) zb[e] = 0.0;
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const uint32_t src = (uint32_t)__cvta_generic_to_shared(zb);
+  const size_t nstream = (size_t)gridDim.x * S;
+  size_t cur[16], end[16];
+  for (int u = 0; u < S; ++u) {
+    const size_t sid = (size_t)blockIdx.x * S + u;
+    cur[u] = (count * sid / nstream) & ~(size_t)1;
+    end[u] = (sid + 1 == nstream) ? count : ((count * (sid + 1) / nstream) & ~(size_t)1);
+  }
+  bool any = true;
+  while (any) {
+    any = false;
+    for (int u = 0; u < S; ++u) {
+      if (cur[u] >= end[u]) continue;
+      any = true;
+      const size_t cnt = (end[u] - cur[u]) < PIECE ? (end[u] - cur[u]) : PIECE;
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(a + cur[u]), "r"(src), "r"((uint32_t)(cnt * 8)) : "memory");
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      cur[u] += cnt;
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
 __global__ void st_contig(double* a, size_t count) {
   const size_t lo = (count * blockIdx.x / gridDim.x) & ~(size_t)3, hi = (blockIdx.x + 1 == gridDim.x) ? count : ((count * (blockIdx.x + 1) / gridDim.x) & ~(size_t)3);
   for (size_t i = lo + 4 * threadIdx.x; i < hi; i += 4 * blockDim.x)
@@ -90,6 +120,12 @@ int main() {
   for (int g : {1184, 2368}) {
     char nm[64]; snprintf(nm, 64, "st.cs v4.f64 grid %d x 512", g);
     timeit(nm, [&] { st_kernel_v8<<<g, 512>>>((double4*)a, count / 4); });
+  }
+  cudaFuncSetAttribute(bulk_streams<2048>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2048 * 8);
+  for (int S : {1, 2, 4, 8, 16}) {
+    char nm[64];
+    snprintf(nm, 64, "bulk 16K streams grid 148 S %d", S);
+    timeit(nm, [&] { bulk_streams<2048><<<148, 32, 2048 * 8>>>(a, count, S); });
   }
   cudaFuncSetAttribute(bulk_contig<2048>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2048 * 8);
   cudaFuncSetAttribute(bulk_contig<8192>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8);

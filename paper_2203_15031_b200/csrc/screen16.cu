@@ -42,7 +42,10 @@ constexpr int S16_THREADS = (S16_MMA_WARPS + 1) * 32;
 #define SPMESL_S16_NST 4
 #endif
 constexpr int S16_NST = SPMESL_S16_NST;     // ring stages (2 tiles = 32 KB each)
-constexpr int S16_ZPIECE = 2048;            // doubles per Theta zero-fill bulk store
+#ifndef SPMESL_S16_ZPIECE
+#define SPMESL_S16_ZPIECE 2048
+#endif
+constexpr int S16_ZPIECE = SPMESL_S16_ZPIECE;   // doubles per Theta zero-fill bulk store
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -293,7 +296,10 @@ constexpr int T5_EPI_WARPS = 8;
 constexpr int T5_THREADS = (2 + T5_EPI_WARPS) * 32;
 
 template <int BN>
-__host__ __device__ constexpr int t5_nst() { return BN == 256 ? 4 : 4; }
+#ifndef SPMESL_T5_NST
+#define SPMESL_T5_NST 4
+#endif
+__host__ __device__ constexpr int t5_nst() { return BN == 256 ? SPMESL_T5_NST : 4; }
 template <int BN>
 __host__ __device__ constexpr size_t t5_smem() {
   return 1024 + (size_t)t5_nst<BN>() * (1 + BN / 128) * S16_TILE_HALVES * 2 + (size_t)S16_ZPIECE * 8;
