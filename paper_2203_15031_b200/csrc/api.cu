@@ -86,6 +86,7 @@ struct Workspace {
   int device = -1;
   int sms = 0;
   int smem_optin = 0;
+  int smem_sm = 0;      // shared memory per SM (all resident CTAs)
   int cc_major = 0;
   Buffer xb, gband, mean, scale, counters, queue, sigma_std, iters, sweeps, conv, nz_count, nz_cur,
       nz_rows, nz_vals, col_ptr, csc_rows, csc_vals;
@@ -148,6 +149,7 @@ int ws_init(Workspace& W, int dev) {
   W.device = dev;
   W.sms = prop.multiProcessorCount;
   W.smem_optin = (int)prop.sharedMemPerBlockOptin;
+  W.smem_sm = (int)prop.sharedMemPerMultiprocessor;
   W.cc_major = prop.major;
   CUDA_TRY(cudaMallocHost((void**)&W.host_counters, sizeof(DevCounters)));
   CUDA_TRY(cudaMallocHost((void**)&W.lam_pinned, sizeof(double) * SPMESL_MAX_LAM));
@@ -218,11 +220,18 @@ struct FitOut {
 
 // Gram-column prefetch in the sweep kernel when two p-vectors fit in shared memory and the
 // columns are 16-byte aligned (p even); SPMESL_TAIL_NOPREFETCH=1 disables it (development).
+// Sweep-kernel launch shape: two column CTAs per SM whenever their state fits side by side
+// (their latency-bound search rounds and barriers interleave: config 4 band 3.1 -> 2.0 ms), else
+// one CTA per SM with the Gram columns of the current nonzeros prefetched into shared memory.
 void set_prefetch(const Workspace& W, TailParams& T) {
   static const bool off = getenv("SPMESL_TAIL_NOPREFETCH") && atoi(getenv("SPMESL_TAIL_NOPREFETCH"));
-  T.prefetch = !off && (T.p % 2 == 0) &&
-               tail_smem_bytes(T.p, T.n_pad, T.nzcap) + tail_prefetch_bytes(T.p) <=
-                   (size_t)W.smem_optin;
+  static const int occ_env = getenv("SPMESL_TAIL_OCC") ? atoi(getenv("SPMESL_TAIL_OCC")) : 0;
+  const size_t base = tail_smem_bytes(T.p, T.n_pad, T.nzcap);
+  const bool two = 2 * (base + 1024) <= (size_t)W.smem_sm;
+  T.occ = occ_env > 0 ? std::min(occ_env, 2) : (two ? 2 : 1);
+  if (T.occ == 2 && !two) T.occ = 1;
+  T.prefetch = T.occ == 1 && !off && (T.p % 2 == 0) &&
+               base + tail_prefetch_bytes(T.p) <= (size_t)W.smem_optin;
 }
 
 bool tail_enabled(const Workspace& W, const spmesl_options& o, const Layout& L, int nzcap) {

@@ -123,6 +123,7 @@ struct TailParams {
   int* sweeps_count;       // sweeps performed here
   int z_from_gtab;         // 1: z starts as Gtab[:, col] (Gram solver: b = 0, r = x~_c)
   int gtab_full;           // 1: every Gram column is present (no on-demand path)
+  int occ;                 // column CTAs per SM the launch provides for (grid multiplier)
   int prefetch;            // 1: stream the Gram columns of the current nonzeros into shared
                            //    memory ahead of their visits (needs tail_prefetch_bytes more)
   int* flags;

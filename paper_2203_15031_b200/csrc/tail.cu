@@ -374,7 +374,7 @@ __device__ void ensure_gram_column(const TailParams& P, int j, TailShared& TS, d
   bsync();
 }
 
-__global__ void __launch_bounds__(TAIL_THREADS, 1) tail_sweep_kernel(const TailParams P) {
+__global__ void __launch_bounds__(TAIL_THREADS, 2) tail_sweep_kernel(const TailParams P) {
   extern __shared__ __align__(128) unsigned char sm[];
   const int p = P.p, n = P.n, n_pad = P.n_pad, nchunk = P.nchunk, nzcap = P.nzcap;
   double* tx = (double*)sm;                                  // [J*XS]
@@ -654,6 +654,7 @@ cudaError_t launch_tail_mark(const TailState* tail, int M, const int* nz_rows, i
 cudaError_t launch_tail_sweeps(const TailParams& P, int grid, cudaStream_t s) {
   size_t smem = tail_smem_bytes(P.p, P.n_pad, P.nzcap);
   if (P.prefetch) smem += tail_prefetch_bytes(P.p);
+  if (P.occ > 1) grid *= P.occ;   // several column CTAs per SM (set_prefetch)
   cudaError_t e = cudaFuncSetAttribute(tail_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
