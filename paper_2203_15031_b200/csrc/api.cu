@@ -1167,7 +1167,6 @@ int fit_gram_columns_core(Workspace& W, const double* dX, int64_t n, int64_t p, 
   const bool cand = o.solver != 2;   // dHit: candidates of the certified screening (solver 0/3)
   set_layout(L, n, p);
   int nzcap = initial_nzcap(n, p);
-  std::vector<uint8_t> hh(m);
   for (int attempt = 0; attempt < 4; ++attempt) {
     int rc = alloc_core(W, L, m, nzcap);
     if (rc) return rc;
@@ -1179,16 +1178,11 @@ int fit_gram_columns_core(Workspace& W, const double* dX, int64_t n, int64_t p, 
     if ((rc = ensure(W.ssq, (size_t)p * 8))) return rc;
     DevCounters* dc = (DevCounters*)W.counters.ptr;
     if ((rc = run_prep(W, dX, m, o, L, s, /*band=*/false))) return rc;
-    CUDA_TRY(cudaMemcpyAsync(hh.data(), dHit + cb, (size_t)m, cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
-    std::vector<int> U;
-    for (int64_t c = 0; c < m; ++c)
-      if (hh[c]) U.push_back((int)(cb + c));
-    const int nU = (int)U.size();
-    std::vector<int> gstate(p, 0);
-    for (int j : U) gstate[j] = 2;
-    CUDA_TRY(cudaMemcpyAsync(W.umap.ptr, gstate.data(), (size_t)p * 4, cudaMemcpyHostToDevice, s));
-    if (nU) CUDA_TRY(cudaMemcpyAsync(W.uvars.ptr, U.data(), (size_t)nU * 4, cudaMemcpyHostToDevice, s));
+    // the flagged columns of this block: their Gram columns are computed up front (device-side
+    // list, no host round trip); any other column a sweep needs is computed on first use
+    DevCounters* dcs = (DevCounters*)W.counters.ptr;
+    CUDA_TRY(launch_cand_compact(dHit, (int)p, (int*)W.uvars.ptr, &dcs->s16_nU, (int*)W.umap.ptr,
+                                 s, (int)cb, (int)ce));
     const uint8_t* hit = dHit;
     if (cand) {
       // dHit holds candidates (certified screening): their exact Gram columns decide
@@ -1198,13 +1192,15 @@ int fit_gram_columns_core(Workspace& W, const double* dX, int64_t n, int64_t p, 
       CUDA_TRY(cudaMemcpyAsync(W.lam_dev.ptr, W.lam_pinned, 8, cudaMemcpyHostToDevice, s));
       CUDA_TRY(cudaMemsetAsync(W.hit.ptr, 0, (size_t)p, s));
       CUDA_TRY(launch_gram_cols((const double*)W.xb.ptr, (int)L.nblk, L.nchunk, (int)n, (int)p,
-                                (const int*)W.uvars.ptr, nU, nullptr, W.sms, (double*)W.ondemand.ptr,
-                                (uint8_t*)W.hit.ptr, (const double*)W.lam_dev.ptr, 1, nullptr, s));
+                                (const int*)W.uvars.ptr, 0, &dcs->s16_nU, W.sms,
+                                (double*)W.ondemand.ptr, (uint8_t*)W.hit.ptr,
+                                (const double*)W.lam_dev.ptr, 1, nullptr, s, /*fallback=*/false));
       hit = (const uint8_t*)W.hit.ptr;
     } else {
-      CUDA_TRY(launch_gram_pass((const double*)W.xb.ptr, (int)L.nblk, L.nchunk, (int)n, (int)p,
-                                nullptr, 0, (const int*)W.uvars.ptr, nU, nullptr,
-                                (double*)W.ondemand.ptr, s));
+      CUDA_TRY(launch_gram_cols((const double*)W.xb.ptr, (int)L.nblk, L.nchunk, (int)n, (int)p,
+                                (const int*)W.uvars.ptr, 0, &dcs->s16_nU, W.sms,
+                                (double*)W.ondemand.ptr, nullptr, nullptr, 0, nullptr, s,
+                                /*fallback=*/false));
     }
     CUDA_TRY(ev_record(W, W.ev[7], s));
     GramParams G{};
@@ -1258,7 +1254,7 @@ int fit_gram_columns_core(Workspace& W, const double* dX, int64_t n, int64_t p, 
       if (st) {
         st->solver = cand ? 3 : 2;
         st->kernel_launches += 4;
-        if (cand) st->screen_candidates = nU;
+        if (cand) st->screen_candidates = W.host_counters->s16_nU;
         st->ms_gram = ev_ms(W.ev[1], W.ev[7]);
         st->ms_tail = ev_ms(W.ev[5], W.ev[6]);
         st->tail_columns = W.host_counters->tail_count;

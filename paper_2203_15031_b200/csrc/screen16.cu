@@ -516,12 +516,13 @@ __global__ void __launch_bounds__(T5_THREADS, 1) screen16_tc_kernel(const Screen
 // Candidate list on the device (no host round trip): U[0..nU) = {c : cand[c]} in any order
 // (every consumer indexes its results by c), gstate[c] = 2 for candidates (their Gram column
 // will be present), 0 otherwise.
-__global__ void cand_compact_kernel(const uint8_t* __restrict__ cand, int p, int* __restrict__ U,
-                                    int* __restrict__ nU, int* __restrict__ gstate) {
+__global__ void cand_compact_kernel(const uint8_t* __restrict__ cand, int p, int cb, int ce,
+                                    int* __restrict__ U, int* __restrict__ nU,
+                                    int* __restrict__ gstate) {
   const int lane = threadIdx.x & 31;
   for (int base = blockIdx.x * blockDim.x; base < p; base += gridDim.x * blockDim.x) {
     const int c = base + threadIdx.x;
-    const bool f = c < p && cand[c];
+    const bool f = c >= cb && c < ce && cand[c];
     if (c < p) gstate[c] = f ? 2 : 0;
     const unsigned bal = __ballot_sync(0xffffffffu, f);
     int first = 0;
@@ -550,9 +551,10 @@ __global__ void sqrt_kernel(const double* __restrict__ in, double* __restrict__ 
 }  // namespace
 
 cudaError_t launch_cand_compact(const uint8_t* cand, int p, int* U, int* nU, int* gstate,
-                                cudaStream_t s) {
+                                cudaStream_t s, int cb, int ce) {
   const int blocks = std::max(1, std::min(296, (p + 255) / 256));
-  cand_compact_kernel<<<blocks, 256, 0, s>>>(cand, p, U, nU, gstate);
+  if (ce < 0) ce = p;
+  cand_compact_kernel<<<blocks, 256, 0, s>>>(cand, p, cb, ce, U, nU, gstate);
   return cudaGetLastError();
 }
 

@@ -186,8 +186,9 @@ double screen16_eps(int n_pad);
 cudaError_t launch_to_f16(const double* Xb, const double* nrm, int p, int n_pad, int nchunk32,
                           __half* Y16, cudaStream_t s);
 cudaError_t launch_screen16(const Screen16Params& P, int grid, cudaStream_t s);
+// candidates restricted to the columns [cb, ce) (ce < 0: all p); gstate[c] = 2 for those, else 0
 cudaError_t launch_cand_compact(const uint8_t* cand, int p, int* U, int* nU, int* gstate,
-                                cudaStream_t s);
+                                cudaStream_t s, int cb = 0, int ce = -1);
 cudaError_t launch_sqrt(const double* in, double* out, float* inv_sq, float* lam_n,
                         double lambda0, int n, int p, int p_pad, cudaStream_t s);
 cudaError_t launch_syrk_screen(const GramParams& P, int grid, cudaStream_t s);
@@ -207,7 +208,8 @@ cudaError_t launch_tail_residuals(const double* Xb, const TailState* tail, int M
 // device count and 2 nU > p the kernel only sets gstate[:] = 2 — the full Gram kernel decides)
 cudaError_t launch_gram_cols(const double* Xb, int nblk, int nchunk, int n, int p, const int* U,
                              int nU, const int* nU_dev, int sms, double* Gtab, uint8_t* hit,
-                             const double* lams, int nlam, int* gstate, cudaStream_t s);
+                             const double* lams, int nlam, int* gstate, cudaStream_t s,
+                             bool fallback = true);
 // hit (optional): hit[l p + c] = 1 for every candidate c = U[.] with some |G_jc| > lams[l], j != c
 // (hit must be zeroed first; only ones are written)
 cudaError_t launch_gram_pass(const double* Xb, int nblk, int nchunk, int n, int p, const double* V,

@@ -213,7 +213,8 @@ __global__ void __launch_bounds__(GC_MAXW * 32, 1) gram_cols_kernel(const double
                                                                  double* __restrict__ Gtab,
                                                                  uint8_t* __restrict__ hit,
                                                                  const double* __restrict__ lams,
-                                                                 int nlam, int* __restrict__ gstate) {
+                                                                 int nlam, int* __restrict__ gstate,
+                                                                 int fallback) {
   extern __shared__ __align__(128) double gsm[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nthr = blockDim.x;
   const int T = nthr >> 5;
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(GC_MAXW * 32, 1) gram_cols_kernel(const double
   const int m0 = (int)((int64_t)blockIdx.x * nmt / gridDim.x);
   const int m1 = (int)((int64_t)(blockIdx.x + 1) * nmt / gridDim.x);
   const int nU = nU_dev ? *(volatile const int*)nU_dev : nU_host;
-  if (nU_dev && 2 * (int64_t)nU > p) {
+  if (nU_dev && fallback && 2 * (int64_t)nU > p) {
     if (gstate)
       for (int r = m0 * 8 + tid; r < min(p, m1 * 8); r += nthr) gstate[r] = 2;
     return;
@@ -596,7 +597,8 @@ cudaError_t launch_tail_residuals(const double* Xb, const TailState* tail, int M
 
 cudaError_t launch_gram_cols(const double* Xb, int nblk, int nchunk, int n, int p, const int* U,
                              int nU, const int* nU_dev, int sms, double* Gtab, uint8_t* hit,
-                             const double* lams, int nlam, int* gstate, cudaStream_t s) {
+                             const double* lams, int nlam, int* gstate, cudaStream_t s,
+                             bool fallback) {
   if (!nU_dev && nU <= 0) return cudaSuccess;
   if (sms <= 0) {
     int dev = 0;
@@ -624,7 +626,7 @@ cudaError_t launch_gram_cols(const double* Xb, int nblk, int nchunk, int n, int 
     attr = true;
   }
   gram_cols_kernel<<<grid, T * 32, smem, s>>>(Xb, nchunk, n, p, U, nU, nU_dev, Gtab, hit, lams,
-                                             nlam, gstate);
+                                             nlam, gstate, fallback ? 1 : 0);
   return cudaGetLastError();
 }
 
