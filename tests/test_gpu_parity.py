@@ -7,6 +7,7 @@ import pytest
 
 from synth import generators as G
 from tests.parity import assert_parity, compare
+from tests.conftest import ROOT
 
 pytestmark = pytest.mark.gpu
 
@@ -456,3 +457,39 @@ def test_graph_replay_matches_eager(S, oracle):
     assert r.stats["graph_replay"] == 1
     e = S.fit_device(Xd, lam, out=outs(), eager=True)
     assert torch.equal(r.Theta, e.Theta) and torch.equal(r.sweeps, e.sweeps)
+
+
+@pytest.mark.parametrize("env", [{"SPMESL_S16_MMA_SYNC": "1"}, {"SPMESL_S16_BN": "128"},
+                                 {"SPMESL_S16_ZFRAC": "0.4"}, {"SPMESL_NO_GRAPH": "1"}])
+def test_screening_variants_identical(S, oracle, env, tmp_path):
+    """The alternative screening kernels (mma.sync; 128 x 128 tcgen05 tiles), the split Theta
+    zero fill and the eager (no-graph) path give the default fit bit for bit (each runs in a
+    fresh process: the switches are read once)."""
+    import subprocess, sys, os, torch
+    X, _, _ = G.make_config(5, p=4000)
+    n, p = X.shape
+    lam = oracle.lambda_ub(n, p)
+    np.save(tmp_path / "X.npy", X)
+    code = f"""
+import numpy as np, torch, sys
+sys.path.insert(0, {ROOT!r})
+import paper_2203_15031_b200 as S
+X = np.load({str(tmp_path / 'X.npy')!r})
+Xd = torch.from_numpy(np.ascontiguousarray(X.T)).cuda().t()
+out = dict(theta=torch.empty(({p}, {p}), dtype=torch.float64, device="cuda"),
+           sigma=torch.empty({p}, dtype=torch.float64, device="cuda"),
+           iters=torch.empty({p}, dtype=torch.int32, device="cuda"),
+           sweeps=torch.empty({p}, dtype=torch.int32, device="cuda"),
+           conv=torch.empty({p}, dtype=torch.uint8, device="cuda"))
+for _ in range(3):
+    r = S.fit_device(Xd, {lam!r}, out=out)
+np.save({str(tmp_path / 'T.npy')!r}, r.Theta.cpu().numpy())
+np.save({str(tmp_path / 'sw.npy')!r}, r.sweeps.cpu().numpy())
+"""
+    e = dict(os.environ)
+    e.update(env)
+    subprocess.run([sys.executable, "-c", code], check=True, env=e, timeout=600)
+    Xd = torch.from_numpy(np.ascontiguousarray(X.T)).cuda().t()
+    ref = S.fit_device(Xd, lam, eager=True)
+    assert np.array_equal(np.load(tmp_path / "T.npy"), ref.Theta.cpu().numpy())
+    assert np.array_equal(np.load(tmp_path / "sw.npy"), ref.sweeps.cpu().numpy())
