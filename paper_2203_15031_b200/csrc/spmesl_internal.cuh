@@ -197,7 +197,10 @@ cudaError_t launch_level_flags(const GramParams& P, cudaStream_t s);
 int gram_tile_count(int64_t p);
 
 constexpr int TAIL_THREADS = 256;
-constexpr int TAIL_SCAN = 4 * TAIL_THREADS;   // rows tested per search round
+#ifndef SPMESL_TAIL_SCAN_R
+#define SPMESL_TAIL_SCAN_R 4
+#endif
+constexpr int TAIL_SCAN = SPMESL_TAIL_SCAN_R * TAIL_THREADS;   // rows tested per search round
 constexpr int TAIL_ODC = 8;          // on-demand Gram column cache entries per CTA
 __host__ __device__ size_t tail_smem_bytes(int p, int n_pad, int nzcap);
 size_t tail_prefetch_bytes(int p);

@@ -331,7 +331,7 @@ __global__ void tail_mark_kernel(const TailState* __restrict__ tail, int M, cons
 struct TailShared {
   uint64_t pf_bar[2];    // prefetch buffers' mbarriers
   double red[TAIL_THREADS / 32];
-  int wmin[TAIL_THREADS / 32];
+  int wmin[2][TAIL_THREADS / 32];   // per-warp first hits, double-buffered across rounds
   int oc_var[TAIL_ODC];
   int oc_next;
   int k;
@@ -438,7 +438,21 @@ __global__ void __launch_bounds__(TAIL_THREADS, 2) tail_sweep_kernel(const TailP
     if (P.z_from_gtab) {
       ensure_gram_column(P, gc, TS, tx, tvv);
       const double* gz = P.Gtab + (size_t)gc * p;
-      for (int j = tid; j < p; j += TAIL_THREADS) z[j] = __ldcs(gz + j);
+      // (16 independent L2 loads in flight per thread: the column is 8p bytes)
+      constexpr int UB = 16;
+      for (int j0 = 0; j0 < p; j0 += UB * TAIL_THREADS) {
+        double gv[UB];
+#pragma unroll
+        for (int u = 0; u < UB; ++u) {
+          const int j = j0 + u * TAIL_THREADS + tid;
+          gv[u] = j < p ? __ldcs(gz + j) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < UB; ++u) {
+          const int j = j0 + u * TAIL_THREADS + tid;
+          if (j < p) z[j] = gv[u];
+        }
+      }
     } else {
       for (int j = tid; j < p; j += TAIL_THREADS) z[j] = P.Zz[(size_t)k * p + j];
     }
@@ -460,23 +474,26 @@ __global__ void __launch_bounds__(TAIL_THREADS, 2) tail_sweep_kernel(const TailP
       for (;;) {
         const int na = cursor < ocnt ? orow[cursor] : p;     // next row with b_j != 0
         // first row in [pos, na) with |z_j| > lambda (j != this column)
-        // (rounds of TAIL_SCAN rows: thread t tests rows base + t + TAIL_THREADS r, r < 4;
-        // the first hit is the block-wide minimum of the hit rows)
+        // (rounds of TAIL_SCAN rows: thread t tests rows base + t + TAIL_THREADS r,
+        // r < TAIL_SCAN / TAIL_THREADS; the first hit is the block-wide minimum of the hit rows;
+        // one barrier per round: the per-warp minima alternate between two buffers, and a
+        // buffer is rewritten only after the next round's barrier, which every reader of it
+        // has passed)
         int j = na;
-        for (int base = pos; base < na; base += TAIL_SCAN) {
+        int rbuf = 0;
+        for (int base = pos; base < na; base += TAIL_SCAN, rbuf ^= 1) {
           int my = 0x7fffffff;
 #pragma unroll
-          for (int r = 3; r >= 0; --r) {
+          for (int r = TAIL_SCAN / TAIL_THREADS - 1; r >= 0; --r) {
             const int jj = base + tid + r * TAIL_THREADS;
             if (jj < na && jj != gc && fabs(z[jj]) > lam) my = jj;
           }
           my = __reduce_min_sync(0xffffffffu, my);
-          if (lane == 0) TS.wmin[warp] = my;
+          if (lane == 0) TS.wmin[rbuf][warp] = my;
           bsync();
           int best = 0x7fffffff;
 #pragma unroll
-          for (int w = 0; w < TAIL_THREADS / 32; ++w) best = min(best, TS.wmin[w]);
-          bsync();
+          for (int w = 0; w < TAIL_THREADS / 32; ++w) best = min(best, TS.wmin[rbuf][w]);
           if (best != 0x7fffffff) { j = best; break; }
         }
         if (j >= p) break;
@@ -543,14 +560,16 @@ __global__ void __launch_bounds__(TAIL_THREADS, 2) tail_sweep_kernel(const TailP
       bsync();
       if (maxd < P.tol || inner >= P.max_inner) {
         if (!(maxd < P.tol)) flags |= 2;
-        // fresh residual and sigma (reading g4), warp 0 in the CD kernel's order
+        // fresh residual and sigma (reading g4): every thread builds its samples'
+        // r_i = x~_ci - sum_m x~_{j_m i} b_m (m ascending, the CD kernel's per-element order),
+        // then warp 0 sums r_i^2 in the CD kernel's order
+        for (int i = tid; i < n_pad; i += TAIL_THREADS) {
+          double ri = P.Xb[xb_index(i, gc, nchunk)];
+          for (int m = 0; m < ocnt; ++m) ri = fma(-P.Xb[xb_index(i, orow[m], nchunk)], ov[m], ri);
+          r[i] = ri;
+        }
+        bsync();
         if (warp == 0) {
-          for (int i = lane; i < n_pad; i += 32) r[i] = P.Xb[xb_index(i, gc, nchunk)];
-          for (int m = 0; m < ocnt; ++m) {
-            const int jj = orow[m];
-            const double bj = ov[m];
-            for (int i = lane; i < n_pad; i += 32) r[i] = fma(-P.Xb[xb_index(i, jj, nchunk)], bj, r[i]);
-          }
           double ss = 0.0;
           for (int i = lane; i < n; i += 32) ss = fma(r[i], r[i], ss);
 #pragma unroll
