@@ -277,13 +277,8 @@ cudaError_t launch_csc_build(const int* nz_count, const int* nz_cur, const int* 
                              const double* nz_vals, int ncols, int nzcap, int64_t* col_ptr,
                              int32_t* rows, double* vals, int64_t* total, cudaStream_t s) {
   const bool staged = (size_t)ncols * 4 <= 160 * 1024;
-  if (staged) {
-    static int attr = 0;
-    if (!attr) {
-      cudaFuncSetAttribute(csc_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      attr = 1;
-    }
-  }
+  if (staged)   // (per call: the attribute belongs to the current device)
+    cudaFuncSetAttribute(csc_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
   csc_scan_kernel<<<1, 1024, staged ? (size_t)ncols * 4 : 0, s>>>(nz_count, ncols, col_ptr, total,
                                                                  staged ? 1 : 0);
   const int wpb = 8;
@@ -434,12 +429,9 @@ cudaError_t launch_zero_fill(double* a, size_t count, int sms, cudaStream_t s) {
   if (((uintptr_t)a & 15) != 0 || (count & 1)) return cudaMemsetAsync(a, 0, count * 8, s);
   // same shared-memory carve-out as the solver kernels, so an SM running this kernel can take a
   // solver CTA without being reconfigured (which would serialize the two)
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(zero_fill_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         (int)cudaSharedmemCarveoutMaxShared);
-    attr = true;
-  }
+  cudaFuncSetAttribute(zero_fill_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       (int)cudaSharedmemCarveoutMaxShared);
+
   zero_fill_kernel<<<sms, 256, 0, s>>>((double2*)a, count / 2);
   return cudaGetLastError();
 }

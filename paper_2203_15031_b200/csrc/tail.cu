@@ -637,12 +637,10 @@ cudaError_t launch_gram_cols(const double* Xb, int nblk, int nchunk, int n, int 
   const int T = std::max(1, std::min(max_warps, (nmt + sms - 1) / sms));
   const int grid = std::max(1, std::min(sms, (nmt + T - 1) / T));
   const size_t smem = (size_t)GC_STAGES * (T * 8 * XS + GC_NTMAX * 8 * XS) * 8;
-  static bool attr = false;
-  if (!attr) {
+  {   // (per call: the attribute belongs to the current device)
     cudaError_t e = cudaFuncSetAttribute(gram_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)((size_t)GC_STAGES * (GC_MAXW * 8 * XS + GC_NTMAX * 8 * XS) * 8));
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   gram_cols_kernel<<<grid, T * 32, smem, s>>>(Xb, nchunk, n, p, U, nU, nU_dev, Gtab, hit, lams,
                                              nlam, gstate, fallback ? 1 : 0);
