@@ -115,6 +115,8 @@ struct Workspace {
   std::vector<unsigned char> gkey;        // arguments of the captured graph
   std::vector<unsigned char> last_key;    // arguments of the previous eager device-path fit
   int graph_nzcap = 0;                    // coefficient-list capacity the graph was built for
+  int64_t graph_screen_fill = 0;          // host-side facts of the captured fit (for its stats)
+  int graph_launches = 0;
   bool zero_join = false;     // part of Theta's zero fill runs on `side` (join ev_join)
   int64_t screen_fill = 0;    // doubles of Theta the screening kernel zero-filled (last fit)
   int gram_launches = 0;      // kernels fit_gram_enqueue launched (last fit)
@@ -1025,6 +1027,8 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
       if (use_graph && W.gexec && key == W.gkey) {
         // replay: one launch for the whole fit (the penalty level is re-staged first)
         W.lam_pinned[0] = lambda0;
+        W.screen_fill = W.graph_screen_fill;
+        W.gram_launches = W.graph_launches;
         CUDA_TRY(cudaGraphLaunch(W.gexec, s));
         launched = true;
       } else if (use_graph && key == W.last_key) {
@@ -1044,6 +1048,8 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
               cudaGraphInstantiate(&W.gexec, g, 0) == cudaSuccess) {
             W.gkey = key;
             W.graph_nzcap = nzcap;
+            W.graph_screen_fill = W.screen_fill;
+            W.graph_launches = W.gram_launches;
           } else {
             W.gexec = nullptr;
           }
