@@ -1019,7 +1019,12 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
     const bool use_graph = !no_graph && !o.eager && getenv("SPMESL_DEV_SIDE_ZERO") == nullptr &&
                            getenv("SPMESL_S16_ZFRAC") == nullptr && o.solver != 2 &&
                            (((uintptr_t)dTheta & 15) == 0) && (((size_t)p * (size_t)p) & 1) == 0;
-    nzcap = (W.graph_nzcap > 0 && !W.gkey.empty()) ? W.graph_nzcap : initial_nzcap(n, p);
+    // the captured fit's list capacity if these are its arguments, else the initial one
+    nzcap = initial_nzcap(n, p);
+    if (W.gexec && W.graph_nzcap > 0 &&
+        graph_key(dX, n, p, lambda0, tol, max_iter, o, dTheta, dSigma, dIters, dSweeps, dConv,
+                  W.graph_nzcap, s) == W.gkey)
+      nzcap = W.graph_nzcap;
     for (int attempt = 0; attempt < 4; ++attempt) {
       std::vector<unsigned char> key = graph_key(dX, n, p, lambda0, tol, max_iter, o, dTheta,
                                                  dSigma, dIters, dSweeps, dConv, nzcap, s);
