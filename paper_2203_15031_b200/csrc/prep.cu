@@ -13,6 +13,7 @@
 //   rows j' of blocks b-1 and b, which let the CD kernel process Proposition 2's row order
 //    32 rows at a time with a lag-1 pipeline.  2 p 32 n FMAs, tiny.
 #include <algorithm>
+#include <cstdlib>
 #include "spmesl_internal.cuh"
 
 namespace spmesl {
@@ -33,7 +34,9 @@ __device__ __forceinline__ size_t y16_index(int64_t k, int64_t i, int nchunk64) 
 __global__ void standardize_kernel(const double* __restrict__ X, int64_t n, int64_t p, int nchunk,
                                    int64_t nrows, int standardize, double* __restrict__ Xb,
                                    double* mu, double* scale, int* err, unsigned long long* bad_key,
-                                   double* nrm, S16Prep y, double* ssq) {
+                                   double* nrm, S16Prep y, double* ssq, int stage_n) {
+  extern __shared__ __align__(16) double colbuf[];   // [warps][stage_n] (stage_n > 0)
+  __shared__ __align__(8) uint64_t colbar[8];
   const int lane = threadIdx.x & 31;
   const int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int64_t n_pad = (int64_t)nchunk * KC;
@@ -50,6 +53,32 @@ __global__ void standardize_kernel(const double* __restrict__ X, int64_t n, int6
     return;
   }
   const double* x = X + k * n;
+  if (stage_n > 0) {
+    // the whole column in one bulk copy (all of its bytes in flight at once; the passes below
+    // then read shared memory)
+    const int w = threadIdx.x >> 5;
+    double* buf = colbuf + (size_t)w * stage_n;
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&colbar[w]);
+    if (lane == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar));
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar),
+                   "r"((uint32_t)(n * 8))
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+              (uint32_t)__cvta_generic_to_shared(buf)),
+          "l"(x), "r"((uint32_t)(n * 8)), "r"(bar)
+          : "memory");
+    }
+    __syncwarp();
+    asm volatile(
+        "{\n.reg .pred P1;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
+        "@!P1 bra WAIT_%=;\n}\n" ::"r"(bar)
+        : "memory");
+    x = buf;
+  }
   double sum = 0.0, mx = 0.0;
   bool finite = true;
   for (int64_t i = lane; i < n; i += 32) {
@@ -179,8 +208,15 @@ cudaError_t launch_standardize(const double* X, const Layout& L, int standardize
   const int64_t nrows = L.nblk * J;                 // Xb rows incl. padding
   const int64_t cols = std::max<int64_t>(nrows, yy.Y16 ? yy.p_pad : 0);
   dim3 grid((unsigned)((cols + wpb - 1) / wpb));
-  standardize_kernel<<<grid, wpb * 32, 0, s>>>(X, L.n, L.p, L.nchunk, nrows, standardize, Xb, mu,
-                                               scale, err, bad_key, nrm, yy, ssq);
+  // stage each column in shared memory by one bulk copy when it is 16-byte aligned and small
+  static const bool no_stage = getenv("SPMESL_DEV_STD_NOSTAGE") != nullptr;   // (dev)
+  const int stage_n = (!no_stage && L.n % 2 == 0 && ((uintptr_t)X & 15) == 0 && L.n <= 1024)
+                          ? (int)L.n : 0;
+  const size_t smem = (size_t)wpb * stage_n * 8;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(standardize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  standardize_kernel<<<grid, wpb * 32, smem, s>>>(X, L.n, L.p, L.nchunk, nrows, standardize, Xb,
+                                                  mu, scale, err, bad_key, nrm, yy, ssq, stage_n);
   return cudaGetLastError();
 }
 
