@@ -330,6 +330,7 @@ __global__ void tail_mark_kernel(const TailState* __restrict__ tail, int M, cons
 // ------------------------------------------------------------------ per-column sweeps
 struct TailShared {
   uint64_t pf_bar[2];    // prefetch buffers' mbarriers
+  uint64_t z_bar;        // z <- G[:, c] bulk copy
   double red[TAIL_THREADS / 32];
   int wmin[2][TAIL_THREADS / 32];   // per-warp first hits, double-buffered across rounds
   int oc_var[TAIL_ODC];
@@ -403,9 +404,11 @@ __global__ void __launch_bounds__(TAIL_THREADS, 2) tail_sweep_kernel(const TailP
     if (pf) {
       mbar_init_t(&TS.pf_bar[0], 1);
       mbar_init_t(&TS.pf_bar[1], 1);
-      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
+    mbar_init_t(&TS.z_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  uint32_t z_ph = 0;
   // (one thread) start loading the Gram column of old-list entry c into buffer c & 1
   auto pf_issue = [&](int c, int cnt) {
     if (c < cnt) {
@@ -438,9 +441,17 @@ __global__ void __launch_bounds__(TAIL_THREADS, 2) tail_sweep_kernel(const TailP
     if (P.z_from_gtab) {
       ensure_gram_column(P, gc, TS, tx, tvv);
       const double* gz = P.Gtab + (size_t)gc * p;
+      if ((p & 1) == 0) {   // the whole column in one bulk copy (8p bytes, 16-byte multiple)
+        if (tid == 0) {
+          prefetch_col(z, gz, (uint32_t)p * 8, &TS.z_bar);
+          mbar_wait_t(&TS.z_bar, z_ph);
+        }
+        z_ph ^= 1u;
+        bsync();
+      } else
       // (16 independent L2 loads in flight per thread: the column is 8p bytes)
-      constexpr int UB = 16;
-      for (int j0 = 0; j0 < p; j0 += UB * TAIL_THREADS) {
+      for (int j0 = 0; j0 < p; j0 += 16 * TAIL_THREADS) {
+        constexpr int UB = 16;
         double gv[UB];
 #pragma unroll
         for (int u = 0; u < UB; ++u) {
