@@ -55,6 +55,7 @@ struct DevCounters {
   unsigned long long st_sweeps;    // column statistics (column_stats_kernel)
   int st_max_sweeps, st_max_outer, st_unconv, pad4;
   int s16_nU, pad5;                // solver 3: candidate columns of the certified screening
+  int joint_nslots, joint_nwork;   // mode 1 on the Gram form: sweep slots, slots this sweep
 };
 
 struct Buffer {
@@ -92,6 +93,7 @@ struct Workspace {
       nz_rows, nz_vals, col_ptr, csc_rows, csc_vals;
   Buffer tail, umark, umap, uvars, tailV, zall, ondemand;   // tail solver
   Buffer ej, act0, act1, keep, jflags;                      // mode 1 (Algorithm 3)
+  Buffer jtail, slotmap, jwork, zj;                         // mode 1 on the Gram form
   Buffer hit;                                               // Gram solver screening flags
   Buffer lam_dev;                                           // multi-lambda: penalty levels
   Buffer nrm, sq, y16, cand;                                // certified f16 screening
@@ -596,7 +598,7 @@ int fit_joint_core(Workspace& W, const double* dX, int64_t n, int64_t p, int64_t
     }
     if (!overflow) {
       CUDA_TRY(ev_record(W, W.ev[2], s));
-      if (st) { st->tile_cols = T0; st->num_ctas = ctas0; st->kernel_launches += launches; }
+      if (st) { st->solver = 1; st->tile_cols = T0; st->num_ctas = ctas0; st->kernel_launches += launches; }
       *nzcap_used = nzcap;
       return SPMESL_OK;
     }
@@ -632,7 +634,7 @@ bool gram_applicable(const Workspace& W, const spmesl_options& o, int64_t n, int
 int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, double lambda0,
                      double tol, int32_t max_iter, const spmesl_options& o, const FitOut& out,
                      cudaStream_t s, Layout& L, int nzcap, const double* lams = nullptr,
-                     int nlam = 1, bool screen16 = false) {
+                     int nlam = 1, bool screen16 = false, bool screen_only = false) {
   // nlam > 1: several penalty levels share X~, S and its screening pass (regularization path);
   // the outputs of level l, column c sit at l p + c
   const int64_t m = p;
@@ -789,6 +791,9 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
     if (nlam > 1) CUDA_TRY(launch_level_flags(G, s));
     launches += 1 + (nlam > 1);
   }
+  // (mode 1 on the Gram form continues from here with its own sweep loop: W.hit holds the
+  // exact first-sweep decisions, W.ondemand the Gram columns of the hit columns)
+  if (screen_only) { W.gram_launches = launches; return SPMESL_OK; }
   CUDA_TRY(launch_gram_init(G, s));
   CUDA_TRY(ev_record(W, W.ev[5], s));
   // the sweep kernel reads the number of columns with hits from the device counter (no host
@@ -867,15 +872,192 @@ int fit_gram_core(Workspace& W, const double* dX, int64_t n, int64_t p, double l
   return fail(SPMESL_ERR_OOM, "coefficient list overflow");
 }
 
+// Algorithm 3 (mode 1) on the Gram form: the first joint sweep of every
+// column is the screening pass (solver 3's certified f16 screening or solver 2's FP64 Gram
+// kernel, with the exact decisions); only the columns with a hit get a sweep slot, whose z is
+// carried between the joint sweeps, each joint sweep being one launch of the sweep kernel over
+// the active slots with max |db| reduced on the device.  The others are exact no-ops
+// (b = 0 and every |z_j| <= lambda) until their sigma refit; an active column without a slot
+// after a refit (sigma moved: lambda changed) gets one.  The outer boundary is the residual
+// path's: fresh residual, sigma, F_c, in-order compaction (joint.cu).  One host synchronisation
+// per joint sweep, as in the residual path.
+int fit_joint_gram_core(Workspace& W, const double* dX, int64_t n, int64_t p, double lambda0,
+                        double tol, int32_t max_iter, const spmesl_options& o, const FitOut& out,
+                        cudaStream_t s, spmesl_stats* st, Layout& L, int* nzcap_used) {
+  const int64_t m = p;
+  const bool s16 = o.solver != 2;
+  int nzcap = initial_nzcap(n, p);
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    int rc = fit_gram_enqueue(W, dX, n, p, lambda0, tol, max_iter, o, out, s, L, nzcap, nullptr, 1,
+                              s16, /*screen_only=*/true);
+    if (rc) return rc;
+    int launches = W.gram_launches + 1;
+    const int full = W.screen_fill ? 0 : 0;
+    (void)full;
+    if ((rc = ensure(W.ej, (size_t)m * L.n_pad * 8))) return rc;
+    if ((rc = ensure(W.act0, (size_t)m * 4))) return rc;
+    if ((rc = ensure(W.act1, (size_t)m * 4))) return rc;
+    if ((rc = ensure(W.keep, (size_t)m))) return rc;
+    if ((rc = ensure(W.jflags, (size_t)m))) return rc;
+    if ((rc = ensure(W.jtail, (size_t)m * sizeof(TailState)))) return rc;
+    if ((rc = ensure(W.slotmap, (size_t)m * 4))) return rc;
+    if ((rc = ensure(W.jwork, (size_t)m * 4))) return rc;
+    DevCounters* dc = (DevCounters*)W.counters.ptr;
+    CUDA_TRY(launch_joint_live_init((const uint8_t*)W.hit.ptr, (int)m, &dc->joint_nslots,
+                                    (TailState*)W.jtail.ptr, (int*)W.slotmap.ptr, s));
+    CUDA_TRY(cudaMemsetAsync(out.iters, 0, 4 * (size_t)m, s));
+    CUDA_TRY(cudaMemsetAsync(out.sweeps, 0, 4 * (size_t)m, s));
+    CUDA_TRY(cudaMemsetAsync(out.conv, 0, (size_t)m, s));
+    CUDA_TRY(cudaMemsetAsync(W.jflags.ptr, 0, (size_t)m, s));
+    CUDA_TRY(launch_joint_init((const double*)W.xb.ptr, 0, (int)m, L.n_pad, L.nchunk,
+                               (int*)W.act0.ptr, out.sigma_std, (double*)W.ej.ptr, s));
+    launches += 2;
+    if ((rc = read_counters(W, s))) return rc;
+    if (W.host_counters->err) return std_error(W, st);
+    int nslots = W.host_counters->joint_nslots;
+    if ((rc = ensure(W.zj, (size_t)std::max(nslots, 1) * (size_t)p * 8))) return rc;
+    size_t zcap = W.zj.bytes / ((size_t)p * 8);
+    int* act = (int*)W.act0.ptr;
+    int* act_next = (int*)W.act1.ptr;
+    int nact = (int)m;
+    bool overflow = false;
+    int64_t joint_sweeps = 0;
+    for (int r = 0; r < max_iter && nact > 0 && !overflow; ++r) {
+      if (r > 0) {
+        // active columns without a slot (their sigma moved, so lambda did): give them one
+        CUDA_TRY(cudaMemsetAsync(&dc->joint_nwork, 0, 4, s));
+        CUDA_TRY(launch_joint_count_unslotted(act, nact, (const int*)W.slotmap.ptr,
+                                              &dc->joint_nwork, s));
+        if ((rc = read_counters(W, s))) return rc;
+        const int need = W.host_counters->joint_nwork;
+        ++launches;
+      if (need > 0) {
+        const int before = nslots;
+        if ((size_t)(nslots + need) > zcap) {   // grow z storage, keeping the slots' contents
+          Buffer nb;
+          const size_t ncap = std::max((size_t)nslots + (size_t)need, 2 * zcap);
+          if ((rc = ensure(nb, ncap * (size_t)p * 8))) return rc;
+          if (nslots) CUDA_TRY(cudaMemcpyAsync(nb.ptr, W.zj.ptr, (size_t)nslots * p * 8,
+                                               cudaMemcpyDeviceToDevice, s));
+          CUDA_TRY(cudaStreamSynchronize(s));
+          cudaFree(W.zj.ptr);
+          W.zj = nb;
+          zcap = ncap;
+        }
+        CUDA_TRY(launch_joint_live_add(act, nact, (int*)W.slotmap.ptr, (TailState*)W.jtail.ptr,
+                                       &dc->joint_nslots, (const int*)W.nz_cur.ptr, s));
+        if ((rc = read_counters(W, s))) return rc;
+        nslots = W.host_counters->joint_nslots;
+        (void)before;
+        ++launches;
+      }
+      }
+      int inner = 0;
+      double jm = 0.0;
+      // the slots of this outer iteration's active set (fixed during its sweeps)
+      CUDA_TRY(cudaMemsetAsync(&dc->joint_nwork, 0, 4, s));
+      CUDA_TRY(launch_joint_work(act, nact, (const int*)W.slotmap.ptr, (int*)W.jwork.ptr,
+                                 &dc->joint_nwork, s));
+      ++launches;
+      do {
+        CUDA_TRY(cudaMemsetAsync(&dc->joint_maxd, 0, 8, s));
+        CUDA_TRY(cudaMemsetAsync(&dc->tail_next, 0, 4, s));
+        TailParams T{};
+        T.Xb = (const double*)W.xb.ptr;
+        T.n = (int)n; T.n_pad = L.n_pad; T.nchunk = L.nchunk; T.p = (int)p; T.nblk = (int)L.nblk;
+        T.col_begin = 0;
+        T.lambda0 = lambda0; T.tol = tol; T.sigma_floor = o.sigma_floor;
+        T.sqrt_n = std::sqrt((double)n);
+        T.max_outer = max_iter; T.max_inner = o.max_inner;
+        T.nzcap = nzcap;
+        T.M = 0;
+        T.M_dev = &dc->joint_nwork;
+        T.Gtab = (double*)W.ondemand.ptr;
+        T.gstate = s16 ? (int*)W.umap.ptr : nullptr;
+        T.z_from_gtab = 1;
+        T.gtab_full = s16 ? 0 : 1;
+        T.next = &dc->tail_next;
+        T.ondemand_count = &dc->gram_ondemand;
+        T.sweeps_count = &dc->tail_sweeps;
+        T.flags = &dc->err;
+        T.nz_rows = (int*)W.nz_rows.ptr; T.nz_vals = (double*)W.nz_vals.ptr;
+        T.nz_count = (int*)W.nz_count.ptr; T.nz_cur = (int*)W.nz_cur.ptr;
+        T.sigma_std = out.sigma_std; T.iters = out.iters; T.sweeps = out.sweeps;
+        T.converged = out.conv;
+        T.joint = 1;
+        T.jtail = (TailState*)W.jtail.ptr;
+        T.work = (const int*)W.jwork.ptr;
+        T.Zj = (double*)W.zj.ptr;
+        T.joint_maxd = &dc->joint_maxd;
+        set_prefetch(W, T);
+        CUDA_TRY(launch_tail_sweeps(T, (int)std::max(1, std::min(W.sms, nslots)), s));
+        ++launches;
+        ++joint_sweeps;
+        if ((rc = read_counters(W, s))) return rc;
+        if (W.host_counters->err) return std_error(W, st);
+        if (W.host_counters->overflow) { overflow = true; break; }
+        std::memcpy(&jm, &W.host_counters->joint_maxd, 8);
+        ++inner;
+      } while (!(jm < tol) && inner < o.max_inner);
+      if (overflow) break;
+      CUDA_TRY(launch_joint_add_sweeps(act, nact, inner, out.sweeps, s));
+      CUDA_TRY(launch_joint_sigma((const double*)W.xb.ptr, 0, act, nact, (const int*)W.nz_rows.ptr,
+                                  (const double*)W.nz_vals.ptr, (const int*)W.nz_count.ptr,
+                                  (const int*)W.nz_cur.ptr, nzcap, (int)n, L.n_pad, L.nchunk,
+                                  std::sqrt((double)n), o.sigma_floor, tol, !(jm < tol),
+                                  out.sigma_std, out.iters, (uint8_t*)W.jflags.ptr, out.conv,
+                                  (double*)W.ej.ptr, (uint8_t*)W.keep.ptr, s));
+      CUDA_TRY(launch_joint_compact(act, (const uint8_t*)W.keep.ptr, nact, act_next,
+                                    &dc->joint_nact, s));
+      launches += 3;
+      if ((rc = read_counters(W, s))) return rc;
+      nact = W.host_counters->joint_nact;
+      std::swap(act, act_next);
+    }
+    if (!overflow) {
+      CUDA_TRY(ev_record(W, W.ev[2], s));
+      if (st) {
+        st->solver = s16 ? 3 : 2;
+        st->tile_cols = 0;
+        st->num_ctas = W.sms;
+        st->kernel_launches += launches;
+        st->tail_columns = nslots;
+        st->tail_sweeps = W.host_counters->tail_sweeps;
+        st->tail_gram_ondemand = W.host_counters->gram_ondemand;
+        st->screen_candidates = s16 ? W.host_counters->s16_nU : 0;
+        st->ms_gram = ev_ms(W.ev[1], W.ev[7]);
+        st->ms_screen = ev_ms(W.ev[8], W.ev[9]);
+      }
+      *nzcap_used = nzcap;
+      return SPMESL_OK;
+    }
+    if (nzcap >= p) break;
+    nzcap = (int)std::min<int64_t>(p, (int64_t)nzcap * 4);
+  }
+  return fail(SPMESL_ERR_OOM, "coefficient list overflow");
+}
+
 // Runs CD for [cb, ce) with automatic coefficient-list regrowth on overflow.
 int fit_columns_core(Workspace& W, const double* dX, int64_t n, int64_t p, int64_t cb, int64_t ce,
                      double lambda0, double tol, int32_t max_iter, const spmesl_options& o,
                      const FitOut& out, cudaStream_t s, spmesl_stats* st, Layout& L,
                      int* nzcap_used) {
   const int64_t m = ce - cb;
-  if (o.mode == 1)
+  if (o.mode == 1) {
+    // Algorithm 3 on the Gram form when the whole column range is fitted here and the Gram
+    // solver's state fits (solver 0/2/3); else (or solver 1) on the residual CD kernel
+    static const bool no_jgram = getenv("SPMESL_DEV_JOINT_RESIDUAL") != nullptr;   // (dev)
+    spmesl_options o0 = o;
+    o0.mode = 0;
+    std::string why;
+    if (!no_jgram && o.solver != 1 && gram_applicable(W, o0, n, p, cb, ce, &why))
+      return fit_joint_gram_core(W, dX, n, p, lambda0, tol, max_iter, o, out, s, st, L,
+                                 nzcap_used);
+    if (o.solver == 2 || o.solver == 3)
+      return fail(SPMESL_ERR_UNSUPPORTED, "Gram solver: " + why);
     return fit_joint_core(W, dX, n, p, cb, ce, lambda0, tol, max_iter, o, out, s, st, L,
                           nzcap_used);
+  }
   {
     std::string why;
     const bool ok = gram_applicable(W, o, n, p, cb, ce, &why);
@@ -1322,7 +1504,7 @@ int spmesl_release_workspace(void) {
                       &w->hx, &w->htheta, &w->hsigma, &w->hiters, &w->hsweeps, &w->hconv,
                       &w->coo_r, &w->coo_c, &w->coo_v, &w->hdiag, &w->zeros, &w->ej, &w->act0,
                       &w->act1, &w->keep, &w->jflags, &w->hit, &w->lam_dev, &w->nrm, &w->sq,
-                      &w->y16, &w->cand, &w->ssq};
+                      &w->y16, &w->cand, &w->ssq, &w->jtail, &w->slotmap, &w->jwork, &w->zj};
     drop_graph(*w);
     w->last_key.clear();
     g_alloc_gen.fetch_add(1);

@@ -4,6 +4,7 @@
 // delta leave the active set (F_j).  The sweeps themselves run in the persistent CD
 // kernel (cd_sweep.cu, CDParams::joint: one sweep per launch, residuals carried in Ej); this
 // file holds the outer-boundary kernels the host driver (api.cu, fit_joint_core) chains.
+#include <algorithm>
 #include "spmesl_internal.cuh"
 
 namespace spmesl {
@@ -105,7 +106,106 @@ __global__ void joint_compact_kernel(const int* __restrict__ act, const uint8_t*
   if (tid == 0) *nact_out = base_s;
 }
 
+// Mode 1 on the Gram form: the columns with a first-sweep hit become sweep slots (their z is
+// carried between joint sweeps); the others sweep as no-ops until their sigma converges.
+__global__ void joint_live_init_kernel(const uint8_t* __restrict__ hit, int m, int* __restrict__ nslots,
+                                       TailState* __restrict__ jtail, int* __restrict__ slotmap) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < m; c += gridDim.x * blockDim.x) {
+    if (hit[c]) {
+      const int sl = atomicAdd(nslots, 1);
+      TailState t;
+      t.col = c; t.outer = 0; t.sweeps = 0; t.inner = 0; t.flags = 0; t.cur = 0; t.cnt = 0;
+      t.lam = 0; t.sigma = 1.0;
+      jtail[sl] = t;
+      slotmap[c] = sl;
+    } else {
+      slotmap[c] = -1;
+    }
+  }
+}
+
+// active columns without a slot get one (z from their Gram column, b = 0 so far)
+__global__ void joint_live_add_kernel(const int* __restrict__ act, int nact, int* __restrict__ slotmap,
+                                      TailState* __restrict__ jtail, int* __restrict__ nslots,
+                                      const int* __restrict__ nz_cur) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nact; q += gridDim.x * blockDim.x) {
+    const int c = act[q];
+    if (slotmap[c] >= 0) continue;
+    const int sl = atomicAdd(nslots, 1);
+    TailState t;
+    t.col = c; t.outer = 0; t.sweeps = 0; t.inner = 0; t.flags = 0; t.cur = nz_cur[c]; t.cnt = 0;
+    t.lam = 0; t.sigma = 1.0;
+    jtail[sl] = t;
+    slotmap[c] = sl;
+  }
+}
+
+// how many active columns have no slot yet
+__global__ void joint_count_unslotted_kernel(const int* __restrict__ act, int nact,
+                                             const int* __restrict__ slotmap, int* __restrict__ cnt) {
+  int c = 0;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nact; q += gridDim.x * blockDim.x)
+    c += slotmap[act[q]] < 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt, c);
+}
+
+// the slots of the active columns (work list of one joint sweep, any order)
+__global__ void joint_work_kernel(const int* __restrict__ act, int nact, const int* __restrict__ slotmap,
+                                  int* __restrict__ work, int* __restrict__ nwork) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nact; q += gridDim.x * blockDim.x) {
+    const int sl = slotmap[act[q]];
+    if (sl >= 0) work[atomicAdd(nwork, 1)] = sl;
+  }
+}
+
+// every active column swept `inner` times in this outer iteration
+__global__ void joint_add_sweeps_kernel(const int* __restrict__ act, int nact, int inner,
+                                        int* __restrict__ sweeps) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nact; q += gridDim.x * blockDim.x)
+    sweeps[act[q]] += inner;
+}
+
 }  // namespace
+
+cudaError_t launch_joint_live_init(const uint8_t* hit, int m, int* nslots, TailState* jtail,
+                                   int* slotmap, cudaStream_t s) {
+  joint_live_init_kernel<<<std::max(1, std::min(296, (m + 255) / 256)), 256, 0, s>>>(hit, m, nslots,
+                                                                                  jtail, slotmap);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_joint_live_add(const int* act, int nact, int* slotmap, TailState* jtail,
+                                  int* nslots, const int* nz_cur, cudaStream_t s) {
+  if (nact <= 0) return cudaSuccess;
+  joint_live_add_kernel<<<std::max(1, std::min(296, (nact + 255) / 256)), 256, 0, s>>>(
+      act, nact, slotmap, jtail, nslots, nz_cur);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_joint_count_unslotted(const int* act, int nact, const int* slotmap, int* cnt,
+                                         cudaStream_t s) {
+  if (nact <= 0) return cudaSuccess;
+  joint_count_unslotted_kernel<<<std::max(1, std::min(296, (nact + 255) / 256)), 256, 0, s>>>(
+      act, nact, slotmap, cnt);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_joint_work(const int* act, int nact, const int* slotmap, int* work, int* nwork,
+                              cudaStream_t s) {
+  if (nact <= 0) return cudaSuccess;
+  joint_work_kernel<<<std::max(1, std::min(296, (nact + 255) / 256)), 256, 0, s>>>(act, nact, slotmap,
+                                                                                 work, nwork);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_joint_add_sweeps(const int* act, int nact, int inner, int* sweeps, cudaStream_t s) {
+  if (nact <= 0 || inner <= 0) return cudaSuccess;
+  joint_add_sweeps_kernel<<<std::max(1, std::min(296, (nact + 255) / 256)), 256, 0, s>>>(act, nact,
+                                                                                       inner, sweeps);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_joint_init(const double* Xb, int64_t col_begin, int m, int n_pad, int nchunk,
                               int* act, double* sigma, double* Ej, cudaStream_t s) {

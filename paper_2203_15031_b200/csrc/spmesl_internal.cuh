@@ -135,6 +135,15 @@ struct TailParams {
   int* iters;
   int* sweeps;
   uint8_t* converged;
+  // Algorithm 3 (mode 1) on the Gram form: each launch performs ONE sweep of every listed work
+  // item (TailState slots work[0 .. *M_dev)), at lambda = sigma_std[col] lambda0, keeps z in
+  // Zj[slot] between launches, max-reduces |db| into joint_maxd and writes the state back; the
+  // outer boundary (sigma refit, F_c, compaction) and the sweep counts are the host loop's.
+  int joint;
+  TailState* jtail;                  // [slots] state written back after each sweep
+  const int* work;                   // slots to sweep in this launch
+  double* Zj;                        // [slots][p]
+  unsigned long long* joint_maxd;    // max |db| (double bits; non-negative, so integer max)
 };
 // Gram solver (gram_full.cu): symmetric S = X~^T X~ / n with fused first-sweep screening.
 struct GramParams {
@@ -223,6 +232,15 @@ cudaError_t launch_tail_mark(const TailState* tail, int M, const int* nz_rows, i
 cudaError_t launch_tail_sweeps(const TailParams& P, int grid, cudaStream_t s);
 
 // Algorithm 3 joint mode helpers (joint.cu)
+cudaError_t launch_joint_live_init(const uint8_t* hit, int m, int* nslots, TailState* jtail,
+                                   int* slotmap, cudaStream_t s);
+cudaError_t launch_joint_work(const int* act, int nact, const int* slotmap, int* work, int* nwork,
+                              cudaStream_t s);
+cudaError_t launch_joint_live_add(const int* act, int nact, int* slotmap, TailState* jtail,
+                                  int* nslots, const int* nz_cur, cudaStream_t s);
+cudaError_t launch_joint_count_unslotted(const int* act, int nact, const int* slotmap, int* cnt,
+                                         cudaStream_t s);
+cudaError_t launch_joint_add_sweeps(const int* act, int nact, int inner, int* sweeps, cudaStream_t s);
 cudaError_t launch_joint_init(const double* Xb, int64_t col_begin, int m, int n_pad, int nchunk,
                               int* act, double* sigma, double* Ej, cudaStream_t s);
 cudaError_t launch_joint_sigma(const double* Xb, int64_t col_begin, const int* act, int nact,

@@ -429,18 +429,20 @@ __global__ void __launch_bounds__(TAIL_THREADS, 2) tail_sweep_kernel(const TailP
     bsync();
     const int k = TS.k;
     if (k >= M) break;
-    const TailState ts = P.tail[k];
+    const int slot = P.joint ? P.work[k] : k;
+    const TailState ts = P.joint ? P.jtail[slot] : P.tail[k];
     const int col = ts.lam * P.slot_stride + ts.col;         // lists / outputs index
     const int gc = (int)(P.col_begin + ts.col);              // the variable itself
     const double lambda0 = P.lambdas ? P.lambdas[ts.lam] : P.lambda0;
-    double sigma = ts.sigma;
+    double sigma = P.joint ? P.sigma_std[col] : ts.sigma;     // (joint: refit by the host loop)
     int outer = ts.outer, sweeps = ts.sweeps, inner = ts.inner, flags = ts.flags;
     int cur = ts.cur;
     int ocnt = min(ts.cnt, nzcap);
     bool overflow = ts.cnt > nzcap;
-    if (P.z_from_gtab) {
-      ensure_gram_column(P, gc, TS, tx, tvv);
-      const double* gz = P.Gtab + (size_t)gc * p;
+    const bool z_saved = P.joint && (ts.flags & 16);          // joint: z kept between launches
+    if (P.z_from_gtab || z_saved) {
+      if (!z_saved) ensure_gram_column(P, gc, TS, tx, tvv);
+      const double* gz = z_saved ? P.Zj + (size_t)slot * p : P.Gtab + (size_t)gc * p;
       if ((p & 1) == 0) {   // the whole column in one bulk copy (8p bytes, 16-byte multiple)
         if (tid == 0) {
           prefetch_col(z, gz, (uint32_t)p * 8, &TS.z_bar);
@@ -568,7 +570,15 @@ __global__ void __launch_bounds__(TAIL_THREADS, 2) tail_sweep_kernel(const TailP
       // the new list becomes the current one
       for (int m = tid; m < min(ncnt, nzcap); m += TAIL_THREADS) { orow[m] = nrow[m]; ov[m] = nv[m]; }
       ocnt = min(ncnt, nzcap);
+      if (ncnt > nzcap) overflow = true;
       bsync();
+      if (P.joint) {
+        // one sweep per launch: publish max |db|, keep z and the state for the next launch
+        if (tid == 0) atomicMax(P.joint_maxd, (unsigned long long)__double_as_longlong(maxd));
+        double* zs = P.Zj + (size_t)slot * p;
+        for (int t = tid; t < p; t += TAIL_THREADS) zs[t] = z[t];
+        break;
+      }
       if (maxd < P.tol || inner >= P.max_inner) {
         if (!(maxd < P.tol)) flags |= 2;
         // fresh residual and sigma (reading g4): every thread builds its samples'
@@ -605,12 +615,18 @@ __global__ void __launch_bounds__(TAIL_THREADS, 2) tail_sweep_kernel(const TailP
     if (tid == 0) {
       P.nz_count[col] = ocnt;
       P.nz_cur[col] = dst;
-      P.sigma_std[col] = sigma;
-      P.iters[col] = outer;
-      P.sweeps[col] = sweeps;
-      P.converged[col] = (uint8_t)((flags & 1) && !(flags & 2));
       if (overflow) atomicExch(&P.flags[FLAG_OVERFLOW], 1);
       atomicAdd(P.sweeps_count, sweeps - ts.sweeps);
+      if (P.joint) {   // (sigma, iters, sweeps, converged: the host loop's joint kernels)
+        TailState t2 = ts;
+        t2.cur = dst; t2.cnt = ocnt; t2.sweeps = sweeps; t2.flags = ts.flags | 16;
+        P.jtail[slot] = t2;
+      } else {
+        P.sigma_std[col] = sigma;
+        P.iters[col] = outer;
+        P.sweeps[col] = sweeps;
+        P.converged[col] = (uint8_t)((flags & 1) && !(flags & 2));
+      }
     }
   }
 }

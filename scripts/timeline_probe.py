@@ -5,6 +5,7 @@ import numpy as np, torch
 import paper_2203_15031_b200 as S
 from synth import generators as G
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 5
+mode = sys.argv[2] if len(sys.argv) > 2 else "per_column"
 X, gt, spec = G.make_config(cfg)
 n, p = X.shape
 lam = S.lambda_ub(n, p) if spec["rule"] == "ub" else S.lambda_univ(n, p)
@@ -15,12 +16,12 @@ out = dict(theta=torch.empty((p, p), dtype=torch.float64, device="cuda"),
            sweeps=torch.empty(p, dtype=torch.int32, device="cuda"),
            conv=torch.empty(p, dtype=torch.uint8, device="cuda"))
 for _ in range(3):
-    S.fit_device(Xd, lam, out=out)
+    S.fit_device(Xd, lam, out=out, mode=mode)
 torch.cuda.synchronize()
 from torch.profiler import profile, ProfilerActivity
 with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
     for _ in range(2):
-        S.fit_device(Xd, lam, out=out)
+        S.fit_device(Xd, lam, out=out, mode=mode)
     torch.cuda.synchronize()
 prof.export_chrome_trace("gpurun_out/trace.json")
 ev = json.load(open("gpurun_out/trace.json"))["traceEvents"]
