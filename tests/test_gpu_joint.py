@@ -29,12 +29,16 @@ JCASES = [
 
 @pytest.mark.parametrize("cfg,over", JCASES)
 @pytest.mark.parametrize("delta", [1e-4, 1e-10])
-def test_joint_parity(S, oracle, cfg, over, delta):
+@pytest.mark.parametrize("solver", ["auto", "gram", "residual"])
+def test_joint_parity(S, oracle, cfg, over, delta, solver):
+    # auto / gram: Algorithm 3 on the Gram form (certified f16 or FP64 screening for the first
+    # joint sweep, sweep slots for the columns with a hit); residual: the CD kernel per sweep
     X, _, _ = G.make_config(cfg, **over)
     n, p = X.shape
     lam = oracle.lambda_univ(n, p)
     ora = oracle.spmesl_fit_joint(X, lam, delta=delta)
-    res = S.fit(X, lam, tol=delta, max_iter=100, mode="joint")
+    res = S.fit(X, lam, tol=delta, max_iter=100, mode="joint", solver=solver)
+    assert res.stats["solver"] == {"auto": 3, "gram": 2, "residual": 1}[solver]
     rep = compare(res.Theta, res.sigma, res.iters, res.sweeps, ora)
     print(cfg, over, delta, rep, res.stats["kernel_launches"])
     assert_parity(rep)
@@ -46,8 +50,8 @@ def test_joint_parity(S, oracle, cfg, over, delta):
 def test_joint_bit_identical_across_tile_sizes(S, oracle, T):
     X, _, _ = G.make_config(2)
     lam = oracle.lambda_univ(*X.shape)
-    ref = S.fit(X, lam, tol=1e-4, mode="joint", tile_cols=32)
-    r = S.fit(X, lam, tol=1e-4, mode="joint", tile_cols=T)
+    ref = S.fit(X, lam, tol=1e-4, mode="joint", tile_cols=32, solver="residual")
+    r = S.fit(X, lam, tol=1e-4, mode="joint", tile_cols=T, solver="residual")
     assert np.array_equal(r.Theta, ref.Theta) and np.array_equal(r.sweeps, ref.sweeps)
 
 
@@ -78,3 +82,24 @@ def test_joint_columns_api_rejects_partial_range(S):
     X, _, _ = G.make_config(1)
     with pytest.raises(S.SpmeslError):
         S.fit_columns_device(torch.from_numpy(X).cuda(), 0, X.shape[1] // 2, 0.1, mode="joint")
+
+
+def test_joint_gram_forms_identical_and_unstandardized(S, oracle):
+    """Mode 1 on the Gram form: the certified f16 and the FP64 screening give bit-identical
+    fits; with standardize = 0 and column norms ||x_k||^2 / n in [0.64, 1.44] the columns
+    without a first-sweep hit refit sigma != 1 and stay active (they get sweep slots then), and
+    the result still matches the joint oracle."""
+    X, _, _ = G.make_config(4, p=400, n=200, family="hub")
+    n, p = X.shape
+    lam = oracle.lambda_univ(n, p)
+    a = S.fit(X, lam, tol=1e-4, mode="joint", solver="gram")
+    b = S.fit(X, lam, tol=1e-4, mode="joint", solver="gram16")
+    assert np.array_equal(a.Theta, b.Theta) and np.array_equal(a.sweeps, b.sweeps)
+    Xs, _, _ = oracle.standardize(X)
+    Xs = Xs * np.linspace(0.8, 1.2, p)[None, :]
+    ora = oracle.spmesl_fit_joint(Xs, lam, delta=1e-4, standardize=False)
+    for solver in ("auto", "residual"):
+        res = S.fit(Xs, lam, tol=1e-4, mode="joint", standardize=False, solver=solver)
+        rep = compare(res.Theta, res.sigma, res.iters, res.sweeps, ora)
+        print(solver, rep)
+        assert_parity(rep)
