@@ -161,6 +161,23 @@ int spmesl_fit_device(const double* dX, int64_t n, int64_t p, double lambda0, do
                       void* cuda_stream, spmesl_stats* st);
 
 /*
+ * Sparse-output device entry point: as spmesl_fit_device, but Theta —
+ * symmetrized per options.symmetrize, rescaled per options.standardize, diagonal included —
+ * is returned in compressed sparse column form instead of a dense p x p array (no 8 p^2-byte
+ * fill): dColPtr[p + 1] (int64, device), dRows[cap] (int32, device; ascending within each
+ * column), dVals[cap] (double, device).  Theta is symmetric, so this is also its CSR form.
+ * Every entry equals the dense path's bit for bit; the absent ones are zeros there.
+ * *nnz_out (host) receives the entry count; if it exceeds cap the call returns SPMESL_ERR_ARG
+ * with dColPtr filled and dRows/dVals untouched.  dSigma / dIters [p] as spmesl_fit_device;
+ * dSweeps / dConverged nullable.  Any mode / solver.  Blocking.
+ */
+int spmesl_fit_sparse_device(const double* dX, int64_t n, int64_t p, double lambda0, double tol,
+                             int32_t max_iter, const spmesl_options* opt, int64_t* dColPtr,
+                             int32_t* dRows, double* dVals, int64_t cap, int64_t* nnz_out,
+                             double* dSigma, int32_t* dIters, int32_t* dSweeps,
+                             uint8_t* dConverged, void* cuda_stream, spmesl_stats* st);
+
+/*
  * Multi-GPU building blocks (one process per GPU; columns [col_begin, col_end) on this rank,
  * X replicated; BASELINE.json north_star "column-block sharding ... one all-gather").
  *

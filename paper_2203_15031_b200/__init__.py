@@ -136,6 +136,56 @@ def fit_device(X, lambda0: float, tol: float = 1e-4, max_iter: int = 100, *, str
                      out["conv"].view(torch.bool), st.asdict())
 
 
+def fit_sparse_device(X, lambda0: float, tol: float = 1e-4, max_iter: int = 100, *,
+                      stream=None, cap=None, **options) -> dict:
+    """spmesl_fit_sparse_device: Theta in CSC form (col_ptr int64 [p+1], rows int32, vals
+    float64; symmetric, so also CSR) without the dense p x p array, plus sigma / iters / sweeps
+    / converged.  cap: entry capacity (default p + 64 p; grown and retried once if short)."""
+    import torch
+    if not X.is_cuda or X.dtype != torch.float64:
+        raise TypeError("X must be a float64 CUDA tensor")
+    X = as_colmajor(X)
+    n, p = X.shape
+    dev = X.device
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    o = _opts(**options)
+    cap = int(cap) if cap is not None else p + 64 * p
+    col_ptr = torch.empty(p + 1, dtype=torch.int64, device=dev)
+    sigma = torch.empty(p, dtype=torch.float64, device=dev)
+    iters = torch.empty(p, dtype=torch.int32, device=dev)
+    sweeps = torch.empty(p, dtype=torch.int32, device=dev)
+    conv = torch.empty(p, dtype=torch.uint8, device=dev)
+    for _ in range(2):
+        rows = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+        vals = torch.empty(max(cap, 1), dtype=torch.float64, device=dev)
+        nnz = ctypes.c_int64(0)
+        st = Stats()
+        with torch.cuda.device(dev):
+            rc = load().spmesl_fit_sparse_device(
+                _vp(X), n, p, float(lambda0), float(tol), int(max_iter), ctypes.byref(o),
+                _vp(col_ptr), _vp(rows), _vp(vals), cap, ctypes.byref(nnz), _vp(sigma),
+                _vp(iters), _vp(sweeps), _vp(conv), ctypes.c_void_p(s.cuda_stream),
+                ctypes.byref(st))
+        if rc == _lib.ERR_ARG and nnz.value > cap:
+            cap = int(nnz.value)
+            continue
+        _lib.check(rc, st)
+        break
+    k = nnz.value
+    return dict(code=rc, col_ptr=col_ptr, rows=rows[:k], vals=vals[:k], sigma=sigma,
+                iters=iters, sweeps=sweeps, converged=conv.view(torch.bool), stats=st.asdict())
+
+
+def sparse_to_dense(col_ptr, rows, vals, p: int):
+    """Dense p x p (column-major view) of a CSC matrix from fit_sparse_device (testing aid)."""
+    import torch
+    T = torch.zeros((p, p), dtype=torch.float64, device=vals.device)   # T[k, j] = Theta[j, k]
+    cols = torch.repeat_interleave(torch.arange(p, device=vals.device),
+                                   (col_ptr[1:] - col_ptr[:-1]))
+    T[cols, rows.long()] = vals
+    return T.t()
+
+
 def gram_supported(n: int, p: int) -> bool:
     """spmesl_gram_supported: the Gram solver's sweep state fits on chip for (n, p)."""
     return bool(load().spmesl_gram_supported(int(n), int(p)))

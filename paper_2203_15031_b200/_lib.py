@@ -76,7 +76,7 @@ EXPORTS = [
     "spmesl_default_options", "spmesl_fit", "spmesl_fit_ex", "spmesl_fit_device",
     "spmesl_fit_columns_device", "spmesl_assemble_device", "spmesl_gram_tile_count",
     "spmesl_gram_screen_device", "spmesl_fit_columns_gram_device", "spmesl_gram_supported",
-    "spmesl_fit_path_device", "spmesl_screen_tile_count",
+    "spmesl_fit_path_device", "spmesl_screen_tile_count", "spmesl_fit_sparse_device",
     "spmesl_lambda_univ",
     "spmesl_lambda_ub", "spmesl_lambda_pb", "spmesl_solve_k", "spmesl_last_error",
     "spmesl_release_workspace", "spmesl_version",
@@ -116,6 +116,9 @@ def load() -> ctypes.CDLL:
     L.spmesl_gram_supported.restype = ctypes.c_int
     L.spmesl_gram_tile_count.argtypes = [i64]
     L.spmesl_gram_tile_count.restype = i64
+    L.spmesl_fit_sparse_device.argtypes = [vp, i64, i64, dbl, dbl, i32, popt, vp, vp, vp, i64,
+                                           ctypes.POINTER(ctypes.c_int64), vp, vp, vp, vp, vp, pst]
+    L.spmesl_fit_sparse_device.restype = ctypes.c_int
     L.spmesl_screen_tile_count.argtypes = [i64, popt]
     L.spmesl_screen_tile_count.restype = i64
     L.spmesl_gram_screen_device.argtypes = [vp, i64, i64, dbl, i64, i64, popt, vp, vp, pst]

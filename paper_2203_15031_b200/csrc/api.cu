@@ -98,6 +98,7 @@ struct Workspace {
   Buffer lam_dev;                                           // multi-lambda: penalty levels
   Buffer nrm, sq, y16, cand;                                // certified f16 screening
   Buffer ssq;                                               // x~_c^T x~_c (Gram solvers)
+  Buffer ccount;                                            // sparse Theta: entries per column
   // host-API staging
   Buffer hx, htheta, hsigma, hiters, hsweeps, hconv, coo_r, coo_c, coo_v, hdiag, zeros;
   DevCounters* host_counters = nullptr;   // pinned
@@ -1504,7 +1505,7 @@ int spmesl_release_workspace(void) {
                       &w->hx, &w->htheta, &w->hsigma, &w->hiters, &w->hsweeps, &w->hconv,
                       &w->coo_r, &w->coo_c, &w->coo_v, &w->hdiag, &w->zeros, &w->ej, &w->act0,
                       &w->act1, &w->keep, &w->jflags, &w->hit, &w->lam_dev, &w->nrm, &w->sq,
-                      &w->y16, &w->cand, &w->ssq, &w->jtail, &w->slotmap, &w->jwork, &w->zj};
+                      &w->y16, &w->cand, &w->ssq, &w->jtail, &w->slotmap, &w->jwork, &w->zj, &w->ccount};
     drop_graph(*w);
     w->last_key.clear();
     g_alloc_gen.fetch_add(1);
@@ -1543,6 +1544,67 @@ int spmesl_fit_device(const double* dX, int64_t n, int64_t p, double lambda0, do
   if (W->cc_major < 10) return fail(SPMESL_ERR_UNSUPPORTED, "needs an sm_100 device");
   return fit_device_impl(dX, n, p, lambda0, tol, max_iter, o, dTheta, dSigma, dIters, dSweeps,
                          dConverged, (cudaStream_t)cuda_stream, st, *W);
+}
+
+int spmesl_fit_sparse_device(const double* dX, int64_t n, int64_t p, double lambda0, double tol,
+                             int32_t max_iter, const spmesl_options* opt, int64_t* dColPtr,
+                             int32_t* dRows, double* dVals, int64_t cap, int64_t* nnz_out,
+                             double* dSigma, int32_t* dIters, int32_t* dSweeps,
+                             uint8_t* dConverged, void* cuda_stream, spmesl_stats* st) {
+  init_stats(st);
+  spmesl_options o = resolve(opt);
+  int rc = validate(dX, n, p, lambda0, tol, max_iter, o);
+  if (rc) return rc;
+  if (!dColPtr || !dRows || !dVals || !nnz_out || !dSigma || !dIters)
+    return fail(SPMESL_ERR_ARG, "output pointer is NULL");
+  int dev;
+  if ((rc = current_device(-1, &dev))) return rc;
+  Workspace* W = workspace_for(dev);
+  std::lock_guard<std::mutex> lk(W->mu);
+  if ((rc = ws_init(*W, dev))) return rc;
+  if (W->cc_major < 10) return fail(SPMESL_ERR_UNSUPPORTED, "needs an sm_100 device");
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  if ((rc = ensure(W->sigma_std, (size_t)p * 8))) return rc;
+  if (!dSweeps) { if ((rc = ensure(W->sweeps, (size_t)p * 4))) return rc; dSweeps = (int32_t*)W->sweeps.ptr; }
+  if (!dConverged) { if ((rc = ensure(W->conv, (size_t)p))) return rc; dConverged = (uint8_t*)W->conv.ptr; }
+  FitOut out{0, p, (double*)W->sigma_std.ptr, dIters, dSweeps, dConverged};
+  Layout L;
+  int nzcap = 0;
+  // the fit itself (any mode / solver; no dense Theta, so no fill)
+  if ((rc = fit_columns_core(*W, dX, n, p, 0, p, lambda0, tol, max_iter, o, out, s, st, L, &nzcap)))
+    return rc;
+  if ((rc = ensure(W->ccount, (size_t)p * 4))) return rc;
+  DevCounters* dc = (DevCounters*)W->counters.ptr;
+  CUDA_TRY(ev_record(*W, W->ev[3], s));
+  CUDA_TRY(launch_sparse_count(p, (const int*)W->nz_count.ptr, (const int*)W->nz_cur.ptr,
+                               (const int*)W->nz_rows.ptr, (const double*)W->nz_vals.ptr, nzcap,
+                               o.symmetrize, (int*)W->ccount.ptr, s));
+  CUDA_TRY(launch_csc_scan((const int*)W->ccount.ptr, (int)p, dColPtr, &dc->csc_total, s));
+  if ((rc = device_stats(*W, dIters, dSweeps, dConverged, p, s))) return rc;
+  if ((rc = read_counters(*W, s))) return rc;
+  const int64_t total = W->host_counters->csc_total;
+  *nnz_out = total;
+  if (total > cap)
+    return fail(SPMESL_ERR_ARG, "sparse Theta capacity too small: need " + std::to_string(total));
+  CUDA_TRY(launch_sparse_write(p, (const int*)W->nz_count.ptr, (const int*)W->nz_cur.ptr,
+                               (const int*)W->nz_rows.ptr, (const double*)W->nz_vals.ptr, nzcap,
+                               (const double*)W->sigma_std.ptr,
+                               o.standardize ? (const double*)W->scale.ptr : nullptr, o.symmetrize,
+                               dColPtr, dRows, dVals, dSigma, s));
+  CUDA_TRY(ev_record(*W, W->ev[4], s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  int any_unconv = 0;
+  stats_from_counters(*W->host_counters, p, st, &any_unconv);
+  if (st) {
+    st->nnz = total - p;   // off-diagonal entries of Theta
+    st->ms_standardize = ev_ms(W->ev[0], W->ev[1]);
+    st->ms_cd = ev_ms(W->ev[1], W->ev[2]);
+    st->ms_assemble = ev_ms(W->ev[3], W->ev[4]);
+    st->ms_total = ev_ms(W->ev[0], W->ev[4]);
+    st->kernel_launches += 5;   // standardize, sparse count, scan, write, column stats
+    st->bad_column = -1;
+  }
+  return any_unconv ? SPMESL_WARN_NOT_CONVERGED : SPMESL_OK;
 }
 
 int spmesl_fit_path_device(const double* dX, int64_t n, int64_t p, const double* lambdas,

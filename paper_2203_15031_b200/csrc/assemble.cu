@@ -310,6 +310,140 @@ cudaError_t launch_assemble(int64_t p, int64_t col_begin, int64_t col_end, const
   return cudaGetLastError();
 }
 
+// Sparse Θ (§8(f) f3): per column k the kept off-diagonal entries (symmetrize: the partner
+// b_kj is nonzero — the dense path writes exactly these) plus the diagonal, rows ascending.
+__device__ __forceinline__ bool theta_kept(int k, int j, const int* __restrict__ cnt,
+                                           const int* __restrict__ cur,
+                                           const int* __restrict__ nz_rows,
+                                           const double* __restrict__ nz_vals, int nzcap,
+                                           int symmetrize, double* b_kj_out) {
+  if (!symmetrize) return true;
+  const size_t bj = (size_t)j * 2 * nzcap + (size_t)cur[j] * nzcap;
+  int lo = 0, hi = min(cnt[j], nzcap);
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    const int v = nz_rows[bj + mid];
+    if (v == k) { *b_kj_out = nz_vals[bj + mid]; return nz_vals[bj + mid] != 0.0; }
+    if (v < k) lo = mid + 1;
+    else hi = mid;
+  }
+  return false;
+}
+
+__global__ void sparse_count_kernel(int64_t p, const int* __restrict__ cnt, const int* __restrict__ cur,
+                                    const int* __restrict__ nz_rows, const double* __restrict__ nz_vals,
+                                    int nzcap, int symmetrize, int* __restrict__ ccount) {
+  const int lane = threadIdx.x & 31;
+  const int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (k >= p) return;
+  const int m = min(cnt[k], nzcap);
+  const size_t base = (size_t)k * 2 * nzcap + (size_t)cur[k] * nzcap;
+  int kept = 0;
+  for (int e = lane; e < m; e += 32) {
+    double bkj = 0.0;
+    kept += theta_kept((int)k, nz_rows[base + e], cnt, cur, nz_rows, nz_vals, nzcap, symmetrize, &bkj);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) kept += __shfl_xor_sync(0xffffffffu, kept, o);
+  if (lane == 0) ccount[k] = kept + 1;   // + the diagonal
+}
+
+__global__ void sparse_write_kernel(int64_t p, const int* __restrict__ cnt, const int* __restrict__ cur,
+                                    const int* __restrict__ nz_rows, const double* __restrict__ nz_vals,
+                                    int nzcap, const double* __restrict__ sigma_std,
+                                    const double* __restrict__ scale, int symmetrize, int rescale,
+                                    const int64_t* __restrict__ col_ptr, int32_t* __restrict__ rows,
+                                    double* __restrict__ vals, double* __restrict__ sigma_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (k >= p) return;
+  const int m = min(cnt[k], nzcap);
+  const size_t base = (size_t)k * 2 * nzcap + (size_t)cur[k] * nzcap;
+  const double sk = rescale ? scale[k] : 1.0;
+  int64_t pos = col_ptr[k];
+  bool diag_done = false;
+  for (int e0 = 0; e0 < m; e0 += 32) {
+    const int e = e0 + lane;
+    int j = 0x7fffffff;
+    double out = 0.0;
+    bool kept = false;
+    if (e < m) {
+      j = nz_rows[base + e];
+      const double sj = rescale ? scale[j] : 1.0;
+      const double t_jk = theta1(nz_vals[base + e], sigma_std[k], sj, sk, rescale != 0);
+      double b_kj = 0.0;
+      kept = theta_kept((int)k, j, cnt, cur, nz_rows, nz_vals, nzcap, symmetrize, &b_kj);
+      out = t_jk;
+      if (kept && symmetrize) {   // as assemble_lists_kernel
+        const double t_kj = theta1(b_kj, sigma_std[j], sk, sj, rescale != 0);
+        const double u = (j < k) ? t_jk : t_kj;
+        const double l = (j < k) ? t_kj : t_jk;
+        out = (fabs(u) > fabs(l)) ? l : u;
+      }
+    }
+    // the diagonal goes before the first kept row above k
+    const unsigned kept_mask = __ballot_sync(0xffffffffu, kept);
+    const unsigned above = __ballot_sync(0xffffffffu, kept && j > k);
+    int dpos = -1;
+    if (!diag_done && above) { dpos = __popc(kept_mask & ((above & -above) - 1u)); diag_done = true; }
+    if (kept) {
+      const int before = __popc(kept_mask & ((1u << lane) - 1u));
+      const int shift = (dpos >= 0 && before >= dpos) ? 1 : 0;
+      rows[pos + before + shift] = j;
+      vals[pos + before + shift] = out;
+    }
+    if (dpos >= 0 && lane == 0) rows[pos + dpos] = (int32_t)k;
+    if (dpos >= 0 && lane == 0) {
+      const double sg = sigma_std[k];
+      double w = 1.0 / (sg * sg);
+      if (rescale) w = w / (sk * sk);
+      vals[pos + dpos] = w;
+    }
+    pos += __popc(kept_mask) + (dpos >= 0 ? 1 : 0);
+  }
+  if (lane == 0) {
+    if (!diag_done) {
+      const double sg = sigma_std[k];
+      double w = 1.0 / (sg * sg);
+      if (rescale) w = w / (sk * sk);
+      rows[pos] = (int32_t)k;
+      vals[pos] = w;
+    }
+    if (sigma_out) sigma_out[k] = rescale ? sk * sigma_std[k] : sigma_std[k];
+  }
+}
+
+cudaError_t launch_sparse_count(int64_t p, const int* cnt, const int* cur, const int* nz_rows,
+                                const double* nz_vals, int nzcap, int symmetrize, int* ccount,
+                                cudaStream_t s) {
+  const int wpb = 8;
+  sparse_count_kernel<<<(unsigned)((p + wpb - 1) / wpb), wpb * 32, 0, s>>>(p, cnt, cur, nz_rows,
+                                                                          nz_vals, nzcap, symmetrize,
+                                                                          ccount);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sparse_write(int64_t p, const int* cnt, const int* cur, const int* nz_rows,
+                                const double* nz_vals, int nzcap, const double* sigma_std,
+                                const double* scale, int symmetrize, const int64_t* col_ptr,
+                                int32_t* rows, double* vals, double* sigma_out, cudaStream_t s) {
+  const int wpb = 8;
+  sparse_write_kernel<<<(unsigned)((p + wpb - 1) / wpb), wpb * 32, 0, s>>>(
+      p, cnt, cur, nz_rows, nz_vals, nzcap, sigma_std, scale, symmetrize, scale != nullptr,
+      col_ptr, rows, vals, sigma_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_csc_scan(const int* cnt, int ncols, int64_t* col_ptr, int64_t* total,
+                            cudaStream_t s) {
+  const bool staged = (size_t)ncols * 4 <= 160 * 1024;
+  if (staged)
+    cudaFuncSetAttribute(csc_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  csc_scan_kernel<<<1, 1024, staged ? (size_t)ncols * 4 : 0, s>>>(cnt, ncols, col_ptr, total,
+                                                                 staged ? 1 : 0);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_assemble_lists(int64_t p, const int* nz_count, const int* nz_cur,
                                   const int* nz_rows, const double* nz_vals, int nzcap,
                                   const double* sigma_std, const double* scale, int symmetrize,

@@ -289,6 +289,15 @@ cudaError_t launch_zero_fill_bulk(double* a, size_t count, int grid, cudaStream_
 cudaError_t launch_reset(void* counters, int counters_bytes, int key_off, int* queue, int* nz_count,
                          int* nz_cur, int64_t m, cudaStream_t s);
 cudaError_t launch_csc_counts(const int* nz_count, int ncols, int32_t* out, cudaStream_t s);
+cudaError_t launch_sparse_count(int64_t p, const int* cnt, const int* cur, const int* nz_rows,
+                                const double* nz_vals, int nzcap, int symmetrize, int* ccount,
+                                cudaStream_t s);
+cudaError_t launch_sparse_write(int64_t p, const int* cnt, const int* cur, const int* nz_rows,
+                                const double* nz_vals, int nzcap, const double* sigma_std,
+                                const double* scale, int symmetrize, const int64_t* col_ptr,
+                                int32_t* rows, double* vals, double* sigma_out, cudaStream_t s);
+cudaError_t launch_csc_scan(const int* cnt, int ncols, int64_t* col_ptr, int64_t* total,
+                            cudaStream_t s);
 cudaError_t launch_assemble_lists(int64_t p, const int* nz_count, const int* nz_cur,
                                   const int* nz_rows, const double* nz_vals, int nzcap,
                                   const double* sigma_std, const double* scale, int symmetrize,

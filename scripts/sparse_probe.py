@@ -1,0 +1,19 @@
+"""Dev: sparse-output fit (no dense Theta) time at config 5."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_2203_15031_b200 as S
+from synth import generators as G
+X, _, spec = G.make_config(5)
+n, p = X.shape
+lam = S.lambda_ub(n, p)
+Xd = torch.from_numpy(np.ascontiguousarray(X.T)).cuda().t()
+for mode in ("per_column", "joint"):
+    ts = []
+    for it in range(6):
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(); e0.record()
+        r = S.fit_sparse_device(Xd, lam, mode=mode)
+        e1.record(); torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    print(mode, "sparse fit ms", [round(t, 3) for t in ts], "nnz", r["stats"]["nnz"], "device total", round(r["stats"]["ms_total"], 3))

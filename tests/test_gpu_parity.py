@@ -493,3 +493,31 @@ np.save({str(tmp_path / 'sw.npy')!r}, r.sweeps.cpu().numpy())
     ref = S.fit_device(Xd, lam, eager=True)
     assert np.array_equal(np.load(tmp_path / "T.npy"), ref.Theta.cpu().numpy())
     assert np.array_equal(np.load(tmp_path / "sw.npy"), ref.sweeps.cpu().numpy())
+
+
+@pytest.mark.parametrize("solver,mode,cfg,over,sym", [
+    ("auto", "per_column", 5, dict(p=3000), True),
+    ("auto", "per_column", 4, dict(p=777, n=203), True),     # ragged, multi-sweep
+    ("residual", "per_column", 2, {}, True),
+    ("auto", "per_column", 2, {}, False),                    # Theta_1 (unsymmetrized)
+    ("auto", "joint", 4, dict(p=300, n=150, family="hub"), True),
+])
+def test_sparse_output_equals_dense(S, oracle, solver, mode, cfg, over, sym):
+    """spmesl_fit_sparse_device (§8(f) f3): Theta as CSC without the dense array equals the
+    dense device fit entry for entry (bit for bit), rows ascending, diagonal present."""
+    import torch
+    X, _, _ = G.make_config(cfg, **over)
+    n, p = X.shape
+    lam = oracle.lambda_univ(n, p)
+    Xd = torch.from_numpy(np.ascontiguousarray(X.T)).cuda().t()
+    dense = S.fit_device(Xd, lam, solver=solver, mode=mode, symmetrize=sym, eager=True)
+    sp = S.fit_sparse_device(Xd, lam, solver=solver, mode=mode, symmetrize=sym, cap=p + 4)
+    cp, rows, vals = sp["col_ptr"].cpu().numpy(), sp["rows"].cpu().numpy(), sp["vals"].cpu().numpy()
+    assert cp[0] == 0 and cp[-1] == len(rows)
+    for k in range(p):
+        r = rows[cp[k]:cp[k + 1]]
+        assert np.all(np.diff(r) > 0) and k in r
+    T = S.sparse_to_dense(sp["col_ptr"], sp["rows"], sp["vals"], p)
+    assert torch.equal(T, dense.Theta)
+    assert torch.equal(sp["sigma"], dense.sigma) and torch.equal(sp["sweeps"], dense.sweeps)
+    assert sp["stats"]["nnz"] == len(rows) - p
