@@ -830,7 +830,8 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   return SPMESL_OK;
 }
 
-void gram_stats(Workspace& W, int64_t p, int nzcap, spmesl_stats* st, bool screen16 = false) {
+void gram_stats(Workspace& W, int64_t p, int nzcap, spmesl_stats* st, bool screen16 = false,
+                bool replay = false) {
   (void)nzcap;
   if (!st) return;
   const int nT = (int)((((p + J - 1) / J) + 3) / 4);
@@ -842,10 +843,11 @@ void gram_stats(Workspace& W, int64_t p, int nzcap, spmesl_stats* st, bool scree
   st->tile_cols = 0;
   st->num_ctas = std::min(W.sms, nT * (nT + 1) / 2);
   st->kernel_launches += W.gram_launches;
-  st->ms_gram = ev_ms(W.ev[1], W.ev[7]);
+  // (a replay records only the events of ms_total and ms_screen: see ev_record)
+  st->ms_gram = replay ? -1.0 : ev_ms(W.ev[1], W.ev[7]);
   st->ms_screen = ev_ms(W.ev[8], W.ev[9]);
   st->screen_fill_bytes = W.screen_fill * 8;
-  st->ms_tail = ev_ms(W.ev[5], W.ev[6]);
+  st->ms_tail = replay ? -1.0 : ev_ms(W.ev[5], W.ev[6]);
   st->tail_columns = W.host_counters->tail_count;
   st->tail_sweeps = W.host_counters->tail_sweeps;
 }
@@ -1141,13 +1143,14 @@ int gram_fit_enqueue_all(Workspace& W, const double* dX, int64_t n, int64_t p, d
   return SPMESL_OK;
 }
 
-void finish_stats(Workspace& W, int64_t p, spmesl_stats* st, int* any_unconv, int launches) {
+void finish_stats(Workspace& W, int64_t p, spmesl_stats* st, int* any_unconv, int launches,
+                  bool replay = false) {
   stats_from_counters(*W.host_counters, p, st, any_unconv);
   if (st) {
     st->nnz = W.host_counters->csc_total;
-    st->ms_standardize = ev_ms(W.ev[0], W.ev[1]);
-    st->ms_cd = ev_ms(W.ev[1], W.ev[2]);
-    st->ms_assemble = ev_ms(W.ev[3], W.ev[4]);
+    st->ms_standardize = replay ? -1.0 : ev_ms(W.ev[0], W.ev[1]);
+    st->ms_cd = replay ? -1.0 : ev_ms(W.ev[1], W.ev[2]);
+    st->ms_assemble = replay ? -1.0 : ev_ms(W.ev[3], W.ev[4]);
     st->ms_total = ev_ms(W.ev[0], W.ev[4]);
     st->kernel_launches += launches;   // (+ the solver kernels, counted by the solver)
     st->bad_column = -1;
@@ -1261,7 +1264,7 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
       CUDA_TRY(cudaStreamSynchronize(s));
       if (W.host_counters->err) return std_error(W, st);
       if (!W.host_counters->overflow) {
-        gram_stats(W, p, nzcap, st, o.solver != 2);
+        gram_stats(W, p, nzcap, st, o.solver != 2, launched);
         if (st) st->graph_replay = launched ? 1 : 0;
         break;
       }
@@ -1271,10 +1274,8 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
       // (Theta's zero fill is redone by the next attempt: the assembly above wrote into it)
     }
     int any_unconv = 0;
-    finish_stats(W, p, st, &any_unconv, 3);   // standardize, assemble_lists, column_stats
-    if (st && st->graph_replay) {   // phase events not recorded by the replay (ev_record)
-      st->ms_standardize = st->ms_cd = st->ms_assemble = st->ms_tail = st->ms_gram = -1.0;
-    }
+    // (standardize, assemble_lists, column_stats)
+    finish_stats(W, p, st, &any_unconv, 3, st && st->graph_replay);
     return any_unconv ? SPMESL_WARN_NOT_CONVERGED : SPMESL_OK;
   }
   // residual solver / joint mode: enqueue per call
