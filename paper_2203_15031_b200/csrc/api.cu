@@ -56,6 +56,7 @@ struct DevCounters {
   int st_max_sweeps, st_max_outer, st_unconv, pad4;
   int s16_nU, pad5;                // solver 3: candidate columns of the certified screening
   int joint_nslots, joint_nwork;   // mode 1 on the Gram form: sweep slots, slots this sweep
+  unsigned long long t_start, t_end;   // device clock (ns) at the fit's first / last kernel
 };
 
 struct Buffer {
@@ -133,7 +134,7 @@ struct Workspace {
 // (ev[8], ev[9], the roofline's denominator); the other phase times read -1 after a replay.
 cudaError_t ev_record(const Workspace& W, cudaEvent_t e, cudaStream_t s) {
   if (!W.capturing) return cudaEventRecord(e, s);
-  if (e != W.ev[0] && e != W.ev[4] && e != W.ev[8] && e != W.ev[9]) return cudaSuccess;
+  if (e != W.ev[8] && e != W.ev[9]) return cudaSuccess;   // (ms_total: the device clock)
   return cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
 }
 
@@ -318,7 +319,8 @@ int run_tail(Workspace& W, const Layout& L, int64_t cb, double lambda0, double t
 int run_prep(Workspace& W, const double* dX, int64_t m, const spmesl_options& o, const Layout& L,
              cudaStream_t s, bool band = true, const S16Prep* y16 = nullptr) {
   CUDA_TRY(launch_reset(W.counters.ptr, (int)sizeof(DevCounters), (int)offsetof(DevCounters, bad_key),
-                        (int*)W.queue.ptr, (int*)W.nz_count.ptr, (int*)W.nz_cur.ptr, m, s));
+                        (int)offsetof(DevCounters, t_start), (int*)W.queue.ptr,
+                        (int*)W.nz_count.ptr, (int*)W.nz_cur.ptr, m, s));
   CUDA_TRY(ev_record(W, W.ev[0], s));
   DevCounters* dc = (DevCounters*)W.counters.ptr;
   CUDA_TRY(launch_standardize(dX, L, o.standardize, (double*)W.xb.ptr, (double*)W.mean.ptr,
@@ -479,7 +481,7 @@ int device_stats(Workspace& W, const int32_t* dIters, const int32_t* dSweeps, co
   DevCounters* dc = (DevCounters*)W.counters.ptr;
   // (st_* start at zero: every fit resets the whole counter block in run_prep)
   CUDA_TRY(launch_column_stats(dIters, dSweeps, dConv, m, &dc->st_sweeps, &dc->st_max_sweeps,
-                               &dc->st_max_outer, &dc->st_unconv, s));
+                               &dc->st_max_outer, &dc->st_unconv, s, &dc->t_end));
   return SPMESL_OK;
 }
 
@@ -1151,7 +1153,11 @@ void finish_stats(Workspace& W, int64_t p, spmesl_stats* st, int* any_unconv, in
     st->ms_standardize = replay ? -1.0 : ev_ms(W.ev[0], W.ev[1]);
     st->ms_cd = replay ? -1.0 : ev_ms(W.ev[1], W.ev[2]);
     st->ms_assemble = replay ? -1.0 : ev_ms(W.ev[3], W.ev[4]);
-    st->ms_total = ev_ms(W.ev[0], W.ev[4]);
+    // (the device clock from the fit's first kernel to its statistics kernel: no timing-event
+    // nodes needed in a captured fit)
+    const DevCounters& hc = *W.host_counters;
+    st->ms_total = hc.t_end > hc.t_start ? (double)(hc.t_end - hc.t_start) * 1e-6
+                                         : ev_ms(W.ev[0], W.ev[4]);
     st->kernel_launches += launches;   // (+ the solver kernels, counted by the solver)
     st->bad_column = -1;
   }

@@ -456,11 +456,18 @@ cudaError_t launch_assemble_lists(int64_t p, const int* nz_count, const int* nz_
   return cudaGetLastError();
 }
 
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // Per-column statistics on the device (no host copy of iters/sweeps/converged):
 // out[0] += sum sweeps (64-bit), out[2] = max sweeps, out[3] = max iters, out[4] += unconverged.
 __global__ void column_stats_kernel(const int32_t* __restrict__ iters, const int32_t* __restrict__ sweeps,
                                     const uint8_t* __restrict__ conv, int64_t m,
-                                    unsigned long long* tot, int* mx_sweeps, int* mx_outer, int* nunc) {
+                                    unsigned long long* tot, int* mx_sweeps, int* mx_outer, int* nunc,
+                                    unsigned long long* t_end) {
   unsigned long long t = 0;
   int ms = 0, mo = 0, nu = 0;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m;
@@ -481,15 +488,17 @@ __global__ void column_stats_kernel(const int32_t* __restrict__ iters, const int
     atomicMax(mx_sweeps, ms);
     atomicMax(mx_outer, mo);
     if (nu) atomicAdd(nunc, nu);
+    if (t_end) atomicMax(t_end, global_ns());   // the fit's end (ms_total)
   }
 }
 
 cudaError_t launch_column_stats(const int32_t* iters, const int32_t* sweeps, const uint8_t* conv,
                                 int64_t m, unsigned long long* tot, int* mx_sweeps, int* mx_outer,
-                                int* nunc, cudaStream_t s) {
+                                int* nunc, cudaStream_t s, unsigned long long* t_end) {
   if (m <= 0) return cudaSuccess;
   const int blocks = (int)std::min<int64_t>(64, (m + 255) / 256);
-  column_stats_kernel<<<blocks, 256, 0, s>>>(iters, sweeps, conv, m, tot, mx_sweeps, mx_outer, nunc);
+  column_stats_kernel<<<blocks, 256, 0, s>>>(iters, sweeps, conv, m, tot, mx_sweeps, mx_outer, nunc,
+                                             t_end);
   return cudaGetLastError();
 }
 
@@ -532,22 +541,31 @@ __global__ void __launch_bounds__(32) zero_fill_bulk_kernel(double* __restrict__
 // Per-fit scratch reset in one launch (instead of five memsets): the counter block (zeros,
 // with the 8-byte bad-column key at key_off set to all ones), the 16-byte work queue and the
 // per-slot list counters nz_count / nz_cur.
-__global__ void reset_kernel(unsigned char* counters, int counters_bytes, int key_off, int* queue,
-                             int* nz_count, int* nz_cur, int64_t m) {
+// (also stamps the fit's start, t_off: the device-side clock of ms_total, so that a captured
+// fit needs no timing-event nodes for it; the counter block is <= 256 bytes, so block 0 alone
+// resets it and the stamp cannot be overwritten)
+__global__ void reset_kernel(unsigned char* counters, int counters_bytes, int key_off, int t_off,
+                             int* queue, int* nz_count, int* nz_cur, int64_t m) {
+  const unsigned long long t0 = global_ns();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = t; i < counters_bytes; i += stride)
     counters[i] = (i >= key_off && i < key_off + 8) ? 0xff : 0;
   if (t < 4) queue[t] = 0;
   for (int64_t i = t; i < m; i += stride) { nz_count[i] = 0; nz_cur[i] = 0; }
+  if (blockIdx.x == 0) {
+    __syncthreads();
+    if (threadIdx.x == 0) *(unsigned long long*)(counters + t_off) = t0;
+  }
 }
 
-cudaError_t launch_reset(void* counters, int counters_bytes, int key_off, int* queue, int* nz_count,
-                         int* nz_cur, int64_t m, cudaStream_t s) {
+cudaError_t launch_reset(void* counters, int counters_bytes, int key_off, int t_off, int* queue,
+                         int* nz_count, int* nz_cur, int64_t m, cudaStream_t s) {
+  if (counters_bytes > 256) return cudaErrorInvalidValue;   // (block 0 resets it alone)
   const int64_t work = std::max<int64_t>(m, counters_bytes);
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(296, (work + 255) / 256));
-  reset_kernel<<<blocks, 256, 0, s>>>((unsigned char*)counters, counters_bytes, key_off, queue,
-                                      nz_count, nz_cur, m);
+  reset_kernel<<<blocks, 256, 0, s>>>((unsigned char*)counters, counters_bytes, key_off, t_off,
+                                      queue, nz_count, nz_cur, m);
   return cudaGetLastError();
 }
 

@@ -283,11 +283,11 @@ cudaError_t launch_assemble_coo(int64_t p, const int64_t* col_ptr, const int32_t
                                 int* coo_count, double* diag, double* sigma_out, cudaStream_t s);
 cudaError_t launch_column_stats(const int32_t* iters, const int32_t* sweeps, const uint8_t* conv,
                                 int64_t m, unsigned long long* tot, int* mx_sweeps, int* mx_outer,
-                                int* nunc, cudaStream_t s);
+                                int* nunc, cudaStream_t s, unsigned long long* t_end = nullptr);
 cudaError_t launch_zero_fill(double* a, size_t count, int sms, cudaStream_t s);
 cudaError_t launch_zero_fill_bulk(double* a, size_t count, int grid, cudaStream_t s);
-cudaError_t launch_reset(void* counters, int counters_bytes, int key_off, int* queue, int* nz_count,
-                         int* nz_cur, int64_t m, cudaStream_t s);
+cudaError_t launch_reset(void* counters, int counters_bytes, int key_off, int t_off, int* queue,
+                         int* nz_count, int* nz_cur, int64_t m, cudaStream_t s);
 cudaError_t launch_csc_counts(const int* nz_count, int ncols, int32_t* out, cudaStream_t s);
 cudaError_t launch_sparse_count(int64_t p, const int* cnt, const int* cur, const int* nz_rows,
                                 const double* nz_vals, int nzcap, int symmetrize, int* ccount,
