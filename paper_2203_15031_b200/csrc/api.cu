@@ -317,10 +317,12 @@ int run_tail(Workspace& W, const Layout& L, int64_t cb, double lambda0, double t
 // (Xb's padding is written by the standardization itself; y16: the certified screening's
 // operands, written by the same kernel)
 int run_prep(Workspace& W, const double* dX, int64_t m, const spmesl_options& o, const Layout& L,
-             cudaStream_t s, bool band = true, const S16Prep* y16 = nullptr) {
+             cudaStream_t s, bool band = true, const S16Prep* y16 = nullptr,
+             void* z0 = nullptr, size_t z0_bytes = 0, void* z1 = nullptr, size_t z1_bytes = 0) {
   CUDA_TRY(launch_reset(W.counters.ptr, (int)sizeof(DevCounters), (int)offsetof(DevCounters, bad_key),
                         (int)offsetof(DevCounters, t_start), (int*)W.queue.ptr,
-                        (int*)W.nz_count.ptr, (int*)W.nz_cur.ptr, m, s));
+                        (int*)W.nz_count.ptr, (int*)W.nz_cur.ptr, m, s, z0, z0_bytes, z1,
+                        z1_bytes));
   CUDA_TRY(ev_record(W, W.ev[0], s));
   DevCounters* dc = (DevCounters*)W.counters.ptr;
   CUDA_TRY(launch_standardize(dX, L, o.standardize, (double*)W.xb.ptr, (double*)W.mean.ptr,
@@ -675,8 +677,11 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
     yprep.sq = sqv; yprep.inv_sq = inv_sq; yprep.lam_n = lam_n;
     yprep.lambda0 = lam_screen;
   }
-  if ((rc = run_prep(W, dX, m * nlam, o, L, s, /*band=*/false, screen16 ? &yprep : nullptr))) return rc;
-  CUDA_TRY(cudaMemsetAsync(W.hit.ptr, 0, (size_t)p * nlam, s));
+  // (the reset kernel also clears the screening flags and the candidate flags)
+  if ((rc = run_prep(W, dX, m * nlam, o, L, s, /*band=*/false, screen16 ? &yprep : nullptr,
+                     W.hit.ptr, (size_t)p * nlam, screen16 ? W.cand.ptr : nullptr,
+                     screen16 ? (size_t)p : 0)))
+    return rc;
   {
     double lv[SPMESL_MAX_LAM];
     for (int l = 0; l < nlam; ++l) lv[l] = nlam > 1 ? lams[l] : lambda0;
@@ -720,7 +725,7 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
     // certified f16 screening (screen16.cu): candidate columns, then their exact FP64 Gram
     // columns and the exact decision; one host round trip for the candidate list
     // (y16 operands and threshold factors were written by the standardization)
-    CUDA_TRY(cudaMemsetAsync(W.cand.ptr, 0, (size_t)p, s));
+
     Screen16Params Q{};
     Q.Y16 = (const __half*)W.y16.ptr;
     Q.sq = sqv;
@@ -780,8 +785,9 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
     }
     CUDA_TRY(launch_gram_cols((const double*)W.xb.ptr, (int)L.nblk, L.nchunk, (int)n, (int)p,
                               (const int*)W.uvars.ptr, 0, nU_dev, W.sms, (double*)W.ondemand.ptr,
-                              (uint8_t*)W.hit.ptr, (const double*)W.lam_dev.ptr, nlam,
-                              (int*)W.umap.ptr, s));
+                              (uint8_t*)W.hit.ptr,
+                              nlam > 1 ? (const double*)W.lam_dev.ptr : nullptr, nlam,
+                              (int*)W.umap.ptr, s, /*fallback=*/true, lambda0));
     launches += 3 + (nlam > 1);
     CUDA_TRY(ev_record(W, W.ev[7], s));
   } else {

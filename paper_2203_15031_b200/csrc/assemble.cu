@@ -545,7 +545,8 @@ __global__ void __launch_bounds__(32) zero_fill_bulk_kernel(double* __restrict__
 // fit needs no timing-event nodes for it; the counter block is <= 256 bytes, so block 0 alone
 // resets it and the stamp cannot be overwritten)
 __global__ void reset_kernel(unsigned char* counters, int counters_bytes, int key_off, int t_off,
-                             int* queue, int* nz_count, int* nz_cur, int64_t m) {
+                             int* queue, int* nz_count, int* nz_cur, int64_t m, uint8_t* z0,
+                             size_t z0_bytes, uint8_t* z1, size_t z1_bytes) {
   const unsigned long long t0 = global_ns();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -553,6 +554,8 @@ __global__ void reset_kernel(unsigned char* counters, int counters_bytes, int ke
     counters[i] = (i >= key_off && i < key_off + 8) ? 0xff : 0;
   if (t < 4) queue[t] = 0;
   for (int64_t i = t; i < m; i += stride) { nz_count[i] = 0; nz_cur[i] = 0; }
+  for (int64_t i = t; i < (int64_t)z0_bytes; i += stride) z0[i] = 0;
+  for (int64_t i = t; i < (int64_t)z1_bytes; i += stride) z1[i] = 0;
   if (blockIdx.x == 0) {
     __syncthreads();
     if (threadIdx.x == 0) *(unsigned long long*)(counters + t_off) = t0;
@@ -560,12 +563,15 @@ __global__ void reset_kernel(unsigned char* counters, int counters_bytes, int ke
 }
 
 cudaError_t launch_reset(void* counters, int counters_bytes, int key_off, int t_off, int* queue,
-                         int* nz_count, int* nz_cur, int64_t m, cudaStream_t s) {
+                         int* nz_count, int* nz_cur, int64_t m, cudaStream_t s, void* z0,
+                         size_t z0_bytes, void* z1, size_t z1_bytes) {
   if (counters_bytes > 256) return cudaErrorInvalidValue;   // (block 0 resets it alone)
-  const int64_t work = std::max<int64_t>(m, counters_bytes);
+  const int64_t work = std::max<int64_t>(std::max<int64_t>(m, counters_bytes),
+                                         (int64_t)std::max(z0_bytes, z1_bytes));
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(296, (work + 255) / 256));
   reset_kernel<<<blocks, 256, 0, s>>>((unsigned char*)counters, counters_bytes, key_off, t_off,
-                                      queue, nz_count, nz_cur, m);
+                                      queue, nz_count, nz_cur, m, (uint8_t*)z0, z0_bytes,
+                                      (uint8_t*)z1, z1_bytes);
   return cudaGetLastError();
 }
 

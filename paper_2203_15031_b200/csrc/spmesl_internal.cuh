@@ -221,7 +221,7 @@ cudaError_t launch_tail_residuals(const double* Xb, const TailState* tail, int M
 cudaError_t launch_gram_cols(const double* Xb, int nblk, int nchunk, int n, int p, const int* U,
                              int nU, const int* nU_dev, int sms, double* Gtab, uint8_t* hit,
                              const double* lams, int nlam, int* gstate, cudaStream_t s,
-                             bool fallback = true);
+                             bool fallback = true, double lam1 = 0.0);   // lams == nullptr: lam1
 // hit (optional): hit[l p + c] = 1 for every candidate c = U[.] with some |G_jc| > lams[l], j != c
 // (hit must be zeroed first; only ones are written)
 cudaError_t launch_gram_pass(const double* Xb, int nblk, int nchunk, int n, int p, const double* V,
@@ -286,8 +286,11 @@ cudaError_t launch_column_stats(const int32_t* iters, const int32_t* sweeps, con
                                 int* nunc, cudaStream_t s, unsigned long long* t_end = nullptr);
 cudaError_t launch_zero_fill(double* a, size_t count, int sms, cudaStream_t s);
 cudaError_t launch_zero_fill_bulk(double* a, size_t count, int grid, cudaStream_t s);
+// (z0 / z1: optional extra byte ranges to zero in the same launch)
 cudaError_t launch_reset(void* counters, int counters_bytes, int key_off, int t_off, int* queue,
-                         int* nz_count, int* nz_cur, int64_t m, cudaStream_t s);
+                         int* nz_count, int* nz_cur, int64_t m, cudaStream_t s,
+                         void* z0 = nullptr, size_t z0_bytes = 0, void* z1 = nullptr,
+                         size_t z1_bytes = 0);
 cudaError_t launch_csc_counts(const int* nz_count, int ncols, int32_t* out, cudaStream_t s);
 cudaError_t launch_sparse_count(int64_t p, const int* cnt, const int* cur, const int* nz_rows,
                                 const double* nz_vals, int nzcap, int symmetrize, int* ccount,

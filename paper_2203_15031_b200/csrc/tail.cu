@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(GC_MAXW * 32, 1) gram_cols_kernel(const double
                                                                  uint8_t* __restrict__ hit,
                                                                  const double* __restrict__ lams,
                                                                  int nlam, int* __restrict__ gstate,
-                                                                 int fallback) {
+                                                                 int fallback, double lam1) {
   extern __shared__ __align__(128) double gsm[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nthr = blockDim.x;
   const int T = nthr >> 5;
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(GC_MAXW * 32, 1) gram_cols_kernel(const double
               Gtab[(size_t)c * p + row] = g_rc;
               if (hit && row != c)   // exact screening decision: some |S_jc| > lambda, j != c
                 for (int l = 0; l < nlam; ++l)
-                  if (fabs(g_rc) > lams[l]) hit[(size_t)l * p + c] = 1;
+                  if (fabs(g_rc) > (lams ? lams[l] : lam1)) hit[(size_t)l * p + c] = 1;
             }
           }
       }
@@ -644,7 +644,7 @@ cudaError_t launch_tail_residuals(const double* Xb, const TailState* tail, int M
 cudaError_t launch_gram_cols(const double* Xb, int nblk, int nchunk, int n, int p, const int* U,
                              int nU, const int* nU_dev, int sms, double* Gtab, uint8_t* hit,
                              const double* lams, int nlam, int* gstate, cudaStream_t s,
-                             bool fallback) {
+                             bool fallback, double lam1) {
   if (!nU_dev && nU <= 0) return cudaSuccess;
   if (sms <= 0) {
     int dev = 0;
@@ -670,7 +670,7 @@ cudaError_t launch_gram_cols(const double* Xb, int nblk, int nchunk, int n, int 
     if (e != cudaSuccess) return e;
   }
   gram_cols_kernel<<<grid, T * 32, smem, s>>>(Xb, nchunk, n, p, U, nU, nU_dev, Gtab, hit, lams,
-                                             nlam, gstate, fallback ? 1 : 0);
+                                             nlam, gstate, fallback ? 1 : 0, lam1);
   return cudaGetLastError();
 }
 
