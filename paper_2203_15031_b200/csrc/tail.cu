@@ -190,7 +190,11 @@ __global__ void __launch_bounds__(256) gram_pass_kernel(const double* __restrict
 // sample), so every caller sees bit-identical columns.  Optional exact screening decision as
 // in gram_tile.
 constexpr int GC_NTMAX = 16;            // n-tiles of 8 vectors per vector group (128 columns)
-constexpr int GC_STAGES = 3;            // 3 x (34 + 32) KB at 17 warps
+constexpr int GC_STAGES = 3;
+#ifndef SPMESL_GC_GROUP
+#define SPMESL_GC_GROUP 3
+#endif
+constexpr int GC_GROUP = SPMESL_GC_GROUP;   // n-tiles per group of independent DMMAs            // 3 x (34 + 32) KB at 17 warps
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
@@ -277,19 +281,19 @@ __global__ void __launch_bounds__(GC_MAXW * 32, 1) gram_cols_kernel(const double
             // groups of 4 n-tiles: the even samples of the group, then the odd ones — per
             // output the chain is unchanged (even then odd), consecutive DMMAs are independent
 #pragma unroll
-            for (int t0 = 0; t0 < GC_NTMAX; t0 += 4) {
+            for (int t0 = 0; t0 < GC_NTMAX; t0 += GC_GROUP) {
               if (t0 < ntc) {
-                double2 b2[4];
+                double2 b2[GC_GROUP];
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-                  if (t0 + u < ntc)
+                for (int u = 0; u < GC_GROUP; ++u)
+                  if (t0 + u < ntc && t0 + u < GC_NTMAX)
                     b2[u] = *(const double2*)(sv + ((t0 + u) * 8 + g) * XS + 2 * t4 + (kp ^ sw) * 8);
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-                  if (t0 + u < ntc) dmma_t(acc[t0 + u][0], acc[t0 + u][1], a.x, b2[u].x);
+                for (int u = 0; u < GC_GROUP; ++u)
+                  if (t0 + u < ntc && t0 + u < GC_NTMAX) dmma_t(acc[t0 + u][0], acc[t0 + u][1], a.x, b2[u].x);
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-                  if (t0 + u < ntc) dmma_t(acc[t0 + u][0], acc[t0 + u][1], a.y, b2[u].y);
+                for (int u = 0; u < GC_GROUP; ++u)
+                  if (t0 + u < ntc && t0 + u < GC_NTMAX) dmma_t(acc[t0 + u][0], acc[t0 + u][1], a.y, b2[u].y);
               }
             }
           }
