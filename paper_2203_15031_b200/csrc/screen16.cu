@@ -297,7 +297,7 @@ constexpr int T5_THREADS = (2 + T5_EPI_WARPS) * 32;
 
 template <int BN>
 #ifndef SPMESL_T5_NST
-#define SPMESL_T5_NST 4
+#define SPMESL_T5_NST 3
 #endif
 __host__ __device__ constexpr int t5_nst() { return BN == 256 ? SPMESL_T5_NST : 4; }
 template <int BN>
