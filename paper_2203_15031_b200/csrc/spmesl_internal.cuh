@@ -205,7 +205,8 @@ cudaError_t launch_gram_init(const GramParams& P, cudaStream_t s);
 cudaError_t launch_level_flags(const GramParams& P, cudaStream_t s);
 int gram_tile_count(int64_t p);
 
-constexpr int TAIL_THREADS = 256;
+constexpr int TAIL_THREADS = 256;   // (the sweep kernel also runs with 512: TAIL_MAXW warps)
+constexpr int TAIL_MAXW = 16;
 #ifndef SPMESL_TAIL_SCAN_R
 #define SPMESL_TAIL_SCAN_R 4
 #endif

@@ -126,6 +126,7 @@ __device__ __forceinline__ void gram_tile(const double* Xb, int b, int nchunk, i
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t4 = lane & 3, sw = g & 1;
   const int mt = warp & 3, nt0 = (warp >> 2) * 2;
+  const bool mma_warp = warp < 8;   // (8 warps own the 32 x 32 output tile; more only load)
   double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
   for (int q = 0; q < nchunk; ++q) {
     const double2* src = (const double2*)(Xb + ((size_t)b * nchunk + q) * CHUNK_DOUBLES);
@@ -134,18 +135,21 @@ __device__ __forceinline__ void gram_tile(const double* Xb, int b, int nchunk, i
       load_vec_chunk(tv, vr, vt * 32 + vr, q, lane, Xb, nchunk, V, M, U, nU, n_pad);
     bsync();
     const double* xa = tx + (mt * 8 + g) * XS + 2 * t4;
+    if (mma_warp) {
 #pragma unroll
-    for (int kp = 0; kp < KC / 8; ++kp) {
-      const double2 a = *(const double2*)(xa + (kp ^ sw) * 8);
+      for (int kp = 0; kp < KC / 8; ++kp) {
+        const double2 a = *(const double2*)(xa + (kp ^ sw) * 8);
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const double2 bb = *(const double2*)(tv + ((nt0 + u) * 8 + g) * XS + 2 * t4 + (kp ^ sw) * 8);
-        dmma_t(acc[u][0], acc[u][1], a.x, bb.x);
-        dmma_t(acc[u][0], acc[u][1], a.y, bb.y);
+        for (int u = 0; u < 2; ++u) {
+          const double2 bb = *(const double2*)(tv + ((nt0 + u) * 8 + g) * XS + 2 * t4 + (kp ^ sw) * 8);
+          dmma_t(acc[u][0], acc[u][1], a.x, bb.x);
+          dmma_t(acc[u][0], acc[u][1], a.y, bb.y);
+        }
       }
     }
     bsync();
   }
+  if (!mma_warp) return;
   const double inv_n = 1.0 / (double)n;
   const int row = b * J + mt * 8 + g;
 #pragma unroll
@@ -335,8 +339,8 @@ __global__ void tail_mark_kernel(const TailState* __restrict__ tail, int M, cons
 struct TailShared {
   uint64_t pf_bar[2];    // prefetch buffers' mbarriers
   uint64_t z_bar;        // z <- G[:, c] bulk copy
-  double red[TAIL_THREADS / 32];
-  int wmin[2][TAIL_THREADS / 32];   // per-warp first hits, double-buffered across rounds
+  double red[TAIL_MAXW];
+  int wmin[2][TAIL_MAXW];   // per-warp first hits, double-buffered across rounds
   int oc_var[TAIL_ODC];
   int oc_next;
   int k;
@@ -380,7 +384,9 @@ __device__ void ensure_gram_column(const TailParams& P, int j, TailShared& TS, d
   bsync();
 }
 
-__global__ void __launch_bounds__(TAIL_THREADS, 2) tail_sweep_kernel(const TailParams P) {
+template <int NT>
+__global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) tail_sweep_kernel(const TailParams P) {
+  constexpr int TSCAN = SPMESL_TAIL_SCAN_R * NT;   // rows tested per search round
   extern __shared__ __align__(128) unsigned char sm[];
   const int p = P.p, n = P.n, n_pad = P.n_pad, nchunk = P.nchunk, nzcap = P.nzcap;
   double* tx = (double*)sm;                                  // [J*XS]
@@ -456,26 +462,26 @@ __global__ void __launch_bounds__(TAIL_THREADS, 2) tail_sweep_kernel(const TailP
         bsync();
       } else
       // (16 independent L2 loads in flight per thread: the column is 8p bytes)
-      for (int j0 = 0; j0 < p; j0 += 16 * TAIL_THREADS) {
+      for (int j0 = 0; j0 < p; j0 += 16 * NT) {
         constexpr int UB = 16;
         double gv[UB];
 #pragma unroll
         for (int u = 0; u < UB; ++u) {
-          const int j = j0 + u * TAIL_THREADS + tid;
+          const int j = j0 + u * NT + tid;
           gv[u] = j < p ? __ldcs(gz + j) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < UB; ++u) {
-          const int j = j0 + u * TAIL_THREADS + tid;
+          const int j = j0 + u * NT + tid;
           if (j < p) z[j] = gv[u];
         }
       }
     } else {
-      for (int j = tid; j < p; j += TAIL_THREADS) z[j] = P.Zz[(size_t)k * p + j];
+      for (int j = tid; j < p; j += NT) z[j] = P.Zz[(size_t)k * p + j];
     }
     {
       const size_t lo = (size_t)col * list_stride + (size_t)cur * nzcap;
-      for (int m = tid; m < ocnt; m += TAIL_THREADS) { orow[m] = P.nz_rows[lo + m]; ov[m] = P.nz_vals[lo + m]; }
+      for (int m = tid; m < ocnt; m += NT) { orow[m] = P.nz_rows[lo + m]; ov[m] = P.nz_vals[lo + m]; }
     }
     bsync();
     bool retire = false;
@@ -491,18 +497,18 @@ __global__ void __launch_bounds__(TAIL_THREADS, 2) tail_sweep_kernel(const TailP
       for (;;) {
         const int na = cursor < ocnt ? orow[cursor] : p;     // next row with b_j != 0
         // first row in [pos, na) with |z_j| > lambda (j != this column)
-        // (rounds of TAIL_SCAN rows: thread t tests rows base + t + TAIL_THREADS r,
-        // r < TAIL_SCAN / TAIL_THREADS; the first hit is the block-wide minimum of the hit rows;
+        // (rounds of TSCAN rows: thread t tests rows base + t + NT r,
+        // r < TSCAN / NT; the first hit is the block-wide minimum of the hit rows;
         // one barrier per round: the per-warp minima alternate between two buffers, and a
         // buffer is rewritten only after the next round's barrier, which every reader of it
         // has passed)
         int j = na;
         int rbuf = 0;
-        for (int base = pos; base < na; base += TAIL_SCAN, rbuf ^= 1) {
+        for (int base = pos; base < na; base += TSCAN, rbuf ^= 1) {
           int my = 0x7fffffff;
 #pragma unroll
-          for (int r = TAIL_SCAN / TAIL_THREADS - 1; r >= 0; --r) {
-            const int jj = base + tid + r * TAIL_THREADS;
+          for (int r = TSCAN / NT - 1; r >= 0; --r) {
+            const int jj = base + tid + r * NT;
             if (jj < na && jj != gc && fabs(z[jj]) > lam) my = jj;
           }
           my = __reduce_min_sync(0xffffffffu, my);
@@ -510,7 +516,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 2) tail_sweep_kernel(const TailP
           bsync();
           int best = 0x7fffffff;
 #pragma unroll
-          for (int w = 0; w < TAIL_THREADS / 32; ++w) best = min(best, TS.wmin[rbuf][w]);
+          for (int w = 0; w < NT / 32; ++w) best = min(best, TS.wmin[rbuf][w]);
           if (best != 0x7fffffff) { j = best; break; }
         }
         if (j >= p) break;
@@ -544,23 +550,23 @@ __global__ void __launch_bounds__(TAIL_THREADS, 2) tail_sweep_kernel(const TailP
         if (d != 0.0 && pfb >= 0) {
           maxd = fmax(maxd, fabs(d));
           const double* gs = gbuf + (size_t)pfb * p;          // G[:, j] in shared memory
-          for (int t = tid; t < p; t += TAIL_THREADS) z[t] = fma(d, gs[t], z[t]);
+          for (int t = tid; t < p; t += NT) z[t] = fma(d, gs[t], z[t]);
         } else if (d != 0.0) {
           maxd = fmax(maxd, fabs(d));
           const double* gcol = P.Gtab + (size_t)j * p;
           ensure_gram_column(P, j, TS, tx, tvv);
           // (up to 16 independent L2 loads in flight per thread: one round trip per 4096 rows)
           constexpr int UB = 16;
-          for (int t0 = 0; t0 < p; t0 += UB * TAIL_THREADS) {
+          for (int t0 = 0; t0 < p; t0 += UB * NT) {
             double gv[UB];
 #pragma unroll
             for (int u = 0; u < UB; ++u) {
-              const int t = t0 + u * TAIL_THREADS + tid;
+              const int t = t0 + u * NT + tid;
               gv[u] = t < p ? __ldcg(gcol + t) : 0.0;
             }
 #pragma unroll
             for (int u = 0; u < UB; ++u) {
-              const int t = t0 + u * TAIL_THREADS + tid;
+              const int t = t0 + u * NT + tid;
               if (t < p) z[t] = fma(d, gv[u], z[t]);
             }
           }
@@ -572,7 +578,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 2) tail_sweep_kernel(const TailP
       ++sweeps;
       ++inner;
       // the new list becomes the current one
-      for (int m = tid; m < min(ncnt, nzcap); m += TAIL_THREADS) { orow[m] = nrow[m]; ov[m] = nv[m]; }
+      for (int m = tid; m < min(ncnt, nzcap); m += NT) { orow[m] = nrow[m]; ov[m] = nv[m]; }
       ocnt = min(ncnt, nzcap);
       if (ncnt > nzcap) overflow = true;
       bsync();
@@ -580,7 +586,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 2) tail_sweep_kernel(const TailP
         // one sweep per launch: publish max |db|, keep z and the state for the next launch
         if (tid == 0) atomicMax(P.joint_maxd, (unsigned long long)__double_as_longlong(maxd));
         double* zs = P.Zj + (size_t)slot * p;
-        for (int t = tid; t < p; t += TAIL_THREADS) zs[t] = z[t];
+        for (int t = tid; t < p; t += NT) zs[t] = z[t];
         break;
       }
       if (maxd < P.tol || inner >= P.max_inner) {
@@ -588,7 +594,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 2) tail_sweep_kernel(const TailP
         // fresh residual and sigma (reading g4): every thread builds its samples'
         // r_i = x~_ci - sum_m x~_{j_m i} b_m (m ascending, the CD kernel's per-element order),
         // then warp 0 sums r_i^2 in the CD kernel's order
-        for (int i = tid; i < n_pad; i += TAIL_THREADS) {
+        for (int i = tid; i < n_pad; i += NT) {
           double ri = P.Xb[xb_index(i, gc, nchunk)];
           for (int m = 0; m < ocnt; ++m) ri = fma(-P.Xb[xb_index(i, orow[m], nchunk)], ov[m], ri);
           r[i] = ri;
@@ -615,7 +621,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 2) tail_sweep_kernel(const TailP
     // outputs: coefficients into the column's other list, per-column results
     const int dst = cur ^ 1;
     const size_t lo = (size_t)col * list_stride + (size_t)dst * nzcap;
-    for (int m = tid; m < ocnt; m += TAIL_THREADS) { P.nz_rows[lo + m] = orow[m]; P.nz_vals[lo + m] = ov[m]; }
+    for (int m = tid; m < ocnt; m += NT) { P.nz_rows[lo + m] = orow[m]; P.nz_vals[lo + m] = ov[m]; }
     if (tid == 0) {
       P.nz_count[col] = ocnt;
       P.nz_cur[col] = dst;
@@ -705,10 +711,21 @@ cudaError_t launch_tail_sweeps(const TailParams& P, int grid, cudaStream_t s) {
   size_t smem = tail_smem_bytes(P.p, P.n_pad, P.nzcap);
   if (P.prefetch) smem += tail_prefetch_bytes(P.p);
   if (P.occ > 1) grid *= P.occ;   // several column CTAs per SM (set_prefetch)
-  cudaError_t e = cudaFuncSetAttribute(tail_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(tail_sweep_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  tail_sweep_kernel<<<grid, TAIL_THREADS, smem, s>>>(P);
+  // 512 threads when a single column CTA owns the SM (large p: the search rounds and the z
+  // updates split over twice the threads), 256 when two share it
+  static const int nt_env = getenv("SPMESL_TAIL_NT") ? atoi(getenv("SPMESL_TAIL_NT")) : 0;
+  const bool wide = nt_env ? nt_env == 512 : P.occ == 1;
+  if (wide) {
+    cudaError_t e2 = cudaFuncSetAttribute(tail_sweep_kernel<512>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e2 != cudaSuccess) return e2;
+    tail_sweep_kernel<512><<<grid, 512, smem, s>>>(P);
+  } else {
+    tail_sweep_kernel<256><<<grid, 256, smem, s>>>(P);
+  }
   return cudaGetLastError();
 }
 
