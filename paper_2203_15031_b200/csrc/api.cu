@@ -707,11 +707,12 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   G.ssq = (const double*)W.ssq.ptr;
   G.tile_begin = 0;
   G.tile_end = gram_tile_count(p);
-  if (W.pending_zero == nullptr && W.take_zero && (((uintptr_t)W.take_zero & 15) == 0) &&
-      (W.take_count & 1) == 0) {
-    // the Gram kernel's producer zero-fills Theta with bulk stores while it computes
+  if (W.pending_zero == nullptr && W.take_zero && (((uintptr_t)W.take_zero & 15) == 0)) {
+    // the Gram kernel's producer zero-fills Theta with bulk stores while it computes (16-byte
+    // pieces: an odd element count leaves the last double to one plain store)
     G.zero_ptr = W.take_zero;
-    G.zero_count = W.take_count;
+    G.zero_count = W.take_count & ~(size_t)1;
+    G.zero_last = (W.take_count & 1) ? W.take_zero + (W.take_count - 1) : nullptr;
   }
   G.tail = (TailState*)W.tail.ptr;
   G.tail_count = &dc->tail_count;
@@ -751,6 +752,7 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
     if (zfused > G.zero_count) zfused = G.zero_count;
     Q.zero_ptr = zfused ? G.zero_ptr : nullptr;
     Q.zero_count = zfused;
+    Q.zero_last = G.zero_last;
     if (getenv("SPMESL_DEV_S16_NOZERO")) { Q.zero_ptr = nullptr; Q.zero_count = 0; }   // (dev)
     W.screen_fill = (int64_t)Q.zero_count;
     CUDA_TRY(ev_record(W, W.ev[8], s));
@@ -1122,7 +1124,7 @@ int gram_fit_enqueue_all(Workspace& W, const double* dX, int64_t n, int64_t p, d
   // the screening kernel zero-fills Theta itself (bulk stores from its producer warp) when the
   // buffer allows 16-byte pieces; otherwise a side-stream kernel does, after standardization
   static const bool side_zero = getenv("SPMESL_DEV_SIDE_ZERO") != nullptr;   // (dev)
-  const bool take = !side_zero && (((uintptr_t)dTheta & 15) == 0) && (pp & 1) == 0;
+  const bool take = !side_zero && (((uintptr_t)dTheta & 15) == 0);
   if (take) { W.take_zero = dTheta; W.take_count = pp; }
   else { W.pending_zero = dTheta; W.pending_count = pp; }
   rc = fit_gram_enqueue(W, dX, n, p, lambda0, tol, max_iter, o, out, cs, L, nzcap, nullptr, 1,
@@ -1216,7 +1218,7 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
     // (no side-stream work may be captured: the fill must be the screening kernel's own)
     const bool use_graph = !no_graph && !o.eager && getenv("SPMESL_DEV_SIDE_ZERO") == nullptr &&
                            getenv("SPMESL_S16_ZFRAC") == nullptr && o.solver != 2 &&
-                           (((uintptr_t)dTheta & 15) == 0) && (((size_t)p * (size_t)p) & 1) == 0;
+                           (((uintptr_t)dTheta & 15) == 0);
     // the captured fit's list capacity if these are its arguments, else the initial one
     nzcap = initial_nzcap(n, p);
     if (W.gexec && W.graph_nzcap > 0 &&

@@ -106,6 +106,7 @@ __device__ __forceinline__ void tri_tile(int t, int nT, int& I, int& Jt) {
 __global__ void __launch_bounds__(G_THREADS, 1) syrk_screen_kernel(const GramParams P) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   if (P.cond_nU && 2 * (int64_t)*(volatile const int*)P.cond_nU <= P.p) return;
+  if (P.zero_last && blockIdx.x == 0 && threadIdx.x == 0) *P.zero_last = 0.0;
   uint64_t* full = (uint64_t*)smem_raw;
   uint64_t* empty = full + G_MAX_NST;
   double* Xs = (double*)(smem_raw + 128);

@@ -134,6 +134,7 @@ __device__ __forceinline__ void hmma(float (&c)[4], const uint32_t (&a)[4], uint
 }
 
 __global__ void __launch_bounds__(S16_THREADS, 1) screen16_kernel(const Screen16Params P) {
+  if (P.zero_last && blockIdx.x == 0 && threadIdx.x == 0) *P.zero_last = 0.0;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   uint64_t* full = (uint64_t*)smem_raw;
   uint64_t* empty = full + S16_NST;
@@ -331,6 +332,7 @@ __device__ __forceinline__ void t5_tile(int t, int nT, int& I, int& Jb) {
 
 template <int BN>
 __global__ void __launch_bounds__(T5_THREADS, 1) screen16_tc_kernel(const Screen16Params P) {
+  if (P.zero_last && blockIdx.x == 0 && threadIdx.x == 0) *P.zero_last = 0.0;
   constexpr int NBT = BN / 128;                    // B sub-tiles per stage
   constexpr int NST = t5_nst<BN>();
   constexpr int STAGE_HALVES = (1 + NBT) * S16_TILE_HALVES;

@@ -162,6 +162,7 @@ struct GramParams {
   int tile_begin, tile_end;   // upper-triangle tiles to process (multi-GPU share)
   double* zero_ptr;        // optional: zero-filled by the producer's bulk stores (Theta)
   size_t zero_count;       // doubles (even; zero_ptr 16-byte aligned)
+  double* zero_last;       // optional: one more double to zero (odd Theta sizes)
   const int* cond_nU;      // optional: run only if 2 * *cond_nU > p (solver 3 fallback)
   TailState* tail;         // columns for the sweep kernel
   int* tail_count;
@@ -187,6 +188,7 @@ struct Screen16Params {
   uint8_t* cand;           // [p] column may have a hit (must be checked exactly)
   double* zero_ptr;        // optional Theta zero fill (as GramParams)
   size_t zero_count;
+  double* zero_last;       // optional: one more double to zero (odd Theta sizes)
 };
 size_t screen16_y_halves(int64_t p, int n_pad);
 int screen16_tile_count(int64_t p);

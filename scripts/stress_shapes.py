@@ -26,8 +26,7 @@ for n, p in [(2, 5), (3, 40), (7, 129), (33, 255), (64, 257), (129, 513), (1100,
                    conv=torch.empty(p, dtype=torch.uint8, device="cuda"))
         for _ in range(3):
             g = S.fit_device(Xd, lam, out=out)
-        # (odd p: Theta cannot take 16-byte fill pieces, so the fit stays eager)
-        ok3 = torch.equal(g.Theta, b.Theta) and g.stats["graph_replay"] == (1 if p % 2 == 0 else 0)
+        ok3 = torch.equal(g.Theta, b.Theta) and g.stats["graph_replay"] == 1
         ora = O.spmesl_fit(X, lam, delta=1e-4)
         rep = compare(b.Theta.cpu().numpy(), b.sigma.cpu().numpy(), b.iters.cpu().numpy(), b.sweeps.cpu().numpy(), ora)
         try:
