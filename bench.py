@@ -293,6 +293,9 @@ def run_ours(args):
 
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    for e in ev0 + ev1:   # (torch creates CUDA events lazily at the first record: do it here,
+        e.record(stream)  # not between a timed step's end and its closing record)
+    torch.cuda.synchronize()
     cd_ms, updates, stats_last = [], 0, None
     # the clock sampler starts before the warm-up (its first nvidia-smi queries can stall the
     # GPU briefly) and its summary covers the timed steps
@@ -302,7 +305,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         clk.mark()
         for k in range(args.steps):
-            flush.fill_(k & 0xff)
+            flush.fill_(k % 255 + 1)   # (never 0: a zero fill may take a memset path)
             torch.cuda.synchronize()
             barrier()
             torch.cuda.synchronize()
@@ -445,7 +448,7 @@ def run_ours(args):
             e2e_step()
         e_ms = []
         for k in range(max(1, min(args.steps, 3))):
-            flush.fill_(k)
+            flush.fill_(k % 255 + 1)
             torch.cuda.synchronize()
             barrier()
             t0 = time.perf_counter()
