@@ -137,10 +137,12 @@ def fit_device(X, lambda0: float, tol: float = 1e-4, max_iter: int = 100, *, str
 
 
 def fit_sparse_device(X, lambda0: float, tol: float = 1e-4, max_iter: int = 100, *,
-                      stream=None, cap=None, **options) -> dict:
+                      stream=None, cap=None, out=None, **options) -> dict:
     """spmesl_fit_sparse_device: Theta in CSC form (col_ptr int64 [p+1], rows int32, vals
     float64; symmetric, so also CSR) without the dense p x p array, plus sigma / iters / sweeps
-    / converged.  cap: entry capacity (default p + 64 p; grown and retried once if short)."""
+    / converged.  cap: entry capacity (default p + 64 p; grown and retried once if short).
+    out (optional): preallocated col_ptr / rows / vals / sigma / iters / sweeps / conv tensors
+    (reused buffers let repeated fits replay their CUDA graph)."""
     import torch
     if not X.is_cuda or X.dtype != torch.float64:
         raise TypeError("X must be a float64 CUDA tensor")
@@ -149,15 +151,22 @@ def fit_sparse_device(X, lambda0: float, tol: float = 1e-4, max_iter: int = 100,
     dev = X.device
     s = stream if stream is not None else torch.cuda.current_stream(dev)
     o = _opts(**options)
+    if out is not None:
+        cap = out["rows"].numel()
     cap = int(cap) if cap is not None else p + 64 * p
-    col_ptr = torch.empty(p + 1, dtype=torch.int64, device=dev)
-    sigma = torch.empty(p, dtype=torch.float64, device=dev)
-    iters = torch.empty(p, dtype=torch.int32, device=dev)
-    sweeps = torch.empty(p, dtype=torch.int32, device=dev)
-    conv = torch.empty(p, dtype=torch.uint8, device=dev)
-    for _ in range(2):
-        rows = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
-        vals = torch.empty(max(cap, 1), dtype=torch.float64, device=dev)
+    out = out or {}
+    col_ptr = out.get("col_ptr", None)
+    col_ptr = col_ptr if col_ptr is not None else torch.empty(p + 1, dtype=torch.int64, device=dev)
+    sigma = out["sigma"] if "sigma" in out else torch.empty(p, dtype=torch.float64, device=dev)
+    iters = out["iters"] if "iters" in out else torch.empty(p, dtype=torch.int32, device=dev)
+    sweeps = out["sweeps"] if "sweeps" in out else torch.empty(p, dtype=torch.int32, device=dev)
+    conv = out["conv"] if "conv" in out else torch.empty(p, dtype=torch.uint8, device=dev)
+    for attempt in range(2):
+        if attempt == 0 and "rows" in out and "vals" in out:
+            rows, vals = out["rows"], out["vals"]
+        else:
+            rows = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+            vals = torch.empty(max(cap, 1), dtype=torch.float64, device=dev)
         nnz = ctypes.c_int64(0)
         st = Stats()
         with torch.cuda.device(dev):

@@ -119,6 +119,9 @@ struct Workspace {
   std::vector<unsigned char> gkey;        // arguments of the captured graph
   std::vector<unsigned char> last_key;    // arguments of the previous eager device-path fit
   int graph_nzcap = 0;                    // coefficient-list capacity the graph was built for
+  // sparse-output fit (spmesl_fit_sparse_device): Theta as CSC instead of the dense array
+  struct SparseOut { int64_t* col_ptr; int32_t* rows; double* vals; int64_t cap; };
+  const SparseOut* sparse = nullptr;
   int64_t graph_screen_fill = 0;          // host-side facts of the captured fit (for its stats)
   int graph_launches = 0;
   bool zero_join = false;     // part of Theta's zero fill runs on `side` (join ev_join)
@@ -1124,9 +1127,10 @@ int gram_fit_enqueue_all(Workspace& W, const double* dX, int64_t n, int64_t p, d
   // the screening kernel zero-fills Theta itself (bulk stores from its producer warp) when the
   // buffer allows 16-byte pieces; otherwise a side-stream kernel does, after standardization
   static const bool side_zero = getenv("SPMESL_DEV_SIDE_ZERO") != nullptr;   // (dev)
-  const bool take = !side_zero && (((uintptr_t)dTheta & 15) == 0);
+  const bool sparse = W.sparse != nullptr;   // (CSC output: no dense Theta, no fill)
+  const bool take = !sparse && !side_zero && (((uintptr_t)dTheta & 15) == 0);
   if (take) { W.take_zero = dTheta; W.take_count = pp; }
-  else { W.pending_zero = dTheta; W.pending_count = pp; }
+  else if (!sparse) { W.pending_zero = dTheta; W.pending_count = pp; }
   rc = fit_gram_enqueue(W, dX, n, p, lambda0, tol, max_iter, o, out, cs, L, nzcap, nullptr, 1,
                         o.solver != 2);
   W.take_zero = nullptr;
@@ -1134,18 +1138,35 @@ int gram_fit_enqueue_all(Workspace& W, const double* dX, int64_t n, int64_t p, d
     W.pending_zero = nullptr;
     if (!rc) rc = fail(SPMESL_ERR_CUDA, "internal: Theta zero fill was not launched");
   }
-  const bool join = !take || W.zero_join;
+  const bool join = (!take && !sparse) || W.zero_join;
   W.zero_join = false;
   if (rc) { if (join) cudaStreamWaitEvent(cs, W.ev_join, 0); return rc; }
   if (join) CUDA_TRY(cudaStreamWaitEvent(cs, W.ev_join, 0));
   DevCounters* dc = (DevCounters*)W.counters.ptr;
   CUDA_TRY(ev_record(W, W.ev[3], cs));
-  // assembly + symmetrization straight from the coefficient lists (no CSC packing)
-  CUDA_TRY(launch_assemble_lists(p, (const int*)W.nz_count.ptr, (const int*)W.nz_cur.ptr,
+  if (sparse) {
+    // Theta as CSC: entries per column, scan, then the entries (skipped on the device when
+    // they would exceed the caller's capacity; the host reports the count)
+    if ((rc = ensure(W.ccount, (size_t)p * 4))) return rc;
+    CUDA_TRY(launch_sparse_count(p, (const int*)W.nz_count.ptr, (const int*)W.nz_cur.ptr,
+                                 (const int*)W.nz_rows.ptr, (const double*)W.nz_vals.ptr, nzcap,
+                                 o.symmetrize, (int*)W.ccount.ptr, cs));
+    CUDA_TRY(launch_csc_scan((const int*)W.ccount.ptr, (int)p, W.sparse->col_ptr, &dc->csc_total,
+                             cs));
+    CUDA_TRY(launch_sparse_write(p, (const int*)W.nz_count.ptr, (const int*)W.nz_cur.ptr,
                                  (const int*)W.nz_rows.ptr, (const double*)W.nz_vals.ptr, nzcap,
                                  (const double*)W.sigma_std.ptr,
                                  o.standardize ? (const double*)W.scale.ptr : nullptr,
-                                 o.symmetrize, dTheta, dSigma, &dc->csc_total, cs));
+                                 o.symmetrize, W.sparse->col_ptr, W.sparse->rows,
+                                 W.sparse->vals, dSigma, cs, W.sparse->cap));
+  } else {
+    // assembly + symmetrization straight from the coefficient lists (no CSC packing)
+    CUDA_TRY(launch_assemble_lists(p, (const int*)W.nz_count.ptr, (const int*)W.nz_cur.ptr,
+                                   (const int*)W.nz_rows.ptr, (const double*)W.nz_vals.ptr, nzcap,
+                                   (const double*)W.sigma_std.ptr,
+                                   o.standardize ? (const double*)W.scale.ptr : nullptr,
+                                   o.symmetrize, dTheta, dSigma, &dc->csc_total, cs));
+  }
   CUDA_TRY(ev_record(W, W.ev[4], cs));
   if ((rc = device_stats(W, dIters, dSweeps, dConv, p, cs))) return rc;
   CUDA_TRY(cudaMemcpyAsync(W.host_counters, W.counters.ptr, sizeof(DevCounters),
@@ -1177,15 +1198,17 @@ std::vector<unsigned char> graph_key(const double* dX, int64_t n, int64_t p, dou
                                      double tol, int32_t max_iter, const spmesl_options& o,
                                      const void* dTheta, const void* dSigma, const void* dIters,
                                      const void* dSweeps, const void* dConv, int nzcap,
-                                     cudaStream_t s) {
+                                     cudaStream_t s, const Workspace::SparseOut* sp = nullptr) {
   struct K {
     const void* x; int64_t n, p; double lam, tol; int32_t mi, nzcap; spmesl_options o;
     const void *th, *sg, *it, *sw, *cv; uint64_t gen; int dev;
+    const void *scp, *srows, *svals; int64_t scap;
   } k;
   std::memset(&k, 0, sizeof(k));
   k.x = dX; k.n = n; k.p = p; k.lam = lambda0; k.tol = tol; k.mi = max_iter; k.nzcap = nzcap;
   k.o = o; k.th = dTheta; k.sg = dSigma; k.it = dIters; k.sw = dSweeps; k.cv = dConv;
   k.gen = g_alloc_gen.load();
+  if (sp) { k.scp = sp->col_ptr; k.srows = sp->rows; k.svals = sp->vals; k.scap = sp->cap; }
   cudaGetDevice(&k.dev);
   (void)s;
   const unsigned char* b = (const unsigned char*)&k;
@@ -1223,11 +1246,11 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
     nzcap = initial_nzcap(n, p);
     if (W.gexec && W.graph_nzcap > 0 &&
         graph_key(dX, n, p, lambda0, tol, max_iter, o, dTheta, dSigma, dIters, dSweeps, dConv,
-                  W.graph_nzcap, s) == W.gkey)
+                  W.graph_nzcap, s, W.sparse) == W.gkey)
       nzcap = W.graph_nzcap;
     for (int attempt = 0; attempt < 4; ++attempt) {
       std::vector<unsigned char> key = graph_key(dX, n, p, lambda0, tol, max_iter, o, dTheta,
-                                                 dSigma, dIters, dSweeps, dConv, nzcap, s);
+                                                 dSigma, dIters, dSweeps, dConv, nzcap, s, W.sparse);
       bool launched = false;
       if (use_graph && W.gexec && key == W.gkey) {
         // replay: one launch for the whole fit (the penalty level is re-staged first)
@@ -1582,10 +1605,29 @@ int spmesl_fit_sparse_device(const double* dX, int64_t n, int64_t p, double lamb
   if ((rc = ensure(W->sigma_std, (size_t)p * 8))) return rc;
   if (!dSweeps) { if ((rc = ensure(W->sweeps, (size_t)p * 4))) return rc; dSweeps = (int32_t*)W->sweeps.ptr; }
   if (!dConverged) { if ((rc = ensure(W->conv, (size_t)p))) return rc; dConverged = (uint8_t*)W->conv.ptr; }
+  {
+    // mode 0 on a Gram solver: the device-path fit with the CSC written in place of the dense
+    // assembly (one synchronisation; CUDA-graph replay of repeated calls)
+    std::string why;
+    if (o.mode == 0 && o.solver != 1 && gram_applicable(*W, o, n, p, 0, p, &why)) {
+      const Workspace::SparseOut so{dColPtr, dRows, dVals, cap};
+      W->sparse = &so;
+      rc = fit_device_impl(dX, n, p, lambda0, tol, max_iter, o, nullptr, dSigma, dIters, dSweeps,
+                           dConverged, s, st, *W);
+      W->sparse = nullptr;
+      if (rc < 0) return rc;
+      const int64_t total = W->host_counters->csc_total;
+      *nnz_out = total;
+      if (st) st->nnz = total - p;   // off-diagonal entries of Theta
+      if (total > cap)
+        return fail(SPMESL_ERR_ARG, "sparse Theta capacity too small: need " + std::to_string(total));
+      return rc;
+    }
+  }
   FitOut out{0, p, (double*)W->sigma_std.ptr, dIters, dSweeps, dConverged};
   Layout L;
   int nzcap = 0;
-  // the fit itself (any mode / solver; no dense Theta, so no fill)
+  // the fit itself (residual solver / mode 1; no dense Theta, so no fill)
   if ((rc = fit_columns_core(*W, dX, n, p, 0, p, lambda0, tol, max_iter, o, out, s, st, L, &nzcap)))
     return rc;
   if ((rc = ensure(W->ccount, (size_t)p * 4))) return rc;

@@ -353,10 +353,15 @@ __global__ void sparse_write_kernel(int64_t p, const int* __restrict__ cnt, cons
                                     int nzcap, const double* __restrict__ sigma_std,
                                     const double* __restrict__ scale, int symmetrize, int rescale,
                                     const int64_t* __restrict__ col_ptr, int32_t* __restrict__ rows,
-                                    double* __restrict__ vals, double* __restrict__ sigma_out) {
+                                    double* __restrict__ vals, double* __restrict__ sigma_out,
+                                    int64_t cap) {
   const int lane = threadIdx.x & 31;
   const int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (k >= p) return;
+  if (cap >= 0 && col_ptr[p] > cap) {   // too small: the arrays stay untouched (host reports)
+    if (lane == 0 && sigma_out) sigma_out[k] = scale ? scale[k] * sigma_std[k] : sigma_std[k];
+    return;
+  }
   const int m = min(cnt[k], nzcap);
   const size_t base = (size_t)k * 2 * nzcap + (size_t)cur[k] * nzcap;
   const double sk = rescale ? scale[k] : 1.0;
@@ -426,11 +431,12 @@ cudaError_t launch_sparse_count(int64_t p, const int* cnt, const int* cur, const
 cudaError_t launch_sparse_write(int64_t p, const int* cnt, const int* cur, const int* nz_rows,
                                 const double* nz_vals, int nzcap, const double* sigma_std,
                                 const double* scale, int symmetrize, const int64_t* col_ptr,
-                                int32_t* rows, double* vals, double* sigma_out, cudaStream_t s) {
+                                int32_t* rows, double* vals, double* sigma_out, cudaStream_t s,
+                                int64_t cap) {
   const int wpb = 8;
   sparse_write_kernel<<<(unsigned)((p + wpb - 1) / wpb), wpb * 32, 0, s>>>(
       p, cnt, cur, nz_rows, nz_vals, nzcap, sigma_std, scale, symmetrize, scale != nullptr,
-      col_ptr, rows, vals, sigma_out);
+      col_ptr, rows, vals, sigma_out, cap);
   return cudaGetLastError();
 }
 

@@ -301,7 +301,8 @@ cudaError_t launch_sparse_count(int64_t p, const int* cnt, const int* cur, const
 cudaError_t launch_sparse_write(int64_t p, const int* cnt, const int* cur, const int* nz_rows,
                                 const double* nz_vals, int nzcap, const double* sigma_std,
                                 const double* scale, int symmetrize, const int64_t* col_ptr,
-                                int32_t* rows, double* vals, double* sigma_out, cudaStream_t s);
+                                int32_t* rows, double* vals, double* sigma_out, cudaStream_t s,
+                                int64_t cap = -1);   // cap >= 0: write only if nnz <= cap
 cudaError_t launch_csc_scan(const int* cnt, int ncols, int64_t* col_ptr, int64_t* total,
                             cudaStream_t s);
 cudaError_t launch_assemble_lists(int64_t p, const int* nz_count, const int* nz_cur,
