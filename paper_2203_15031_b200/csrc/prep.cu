@@ -112,11 +112,15 @@ __global__ void standardize_kernel(const double* __restrict__ X, int64_t n, int6
   }
   if (lane == 0) { mu[k] = m; scale[k] = s; }
   double g = 0.0;
+  // (staged column: keep x~ in the shared buffer for the f16 pass — one division per element)
+  double* xw = stage_n > 0 ? const_cast<double*>(x) : nullptr;
   for (int64_t i = lane; i < n_pad; i += 32) {
     const double v = i < n ? (standardize ? (x[i] - m) / s : x[i]) : 0.0;
     Xb[xb_index(i, k, nchunk)] = v;
+    if (xw && i < n) xw[i] = v;
     g = fma(v, v, g);
   }
+  __syncwarp();
   g = warp_sum(g);
   const double Nk = g / (double)n;                   // N_k = x~_k^T x~_k / n (= S_kk)
   if (lane == 0 && nrm) nrm[k] = Nk;
@@ -132,7 +136,7 @@ __global__ void standardize_kernel(const double* __restrict__ X, int64_t n, int6
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
         const int64_t i = i0 + t;
-        const double v = i < n ? (standardize ? (x[i] - m) / s : x[i]) : 0.0;
+        const double v = i < n ? (xw ? xw[i] : (standardize ? (x[i] - m) / s : x[i])) : 0.0;
         h[t] = __double2half(v * sc);
       }
       *(uint4*)(y.Y16 + y16_index(k, i0, y.nchunk64)) = *(const uint4*)h;
