@@ -103,3 +103,37 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cpp", ".cuh", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in txt.lower().replace("oracle-free", ""), f
+
+
+def test_ctypes_layouts_match_the_c_header(tmp_path):
+    """The ctypes mirrors of spmesl_options / spmesl_stats have the C structs' size and field
+    offsets (compiled from include/spmesl.h with the host compiler; no GPU needed)."""
+    import shutil
+    import subprocess
+    from paper_2203_15031_b200 import _lib
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no host C compiler")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    fields = {"spmesl_options": [f for f, _ in _lib.Options._fields_],
+              "spmesl_stats": [f for f, _ in _lib.Stats._fields_]}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "spmesl.h"', "int main(void) {"]
+    for struct, names in fields.items():
+        lines.append(f'printf("{struct} size %zu\\n", sizeof({struct}));')
+        for f in names:
+            lines.append(f'printf("{struct} {f} %zu\\n", offsetof({struct}, {f}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run([cc, "-I", os.path.join(root, "include"), str(src), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    got = {}
+    for ln in out:
+        if ln.strip():
+            struct, key, val = ln.split()
+            got[(struct, key)] = int(val)
+    for struct, cls in (("spmesl_options", _lib.Options), ("spmesl_stats", _lib.Stats)):
+        assert got[(struct, "size")] == ctypes.sizeof(cls), struct
+        for f in fields[struct]:
+            assert got[(struct, f)] == getattr(cls, f).offset, (struct, f)
