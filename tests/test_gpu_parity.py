@@ -521,3 +521,28 @@ def test_sparse_output_equals_dense(S, oracle, solver, mode, cfg, over, sym):
     assert torch.equal(T, dense.Theta)
     assert torch.equal(sp["sigma"], dense.sigma) and torch.equal(sp["sweeps"], dense.sweeps)
     assert sp["stats"]["nnz"] == len(rows) - p
+
+
+@pytest.mark.parametrize("solver", ["residual", "gram", "gram16"])
+def test_degenerate_penalties_closed_forms(S, oracle, solver):
+    """lambda0 = 0 (allowed: S:42-44 rejects only lambda0 < 0): every column regression is plain
+    least squares, so at convergence Theta_1 = S_n^{-1}, the inverse sample covariance with
+    divisor n (Eq. relation P:268-272 with sigma_k^2 = RSS_k/n; Prop. 1 P:312-365 for the
+    original scale) — symmetric already, so the symmetrization keeps it.  lambda0 above every
+    |x~_j^T x~_k|/n: B = 0, sigma = 1 on the standardized scale, Theta = diag(1/s_k^2)."""
+    rng = np.random.default_rng(11)
+    n, p = 400, 24
+    X = rng.standard_normal((n, p)) @ (np.eye(p) + 0.1 * rng.standard_normal((p, p))) \
+        * rng.uniform(0.5, 2.0, p)
+    Xc = X - X.mean(axis=0)
+    Sn = Xc.T @ Xc / n
+    r = S.fit(X, 0.0, tol=1e-10, max_iter=100, solver=solver)
+    assert np.all(r.converged)
+    inv = np.linalg.inv(Sn)              # (condition number of the correlation matrix ~ 3)
+    assert np.abs(r.Theta - inv).max() <= 1e-8 * np.abs(inv).max()
+    ora = oracle.spmesl_fit(X, 0.0, delta=1e-10)
+    assert_parity(compare(r.Theta, r.sigma, r.iters, r.sweeps, ora))
+    big = 1.5 * np.abs(np.corrcoef(X, rowvar=False) - np.eye(p)).max()
+    r = S.fit(X, big, solver=solver)
+    np.testing.assert_allclose(r.Theta, np.diag(1.0 / Sn.diagonal()), rtol=1e-12, atol=0)
+    assert np.all(r.iters <= 2)

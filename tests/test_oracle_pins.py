@@ -275,6 +275,22 @@ def test_null_case(oracle):
     np.testing.assert_allclose(r.Theta, np.diag(1 / s ** 2), rtol=1e-13, atol=0)
 
 
+def test_unpenalized_limit_is_inverse_sample_covariance(oracle):
+    # lambda0 = 0: each column regression is least squares, sigma_k^2 = RSS_k / n, and
+    # Theta_1 = -B D (Eq. relation) with Prop. 1 is the inverse of the
+    # sample covariance with divisor n — symmetric, so Eq. (symm) keeps it.  A dropped term in
+    # the sweep, a wrong sign in the assembly or a wrong rescaling all fail this.
+    rng = np.random.default_rng(11)
+    n, p = 400, 24
+    X = rng.standard_normal((n, p)) @ (np.eye(p) + 0.1 * rng.standard_normal((p, p))) \
+        * rng.uniform(0.5, 2.0, p)
+    Xc = X - X.mean(axis=0)
+    inv = np.linalg.inv(Xc.T @ Xc / n)
+    r = oracle.spmesl_fit(X, 0.0, delta=1e-10)
+    assert np.all(r.converged == 1)
+    assert np.abs(r.Theta - inv).max() <= 1e-8 * np.abs(inv).max()
+
+
 # ---------------------------------------------------------------- assembly / symmetrization
 def test_assemble_example(oracle):
     # Eq. (relation): beta_12 = 0.3, sigma_2 = 2 -> omega_12 = -0.075, omega_22 = 0.25
