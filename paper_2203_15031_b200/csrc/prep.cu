@@ -206,7 +206,10 @@ __global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ Xb
 cudaError_t launch_standardize(const double* X, const Layout& L, int standardize, double* Xb,
                                double* mu, double* scale, int* err, unsigned long long* bad_key,
                                cudaStream_t s, double* nrm, const S16Prep* y, double* ssq) {
-  const int wpb = 8;
+  // 4 warps (columns) per CTA: a finer last wave than 8 (ncu, config 5: 0.0535 -> 0.0516 ms;
+  // 2 and 1 the same as 4)
+  static const int wpb_env = getenv("SPMESL_DEV_STD_WPB") ? atoi(getenv("SPMESL_DEV_STD_WPB")) : 4;   // (dev)
+  const int wpb = std::min(8, std::max(1, wpb_env));
   S16Prep yy{};
   if (y) yy = *y;
   const int64_t nrows = L.nblk * J;                 // Xb rows incl. padding
