@@ -257,6 +257,24 @@ int spmesl_fit_columns_gram_device(const double* dX, int64_t n, int64_t p, int64
                                    int32_t* dIters, int32_t* dSweeps, uint8_t* dConverged,
                                    void* cuda_stream, spmesl_stats* st);
 
+/*
+ * TEST-ONLY (not on the fit path): the certified f16 screening (solvers 0 / 3) over all of its
+ * tiles, writing the raw f32 tensor-core accumulators acc_jc = n R_hat_jc = sum_i fp16(y_ij)
+ * fp16(y_ic) (y_k = x~_k / sqrt(N_k), N_k = x~_k^T x~_k / n) of every pair (j, c)
+ * the tiles cover into dAcc[c * acc_ld + j] (device float array, acc_ld >= p rounded up to 256,
+ * at least acc_ld columns; the caller zero-fills it: pairs no tile covers stay untouched —
+ * every j <= c is covered), and the candidate flags into dCand[p] (device, zero-filled by the
+ * caller) at lambda0 = 0.  dY16 (nullable, device): receives the f16 operand tiles the
+ * contraction read, 2 * ceil(p / 256) x ceil(n_pad / 64) tiles of 128 variables x 64 samples
+ * (n_pad = n rounded up to 32), each 16 KB, [tile row][sample chunk][variable][sample] with the
+ * 16-byte groups of each 128-byte row XOR-swizzled by (variable & 7) (screen16.cu header).
+ * Lets tests measure |R_hat - R| of the real tcgen05 accumulation against the bound eps(n_pad)
+ * the certification assumes.  Blocking; errors as spmesl_fit.
+ */
+int spmesl_screen_accumulators_device(const double* dX, int64_t n, int64_t p,
+                                      const spmesl_options* opt, float* dAcc, int64_t acc_ld,
+                                      uint8_t* dCand, void* dY16, void* cuda_stream);
+
 int spmesl_assemble_device(int64_t p, int64_t col_begin, int64_t col_end, const int64_t* dColPtr,
                            const int32_t* dRows, const double* dVals, const double* dSigmaStd,
                            const double* dScale, const spmesl_options* opt, double* dTheta,

@@ -248,6 +248,37 @@ def _columns_outputs(X, m, p, cap):
                 conv=torch.empty(m, dtype=torch.uint8, device=dev)), cap
 
 
+def screen_accumulators_device(X, *, stream=None, **options):
+    """spmesl_screen_accumulators_device (TEST-ONLY): the raw f32 accumulators n R_hat of the
+    certified f16 screening (tcgen05) for every pair its tiles cover, as a (p_pad, p_pad) float32
+    tensor A with A[c, j] = acc_jc (NaN where no tile wrote), plus the candidate flags at
+    lambda0 = 0, and the f16 operands as a (p_pad, n64) float16 tensor (variable, sample; the
+    tile layout undone).  X: (n, p) float64 CUDA tensor."""
+    import torch
+    X = as_colmajor(X)
+    n, p = X.shape
+    ld = -(-p // 256) * 256
+    n_pad = -(-n // 32) * 32
+    nc = -(-n_pad // 64)
+    acc = torch.full((ld, ld), float("nan"), dtype=torch.float32, device=X.device)
+    cand = torch.zeros(p, dtype=torch.uint8, device=X.device)
+    y16 = torch.empty((ld // 128, nc, 128, 8, 8), dtype=torch.float16, device=X.device)
+    s = stream if stream is not None else torch.cuda.current_stream(X.device)
+    o = _opts(**options)
+    with torch.cuda.device(X.device):
+        rc = load().spmesl_screen_accumulators_device(_vp(X), n, p, ctypes.byref(o), _vp(acc), ld,
+                                                      _vp(cand), _vp(y16),
+                                                      ctypes.c_void_p(s.cuda_stream))
+    _lib.check(rc)
+    # undo the 16-byte-group swizzle (group g of row r sits at g ^ (r & 7)), then the tiling
+    r = torch.arange(128, device=X.device)
+    g = torch.arange(8, device=X.device)
+    src = (g[None, :] ^ (r[:, None] & 7))                       # [128, 8]
+    y = torch.gather(y16, 3, src[None, None, :, :, None].expand(y16.shape))
+    Y = y.permute(0, 2, 1, 3, 4).reshape(ld, nc * 64)
+    return acc, cand, Y
+
+
 def fit_columns_gram_device(X, col_begin: int, col_end: int, lambda0: float, hit,
                             tol: float = 1e-4, max_iter: int = 100, *, stream=None, cap=None,
                             **options):

@@ -77,7 +77,7 @@ EXPORTS = [
     "spmesl_fit_columns_device", "spmesl_assemble_device", "spmesl_gram_tile_count",
     "spmesl_gram_screen_device", "spmesl_fit_columns_gram_device", "spmesl_gram_supported",
     "spmesl_fit_path_device", "spmesl_screen_tile_count", "spmesl_fit_sparse_device",
-    "spmesl_lambda_univ",
+    "spmesl_screen_accumulators_device", "spmesl_lambda_univ",
     "spmesl_lambda_ub", "spmesl_lambda_pb", "spmesl_solve_k", "spmesl_last_error",
     "spmesl_release_workspace", "spmesl_version",
 ]
@@ -129,6 +129,8 @@ def load() -> ctypes.CDLL:
     L.spmesl_fit_columns_gram_device.restype = ctypes.c_int
     L.spmesl_assemble_device.argtypes = [i64, i64, i64, vp, vp, vp, vp, vp, popt, vp, vp, vp]
     L.spmesl_assemble_device.restype = ctypes.c_int
+    L.spmesl_screen_accumulators_device.argtypes = [vp, i64, i64, popt, vp, i64, vp, vp, vp]
+    L.spmesl_screen_accumulators_device.restype = ctypes.c_int
     for f in ("spmesl_lambda_univ",):
         getattr(L, f).argtypes = [i64, i64]
         getattr(L, f).restype = dbl

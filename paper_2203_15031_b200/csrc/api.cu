@@ -228,18 +228,15 @@ struct FitOut {
 };
 
 // Gram-column prefetch in the sweep kernel when two p-vectors fit in shared memory and the
-// columns are 16-byte aligned (p even); SPMESL_TAIL_NOPREFETCH=1 disables it (development).
+// columns are 16-byte aligned (p even).
 // Sweep-kernel launch shape: two column CTAs per SM whenever their state fits side by side
 // (their latency-bound search rounds and barriers interleave: config 4 band 3.1 -> 2.0 ms), else
 // one CTA per SM with the Gram columns of the current nonzeros prefetched into shared memory.
 void set_prefetch(const Workspace& W, TailParams& T) {
-  static const bool off = getenv("SPMESL_TAIL_NOPREFETCH") && atoi(getenv("SPMESL_TAIL_NOPREFETCH"));
-  static const int occ_env = getenv("SPMESL_TAIL_OCC") ? atoi(getenv("SPMESL_TAIL_OCC")) : 0;
   const size_t base = tail_smem_bytes(T.p, T.n_pad, T.nzcap);
   const bool two = 2 * (base + 1024) <= (size_t)W.smem_sm;
-  T.occ = occ_env > 0 ? std::min(occ_env, 2) : (two ? 2 : 1);
-  if (T.occ == 2 && !two) T.occ = 1;
-  T.prefetch = T.occ == 1 && !off && (T.p % 2 == 0) &&
+  T.occ = two ? 2 : 1;
+  T.prefetch = T.occ == 1 && (T.p % 2 == 0) &&
                base + tail_prefetch_bytes(T.p) <= (size_t)W.smem_optin;
 }
 
@@ -337,11 +334,7 @@ int run_prep(Workspace& W, const double* dX, int64_t m, const spmesl_options& o,
   if (W.pending_zero) {
     // Theta's zero fill (HBM-bound) overlaps the solver (compute-bound), not standardization
     CUDA_TRY(cudaStreamWaitEvent(W.side, W.ev[1], 0));
-    static const int pz_bulk = getenv("SPMESL_DEV_PZ_BULK") ? atoi(getenv("SPMESL_DEV_PZ_BULK")) : 0;
-    if (pz_bulk > 0)
-      CUDA_TRY(launch_zero_fill_bulk(W.pending_zero, W.pending_count, pz_bulk, W.side));
-    else
-      CUDA_TRY(launch_zero_fill(W.pending_zero, W.pending_count, W.sms, W.side));
+    CUDA_TRY(launch_zero_fill(W.pending_zero, W.pending_count, W.sms, W.side));
     CUDA_TRY(cudaEventRecord(W.ev_join, W.side));
     W.pending_zero = nullptr;
   }
@@ -370,10 +363,6 @@ CDParams cd_params(Workspace& W, const Layout& L, int64_t cb, int64_t m, double 
   P.max_inner = o.max_inner;
   P.T = T;
   P.nst = cd_stages(T, L.n_pad, W.smem_optin);
-  if (const char* e = getenv("SPMESL_CD_NST")) {   // development: cap the X ring depth
-    const int v = atoi(e) & ~1;
-    if (v >= 2 && v < P.nst) P.nst = v;
-  }
   P.nzcap = nzcap;
   P.evict_after = tail_enabled(W, o, L, nzcap) ? o.tail_after : 0;
   P.tail_count = &dc->tail_count;
@@ -401,41 +390,9 @@ int run_cd(Workspace& W, const double* dX, int64_t n, int64_t p, int64_t cb, int
   int rc;
   if ((rc = run_prep(W, dX, m, o, L, s))) return rc;
   CDParams P = cd_params(W, L, cb, m, lambda0, tol, max_iter, o, nzcap, out, T);
-  { const char* d = getenv("SPMESL_CD_DEBUG"); P.debug = d ? atoi(d) : 0; }
-  static long long* dbg_buf = nullptr;
-  if (P.debug & 12) {
-    if (!dbg_buf) cudaMalloc(&dbg_buf, (16 + 4 * 1024) * sizeof(long long));
-    cudaMemsetAsync(dbg_buf, 0, (16 + 4 * 1024) * sizeof(long long), s);
-  }
-  P.dbg = dbg_buf;
   const int ctas = (int)std::min<int64_t>(W.sms, (m + T - 1) / T);
   *num_ctas = ctas;
   CUDA_TRY(launch_cd(P, ctas, s));
-  if (P.debug & 8) {
-    std::vector<long long> h(16 + 4 * ctas);
-    cudaMemcpyAsync(h.data(), dbg_buf, h.size() * 8, cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    long long t0 = h[16 + 2], t1 = h[16 + 2];
-    for (int c = 0; c < ctas; ++c) { t0 = std::min(t0, h[16 + c * 4 + 2]); t1 = std::max(t1, h[16 + c * 4 + 2]); }
-    FILE* f = fopen("gpurun_out/cta_trace.csv", "w");
-    if (f) {
-      fprintf(f, "cta,tile_sweeps,columns,end_us_after_first,small_sweeps\n");
-      for (int c = 0; c < ctas; ++c)
-        fprintf(f, "%d,%lld,%lld,%.1f,%lld\n", c, h[16 + c * 4], h[16 + c * 4 + 1], (h[16 + c * 4 + 2] - t0) / 1e3, h[16 + c * 4 + 3]);
-      fclose(f);
-    }
-    fprintf(stderr, "[cd trace] CTA end-time spread %.3f ms\n", (t1 - t0) / 1e6);
-  }
-  if (P.debug & 4) {
-    long long h[16];
-    cudaMemcpyAsync(h, dbg_buf, sizeof(h), cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    const char* nm[3] = {"mma-g0", "mma-g1", "epi"};
-    for (int w = 0; w < 3; ++w)
-      fprintf(stderr, "[cd phases] %-6s work %.3f ms  step-barrier %.3f ms  r-update %.3f ms (avg/CTA @1.965GHz)\n", nm[w],
-              h[w * 4 + 0] / (double)ctas / 1.965e6, h[w * 4 + 1] / (double)ctas / 1.965e6,
-              h[w * 4 + 2] / (double)ctas / 1.965e6);
-  }
   CUDA_TRY(ev_record(W, W.ev[2], s));
   return SPMESL_OK;
 }
@@ -744,34 +701,16 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
     Q.eps = screen16_eps(L.n_pad);
     Q.epsn = screen16_epsn(n, Q.eps);
     Q.cand = (uint8_t*)W.cand.ptr;
-    // Theta's zero fill is split: the screening kernel writes the first part under its
-    // contraction, a side-stream kernel the rest while the exact Gram columns and the sweeps
-    // (latency-bound, little HBM traffic) run; the caller joins it before the assembly
-    // (measured on config 5 with the 128 x 256 tiles: all fused 1.04 ms per fit, half and half
-    // 1.03 ms — within noise, so the simpler schedule: the screening kernel writes all of it
-    // at 0.95 of the HBM copy bandwidth)
-    static const double zfrac = getenv("SPMESL_S16_ZFRAC") ? atof(getenv("SPMESL_S16_ZFRAC")) : 1.0;
-    size_t zfused = (size_t)(zfrac * (double)G.zero_count) & ~(size_t)1;
-    if (zfused > G.zero_count) zfused = G.zero_count;
-    Q.zero_ptr = zfused ? G.zero_ptr : nullptr;
-    Q.zero_count = zfused;
+    // Theta's zero fill rides along the screening kernel's contraction (bulk stores from its
+    // producer): it is the kernel's HBM floor at large p (a side-stream fill of part of it, run
+    // under the exact Gram columns and the sweeps instead, measured the same: DESIGN.md §10)
+    Q.zero_ptr = G.zero_ptr;
+    Q.zero_count = G.zero_ptr ? G.zero_count : 0;
     Q.zero_last = G.zero_last;
-    if (getenv("SPMESL_DEV_S16_NOZERO")) { Q.zero_ptr = nullptr; Q.zero_count = 0; }   // (dev)
     W.screen_fill = (int64_t)Q.zero_count;
     CUDA_TRY(ev_record(W, W.ev[8], s));
     CUDA_TRY(launch_screen16(Q, std::min(W.sms, Q.tile_end), s));
     CUDA_TRY(ev_record(W, W.ev[9], s));
-    if (G.zero_ptr && zfused < G.zero_count) {
-      CUDA_TRY(cudaStreamWaitEvent(W.side, W.ev[9], 0));
-      static const int zgrid = getenv("SPMESL_ZB_GRID") ? atoi(getenv("SPMESL_ZB_GRID")) : W.sms;
-      if (zgrid > 0)
-        CUDA_TRY(launch_zero_fill_bulk(G.zero_ptr + zfused, G.zero_count - zfused, zgrid, W.side));
-      else
-        CUDA_TRY(launch_zero_fill(G.zero_ptr + zfused, G.zero_count - zfused, W.sms, W.side));
-      CUDA_TRY(cudaEventRecord(W.ev_join, W.side));
-      W.zero_join = true;
-      ++launches;
-    }
     launches += 1;   // screen16
     // candidate list on the device; then, by its count (read on the device), either the exact
     // Gram columns of the candidates (2 n p nU flops) or — when most columns are candidates
@@ -1062,11 +1001,10 @@ int fit_columns_core(Workspace& W, const double* dX, int64_t n, int64_t p, int64
   if (o.mode == 1) {
     // Algorithm 3 on the Gram form when the whole column range is fitted here and the Gram
     // solver's state fits (solver 0/2/3); else (or solver 1) on the residual CD kernel
-    static const bool no_jgram = getenv("SPMESL_DEV_JOINT_RESIDUAL") != nullptr;   // (dev)
     spmesl_options o0 = o;
     o0.mode = 0;
     std::string why;
-    if (!no_jgram && o.solver != 1 && gram_applicable(W, o0, n, p, cb, ce, &why))
+    if (o.solver != 1 && gram_applicable(W, o0, n, p, cb, ce, &why))
       return fit_joint_gram_core(W, dX, n, p, lambda0, tol, max_iter, o, out, s, st, L,
                                  nzcap_used);
     if (o.solver == 2 || o.solver == 3)
@@ -1126,9 +1064,8 @@ int gram_fit_enqueue_all(Workspace& W, const double* dX, int64_t n, int64_t p, d
   const size_t pp = (size_t)p * (size_t)p;
   // the screening kernel zero-fills Theta itself (bulk stores from its producer warp) when the
   // buffer allows 16-byte pieces; otherwise a side-stream kernel does, after standardization
-  static const bool side_zero = getenv("SPMESL_DEV_SIDE_ZERO") != nullptr;   // (dev)
   const bool sparse = W.sparse != nullptr;   // (CSC output: no dense Theta, no fill)
-  const bool take = !sparse && !side_zero && (((uintptr_t)dTheta & 15) == 0);
+  const bool take = !sparse && (((uintptr_t)dTheta & 15) == 0);
   if (take) { W.take_zero = dTheta; W.take_count = pp; }
   else if (!sparse) { W.pending_zero = dTheta; W.pending_count = pp; }
   rc = fit_gram_enqueue(W, dX, n, p, lambda0, tol, max_iter, o, out, cs, L, nzcap, nullptr, 1,
@@ -1237,11 +1174,8 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
     return fail(SPMESL_ERR_UNSUPPORTED, "Gram solver: " + why);
   const bool gram = gram_ok && o.solver != 1 && o.mode == 0;
   if (gram) {
-    static const bool no_graph = getenv("SPMESL_NO_GRAPH") != nullptr;
     // (no side-stream work may be captured: the fill must be the screening kernel's own)
-    const bool use_graph = !no_graph && !o.eager && getenv("SPMESL_DEV_SIDE_ZERO") == nullptr &&
-                           getenv("SPMESL_S16_ZFRAC") == nullptr && o.solver != 2 &&
-                           (((uintptr_t)dTheta & 15) == 0);
+    const bool use_graph = !o.eager && o.solver != 2 && (((uintptr_t)dTheta & 15) == 0);
     // the captured fit's list capacity if these are its arguments, else the initial one
     nzcap = initial_nzcap(n, p);
     if (W.gexec && W.graph_nzcap > 0 &&
@@ -1781,12 +1715,8 @@ int spmesl_fit_ex(const double* X, int64_t n, int64_t p, double lambda0, double 
   // computes — by the copy engine (D2H of a device zero buffer, when Theta is pinned) and by host
   // threads, in parallel; only the nonzero entries (COO) and the diagonal cross PCIe afterwards.
   size_t dma_elems = 0;
-  const bool e2e_dbg = getenv("SPMESL_E2E_DEBUG") != nullptr;
-  auto now_ms = [] {
-    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
-  };
-  const double t_start = now_ms();
-  const double dma_frac = getenv("SPMESL_E2E_DMA") ? atof(getenv("SPMESL_E2E_DMA")) : 0.3;
+  // (share of Theta's zero fill given to the copy engine: the host threads do the rest)
+  const double dma_frac = 0.3;
   {
     cudaPointerAttributes pa;
     const bool pinned = cudaPointerGetAttributes(&pa, Theta) == cudaSuccess &&
@@ -1812,7 +1742,7 @@ int spmesl_fit_ex(const double* X, int64_t n, int64_t p, double lambda0, double 
   {
     const size_t rest = pp - dma_elems;
     const unsigned hc = std::max(1u, std::thread::hardware_concurrency());
-    const unsigned cap_th = getenv("SPMESL_E2E_THREADS") ? (unsigned)atoi(getenv("SPMESL_E2E_THREADS")) : 16u;
+    const unsigned cap_th = 16u;
     const size_t nth = std::min<size_t>(std::min(cap_th, hc), std::max<size_t>(1, rest >> 20));
     const size_t per = (rest + nth - 1) / nth;
     for (size_t t = 0; t < nth; ++t) {
@@ -1820,12 +1750,9 @@ int spmesl_fit_ex(const double* X, int64_t n, int64_t p, double lambda0, double 
       if (lo < hi) zero.emplace_back([=] { std::memset(Theta + lo, 0, (hi - lo) * sizeof(double)); });
     }
   }
-  double t_threads = 0, t_dma = 0;
   auto join = [&] {
     for (auto& th : zero) if (th.joinable()) th.join();
-    t_threads = now_ms();
     if (dma_elems) cudaStreamSynchronize(W->side);
-    t_dma = now_ms();
   };
   auto bail = [&](int code) { join(); return code; };
   if ((rc = ensure(W->hx, np * 8))) return bail(rc);
@@ -1901,13 +1828,9 @@ int spmesl_fit_ex(const double* X, int64_t n, int64_t p, double lambda0, double 
     return bail(rc);
   if ((rc = read_counters(*W, s))) return bail(rc);
   stats_from_counters(*W->host_counters, p, st, &any_unconv);
-  const double t_dev = now_ms();
   join();
   for (int e = 0; e < ncoo; ++e) Theta[(size_t)cc[e] * p + cr[e]] = cv[e];
   for (int64_t k = 0; k < p; ++k) Theta[(size_t)k * p + k] = diag[k];
-  if (e2e_dbg)
-    fprintf(stderr, "[e2e] device done %.2f ms, zero threads %.2f ms, dma %.2f ms, end %.2f ms\n",
-            t_dev - t_start, t_threads - t_start, t_dma - t_start, now_ms() - t_start);
   if (st) {
     st->nnz = W->host_counters->csc_total;
     st->ms_standardize = ev_ms(W->ev[0], W->ev[1]);
@@ -1987,9 +1910,14 @@ int64_t spmesl_screen_tile_count(int64_t p, const spmesl_options* opt) {
   return o.solver == 2 ? gram_tile_count(p) : screen16_tile_count(p);
 }
 
-int spmesl_gram_screen_device(const double* dX, int64_t n, int64_t p, double lambda0,
-                              int64_t tile_begin, int64_t tile_end, const spmesl_options* opt,
-                              uint8_t* dHit, void* cuda_stream, spmesl_stats* st) {
+}  // extern "C"
+
+namespace {
+// The screening pass over tiles [tile_begin, tile_end) (spmesl_gram_screen_device); acc (tests
+// only, solver 3): the raw f32 accumulators n R_hat_jc of every tile into acc[c * acc_ld + j].
+int gram_screen_impl(const double* dX, int64_t n, int64_t p, double lambda0, int64_t tile_begin,
+                     int64_t tile_end, const spmesl_options* opt, uint8_t* dHit,
+                     void* cuda_stream, spmesl_stats* st, float* acc, int64_t acc_ld) {
   init_stats(st);
   spmesl_options o = resolve(opt);
   int rc = validate(dX, n, p, lambda0, 1.0, 1, o);
@@ -2009,23 +1937,30 @@ int spmesl_gram_screen_device(const double* dX, int64_t n, int64_t p, double lam
   Layout L;
   set_layout(L, n, p);
   if ((rc = alloc_core(*W, L, 1, 8))) return rc;
+  S16Prep yprep{};
+  const int64_t p_pad = screen16_pad(p);
+  float* inv_sq = nullptr;
+  float* lam_n = nullptr;
+  double* sqv = nullptr;
   if (s16) {
     if ((rc = ensure(W->nrm, (size_t)p * 8))) return rc;
-    if ((rc = ensure(W->sq, (size_t)screen16_pad(p) * 8 + (size_t)p * 8))) return rc;
+    if ((rc = ensure(W->sq, (size_t)p_pad * 8 + (size_t)p * 8))) return rc;
     if ((rc = ensure(W->y16, screen16_y_halves(p, L.n_pad) * 2))) return rc;
+    inv_sq = (float*)W->sq.ptr;
+    lam_n = inv_sq + p_pad;
+    sqv = (double*)(lam_n + p_pad);
+    // the certified operands y = x~ / sqrt(N) and the threshold factors come from the
+    // standardization's fused writer, exactly as in the single-device fit
+    yprep.Y16 = (__half*)W->y16.ptr;
+    yprep.nchunk64 = (L.n_pad + 63) / 64;
+    yprep.p_pad = p_pad;
+    yprep.sq = sqv; yprep.inv_sq = inv_sq; yprep.lam_n = lam_n;
+    yprep.lambda0 = lambda0;
   }
-  if ((rc = run_prep(*W, dX, 1, o, L, s, /*band=*/false))) return rc;
+  if ((rc = run_prep(*W, dX, 1, o, L, s, /*band=*/false, s16 ? &yprep : nullptr))) return rc;
   if (s16) {
     // dHit[c] = 1 for the columns the certified f16 screening of these tiles cannot clear
     // (candidates: a superset of the columns with a hit there)
-    const int64_t p_pad = screen16_pad(p);
-    float* inv_sq = (float*)W->sq.ptr;
-    float* lam_n = inv_sq + p_pad;
-    double* sqv = (double*)(lam_n + p_pad);
-    CUDA_TRY(launch_sqrt((const double*)W->nrm.ptr, sqv, inv_sq, lam_n, lambda0, (int)n, (int)p,
-                         (int)p_pad, s));
-    CUDA_TRY(launch_to_f16((const double*)W->xb.ptr, (const double*)W->nrm.ptr, (int)p, L.n_pad,
-                           L.nchunk, (__half*)W->y16.ptr, s));
     Screen16Params Q{};
     Q.Y16 = (const __half*)W->y16.ptr;
     Q.sq = sqv;
@@ -2040,6 +1975,8 @@ int spmesl_gram_screen_device(const double* dX, int64_t n, int64_t p, double lam
     Q.eps = screen16_eps(L.n_pad);
     Q.epsn = screen16_epsn(n, Q.eps);
     Q.cand = dHit;
+    Q.acc_out = acc;
+    Q.acc_ld = acc_ld;
     CUDA_TRY(ev_record(*W, W->ev[8], s));
     CUDA_TRY(launch_screen16(Q, (int)std::min<int64_t>(W->sms, std::max<int64_t>(1, tile_end - tile_begin)), s));
     CUDA_TRY(ev_record(*W, W->ev[9], s));
@@ -2051,7 +1988,7 @@ int spmesl_gram_screen_device(const double* dX, int64_t n, int64_t p, double lam
       st->ms_standardize = ev_ms(W->ev[0], W->ev[1]);
       st->ms_gram = ev_ms(W->ev[1], W->ev[7]);
       st->ms_screen = ev_ms(W->ev[8], W->ev[9]);
-      st->kernel_launches = 4;
+      st->kernel_launches = 3;   // reset, standardize (+ f16 operands), screening
       st->bad_column = -1;
     }
     return SPMESL_OK;
@@ -2077,6 +2014,39 @@ int spmesl_gram_screen_device(const double* dX, int64_t n, int64_t p, double lam
     st->kernel_launches = 2;
     st->bad_column = -1;
   }
+  return SPMESL_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int spmesl_gram_screen_device(const double* dX, int64_t n, int64_t p, double lambda0,
+                              int64_t tile_begin, int64_t tile_end, const spmesl_options* opt,
+                              uint8_t* dHit, void* cuda_stream, spmesl_stats* st) {
+  return gram_screen_impl(dX, n, p, lambda0, tile_begin, tile_end, opt, dHit, cuda_stream, st,
+                          nullptr, 0);
+}
+
+int spmesl_screen_accumulators_device(const double* dX, int64_t n, int64_t p,
+                                      const spmesl_options* opt, float* dAcc, int64_t acc_ld,
+                                      uint8_t* dCand, void* dY16, void* cuda_stream) {
+  spmesl_options o = resolve(opt);
+  if (o.solver == 1 || o.solver == 2)
+    return fail(SPMESL_ERR_ARG, "the accumulators exist for the certified screening (solver 0/3)");
+  if (!dAcc || !dCand || acc_ld < screen16_pad(p)) return fail(SPMESL_ERR_ARG, "bad accumulator buffer");
+  if (p < 1 || p > (int64_t)0x7fffffff) return fail(SPMESL_ERR_ARG, "bad p");
+  int rc = gram_screen_impl(dX, n, p, 0.0, 0, screen16_tile_count(p), opt, dCand, cuda_stream,
+                            nullptr, dAcc, acc_ld);
+  if (rc || !dY16) return rc;
+  int dev;
+  if ((rc = current_device(-1, &dev))) return rc;
+  Workspace* W = workspace_for(dev);
+  std::lock_guard<std::mutex> lk(W->mu);
+  const int n_pad = (int)(((n + KC - 1) / KC) * KC);
+  CUDA_TRY(cudaMemcpyAsync(dY16, W->y16.ptr, screen16_y_halves(p, n_pad) * 2,
+                           cudaMemcpyDeviceToDevice, (cudaStream_t)cuda_stream));
+  CUDA_TRY(cudaStreamSynchronize((cudaStream_t)cuda_stream));
   return SPMESL_OK;
 }
 

@@ -136,7 +136,8 @@ __global__ void assemble_entries_kernel(int64_t p, int64_t col_begin, int64_t co
     }
     const int64_t k = lo;
     const int32_t j = rows[e];
-    const double sj = scale[j], sk = scale[k];
+    // (scale is NULL when the fit did not standardize: no rescaling then)
+    const double sj = rescale ? scale[j] : 1.0, sk = rescale ? scale[k] : 1.0;
     const double t_jk = theta1(vals[e], sigma_std[k], sj, sk, rescale != 0);
     double out = t_jk;
     if (symmetrize) {

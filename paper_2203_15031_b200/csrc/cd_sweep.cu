@@ -104,9 +104,6 @@ __device__ __forceinline__ double soft(double a, double lam) {
 
 constexpr int MAX_NST = 12;  // max X chunk pipeline depth (runtime: as many as smem allows)
 
-// development-only phase timers (P.debug & 4): per-CTA cycle totals in P.dbg[cta][16]
-#define PH_T0() long long _t0 = (P.debug & 4) ? clock64() : 0
-#define PH_ADD(slot) do { if (P.debug & 4) { long long _t1 = clock64(); if (lane == 0) dbg_acc[slot] += _t1 - _t0; _t0 = _t1; } } while (0)
 constexpr int JP = J + 1;    // padded row-block stride of the per-column [c][row] tiles
 
 struct SlotState {
@@ -289,8 +286,6 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
   const int n = P.n, n_pad = P.n_pad, nchunk = P.nchunk, p = P.p, nblk = P.nblk;
   const int nzcap = P.nzcap;
   const double inv_n = 1.0 / (double)n;
-  long long dbg_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  long long dbg_sweeps = 0, dbg_cols = 0, dbg_sweeps_small = 0;
 
   if (tid == 0) {
     // one ring per parity group: every phase of a stage is consumed by the same 4 warps, so a
@@ -533,7 +528,6 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
       }
     }
     const int A = S.A;
-    if (tid == 0 && A > 0) { dbg_sweeps++; dbg_cols += S.nloads; dbg_sweeps_small += (A <= 8); }
     __threadfence_block();
     work_sync();
     named_bar_arrive(BAR_PROD, CD_THREADS);   // release the producer for this sweep (or exit)
@@ -562,21 +556,16 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
       if (cnt_old > 0) { nx_row = lst_old_r[0]; nx_val = lst_old_v[0]; }
     }
     for (int t = 0; t <= nblk; ++t) {
-      PH_T0();
       if (is_mma) {
         // ======== MMA warps: Z_t
         if (t < nblk) {
           double* Zb = Zp + (size_t)(t & 1) * T * JP;
-          if (P.debug & 1)
-            run_gemm<false>(NTa, grp, wg, Xr, Rs, Zb, fr, er, nchunk, NSTG, ring_s, ring_ph, SR,
-                            inv_n, lane);
-          else
-            run_gemm<true>(NTa, grp, wg, Xr, Rs, Zb, fr, er, nchunk, NSTG, ring_s, ring_ph, SR,
-                           inv_n, lane);
+          run_gemm<true>(NTa, grp, wg, Xr, Rs, Zb, fr, er, nchunk, NSTG, ring_s, ring_ph, SR,
+                         inv_n, lane);
         }
       } else if (c_act) {
         // ======== epilogue warp, lane = column c: finish block b = t-1 row by row
-        if (t >= 1 && !(P.debug & 2)) {
+        if (t >= 1) {
           const int b = t - 1;
           const int j0 = b * J;
           const int xb = b & 1, xp = xb ^ 1;   // chg buffers: this block / previous block
@@ -639,9 +628,7 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
           S.nchg[xb][lane] = nch;
         }
       }
-      PH_ADD(0);     // slot 0: this warp's own work in the step
       work_sync();   // ---- end of step t
-      PH_ADD(1);     // slot 1: waiting at the step barrier
       // -- residual updates e_c += x_j d for block t-1's changes (Prop. 2); rare
       if (t >= 1) {
         const int xb = (t - 1) & 1;
@@ -663,25 +650,12 @@ __global__ void __launch_bounds__(CD_THREADS, 1) cd_sweep_kernel(const CDParams 
           work_sync();
         }
       }
-      PH_ADD(2);     // slot 2: residual updates between steps
     }
     if (c_act) {
       S.maxd[lane] = maxd;
       S.cnt_new[lane] = cnt_new;
     }
     work_sync();
-  }
-  if ((P.debug & 8) && tid == 0) {   // per-CTA trace: tile-sweeps, columns, end time
-    unsigned long long tnow;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
-    P.dbg[16 + blockIdx.x * 4 + 0] = dbg_sweeps;
-    P.dbg[16 + blockIdx.x * 4 + 1] = dbg_cols;
-    P.dbg[16 + blockIdx.x * 4 + 2] = (long long)tnow;
-    P.dbg[16 + blockIdx.x * 4 + 3] = dbg_sweeps_small;
-  }
-  if ((P.debug & 4) && lane == 0 && (warp == 0 || warp == 4 || warp == NMW)) {
-    const int w = warp == 0 ? 0 : (warp == 4 ? 1 : 2);
-    for (int k = 0; k < 3; ++k) atomicAdd((unsigned long long*)&P.dbg[w * 4 + k], (unsigned long long)dbg_acc[k]);
   }
 }
 

@@ -116,8 +116,11 @@ __global__ void __launch_bounds__(G_THREADS, 1) syrk_screen_kernel(const GramPar
   const int nchunk = P.nchunk, nblk = P.nblk, p = P.p;
   const int nT = (nblk + GB - 1) / GB;
   const int t_begin = P.tile_begin, t_end = P.tile_end;
-  if (P.zero_ptr)
+  if (P.zero_ptr) {
     for (int e = tid; e < G_ZPIECE; e += blockDim.x) zbuf[e] = 0.0;
+    // the producer's bulk stores (async proxy) read zbuf: every writer fences its stores first
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
   if (tid == 0) {
     for (int s = 0; s < nst; ++s) {
       mbar_init_g(&full[s], 1);

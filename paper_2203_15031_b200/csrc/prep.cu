@@ -208,16 +208,14 @@ cudaError_t launch_standardize(const double* X, const Layout& L, int standardize
                                cudaStream_t s, double* nrm, const S16Prep* y, double* ssq) {
   // 4 warps (columns) per CTA: a finer last wave than 8 (ncu, config 5: 0.0535 -> 0.0516 ms;
   // 2 and 1 the same as 4)
-  static const int wpb_env = getenv("SPMESL_DEV_STD_WPB") ? atoi(getenv("SPMESL_DEV_STD_WPB")) : 4;   // (dev)
-  const int wpb = std::min(8, std::max(1, wpb_env));
+  constexpr int wpb = 4;
   S16Prep yy{};
   if (y) yy = *y;
   const int64_t nrows = L.nblk * J;                 // Xb rows incl. padding
   const int64_t cols = std::max<int64_t>(nrows, yy.Y16 ? yy.p_pad : 0);
   dim3 grid((unsigned)((cols + wpb - 1) / wpb));
   // stage each column in shared memory by one bulk copy when it is 16-byte aligned and small
-  static const bool no_stage = getenv("SPMESL_DEV_STD_NOSTAGE") != nullptr;   // (dev)
-  const int stage_n = (!no_stage && L.n % 2 == 0 && ((uintptr_t)X & 15) == 0 && L.n <= 1024)
+  const int stage_n = (L.n % 2 == 0 && ((uintptr_t)X & 15) == 0 && L.n <= 1024)
                           ? (int)L.n : 0;
   const size_t smem = (size_t)wpb * stage_n * 8;
   if (smem > 48 * 1024)

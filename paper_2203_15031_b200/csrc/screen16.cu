@@ -3,8 +3,7 @@
 // The first sweep of column c changes some b_jc iff |S_jc| > lambda0 for some j != c
 // (sigma^(0) = 1), S = X~^T X~ / n.  Deciding that needs S only to the extent of a
 // comparison, so it is done on the f16 tensor cores (tcgen05.mma kind::f16 with the f32
-// accumulator in TMEM — default — or mma.sync m16n8k16 with SPMESL_S16_MMA_SYNC=1) with a
-// rigorous error bound, and only the columns that cannot be certified hit-free get their exact
+// accumulator in TMEM) with a rigorous error bound, and only the columns that cannot be certified hit-free get their exact
 // FP64 Gram column (DMMA, gram_pass in tail.cu, which also takes the exact decision).  No
 // low-precision value ever enters the iterates.
 //
@@ -23,7 +22,7 @@
 //
 // Layout of Y16: tiles of 128 variables x 64 samples, one contiguous 16 KB block per tile
 // ([nblk128][nchunk64][128][64] halves), each 128-byte row's 16-byte chunks XOR-swizzled by
-// (row & 7) so the ldmatrix row fetches hit distinct bank groups.
+// (row & 7): the canonical K-major SWIZZLE_128B layout tcgen05.mma reads.
 #include <algorithm>
 #include <cstdlib>
 #include <cuda_fp16.h>
@@ -36,12 +35,6 @@ namespace {
 constexpr int S16_TB = 128;                 // variables per tile side
 constexpr int S16_KC = 64;                  // samples per chunk
 constexpr int S16_TILE_HALVES = S16_TB * S16_KC;     // 8192 halves = 16 KB
-constexpr int S16_MMA_WARPS = 8;
-constexpr int S16_THREADS = (S16_MMA_WARPS + 1) * 32;
-#ifndef SPMESL_S16_NST
-#define SPMESL_S16_NST 4
-#endif
-constexpr int S16_NST = SPMESL_S16_NST;     // ring stages (2 tiles = 32 KB each)
 #ifndef SPMESL_S16_ZPIECE
 #define SPMESL_S16_ZPIECE 2048
 #endif
@@ -56,7 +49,6 @@ __device__ __forceinline__ void mbar_wait_s(uint64_t* bar, uint32_t parity) {
       "@!P1 bra WAIT_%=;\n}\n" ::"r"(su32(bar)), "r"(parity) : "memory");
 }
 
-// Xb (FP64 tiles) -> Y16 (normalized f16 tiles).  One CTA per (128-block, 64-chunk) tile.
 // Theta's zero fill is spread over the producer's chunks in proportion, so the 8 p^2-byte write
 // (the kernel's HBM floor at large p) overlaps the whole contraction instead of trailing it.
 __device__ __forceinline__ size_t zero_quota(const Screen16Params& P, size_t npieces, int nchunk) {
@@ -89,196 +81,6 @@ __device__ __forceinline__ void zero_pieces(const Screen16Params& P, const doubl
   }
 }
 
-__global__ void to_f16_kernel(const double* __restrict__ Xb, const double* __restrict__ nrm,
-                              int p, int nchunk32, int nchunk64, __half* __restrict__ Y16) {
-  const int blk = blockIdx.x, q = blockIdx.y;
-  __half* tile = Y16 + ((size_t)blk * nchunk64 + q) * S16_TILE_HALVES;
-  for (int e = threadIdx.x; e < S16_TB * (S16_KC / 8); e += blockDim.x) {
-    const int r = e >> 3, ch = e & 7;               // row (variable), 16-byte chunk
-    const int j = blk * S16_TB + r;
-    const int k0 = q * S16_KC + ch * 8;
-    __align__(16) __half v[8];
-    const double sc = (j < p) ? rsqrt(nrm[j]) : 0.0;
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const int i = k0 + t;
-      double x = 0.0;
-      if (j < p && i < nchunk32 * KC) x = Xb[xb_index(i, j, nchunk32)] * sc;
-      v[t] = __double2half(x);
-    }
-    *(uint4*)(tile + r * S16_KC + ((ch ^ (r & 7)) << 3)) = *(const uint4*)v;
-  }
-}
-
-// upper-triangle tile t -> (I, J), row-major by I
-__device__ __forceinline__ void tri_tile16(int t, int nT, int& I, int& Jt) {
-  int i = 0, rowlen = nT;
-  while (t >= rowlen) { t -= rowlen; ++i; --rowlen; }
-  I = i;
-  Jt = i + t;
-}
-
-__device__ __forceinline__ void ldsm_x4(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3,
-                                        const void* addr) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(su32(addr)));
-}
-
-__device__ __forceinline__ void hmma(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};\n"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-__global__ void __launch_bounds__(S16_THREADS, 1) screen16_kernel(const Screen16Params P) {
-  if (P.zero_last && blockIdx.x == 0 && threadIdx.x == 0) *P.zero_last = 0.0;
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  uint64_t* full = (uint64_t*)smem_raw;
-  uint64_t* empty = full + S16_NST;
-  __half* ring = (__half*)(smem_raw + 128);                 // [NST][2 tiles]
-  double* zbuf = (double*)(ring + (size_t)S16_NST * 2 * S16_TILE_HALVES);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nT = P.ntb;                                     // 128-variable blocks
-  const int nchunk = P.nchunk64;
-  if (P.zero_ptr)
-    for (int e = tid; e < S16_ZPIECE; e += blockDim.x) zbuf[e] = 0.0;
-  if (tid == 0) {
-    for (int s = 0; s < S16_NST; ++s) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(&full[s])), "r"(1));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(&empty[s])),
-                   "r"(S16_MMA_WARPS));
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-  }
-  __syncthreads();
-
-  if (warp == S16_MMA_WARPS) {
-    // ------------------------------------------------------------------ producer
-    if (lane == 0) {
-      int s = 0;
-      uint32_t ph = 0;
-      const size_t npieces = P.zero_ptr ? (P.zero_count + S16_ZPIECE - 1) / S16_ZPIECE : 0;
-      size_t zp = blockIdx.x;
-      const size_t zquota = zero_quota(P, npieces, nchunk);
-      for (int t = P.tile_begin + blockIdx.x; t < P.tile_end; t += gridDim.x) {
-        int I, Jt;
-        tri_tile16(t, nT, I, Jt);
-        for (int q = 0; q < nchunk; ++q) {
-          mbar_wait_s(&empty[s], ph ^ 1u);
-          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(&full[s])),
-                       "r"(2u * S16_TILE_HALVES * 2u)
-                       : "memory");
-          const __half* srcA = P.Y16 + ((size_t)I * nchunk + q) * S16_TILE_HALVES;
-          const __half* srcB = P.Y16 + ((size_t)Jt * nchunk + q) * S16_TILE_HALVES;
-          __half* dst = ring + (size_t)s * 2 * S16_TILE_HALVES;
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                  su32(dst)),
-              "l"(srcA), "r"((uint32_t)S16_TILE_HALVES * 2u), "r"(su32(&full[s]))
-              : "memory");
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                  su32(dst + S16_TILE_HALVES)),
-              "l"(srcB), "r"((uint32_t)S16_TILE_HALVES * 2u), "r"(su32(&full[s]))
-              : "memory");
-          zero_pieces(P, zbuf, zp, npieces, zquota);   // Theta's zero fill rides along
-          if (++s == S16_NST) { s = 0; ph ^= 1u; }
-        }
-      }
-      zero_pieces(P, zbuf, zp, npieces, npieces);
-      asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
-    }
-    return;
-  }
-
-  // -------------------------------------------------------------------- MMA warps: 64 x 32 each
-  const int mq = warp & 1, nq = warp >> 1;
-  const int g = lane >> 2, t4 = lane & 3;
-  const double inv_n = 1.0 / (double)P.n;
-  int s = 0;
-  uint32_t ph = 0;
-  for (int t = P.tile_begin + blockIdx.x; t < P.tile_end; t += gridDim.x) {
-    int I, Jt;
-    tri_tile16(t, nT, I, Jt);
-    float acc[4][4][4];
-#pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-      for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = acc[mi][ni][2] = acc[mi][ni][3] = 0.f;
-    for (int q = 0; q < nchunk; ++q) {
-      mbar_wait_s(&full[s], ph);
-      const __half* tA = ring + (size_t)s * 2 * S16_TILE_HALVES;
-      const __half* tB = tA + S16_TILE_HALVES;
-      // fragments of k-step kk + 1 are loaded while the MMAs of k-step kk issue
-      uint32_t a[2][4][4], b[2][4][2];
-      auto load_frags = [&](int kk, int buf) {
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi) {   // A: rows mq*64 + mi*16 + (lane & 15), chunk 2kk + lane/16
-          const int r = mq * 64 + mi * 16 + (lane & 15);
-          const int ch = 2 * kk + (lane >> 4);
-          ldsm_x4(a[buf][mi][0], a[buf][mi][1], a[buf][mi][2], a[buf][mi][3],
-                  tA + r * S16_KC + ((ch ^ (r & 7)) << 3));
-        }
-#pragma unroll
-        for (int np = 0; np < 2; ++np) {   // B: (cols 0-7, k lo/hi), (cols 8-15, k lo/hi)
-          const int r = nq * 32 + np * 16 + (lane & 7) + ((lane >> 4) << 3);
-          const int ch = 2 * kk + ((lane >> 3) & 1);
-          ldsm_x4(b[buf][2 * np][0], b[buf][2 * np][1], b[buf][2 * np + 1][0], b[buf][2 * np + 1][1],
-                  tB + r * S16_KC + ((ch ^ (r & 7)) << 3));
-        }
-      };
-      load_frags(0, 0);
-#pragma unroll
-      for (int kk = 0; kk < S16_KC / 16; ++kk) {
-        if (kk + 1 < S16_KC / 16) load_frags(kk + 1, (kk + 1) & 1);
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-          for (int ni = 0; ni < 4; ++ni) hmma(acc[mi][ni], a[kk & 1][mi], b[kk & 1][ni][0], b[kk & 1][ni][1]);
-      }
-      __syncwarp();
-      if (lane == 0)
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(&empty[s])) : "memory");
-      if (++s == S16_NST) { s = 0; ph ^= 1u; }
-    }
-    // epilogue: certify or flag (both orientations of an off-diagonal tile).  The pair is
-    // certified when |acc| <= n lambda0 / (sq_j sq_c) - n eps; that threshold is evaluated as
-    // one f32 fma rounded downwards from factors rounded downwards (n eps rounded upwards), so
-    // it can only come out smaller (a smaller threshold only adds candidates).  Padding
-    // columns carry inv_sq = +inf (never flag).
-    const bool diag_tile = (I == Jt);
-    float cB[4][2];
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) cB[ni][e] = P.inv_sq[Jt * S16_TB + nq * 32 + ni * 8 + 2 * t4 + e];
-#pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int j = I * S16_TB + mq * 64 + mi * 16 + g + 8 * h;
-        if (j >= P.p) continue;
-        const float rA = P.lam_n[j];
-#pragma unroll
-        for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int c = Jt * S16_TB + nq * 32 + ni * 8 + 2 * t4 + e;
-            const float thr = __fmaf_rd(rA, cB[ni][e], -P.epsn);
-            if (fabsf(acc[mi][ni][2 * h + e]) > thr && c != j) {
-              P.cand[c] = 1;
-              if (!diag_tile) P.cand[j] = 1;
-            }
-          }
-      }
-  }
-}
-
-
 // ------------------------------------------------------------------ tcgen05 version
 // The same screening contraction on the 5th-generation tensor cores: the 128 x 64 f16 tiles of
 // Y16 are already the canonical K-major SWIZZLE_128B layout (128-byte rows, 16-byte chunks
@@ -288,7 +90,7 @@ __global__ void __launch_bounds__(S16_THREADS, 1) screen16_kernel(const Screen16
 // tile t + 1), and eight epilogue warps read it back with tcgen05.ld.  Roles: warp 0 TMA
 // producer (+ Theta zero fill), warp 1 MMA issuer and TMEM owner, warps 2-9 epilogue (two per
 // TMEM lane quarter, each half of the columns).
-// BN = 256 (default): tiles of 128 rows x 256 columns, 1.5 B of operand traffic per output
+// BN = 256: tiles of 128 rows x 256 columns, 1.5 B of operand traffic per output
 // instead of 2 (the kernel is bound by L2 -> SM operand traffic, not by the tensor cores).
 // Tile set: column block Jb (256 wide) pairs with row blocks I = 0 .. min(2 Jb + 1, ntb - 1),
 // which covers every pair of the upper triangle (plus one redundant 128 x 128 sub-block below
@@ -296,14 +98,10 @@ __global__ void __launch_bounds__(S16_THREADS, 1) screen16_kernel(const Screen16
 constexpr int T5_EPI_WARPS = 8;
 constexpr int T5_THREADS = (2 + T5_EPI_WARPS) * 32;
 
-template <int BN>
-#ifndef SPMESL_T5_NST
-#define SPMESL_T5_NST 3
-#endif
-__host__ __device__ constexpr int t5_nst() { return BN == 256 ? SPMESL_T5_NST : 4; }
-template <int BN>
-__host__ __device__ constexpr size_t t5_smem() {
-  return 1024 + (size_t)t5_nst<BN>() * (1 + BN / 128) * S16_TILE_HALVES * 2 + (size_t)S16_ZPIECE * 8;
+constexpr int BN = 256;
+constexpr int T5_NST = 3;                   // operand ring stages (3 x 48 KB; 4 measured the same)
+constexpr size_t t5_smem() {
+  return 1024 + (size_t)T5_NST * (1 + BN / 128) * S16_TILE_HALVES * 2 + (size_t)S16_ZPIECE * 8;
 }
 
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
@@ -324,17 +122,10 @@ __device__ __forceinline__ void wide_tile(int t, int& I, int& Jb) {
   I = t - jb * (jb + 1);
 }
 
-template <int BN>
-__device__ __forceinline__ void t5_tile(int t, int nT, int& I, int& Jb) {
-  if (BN == 256) wide_tile(t, I, Jb);
-  else tri_tile16(t, nT, I, Jb);
-}
-
-template <int BN>
 __global__ void __launch_bounds__(T5_THREADS, 1) screen16_tc_kernel(const Screen16Params P) {
   if (P.zero_last && blockIdx.x == 0 && threadIdx.x == 0) *P.zero_last = 0.0;
   constexpr int NBT = BN / 128;                    // B sub-tiles per stage
-  constexpr int NST = t5_nst<BN>();
+  constexpr int NST = T5_NST;
   constexpr int STAGE_HALVES = (1 + NBT) * S16_TILE_HALVES;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // [0, 1024): barriers + TMEM address; ring at 1024 (1024-aligned tiles); zero piece after it
@@ -346,9 +137,13 @@ __global__ void __launch_bounds__(T5_THREADS, 1) screen16_tc_kernel(const Screen
   __half* ring = (__half*)(smem_raw + 1024);
   double* zbuf = (double*)(ring + (size_t)NST * STAGE_HALVES);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nT = P.ntb, nchunk = P.nchunk64;
-  if (P.zero_ptr)
+  const int nchunk = P.nchunk64;
+  if (P.zero_ptr) {
     for (int e = tid; e < S16_ZPIECE; e += blockDim.x) zbuf[e] = 0.0;
+    // the producer's bulk stores (async proxy) read zbuf: every writer orders its generic-proxy
+    // stores before them, then the barrier below publishes that to the producer
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(&full[s])), "r"(1));
@@ -381,7 +176,7 @@ __global__ void __launch_bounds__(T5_THREADS, 1) screen16_tc_kernel(const Screen
       const size_t zquota = zero_quota(P, npieces, nchunk);
       for (int t = P.tile_begin + blockIdx.x; t < P.tile_end; t += gridDim.x) {
         int I, Jb;
-        t5_tile<BN>(t, nT, I, Jb);
+        wide_tile(t, I, Jb);
         for (int q = 0; q < nchunk; ++q) {
           mbar_wait_s(&empty[s], ph ^ 1u);
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(&full[s])),
@@ -457,7 +252,7 @@ __global__ void __launch_bounds__(T5_THREADS, 1) screen16_tc_kernel(const Screen
     uint32_t ph_tf[2] = {0u, 0u};
     for (int t = P.tile_begin + blockIdx.x; t < P.tile_end; t += gridDim.x, ++it) {
       int I, Jb;
-      t5_tile<BN>(t, nT, I, Jb);
+      wide_tile(t, I, Jb);
       const int ab = it & 1;
       mbar_wait_s(&tfull[ab], ph_tf[ab]);
       ph_tf[ab] ^= 1u;
@@ -479,8 +274,14 @@ __global__ void __launch_bounds__(T5_THREADS, 1) screen16_tc_kernel(const Screen
               "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        if (jok && P.acc_out) {   // (test-only: the raw accumulators n R_hat_jc)
+          const int c0 = Jb * BN + 32 * cg;
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            P.acc_out[(size_t)(c0 + i) * (size_t)P.acc_ld + (size_t)j] = __uint_as_float(v[i]);
+        }
         if (jok) {
-          // thresholds as in screen16_kernel; the 32 columns' factors are warp-uniform loads
+          // the certification threshold (header); the 32 columns' factors are warp-uniform loads
           const int c0 = Jb * BN + 32 * cg;
           const bool diag_sub = (c0 >> 7) == I;           // the 128 x 128 diagonal sub-block
           const float4* iv = reinterpret_cast<const float4*>(P.inv_sq + c0);
@@ -534,22 +335,6 @@ __global__ void cand_compact_kernel(const uint8_t* __restrict__ cand, int p, int
   }
 }
 
-__global__ void sqrt_kernel(const double* __restrict__ in, double* __restrict__ out,
-                            float* __restrict__ inv_sq, float* __restrict__ lam_n, double lambda0,
-                            int n, int p, int p_pad) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < p) {
-    const double q = sqrt(in[k]);
-    out[k] = q;
-    // directed roundings: the epilogue's f32 threshold may only come out smaller
-    inv_sq[k] = __double2float_rd(1.0 / q * (1.0 - 0x1p-40));
-    lam_n[k] = __double2float_rd((double)n * lambda0 / q * (1.0 - 0x1p-40));
-  } else if (k < p_pad) {   // padding columns never flag (threshold +inf), padding rows are skipped
-    inv_sq[k] = __int_as_float(0x7f800000);
-    lam_n[k] = 0.f;
-  }
-}
-
 }  // namespace
 
 cudaError_t launch_cand_compact(const uint8_t* cand, int p, int* U, int* nU, int* gstate,
@@ -558,22 +343,6 @@ cudaError_t launch_cand_compact(const uint8_t* cand, int p, int* U, int* nU, int
   if (ce < 0) ce = p;
   cand_compact_kernel<<<blocks, 256, 0, s>>>(cand, p, cb, ce, U, nU, gstate);
   return cudaGetLastError();
-}
-
-cudaError_t launch_sqrt(const double* in, double* out, float* inv_sq, float* lam_n,
-                        double lambda0, int n, int p, int p_pad, cudaStream_t s) {
-  sqrt_kernel<<<(p_pad + 255) / 256, 256, 0, s>>>(in, out, inv_sq, lam_n, lambda0, n, p, p_pad);
-  return cudaGetLastError();
-}
-
-// which tcgen05 tile width runs (256 default; SPMESL_S16_BN=128 for the square-tile variant)
-static int s16_bn() {
-  static const int bn = getenv("SPMESL_S16_BN") ? atoi(getenv("SPMESL_S16_BN")) : 256;
-  return bn == 128 ? 128 : 256;
-}
-static bool s16_mma_sync() {
-  static const bool v = getenv("SPMESL_S16_MMA_SYNC") && atoi(getenv("SPMESL_S16_MMA_SYNC"));
-  return v;
 }
 
 // Y16 holds an even number of 128-row tiles (the 256-column blocks read two; the padding
@@ -592,48 +361,20 @@ int64_t screen16_pad(int64_t p) { return (p + 2 * S16_TB - 1) / (2 * S16_TB) * (
 
 int screen16_tile_count(int64_t p) {
   const int64_t nT = (p + S16_TB - 1) / S16_TB;
-  if (s16_mma_sync() || s16_bn() == 128) return (int)(nT * (nT + 1) / 2);
   const int64_t ncb = (nT + 1) / 2;
   int64_t tot = 0;
   for (int64_t jb = 0; jb < ncb; ++jb) tot += std::min<int64_t>(2 * jb + 2, nT);
   return (int)tot;
 }
 
-cudaError_t launch_to_f16(const double* Xb, const double* nrm, int p, int n_pad, int nchunk32,
-                          __half* Y16, cudaStream_t s) {
-  const int nb = (p + 2 * S16_TB - 1) / (2 * S16_TB) * 2;
-  const int nc = (n_pad + S16_KC - 1) / S16_KC;
-  dim3 grid((unsigned)nb, (unsigned)nc);
-  to_f16_kernel<<<grid, 256, 0, s>>>(Xb, nrm, p, nchunk32, nc, Y16);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_screen16(const Screen16Params& P, int grid, cudaStream_t s) {
   if (P.tile_end <= P.tile_begin) return cudaSuccess;
-  if (!s16_mma_sync()) {   // tcgen05 (default)
-    static_assert(T5_EPI_WARPS == 8, "epilogue: two warps per TMEM lane quarter");
-    if (s16_bn() == 256) {
-      cudaError_t e = cudaFuncSetAttribute(screen16_tc_kernel<256>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)t5_smem<256>());
-      if (e != cudaSuccess) return e;
-      screen16_tc_kernel<256><<<grid, T5_THREADS, t5_smem<256>(), s>>>(P);
-    } else {
-      cudaError_t e = cudaFuncSetAttribute(screen16_tc_kernel<128>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)t5_smem<128>());
-      if (e != cudaSuccess) return e;
-      screen16_tc_kernel<128><<<grid, T5_THREADS, t5_smem<128>(), s>>>(P);
-    }
-    return cudaGetLastError();
-  }
-  const size_t smem = 128 + (size_t)S16_NST * 2 * S16_TILE_HALVES * 2 + (size_t)S16_ZPIECE * 8;
-  cudaError_t e = cudaFuncSetAttribute(screen16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  static_assert(T5_EPI_WARPS == 8, "epilogue: two warps per TMEM lane quarter");
+  cudaError_t e = cudaFuncSetAttribute(screen16_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)t5_smem());
   if (e != cudaSuccess) return e;
-  screen16_kernel<<<grid, S16_THREADS, smem, s>>>(P);
+  screen16_tc_kernel<<<grid, T5_THREADS, t5_smem(), s>>>(P);
   return cudaGetLastError();
 }
-
 
 }  // namespace spmesl

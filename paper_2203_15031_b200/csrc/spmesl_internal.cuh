@@ -82,8 +82,6 @@ struct CDParams {
                            //   solver (0: never)
   int* tail_count;         // number of columns handed over
   TailState* tail;         // [ncols]
-  int debug;               // development timing switches (SPMESL_CD_DEBUG; 0 in production)
-  long long* dbg;          // development phase timers (debug & 4)
   int* queue;              // atomic head (queue index)
   int* flags;              // FLAG_*
   const int* err_in;       // standardization error code (CD exits early when nonzero)
@@ -189,19 +187,17 @@ struct Screen16Params {
   double* zero_ptr;        // optional Theta zero fill (as GramParams)
   size_t zero_count;
   double* zero_last;       // optional: one more double to zero (odd Theta sizes)
+  float* acc_out;          // optional (tests): raw accumulators n R_hat_jc at [c * acc_ld + j]
+  int64_t acc_ld;
 };
 size_t screen16_y_halves(int64_t p, int n_pad);
 int screen16_tile_count(int64_t p);
 int64_t screen16_pad(int64_t p);   // p rounded up to the 128-column tiles
 double screen16_eps(int n_pad);
-cudaError_t launch_to_f16(const double* Xb, const double* nrm, int p, int n_pad, int nchunk32,
-                          __half* Y16, cudaStream_t s);
 cudaError_t launch_screen16(const Screen16Params& P, int grid, cudaStream_t s);
 // candidates restricted to the columns [cb, ce) (ce < 0: all p); gstate[c] = 2 for those, else 0
 cudaError_t launch_cand_compact(const uint8_t* cand, int p, int* U, int* nU, int* gstate,
                                 cudaStream_t s, int cb = 0, int ce = -1);
-cudaError_t launch_sqrt(const double* in, double* out, float* inv_sq, float* lam_n,
-                        double lambda0, int n, int p, int p_pad, cudaStream_t s);
 cudaError_t launch_syrk_screen(const GramParams& P, int grid, cudaStream_t s);
 cudaError_t launch_gram_init(const GramParams& P, cudaStream_t s);
 cudaError_t launch_level_flags(const GramParams& P, cudaStream_t s);

@@ -667,8 +667,6 @@ cudaError_t launch_gram_cols(const double* Xb, int nblk, int nchunk, int n, int 
     cudaFuncAttributes fa;
     if (cudaFuncGetAttributes(&fa, gram_cols_kernel) != cudaSuccess) return cudaGetLastError();
     max_warps = std::max(1, std::min(GC_MAXW, fa.maxThreadsPerBlock / 32));
-    if (getenv("SPMESL_DEV_GC_DEBUG"))
-      fprintf(stderr, "gram_cols: maxThreadsPerBlock %d numRegs %d\n", fa.maxThreadsPerBlock, fa.numRegs);
   }
   const int nmt = (p + 7) / 8;
   const int T = std::max(1, std::min(max_warps, (nmt + sms - 1) / sms));
@@ -689,8 +687,7 @@ cudaError_t launch_gram_pass(const double* Xb, int nblk, int nchunk, int n, int 
                              uint8_t* hit, const double* lams, int nlam) {
   const int ntile = (M + nU + 31) / 32;
   if (ntile == 0) return cudaSuccess;
-  static const bool old_pass = getenv("SPMESL_DEV_OLD_GRAM_PASS") != nullptr;   // (dev)
-  if (M == 0 && !old_pass)
+  if (M == 0)
     return launch_gram_cols(Xb, nblk, nchunk, n, p, U, nU, nullptr, 0, Gtab, hit, lams, nlam,
                             nullptr, s);
   dim3 grid((unsigned)nblk, (unsigned)ntile);
@@ -716,8 +713,7 @@ cudaError_t launch_tail_sweeps(const TailParams& P, int grid, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   // 512 threads when a single column CTA owns the SM (large p: the search rounds and the z
   // updates split over twice the threads), 256 when two share it
-  static const int nt_env = getenv("SPMESL_TAIL_NT") ? atoi(getenv("SPMESL_TAIL_NT")) : 0;
-  const bool wide = nt_env ? nt_env == 512 : P.occ == 1;
+  const bool wide = P.occ == 1;
   if (wide) {
     cudaError_t e2 = cudaFuncSetAttribute(tail_sweep_kernel<512>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -107,6 +107,12 @@ def fit_distributed(X: torch.Tensor, lambda0: float, tol: float = 1e-4, max_iter
     "residual"."""
     from . import (as_colmajor, assemble_device, fit_columns_device, fit_columns_gram_device,
                    gram_screen_device, gram_supported, gram_tile_count)
+    if stream is not None:
+        # every library call, collective and torch op of this fit on the caller's stream, in
+        # order (a collective's result is read by the next library call)
+        with torch.cuda.stream(stream):
+            return fit_distributed(X, lambda0, tol, max_iter, group=group, stream=None,
+                                   solver=solver, **options)
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     n, p = X.shape
     c0, c1 = column_range(p, rank, world)

@@ -71,7 +71,7 @@ def test_bit_identical_across_tile_sizes(S, oracle, T):
     assert np.array_equal(r.sweeps, ref.sweeps)
 
 
-@pytest.mark.parametrize("solver", ["residual", "gram"])
+@pytest.mark.parametrize("solver", ["residual", "gram", "gram16", "auto"])
 def test_theta1_unsymmetrized_and_unstandardized(S, oracle, solver):
     X, _, _ = G.make_config(2)
     n, p = X.shape
@@ -127,7 +127,7 @@ def test_column_blocks_reproduce_full_fit(S, oracle):
     assert np.array_equal(th2.cpu().numpy(), full.Theta[:, 300:700])
 
 
-@pytest.mark.parametrize("solver", ["residual", "gram"])
+@pytest.mark.parametrize("solver", ["residual", "gram", "gram16", "auto"])
 def test_null_case_and_small_p(S, oracle, solver):
     rng = np.random.default_rng(5)
     for (n, p) in [(7, 2), (33, 3), (64, 31), (65, 33), (40, 129)]:
@@ -138,7 +138,7 @@ def test_null_case_and_small_p(S, oracle, solver):
             assert_parity(compare(r.Theta, r.sigma, r.iters, r.sweeps, ora))
 
 
-@pytest.mark.parametrize("solver", ["residual", "gram"])
+@pytest.mark.parametrize("solver", ["residual", "gram", "gram16", "auto"])
 def test_errors(S, solver):
     X = np.random.default_rng(1).standard_normal((20, 40))
     X[:, 17] = 2.5
@@ -157,7 +157,7 @@ def test_errors(S, solver):
     S.fit(X, 0.3, solver=solver)
 
 
-@pytest.mark.parametrize("solver", ["residual", "gram"])
+@pytest.mark.parametrize("solver", ["residual", "gram", "gram16", "auto"])
 def test_max_iter_cap_flags_columns(S, oracle, solver):
     X, _, _ = G.make_config(2)
     lam = oracle.lambda_univ(*X.shape)
@@ -232,10 +232,19 @@ def test_two_ranks_sharing_one_gpu_match_single_fit(S, oracle, solver):
     for pr in procs:
         pr.join(timeout=60)
         assert pr.exitcode == 0
+    ora = oracle.spmesl_fit(X, lam)
     for rank, (c0, c1), th, sg, it, sw in res:
         assert np.array_equal(th, full.Theta[:, c0:c1])
         assert np.array_equal(sg, full.sigma[c0:c1])
         assert np.array_equal(it, full.iters[c0:c1]) and np.array_equal(sw, full.sweeps[c0:c1])
+        # each rank's column block against the oracle directly
+        cols = np.arange(c0, c1)
+        rep = compare(np.concatenate([np.zeros((th.shape[0], c0)), th,
+                                      np.zeros((th.shape[0], X.shape[1] - c1))], axis=1),
+                      np.concatenate([ora.sigma[:c0], sg, ora.sigma[c1:]]),
+                      np.concatenate([ora.outer[:c0], it, ora.outer[c1:]]),
+                      np.concatenate([ora.sweeps[:c0], sw, ora.sweeps[c1:]]), ora, cols=cols)
+        assert_parity(rep)
 
 
 @pytest.mark.parametrize("tail_after", [0, 1, 3])
@@ -279,7 +288,7 @@ def test_tail_solver_on_demand_gram_columns(S, oracle):
         assert np.all(np.abs(got - want) <= 1e-8 * np.abs(want) + 1e-12 * abs(want[k])), k
 
 
-@pytest.mark.parametrize("solver", ["residual", "gram"])
+@pytest.mark.parametrize("solver", ["residual", "gram", "gram16", "auto"])
 @pytest.mark.parametrize("mi", [1, 100])
 def test_unstandardized_scaled_columns_and_caps(S, oracle, solver, mi):
     # standardize = 0 with column norms ||x_k||^2 / n in [0.64, 1.44] (sigma of a column whose
@@ -459,42 +468,6 @@ def test_graph_replay_matches_eager(S, oracle):
     assert torch.equal(r.Theta, e.Theta) and torch.equal(r.sweeps, e.sweeps)
 
 
-@pytest.mark.parametrize("env", [{"SPMESL_S16_MMA_SYNC": "1"}, {"SPMESL_S16_BN": "128"},
-                                 {"SPMESL_S16_ZFRAC": "0.4"}, {"SPMESL_NO_GRAPH": "1"}])
-def test_screening_variants_identical(S, oracle, env, tmp_path):
-    """The alternative screening kernels (mma.sync; 128 x 128 tcgen05 tiles), the split Theta
-    zero fill and the eager (no-graph) path give the default fit bit for bit (each runs in a
-    fresh process: the switches are read once)."""
-    import subprocess, sys, os, torch
-    X, _, _ = G.make_config(5, p=4000)
-    n, p = X.shape
-    lam = oracle.lambda_ub(n, p)
-    np.save(tmp_path / "X.npy", X)
-    code = f"""
-import numpy as np, torch, sys
-sys.path.insert(0, {ROOT!r})
-import paper_2203_15031_b200 as S
-X = np.load({str(tmp_path / 'X.npy')!r})
-Xd = torch.from_numpy(np.ascontiguousarray(X.T)).cuda().t()
-out = dict(theta=torch.empty(({p}, {p}), dtype=torch.float64, device="cuda"),
-           sigma=torch.empty({p}, dtype=torch.float64, device="cuda"),
-           iters=torch.empty({p}, dtype=torch.int32, device="cuda"),
-           sweeps=torch.empty({p}, dtype=torch.int32, device="cuda"),
-           conv=torch.empty({p}, dtype=torch.uint8, device="cuda"))
-for _ in range(3):
-    r = S.fit_device(Xd, {lam!r}, out=out)
-np.save({str(tmp_path / 'T.npy')!r}, r.Theta.cpu().numpy())
-np.save({str(tmp_path / 'sw.npy')!r}, r.sweeps.cpu().numpy())
-"""
-    e = dict(os.environ)
-    e.update(env)
-    subprocess.run([sys.executable, "-c", code], check=True, env=e, timeout=600)
-    Xd = torch.from_numpy(np.ascontiguousarray(X.T)).cuda().t()
-    ref = S.fit_device(Xd, lam, eager=True)
-    assert np.array_equal(np.load(tmp_path / "T.npy"), ref.Theta.cpu().numpy())
-    assert np.array_equal(np.load(tmp_path / "sw.npy"), ref.sweeps.cpu().numpy())
-
-
 @pytest.mark.parametrize("solver,mode,cfg,over,sym", [
     ("auto", "per_column", 5, dict(p=3000), True),
     ("auto", "per_column", 4, dict(p=777, n=203), True),     # ragged, multi-sweep
@@ -546,3 +519,97 @@ def test_degenerate_penalties_closed_forms(S, oracle, solver):
     r = S.fit(X, big, solver=solver)
     np.testing.assert_allclose(r.Theta, np.diag(1.0 / Sn.diagonal()), rtol=1e-12, atol=0)
     assert np.all(r.iters <= 2)
+
+
+@pytest.mark.parametrize("solver", ["residual", "gram", "gram16", "auto"])
+def test_sigma_floor_binds(S, oracle, solver):
+    """The sigma floor (reading g5) applied identically on both sides where it binds:
+    sigma_floor = 0.9 on config 2 at lambda_univ clamps the columns whose residual scale
+    ||r||/sqrt(n) falls below 0.9 (their lambda is then 0.9 lambda0)."""
+    X, _, _ = G.make_config(2)
+    n, p = X.shape
+    lam = oracle.lambda_univ(n, p)
+    ora = oracle.spmesl_fit(X, lam, sigma_floor=0.9)
+    Xs, mu, s = oracle.standardize(X)
+    clamped = np.isclose(ora.sigma / s, 0.9, rtol=0, atol=1e-15)
+    assert clamped.sum() > 10, clamped.sum()          # the floor really binds
+    r = S.fit(X, lam, sigma_floor=0.9, solver=solver)
+    assert_parity(compare(r.Theta, r.sigma, r.iters, r.sweeps, ora))
+    # and the unclamped fit differs on those columns (the branch changes the result)
+    free = oracle.spmesl_fit(X, lam)
+    assert np.any(free.sigma[clamped] < ora.sigma[clamped])
+
+
+@pytest.mark.parametrize("solver", ["residual", "gram16"])
+def test_near_constant_column_rule(S, oracle, solver):
+    """The constant-column rule s_k <= 1e-13 max_i |x_ik| (reading g15) on both sides: a
+    column 10x below the threshold is an error (the same column on both sides), one 10x above
+    is fitted without error by both."""
+    rng = np.random.default_rng(3)
+    n, p = 100, 40
+    X = rng.standard_normal((n, p))
+    for a, constant in ((1e-14, True), (1e-12, False)):
+        Y = X.copy()
+        Y[:, 13] = 1.0 + a * rng.standard_normal(n)
+        if constant:
+            with pytest.raises(oracle.OracleError) as eo:
+                oracle.spmesl_fit(Y, 0.3)
+            with pytest.raises(S.SpmeslError) as eg:
+                S.fit(Y, 0.3, solver=solver)
+            assert eo.value.code == -2 and eg.value.code == -2
+            assert eo.value.bad_col == 13 and eg.value.bad_column == 13
+        else:
+            ora = oracle.spmesl_fit(Y, 0.3)
+            r = S.fit(Y, 0.3, solver=solver)
+            assert ora.code >= 0 and r.code >= 0
+            assert np.all(np.isfinite(r.Theta)) and np.all(np.isfinite(r.sigma))
+
+
+def _bare_fit(S, X, lam, tol=1e-4, max_iter=100):
+    """spmesl_fit (the BASELINE.json signature) through ctypes with host buffers."""
+    import ctypes
+    X = np.asfortranarray(X, dtype=np.float64)
+    n, p = X.shape
+    Theta = np.empty((p, p), order="F")
+    sigma = np.empty(p)
+    iters = np.empty(p, np.int32)
+    rc = S.load().spmesl_fit(ctypes.c_void_p(X.ctypes.data), n, p, float(lam), float(tol),
+                             int(max_iter), ctypes.c_void_p(Theta.ctypes.data),
+                             ctypes.c_void_p(sigma.ctypes.data), ctypes.c_void_p(iters.ctypes.data))
+    return rc, Theta, sigma, iters
+
+
+@pytest.mark.parametrize("cfg,over", [(2, {}), (5, dict(p=3000))])
+def test_bare_spmesl_fit_signature(S, oracle, cfg, over):
+    X, _, spec = G.make_config(cfg, **over)
+    n, p = X.shape
+    lam = oracle.lambda_univ(n, p) if spec["rule"] == "univ" else oracle.lambda_ub(n, p)
+    ora = oracle.spmesl_fit(X, lam)
+    rc, Theta, sigma, iters = _bare_fit(S, X, lam)
+    assert rc == (1 if not ora.converged.all() else 0)
+    assert np.array_equal(iters, ora.outer)
+    # (sweeps are not returned by the bare signature: iters + Theta + sigma are compared)
+    rep = compare(Theta, sigma, iters, ora.sweeps, ora)
+    rep["sweeps_mismatch"] = []
+    assert_parity(rep)
+
+
+def test_bare_spmesl_fit_status_codes(S, oracle):
+    """Every status code the BASELINE-signature entry point can return on this path."""
+    X, _, _ = G.make_config(2)
+    n, p = X.shape
+    lam = oracle.lambda_univ(n, p)
+    assert _bare_fit(S, X, lam)[0] == 0                               # SPMESL_OK
+    rc, _, _, iters = _bare_fit(S, X, lam, max_iter=1)                # outer cap hit
+    assert rc == 1 and iters.max() == 1                               # SPMESL_WARN_NOT_CONVERGED
+    assert _bare_fit(S, X, -1.0)[0] == -1                             # SPMESL_ERR_ARG
+    assert _bare_fit(S, X, lam, tol=0.0)[0] == -1
+    assert _bare_fit(S, X, lam, max_iter=0)[0] == -1
+    assert _bare_fit(S, X[:1], lam)[0] == -1                          # n < 2
+    Y = X.copy()
+    Y[:, 7] = 3.0
+    assert _bare_fit(S, Y, lam)[0] == -2                              # SPMESL_ERR_CONSTANT_COLUMN
+    Y = X.copy()
+    Y[5, 9] = np.nan
+    assert _bare_fit(S, Y, lam)[0] == -3                              # SPMESL_ERR_NONFINITE
+    assert _bare_fit(S, X, lam)[0] == 0                               # and it recovers
