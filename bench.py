@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-per-config", action="store_true")
+    ap.add_argument("--per-config-seeds", type=int, default=3)
     ap.add_argument("--mode", default="per_column", choices=["per_column", "joint"],
                     help="per_column (default; Alg. 1/2 stop) or joint (Algorithm 3, P:938-990)")
     ap.add_argument("--solver", default="auto", choices=["auto", "residual", "gram", "gram16"])
@@ -203,7 +205,93 @@ def cpu_baseline(X, lam, seconds, seed=0):
     v = sweeps * (p - 1)
     return {"value": v / t_tot, "unit": UNIT, "cores": threads, "kind": "oracle",
             "sample": f"{done} of {p} columns (each with all p-1 predictors), {t_tot:.1f} s",
-            "seconds": t_tot, "columns": done, "sweeps": sweeps}
+            "seconds": t_tot, "columns": done, "sweeps": sweeps, "cols": order[:done]}
+
+
+# ----------------------------------------------------------------------------- per-config block
+PER_CONFIG = [
+    # (label, BASELINE config, generator overrides, penalty rule)
+    ("config 4: n=400, p=5000, band(3), lambda_ub", 4, {"family": "band3"}, "ub"),
+    ("config 4: n=400, p=5000, hub, lambda_ub", 4, {"family": "hub"}, "ub"),
+    ("config 5: n=500, p=20000, ER, lambda_univ", 5, {}, "univ"),
+]
+
+
+def l2_read_peak():
+    """Measured L2 read bandwidth of this pool's B200 (microbench/peaks.cu, profiles/)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "r01_peaks_microbench.json")))
+        return float(d["l2_read_gbs"]), "profiles/r01_peaks_microbench.json l2_read_gbs (measured)"
+    except Exception:
+        return 16700.0, "fallback 16.7 TB/s (round-1 microbench)"
+
+
+def per_config_block(S, dev, stream, flush, seeds=3, fits=5):
+    """The rest of the metric's range (p = 5k-20k, BASELINE configs 4 and 5 at the paper's
+    recommended lambda_univ): per workload and seed, the device time per fit
+    (CUDA-graph replays, L2 flushed before each, CUDA events on the launching stream), the
+    algorithmic coordinate updates per second, the sweep counts, and the covariance-update sweep
+    kernel's own time from an eager fit with its L2 fraction (8 p bytes of Gram column per
+    coordinate change + 8 p per column for its z, over the measured L2 read bandwidth).
+    Mean +- SE over `seeds` datasets (P:1121-1127 reports means over datasets)."""
+    import torch
+    from synth import generators as G
+    l2pk, l2src = l2_read_peak()
+    out = []
+    for label, cfg, over, rule in PER_CONFIG:
+        rows = []
+        for k in range(seeds):
+            X, _, spec = G.make_config(cfg, seed=2203 + cfg + 1000 * k, **over)
+            n, p = X.shape
+            lam = S.lambda_ub(n, p) if rule == "ub" else S.lambda_univ(n, p)
+            Xd = torch.from_numpy(np.ascontiguousarray(X.T)).to(dev).t()
+            ob = dict(theta=torch.empty((p, p), dtype=torch.float64, device=dev),
+                      sigma=torch.empty(p, dtype=torch.float64, device=dev),
+                      iters=torch.empty(p, dtype=torch.int32, device=dev),
+                      sweeps=torch.empty(p, dtype=torch.int32, device=dev),
+                      conv=torch.empty(p, dtype=torch.uint8, device=dev))
+            eager = S.fit_device(Xd, lam, TOL, MAX_ITER, stream=stream, out=ob, eager=True)
+            st = eager.stats
+            for _ in range(3):      # (the second call captures the graph)
+                S.fit_device(Xd, lam, TOL, MAX_ITER, stream=stream, out=ob)
+            e0 = [torch.cuda.Event(enable_timing=True) for _ in range(fits)]
+            e1 = [torch.cuda.Event(enable_timing=True) for _ in range(fits)]
+            for i in range(fits):
+                flush.fill_(i % 255 + 1)
+                torch.cuda.synchronize()
+                e0[i].record(stream)
+                S.fit_device(Xd, lam, TOL, MAX_ITER, stream=stream, out=ob)
+                e1[i].record(stream)
+                torch.cuda.synchronize()
+            ms = float(np.median([a.elapsed_time(b) for a, b in zip(e0, e1)]))
+            sweep_ms = float(st.get("ms_tail", 0.0))
+            sweep_bytes = 8.0 * p * (st.get("tail_changes", 0) + st.get("tail_columns", 0))
+            rows.append(dict(ms=ms, ups=st["coord_updates"] / (ms / 1000.0),
+                             sweeps=st["total_sweeps"], max_sweeps=st["max_sweeps"],
+                             multi=st["tail_columns"], nnz=st["nnz"], sweep_ms=sweep_ms,
+                             l2=(sweep_bytes / (sweep_ms / 1000.0) / 1e9 / l2pk) if sweep_ms > 0 else None,
+                             changes=st.get("tail_changes", 0), cand=st.get("screen_candidates"),
+                             seed=spec["seed"]))
+            del ob, Xd
+        def ms_se(key):
+            v = np.array([r[key] for r in rows], dtype=np.float64)
+            return float(v.mean()), float(v.std(ddof=1) / np.sqrt(len(v))) if len(v) > 1 else 0.0
+        fit_ms, fit_se = ms_se("ms")
+        ups, ups_se = ms_se("ups")
+        sw_ms, sw_se = ms_se("sweep_ms")
+        out.append({"workload": label, "n": n, "p": p, "lambda0_rule": rule, "seeds": [r["seed"] for r in rows],
+                    "fit_ms": fit_ms, "fit_ms_se": fit_se, "value": ups, "value_se": ups_se,
+                    "unit": UNIT, "sweeps_total": [r["sweeps"] for r in rows],
+                    "max_sweeps": [r["max_sweeps"] for r in rows],
+                    "multi_sweep_columns": [r["multi"] for r in rows], "nnz": [r["nnz"] for r in rows],
+                    "screen_candidates": [r["cand"] for r in rows],
+                    "sweep_kernel": {"kernel": "tail_sweep_kernel", "ms": sw_ms, "ms_se": sw_se,
+                                     "bound": "l2", "changes": [r["changes"] for r in rows],
+                                     "algorithmic": "8 p bytes of Gram column per coordinate change + 8 p per column (its z)",
+                                     "frac_of_l2": [r["l2"] for r in rows], "peak_gbs": l2pk,
+                                     "peak_source": l2src,
+                                     "timing": "eager fit (CUDA events around the kernel)"}})
+    return out
 
 
 # ----------------------------------------------------------------------------- main arms
@@ -468,9 +556,17 @@ def run_ours(args):
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e_tot,
                "api": "spmesl_fit_ex (host pointers)" if world == 1 else
                       "fit_distributed with host pinned H2D/D2H"}
+    per_config = None
+    if world == 1 and not args.no_per_config and args.mode == "per_column" and args.solver == "auto":
+        per_config = per_config_block(S, dev, stream, flush, seeds=args.per_config_seeds)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.mode == "per_column":
         cpu = cpu_baseline(X, lam, args.cpu_seconds)
+        # the GPU's sweep total on the same columns (same algorithmic work, per-column counts
+        # are identical to the oracle's: tests/test_gpu_fullsize.py)
+        gsw = res.sweeps.cpu().numpy() if world == 1 else None
+        if gsw is not None:
+            cpu["gpu_sweeps_same_columns"] = int(gsw[cpu["cols"]].sum())
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
@@ -492,6 +588,10 @@ def run_ours(args):
                 "graph_replay": bool(stats_last.get("graph_replay", 0))}
         if cpu:
             line["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            line["cpu_baseline"]["oracle_sweeps"] = cpu["sweeps"]
+            line["cpu_baseline"]["gpu_sweeps_same_columns"] = cpu.get("gpu_sweeps_same_columns")
+        if per_config is not None:
+            line["per_config"] = per_config
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

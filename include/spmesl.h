@@ -128,6 +128,12 @@ typedef struct {
   int32_t graph_replay;   /* 1 if this call ran as one CUDA-graph launch (options.eager); then
                              only ms_total and ms_screen are measured, the other ms_* read -1 */
   int32_t pad1;
+  int64_t tail_changes;   /* coordinate changes (b_jk moved) made by the covariance-update sweep
+                             kernel; each reads one Gram column (8 p bytes: its algorithmic
+                             traffic) */
+  int64_t tail_passes;    /* segments (speculative chain + one pass over the rows) the sweep
+                             kernel ran: one per sweep plus one per row that entered the support
+                             within a sweep */
 } spmesl_stats;
 
 /* Fill *opt with the defaults listed above. */

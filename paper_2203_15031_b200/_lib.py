@@ -66,6 +66,8 @@ class Stats(ctypes.Structure):
         ("screen_fill_bytes", ctypes.c_int64),
         ("graph_replay", ctypes.c_int32),
         ("pad1", ctypes.c_int32),
+        ("tail_changes", ctypes.c_int64),
+        ("tail_passes", ctypes.c_int64),
     ]
 
     def asdict(self):

@@ -57,6 +57,8 @@ struct DevCounters {
   int s16_nU, pad5;                // solver 3: candidate columns of the certified screening
   int joint_nslots, joint_nwork;   // mode 1 on the Gram form: sweep slots, slots this sweep
   unsigned long long t_start, t_end;   // device clock (ns) at the fit's first / last kernel
+  unsigned long long tail_changes;     // coordinate changes made by the sweep kernel
+  unsigned long long tail_passes;      // its chain + pass segments
 };
 
 struct Buffer {
@@ -227,17 +229,17 @@ struct FitOut {
   uint8_t* conv;
 };
 
-// Gram-column prefetch in the sweep kernel when two p-vectors fit in shared memory and the
-// columns are 16-byte aligned (p even).
-// Sweep-kernel launch shape: two column CTAs per SM whenever their state fits side by side
-// (their latency-bound search rounds and barriers interleave: config 4 band 3.1 -> 2.0 ms), else
-// one CTA per SM with the Gram columns of the current nonzeros prefetched into shared memory.
-void set_prefetch(const Workspace& W, TailParams& T) {
+// Sweep-kernel launch shape: two column CTAs per SM whenever their state fits side
+// by side (their latency-bound chains and passes interleave), preferably each with the second z
+// buffer (a pass without a new row then commits by swapping buffers instead of re-reading the
+// chain's Gram columns in the next pass); else one CTA of 512 threads per SM.
+void set_tail_shape(const Workspace& W, TailParams& T) {
   const size_t base = tail_smem_bytes(T.p, T.n_pad, T.nzcap);
-  const bool two = 2 * (base + 1024) <= (size_t)W.smem_sm;
-  T.occ = two ? 2 : 1;
-  T.prefetch = T.occ == 1 && (T.p % 2 == 0) &&
-               base + tail_prefetch_bytes(T.p) <= (size_t)W.smem_optin;
+  const size_t z2b = tail_z2_bytes(T.p);
+  const size_t sm = (size_t)W.smem_sm, optin = (size_t)W.smem_optin;
+  if (2 * (base + z2b + 1024) <= sm && base + z2b <= optin) { T.occ = 2; T.z2 = 1; }
+  else if (2 * (base + 1024) <= sm) { T.occ = 2; T.z2 = 0; }
+  else { T.occ = 1; T.z2 = base + z2b <= optin ? 1 : 0; }
 }
 
 bool tail_enabled(const Workspace& W, const spmesl_options& o, const Layout& L, int nzcap) {
@@ -302,11 +304,12 @@ int run_tail(Workspace& W, const Layout& L, int64_t cb, double lambda0, double t
   T.next = &dc->tail_next;
   T.ondemand_count = &dc->gram_ondemand;
   T.sweeps_count = &dc->tail_sweeps;
+  T.changes_count = &dc->tail_changes;
   T.flags = &dc->err;
   T.nz_rows = (int*)W.nz_rows.ptr; T.nz_vals = (double*)W.nz_vals.ptr;
   T.nz_count = (int*)W.nz_count.ptr; T.nz_cur = (int*)W.nz_cur.ptr;
   T.sigma_std = out.sigma_std; T.iters = out.iters; T.sweeps = out.sweeps; T.converged = out.conv;
-  set_prefetch(W, T);
+  set_tail_shape(W, T);
   CUDA_TRY(launch_tail_sweeps(T, grid, s));
   CUDA_TRY(ev_record(W, W.ev[6], s));   // end of the tail solver
   if (st) { st->tail_columns = M; st->kernel_launches += 4; }
@@ -769,12 +772,13 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   T.next = &dc->tail_next;
   T.ondemand_count = &dc->gram_ondemand;
   T.sweeps_count = &dc->tail_sweeps;
+  T.changes_count = &dc->tail_changes;
   T.flags = &dc->err;
   T.nz_rows = (int*)W.nz_rows.ptr; T.nz_vals = (double*)W.nz_vals.ptr;
   T.nz_count = (int*)W.nz_count.ptr; T.nz_cur = (int*)W.nz_cur.ptr;
   T.sigma_std = out.sigma_std; T.iters = out.iters; T.sweeps = out.sweeps; T.converged = out.conv;
   if (nlam > 1) { T.lambdas = (const double*)W.lam_dev.ptr; T.slot_stride = (int)p; }
-  set_prefetch(W, T);
+  set_tail_shape(W, T);
   CUDA_TRY(launch_tail_sweeps(T, (int)std::min<int64_t>(W.sms, p * nlam), s));
   CUDA_TRY(ev_record(W, W.ev[6], s));
   CUDA_TRY(ev_record(W, W.ev[2], s));
@@ -802,6 +806,8 @@ void gram_stats(Workspace& W, int64_t p, int nzcap, spmesl_stats* st, bool scree
   st->ms_tail = replay ? -1.0 : ev_ms(W.ev[5], W.ev[6]);
   st->tail_columns = W.host_counters->tail_count;
   st->tail_sweeps = W.host_counters->tail_sweeps;
+  st->tail_changes = (int64_t)W.host_counters->tail_changes;
+  st->tail_passes = (int64_t)W.host_counters->tail_passes;
 }
 
 // The Gram solver with its own synchronisation and coefficient-list regrowth (for callers that
@@ -934,6 +940,7 @@ int fit_joint_gram_core(Workspace& W, const double* dX, int64_t n, int64_t p, do
         T.next = &dc->tail_next;
         T.ondemand_count = &dc->gram_ondemand;
         T.sweeps_count = &dc->tail_sweeps;
+  T.changes_count = &dc->tail_changes;
         T.flags = &dc->err;
         T.nz_rows = (int*)W.nz_rows.ptr; T.nz_vals = (double*)W.nz_vals.ptr;
         T.nz_count = (int*)W.nz_count.ptr; T.nz_cur = (int*)W.nz_cur.ptr;
@@ -944,7 +951,7 @@ int fit_joint_gram_core(Workspace& W, const double* dX, int64_t n, int64_t p, do
         T.work = (const int*)W.jwork.ptr;
         T.Zj = (double*)W.zj.ptr;
         T.joint_maxd = &dc->joint_maxd;
-        set_prefetch(W, T);
+        set_tail_shape(W, T);
         CUDA_TRY(launch_tail_sweeps(T, (int)std::max(1, std::min(W.sms, nslots)), s));
         ++launches;
         ++joint_sweeps;
@@ -1406,11 +1413,12 @@ int fit_gram_columns_core(Workspace& W, const double* dX, int64_t n, int64_t p, 
     T.next = &dc->tail_next;
     T.ondemand_count = &dc->gram_ondemand;
     T.sweeps_count = &dc->tail_sweeps;
+  T.changes_count = &dc->tail_changes;
     T.flags = &dc->err;
     T.nz_rows = (int*)W.nz_rows.ptr; T.nz_vals = (double*)W.nz_vals.ptr;
     T.nz_count = (int*)W.nz_count.ptr; T.nz_cur = (int*)W.nz_cur.ptr;
     T.sigma_std = out.sigma_std; T.iters = out.iters; T.sweeps = out.sweeps; T.converged = out.conv;
-    set_prefetch(W, T);
+    set_tail_shape(W, T);
     CUDA_TRY(launch_tail_sweeps(T, (int)std::min<int64_t>(W.sms, m), s));
     CUDA_TRY(ev_record(W, W.ev[6], s));
     CUDA_TRY(ev_record(W, W.ev[2], s));

@@ -119,11 +119,12 @@ struct TailParams {
   int* next;               // atomic work counter
   int* ondemand_count;     // Gram columns computed on first use
   int* sweeps_count;       // sweeps performed here
+  unsigned long long* changes_count;   // optional [2]: coordinate changes (d != 0), passes
   int z_from_gtab;         // 1: z starts as Gtab[:, col] (Gram solver: b = 0, r = x~_c)
   int gtab_full;           // 1: every Gram column is present (no on-demand path)
   int occ;                 // column CTAs per SM the launch provides for (grid multiplier)
-  int prefetch;            // 1: stream the Gram columns of the current nonzeros into shared
-                           //    memory ahead of their visits (needs tail_prefetch_bytes more)
+  int z2;                  // 1: a second z buffer (tail_z2_bytes more shared memory): a pass
+                           //    that finds no new row swaps in z + all chain changes
   int* flags;
   int* nz_rows;            // column coefficient lists (as in CDParams)
   double* nz_vals;
@@ -211,7 +212,7 @@ constexpr int TAIL_MAXW = 16;
 constexpr int TAIL_SCAN = SPMESL_TAIL_SCAN_R * TAIL_THREADS;   // rows tested per search round
 constexpr int TAIL_ODC = 8;          // on-demand Gram column cache entries per CTA
 __host__ __device__ size_t tail_smem_bytes(int p, int n_pad, int nzcap);
-size_t tail_prefetch_bytes(int p);
+__host__ __device__ size_t tail_z2_bytes(int p);
 cudaError_t launch_tail_residuals(const double* Xb, const TailState* tail, int M, const int* nz_rows,
                                   const double* nz_vals, int nzcap, int64_t col_begin, int n,
                                   int n_pad, int nchunk, double* V, cudaStream_t s);
@@ -229,6 +230,7 @@ cudaError_t launch_gram_pass(const double* Xb, int nblk, int nchunk, int n, int 
 cudaError_t launch_tail_mark(const TailState* tail, int M, const int* nz_rows, int nzcap, int* umark,
                              cudaStream_t s);
 cudaError_t launch_tail_sweeps(const TailParams& P, int grid, cudaStream_t s);
+
 
 // Algorithm 3 joint mode helpers (joint.cu)
 cudaError_t launch_joint_live_init(const uint8_t* hit, int m, int* nslots, TailState* jtail,

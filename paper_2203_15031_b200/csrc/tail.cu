@@ -14,18 +14,16 @@
 // function of the column (the Gram columns come from one DMMA routine, whether precomputed in
 // the batched pass or computed on demand), so results do not depend on scheduling.
 //
-// Gram-column prefetch (TailParams::prefetch, when two p-vectors fit in shared memory): the rows
-// of the column's current nonzeros are visited in order every sweep and almost every visit
-// changes b_j, so the Gram columns of the next two such rows are streamed L2 -> shared memory
-// by cp.async.bulk while the sweep proceeds; the z update then reads shared memory instead of
-// paying an L2 round trip per change (the straggler columns of hub graphs make hundreds of
-// sweeps with ~10 changes each).
+// One sweep is processed as a speculative chain over the column's current nonzeros plus one
+// block-wide pass over the rows per segment (see "per-column sweeps" below), so the dependent
+// latency per sweep is a few passes, not one block-wide update and search per change.
 #include <cstdio>
 #include <algorithm>
 #include <cstdlib>
 #include "spmesl_internal.cuh"
 
 namespace spmesl {
+
 
 __device__ __forceinline__ void dmma_t(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -336,29 +334,68 @@ __global__ void tail_mark_kernel(const TailState* __restrict__ tail, int M, cons
 }
 
 // ------------------------------------------------------------------ per-column sweeps
+// Chain + pass formulation of one sweep.  Algorithm 1 visits the rows in cyclic
+// order; a visit can only change b_j if b_j != 0 (an "old" row: the column's current nonzeros,
+// known at sweep start) or |z_j| > lambda (a "new" row).  The sweep is processed in segments:
+//   chain  (warp 0): assume no new row appears before the next K <= KMAX old rows O_0 < O_1 <
+//          ...; their visits form a dependent chain that needs only z at those rows and the
+//          K x K Gram block G[O, O]:  a_k = z_{O_k} + sum_{l < k} d_l G[O_k, O_l] (+ pending
+//          changes first), b' = Soft(a_k + b_k), d_k = b_k - b' — one lane per row, d_k
+//          broadcast by shuffle, serial latency ~K shuffles instead of K block-wide passes;
+//   pass   (all threads, one sweep over the rows): apply the pending changes to every z_i
+//          (committed), form each row's value at its visit w_i = z_i + sum_{l: O_l < i} d_l
+//          G[i, O_l] and find the first row in [pos, next unprocessed old row) with b_i = 0 and
+//          |w_i| > lambda (a new row), by one block-wide min reduction;
+//   commit: chain entries before that row are valid (their changes become pending; with a
+//          second z buffer, when no new row appeared, z2 = z + all chain changes is swapped in
+//          instead); the new row is visited with a = w_i, its change becomes pending too, and
+//          the next segment starts right after it.
+// Every z_i receives exactly the FMAs z_i <- fma(d, G[i, j], z_i) of the one-row-at-a-time
+// covariance-update loop, in the same order (changes in row order), and every visit sees the
+// same value — the iterates are bit-identical to it.  Per sweep the dependent chain is one
+// pass (plus one per new row) instead of one block-wide update + search per change.
+constexpr int KMAX = 31;    // old rows per speculative chain (lanes of warp 0)
+constexpr int PMAX = 32;    // pending changes (valid chain entries + one new row)
+constexpr int PASS_U = 4;   // row pairs per thread per chunk of the pass (one LDG.128 each)
+constexpr int PASS_PD = 2;  // columns whose loads are in flight (deeper spills: slower)
+
 struct TailShared {
-  uint64_t pf_bar[2];    // prefetch buffers' mbarriers
   uint64_t z_bar;        // z <- G[:, c] bulk copy
   double red[TAIL_MAXW];
-  int wmin[2][TAIL_MAXW];   // per-warp first hits, double-buffered across rounds
+  int wmin[TAIL_MAXW];   // per-warp first new row of a pass
+  double wval[TAIL_MAXW];
   int oc_var[TAIL_ODC];
   int oc_next;
   int k;
   int k2;
-  int pf_row[2];         // variable whose Gram column is (being) loaded into each buffer, or -1
+  int ncol;
+  int sg_n;              // the chain rows SG (in the tiles) was gathered for: sg_rows[0..sg_n)
+  int sg_rows[KMAX];     //   (-1: invalid — the tiles were used for an on-demand Gram column)
+  int so[KMAX];          // chain rows (old rows O_cursor ...)
+  double sd[KMAX];       // chain changes d_l
+  double sbn[KMAX];      // chain new values b'_l
+  int prow[PMAX];        // pending changes (rows ascending, not yet applied to z)
+  double pd[PMAX];
+  int crow[PMAX + KMAX]; // the pass's Gram columns: pending changes, then nonzero chain changes
+  double cd[PMAX + KMAX];
+  int cO[PMAX + KMAX];   // (chain columns: their row O_l; pending: -1)
 };
+constexpr size_t TS_BYTES = (sizeof(TailShared) + 127) & ~(size_t)127;
 
-// doubles: tiles [2][J*XS], z [p], r [n_pad], old/new list values [2][nzcap];
-// ints: old/new list rows [2][nzcap]; then TailShared (8-aligned)
+// Shared-memory layout (byte offsets; TailShared first so its address is a constant):
+//   TailShared | tiles [2][J*XS] doubles (on-demand Gram columns; the chain's Gram blocks alias
+//   them) | z [p] | r [n_pad] | old/new list values [2][nzcap] | old/new list rows [2][nzcap]
+//   | old-row bitmap [ceil(p/32)] | (z2 [p], optional, after the base)
+__host__ __device__ inline size_t tail_off_z() { return TS_BYTES + (size_t)2 * J * XS * 8; }
+__host__ __device__ inline size_t tail_off_r(int p) { return tail_off_z() + (((size_t)p * 8 + 15) & ~(size_t)15); }
 __host__ __device__ size_t tail_smem_bytes(int p, int n_pad, int nzcap) {
-  size_t b = ((size_t)2 * J * XS + p + n_pad + 2 * (size_t)nzcap) * 8;
-  b += (size_t)2 * nzcap * 4;
-  b = (b + 15) & ~(size_t)15;
-  b += sizeof(TailShared);
+  size_t b = tail_off_r(p) + (size_t)n_pad * 8 + (size_t)2 * nzcap * 8 + (size_t)2 * nzcap * 4 +
+             (size_t)((p + 31) / 32) * 4;
   return (b + 127) & ~(size_t)127;
 }
 
-size_t tail_prefetch_bytes(int p) { return (((size_t)2 * p * 8) + 127) & ~(size_t)127; }
+// the optional second z buffer (z2, after the base layout)
+__host__ __device__ size_t tail_z2_bytes(int p) { return (((size_t)p * 8) + 127) & ~(size_t)127; }
 
 // Gram column G[:, j] of the fit-wide table: precomputed, or computed here once (claim 0 -> 1,
 // write, publish 2) by the same DMMA routine as the batched pass; every CTA is resident, so
@@ -376,7 +413,11 @@ __device__ void ensure_gram_column(const TailParams& P, int j, TailShared& TS, d
                 tvv, nullptr, P.Gtab);
     __threadfence();
     bsync();
-    if (tid == 0) { atomicExch(&P.gstate[j], 2); atomicAdd(P.ondemand_count, 1); }
+    if (tid == 0) {
+      atomicExch(&P.gstate[j], 2);
+      atomicAdd(P.ondemand_count, 1);
+      TS.sg_n = -1;   // (the tiles held the chain's cached Gram block)
+    }
   } else if (tid == 0) {
     while (*(volatile int*)&P.gstate[j] != 2) __nanosleep(200);
   }
@@ -384,56 +425,193 @@ __device__ void ensure_gram_column(const TailParams& P, int j, TailShared& TS, d
   bsync();
 }
 
-template <int NT>
-__global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) tail_sweep_kernel(const TailParams P) {
-  constexpr int TSCAN = SPMESL_TAIL_SCAN_R * NT;   // rows tested per search round
+// rows of pair u of a thread in a pass chunk: base + 2 (u NT + tid) + {0, 1}
+template <bool EVEN>
+__device__ __forceinline__ double2 ld_pair_s(const double* z, int i, int p) {
+  if (EVEN) return *(const double2*)(z + i);
+  double2 v = make_double2(0.0, 0.0);
+  v.x = z[i];
+  if (i + 1 < p) v.y = z[i + 1];
+  return v;
+}
+template <bool EVEN>
+__device__ __forceinline__ void st_pair_s(double* z, int i, int p, double2 v) {
+  if (EVEN) { *(double2*)(z + i) = v; return; }
+  z[i] = v.x;
+  if (i + 1 < p) z[i + 1] = v.y;
+}
+
+// One pass over the rows: chunks of RN = 2 U NT rows (each thread U pairs of
+// adjacent rows, one LDG.128 per pair and column); per chunk the Gram columns it needs, in
+// order, the next column's loads in flight while one is applied.  A chunk with no chain row
+// inside it sees every row's visit value at one point — after the pending columns and the chain
+// columns of rows before the chunk (split) — and tests it there; a chunk with a chain row inside
+// tests each row just before the first chain column at or after it.
+struct PassArgs {
+  double* z;
+  double* z2;
+  const uint32_t* oldmask;
+  const double* Gtab;
+  int p, npend, C, pos, range_end, gc;
+  bool spec_all;
+  double lam;
+};
+
+template <int NT, bool EVEN, int U, int PD>
+__device__ __forceinline__ void run_pass(const PassArgs& A, const TailShared& TS, int& best,
+                                         double& bestw) {
+  constexpr int RN = 2 * U * NT;
+  const int tid = threadIdx.x;
+  const int p = A.p, npend = A.npend, C = A.C, pos = A.pos, range_end = A.range_end;
+  const double lam = A.lam;
+  const int nch = (p + RN - 1) / RN;
+  // a new row: |w_i| > lambda (Soft != 0), i in [pos, range_end), b_i = 0 (not an old row),
+  // i != c; the first one wins
+  auto test = [&](int i, double w) {
+    if (fabs(w) > lam && i >= pos && i < range_end && i < best && i != A.gc &&
+        !((A.oldmask[i >> 5] >> (i & 31)) & 1u)) { best = i; bestw = w; }
+  };
+  for (int c = 0; c < nch; ++c) {
+    const int base = c * RN;
+    const bool det = base < range_end && base + RN > pos;
+    if (npend == 0 && !A.spec_all && !det) continue;
+    // chain columns of rows before the chunk (split), a chain row inside it (complex chunk)
+    int split = npend;
+    while (split < C && TS.cO[split] < base) ++split;
+    const bool cx = det && split < C && TS.cO[split] < base + RN - 1;
+    // columns this chunk needs: all for z2; else the pending ones and, when it holds detection
+    // rows, the chain columns before its rows
+    const int lend = A.spec_all ? C : (det ? (cx ? C : split) : npend);
+    const int ptr0 = base + 2 * tid;
+    double2 acc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = ptr0 + 2 * u * NT;
+      acc[u] = i < p ? ld_pair_s<EVEN>(A.z, i, p) : make_double2(0.0, 0.0);
+    }
+    uint32_t tm = 0;                // complex chunk: rows tested so far (2 bits per pair)
+    bool tested = !det;
+    auto test_all = [&]() {         // every untested row, value = the accumulator now
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = ptr0 + 2 * u * NT;
+        if (fabs(acc[u].x) > lam && !((tm >> (2 * u)) & 1u)) test(i, acc[u].x);
+        if (fabs(acc[u].y) > lam && !((tm >> (2 * u + 1)) & 1u)) test(i + 1, acc[u].y);
+      }
+      tested = true;
+    };
+    auto apply = [&](int l, const double2 (&g)[U]) {
+      if (!tested && l >= split) {
+        if (!cx) test_all();
+        else {
+          const int O = TS.cO[l];
+          if (O >= base + RN - 1) test_all();
+          else {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const int i = ptr0 + 2 * u * NT;
+              if (i <= O && !((tm >> (2 * u)) & 1u)) { test(i, acc[u].x); tm |= 1u << (2 * u); }
+              if (i + 1 <= O && !((tm >> (2 * u + 1)) & 1u)) { test(i + 1, acc[u].y); tm |= 2u << (2 * u); }
+            }
+          }
+        }
+      }
+      const double d = TS.cd[l];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        acc[u].x = fma(d, g[u].x, acc[u].x);
+        acc[u].y = fma(d, g[u].y, acc[u].y);
+      }
+      if (l == npend - 1) {         // committed: every pending change applied
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = ptr0 + 2 * u * NT;
+          if (i < p) st_pair_s<EVEN>(A.z, i, p, acc[u]);
+        }
+      }
+    };
+    if (lend > 0) {
+      auto load = [&](int l, double2 (&g)[U]) {
+        const double* gcol = A.Gtab + (size_t)TS.crow[l] * p + ptr0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = ptr0 + 2 * u * NT;
+          double2 v = make_double2(0.0, 0.0);
+          if (i < p) {
+            if (EVEN) v = __ldcg((const double2*)(gcol + 2 * u * NT));
+            else {
+              v.x = __ldcg(gcol + 2 * u * NT);
+              if (i + 1 < p) v.y = __ldcg(gcol + 2 * u * NT + 1);
+            }
+          }
+          g[u] = v;
+        }
+      };
+      // a rolling window of PD columns in flight: column l + PD - 1 is requested into the
+      // slot column l - 1 just freed, then column l is applied
+      double2 g[PD][U];
+#pragma unroll
+      for (int q = 0; q < PD - 1; ++q)
+        if (q < lend) load(q, g[q]);
+      for (int l0 = 0; l0 < lend; l0 += PD) {
+#pragma unroll
+        for (int q = 0; q < PD; ++q) {
+          const int l = l0 + q;
+          if (l < lend) {
+            if (l + PD - 1 < lend) load(l + PD - 1, g[(q + PD - 1) % PD]);
+            apply(l, g[q]);
+          }
+        }
+      }
+    }
+    if (!tested) test_all();        // rows after every chain column
+    if (A.spec_all) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = ptr0 + 2 * u * NT;
+        if (i < p) st_pair_s<EVEN>(A.z2, i, p, acc[u]);
+      }
+    }
+  }
+}
+
+template <int NT, bool EVEN, int MINB>
+__global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P) {
   extern __shared__ __align__(128) unsigned char sm[];
   const int p = P.p, n = P.n, n_pad = P.n_pad, nchunk = P.nchunk, nzcap = P.nzcap;
-  double* tx = (double*)sm;                                  // [J*XS]
+  TailShared& TS = *(TailShared*)sm;
+  double* tx = (double*)(sm + TS_BYTES);                     // [J*XS]
   double* tvv = tx + J * XS;                                 // [J*XS]
-  double* z = tvv + J * XS;                                  // [p]
-  double* r = z + p;                                         // [n_pad]
+  double* zA = (double*)(sm + tail_off_z());                 // [p]
+  double* r = (double*)(sm + tail_off_r(p));                 // [n_pad]
   double* ov = r + n_pad;                                    // [nzcap] old list values
   double* nv = ov + nzcap;                                   // [nzcap] new list values
   int* orow = (int*)(nv + nzcap);                            // [nzcap]
   int* nrow = orow + nzcap;                                  // [nzcap]
-  size_t ts_off = ((size_t)2 * J * XS + p + n_pad + 2 * (size_t)nzcap) * 8 + (size_t)2 * nzcap * 4;
-  ts_off = (ts_off + 15) & ~(size_t)15;
-  TailShared& TS = *(TailShared*)(sm + ts_off);
+  uint32_t* oldmask = (uint32_t*)(nrow + nzcap);             // [ceil(p/32)]
+  // the chain's Gram blocks alias the on-demand tiles (never live at the same time):
+  // SG[k][m] = G[O_m, O_k] (k < m), PG[j][m] = G[O_m, pending row j]
+  double* SG = tx;
+  double* PG = tvv;
+  const bool use_z2 = P.z2 != 0;
+  double* zB = use_z2 ? (double*)(sm + tail_smem_bytes(p, n_pad, nzcap)) : nullptr;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const size_t list_stride = (size_t)2 * nzcap;
   const int M = P.M_dev ? *(volatile const int*)P.M_dev : P.M;
-  // prefetch buffers [2][p] after the base layout (128-byte aligned)
-  double* gbuf = (double*)(sm + tail_smem_bytes(p, n_pad, nzcap));
-  const bool pf = P.prefetch != 0;
-  uint32_t pf_ph[2] = {0u, 0u};
+  const int nmask = (p + 31) / 32;
   if (tid < TAIL_ODC) TS.oc_var[tid] = -1;
   if (tid == 0) {
     TS.oc_next = 0;
-    TS.pf_row[0] = TS.pf_row[1] = -1;
-    if (pf) {
-      mbar_init_t(&TS.pf_bar[0], 1);
-      mbar_init_t(&TS.pf_bar[1], 1);
-    }
+    TS.sg_n = -1;
     mbar_init_t(&TS.z_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   uint32_t z_ph = 0;
-  // (one thread) start loading the Gram column of old-list entry c into buffer c & 1
-  auto pf_issue = [&](int c, int cnt) {
-    if (c < cnt) {
-      const int jv = orow[c];
-      if (P.gtab_full || *(volatile int*)&P.gstate[jv] == 2) {
-        prefetch_col(gbuf + (size_t)(c & 1) * p, P.Gtab + (size_t)jv * p, (uint32_t)p * 8,
-                     &TS.pf_bar[c & 1]);
-        TS.pf_row[c & 1] = jv;
-        return;
-      }
-    }
-    TS.pf_row[c & 1] = -1;
-  };
 
   for (;;) {
+    // (z is refilled by a bulk copy — async proxy — below: every thread orders its own
+    // generic-proxy accesses to it before that, then the barrier publishes them)
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     bsync();
     if (tid == 0) TS.k = atomicAdd(P.next, 1);
     bsync();
@@ -449,11 +627,13 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) tail_sweep_kernel(const
     int cur = ts.cur;
     int ocnt = min(ts.cnt, nzcap);
     bool overflow = ts.cnt > nzcap;
+    double* z = zA;
+    double* z2 = zB;
     const bool z_saved = P.joint && (ts.flags & 16);          // joint: z kept between launches
     if (P.z_from_gtab || z_saved) {
       if (!z_saved) ensure_gram_column(P, gc, TS, tx, tvv);
       const double* gz = z_saved ? P.Zj + (size_t)slot * p : P.Gtab + (size_t)gc * p;
-      if ((p & 1) == 0) {   // the whole column in one bulk copy (8p bytes, 16-byte multiple)
+      if (EVEN) {   // the whole column in one bulk copy (8p bytes, 16-byte multiple)
         if (tid == 0) {
           prefetch_col(z, gz, (uint32_t)p * 8, &TS.z_bar);
           mbar_wait_t(&TS.z_bar, z_ph);
@@ -479,10 +659,20 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) tail_sweep_kernel(const
     } else {
       for (int j = tid; j < p; j += NT) z[j] = P.Zz[(size_t)k * p + j];
     }
+    for (int w = tid; w < nmask; w += NT) oldmask[w] = 0u;
+    bsync();
     {
       const size_t lo = (size_t)col * list_stride + (size_t)cur * nzcap;
-      for (int m = tid; m < ocnt; m += NT) { orow[m] = P.nz_rows[lo + m]; ov[m] = P.nz_vals[lo + m]; }
+      for (int m = tid; m < ocnt; m += NT) {
+        const int j = P.nz_rows[lo + m];
+        orow[m] = j;
+        ov[m] = P.nz_vals[lo + m];
+        atomicOr(&oldmask[j >> 5], 1u << (j & 31));
+      }
     }
+    int npend = 0;                   // pending changes (TS.prow / TS.pd), carried across sweeps
+    long long nchg = 0;              // coordinate changes d != 0 (each reads one Gram column)
+    long long npass = 0;             // chain + pass segments
     bsync();
     bool retire = false;
     while (!retire) {
@@ -490,95 +680,155 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) tail_sweep_kernel(const
       const double lam = sigma * lambda0;
       double maxd = 0.0;
       int pos = 0, cursor = 0, ncnt = 0;
-      if (pf) {
-        if (tid == 0) { pf_issue(0, ocnt); pf_issue(1, ocnt); }
-        bsync();
-      }
+      bool flush = false;            // (joint mode: a last pass that only applies the pending)
       for (;;) {
-        const int na = cursor < ocnt ? orow[cursor] : p;     // next row with b_j != 0
-        // first row in [pos, na) with |z_j| > lambda (j != this column)
-        // (rounds of TSCAN rows: thread t tests rows base + t + NT r,
-        // r < TSCAN / NT; the first hit is the block-wide minimum of the hit rows;
-        // one barrier per round: the per-warp minima alternate between two buffers, and a
-        // buffer is rewritten only after the next round's barrier, which every reader of it
-        // has passed)
-        int j = na;
-        int rbuf = 0;
-        for (int base = pos; base < na; base += TSCAN, rbuf ^= 1) {
-          int my = 0x7fffffff;
-#pragma unroll
-          for (int r = TSCAN / NT - 1; r >= 0; --r) {
-            const int jj = base + tid + r * NT;
-            if (jj < na && jj != gc && fabs(z[jj]) > lam) my = jj;
-          }
-          my = __reduce_min_sync(0xffffffffu, my);
-          if (lane == 0) TS.wmin[rbuf][warp] = my;
-          bsync();
-          int best = 0x7fffffff;
-#pragma unroll
-          for (int w = 0; w < NT / 32; ++w) best = min(best, TS.wmin[rbuf][w]);
-          if (best != 0x7fffffff) { j = best; break; }
+        const int K = flush ? 0 : min(ocnt - cursor, KMAX);
+        const int range_end = flush ? 0 : (cursor + K < ocnt ? orow[cursor + K] : p);
+        ++npass;
+        // ---- chain inputs: rows, Gram blocks (all threads); SG is kept from the previous
+        // segment with the same chain rows (a stable support: every sweep's chain is the same)
+        int mine = 1;
+        for (int l = tid; l < K; l += NT) {
+          const int o = orow[cursor + l];
+          TS.so[l] = o;
+          if (TS.sg_rows[l] != o) mine = 0;
         }
-        if (j >= p) break;
-        double bo = 0.0;
-        int pfb = -1;                 // prefetch buffer holding G[:, j], if any
-        int pf_next = -1;             // old-list entry to prefetch after this visit
-        if (j == na) {
-          bo = ov[cursor];
-          if (pf) {
-            const int b = cursor & 1;
-            if (TS.pf_row[b] == j) {   // consume the load (wait even if b_j does not change):
-              if (tid == 0) {          // the issuing thread waits, the barrier publishes it
-                mbar_wait_t(&TS.pf_bar[b], pf_ph[b]);
-                pf_ph[b] ^= 1u;
-              }
-              bsync();
-              pfb = b;
+#ifdef SPMESL_TAIL_NO_SGCACHE
+        mine = 0;
+#endif
+        if (!__syncthreads_and(mine && TS.sg_n == K)) {
+          for (int e = tid; e < K * K; e += NT) {
+            const int kk = e / K, m = e - kk * K;
+            if (kk < m) SG[kk * 32 + m] = __ldcg(P.Gtab + (size_t)orow[cursor + kk] * p + orow[cursor + m]);
+          }
+          for (int l = tid; l < K; l += NT) TS.sg_rows[l] = orow[cursor + l];
+          if (tid == 0) TS.sg_n = K;
+        }
+        for (int e = tid; e < npend * K; e += NT) {
+          const int j = e / K, m = e - j * K;
+          PG[j * 32 + m] = __ldcg(P.Gtab + (size_t)TS.prow[j] * p + orow[cursor + m]);
+        }
+        bsync();
+        // ---- chain (warp 0, lane = chain row), then the pass's column list
+        if (warp == 0) {
+          if (K > 0) {
+            double a = 0.0, bo = 0.0;
+            if (lane < K) {
+              a = z[TS.so[lane]];
+              for (int j = 0; j < npend; ++j) a = fma(TS.pd[j], PG[j * 32 + lane], a);
+              bo = ov[cursor + lane];
             }
-            pf_next = cursor + 2;
+            for (int kk = 0; kk < K; ++kk) {
+              double dk = 0.0;
+              if (lane == kk) {
+                const double bn = soft_t(a + bo, lam);
+                dk = bo - bn;                                   // e += x_j d
+                TS.sd[kk] = dk;
+                TS.sbn[kk] = bn;
+              }
+              dk = __shfl_sync(0xffffffffu, dk, kk);
+              if (lane > kk && lane < K && dk != 0.0) a = fma(dk, SG[kk * 32 + lane], a);
+            }
           }
-          ++cursor;
+          // the pass's columns: pending changes in order, then the nonzero chain changes in order
+          if (lane < npend) { TS.crow[lane] = TS.prow[lane]; TS.cd[lane] = TS.pd[lane]; TS.cO[lane] = -1; }
+          __syncwarp();
+          const bool nz = lane < K && TS.sd[lane] != 0.0;
+          const unsigned bal = __ballot_sync(0xffffffffu, nz);
+          if (nz) {
+            const int c = npend + __popc(bal & ((1u << lane) - 1u));
+            TS.crow[c] = TS.so[lane]; TS.cd[c] = TS.sd[lane]; TS.cO[c] = TS.so[lane];
+          }
+          if (lane == 0) TS.ncol = npend + __popc(bal);
         }
-        const double a = z[j] + bo;
-        const double bn = soft_t(a, lam);
-        const double d = bo - bn;                             // e += x_j d
-        if (bn != 0.0) {
-          if (ncnt < nzcap) { if (tid == 0) { nrow[ncnt] = j; nv[ncnt] = bn; } }
+        bsync();
+        // ---- pass over the rows (all threads; run_pass)
+        int best = 0x7fffffff;
+        double bestw = 0.0;
+        const int C = TS.ncol;
+        const bool spec_all = use_z2 && !flush && C > npend;   // z2 = committed + every change
+        if (C == 0) {
+          // no change to apply: detection only, from z
+          for (int i = pos + tid; i < range_end; i += NT)
+            if (fabs(z[i]) > lam && i != gc && !((oldmask[i >> 5] >> (i & 31)) & 1u)) {
+              best = i;
+              bestw = z[i];
+              break;
+            }
+        } else {
+          const PassArgs A{z, z2, oldmask, P.Gtab, p, npend, C, pos, range_end, gc, spec_all, lam};
+          run_pass<NT, EVEN, PASS_U, PASS_PD>(A, TS, best, bestw);
+        }
+        // first new row: block-wide minimum (and its visit value)
+        {
+          const int wb = __reduce_min_sync(0xffffffffu, best);
+          if (best == wb && best != 0x7fffffff) TS.wval[warp] = bestw;
+          if (lane == 0) TS.wmin[warp] = wb;
+        }
+        bsync();
+        int jstar = 0x7fffffff, wsrc = 0;
+#pragma unroll
+        for (int w = 0; w < NT / 32; ++w)
+          if (TS.wmin[w] < jstar) { jstar = TS.wmin[w]; wsrc = w; }
+        if (flush) { npend = 0; break; }
+        // ---- commit (every thread takes the same decisions from shared memory)
+        int nvalid = K;
+        if (jstar != 0x7fffffff) { nvalid = 0; while (nvalid < K && TS.so[nvalid] < jstar) ++nvalid; }
+        const bool swap = spec_all && jstar == 0x7fffffff;   // (z2 holds z + every change)
+        int np2 = 0;
+        for (int l = 0; l < nvalid; ++l) {
+          const double bn = TS.sbn[l], d = TS.sd[l];
+          if (bn != 0.0) {
+            if (ncnt < nzcap) { if (tid == 0) { nrow[ncnt] = TS.so[l]; nv[ncnt] = bn; } }
+            else overflow = true;
+            ++ncnt;
+          }
+          if (d != 0.0) {
+            maxd = fmax(maxd, fabs(d));
+            ++nchg;
+            if (!swap) {
+              if (tid == 0) { TS.prow[np2] = TS.so[l]; TS.pd[np2] = d; }
+              ++np2;
+            }
+          }
+        }
+        if (swap) { double* t = z; z = z2; z2 = t; }
+        cursor += nvalid;
+        if (jstar != 0x7fffffff) {
+          const double a = TS.wval[wsrc];                      // b = 0: a = z_j
+          const double bn = soft_t(a, lam);                    // nonzero (|a| > lambda)
+          const double d = 0.0 - bn;
+          if (ncnt < nzcap) { if (tid == 0) { nrow[ncnt] = jstar; nv[ncnt] = bn; } }
           else overflow = true;
           ++ncnt;
+          maxd = fmax(maxd, fabs(d));
+          ++nchg;
+          if (tid == 0) { TS.prow[np2] = jstar; TS.pd[np2] = d; }
+          ++np2;
+          npend = np2;
+          pos = jstar + 1;
+          ensure_gram_column(P, jstar, TS, tx, tvv);          // (its barriers publish TS)
+          bsync();
+          continue;
         }
-        if (d != 0.0 && pfb >= 0) {
-          maxd = fmax(maxd, fabs(d));                         // P:630
-          const double* gs = gbuf + (size_t)pfb * p;          // G[:, j] in shared memory
-          for (int t = tid; t < p; t += NT) z[t] = fma(d, gs[t], z[t]);
-        } else if (d != 0.0) {
-          maxd = fmax(maxd, fabs(d));                         // P:630
-          const double* gcol = P.Gtab + (size_t)j * p;
-          ensure_gram_column(P, j, TS, tx, tvv);
-          // (up to 16 independent L2 loads in flight per thread: one round trip per 4096 rows)
-          constexpr int UB = 16;
-          for (int t0 = 0; t0 < p; t0 += UB * NT) {
-            double gv[UB];
-#pragma unroll
-            for (int u = 0; u < UB; ++u) {
-              const int t = t0 + u * NT + tid;
-              gv[u] = t < p ? __ldcg(gcol + t) : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < UB; ++u) {
-              const int t = t0 + u * NT + tid;
-              if (t < p) z[t] = fma(d, gv[u], z[t]);
-            }
-          }
-        }
+        npend = np2;
+        pos = range_end;
         bsync();
-        if (pf_next >= 0 && tid == 0) pf_issue(pf_next, ocnt);   // (buffer just released)
-        pos = j + 1;
+        if (cursor >= ocnt) {
+          if (P.joint && npend > 0) { flush = true; continue; }   // z saved complete
+          break;
+        }
       }
       ++sweeps;
       ++inner;
-      // the new list becomes the current one
-      for (int m = tid; m < min(ncnt, nzcap); m += NT) { orow[m] = nrow[m]; ov[m] = nv[m]; }
+      // the new list becomes the current one (and the old-row bitmap with it)
+      for (int m = tid; m < ocnt; m += NT) atomicAnd(&oldmask[orow[m] >> 5], ~(1u << (orow[m] & 31)));
+      bsync();
+      for (int m = tid; m < min(ncnt, nzcap); m += NT) {
+        orow[m] = nrow[m];
+        ov[m] = nv[m];
+        atomicOr(&oldmask[nrow[m] >> 5], 1u << (nrow[m] & 31));
+      }
       ocnt = min(ncnt, nzcap);
       if (ncnt > nzcap) overflow = true;
       bsync();
@@ -627,6 +877,10 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) tail_sweep_kernel(const
       P.nz_cur[col] = dst;
       if (overflow) atomicExch(&P.flags[FLAG_OVERFLOW], 1);
       atomicAdd(P.sweeps_count, sweeps - ts.sweeps);
+      if (P.changes_count) {
+        atomicAdd(P.changes_count, (unsigned long long)nchg);
+        atomicAdd(P.changes_count + 1, (unsigned long long)npass);
+      }
       if (P.joint) {   // (sigma, iters, sweeps, converged: the host loop's joint kernels)
         TailState t2 = ts;
         t2.cur = dst; t2.cnt = ocnt; t2.sweeps = sweeps; t2.flags = ts.flags | 16;
@@ -640,6 +894,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) tail_sweep_kernel(const
     }
   }
 }
+
 
 cudaError_t launch_tail_residuals(const double* Xb, const TailState* tail, int M, const int* nz_rows,
                                   const double* nz_vals, int nzcap, int64_t col_begin, int n,
@@ -704,25 +959,25 @@ cudaError_t launch_tail_mark(const TailState* tail, int M, const int* nz_rows, i
   return cudaGetLastError();
 }
 
+template <int NT, bool EVEN, int MINB>
+static cudaError_t launch_tail_t(const TailParams& P, int grid, size_t smem, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute(tail_sweep_kernel<NT, EVEN, MINB>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  tail_sweep_kernel<NT, EVEN, MINB><<<grid, NT, smem, s>>>(P);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_tail_sweeps(const TailParams& P, int grid, cudaStream_t s) {
   size_t smem = tail_smem_bytes(P.p, P.n_pad, P.nzcap);
-  if (P.prefetch) smem += tail_prefetch_bytes(P.p);
-  if (P.occ > 1) grid *= P.occ;   // several column CTAs per SM (set_prefetch)
-  cudaError_t e = cudaFuncSetAttribute(tail_sweep_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
-  if (e != cudaSuccess) return e;
-  // 512 threads when a single column CTA owns the SM (large p: the search rounds and the z
-  // updates split over twice the threads), 256 when two share it
-  const bool wide = P.occ == 1;
-  if (wide) {
-    cudaError_t e2 = cudaFuncSetAttribute(tail_sweep_kernel<512>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e2 != cudaSuccess) return e2;
-    tail_sweep_kernel<512><<<grid, 512, smem, s>>>(P);
-  } else {
-    tail_sweep_kernel<256><<<grid, 256, smem, s>>>(P);
-  }
-  return cudaGetLastError();
+  if (P.z2) smem += tail_z2_bytes(P.p);
+  if (P.occ > 1) grid *= P.occ;   // several column CTAs per SM (set_tail_shape)
+  // 512 threads when a single column CTA owns the SM (large p: the pass splits over twice the
+  // threads), 256 when two share it; even p: 16-byte row pairs everywhere
+  const bool even = (P.p & 1) == 0;
+  if (P.occ == 1)
+    return even ? launch_tail_t<512, true, 1>(P, grid, smem, s) : launch_tail_t<512, false, 1>(P, grid, smem, s);
+  return even ? launch_tail_t<256, true, 2>(P, grid, smem, s) : launch_tail_t<256, false, 2>(P, grid, smem, s);
 }
 
 }  // namespace spmesl
