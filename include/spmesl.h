@@ -49,6 +49,8 @@ extern "C" {
 #define SPMESL_ERR_CONSTANT_COLUMN -2   /* s_k <= 1e-13 max_i |x_ik|; index in stats->bad_column */
 #define SPMESL_ERR_NONFINITE       -3   /* NaN/Inf in X; column index in stats->bad_column */
 #define SPMESL_ERR_CUDA            -4   /* CUDA runtime error (message in spmesl_last_error) */
+#define SPMESL_ERR_NCCL            -5   /* options.num_devices >= 1: NCCL could not be loaded or a
+                                           collective failed (message in spmesl_last_error) */
 #define SPMESL_ERR_OOM             -6   /* device allocation failed (or p*p*8 overflows) */
 #define SPMESL_ERR_UNSUPPORTED     -7   /* n too large for the on-chip residual tile (n > 2688),
                                            or no sm_100 device */
@@ -90,7 +92,19 @@ typedef struct {
                              enqueued fit as a CUDA graph the second time the same arguments
                              (pointers included) arrive and replays it from then on (one launch
                              per fit); 1: enqueue every operation on each call.  Same results. */
-  int32_t reserved[6];
+  int32_t num_devices;    /* host entry points (spmesl_fit, spmesl_fit_ex) only: 0 (default)
+                             fits on one device (`device`); G >= 1 fits on G devices of this
+                             node with NCCL: each device fits a contiguous block
+                             of columns (X replicated), the devices exchange the p first-sweep
+                             screening flags (one max all-reduce) and, after the fit, the
+                             coefficients as CSC (one all-gather); device 0 symmetrizes and
+                             assembles.  Mode 0 only (else SPMESL_ERR_UNSUPPORTED); results
+                             are those of the single-device fit bit for bit; NCCL is loaded at
+                             run time (SPMESL_ERR_NCCL if it cannot be). */
+  int32_t reserved0;
+  const int32_t* device_ids;  /* host array of num_devices distinct CUDA ordinals, or NULL for
+                                 0 .. num_devices - 1 */
+  int32_t reserved[2];
 } spmesl_options;
 
 typedef struct {
@@ -134,6 +148,10 @@ typedef struct {
   int64_t tail_passes;    /* segments (speculative chain + one pass over the rows) the sweep
                              kernel ran: one per sweep plus one per row that entered the support
                              within a sweep */
+  double  ms_comm;        /* options.num_devices >= 1: device time of the collectives (flag
+                             all-reduce + CSC all-gather) on device 0 */
+  int32_t num_devices;    /* devices the fit ran on (0: the single-device path) */
+  int32_t pad2;
 } spmesl_stats;
 
 /* Fill *opt with the defaults listed above. */

@@ -56,7 +56,7 @@ _OPTS_CACHE = {}
 
 def _opts(**kw) -> _lib.Options:
     """Options for these keyword arguments (cached: the device path is called per fit)."""
-    key = tuple(sorted(kw.items()))
+    key = tuple(sorted((k, tuple(v) if isinstance(v, list) else v) for k, v in kw.items()))
     o = _OPTS_CACHE.get(key)
     if o is None:
         o = _OPTS_CACHE[key] = _make_opts(**kw)
@@ -65,16 +65,22 @@ def _opts(**kw) -> _lib.Options:
 
 def _make_opts(max_inner=10000, standardize=True, symmetrize=True, sigma_floor=1e-8, tile_cols=0,
                device=-1, tail_after=1, mode="per_column", solver="auto",
-               eager=False) -> _lib.Options:
+               eager=False, num_devices=0, device_ids=None) -> _lib.Options:
     """mode: "per_column" (Algorithm 1 stop per column) or "joint" (Algorithm 3).
-    solver: "auto", "residual" (CD on X~) or "gram" (covariance updates on X~^T X~ / n)."""
-    return default_options(max_inner=int(max_inner), standardize=int(bool(standardize)),
-                           symmetrize=int(bool(symmetrize)), sigma_floor=float(sigma_floor),
-                           tile_cols=int(tile_cols), device=int(device),
-                           tail_after=int(tail_after),
-                           mode=MODES[mode] if isinstance(mode, str) else int(mode),
-                           solver=SOLVERS[solver] if isinstance(solver, str) else int(solver),
-                           eager=int(bool(eager)))
+    solver: "auto", "residual" (CD on X~) or "gram" (covariance updates on X~^T X~ / n).
+    num_devices / device_ids (host entry points): fit on several devices with NCCL."""
+    o = default_options(max_inner=int(max_inner), standardize=int(bool(standardize)),
+                        symmetrize=int(bool(symmetrize)), sigma_floor=float(sigma_floor),
+                        tile_cols=int(tile_cols), device=int(device),
+                        tail_after=int(tail_after),
+                        mode=MODES[mode] if isinstance(mode, str) else int(mode),
+                        solver=SOLVERS[solver] if isinstance(solver, str) else int(solver),
+                        eager=int(bool(eager)), num_devices=int(num_devices))
+    if device_ids is not None:
+        ids = (ctypes.c_int32 * len(device_ids))(*[int(d) for d in device_ids])
+        o._ids = ids   # (kept alive with the options)
+        o.device_ids = ctypes.cast(ids, ctypes.POINTER(ctypes.c_int32))
+    return o
 
 
 def fit(X, lambda0: float, tol: float = 1e-4, max_iter: int = 100, *, out_theta=None,

@@ -34,7 +34,10 @@ class Options(ctypes.Structure):
         ("tail_after", ctypes.c_int32),
         ("solver", ctypes.c_int32),
         ("eager", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 6),
+        ("num_devices", ctypes.c_int32),
+        ("reserved0", ctypes.c_int32),
+        ("device_ids", ctypes.POINTER(ctypes.c_int32)),
+        ("reserved", ctypes.c_int32 * 2),
     ]
 
 
@@ -68,6 +71,9 @@ class Stats(ctypes.Structure):
         ("pad1", ctypes.c_int32),
         ("tail_changes", ctypes.c_int64),
         ("tail_passes", ctypes.c_int64),
+        ("ms_comm", ctypes.c_double),
+        ("num_devices", ctypes.c_int32),
+        ("pad2", ctypes.c_int32),
     ]
 
     def asdict(self):

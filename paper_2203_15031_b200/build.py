@@ -14,13 +14,33 @@ CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libspmesl.so")
 
-SOURCES = ["prep.cu", "cd_sweep.cu", "tail.cu", "joint.cu", "gram_full.cu", "screen16.cu", "assemble.cu", "api.cu", "penalty.cpp"]
+SOURCES = ["prep.cu", "cd_sweep.cu", "tail.cu", "joint.cu", "gram_full.cu", "screen16.cu", "assemble.cu",
+           "api.cu", "multi.cu", "penalty.cpp"]
+
+
+def _nccl_dirs():
+    """The NCCL header (types only: the library is dlopen-ed at run time) and the pip NCCL's
+    shared library, if present (the run-time fallback after the process's own libnccl.so.2)."""
+    inc, lib = "/usr/include", ""
+    try:
+        import nvidia.nccl as _nv
+        base = list(_nv.__path__)[0]
+        if os.path.exists(os.path.join(base, "include", "nccl.h")):
+            inc = os.path.join(base, "include")
+        cand = os.path.join(base, "lib", "libnccl.so.2")
+        if os.path.exists(cand):
+            lib = cand
+    except Exception:
+        pass
+    return inc, lib
 HEADERS = [os.path.join(CSRC, "spmesl_internal.cuh"), os.path.join(ROOT, "include", "spmesl.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+_NCCL_INC, _NCCL_LIB = _nccl_dirs()
+FLAGS += ["-I", _NCCL_INC, f'-DSPMESL_NCCL_PIP_LIB="{_NCCL_LIB}"']
 # (development: extra -D switches for kernel variants, e.g. SPMESL_NVCC_EXTRA="-DSPMESL_SYRK_MIG=4")
 FLAGS += os.environ.get("SPMESL_NVCC_EXTRA", "").split()
 

@@ -186,6 +186,7 @@ int validate(const void* X, int64_t n, int64_t p, double lambda0, double tol, in
   if (!(o.sigma_floor > 0.0)) return fail(SPMESL_ERR_ARG, "sigma_floor must be > 0");
   if (o.mode != 0 && o.mode != 1) return fail(SPMESL_ERR_ARG, "mode must be 0 (per-column stop) or 1 (Algorithm 3 joint stop)");
   if (o.solver < 0 || o.solver > 3) return fail(SPMESL_ERR_ARG, "solver must be 0, 1, 2 or 3");
+  if (o.num_devices < 0 || o.num_devices > 64) return fail(SPMESL_ERR_ARG, "num_devices must be 0 .. 64");
   if (o.tile_cols != 0 && o.tile_cols != 8 && o.tile_cols != 16 && o.tile_cols != 32)
     return fail(SPMESL_ERR_ARG, "tile_cols must be 0, 8, 16 or 32");
   const double pp = (double)p * (double)p * 8.0;
@@ -1450,6 +1451,13 @@ void init_stats(spmesl_stats* st) {
 
 }  // namespace
 
+namespace spmesl {
+int multi_fail(int code, const std::string& msg) { return fail(code, msg); }
+int fit_multi_device(const double* X, int64_t n, int64_t p, double lambda0, double tol,
+                     int32_t max_iter, const spmesl_options& o, double* Theta, double* sigma,
+                     int32_t* iters, int32_t* sweeps, uint8_t* converged, spmesl_stats* st);
+}  // namespace spmesl
+
 extern "C" {
 
 void spmesl_default_options(spmesl_options* opt) {
@@ -1712,6 +1720,9 @@ int spmesl_fit_ex(const double* X, int64_t n, int64_t p, double lambda0, double 
   int rc = validate(X, n, p, lambda0, tol, max_iter, o);
   if (rc) return rc;
   if (!Theta || !sigma || !iters) return fail(SPMESL_ERR_ARG, "output pointer is NULL");
+  if (o.num_devices > 0)   // several devices with NCCL (multi.cu)
+    return fit_multi_device(X, n, p, lambda0, tol, max_iter, o, Theta, sigma, iters, sweeps,
+                            converged, st);
   int dev;
   if ((rc = current_device(o.device, &dev))) return rc;
   Workspace* W = workspace_for(dev);

@@ -137,3 +137,16 @@ def test_ctypes_layouts_match_the_c_header(tmp_path):
         assert got[(struct, "size")] == ctypes.sizeof(cls), struct
         for f in fields[struct]:
             assert got[(struct, f)] == getattr(cls, f).offset, (struct, f)
+
+
+def test_multi_device_options_validated_before_cuda():
+    """options.num_devices outside 0..64 is an argument error raised before any CUDA call."""
+    import numpy as np
+    import paper_2203_15031_b200 as S
+    X = np.random.default_rng(0).standard_normal((20, 10))
+    with pytest.raises(S.SpmeslError) as e:
+        S.fit(X, 0.3, num_devices=-1)
+    assert e.value.code == -1
+    with pytest.raises(S.SpmeslError) as e:
+        S.fit(X, 0.3, num_devices=65)
+    assert e.value.code == -1
