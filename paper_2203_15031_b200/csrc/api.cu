@@ -795,7 +795,7 @@ void gram_stats(Workspace& W, int64_t p, int nzcap, spmesl_stats* st, bool scree
   st->solver = screen16 ? 3 : 2;
   if (screen16) {
     st->screen_candidates = W.host_counters->s16_nU;
-    st->gram_fallback = 2 * (int64_t)W.host_counters->s16_nU > p;
+    st->gram_fallback = gram_fallback_taken(W.host_counters->s16_nU, p);
   }
   st->tile_cols = 0;
   st->num_ctas = std::min(W.sms, nT * (nT + 1) / 2);

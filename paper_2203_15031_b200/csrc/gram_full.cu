@@ -105,7 +105,7 @@ __device__ __forceinline__ void tri_tile(int t, int nT, int& I, int& Jt) {
 
 __global__ void __launch_bounds__(G_THREADS, 1) syrk_screen_kernel(const GramParams P) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  if (P.cond_nU && 2 * (int64_t)*(volatile const int*)P.cond_nU <= P.p) return;
+  if (P.cond_nU && !gram_fallback_taken(*(volatile const int*)P.cond_nU, P.p)) return;
   if (P.zero_last && blockIdx.x == 0 && threadIdx.x == 0) *P.zero_last = 0.0;
   uint64_t* full = (uint64_t*)smem_raw;
   uint64_t* empty = full + G_MAX_NST;
@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) syrk_screen_kernel(const GramPar
 // lambda_l), from the stored S (one warp per column, coalesced); the Gram kernel's epilogue
 // screens at the smallest level only.
 __global__ void level_flags_kernel(const GramParams P) {
-  if (P.cond_nU && 2 * (int64_t)*(volatile const int*)P.cond_nU <= P.p) return;
+  if (P.cond_nU && !gram_fallback_taken(*(volatile const int*)P.cond_nU, P.p)) return;
   const int lane = threadIdx.x & 31;
   const int c = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
   if (c >= P.p) return;

@@ -174,6 +174,11 @@ struct GramParams {
 };
 size_t syrk_smem_bytes(int nst);
 
+// Certified screening: the exact FP64 decision of its nU candidate columns costs 2 n p nU flops
+// in gram_cols_kernel (~0.44 of the DMMA peak) against n p (p + 1) in the symmetric Gram kernel
+// (~0.9 of it): above p / 4 candidates the full Gram kernel decides instead (measured crossover)
+__host__ __device__ inline bool gram_fallback_taken(int64_t nU, int64_t p) { return 4 * nU > p; }
+
 // Certified f16 screening (screen16.cu)
 struct Screen16Params {
   const __half* Y16;       // normalized f16 tiles
@@ -217,7 +222,8 @@ cudaError_t launch_tail_residuals(const double* Xb, const TailState* tail, int M
                                   const double* nz_vals, int nzcap, int64_t col_begin, int n,
                                   int n_pad, int nchunk, double* V, cudaStream_t s);
 // Exact Gram columns of a candidate list U (count nU, or *nU_dev read on the device; with a
-// device count and 2 nU > p the kernel only sets gstate[:] = 2 — the full Gram kernel decides)
+// device count and gram_fallback_taken(nU, p) the kernel only sets gstate[:] = 2 — the full Gram
+// kernel decides)
 cudaError_t launch_gram_cols(const double* Xb, int nblk, int nchunk, int n, int p, const int* U,
                              int nU, const int* nU_dev, int sms, double* Gtab, uint8_t* hit,
                              const double* lams, int nlam, int* gstate, cudaStream_t s,

@@ -205,7 +205,7 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
                : "memory");
 }
 
-// nU_dev (optional): the candidate count is read on the device; when 2 nU > p the full Gram
+// nU_dev (optional): the candidate count is read on the device; when gram_fallback_taken the full Gram
 // kernel decides instead (solver 3 fallback): this kernel then only marks every column of its
 // rows present (gstate = 2) and exits.
 // Work split: one CTA per SM with T <= 17 warps, one 8-row m-tile per warp; CTA i owns a
@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(GC_MAXW * 32, 1) gram_cols_kernel(const double
   const int m0 = (int)((int64_t)blockIdx.x * nmt / gridDim.x);
   const int m1 = (int)((int64_t)(blockIdx.x + 1) * nmt / gridDim.x);
   const int nU = nU_dev ? *(volatile const int*)nU_dev : nU_host;
-  if (nU_dev && fallback && 2 * (int64_t)nU > p) {
+  if (nU_dev && fallback && gram_fallback_taken(nU, p)) {
     if (gstate)
       for (int r = m0 * 8 + tid; r < min(p, m1 * 8); r += nthr) gstate[r] = 2;
     return;
