@@ -217,6 +217,7 @@ constexpr int TAIL_MAXW = 16;
 constexpr int TAIL_SCAN = SPMESL_TAIL_SCAN_R * TAIL_THREADS;   // rows tested per search round
 constexpr int TAIL_ODC = 8;          // on-demand Gram column cache entries per CTA
 __host__ __device__ size_t tail_smem_bytes(int p, int n_pad, int nzcap);
+
 __host__ __device__ size_t tail_z2_bytes(int p);
 cudaError_t launch_tail_residuals(const double* Xb, const TailState* tail, int M, const int* nz_rows,
                                   const double* nz_vals, int nzcap, int64_t col_begin, int n,

@@ -369,6 +369,7 @@ struct TailShared {
   int k;
   int k2;
   int ncol;
+
   int sg_n;              // the chain rows SG (in the tiles) was gathered for: sg_rows[0..sg_n)
   int sg_rows[KMAX];     //   (-1: invalid — the tiles were used for an on-demand Gram column)
   int so[KMAX];          // chain rows (old rows O_cursor ...)
@@ -387,11 +388,15 @@ constexpr size_t TS_BYTES = (sizeof(TailShared) + 127) & ~(size_t)127;
 //   them) | z [p] | r [n_pad] | old/new list values [2][nzcap] | old/new list rows [2][nzcap]
 //   | old-row bitmap [ceil(p/32)] | (z2 [p], optional, after the base)
 __host__ __device__ inline size_t tail_off_z() { return TS_BYTES + (size_t)2 * J * XS * 8; }
-__host__ __device__ inline size_t tail_off_r(int p) { return tail_off_z() + (((size_t)p * 8 + 15) & ~(size_t)15); }
-__host__ __device__ size_t tail_smem_bytes(int p, int n_pad, int nzcap) {
-  size_t b = tail_off_r(p) + (size_t)n_pad * 8 + (size_t)2 * nzcap * 8 + (size_t)2 * nzcap * 4 +
+__host__ __device__ inline size_t tail_off_r(int pz) { return tail_off_z() + (((size_t)pz * 8 + 15) & ~(size_t)15); }
+// (pz: rows of z this CTA holds — p, or its share of the rows in a cluster)
+__host__ __device__ size_t tail_smem_bytes_rows(int pz, int p, int n_pad, int nzcap) {
+  size_t b = tail_off_r(pz) + (size_t)n_pad * 8 + (size_t)2 * nzcap * 8 + (size_t)2 * nzcap * 4 +
              (size_t)((p + 31) / 32) * 4;
   return (b + 127) & ~(size_t)127;
+}
+__host__ __device__ size_t tail_smem_bytes(int p, int n_pad, int nzcap) {
+  return tail_smem_bytes_rows(p, p, n_pad, nzcap);
 }
 
 // the optional second z buffer (z2, after the base layout)
@@ -455,6 +460,7 @@ struct PassArgs {
   int p, npend, C, pos, range_end, gc;
   bool spec_all;
   double lam;
+  int r0, r1;            // the rows of this pass (z and z2 are indexed by the global row)
 };
 
 template <int NT, bool EVEN, int U, int PD>
@@ -464,15 +470,16 @@ __device__ __forceinline__ void run_pass(const PassArgs& A, const TailShared& TS
   const int tid = threadIdx.x;
   const int p = A.p, npend = A.npend, C = A.C, pos = A.pos, range_end = A.range_end;
   const double lam = A.lam;
-  const int nch = (p + RN - 1) / RN;
+  const int r0 = A.r0, r1 = A.r1;
+  const int nch = (r1 - r0 + RN - 1) / RN;
   // a new row: |w_i| > lambda (Soft != 0), i in [pos, range_end), b_i = 0 (not an old row),
   // i != c; the first one wins
-  auto test = [&](int i, double w) {
-    if (fabs(w) > lam && i >= pos && i < range_end && i < best && i != A.gc &&
+  auto test = [&](int i, double w) {   // (callers have checked |w| > lambda)
+    if (i >= pos && i < range_end && i < best && i != A.gc &&
         !((A.oldmask[i >> 5] >> (i & 31)) & 1u)) { best = i; bestw = w; }
   };
   for (int c = 0; c < nch; ++c) {
-    const int base = c * RN;
+    const int base = r0 + c * RN;
     const bool det = base < range_end && base + RN > pos;
     if (npend == 0 && !A.spec_all && !det) continue;
     // chain columns of rows before the chunk (split), a chain row inside it (complex chunk)
@@ -487,33 +494,31 @@ __device__ __forceinline__ void run_pass(const PassArgs& A, const TailShared& TS
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i = ptr0 + 2 * u * NT;
-      acc[u] = i < p ? ld_pair_s<EVEN>(A.z, i, p) : make_double2(0.0, 0.0);
+      acc[u] = i < r1 ? ld_pair_s<EVEN>(A.z, i, r1) : make_double2(0.0, 0.0);
     }
-    uint32_t tm = 0;                // complex chunk: rows tested so far (2 bits per pair)
-    bool tested = !det;
-    auto test_all = [&]() {         // every untested row, value = the accumulator now
+    // rows tested so far: for each parity v, the pairs u < done[v] (a thread's rows of the
+    // chunk ascend with u, so the rows up to any chain row are a prefix)
+    int done0 = det ? 0 : U, done1 = det ? 0 : U;
+    auto test_upto = [&](int c0, int c1) {   // rows of pairs [done, c) of each parity
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int i = ptr0 + 2 * u * NT;
-        if (fabs(acc[u].x) > lam && !((tm >> (2 * u)) & 1u)) test(i, acc[u].x);
-        if (fabs(acc[u].y) > lam && !((tm >> (2 * u + 1)) & 1u)) test(i + 1, acc[u].y);
+        if (u >= done0 && u < c0 && fabs(acc[u].x) > lam) test(i, acc[u].x);
+        if (u >= done1 && u < c1 && fabs(acc[u].y) > lam) test(i + 1, acc[u].y);
       }
-      tested = true;
+      done0 = max(done0, c0);
+      done1 = max(done1, c1);
     };
     auto apply = [&](int l, const double2 (&g)[U]) {
-      if (!tested && l >= split) {
-        if (!cx) test_all();
+      if (done0 + done1 < 2 * U && l >= split) {
+        if (!cx) test_upto(U, U);
         else {
+          // chain column l (row O_l): rows i <= O_l are visited before it
           const int O = TS.cO[l];
-          if (O >= base + RN - 1) test_all();
-          else {
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-              const int i = ptr0 + 2 * u * NT;
-              if (i <= O && !((tm >> (2 * u)) & 1u)) { test(i, acc[u].x); tm |= 1u << (2 * u); }
-              if (i + 1 <= O && !((tm >> (2 * u + 1)) & 1u)) { test(i + 1, acc[u].y); tm |= 2u << (2 * u); }
-            }
-          }
+          const int n0 = O - ptr0, n1 = n0 - 1;   // row base + 2 (u NT + tid) + v <= O
+          const int c0 = n0 < 0 ? 0 : min(U, n0 / (2 * NT) + 1);
+          const int c1 = n1 < 0 ? 0 : min(U, n1 / (2 * NT) + 1);
+          test_upto(c0, c1);
         }
       }
       const double d = TS.cd[l];
@@ -526,7 +531,7 @@ __device__ __forceinline__ void run_pass(const PassArgs& A, const TailShared& TS
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int i = ptr0 + 2 * u * NT;
-          if (i < p) st_pair_s<EVEN>(A.z, i, p, acc[u]);
+          if (i < r1) st_pair_s<EVEN>(A.z, i, r1, acc[u]);
         }
       }
     };
@@ -537,11 +542,11 @@ __device__ __forceinline__ void run_pass(const PassArgs& A, const TailShared& TS
         for (int u = 0; u < U; ++u) {
           const int i = ptr0 + 2 * u * NT;
           double2 v = make_double2(0.0, 0.0);
-          if (i < p) {
+          if (i < r1) {
             if (EVEN) v = __ldcg((const double2*)(gcol + 2 * u * NT));
             else {
               v.x = __ldcg(gcol + 2 * u * NT);
-              if (i + 1 < p) v.y = __ldcg(gcol + 2 * u * NT + 1);
+              if (i + 1 < r1) v.y = __ldcg(gcol + 2 * u * NT + 1);
             }
           }
           g[u] = v;
@@ -564,12 +569,12 @@ __device__ __forceinline__ void run_pass(const PassArgs& A, const TailShared& TS
         }
       }
     }
-    if (!tested) test_all();        // rows after every chain column
+    if (done0 + done1 < 2 * U) test_upto(U, U);   // rows after every chain column
     if (A.spec_all) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int i = ptr0 + 2 * u * NT;
-        if (i < p) st_pair_s<EVEN>(A.z2, i, p, acc[u]);
+        if (i < r1) st_pair_s<EVEN>(A.z2, i, r1, acc[u]);
       }
     }
   }
@@ -579,6 +584,7 @@ template <int NT, bool EVEN, int MINB>
 __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P) {
   extern __shared__ __align__(128) unsigned char sm[];
   const int p = P.p, n = P.n, n_pad = P.n_pad, nchunk = P.nchunk, nzcap = P.nzcap;
+  const int r0 = 0, r1 = p;
   TailShared& TS = *(TailShared*)sm;
   double* tx = (double*)(sm + TS_BYTES);                     // [J*XS]
   double* tvv = tx + J * XS;                                 // [J*XS]
@@ -635,25 +641,25 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
       const double* gz = z_saved ? P.Zj + (size_t)slot * p : P.Gtab + (size_t)gc * p;
       if (EVEN) {   // the whole column in one bulk copy (8p bytes, 16-byte multiple)
         if (tid == 0) {
-          prefetch_col(z, gz, (uint32_t)p * 8, &TS.z_bar);
+          prefetch_col(z, gz, (uint32_t)(r1 - r0) * 8, &TS.z_bar);
           mbar_wait_t(&TS.z_bar, z_ph);
         }
         z_ph ^= 1u;
         bsync();
       } else
       // (16 independent L2 loads in flight per thread: the column is 8p bytes)
-      for (int j0 = 0; j0 < p; j0 += 16 * NT) {
+      for (int j0 = 0; j0 < r1 - r0; j0 += 16 * NT) {
         constexpr int UB = 16;
         double gv[UB];
 #pragma unroll
         for (int u = 0; u < UB; ++u) {
           const int j = j0 + u * NT + tid;
-          gv[u] = j < p ? __ldcs(gz + j) : 0.0;
+          gv[u] = j < r1 - r0 ? __ldcs(gz + j) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < UB; ++u) {
           const int j = j0 + u * NT + tid;
-          if (j < p) z[j] = gv[u];
+          if (j < r1 - r0) z[j] = gv[u];
         }
       }
     } else {
@@ -749,14 +755,15 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
         const bool spec_all = use_z2 && !flush && C > npend;   // z2 = committed + every change
         if (C == 0) {
           // no change to apply: detection only, from z
-          for (int i = pos + tid; i < range_end; i += NT)
-            if (fabs(z[i]) > lam && i != gc && !((oldmask[i >> 5] >> (i & 31)) & 1u)) {
+          for (int i = max(pos, r0) + tid; i < min(range_end, r1); i += NT)
+            if (fabs(z[i - r0]) > lam && i != gc && !((oldmask[i >> 5] >> (i & 31)) & 1u)) {
               best = i;
-              bestw = z[i];
+              bestw = z[i - r0];
               break;
             }
         } else {
-          const PassArgs A{z, z2, oldmask, P.Gtab, p, npend, C, pos, range_end, gc, spec_all, lam};
+          const PassArgs A{z - r0, z2 ? z2 - r0 : nullptr, oldmask, P.Gtab, p, npend, C, pos,
+                           range_end, gc, spec_all, lam, r0, r1};
           run_pass<NT, EVEN, PASS_U, PASS_PD>(A, TS, best, bestw);
         }
         // first new row: block-wide minimum (and its visit value)
@@ -770,6 +777,7 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
 #pragma unroll
         for (int w = 0; w < NT / 32; ++w)
           if (TS.wmin[w] < jstar) { jstar = TS.wmin[w]; wsrc = w; }
+        const double wstar_c = TS.wval[wsrc];
         if (flush) { npend = 0; break; }
         // ---- commit (every thread takes the same decisions from shared memory)
         int nvalid = K;
@@ -795,7 +803,7 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
         if (swap) { double* t = z; z = z2; z2 = t; }
         cursor += nvalid;
         if (jstar != 0x7fffffff) {
-          const double a = TS.wval[wsrc];                      // b = 0: a = z_j
+          const double a = wstar_c;                            // b = 0: a = z_j
           const double bn = soft_t(a, lam);                    // nonzero (|a| > lambda)
           const double d = 0.0 - bn;
           if (ncnt < nzcap) { if (tid == 0) { nrow[ncnt] = jstar; nv[ncnt] = bn; } }
