@@ -13,6 +13,7 @@ with pinned host buffers (H2D of X and D2H of Theta/sigma/iters inside the timed
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import math
 import os
@@ -556,6 +557,42 @@ def run_ours(args):
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e_tot,
                "api": "spmesl_fit_ex (host pointers)" if world == 1 else
                       "fit_distributed with host pinned H2D/D2H"}
+        if world == 1:
+            # the same fit through the host sparse-output entry (Theta as CSC host arrays: no
+            # 8 p^2-byte host array to fill); context beside the dense BASELINE signature
+            cap = p + 16 * p
+            cph = np.empty(p + 1, np.int64)
+            rh = np.empty(cap, np.int32)
+            vh = np.empty(cap, np.float64)
+            sh2 = np.empty(p)
+            ih2 = np.empty(p, np.int32)
+            L = S.load()
+            o2 = S.default_options(mode=S.MODES[args.mode], solver=S.SOLVERS[args.solver])
+
+            def sparse_step():
+                nz = ctypes.c_int64(0)
+                rc = L.spmesl_fit_sparse(ctypes.c_void_p(Xh.data_ptr()), n, p, lam, TOL, MAX_ITER,
+                                         ctypes.byref(o2), ctypes.c_void_p(cph.ctypes.data),
+                                         ctypes.c_void_p(rh.ctypes.data),
+                                         ctypes.c_void_p(vh.ctypes.data), cap, ctypes.byref(nz),
+                                         ctypes.c_void_p(sh2.ctypes.data),
+                                         ctypes.c_void_p(ih2.ctypes.data), None, None, None)
+                assert rc >= 0, L.spmesl_last_error()
+                return nz.value
+            for _ in range(2):
+                sparse_step()
+            s_ms = []
+            for k in range(max(1, min(args.steps, 5))):
+                flush.fill_(k % 255 + 1)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                nnz_e = sparse_step()
+                s_ms.append(1000 * (time.perf_counter() - t0))
+            sm_ = float(np.median(s_ms))
+            e2e["sparse_output"] = {"value": upd_per_step / (sm_ / 1000.0), "unit": UNIT,
+                                    "ms_per_step": sm_, "h2d_bytes_per_step": 8 * n * p,
+                                    "d2h_bytes_per_step": 8 * (p + 1) + 12 * int(nnz_e) + 12 * p,
+                                    "api": "spmesl_fit_sparse (host pointers, Theta as CSC)"}
     per_config = None
     if world == 1 and not args.no_per_config and args.mode == "per_column" and args.solver == "auto":
         per_config = per_config_block(S, dev, stream, flush, seeds=args.per_config_seeds)

@@ -202,6 +202,21 @@ int spmesl_fit_sparse_device(const double* dX, int64_t n, int64_t p, double lamb
                              uint8_t* dConverged, void* cuda_stream, spmesl_stats* st);
 
 /*
+ * Host sparse-output entry point: as spmesl_fit_ex (host X), with Theta returned in compressed
+ * sparse column form in host buffers — col_ptr[p + 1] (int64), rows[cap] (int32, ascending
+ * within a column), vals[cap] (double); symmetric, so also its CSR form; diagonal included;
+ * every entry equals the dense output's bit for bit (spmesl_fit_sparse_device on the current
+ * or options.device device).  Only the nonzeros cross PCIe and no p x p array is written.
+ * *nnz_out receives the entry count; if it exceeds cap the call returns SPMESL_ERR_ARG with
+ * col_ptr/rows/vals untouched (call again with cap >= *nnz_out).  sigma / iters [p];
+ * sweeps / converged (nullable) [p].  Blocking.
+ */
+int spmesl_fit_sparse(const double* X, int64_t n, int64_t p, double lambda0, double tol,
+                      int32_t max_iter, const spmesl_options* opt, int64_t* col_ptr,
+                      int32_t* rows, double* vals, int64_t cap, int64_t* nnz_out, double* sigma,
+                      int32_t* iters, int32_t* sweeps, uint8_t* converged, spmesl_stats* st);
+
+/*
  * Multi-GPU building blocks (one process per GPU; columns [col_begin, col_end) on this rank,
  * X replicated; BASELINE.json north_star "column-block sharding ... one all-gather").
  *

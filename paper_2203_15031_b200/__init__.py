@@ -102,6 +102,40 @@ def fit(X, lambda0: float, tol: float = 1e-4, max_iter: int = 100, *, out_theta=
     return FitResult(rc, Theta, sigma, iters, sweeps, conv.astype(bool), st.asdict())
 
 
+def fit_sparse(X, lambda0: float, tol: float = 1e-4, max_iter: int = 100, *, cap=None,
+               **options) -> dict:
+    """spmesl_fit_sparse on host memory: Theta as CSC numpy arrays (col_ptr int64 [p+1], rows
+    int32, vals float64; symmetric, so also CSR) without the dense p x p array, plus sigma /
+    iters / sweeps / converged.  cap: entry capacity (default p + 16 p; retried once with the
+    count needed)."""
+    X = np.asfortranarray(np.asarray(X, dtype=np.float64))
+    n, p = X.shape
+    cap = int(cap) if cap is not None else p + 16 * p
+    col_ptr = np.empty(p + 1, np.int64)
+    sigma = np.empty(p)
+    iters = np.empty(p, np.int32)
+    sweeps = np.empty(p, np.int32)
+    conv = np.empty(p, np.uint8)
+    o = _opts(**options)
+    for attempt in range(2):
+        rows = np.empty(max(cap, 1), np.int32)
+        vals = np.empty(max(cap, 1), np.float64)
+        nnz = ctypes.c_int64(0)
+        st = Stats()
+        rc = load().spmesl_fit_sparse(_vp(X), n, p, float(lambda0), float(tol), int(max_iter),
+                                      ctypes.byref(o), _vp(col_ptr), _vp(rows), _vp(vals), cap,
+                                      ctypes.byref(nnz), _vp(sigma), _vp(iters), _vp(sweeps),
+                                      _vp(conv), ctypes.byref(st))
+        if rc == _lib.ERR_ARG and nnz.value > cap:
+            cap = int(nnz.value)
+            continue
+        _lib.check(rc, st)
+        break
+    k = nnz.value
+    return dict(code=rc, col_ptr=col_ptr, rows=rows[:k], vals=vals[:k], sigma=sigma, iters=iters,
+                sweeps=sweeps, converged=conv.astype(bool), stats=st.asdict())
+
+
 def as_colmajor(X):
     """torch (n, p) tensor -> same values with column-major (Fortran) strides."""
     if X.dim() != 2:

@@ -85,7 +85,7 @@ EXPORTS = [
     "spmesl_fit_columns_device", "spmesl_assemble_device", "spmesl_gram_tile_count",
     "spmesl_gram_screen_device", "spmesl_fit_columns_gram_device", "spmesl_gram_supported",
     "spmesl_fit_path_device", "spmesl_screen_tile_count", "spmesl_fit_sparse_device",
-    "spmesl_screen_accumulators_device", "spmesl_lambda_univ",
+    "spmesl_screen_accumulators_device", "spmesl_fit_sparse", "spmesl_lambda_univ",
     "spmesl_lambda_ub", "spmesl_lambda_pb", "spmesl_solve_k", "spmesl_last_error",
     "spmesl_release_workspace", "spmesl_version",
 ]
@@ -139,6 +139,9 @@ def load() -> ctypes.CDLL:
     L.spmesl_assemble_device.restype = ctypes.c_int
     L.spmesl_screen_accumulators_device.argtypes = [vp, i64, i64, popt, vp, i64, vp, vp, vp]
     L.spmesl_screen_accumulators_device.restype = ctypes.c_int
+    L.spmesl_fit_sparse.argtypes = [vp, i64, i64, dbl, dbl, i32, popt, vp, vp, vp, i64,
+                                    ctypes.POINTER(i64), vp, vp, vp, vp, pst]
+    L.spmesl_fit_sparse.restype = ctypes.c_int
     for f in ("spmesl_lambda_univ",):
         getattr(L, f).argtypes = [i64, i64]
         getattr(L, f).restype = dbl

@@ -1451,6 +1451,23 @@ void init_stats(spmesl_stats* st) {
 
 }  // namespace
 
+// staging buffers of the host sparse-output entry, per device
+namespace {
+struct SparseStage {
+  std::mutex mu;
+  Buffer x, colptr, rows, vals, sigma, iters, sweeps, conv;
+};
+std::mutex g_stage_mu;
+std::vector<SparseStage*> g_stage;
+SparseStage* stage_for(int dev) {
+  std::lock_guard<std::mutex> lk(g_stage_mu);
+  if ((int)g_stage.size() <= dev) g_stage.resize(dev + 1, nullptr);
+  if (!g_stage[dev]) g_stage[dev] = new SparseStage();
+  return g_stage[dev];
+}
+}  // namespace
+
+
 namespace spmesl {
 int multi_fail(int code, const std::string& msg) { return fail(code, msg); }
 int fit_multi_device(const double* X, int64_t n, int64_t p, double lambda0, double tol,
@@ -1479,6 +1496,24 @@ const char* spmesl_last_error(void) { return g_last_error.c_str(); }
 const char* spmesl_version(void) { return "spmesl-b200 0.1 (sm_100a)"; }
 
 int spmesl_release_workspace(void) {
+  {
+    std::lock_guard<std::mutex> ls(g_stage_mu);
+    int prev0 = -1;
+    cudaGetDevice(&prev0);
+    for (size_t d = 0; d < g_stage.size(); ++d) {
+      SparseStage* S = g_stage[d];
+      if (!S) continue;
+      std::lock_guard<std::mutex> l2(S->mu);
+      cudaSetDevice((int)d);
+      for (Buffer* b : {&S->x, &S->colptr, &S->rows, &S->vals, &S->sigma, &S->iters, &S->sweeps,
+                        &S->conv}) {
+        if (b->ptr) cudaFree(b->ptr);
+        b->ptr = nullptr;
+        b->bytes = 0;
+      }
+    }
+    if (prev0 >= 0) cudaSetDevice(prev0);
+  }
   std::lock_guard<std::mutex> lk(g_ws_mu);
   int prev = -1;
   cudaGetDevice(&prev);
@@ -1860,6 +1895,58 @@ int spmesl_fit_ex(const double* X, int64_t n, int64_t p, double lambda0, double 
     st->bad_column = -1;
   }
   return any_unconv ? SPMESL_WARN_NOT_CONVERGED : SPMESL_OK;
+}
+
+// Host sparse-output entry (spmesl.h): the device sparse fit on this device's staging buffers
+// (SparseStage, kept per device behind their own lock; the fit serialises on the workspace lock).
+int spmesl_fit_sparse(const double* X, int64_t n, int64_t p, double lambda0, double tol,
+                      int32_t max_iter, const spmesl_options* opt, int64_t* col_ptr,
+                      int32_t* rows, double* vals, int64_t cap, int64_t* nnz_out, double* sigma,
+                      int32_t* iters, int32_t* sweeps, uint8_t* converged, spmesl_stats* st) {
+  init_stats(st);
+  spmesl_options o = resolve(opt);
+  int rc = validate(X, n, p, lambda0, tol, max_iter, o);
+  if (rc) return rc;
+  if (!col_ptr || !rows || !vals || !nnz_out || !sigma || !iters || cap < 0)
+    return fail(SPMESL_ERR_ARG, "output pointer is NULL");
+  int dev;
+  if ((rc = current_device(o.device, &dev))) return rc;
+  SparseStage* S = stage_for(dev);
+  std::lock_guard<std::mutex> lk(S->mu);
+  const size_t np = (size_t)n * (size_t)p;
+  const int64_t dcap = std::max<int64_t>(cap, p + 16 * p);   // (device side: room to report)
+  if ((rc = ensure(S->x, np * 8))) return rc;
+  if ((rc = ensure(S->colptr, (size_t)(p + 1) * 8))) return rc;
+  if ((rc = ensure(S->rows, (size_t)dcap * 4))) return rc;
+  if ((rc = ensure(S->vals, (size_t)dcap * 8))) return rc;
+  if ((rc = ensure(S->sigma, (size_t)p * 8))) return rc;
+  if ((rc = ensure(S->iters, (size_t)p * 4))) return rc;
+  if ((rc = ensure(S->sweeps, (size_t)p * 4))) return rc;
+  if ((rc = ensure(S->conv, (size_t)p))) return rc;
+  cudaStream_t s = nullptr;
+  CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  struct StreamGuard { cudaStream_t s; ~StreamGuard() { cudaStreamDestroy(s); } } sg{s};
+  CUDA_TRY(cudaMemcpyAsync(S->x.ptr, X, np * 8, cudaMemcpyHostToDevice, s));
+  int64_t nnz = 0;
+  rc = spmesl_fit_sparse_device((const double*)S->x.ptr, n, p, lambda0, tol, max_iter, &o,
+                                (int64_t*)S->colptr.ptr, (int32_t*)S->rows.ptr,
+                                (double*)S->vals.ptr, dcap, &nnz, (double*)S->sigma.ptr,
+                                (int32_t*)S->iters.ptr, (int32_t*)S->sweeps.ptr,
+                                (uint8_t*)S->conv.ptr, s, st);
+  *nnz_out = nnz;
+  if (rc < 0) return rc;
+  if (nnz > cap) return fail(SPMESL_ERR_ARG, "sparse Theta capacity too small: need " + std::to_string(nnz));
+  CUDA_TRY(cudaMemcpyAsync(col_ptr, S->colptr.ptr, (size_t)(p + 1) * 8, cudaMemcpyDeviceToHost, s));
+  if (nnz) {
+    CUDA_TRY(cudaMemcpyAsync(rows, S->rows.ptr, (size_t)nnz * 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(vals, S->vals.ptr, (size_t)nnz * 8, cudaMemcpyDeviceToHost, s));
+  }
+  CUDA_TRY(cudaMemcpyAsync(sigma, S->sigma.ptr, (size_t)p * 8, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(iters, S->iters.ptr, (size_t)p * 4, cudaMemcpyDeviceToHost, s));
+  if (sweeps) CUDA_TRY(cudaMemcpyAsync(sweeps, S->sweeps.ptr, (size_t)p * 4, cudaMemcpyDeviceToHost, s));
+  if (converged) CUDA_TRY(cudaMemcpyAsync(converged, S->conv.ptr, (size_t)p, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return rc;
 }
 
 int spmesl_fit(const double* X, int64_t n, int64_t p, double lambda0, double tol,

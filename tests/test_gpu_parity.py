@@ -613,3 +613,26 @@ def test_bare_spmesl_fit_status_codes(S, oracle):
     Y[5, 9] = np.nan
     assert _bare_fit(S, Y, lam)[0] == -3                              # SPMESL_ERR_NONFINITE
     assert _bare_fit(S, X, lam)[0] == 0                               # and it recovers
+
+
+@pytest.mark.parametrize("cfg,over", [(2, {}), (5, dict(p=3000))])
+def test_host_sparse_entry_point(S, oracle, cfg, over):
+    """spmesl_fit_sparse (host X, Theta as host CSC): every entry equals the dense host fit's,
+    which the oracle checks; a capacity that is too small reports the count needed."""
+    X, _, spec = G.make_config(cfg, **over)
+    n, p = X.shape
+    lam = oracle.lambda_univ(n, p)
+    dense = S.fit(X, lam)
+    sp = S.fit_sparse(X, lam, cap=p + 4)       # (retried with the count needed)
+    cp, rows, vals = sp["col_ptr"], sp["rows"], sp["vals"]
+    assert cp[0] == 0 and cp[-1] == len(rows)
+    T = np.zeros((p, p))
+    for k in range(p):
+        r = rows[cp[k]:cp[k + 1]]
+        assert np.all(np.diff(r) > 0) and k in r
+        T[r, k] = vals[cp[k]:cp[k + 1]]
+    assert np.array_equal(T, dense.Theta)
+    assert np.array_equal(sp["sigma"], dense.sigma) and np.array_equal(sp["iters"], dense.iters)
+    assert np.array_equal(sp["sweeps"], dense.sweeps)
+    ora = oracle.spmesl_fit(X, lam)
+    assert_parity(compare(T, sp["sigma"], sp["iters"], sp["sweeps"], ora))
