@@ -354,10 +354,23 @@ __global__ void tail_mark_kernel(const TailState* __restrict__ tail, int M, cons
 // covariance-update loop, in the same order (changes in row order), and every visit sees the
 // same value — the iterates are bit-identical to it.  Per sweep the dependent chain is one
 // pass (plus one per new row) instead of one block-wide update + search per change.
+#ifdef SPMESL_TAIL_PROF   // (development build only: per-phase cycle counters of the sweep kernel)
+__device__ unsigned long long g_tail_prof[32];
+#define TPROF_T(v) const long long v = clock64()
+#define TPROF_C(stmt) stmt
+#define TPROF_ADD(i, val) do { if (threadIdx.x == 0) atomicAdd(&g_tail_prof[i], (unsigned long long)(val)); } while (0)
+#else
+#define TPROF_T(v)
+#define TPROF_ADD(i, val)
+#define TPROF_C(stmt)
+#endif
 constexpr int KMAX = 31;    // old rows per speculative chain (lanes of warp 0)
 constexpr int PMAX = 32;    // pending changes (valid chain entries + one new row)
 constexpr int PASS_U = 4;   // row pairs per thread per chunk of the pass (one LDG.128 each)
 constexpr int PASS_PD = 2;  // columns whose loads are in flight (deeper spills: slower)
+constexpr int KMS = 31;     // multi-sweep mode: at most KMS nonzeros (the whole support in one chain)
+constexpr int MMAX = 32;    //   and at most MMAX sweeps speculated at once (16 when K > 16: the
+constexpr int MDCAP = 512;  //   changes and new values are MDCAP doubles each, stride 16 or 32)
 
 struct TailShared {
   uint64_t z_bar;        // z <- G[:, c] bulk copy
@@ -380,6 +393,11 @@ struct TailShared {
   int crow[PMAX + KMAX]; // the pass's Gram columns: pending changes, then nonzero chain changes
   double cd[PMAX + KMAX];
   int cO[PMAX + KMAX];   // (chain columns: their row O_l; pending: -1)
+  int sg_full;           // SG holds the whole K x K block (multi-sweep), not only k < m
+  int mkey;              // multi-sweep pass: smallest (sweep, row) key of a new row found so far
+  int mi[4];             // multi-sweep commit: old count, cursor, new count, changes
+  double mmaxd;          //   and max |d| of the sweep in progress
+  double mds[MMAX];      // multi-sweep: sum_l |d_sl| per sweep
 };
 constexpr size_t TS_BYTES = (sizeof(TailShared) + 127) & ~(size_t)127;
 
@@ -580,7 +598,151 @@ __device__ __forceinline__ void run_pass(const PassArgs& A, const TailShared& TS
   }
 }
 
-template <int NT, bool EVEN, int MINB>
+// Multi-sweep pass.  When the column's whole support fits one chain (K <= KMS
+// rows O_0 < ... < O_{K-1}) and no change is pending, warp 0 runs the chain for up to 32 whole
+// sweeps ahead (16 when K > 16; assuming no other row enters; it stops at the sweep that ends
+// the inner loop), recording every change d[s][l]; one pass then loads each row's K Gram
+// entries G[i, O_l] once and applies all M K changes in their order (sweep s, then l), testing
+// every row i outside the chain at its visit in each sweep (after the changes of sweep s at rows
+// O_l < i).  SPEC: write the result to zd, record the first (sweep, row) with |w| > lambda as
+// key s p + i.  !SPEC (after a new row at (sstar, istar)): apply only the changes before it —
+// sweeps < sstar, and in sweep sstar the qstar chain rows before istar — to z in place.  The
+// FMAs are the one-row-at-a-time loop's, in its order, plus FMAs with d = 0 (a zero change, the
+// padding beyond K): those leave every z_i unchanged up to the sign of a zero, on which no
+// decision or coefficient depends (|w| > lambda; Soft(+-0 + b) = Soft(b)).  So the iterates are
+// bit-identical to the per-sweep chain + pass and to the one-row-at-a-time loop.
+template <int NT, int KR, int R, bool SPEC>
+__device__ __forceinline__ void run_mpass(const double* zs, double* zd, const uint32_t* oldmask,
+                                          const double* Gtab, const TailShared& TS, const double* MD,
+                                          int KS, const double* MDS, int p, int K, int Msw, int gc,
+                                          double lam, int sstar, int qstar, int* mkey, int& best,
+                                          double& bestw) {
+  // chunks of R NT rows: R rows per thread (rows base + r NT + tid), R K loads in flight per
+  // thread.  Every thread walks every chunk (rows >= p masked), so warp votes see all lanes.
+  constexpr int RN = R * NT;
+  const int tid = threadIdx.x;
+  // a row can only enter in sweep s if |w| > lambda at its visit; |w| <= |a| + max_l |G[i, O_l]|
+  // sum_l |d_sl| (a: its value at the start of the sweep), so a sweep whose bound stays below
+  // lambda (1 - 2^-40) for every row of a warp (the margin covers the rounding of w and of the
+  // bound) needs no test site: its K changes are applied straight
+  const double lamm = lam - lam * 0x1p-40;
+  const int best_in = best;
+  for (int base = 0; base < p; base += RN) {
+    double g[R][KR];
+#pragma unroll
+    for (int l = 0; l < KR; ++l) {
+      const double* gcol = Gtab + (size_t)(l < K ? TS.so[l] : 0) * p;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int i = base + r * NT + tid;
+        g[r][l] = (l < K && i < p) ? __ldcg(gcol + i) : 0.0;
+      }
+    }
+    double acc[R];
+    float gm[R];              // max_l |G[i, O_l]| rounded up
+    int q[R];
+    bool t[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = base + r * NT + tid;
+      acc[r] = i < p ? zs[i] : 0.0;
+      q[r] = 0;
+      gm[r] = 0.0f;
+      t[r] = SPEC && i < p && i != gc && !((oldmask[i >> 5] >> (i & 31)) & 1u);
+    }
+    int smax = sstar + 1;
+    if (SPEC) {
+#pragma unroll
+      for (int l = 0; l < KR; ++l)
+#pragma unroll
+        for (int r = 0; r < R; ++r) gm[r] = fmaxf(gm[r], __double2float_ru(fabs(g[r][l])));
+      for (int l = 0; l < K; ++l) {
+        const int o = TS.so[l];
+#pragma unroll
+        for (int r = 0; r < R; ++r) q[r] += o < base + r * NT + tid;
+      }
+      // a new row already found: later sweeps are moot (warp-uniform: the vote below)
+      const int cut = __reduce_min_sync(0xffffffffu, min(*(volatile const int*)mkey, best));
+      smax = cut == 0x7fffffff ? Msw : min(Msw, cut / p + 1);
+    }
+    auto rec = [&](bool f, int s, int i, double w) {   // (predicated, no branch per site)
+      const int key = s * p + i;
+      const bool take = f && key < best;
+      best = take ? key : best;
+      bestw = take ? w : bestw;
+    };
+    for (int s = 0; s < smax; ++s) {
+      const double* md = MD + s * KS;
+      bool exact = false;
+      if (SPEC) {
+        const double Ds = MDS[s];
+        bool f = false;
+#pragma unroll
+        for (int r = 0; r < R; ++r) f |= t[r] && fma((double)gm[r], Ds, fabs(acc[r])) >= lamm;
+        exact = __any_sync(0xffffffffu, f);
+      }
+      if (!exact && (SPEC || s < sstar)) {
+        // no row of the warp can enter in this sweep: the K changes (MD is zero-padded to KR)
+#pragma unroll
+        for (int l = 0; l < KR; ++l) {
+          const double d = md[l];
+#pragma unroll
+          for (int r = 0; r < R; ++r) acc[r] = fma(d, g[r][l], acc[r]);
+        }
+      } else if (!SPEC) {
+        // (the rollback's last sweep: only the chain rows before the new row)
+#pragma unroll
+        for (int l = 0; l < KR; ++l) {
+          const double d = l < qstar ? md[l] : 0.0;
+#pragma unroll
+          for (int r = 0; r < R; ++r) acc[r] = fma(d, g[r][l], acc[r]);
+        }
+      } else {
+        // test every row at its visit: after the changes of the chain rows before it
+#pragma unroll
+        for (int l = 0; l < KR; ++l) {
+          const double d = md[l];
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            rec(l == q[r] && t[r] && fabs(acc[r]) > lam, s, base + r * NT + tid, acc[r]);
+            acc[r] = fma(d, g[r][l], acc[r]);
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          rec(q[r] >= K && t[r] && fabs(acc[r]) > lam, s, base + r * NT + tid, acc[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = base + r * NT + tid;
+      if (i < p) zd[i] = acc[r];
+    }
+    if (SPEC && best < best_in) atomicMin(mkey, best);
+  }
+}
+
+template <int NT, bool SPEC>
+__device__ __forceinline__ void mpass(const double* zs, double* zd, const uint32_t* oldmask,
+                                      const double* Gtab, const TailShared& TS, const double* MD,
+                                      int KS, const double* MDS, int p, int K, int Msw, int gc,
+                                      double lam, int sstar, int qstar, int* mkey, int& best,
+                                      double& bestw) {
+  if (K <= 4)
+    run_mpass<NT, 4, 4, SPEC>(zs, zd, oldmask, Gtab, TS, MD, KS, MDS, p, K, Msw, gc, lam, sstar,
+                              qstar, mkey, best, bestw);
+  else if (K <= 8)
+    run_mpass<NT, 8, 4, SPEC>(zs, zd, oldmask, Gtab, TS, MD, KS, MDS, p, K, Msw, gc, lam, sstar,
+                              qstar, mkey, best, bestw);
+  else if (K <= 16)
+    run_mpass<NT, 16, 2, SPEC>(zs, zd, oldmask, Gtab, TS, MD, KS, MDS, p, K, Msw, gc, lam, sstar,
+                               qstar, mkey, best, bestw);
+  else
+    run_mpass<NT, 32, 1, SPEC>(zs, zd, oldmask, Gtab, TS, MD, KS, MDS, p, K, Msw, gc, lam, sstar,
+                               qstar, mkey, best, bestw);
+}
+
+template <int NT, bool EVEN, int MINB, bool MULTI>
 __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P) {
   extern __shared__ __align__(128) unsigned char sm[];
   const int p = P.p, n = P.n, n_pad = P.n_pad, nchunk = P.nchunk, nzcap = P.nzcap;
@@ -609,6 +771,7 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
   if (tid == 0) {
     TS.oc_next = 0;
     TS.sg_n = -1;
+    TS.sg_full = 0;
     mbar_init_t(&TS.z_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -623,6 +786,7 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
     bsync();
     const int k = TS.k;
     if (k >= M) break;
+    TPROF_T(tpc);
     const int slot = P.joint ? P.work[k] : k;
     const TailState ts = P.joint ? P.jtail[slot] : P.tail[k];
     const int col = ts.lam * P.slot_stride + ts.col;         // lists / outputs index
@@ -679,6 +843,10 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
     int npend = 0;                   // pending changes (TS.prow / TS.pd), carried across sweeps
     long long nchg = 0;              // coordinate changes d != 0 (each reads one Gram column)
     long long npass = 0;             // chain + pass segments
+    TPROF_C(long long c_ok = 0; long long c_fail = 0; long long c_single = 0; long long c_oksw = 0;
+            long long c_spec = 0; long long c_chain = 0; long long c_single_cyc = 0;)
+    int mult = MMAX;                 // multi-sweep mode: sweeps to speculate next (the chain also
+                                     // stops at the sweep that ends the inner loop)
     bsync();
     bool retire = false;
     while (!retire) {
@@ -687,10 +855,216 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
       double maxd = 0.0;
       int pos = 0, cursor = 0, ncnt = 0;
       bool flush = false;            // (joint mode: a last pass that only applies the pending)
+      bool multi_done = false;       // whole sweeps done by the multi-sweep mode
+      if (MULTI && use_z2 && !P.joint && npend == 0 && ocnt > 0 && ocnt <= KMS && !overflow) {
+        // ---------------------------------------------- multi-sweep mode (run_mpass)
+        const int K = ocnt;
+        const int KS = K <= 16 ? 16 : 32;  // row stride of MD / MBN
+        const int mcap = MDCAP / KS;       // sweeps they hold (32 or 16)
+        double* MD = tvv;                  // [mcap][KS] changes d (aliases PG: no pending;
+                                           //   zero beyond K)
+        double* MBN = tvv + MDCAP;         // [mcap][KS] new values b'
+        double* MDS = TS.mds;              // [mcap] sum_l |d_sl| (the pass's entry bound)
+        ++npass;
+        TPROF_T(tp0);
+        TPROF_ADD(11, K);
+        int mine = 1;
+        for (int l = tid; l < K; l += NT) {
+          const int o = orow[l];
+          TS.so[l] = o;
+          if (TS.sg_rows[l] != o) mine = 0;
+        }
+        if (!__syncthreads_and(mine && TS.sg_n == K && TS.sg_full)) {
+          for (int e = tid; e < K * K; e += NT) {
+            const int kk = e / K, m = e - kk * K;
+            SG[kk * 32 + m] = __ldcg(P.Gtab + (size_t)orow[kk] * p + orow[m]);
+          }
+          for (int l = tid; l < K; l += NT) TS.sg_rows[l] = orow[l];
+          if (tid == 0) { TS.sg_n = K; TS.sg_full = 1; }
+        }
+        if (tid == 0) TS.mkey = 0x7fffffff;
+        bsync();
+        // chain over whole sweeps (warp 0, lane = chain row): a = z at the row's visit
+        if (warp == 0) {
+          double a = 0.0, bo = 0.0;
+          if (lane < K) { a = z[TS.so[lane]]; bo = ov[lane]; }
+          int me = 0;
+          for (int sw = 0; sw < min(mult, mcap); ++sw) {
+            double mx = 0.0, sd = 0.0;
+            if (lane >= K && lane < KS) MD[sw * KS + lane] = 0.0;
+            for (int kk = 0; kk < K; ++kk) {
+              double dk = 0.0;
+              if (lane == kk) {
+                const double bn = soft_t(a + bo, lam);
+                dk = bo - bn;
+                MD[sw * KS + kk] = dk;
+                MBN[sw * KS + kk] = bn;
+                bo = bn;
+              }
+              dk = __shfl_sync(0xffffffffu, dk, kk);
+              mx = fmax(mx, fabs(dk));
+              sd += fabs(dk);
+              if (lane < K && dk != 0.0) a = fma(dk, SG[kk * 32 + lane], a);
+            }
+            if (lane == 0) MDS[sw] = sd;
+            me = sw + 1;
+            if (mx < P.tol || inner + me >= P.max_inner) break;   // the inner loop ends here
+          }
+          if (lane == 0) TS.ncol = me;
+        }
+        bsync();
+        const int Msw = TS.ncol;
+        TPROF_T(tp1);
+        TPROF_ADD(0, tp1 - tp0);
+        TPROF_C(c_chain += tp1 - tp0;)
+        int best = 0x7fffffff;
+        double bestw = 0.0;
+        mpass<NT, true>(z, z2, oldmask, P.Gtab, TS, MD, KS, MDS, p, K, Msw, gc, lam, 0, 0,
+                        &TS.mkey, best, bestw);
+        {
+          const int wb = __reduce_min_sync(0xffffffffu, best);
+          if (best == wb && best != 0x7fffffff) TS.wval[warp] = bestw;
+          if (lane == 0) TS.wmin[warp] = wb;
+        }
+        bsync();
+        int jkey = 0x7fffffff, wsrc = 0;
+#pragma unroll
+        for (int w = 0; w < NT / 32; ++w)
+          if (TS.wmin[w] < jkey) { jkey = TS.wmin[w]; wsrc = w; }
+        const double wstar = TS.wval[wsrc];
+        TPROF_T(tp2);
+        TPROF_ADD(1, tp2 - tp1);
+        TPROF_C(c_spec += tp2 - tp1;)
+        if (jkey == 0x7fffffff) {
+          // every speculated sweep holds: z2 is z after them; the list is the last sweep's
+          { double* t = z; z = z2; z2 = t; }
+          if (warp == 0) {
+            const int sl = Msw - 1;
+            double bn = 0.0, dl = 0.0;
+            int cnt = 0;
+            if (lane < K) {
+              bn = MBN[sl * KS + lane];
+              dl = MD[sl * KS + lane];
+              for (int sw = 0; sw < Msw; ++sw) cnt += MD[sw * KS + lane] != 0.0;
+            }
+            const bool nz = lane < K && bn != 0.0;
+            const unsigned bal = __ballot_sync(0xffffffffu, nz);
+            if (nz) {
+              const int idx = __popc(bal & ((1u << lane) - 1u));
+              nrow[idx] = TS.so[lane];
+              nv[idx] = bn;
+            }
+            double mx = fabs(dl);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+              cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+            }
+            if (lane == 0) { TS.mi[2] = __popc(bal); TS.mi[3] = cnt; TS.mmaxd = mx; }
+          }
+          bsync();
+          ncnt = TS.mi[2];
+          nchg += TS.mi[3];
+          maxd = TS.mmaxd;
+          sweeps += Msw - 1;
+          inner += Msw - 1;
+          multi_done = true;
+          mult = MMAX;
+          TPROF_ADD(5, 1);
+          TPROF_ADD(7, Msw);
+          TPROF_C(++c_ok; c_oksw += Msw;)
+        } else {
+          // a new row at (sstar, istar): z <- z + the changes before it; the list of sweep
+          // sstar's start becomes the old list; sweep sstar continues below from istar
+          const int sstar = jkey / p, istar = jkey - sstar * p;
+          int qstar = 0;
+          for (int l = 0; l < K; ++l) qstar += TS.so[l] < istar;
+          int dummy = 0x7fffffff;
+          double dw = 0.0;
+          mpass<NT, false>(z, z, oldmask, P.Gtab, TS, MD, KS, MDS, p, K, sstar + 1, gc, lam,
+                           sstar, qstar, &TS.mkey, dummy, dw);
+          if (warp == 0) {
+            const int o = lane < K ? TS.so[lane] : 0;
+            double bst = 0.0, bns = 0.0, ds = 0.0;
+            int cnt = 0;
+            if (lane < K) {
+              bst = sstar > 0 ? MBN[(sstar - 1) * KS + lane] : ov[lane];
+              bns = MBN[sstar * KS + lane];
+              ds = lane < qstar ? MD[sstar * KS + lane] : 0.0;
+              for (int sw = 0; sw < sstar; ++sw) cnt += MD[sw * KS + lane] != 0.0;
+              cnt += ds != 0.0;
+            }
+            __syncwarp();
+            // old list at the start of sweep sstar: the chain rows with b != 0 there
+            const bool keep = lane < K && bst != 0.0;
+            const unsigned bk = __ballot_sync(0xffffffffu, keep);
+            if (lane < K && !keep) atomicAnd(&oldmask[o >> 5], ~(1u << (o & 31)));
+            if (keep) {
+              const int idx = __popc(bk & ((1u << lane) - 1u));
+              orow[idx] = o;
+              ov[idx] = bst;
+            }
+            const unsigned bc = __ballot_sync(0xffffffffu, keep && o < istar);
+            // sweep sstar so far: the chain rows before istar with b' != 0
+            const bool nz = lane < qstar && bns != 0.0;
+            const unsigned bn2 = __ballot_sync(0xffffffffu, nz);
+            if (nz) {
+              const int idx = __popc(bn2 & ((1u << lane) - 1u));
+              nrow[idx] = o;
+              nv[idx] = bns;
+            }
+            double mx = fabs(ds);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+              mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+              cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+            }
+            if (lane == 0) {
+              TS.mi[0] = __popc(bk);
+              TS.mi[1] = __popc(bc);
+              TS.mi[2] = __popc(bn2);
+              TS.mi[3] = cnt;
+              TS.mmaxd = mx;
+            }
+          }
+          bsync();
+          ocnt = TS.mi[0];
+          cursor = TS.mi[1];
+          ncnt = TS.mi[2];
+          nchg += TS.mi[3];
+          maxd = TS.mmaxd;
+          sweeps += sstar;
+          inner += sstar;
+          // the new row's visit (b = 0: a = w)
+          const double bn = soft_t(wstar, lam);
+          const double d = 0.0 - bn;
+          if (ncnt < nzcap) { if (tid == 0) { nrow[ncnt] = istar; nv[ncnt] = bn; } }
+          else overflow = true;
+          ++ncnt;
+          maxd = fmax(maxd, fabs(d));
+          ++nchg;
+          if (tid == 0) { TS.prow[0] = istar; TS.pd[0] = d; }
+          npend = 1;
+          pos = istar + 1;
+          mult = min(MMAX, max(4, 2 * (sstar + 1)));
+          TPROF_ADD(6, 1);
+          TPROF_C(++c_fail;)
+          TPROF_ADD(8, sstar);
+          TPROF_ADD(12, Msw);
+          ensure_gram_column(P, istar, TS, tx, tvv);          // (its barriers publish TS)
+          bsync();
+        }
+        TPROF_T(tp3);
+        TPROF_ADD(2, tp3 - tp2);
+      }
+      TPROF_T(tp4);
+      if (!multi_done)
       for (;;) {
         const int K = flush ? 0 : min(ocnt - cursor, KMAX);
         const int range_end = flush ? 0 : (cursor + K < ocnt ? orow[cursor + K] : p);
         ++npass;
+        TPROF_ADD(9, 1);
+        TPROF_C(++c_single;)
         // ---- chain inputs: rows, Gram blocks (all threads); SG is kept from the previous
         // segment with the same chain rows (a stable support: every sweep's chain is the same)
         int mine = 1;
@@ -708,7 +1082,7 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
             if (kk < m) SG[kk * 32 + m] = __ldcg(P.Gtab + (size_t)orow[cursor + kk] * p + orow[cursor + m]);
           }
           for (int l = tid; l < K; l += NT) TS.sg_rows[l] = orow[cursor + l];
-          if (tid == 0) TS.sg_n = K;
+          if (tid == 0) { TS.sg_n = K; TS.sg_full = 0; }
         }
         for (int e = tid; e < npend * K; e += NT) {
           const int j = e / K, m = e - j * K;
@@ -827,6 +1201,11 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
           break;
         }
       }
+      {
+        TPROF_T(tp5);
+        if (!multi_done) TPROF_ADD(3, tp5 - tp4);
+        TPROF_C(if (!multi_done) c_single_cyc += tp5 - tp4;)
+      }
       ++sweeps;
       ++inner;
       // the new list becomes the current one (and the old-row bitmap with it)
@@ -849,6 +1228,7 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
       }
       if (maxd < P.tol || inner >= P.max_inner) {
         if (!(maxd < P.tol)) flags |= 2;
+        TPROF_T(tpr);
         // fresh residual and sigma (reading g4): every thread builds its samples'
         // r_i = x~_ci - sum_m x~_{j_m i} b_m (m ascending, the CD kernel's per-element order),
         // then warp 0 sums r_i^2 in the CD kernel's order
@@ -874,7 +1254,36 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
         sigma = sn;
         inner = 0;
         bsync();
+        {
+          TPROF_T(tpr2);
+          TPROF_ADD(4, tpr2 - tpr);
+        }
       }
+    }
+    {
+      TPROF_T(tpe);
+      TPROF_ADD(10, tpe - tpc);
+#ifdef SPMESL_TAIL_PROF
+      if (tid == 0) {
+        const unsigned long long cyc = (unsigned long long)(tpe - tpc);
+        atomicMax(&g_tail_prof[13], (cyc << 24) | ((unsigned long long)min(npass, 4095ll) << 12) |
+                                        (unsigned long long)min(sweeps - ts.sweeps, 4095));
+        if (cyc > 4000000ull) atomicAdd(&g_tail_prof[14], 1ull);   // columns over ~2 ms
+        if (sweeps - ts.sweeps > 200) {                                // stragglers
+          atomicAdd(&g_tail_prof[16], 1ull);
+          atomicAdd(&g_tail_prof[17], (unsigned long long)c_ok);
+          atomicAdd(&g_tail_prof[18], (unsigned long long)c_fail);
+          atomicAdd(&g_tail_prof[19], (unsigned long long)c_single);
+          atomicAdd(&g_tail_prof[20], (unsigned long long)c_oksw);
+          atomicAdd(&g_tail_prof[21], (unsigned long long)c_spec);
+          atomicAdd(&g_tail_prof[22], (unsigned long long)c_chain);
+          atomicAdd(&g_tail_prof[23], (unsigned long long)c_single_cyc);
+          atomicAdd(&g_tail_prof[24], cyc);
+          atomicAdd(&g_tail_prof[25], (unsigned long long)(sweeps - ts.sweeps));
+        }
+        atomicMax(&g_tail_prof[15], (unsigned long long)(tpe));  // last column end (clock)
+      }
+#endif
     }
     // outputs: coefficients into the column's other list, per-column results
     const int dst = cur ^ 1;
@@ -967,13 +1376,20 @@ cudaError_t launch_tail_mark(const TailState* tail, int M, const int* nz_rows, i
   return cudaGetLastError();
 }
 
-template <int NT, bool EVEN, int MINB>
+template <int NT, bool EVEN, int MINB, bool MULTI>
 static cudaError_t launch_tail_t(const TailParams& P, int grid, size_t smem, cudaStream_t s) {
-  cudaError_t e = cudaFuncSetAttribute(tail_sweep_kernel<NT, EVEN, MINB>,
+  cudaError_t e = cudaFuncSetAttribute(tail_sweep_kernel<NT, EVEN, MINB, MULTI>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  tail_sweep_kernel<NT, EVEN, MINB><<<grid, NT, smem, s>>>(P);
+  tail_sweep_kernel<NT, EVEN, MINB, MULTI><<<grid, NT, smem, s>>>(P);
   return cudaGetLastError();
+}
+
+template <int NT, int MINB, bool MULTI>
+static cudaError_t launch_tail_e(const TailParams& P, int grid, size_t smem, cudaStream_t s) {
+  // even p: 16-byte row pairs everywhere
+  return (P.p & 1) == 0 ? launch_tail_t<NT, true, MINB, MULTI>(P, grid, smem, s)
+                        : launch_tail_t<NT, false, MINB, MULTI>(P, grid, smem, s);
 }
 
 cudaError_t launch_tail_sweeps(const TailParams& P, int grid, cudaStream_t s) {
@@ -981,11 +1397,23 @@ cudaError_t launch_tail_sweeps(const TailParams& P, int grid, cudaStream_t s) {
   if (P.z2) smem += tail_z2_bytes(P.p);
   if (P.occ > 1) grid *= P.occ;   // several column CTAs per SM (set_tail_shape)
   // 512 threads when a single column CTA owns the SM (large p: the pass splits over twice the
-  // threads), 256 when two share it; even p: 16-byte row pairs everywhere
-  const bool even = (P.p & 1) == 0;
+  // threads), 256 when two share it; the multi-sweep mode needs the second z buffer (and is
+  // compiled only into those variants: its registers would cost the others)
+  const bool multi = P.z2 && !P.joint;
   if (P.occ == 1)
-    return even ? launch_tail_t<512, true, 1>(P, grid, smem, s) : launch_tail_t<512, false, 1>(P, grid, smem, s);
-  return even ? launch_tail_t<256, true, 2>(P, grid, smem, s) : launch_tail_t<256, false, 2>(P, grid, smem, s);
+    return multi ? launch_tail_e<512, 1, true>(P, grid, smem, s) : launch_tail_e<512, 1, false>(P, grid, smem, s);
+  return multi ? launch_tail_e<256, 2, true>(P, grid, smem, s) : launch_tail_e<256, 2, false>(P, grid, smem, s);
 }
 
 }  // namespace spmesl
+
+#ifdef SPMESL_TAIL_PROF
+extern "C" int spmesl_dev_tail_prof(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, spmesl::g_tail_prof, sizeof(unsigned long long) * 32) != cudaSuccess) return 1;
+  if (reset) {
+    static const unsigned long long zero[32] = {};
+    if (cudaMemcpyToSymbol(spmesl::g_tail_prof, zero, sizeof(zero)) != cudaSuccess) return 1;
+  }
+  return 0;
+}
+#endif
