@@ -890,22 +890,26 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
           if (lane < K) { a = z[TS.so[lane]]; bo = ov[lane]; }
           int me = 0;
           for (int sw = 0; sw < min(mult, mcap); ++sw) {
-            double mx = 0.0, sd = 0.0;
-            if (lane >= K && lane < KS) MD[sw * KS + lane] = 0.0;
+            double mx = 0.0, sd = 0.0, myd = 0.0;
+            // (critical path per row: Soft, shuffle, one FMA; the Gram entry of the next row is
+            // loaded one step ahead and the lane's d and b' are stored after the sweep)
+            double sgn = lane < K ? SG[lane] : 0.0;
             for (int kk = 0; kk < K; ++kk) {
-              double dk = 0.0;
-              if (lane == kk) {
-                const double bn = soft_t(a + bo, lam);
-                dk = bo - bn;
-                MD[sw * KS + kk] = dk;
-                MBN[sw * KS + kk] = bn;
-                bo = bn;
-              }
-              dk = __shfl_sync(0xffffffffu, dk, kk);
+              const double sg = sgn;
+              if (kk + 1 < K && lane < K) sgn = SG[(kk + 1) * 32 + lane];
+              // every lane evaluates its own visit (no divergent branch); lane kk's counts
+              const double bn = soft_t(a + bo, lam);
+              const double dmine = bo - bn;                     // e += x_j d
+              const bool me_kk = lane == kk;
+              myd = me_kk ? dmine : myd;
+              bo = me_kk ? bn : bo;
+              const double dk = __shfl_sync(0xffffffffu, dmine, kk);
               mx = fmax(mx, fabs(dk));
               sd += fabs(dk);
-              if (lane < K && dk != 0.0) a = fma(dk, SG[kk * 32 + lane], a);
+              if (lane < K && dk != 0.0) a = fma(dk, sg, a);
             }
+            if (lane < KS) MD[sw * KS + lane] = myd;          // (zero beyond K)
+            if (lane < K) MBN[sw * KS + lane] = bo;
             if (lane == 0) MDS[sw] = sd;
             me = sw + 1;
             if (mx < P.tol || inner + me >= P.max_inner) break;   // the inner loop ends here
@@ -1269,6 +1273,9 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
         atomicMax(&g_tail_prof[13], (cyc << 24) | ((unsigned long long)min(npass, 4095ll) << 12) |
                                         (unsigned long long)min(sweeps - ts.sweeps, 4095));
         if (cyc > 4000000ull) atomicAdd(&g_tail_prof[14], 1ull);   // columns over ~2 ms
+        atomicMax(&g_tail_prof[28], (cyc << 16) | ((unsigned long long)min(ocnt, 255) << 8) |
+                                        (unsigned long long)min(c_fail, 255ll));
+        if (cyc > 4000000ull) atomicAdd(&g_tail_prof[29], (unsigned long long)ocnt);
         if (sweeps - ts.sweeps > 200) {                                // stragglers
           atomicAdd(&g_tail_prof[16], 1ull);
           atomicAdd(&g_tail_prof[17], (unsigned long long)c_ok);

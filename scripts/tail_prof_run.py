@@ -38,6 +38,7 @@ for which in (sys.argv[1:] or ["band3", "hub"]):
         print(f"  {nm:14s} {v[i]:>16d}{extra}")
     m = v[13]
     print(f"  slowest column: {m >> 24} cycles, {(m >> 12) & 4095} passes, {m & 4095} sweeps; columns over 4e6 cycles: {v[14]}")
+    print(f"  slowest column: final nnz {(v[28] >> 8) & 255}, failures {v[28] & 255}; mean final nnz of the columns over 4e6 cycles: {v[29] / max(v[14], 1):.1f}")
     if v[16]:
         print(f"  stragglers (>200 sweeps): {v[16]} columns, {v[25]} sweeps, {v[24]} cycles; multi ok {v[17]} "
               f"({v[20]} sweeps), fail {v[18]}, single segments {v[19]}; cycles: spec {v[21]}, chain {v[22]}, "
