@@ -46,7 +46,7 @@ for cfg, over, rule in cases:
     X, _, spec = G.make_config(cfg, **over)
     n, p = X.shape
     lam = S.lambda_ub(n, p) if rule == "ub" else S.lambda_univ(n, p)
-    Xd = torch.from_numpy(np.ascontiguousarray(X.T)).cuda().t().contiguous().t()
+    Xd = torch.from_numpy(np.ascontiguousarray(X.T)).cuda().t()   # n x p, column-major
     for solver in (3, 1):
         if solver == 1 and p > 6000:
             continue
