@@ -390,14 +390,27 @@ struct TailShared {
   double sbn[KMAX];      // chain new values b'_l
   int prow[PMAX];        // pending changes (rows ascending, not yet applied to z)
   double pd[PMAX];
-  int crow[PMAX + KMAX]; // the pass's Gram columns: pending changes, then nonzero chain changes
-  double cd[PMAX + KMAX];
-  int cO[PMAX + KMAX];   // (chain columns: their row O_l; pending: -1)
+  union {   // (per-segment pass / multi-sweep: never live at the same time)
+    struct {
+      int crow[PMAX + KMAX]; // the pass's Gram columns: pending changes, then nonzero chain changes
+      double cd[PMAX + KMAX];
+      int cO[PMAX + KMAX];   // (chain columns: their row O_l; pending: -1)
+    };
+    struct {
+      double mlam[MMAX];     // multi-sweep: lambda, sigma, outer / inner counts and flags in
+      double msig[MMAX];     //   effect in sweep s (the chain refits sigma where an inner loop
+      int mout[MMAX];        //   ends, and continues into the next outer iteration)
+      int minr[MMAX];
+      int mflg[MMAX];
+    };
+  };
   int sg_full;           // SG holds the whole K x K block (multi-sweep), not only k < m
   int mkey;              // multi-sweep pass: smallest (sweep, row) key of a new row found so far
   int mi[4];             // multi-sweep commit: old count, cursor, new count, changes
   double mmaxd;          //   and max |d| of the sweep in progress
   double mds[MMAX];      // multi-sweep: sum_l |d_sl| per sweep
+  double msig_e;         //   the state after the last sweep of the chain
+  int mout_e, minr_e, mflg_e, mret_e;
 };
 constexpr size_t TS_BYTES = (sizeof(TailShared) + 127) & ~(size_t)127;
 
@@ -615,17 +628,16 @@ template <int NT, int KR, int R, bool SPEC>
 __device__ __forceinline__ void run_mpass(const double* zs, double* zd, const uint32_t* oldmask,
                                           const double* Gtab, const TailShared& TS, const double* MD,
                                           int KS, const double* MDS, int p, int K, int Msw, int gc,
-                                          double lam, int sstar, int qstar, int* mkey, int& best,
-                                          double& bestw) {
+                                          const double* mlam, int sstar, int qstar, int* mkey,
+                                          int& best, double& bestw) {
   // chunks of R NT rows: R rows per thread (rows base + r NT + tid), R K loads in flight per
   // thread.  Every thread walks every chunk (rows >= p masked), so warp votes see all lanes.
   constexpr int RN = R * NT;
   const int tid = threadIdx.x;
-  // a row can only enter in sweep s if |w| > lambda at its visit; |w| <= |a| + max_l |G[i, O_l]|
-  // sum_l |d_sl| (a: its value at the start of the sweep), so a sweep whose bound stays below
-  // lambda (1 - 2^-40) for every row of a warp (the margin covers the rounding of w and of the
-  // bound) needs no test site: its K changes are applied straight
-  const double lamm = lam - lam * 0x1p-40;
+  // a row can only enter in sweep s if |w| > lambda_s at its visit; |w| <= |a| + max_l
+  // |G[i, O_l]| sum_l |d_sl| (a: its value at the start of the sweep), so a sweep whose bound
+  // stays below lambda_s (1 - 2^-40) for every row of a warp (the margin covers the rounding of
+  // w and of the bound) needs no test site: its K changes are applied straight
   const int best_in = best;
   for (int base = 0; base < p; base += RN) {
     double g[R][KR];
@@ -674,8 +686,10 @@ __device__ __forceinline__ void run_mpass(const double* zs, double* zd, const ui
     for (int s = 0; s < smax; ++s) {
       const double* md = MD + s * KS;
       bool exact = false;
+      const double lam = SPEC ? mlam[s] : 0.0;
       if (SPEC) {
         const double Ds = MDS[s];
+        const double lamm = lam - lam * 0x1p-40;
         bool f = false;
 #pragma unroll
         for (int r = 0; r < R; ++r) f |= t[r] && fma((double)gm[r], Ds, fabs(acc[r])) >= lamm;
@@ -726,19 +740,19 @@ template <int NT, bool SPEC>
 __device__ __forceinline__ void mpass(const double* zs, double* zd, const uint32_t* oldmask,
                                       const double* Gtab, const TailShared& TS, const double* MD,
                                       int KS, const double* MDS, int p, int K, int Msw, int gc,
-                                      double lam, int sstar, int qstar, int* mkey, int& best,
-                                      double& bestw) {
+                                      const double* mlam, int sstar, int qstar, int* mkey,
+                                      int& best, double& bestw) {
   if (K <= 4)
-    run_mpass<NT, 4, 4, SPEC>(zs, zd, oldmask, Gtab, TS, MD, KS, MDS, p, K, Msw, gc, lam, sstar,
+    run_mpass<NT, 4, 4, SPEC>(zs, zd, oldmask, Gtab, TS, MD, KS, MDS, p, K, Msw, gc, mlam, sstar,
                               qstar, mkey, best, bestw);
   else if (K <= 8)
-    run_mpass<NT, 8, 4, SPEC>(zs, zd, oldmask, Gtab, TS, MD, KS, MDS, p, K, Msw, gc, lam, sstar,
+    run_mpass<NT, 8, 4, SPEC>(zs, zd, oldmask, Gtab, TS, MD, KS, MDS, p, K, Msw, gc, mlam, sstar,
                               qstar, mkey, best, bestw);
   else if (K <= 16)
-    run_mpass<NT, 16, 2, SPEC>(zs, zd, oldmask, Gtab, TS, MD, KS, MDS, p, K, Msw, gc, lam, sstar,
+    run_mpass<NT, 16, 2, SPEC>(zs, zd, oldmask, Gtab, TS, MD, KS, MDS, p, K, Msw, gc, mlam, sstar,
                                qstar, mkey, best, bestw);
   else
-    run_mpass<NT, 32, 1, SPEC>(zs, zd, oldmask, Gtab, TS, MD, KS, MDS, p, K, Msw, gc, lam, sstar,
+    run_mpass<NT, 32, 1, SPEC>(zs, zd, oldmask, Gtab, TS, MD, KS, MDS, p, K, Msw, gc, mlam, sstar,
                                qstar, mkey, best, bestw);
 }
 
@@ -851,11 +865,12 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
     bool retire = false;
     while (!retire) {
       // ------------------------------------------------ one sweep, rows in cyclic order
-      const double lam = sigma * lambda0;
+      double lam = sigma * lambda0;
       double maxd = 0.0;
       int pos = 0, cursor = 0, ncnt = 0;
       bool flush = false;            // (joint mode: a last pass that only applies the pending)
-      bool multi_done = false;       // whole sweeps done by the multi-sweep mode
+      bool multi_done = false;       // whole sweeps done by the multi-sweep mode (with their
+      int msw_done = 0;              //   sigma refits: sweeps, outer, inner, flags, retire set)
       if (MULTI && use_z2 && !P.joint && npend == 0 && ocnt > 0 && ocnt <= KMS && !overflow) {
         // ---------------------------------------------- multi-sweep mode (run_mpass)
         const int K = ocnt;
@@ -889,7 +904,14 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
           double a = 0.0, bo = 0.0;
           if (lane < K) { a = z[TS.so[lane]]; bo = ov[lane]; }
           int me = 0;
+          double sig = sigma, lamc = lam;
+          int outr = outer, inr = inner, flg = flags, ret = 0;
           for (int sw = 0; sw < min(mult, mcap); ++sw) {
+            if (lane == 0) {
+              TS.mlam[sw] = lamc; TS.msig[sw] = sig; TS.mout[sw] = outr; TS.minr[sw] = inr;
+              TS.mflg[sw] = flg;
+            }
+            const double lam = lamc;
             double mx = 0.0, sd = 0.0, myd = 0.0;
             // (critical path per row: Soft, shuffle, one FMA; the Gram entry of the next row is
             // loaded one step ahead and the lane's d and b' are stored after the sweep)
@@ -912,9 +934,60 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
             if (lane < K) MBN[sw * KS + lane] = bo;
             if (lane == 0) MDS[sw] = sd;
             me = sw + 1;
-            if (mx < P.tol || inner + me >= P.max_inner) break;   // the inner loop ends here
+            ++inr;
+            if (mx < P.tol || inr >= P.max_inner) {
+              // the inner loop ends here: fresh residual and sigma, the same
+              // arithmetic as the block-wide refit below (per sample: x~_c minus the nonzeros
+              // in ascending row order; r_i^2 summed per lane in sample order, then the
+              // butterfly), and the outer stop; the chain goes on with the new lambda
+              if (!(mx < P.tol)) flg |= 2;
+              // (samples in tiles of 16 per lane: the 16 loads of one predictor are in flight
+              // together; the b values via shared memory)
+              if (lane < K) TS.sbn[lane] = bo;
+              __syncwarp();
+              double ss = 0.0;
+              for (int t0 = 0; t0 < n; t0 += 16 * 32) {
+                double ri[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                  const int i = t0 + u * 32 + lane;
+                  ri[u] = i < n ? P.Xb[xb_index(i, gc, nchunk)] : 0.0;
+                }
+                for (int m = 0; m < K; ++m) {
+                  const double bm = TS.sbn[m];
+                  if (bm == 0.0) continue;
+                  const int om = TS.so[m];
+                  double xv[16];
+#pragma unroll
+                  for (int u = 0; u < 16; ++u) {
+                    const int i = t0 + u * 32 + lane;
+                    xv[u] = i < n ? P.Xb[xb_index(i, om, nchunk)] : 0.0;
+                  }
+#pragma unroll
+                  for (int u = 0; u < 16; ++u) ri[u] = fma(-xv[u], bm, ri[u]);
+                }
+#pragma unroll
+                for (int u = 0; u < 16; ++u)
+                  if (t0 + u * 32 + lane < n) ss = fma(ri[u], ri[u], ss);
+              }
+              __syncwarp();
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+              double sn = sqrt(ss) / P.sqrt_n;
+              if (sn < P.sigma_floor) sn = P.sigma_floor;
+              ++outr;
+              if (fabs(sn - sig) < P.tol) { flg |= 1; ret = 1; }
+              else if (outr >= P.max_outer) ret = 1;
+              sig = sn;
+              lamc = sig * lambda0;
+              inr = 0;
+              if (ret) break;
+            }
           }
-          if (lane == 0) TS.ncol = me;
+          if (lane == 0) {
+            TS.ncol = me;
+            TS.msig_e = sig; TS.mout_e = outr; TS.minr_e = inr; TS.mflg_e = flg; TS.mret_e = ret;
+          }
         }
         bsync();
         const int Msw = TS.ncol;
@@ -923,7 +996,7 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
         TPROF_C(c_chain += tp1 - tp0;)
         int best = 0x7fffffff;
         double bestw = 0.0;
-        mpass<NT, true>(z, z2, oldmask, P.Gtab, TS, MD, KS, MDS, p, K, Msw, gc, lam, 0, 0,
+        mpass<NT, true>(z, z2, oldmask, P.Gtab, TS, MD, KS, MDS, p, K, Msw, gc, TS.mlam, 0, 0,
                         &TS.mkey, best, bestw);
         {
           const int wb = __reduce_min_sync(0xffffffffu, best);
@@ -970,8 +1043,10 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
           ncnt = TS.mi[2];
           nchg += TS.mi[3];
           maxd = TS.mmaxd;
-          sweeps += Msw - 1;
-          inner += Msw - 1;
+          sweeps += Msw;
+          sigma = TS.msig_e; outer = TS.mout_e; inner = TS.minr_e; flags = TS.mflg_e;
+          retire = TS.mret_e != 0;
+          msw_done = Msw;
           multi_done = true;
           mult = MMAX;
           TPROF_ADD(5, 1);
@@ -985,7 +1060,7 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
           for (int l = 0; l < K; ++l) qstar += TS.so[l] < istar;
           int dummy = 0x7fffffff;
           double dw = 0.0;
-          mpass<NT, false>(z, z, oldmask, P.Gtab, TS, MD, KS, MDS, p, K, sstar + 1, gc, lam,
+          mpass<NT, false>(z, z, oldmask, P.Gtab, TS, MD, KS, MDS, p, K, sstar + 1, gc, TS.mlam,
                            sstar, qstar, &TS.mkey, dummy, dw);
           if (warp == 0) {
             const int o = lane < K ? TS.so[lane] : 0;
@@ -1038,7 +1113,9 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
           nchg += TS.mi[3];
           maxd = TS.mmaxd;
           sweeps += sstar;
-          inner += sstar;
+          // the state in effect in sweep sstar (the chain may have refit sigma before it)
+          lam = TS.mlam[sstar]; sigma = TS.msig[sstar]; outer = TS.mout[sstar];
+          inner = TS.minr[sstar]; flags = TS.mflg[sstar];
           // the new row's visit (b = 0: a = w)
           const double bn = soft_t(wstar, lam);
           const double d = 0.0 - bn;
@@ -1210,8 +1287,10 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
         if (!multi_done) TPROF_ADD(3, tp5 - tp4);
         TPROF_C(if (!multi_done) c_single_cyc += tp5 - tp4;)
       }
-      ++sweeps;
-      ++inner;
+      if (!msw_done) {   // (a multi-sweep set its counters and refit sigma itself)
+        ++sweeps;
+        ++inner;
+      }
       // the new list becomes the current one (and the old-row bitmap with it)
       for (int m = tid; m < ocnt; m += NT) atomicAnd(&oldmask[orow[m] >> 5], ~(1u << (orow[m] & 31)));
       bsync();
@@ -1230,7 +1309,7 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
         for (int t = tid; t < p; t += NT) zs[t] = z[t];
         break;
       }
-      if (maxd < P.tol || inner >= P.max_inner) {
+      if (!msw_done && (maxd < P.tol || inner >= P.max_inner)) {
         if (!(maxd < P.tol)) flags |= 2;
         TPROF_T(tpr);
         // fresh residual and sigma (reading g4): every thread builds its samples'
