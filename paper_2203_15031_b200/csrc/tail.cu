@@ -871,6 +871,54 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
       bool flush = false;            // (joint mode: a last pass that only applies the pending)
       bool multi_done = false;       // whole sweeps done by the multi-sweep mode (with their
       int msw_done = 0;              //   sigma refits: sweeps, outer, inner, flags, retire set)
+      if (MULTI && use_z2 && !P.joint && npend == 0 && ocnt == 0 && sweeps == ts.sweeps &&
+          !overflow) {
+        // ---------------------------------------------- a column's first sweep (b = 0)
+        // The rows with |z| = |G[j, c]| close to lambda join the (empty) old list with b = 0:
+        // the chain visits them like old rows — Soft(a + 0) is exactly a new row's visit, and 0
+        // when |a| <= lambda — so the first sweep (and the sweeps after it) can run as one
+        // multi-sweep instead of one pass per entering row.  Only rows whose Gram column is
+        // present; at most 16 (the loosest of the thresholds 0.9, 0.95, 1.0 lambda that keeps
+        // the count within it); the iterates are unchanged (same visits, same arithmetic).
+        if (tid < 4) TS.mi[tid] = 0;
+        bsync();
+        int c0 = 0, c1 = 0, c2 = 0;
+        for (int i = tid; i < p; i += NT) {
+          const double az = fabs(z[i]);
+          if (az > 0.9 * lam && i != gc && (P.gtab_full || *(volatile const int*)&P.gstate[i] == 2)) {
+            ++c0;
+            if (az > 0.95 * lam) { ++c1; if (az > lam) ++c2; }
+          }
+        }
+        c0 = __reduce_add_sync(0xffffffffu, c0);
+        c1 = __reduce_add_sync(0xffffffffu, c1);
+        c2 = __reduce_add_sync(0xffffffffu, c2);
+        if (lane == 0) { atomicAdd(&TS.mi[0], c0); atomicAdd(&TS.mi[1], c1); atomicAdd(&TS.mi[2], c2); }
+        bsync();
+        const int t0 = TS.mi[0], t1 = TS.mi[1], t2 = TS.mi[2];
+        const double gam = t0 <= 16 ? 0.9 : t1 <= 16 ? 0.95 : 1.0;
+        const int nc = t0 <= 16 ? t0 : t1 <= 16 ? t1 : t2 <= 16 ? t2 : 0;
+        if (nc > 0) {
+          for (int i = tid; i < p; i += NT) {
+            const double az = fabs(z[i]);
+            if (az > gam * lam && i != gc && (P.gtab_full || *(volatile const int*)&P.gstate[i] == 2))
+              TS.so[atomicAdd(&TS.mi[3], 1)] = i;
+          }
+          bsync();
+          if (warp == 0) {   // ascending: lane = entry, rank by value
+            const int v = lane < nc ? TS.so[lane] : 0x7fffffff;
+            int rank = 0;
+            for (int m = 0; m < nc; ++m) rank += __shfl_sync(0xffffffffu, v, m) < v;
+            if (lane < nc) {
+              orow[rank] = v;
+              ov[rank] = 0.0;
+              atomicOr(&oldmask[v >> 5], 1u << (v & 31));
+            }
+          }
+          ocnt = nc;
+          bsync();
+        }
+      }
       if (MULTI && use_z2 && !P.joint && npend == 0 && ocnt > 0 && ocnt <= KMS && !overflow) {
         // ---------------------------------------------- multi-sweep mode (run_mpass)
         const int K = ocnt;
