@@ -218,13 +218,13 @@ PER_CONFIG = [
 ]
 
 
-def l2_read_peak():
-    """Measured L2 read bandwidth of this pool's B200 (microbench/peaks.cu, profiles/)."""
+def dfma_peak():
+    """Measured FP64 FMA throughput of this pool's B200 (microbench/peaks.cu, profiles/)."""
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "r01_peaks_microbench.json")))
-        return float(d["l2_read_gbs"]), "profiles/r01_peaks_microbench.json l2_read_gbs (measured)"
+        return float(d["dfma_tflops"]), "profiles/r01_peaks_microbench.json dfma_tflops (measured)"
     except Exception:
-        return 16700.0, "fallback 16.7 TB/s (round-1 microbench)"
+        return 36.8, "fallback 36.8 TFLOP/s (round-1 microbench)"
 
 
 def per_config_block(S, dev, stream, flush, seeds=3, fits=5):
@@ -232,12 +232,13 @@ def per_config_block(S, dev, stream, flush, seeds=3, fits=5):
     recommended lambda_univ): per workload and seed, the device time per fit
     (CUDA-graph replays, L2 flushed before each, CUDA events on the launching stream), the
     algorithmic coordinate updates per second, the sweep counts, and the covariance-update sweep
-    kernel's own time from an eager fit with its L2 fraction (8 p bytes of Gram column per
-    coordinate change + 8 p per column for its z, over the measured L2 read bandwidth).
+    kernel's own time from an eager fit with its algorithmic FP64 rate (every coordinate change
+    updates all p entries of z: p FMAs) against the measured DFMA peak; the kernel is bound by
+    latency, so that fraction is small.
     Mean +- SE over `seeds` datasets (P:1121-1127 reports means over datasets)."""
     import torch
     from synth import generators as G
-    l2pk, l2src = l2_read_peak()
+    fpk, fsrc = dfma_peak()
     out = []
     for label, cfg, over, rule in PER_CONFIG:
         rows = []
@@ -266,12 +267,13 @@ def per_config_block(S, dev, stream, flush, seeds=3, fits=5):
                 torch.cuda.synchronize()
             ms = float(np.median([a.elapsed_time(b) for a, b in zip(e0, e1)]))
             sweep_ms = float(st.get("ms_tail", 0.0))
-            sweep_bytes = 8.0 * p * (st.get("tail_changes", 0) + st.get("tail_columns", 0))
+            sweep_flops = 2.0 * p * st.get("tail_changes", 0)
             rows.append(dict(ms=ms, ups=st["coord_updates"] / (ms / 1000.0),
                              sweeps=st["total_sweeps"], max_sweeps=st["max_sweeps"],
                              multi=st["tail_columns"], nnz=st["nnz"], sweep_ms=sweep_ms,
-                             l2=(sweep_bytes / (sweep_ms / 1000.0) / 1e9 / l2pk) if sweep_ms > 0 else None,
-                             changes=st.get("tail_changes", 0), cand=st.get("screen_candidates"),
+                             tf=(sweep_flops / (sweep_ms / 1000.0) / 1e12) if sweep_ms > 0 else None,
+                             changes=st.get("tail_changes", 0), passes=st.get("tail_passes", 0),
+                             cand=st.get("screen_candidates"),
                              seed=spec["seed"]))
             del ob, Xd
         def ms_se(key):
@@ -287,10 +289,12 @@ def per_config_block(S, dev, stream, flush, seeds=3, fits=5):
                     "multi_sweep_columns": [r["multi"] for r in rows], "nnz": [r["nnz"] for r in rows],
                     "screen_candidates": [r["cand"] for r in rows],
                     "sweep_kernel": {"kernel": "tail_sweep_kernel", "ms": sw_ms, "ms_se": sw_se,
-                                     "bound": "l2", "changes": [r["changes"] for r in rows],
-                                     "algorithmic": "8 p bytes of Gram column per coordinate change + 8 p per column (its z)",
-                                     "frac_of_l2": [r["l2"] for r in rows], "peak_gbs": l2pk,
-                                     "peak_source": l2src,
+                                     "bound": "latency", "changes": [r["changes"] for r in rows],
+                                     "passes": [r["passes"] for r in rows],
+                                     "algorithmic": "p FP64 FMAs per coordinate change (2 p flops)",
+                                     "achieved_tflops": [r["tf"] for r in rows],
+                                     "frac_of_fp64": [(r["tf"] / fpk) if r["tf"] else None for r in rows],
+                                     "peak_tflops": fpk, "peak_source": fsrc,
                                      "timing": "eager fit (CUDA events around the kernel)"}})
     return out
 

@@ -59,6 +59,7 @@ struct DevCounters {
   unsigned long long t_start, t_end;   // device clock (ns) at the fit's first / last kernel
   unsigned long long tail_changes;     // coordinate changes made by the sweep kernel
   unsigned long long tail_passes;      // its chain + pass segments
+  int tail_ordered, pad6;              // the sweep kernel's work-order grid barrier
 };
 
 struct Buffer {
@@ -94,7 +95,7 @@ struct Workspace {
   int cc_major = 0;
   Buffer xb, gband, mean, scale, counters, queue, sigma_std, iters, sweeps, conv, nz_count, nz_cur,
       nz_rows, nz_vals, col_ptr, csc_rows, csc_vals;
-  Buffer tail, umark, umap, uvars, tailV, zall, ondemand;   // tail solver
+  Buffer tail, tail2, umark, umap, uvars, tailV, zall, ondemand;   // tail solver (tail2: order)
   Buffer ej, act0, act1, keep, jflags;                      // mode 1 (Algorithm 3)
   Buffer jtail, slotmap, jwork, zj;                         // mode 1 on the Gram form
   Buffer hit;                                               // Gram solver screening flags
@@ -613,7 +614,13 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   if (tail_smem_bytes((int)p, L.n_pad, nzcap) > (size_t)W.smem_optin)
     return fail(SPMESL_ERR_UNSUPPORTED, "Gram solver: sweep state does not fit on chip");
   if ((rc = ensure(W.ondemand, (size_t)p * p * 8))) return rc;
-  if ((rc = ensure(W.hit, (size_t)p * nlam))) return rc;
+  // screening flags [nlam][p], then (16-byte aligned) the hit count per column (both zeroed
+  // by the reset kernel)
+  const size_t hit_off = ((size_t)p * nlam + 15) & ~(size_t)15;
+  const size_t hit_bytes = hit_off + (size_t)p * 4 + 1024 * 4;   // + the sweep order's buckets
+  if ((rc = ensure(W.hit, hit_bytes))) return rc;
+  int* hitcnt = (int*)((char*)W.hit.ptr + hit_off);
+  int* bhist = hitcnt + p;
   if ((rc = ensure(W.lam_dev, (size_t)SPMESL_MAX_LAM * 8))) return rc;
   if ((rc = ensure(W.ssq, (size_t)p * 8))) return rc;
   if (screen16) {
@@ -643,7 +650,7 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   }
   // (the reset kernel also clears the screening flags and the candidate flags)
   if ((rc = run_prep(W, dX, m * nlam, o, L, s, /*band=*/false, screen16 ? &yprep : nullptr,
-                     W.hit.ptr, (size_t)p * nlam, screen16 ? W.cand.ptr : nullptr,
+                     W.hit.ptr, hit_bytes, screen16 ? W.cand.ptr : nullptr,
                      screen16 ? (size_t)p : 0)))
     return rc;
   {
@@ -668,6 +675,10 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   G.max_outer = max_iter;
   G.G = (double*)W.ondemand.ptr;
   G.hit = (uint8_t*)W.hit.ptr;
+  G.hitcnt = hitcnt;
+  if ((rc = ensure(W.tail2, (size_t)m * nlam * 8))) return rc;   // tail keys, then the order
+  G.bhist = bhist;
+  G.tail_key = (int*)W.tail2.ptr;
   G.ssq = (const double*)W.ssq.ptr;
   G.tile_begin = 0;
   G.tile_end = gram_tile_count(p);
@@ -779,6 +790,12 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   T.nz_count = (int*)W.nz_count.ptr; T.nz_cur = (int*)W.nz_cur.ptr;
   T.sigma_std = out.sigma_std; T.iters = out.iters; T.sweeps = out.sweeps; T.converged = out.conv;
   if (nlam > 1) { T.lambdas = (const double*)W.lam_dev.ptr; T.slot_stride = (int)p; }
+  // the columns with the most hits first (the sweep kernel orders its list; results do not
+  // depend on the order)
+  T.bhist = bhist;
+  T.tail_key = (const int*)W.tail2.ptr;
+  T.order = (int*)W.tail2.ptr + m * nlam;
+  T.order_bar = &dc->tail_ordered;
   set_tail_shape(W, T);
   CUDA_TRY(launch_tail_sweeps(T, (int)std::min<int64_t>(W.sms, p * nlam), s));
   CUDA_TRY(ev_record(W, W.ev[6], s));
@@ -1521,7 +1538,7 @@ int spmesl_release_workspace(void) {
     if (!w) continue;
     std::lock_guard<std::mutex> lw(w->mu);
     if (w->init) cudaSetDevice(w->device);
-    Buffer* bufs[] = {&w->tail, &w->umark, &w->umap, &w->uvars, &w->tailV, &w->zall, &w->ondemand,
+    Buffer* bufs[] = {&w->tail, &w->tail2, &w->umark, &w->umap, &w->uvars, &w->tailV, &w->zall, &w->ondemand,
                       &w->xb, &w->gband, &w->mean, &w->scale, &w->counters, &w->queue,
                       &w->sigma_std, &w->iters, &w->sweeps, &w->conv, &w->nz_count, &w->nz_cur,
                       &w->nz_rows, &w->nz_vals, &w->col_ptr, &w->csc_rows, &w->csc_vals,

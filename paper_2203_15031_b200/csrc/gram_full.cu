@@ -276,6 +276,10 @@ __global__ void __launch_bounds__(G_THREADS, 1) syrk_screen_kernel(const GramPar
           if (row < p && col < p && row != col && fabs(v) > lam0) {
             P.hit[col] = 1;
             if (!diag_tile) P.hit[row] = 1;
+            if (P.hitcnt) {
+              atomicAdd(&P.hitcnt[col], 1);
+              if (!diag_tile) atomicAdd(&P.hitcnt[row], 1);
+            }
           }
         }
       }
@@ -345,7 +349,14 @@ __global__ void gram_init_kernel(const GramParams P) {
       return;
     }
   }
-  if (lane == 0) P.tail[atomicAdd(P.tail_count, 1)] = ts;
+  if (lane == 0) {
+    const int idx = atomicAdd(P.tail_count, 1);
+    P.tail[idx] = ts;
+    if (P.bhist) {   // (the sweep kernel's work order: hit-count bucket and rank within it)
+      const int b = 1023 - min(P.hitcnt[gc], 1023);
+      P.tail_key[idx] = (b << 20) | atomicAdd(&P.bhist[b], 1);
+    }
+  }
 }
 
 }  // namespace

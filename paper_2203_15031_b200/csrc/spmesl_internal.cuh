@@ -138,6 +138,12 @@ struct TailParams {
   // item (TailState slots work[0 .. *M_dev)), at lambda = sigma_std[col] lambda0, keeps z in
   // Zj[slot] between launches, max-reduces |db| into joint_maxd and writes the state back; the
   // outer boundary (sigma refit, F_c, compaction) and the sweep counts are the host loop's.
+  // optional: the work order by hit count, most first (bhist / tail_key: GramParams'; order:
+  // *M_dev entries; order_bar: a zeroed grid-barrier counter)
+  const int* bhist;
+  const int* tail_key;
+  int* order;
+  int* order_bar;
   int joint;
   TailState* jtail;                  // [slots] state written back after each sweep
   const int* work;                   // slots to sweep in this launch
@@ -155,6 +161,9 @@ struct GramParams {
   int nst;
   double* G;               // [p][p] column-major (nullptr: screening only)
   uint8_t* hit;            // [nlam][p] column has some |G_jc| > lambda0_l, j != c
+  int* hitcnt;             // optional [p]: number of such j at the screening level (zeroed)
+  int* bhist;              // optional [1024]: tail columns per hit-count bucket (zeroed), and
+  int* tail_key;           //   per tail entry: bucket << 20 | rank in it (the sweep order)
   const double* ssq;       // optional [p]: x~_c^T x~_c as the standardization summed it
   int nlam;                // penalty levels screened / fitted together (1..SPMESL_MAX_LAM)
   double lams[8];          // their lambda0 values
@@ -229,6 +238,7 @@ cudaError_t launch_gram_cols(const double* Xb, int nblk, int nchunk, int n, int 
                              int nU, const int* nU_dev, int sms, double* Gtab, uint8_t* hit,
                              const double* lams, int nlam, int* gstate, cudaStream_t s,
                              bool fallback = true, double lam1 = 0.0);   // lams == nullptr: lam1
+
 // hit (optional): hit[l p + c] = 1 for every candidate c = U[.] with some |G_jc| > lams[l], j != c
 // (hit must be zeroed first; only ones are written)
 cudaError_t launch_gram_pass(const double* Xb, int nblk, int nchunk, int n, int p, const double* V,

@@ -411,6 +411,7 @@ struct TailShared {
   double mds[MMAX];      // multi-sweep: sum_l |d_sl| per sweep
   double msig_e;         //   the state after the last sweep of the chain
   int mout_e, minr_e, mflg_e, mret_e;
+  int ordered;           // the work order by hit count is in use
 };
 constexpr size_t TS_BYTES = (sizeof(TailShared) + 127) & ~(size_t)127;
 
@@ -756,6 +757,59 @@ __device__ __forceinline__ void mpass(const double* zs, double* zd, const uint32
                                qstar, mkey, best, bestw);
 }
 
+// Work order by hit count, most first: those columns tend to need the most sweeps, and at
+// config 4 hub the slowest ones would otherwise start late and set the kernel's end.  The
+// exact-decision kernel gave every tail entry its hit-count bucket and a rank in it; here each
+// CTA scans the 1024 bucket sizes, writes the positions of its share of the entries, and all
+// CTAs meet at a grid barrier (all are resident).  The order inside a bucket is arbitrary: it
+// only decides which CTA takes a column when; results do not depend on it.  Returns whether
+// the order is used (not when the counts are too even to matter: the most hits below twice
+// the median + 4, e.g. band(3): 6 vs 3; hub: 70 vs 12).
+template <int NT>
+__device__ bool order_tail(const TailParams& P, int M, int* off) {
+  const int tid = threadIdx.x;
+  for (int b = tid; b < 1024; b += NT) off[b] = P.bhist[b];   // (one round of loads)
+  __syncthreads();
+  if (tid < 32) {   // exclusive scan of the bucket sizes (bucket 0: the most hits), one warp
+    int carry = 0, top = -1, med = -1;
+    for (int b0 = 0; b0 < 1024; b0 += 32) {
+      const int v = off[b0 + tid];
+      int incl = v;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, d);
+        if (tid >= d) incl += t;
+      }
+      off[b0 + tid] = carry + incl - v;
+      const unsigned nz = __ballot_sync(0xffffffffu, v > 0);
+      if (top < 0 && nz) top = b0 + __ffs(nz) - 1;
+      const unsigned hm = __ballot_sync(0xffffffffu, carry + incl >= (M + 1) / 2);
+      if (med < 0 && hm) med = b0 + __ffs(hm) - 1;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (tid == 0) off[1024] = (1023 - top) >= 2 * (1023 - med) + 4;   // hits: top vs median
+#ifdef SPMESL_ORDER_DBG
+    if (tid == 0 && blockIdx.x == 0) printf("order: M %d top hits %d median hits %d use %d\n", M, 1023 - top, 1023 - med, off[1024]);
+#endif
+  }
+  __syncthreads();
+  if (!off[1024]) return false;   // (the same decision in every CTA)
+  const int per = (M + gridDim.x - 1) / gridDim.x;
+  for (int k = blockIdx.x * per + tid; k < min(M, (int)(blockIdx.x + 1) * per); k += NT) {
+    const int key = P.tail_key[k];
+    P.order[off[key >> 20] + (key & 0xFFFFF)] = k;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    atomicAdd(P.order_bar, 1);
+    while (*(volatile const int*)P.order_bar < (int)gridDim.x) __nanosleep(64);
+  }
+  __syncthreads();
+  __threadfence();
+  return true;
+}
+
 template <int NT, bool EVEN, int MINB, bool MULTI>
 __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P) {
   extern __shared__ __align__(128) unsigned char sm[];
@@ -780,6 +834,11 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const size_t list_stride = (size_t)2 * nzcap;
   const int M = P.M_dev ? *(volatile const int*)P.M_dev : P.M;
+  // (fewer columns than CTAs: all start at once; scratch: the tiles region, not in use yet)
+  {
+    const bool ordered = P.bhist && M > (int)gridDim.x && order_tail<NT>(P, M, (int*)(sm + TS_BYTES));
+    if (tid == 0) TS.ordered = ordered ? 1 : 0;   // (read by thread 0 when it takes work)
+  }
   const int nmask = (p + 31) / 32;
   if (tid < TAIL_ODC) TS.oc_var[tid] = -1;
   if (tid == 0) {
@@ -796,7 +855,10 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
     // generic-proxy accesses to it before that, then the barrier publishes them)
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     bsync();
-    if (tid == 0) TS.k = atomicAdd(P.next, 1);
+    if (tid == 0) {
+      const int kq = atomicAdd(P.next, 1);
+      TS.k = (TS.ordered && kq < M) ? P.order[kq] : kq;   // (the hit-count order, if made)
+    }
     bsync();
     const int k = TS.k;
     if (k >= M) break;

@@ -24,6 +24,7 @@ for which in (sys.argv[1:] or ["band3", "hub"]):
     n, p = X.shape
     Xd = torch.from_numpy(np.ascontiguousarray(X.T)).cuda().t()
     lam = S.lambda_univ(n, p) if which == "univ5" else S.lambda_ub(n, p)
+    lib.spmesl_dev_tail_prof(buf, 1)
     S.fit_device(Xd, lam, eager=True)
     torch.cuda.synchronize()
     lib.spmesl_dev_tail_prof(buf, 1)
@@ -39,6 +40,8 @@ for which in (sys.argv[1:] or ["band3", "hub"]):
     m = v[13]
     print(f"  slowest column: {m >> 24} cycles, {(m >> 12) & 4095} passes, {m & 4095} sweeps; columns over 4e6 cycles: {v[14]}")
     print(f"  slowest column: final nnz {(v[28] >> 8) & 255}, failures {v[28] & 255}; mean final nnz of the columns over 4e6 cycles: {v[29] / max(v[14], 1):.1f}")
+    if v[30] and v[30] != 2**64 - 1:
+        print(f"  kernel span {(v[27] - v[30]) / 1e3:.0f} us; latest start of a column over 4e6 cycles: {(v[31] - v[30]) / 1e3:.0f} us after the first")
     if v[16]:
         print(f"  stragglers (>200 sweeps): {v[16]} columns, {v[25]} sweeps, {v[24]} cycles; multi ok {v[17]} "
               f"({v[20]} sweeps), fail {v[18]}, single segments {v[19]}; cycles: spec {v[21]}, chain {v[22]}, "
