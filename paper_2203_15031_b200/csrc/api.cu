@@ -96,6 +96,7 @@ struct Workspace {
   Buffer xb, gband, mean, scale, counters, queue, sigma_std, iters, sweeps, conv, nz_count, nz_cur,
       nz_rows, nz_vals, col_ptr, csc_rows, csc_vals;
   Buffer tail, tail2, umark, umap, uvars, tailV, zall, ondemand;   // tail solver (tail2: order)
+  Buffer z2g;                                                      // its global second z buffers
   Buffer ej, act0, act1, keep, jflags;                      // mode 1 (Algorithm 3)
   Buffer jtail, slotmap, jwork, zj;                         // mode 1 on the Gram form
   Buffer hit;                                               // Gram solver screening flags
@@ -797,7 +798,12 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   T.order = (int*)W.tail2.ptr + m * nlam;
   T.order_bar = &dc->tail_ordered;
   set_tail_shape(W, T);
-  CUDA_TRY(launch_tail_sweeps(T, (int)std::min<int64_t>(W.sms, p * nlam), s));
+  const int tgrid = (int)std::min<int64_t>(W.sms, p * nlam);
+  if (!T.z2) {   // (the multi-sweep mode's second z buffer in global memory, one slice per CTA)
+    if ((rc = ensure(W.z2g, (size_t)tgrid * std::max(T.occ, 1) * p * 8))) return rc;
+    T.z2g = (double*)W.z2g.ptr;
+  }
+  CUDA_TRY(launch_tail_sweeps(T, tgrid, s));
   CUDA_TRY(ev_record(W, W.ev[6], s));
   CUDA_TRY(ev_record(W, W.ev[2], s));
   W.gram_launches = launches + 2;   // + gram_init, tail
@@ -1538,7 +1544,7 @@ int spmesl_release_workspace(void) {
     if (!w) continue;
     std::lock_guard<std::mutex> lw(w->mu);
     if (w->init) cudaSetDevice(w->device);
-    Buffer* bufs[] = {&w->tail, &w->tail2, &w->umark, &w->umap, &w->uvars, &w->tailV, &w->zall, &w->ondemand,
+    Buffer* bufs[] = {&w->tail, &w->tail2, &w->z2g, &w->umark, &w->umap, &w->uvars, &w->tailV, &w->zall, &w->ondemand,
                       &w->xb, &w->gband, &w->mean, &w->scale, &w->counters, &w->queue,
                       &w->sigma_std, &w->iters, &w->sweeps, &w->conv, &w->nz_count, &w->nz_cur,
                       &w->nz_rows, &w->nz_vals, &w->col_ptr, &w->csc_rows, &w->csc_vals,

@@ -125,6 +125,7 @@ struct TailParams {
   int occ;                 // column CTAs per SM the launch provides for (grid multiplier)
   int z2;                  // 1: a second z buffer (tail_z2_bytes more shared memory): a pass
                            //    that finds no new row swaps in z + all chain changes
+  double* z2g;             // (z2 == 0) optional [grid][p] global scratch for the multi-sweep mode
   int* flags;
   int* nz_rows;            // column coefficient lists (as in CDParams)
   double* nz_vals;

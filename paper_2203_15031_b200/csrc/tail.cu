@@ -831,6 +831,10 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
   double* PG = tvv;
   const bool use_z2 = P.z2 != 0;
   double* zB = use_z2 ? (double*)(sm + tail_smem_bytes(p, n_pad, nzcap)) : nullptr;
+  // (no room for z2 on chip: the multi-sweep mode writes its z + changes to this CTA's slice
+  // of a global scratch and copies it back when no new row appeared)
+  double* zG = (!use_z2 && P.z2g) ? P.z2g + (size_t)blockIdx.x * p : nullptr;
+  const bool can_multi = use_z2 || zG != nullptr;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const size_t list_stride = (size_t)2 * nzcap;
   const int M = P.M_dev ? *(volatile const int*)P.M_dev : P.M;
@@ -933,7 +937,7 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
       bool flush = false;            // (joint mode: a last pass that only applies the pending)
       bool multi_done = false;       // whole sweeps done by the multi-sweep mode (with their
       int msw_done = 0;              //   sigma refits: sweeps, outer, inner, flags, retire set)
-      if (MULTI && use_z2 && !P.joint && npend == 0 && ocnt == 0 && sweeps == ts.sweeps &&
+      if (MULTI && can_multi && !P.joint && npend == 0 && ocnt == 0 && sweeps == ts.sweeps &&
           !overflow) {
         // ---------------------------------------------- a column's first sweep (b = 0)
         // The rows with |z| = |G[j, c]| close to lambda join the (empty) old list with b = 0:
@@ -981,7 +985,7 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
           bsync();
         }
       }
-      if (MULTI && use_z2 && !P.joint && npend == 0 && ocnt > 0 && ocnt <= KMS && !overflow) {
+      if (MULTI && can_multi && !P.joint && npend == 0 && ocnt > 0 && ocnt <= KMS && !overflow) {
         // ---------------------------------------------- multi-sweep mode (run_mpass)
         const int K = ocnt;
         const int KS = K <= 16 ? 16 : 32;  // row stride of MD / MBN
@@ -1106,8 +1110,8 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
         TPROF_C(c_chain += tp1 - tp0;)
         int best = 0x7fffffff;
         double bestw = 0.0;
-        mpass<NT, true>(z, z2, oldmask, P.Gtab, TS, MD, KS, MDS, p, K, Msw, gc, TS.mlam, 0, 0,
-                        &TS.mkey, best, bestw);
+        mpass<NT, true>(z, use_z2 ? z2 : zG, oldmask, P.Gtab, TS, MD, KS, MDS, p, K, Msw, gc,
+                        TS.mlam, 0, 0, &TS.mkey, best, bestw);
         {
           const int wb = __reduce_min_sync(0xffffffffu, best);
           if (best == wb && best != 0x7fffffff) TS.wval[warp] = bestw;
@@ -1124,7 +1128,24 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
         TPROF_C(c_spec += tp2 - tp1;)
         if (jkey == 0x7fffffff) {
           // every speculated sweep holds: z2 is z after them; the list is the last sweep's
-          { double* t = z; z = z2; z2 = t; }
+          if (use_z2) { double* t = z; z = z2; z2 = t; }
+          else {
+            // (16 loads in flight per thread; the pass's global writes are this CTA's own,
+            // ordered by the barrier above)
+            for (int j0 = 0; j0 < p; j0 += 16 * NT) {
+              double gv[16];
+#pragma unroll
+              for (int u = 0; u < 16; ++u) {
+                const int j = j0 + u * NT + tid;
+                gv[u] = j < p ? __ldcg(zG + j) : 0.0;
+              }
+#pragma unroll
+              for (int u = 0; u < 16; ++u) {
+                const int j = j0 + u * NT + tid;
+                if (j < p) z[j] = gv[u];
+              }
+            }
+          }
           if (warp == 0) {
             const int sl = Msw - 1;
             double bn = 0.0, dl = 0.0;
@@ -1595,7 +1616,7 @@ cudaError_t launch_tail_sweeps(const TailParams& P, int grid, cudaStream_t s) {
   // 512 threads when a single column CTA owns the SM (large p: the pass splits over twice the
   // threads), 256 when two share it; the multi-sweep mode needs the second z buffer (and is
   // compiled only into those variants: its registers would cost the others)
-  const bool multi = P.z2 && !P.joint;
+  const bool multi = (P.z2 || P.z2g) && !P.joint;
   if (P.occ == 1)
     return multi ? launch_tail_e<512, 1, true>(P, grid, smem, s) : launch_tail_e<512, 1, false>(P, grid, smem, s);
   return multi ? launch_tail_e<256, 2, true>(P, grid, smem, s) : launch_tail_e<256, 2, false>(P, grid, smem, s);

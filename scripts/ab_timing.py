@@ -13,18 +13,23 @@ from paper_2203_15031_b200 import _lib
 from synth import generators as G
 
 vp, i64, i32, dbl = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double
+args = [a for a in sys.argv[1:] if not a.startswith("--cases=")]
+cases = next((a[8:].split(",") for a in sys.argv[1:] if a.startswith("--cases=")), ["band3", "hub"])
 libs = []
-for path in sys.argv[1:]:
+for path in args:
     L = ctypes.CDLL(path)
     L.spmesl_fit_device.argtypes = [vp, i64, i64, dbl, dbl, i32, ctypes.POINTER(_lib.Options), vp, vp,
                                     vp, vp, vp, vp, vp]
     L.spmesl_default_options.argtypes = [ctypes.POINTER(_lib.Options)]
     libs.append(L)
 rounds = 5
-for fam in ("band3", "hub"):
-    X, _, spec = G.make_config(4, family=fam)
+for fam in cases:
+    if fam in ("univ5", "ub5"):
+        X, _, spec = G.make_config(5)
+    else:
+        X, _, spec = G.make_config(4, family=fam)
     n, p = X.shape
-    lam = S.lambda_ub(n, p)
+    lam = S.lambda_univ(n, p) if fam == "univ5" else S.lambda_ub(n, p)
     Xd = torch.from_numpy(np.ascontiguousarray(X.T)).cuda()   # (p x n row-major = n x p column-major)
     bufs = [torch.empty((p, p), dtype=torch.float64, device="cuda"), torch.empty(p, dtype=torch.float64, device="cuda")] + \
            [torch.empty(p, dtype=torch.int32, device="cuda") for _ in range(2)] + [torch.empty(p, dtype=torch.uint8, device="cuda")]
@@ -42,6 +47,6 @@ for fam in ("band3", "hub"):
             if r > 0:
                 times[li].append(st.ms_tail)
             sweeps[li] = int(bufs[3].sum().item())
-    for li, path in enumerate(sys.argv[1:]):
+    for li, path in enumerate(args):
         t = np.array(times[li])
         print(f"{fam:6s} {path:40s} sweep kernel median {np.median(t):.3f} ms (min {t.min():.3f}, max {t.max():.3f}); sweeps {sweeps[li]}")
