@@ -24,12 +24,14 @@ for path in args:
     libs.append(L)
 rounds = 5
 for fam in cases:
-    if fam in ("univ5", "ub5"):
-        X, _, spec = G.make_config(5)
+    fam_, _, seed = fam.partition("@")    # (e.g. hub@3207: another dataset seed)
+    kw = {"seed": int(seed)} if seed else {}
+    if fam_ in ("univ5", "ub5"):
+        X, _, spec = G.make_config(5, **kw)
     else:
-        X, _, spec = G.make_config(4, family=fam)
+        X, _, spec = G.make_config(4, family=fam_, **kw)
     n, p = X.shape
-    lam = S.lambda_univ(n, p) if fam == "univ5" else S.lambda_ub(n, p)
+    lam = S.lambda_univ(n, p) if fam_ == "univ5" else S.lambda_ub(n, p)
     Xd = torch.from_numpy(np.ascontiguousarray(X.T)).cuda()   # (p x n row-major = n x p column-major)
     bufs = [torch.empty((p, p), dtype=torch.float64, device="cuda"), torch.empty(p, dtype=torch.float64, device="cuda")] + \
            [torch.empty(p, dtype=torch.int32, device="cuda") for _ in range(2)] + [torch.empty(p, dtype=torch.uint8, device="cuda")]
