@@ -788,9 +788,6 @@ __device__ bool order_tail(const TailParams& P, int M, int* off) {
       carry += __shfl_sync(0xffffffffu, incl, 31);
     }
     if (tid == 0) off[1024] = (1023 - top) >= 2 * (1023 - med) + 4;   // hits: top vs median
-#ifdef SPMESL_ORDER_DBG
-    if (tid == 0 && blockIdx.x == 0) printf("order: M %d top hits %d median hits %d use %d\n", M, 1023 - top, 1023 - med, off[1024]);
-#endif
   }
   __syncthreads();
   if (!off[1024]) return false;   // (the same decision in every CTA)
@@ -1285,9 +1282,6 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
           TS.so[l] = o;
           if (TS.sg_rows[l] != o) mine = 0;
         }
-#ifdef SPMESL_TAIL_NO_SGCACHE
-        mine = 0;
-#endif
         if (!__syncthreads_and(mine && TS.sg_n == K)) {
           for (int e = tid; e < K * K; e += NT) {
             const int kk = e / K, m = e - kk * K;
