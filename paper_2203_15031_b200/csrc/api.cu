@@ -830,6 +830,7 @@ void gram_stats(Workspace& W, int64_t p, int nzcap, spmesl_stats* st, bool scree
   st->ms_tail = replay ? -1.0 : ev_ms(W.ev[5], W.ev[6]);
   st->tail_columns = W.host_counters->tail_count;
   st->tail_sweeps = W.host_counters->tail_sweeps;
+  st->tail_gram_ondemand = W.host_counters->gram_ondemand;
   st->tail_changes = (int64_t)W.host_counters->tail_changes;
   st->tail_passes = (int64_t)W.host_counters->tail_passes;
 }

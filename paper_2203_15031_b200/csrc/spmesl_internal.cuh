@@ -187,7 +187,16 @@ size_t syrk_smem_bytes(int nst);
 // Certified screening: the exact FP64 decision of its nU candidate columns costs 2 n p nU flops
 // in gram_cols_kernel (~0.44 of the DMMA peak) against n p (p + 1) in the symmetric Gram kernel
 // (~0.9 of it): above p / 4 candidates the full Gram kernel decides instead (measured crossover)
-__host__ __device__ inline bool gram_fallback_taken(int64_t nU, int64_t p) { return 4 * nU > p; }
+// Exact first-sweep decision of the certified screening's nU candidates (device count): the
+// exact Gram columns of the candidates (2 n p nU flops, gram_cols_kernel) for up to p/4 and up
+// to 1024 of them, else the full symmetric Gram kernel (n p (p+1) flops).  Only the
+// candidates' columns are computed on the first path; a sweep that needs another one computes
+// it on first use inside its CTA (about 1 ms each at p = 20000), which more candidates make
+// likelier: at config 5 with 1126 candidates (lambda between univ and ub) one such column made
+// the fit 12.5 ms against 8.3 with the full kernel.
+__host__ __device__ inline bool gram_fallback_taken(int64_t nU, int64_t p) {
+  return 4 * nU > p || nU > 1024;
+}
 
 // Certified f16 screening (screen16.cu)
 struct Screen16Params {

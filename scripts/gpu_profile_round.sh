@@ -1,6 +1,6 @@
 #!/bin/bash
-# Round profile capture (run under gpurun): bench line, launch list, ncu of the dominant kernel
-# (config 5) and of the sweep kernel (config 4 band(3) and hub).  Summaries go to profiles/.
+# Round profile capture (run under gpurun): bench line, reference arm, launch list, ncu of the
+# dominant kernel (config 5) and of the sweep kernel (config 4 band(3) and hub).
 mkdir -p gpurun_out
 timeout 900 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err; echo "bench rc=$?"
 timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"

@@ -420,9 +420,10 @@ def test_certified_screening_equals_full_gram(S):
         b = S.fit_device(Xd, lam, solver="gram16")
         assert b.stats["solver"] == 3 and b.stats["screen_candidates"] >= b.stats["tail_columns"] - 0
         assert torch.equal(a.Theta, b.Theta) and torch.equal(a.sweeps, b.sweeps)
-        # the fallback to the full FP64 Gram kernel is taken on the device iff most columns
-        # are candidates; the screening kernel zero-fills all of Theta (default split)
-        assert b.stats["gram_fallback"] == int(4 * b.stats["screen_candidates"] > p)
+        # the fallback to the full FP64 Gram kernel is taken on the device above p/4 or 1024
+        # candidates; the screening kernel zero-fills all of Theta (default split)
+        nc = b.stats["screen_candidates"]
+        assert b.stats["gram_fallback"] == int(4 * nc > p or nc > 1024)
         assert b.stats["screen_fill_bytes"] == 8 * p * p and b.stats["ms_screen"] > 0
         lams = [S.lambda_pb(n, p), S.lambda_univ(n, p), lam]
         pa = S.fit_path_device(Xd, lams, solver="gram")
