@@ -16,7 +16,14 @@
 //
 // One sweep is processed as a speculative chain over the column's current nonzeros plus one
 // block-wide pass over the rows per segment (see "per-column sweeps" below), so the dependent
-// latency per sweep is a few passes, not one block-wide update and search per change.
+// latency per sweep is a few passes, not one block-wide update and search per change.  When the
+// whole support fits one chain, the multi-sweep mode (run_mpass) lets the chain run up to 32
+// sweeps ahead — refitting sigma where inner loops end — and one pass applies them all; the
+// columns are taken most-hits-first.  Every mode keeps the row-at-a-time loop's FMAs in its
+// order: the iterates are bit-identical whatever mode, order or launch shape processed them.
+//
+// Development build only: -DSPMESL_TAIL_PROF adds per-phase cycle counters (scripts/
+// tail_prof_build.sh); the shipped library has no run-time switches.
 #include <cstdio>
 #include <algorithm>
 #include <cstdlib>
