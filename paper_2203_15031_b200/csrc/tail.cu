@@ -759,6 +759,9 @@ __device__ __forceinline__ void mpass(const double* zs, double* zd, const uint32
   else if (K <= 16)
     run_mpass<NT, 16, 2, SPEC>(zs, zd, oldmask, Gtab, TS, MD, KS, MDS, p, K, Msw, gc, mlam, sstar,
                                qstar, mkey, best, bestw);
+  else if (K <= 24)
+    run_mpass<NT, 24, 1, SPEC>(zs, zd, oldmask, Gtab, TS, MD, KS, MDS, p, K, Msw, gc, mlam, sstar,
+                               qstar, mkey, best, bestw);
   else
     run_mpass<NT, 32, 1, SPEC>(zs, zd, oldmask, Gtab, TS, MD, KS, MDS, p, K, Msw, gc, mlam, sstar,
                                qstar, mkey, best, bestw);
@@ -992,8 +995,8 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
       if (MULTI && can_multi && !P.joint && npend == 0 && ocnt > 0 && ocnt <= KMS && !overflow) {
         // ---------------------------------------------- multi-sweep mode (run_mpass)
         const int K = ocnt;
-        const int KS = K <= 16 ? 16 : 32;  // row stride of MD / MBN
-        const int mcap = MDCAP / KS;       // sweeps they hold (32 or 16)
+        const int KS = K <= 16 ? 16 : K <= 24 ? 24 : 32;  // row stride of MD / MBN (>= the
+        const int mcap = min(MMAX, MDCAP / KS);             //   pass's KR); sweeps they hold
         double* MD = tvv;                  // [mcap][KS] changes d (aliases PG: no pending;
                                            //   zero beyond K)
         double* MBN = tvv + MDCAP;         // [mcap][KS] new values b'

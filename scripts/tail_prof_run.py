@@ -17,13 +17,15 @@ buf = (ctypes.c_ulonglong * 32)()
 names = ["multi_chain", "spec_pass", "commit", "single_seg", "refit", "ok", "fail", "ok_sweeps",
          "fail_sstar", "single_cnt", "column_total", "multi_K", "fail_Msw"]
 for which in (sys.argv[1:] or ["band3", "hub"]):
-    if which == "univ5":
-        X, _, spec = G.make_config(5)
+    fam, _, seed = which.partition("@")     # (e.g. hub@3207: another dataset seed)
+    kw = {"seed": int(seed)} if seed else {}
+    if fam == "univ5":
+        X, _, spec = G.make_config(5, **kw)
     else:
-        X, _, spec = G.make_config(4, family=which)
+        X, _, spec = G.make_config(4, family=fam, **kw)
     n, p = X.shape
     Xd = torch.from_numpy(np.ascontiguousarray(X.T)).cuda().t()
-    lam = S.lambda_univ(n, p) if which == "univ5" else S.lambda_ub(n, p)
+    lam = S.lambda_univ(n, p) if fam == "univ5" else S.lambda_ub(n, p)
     lib.spmesl_dev_tail_prof(buf, 1)
     S.fit_device(Xd, lam, eager=True)
     torch.cuda.synchronize()
