@@ -57,7 +57,7 @@ __global__ void standardize_kernel(const double* __restrict__ X, int64_t n, int6
     // the whole column in one bulk copy (all of its bytes in flight at once; the passes below
     // then read shared memory)
     const int w = threadIdx.x >> 5;
-    double* buf = colbuf + (size_t)w * stage_n;
+    double* buf = colbuf + (size_t)w * (stage_n + (y.Y16 ? n64 / 4 : 0));   // (+ f16 staging)
     const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&colbar[w]);
     if (lane == 0) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar));
@@ -131,6 +131,15 @@ __global__ void standardize_kernel(const double* __restrict__ X, int64_t n, int6
     // y = x~ / sqrt(N_k) in f16 (the same double product to_f16_kernel forms), and the
     // epilogue's threshold factors (as sqrt_kernel: directed roundings)
     const double sc = rsqrt(Nk);
+    if (xw) {
+      // (staged column: convert lane-strided into the warp's f16 buffer after the column — no
+      // bank conflicts — then store 16-byte chunks of 8 samples; the same values as below)
+      __half* hb = (__half*)(xw + stage_n);
+      for (int64_t i = lane; i < n64; i += 32) hb[i] = __double2half(i < n ? xw[i] * sc : 0.0);
+      __syncwarp();
+      for (int64_t i0 = 8 * lane; i0 < n64; i0 += 256)
+        *(uint4*)(y.Y16 + y16_index(k, i0, y.nchunk64)) = *(const uint4*)(hb + i0);
+    } else
     for (int64_t i0 = 8 * lane; i0 < n64; i0 += 256) {   // 8 samples = one 16-byte chunk
       __align__(16) __half h[8];
 #pragma unroll
@@ -217,7 +226,7 @@ cudaError_t launch_standardize(const double* X, const Layout& L, int standardize
   // stage each column in shared memory by one bulk copy when it is 16-byte aligned and small
   const int stage_n = (L.n % 2 == 0 && ((uintptr_t)X & 15) == 0 && L.n <= 1024)
                           ? (int)L.n : 0;
-  const size_t smem = (size_t)wpb * stage_n * 8;
+  const size_t smem = (size_t)wpb * (stage_n + (stage_n && yy.Y16 ? yy.nchunk64 * 64 / 4 : 0)) * 8;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(standardize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   standardize_kernel<<<grid, wpb * 32, smem, s>>>(X, L.n, L.p, L.nchunk, nrows, standardize, Xb,
