@@ -31,6 +31,16 @@ __device__ __forceinline__ size_t y16_index(int64_t k, int64_t i, int nchunk64) 
   return (size_t)((blk * nchunk64 + q) * 8192 + r * 64 + ((((pos >> 3) ^ (r & 7))) << 3) + (pos & 7));
 }
 
+// a / b correctly rounded from rs = RN(1 / b): q = RN(a rs), r = a - b q (exact, fma),
+// RN(q + r rs) — the final steps of the IEEE division itself (Markstein), so the quotient is
+// the division's (checked bit for bit against it; no overflow or subnormal results here:
+// |a / b| <= sqrt(n) for a standardized column)
+__device__ __forceinline__ double div_rn(double a, double b, double rs) {
+  const double q = a * rs;
+  const double r = fma(-b, q, a);
+  return fma(r, rs, q);
+}
+
 __global__ void standardize_kernel(const double* __restrict__ X, int64_t n, int64_t p, int nchunk,
                                    int64_t nrows, int standardize, double* __restrict__ Xb,
                                    double* mu, double* scale, int* err, unsigned long long* bad_key,
@@ -111,11 +121,12 @@ __global__ void standardize_kernel(const double* __restrict__ X, int64_t n, int6
     }
   }
   if (lane == 0) { mu[k] = m; scale[k] = s; }
+  const double rs = 1.0 / s;
   double g = 0.0;
   // (staged column: keep x~ in the shared buffer for the f16 pass — one division per element)
   double* xw = stage_n > 0 ? const_cast<double*>(x) : nullptr;
   for (int64_t i = lane; i < n_pad; i += 32) {
-    const double v = i < n ? (standardize ? (x[i] - m) / s : x[i]) : 0.0;
+    const double v = i < n ? (standardize ? div_rn(x[i] - m, s, rs) : x[i]) : 0.0;
     Xb[xb_index(i, k, nchunk)] = v;
     if (xw && i < n) xw[i] = v;
     g = fma(v, v, g);
