@@ -193,17 +193,20 @@ __global__ void __launch_bounds__(256) gram_pass_kernel(const double* __restrict
 }
 
 // Exact Gram columns G[:, U[v]] = X~^T x~_U[v] / n of a candidate list (no residual vectors):
-// 64 rows x up to 128 columns per CTA, a 3-stage cp.async ring of 32-sample chunks (the two
+// 8 rows per warp x up to 96 columns per vector group, a 3-stage cp.async ring of 32-sample chunks (the two
 // 8 KB row blocks of Xb + the candidates' rows, re-swizzled by destination row parity), and
 // per output the same DMMA chain as gram_tile (chunks ascending, k-pairs 0..3, even then odd
 // sample), so every caller sees bit-identical columns.  Optional exact screening decision as
 // in gram_tile.
-constexpr int GC_NTMAX = 16;            // n-tiles of 8 vectors per vector group (128 columns)
+// n-tiles of 8 vectors per vector group (96 columns; measured at config 5, 65 candidates:
+// 16 -> 85 us, 12 -> 73 us, 9 -> 72 us — fewer accumulators and a smaller ring stage), and
+// the ring's stages
+constexpr int GC_NTMAX = 12;
 constexpr int GC_STAGES = 3;
 #ifndef SPMESL_GC_GROUP
 #define SPMESL_GC_GROUP 3
 #endif
-constexpr int GC_GROUP = SPMESL_GC_GROUP;   // n-tiles per group of independent DMMAs            // 3 x (34 + 32) KB at 17 warps
+constexpr int GC_GROUP = SPMESL_GC_GROUP;   // n-tiles per group of independent DMMAs
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
