@@ -125,9 +125,11 @@ __global__ void standardize_kernel(const double* __restrict__ X, int64_t n, int6
   double g = 0.0;
   // (staged column: keep x~ in the shared buffer for the f16 pass — one division per element)
   double* xw = stage_n > 0 ? const_cast<double*>(x) : nullptr;
-  for (int64_t i = lane; i < n_pad; i += 32) {
+  // (row jl of column block k / J: element i = 32 q + lane sits at base + q J XS + xswz(jl, lane))
+  double* xbk = Xb + xb_index(0, k, nchunk) - xswz((int)(k % J), 0) + xswz((int)(k % J), lane);
+  for (int64_t i = lane; i < n_pad; i += 32, xbk += J * XS) {
     const double v = i < n ? (standardize ? div_rn(x[i] - m, s, rs) : x[i]) : 0.0;
-    Xb[xb_index(i, k, nchunk)] = v;
+    *xbk = v;
     if (xw && i < n) xw[i] = v;
     g = fma(v, v, g);
   }
