@@ -96,14 +96,24 @@ typedef struct {
                              fits on one device (`device`); G >= 1 fits on G devices of this
                              node with NCCL: each device fits a contiguous block
                              of columns (X replicated), the devices exchange the p first-sweep
-                             screening flags (one max all-reduce) and, after the fit, the
-                             coefficients as CSC (one all-gather); device 0 symmetrizes and
-                             assembles.  Mode 0 only (else SPMESL_ERR_UNSUPPORTED); results
-                             are those of the single-device fit bit for bit; NCCL is loaded at
-                             run time (SPMESL_ERR_NCCL if it cannot be). */
-  int32_t reserved0;
-  const int32_t* device_ids;  /* host array of num_devices distinct CUDA ordinals, or NULL for
-                                 0 .. num_devices - 1 */
+                             screening flags and, after the fit, the coefficients (see
+                             `exchange`).  Mode 0 only (else SPMESL_ERR_UNSUPPORTED); results
+                             are those of the single-device fit bit for bit. */
+  int32_t exchange;       /* num_devices >= 1: how the devices exchange.
+                             0 (default): peer-to-peer when every pair of the devices has peer
+                             access (NVLink / NVSwitch), else NCCL.  1: NCCL — one max
+                             all-reduce of the p flags, one all-gather of the coefficients as
+                             CSC; device 0 symmetrizes and assembles (NCCL is loaded at run
+                             time: SPMESL_ERR_NCCL if it cannot be).  2: peer-to-peer — each
+                             device reads the other devices' screening flags and, for the
+                             symmetrization of its own columns (Eq. symm), each
+                             partner b_kj straight from the memory of the device that fitted
+                             column j; every device assembles its own columns (no collective,
+                             no NCCL; SPMESL_ERR_UNSUPPORTED without peer access or for more
+                             than 16 devices).  With exchange 2 (or 0 resolving to it) device
+                             ids may repeat: blocks that share a device. */
+  const int32_t* device_ids;  /* host array of num_devices CUDA ordinals (distinct unless the
+                                 exchange is peer-to-peer), or NULL for 0 .. num_devices - 1 */
   int32_t reserved[2];
 } spmesl_options;
 
@@ -148,10 +158,11 @@ typedef struct {
   int64_t tail_passes;    /* segments (speculative chain + one pass over the rows) the sweep
                              kernel ran: one per sweep plus one per row that entered the support
                              within a sweep */
-  double  ms_comm;        /* options.num_devices >= 1: device time of the collectives (flag
-                             all-reduce + CSC all-gather) on device 0 */
+  double  ms_comm;        /* options.num_devices >= 1: device time of the exchange on device 0
+                             (NCCL: flag all-reduce + CSC all-gather; peer-to-peer: the flag
+                             max over the peers + the symmetrizing assembly that reads them) */
   int32_t num_devices;    /* devices the fit ran on (0: the single-device path) */
-  int32_t pad2;
+  int32_t exchange;       /* multi-device fits: 1 NCCL collectives, 2 peer-to-peer (0: one device) */
 } spmesl_stats;
 
 /* Fill *opt with the defaults listed above. */

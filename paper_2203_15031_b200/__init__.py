@@ -49,6 +49,7 @@ def _vp(a) -> ctypes.c_void_p:
 
 MODES = {"per_column": 0, "joint": 1}
 SOLVERS = {"auto": 0, "residual": 1, "gram": 2, "gram16": 3}
+EXCHANGES = {"auto": 0, "nccl": 1, "p2p": 2}
 
 
 _OPTS_CACHE = {}
@@ -65,17 +66,19 @@ def _opts(**kw) -> _lib.Options:
 
 def _make_opts(max_inner=10000, standardize=True, symmetrize=True, sigma_floor=1e-8, tile_cols=0,
                device=-1, tail_after=1, mode="per_column", solver="auto",
-               eager=False, num_devices=0, device_ids=None) -> _lib.Options:
+               eager=False, num_devices=0, device_ids=None, exchange="auto") -> _lib.Options:
     """mode: "per_column" (Algorithm 1 stop per column) or "joint" (Algorithm 3).
     solver: "auto", "residual" (CD on X~) or "gram" (covariance updates on X~^T X~ / n).
-    num_devices / device_ids (host entry points): fit on several devices with NCCL."""
+    num_devices / device_ids (host entry points): fit on several devices; exchange: "auto",
+    "nccl" (collectives) or "p2p" (peer reads; device ids may repeat) — DESIGN.md §8."""
     o = default_options(max_inner=int(max_inner), standardize=int(bool(standardize)),
                         symmetrize=int(bool(symmetrize)), sigma_floor=float(sigma_floor),
                         tile_cols=int(tile_cols), device=int(device),
                         tail_after=int(tail_after),
                         mode=MODES[mode] if isinstance(mode, str) else int(mode),
                         solver=SOLVERS[solver] if isinstance(solver, str) else int(solver),
-                        eager=int(bool(eager)), num_devices=int(num_devices))
+                        eager=int(bool(eager)), num_devices=int(num_devices),
+                        exchange=EXCHANGES[exchange] if isinstance(exchange, str) else int(exchange))
     if device_ids is not None:
         ids = (ctypes.c_int32 * len(device_ids))(*[int(d) for d in device_ids])
         o._ids = ids   # (kept alive with the options)

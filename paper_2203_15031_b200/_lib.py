@@ -35,7 +35,7 @@ class Options(ctypes.Structure):
         ("solver", ctypes.c_int32),
         ("eager", ctypes.c_int32),
         ("num_devices", ctypes.c_int32),
-        ("reserved0", ctypes.c_int32),
+        ("exchange", ctypes.c_int32),
         ("device_ids", ctypes.POINTER(ctypes.c_int32)),
         ("reserved", ctypes.c_int32 * 2),
     ]
@@ -73,7 +73,7 @@ class Stats(ctypes.Structure):
         ("tail_passes", ctypes.c_int64),
         ("ms_comm", ctypes.c_double),
         ("num_devices", ctypes.c_int32),
-        ("pad2", ctypes.c_int32),
+        ("exchange", ctypes.c_int32),
     ]
 
     def asdict(self):

@@ -189,6 +189,7 @@ int validate(const void* X, int64_t n, int64_t p, double lambda0, double tol, in
   if (o.mode != 0 && o.mode != 1) return fail(SPMESL_ERR_ARG, "mode must be 0 (per-column stop) or 1 (Algorithm 3 joint stop)");
   if (o.solver < 0 || o.solver > 3) return fail(SPMESL_ERR_ARG, "solver must be 0, 1, 2 or 3");
   if (o.num_devices < 0 || o.num_devices > 64) return fail(SPMESL_ERR_ARG, "num_devices must be 0 .. 64");
+  if (o.exchange < 0 || o.exchange > 2) return fail(SPMESL_ERR_ARG, "exchange must be 0 (auto), 1 (NCCL) or 2 (peer-to-peer)");
   if (o.tile_cols != 0 && o.tile_cols != 8 && o.tile_cols != 16 && o.tile_cols != 32)
     return fail(SPMESL_ERR_ARG, "tile_cols must be 0, 8, 16 or 32");
   const double pp = (double)p * (double)p * 8.0;

@@ -441,6 +441,125 @@ cudaError_t launch_sparse_write(int64_t p, const int* cnt, const int* cur, const
   return cudaGetLastError();
 }
 
+// ---- Peer-to-peer exchange of the multi-device fit (§8(f) f3) ----------------
+// Every device fits a contiguous column block (blocks in device order, sizes p/G rounded as
+// column_range does).  Instead of all-gathering the coefficients, each device reads what it
+// needs straight from its peers' memory over NVLink (peer access enabled by the host):
+//   p2p_flag_max — the global first-sweep screening flags, max over every device's share;
+//   assemble_coo_p2p — a8 + a10 of the device's own columns: for each nonzero b_jk of its
+//     block the partner b_kj is looked up by binary search in column j's list *on the device
+//     that owns column j*, and sigma_j is read there too.  Same arithmetic as
+//     assemble_coo_kernel (theta1, the P:391-393 tie rule), so the entries are bit-identical;
+//     the symmetrization is spread over the G devices ("easily parallelizable")
+//     instead of running on one after an all-gather.
+
+// owner block of column j and its first column (column_range in multi.cu: the first p % G
+// blocks have one column more)
+__device__ __forceinline__ int p2p_owner(const P2PBlocks& B, int64_t j, int64_t* c0) {
+  const int64_t base = B.p / B.G, rem = B.p % B.G;
+  const int64_t big = rem * (base + 1);
+  const int o = (j < big) ? (int)(j / (base + 1)) : (int)(rem + (j - big) / base);
+  *c0 = (int64_t)o * base + min((int64_t)o, rem);
+  return o;
+}
+
+__global__ void p2p_flag_max_kernel(P2PBlocks B, uint8_t* __restrict__ out) {
+  const int64_t nw = B.p >> 2;   // whole 32-bit words (cudaMalloc'd buffers: aligned)
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nw;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    unsigned v = 0;
+    for (int e = 0; e < B.G; ++e) v = __vmaxu4(v, ((const unsigned*)B.flags[e])[w]);
+    ((unsigned*)out)[w] = v;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (B.p & 3)) {
+    const int64_t i = (nw << 2) + threadIdx.x;
+    uint8_t v = 0;
+    for (int e = 0; e < B.G; ++e) v = max(v, B.flags[e][i]);
+    out[i] = v;
+  }
+}
+
+__global__ void assemble_coo_p2p_kernel(P2PBlocks B, int self, const double* __restrict__ scale,
+                                        int symmetrize, int rescale,
+                                        int32_t* __restrict__ coo_row, int32_t* __restrict__ coo_col,
+                                        double* __restrict__ coo_val, int* __restrict__ coo_count) {
+  const int64_t* __restrict__ cp = B.col_ptr[self];
+  const int32_t* __restrict__ rows = B.rows[self];
+  const double* __restrict__ vals = B.vals[self];
+  const int64_t base = B.p / B.G, rem = B.p % B.G;
+  const int64_t c0s = (int64_t)self * base + min((int64_t)self, rem);
+  const int64_t m = base + (self < rem ? 1 : 0);
+  const int64_t e1 = cp[m];
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < e1;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = m;   // local column of entry e
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (cp[mid] <= e) lo = mid;
+      else hi = mid;
+    }
+    const int64_t k = c0s + lo;
+    const int32_t j = rows[e];
+    const double sj = rescale ? scale[j] : 1.0, sk = rescale ? scale[k] : 1.0;
+    const double t_jk = theta1(vals[e], B.sigma_std[self][lo], sj, sk, rescale != 0);
+    double out = t_jk;
+    if (symmetrize) {
+      int64_t c0j;
+      const int oj = p2p_owner(B, j, &c0j);
+      const int64_t* __restrict__ cpj = B.col_ptr[oj];
+      const int64_t jl = j - c0j;
+      const double b_kj = csc_lookup(B.rows[oj], B.vals[oj], cpj[jl], cpj[jl + 1], (int32_t)k);
+      if (b_kj == 0.0) continue;
+      const double t_kj = theta1(b_kj, B.sigma_std[oj][jl], sk, sj, rescale != 0);
+      const double u = (j < k) ? t_jk : t_kj;
+      const double l = (j < k) ? t_kj : t_jk;
+      out = (fabs(u) > fabs(l)) ? l : u;
+    }
+    const int slot = atomicAdd(coo_count, 1);
+    coo_row[slot] = j;
+    coo_col[slot] = (int32_t)k;
+    coo_val[slot] = out;
+  }
+}
+
+// diagonal and sigma of the device's own columns (as assemble_diag_kernel)
+__global__ void assemble_diag_block_kernel(int64_t c0, int64_t m, const double* __restrict__ sig,
+                                           const double* __restrict__ scale, int rescale,
+                                           double* __restrict__ diag, double* __restrict__ sigma_out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const int64_t k = c0 + i;
+  const double sg = sig[i];
+  double w = 1.0 / (sg * sg);
+  if (rescale) w = w / (scale[k] * scale[k]);
+  diag[i] = w;
+  sigma_out[i] = rescale ? scale[k] * sg : sg;
+}
+
+cudaError_t launch_p2p_flag_max(const P2PBlocks& B, uint8_t* out, cudaStream_t s) {
+  const int64_t nw = std::max<int64_t>(B.p >> 2, 1);
+  const unsigned grid = (unsigned)std::min<int64_t>((nw + 255) / 256, 148 * 4);
+  p2p_flag_max_kernel<<<grid, 256, 0, s>>>(B, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_assemble_coo_p2p(const P2PBlocks& B, int self, const double* scale,
+                                    int symmetrize, int32_t* coo_row, int32_t* coo_col,
+                                    double* coo_val, int* coo_count, double* diag,
+                                    double* sigma_out, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(coo_count, 0, sizeof(int), s);
+  if (e != cudaSuccess) return e;
+  const int rescale = scale != nullptr;
+  assemble_coo_p2p_kernel<<<148 * 4, 256, 0, s>>>(B, self, scale, symmetrize, rescale, coo_row,
+                                                  coo_col, coo_val, coo_count);
+  const int64_t base = B.p / B.G, rem = B.p % B.G;
+  const int64_t c0 = (int64_t)self * base + std::min<int64_t>(self, rem);
+  const int64_t m = base + (self < rem ? 1 : 0);
+  assemble_diag_block_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(
+      c0, m, B.sigma_std[self], scale, rescale, diag, sigma_out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_csc_scan(const int* cnt, int ncols, int64_t* col_ptr, int64_t* total,
                             cudaStream_t s) {
   const bool staged = (size_t)ncols * 4 <= 160 * 1024;

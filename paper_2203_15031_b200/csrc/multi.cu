@@ -146,17 +146,34 @@ int fit_multi_device(const double* X, int64_t n, int64_t p, double lambda0, doub
   if (cudaGetDeviceCount(&ndev) != cudaSuccess) { cudaGetLastError(); ndev = 0; }
   std::vector<int> devs(G);
   for (int d = 0; d < G; ++d) devs[d] = o.device_ids ? o.device_ids[d] : d;
+  bool dup = false;
   for (int d = 0; d < G; ++d) {
     if (devs[d] < 0 || devs[d] >= ndev)
       return multi_fail(SPMESL_ERR_ARG, "device id " + std::to_string(devs[d]) + " is not a device");
-    for (int e = 0; e < d; ++e)
-      if (devs[e] == devs[d]) return multi_fail(SPMESL_ERR_ARG, "device ids must be distinct");
+    for (int e = 0; e < d; ++e) dup = dup || devs[e] == devs[d];
   }
   if (G > p) return multi_fail(SPMESL_ERR_ARG, "more devices than columns");
   if (o.mode != 0)
     return multi_fail(SPMESL_ERR_UNSUPPORTED, "mode 1 (joint stop over all columns) runs on one device");
+  if (o.exchange < 0 || o.exchange > 2) return multi_fail(SPMESL_ERR_ARG, "bad options.exchange");
+  // exchange: peer-to-peer when every pair of distinct devices has peer access (NVLink /
+  // NVSwitch), else NCCL collectives (options.exchange forces one)
+  bool peer_ok = G <= kP2PMax;
+  for (int d = 0; d < G && peer_ok; ++d)
+    for (int e = 0; e < G && peer_ok; ++e) {
+      if (devs[e] == devs[d]) continue;
+      int can = 0;
+      if (cudaDeviceCanAccessPeer(&can, devs[d], devs[e]) != cudaSuccess) { cudaGetLastError(); can = 0; }
+      peer_ok = can != 0;
+    }
+  const bool p2p = o.exchange == 2 || (o.exchange == 0 && peer_ok);
+  if (p2p && !peer_ok)
+    return multi_fail(SPMESL_ERR_UNSUPPORTED, G > kP2PMax ? "peer-to-peer exchange: at most 16 devices"
+                                                          : "peer-to-peer exchange: no peer access between two of the devices");
+  if (dup && !p2p)
+    return multi_fail(SPMESL_ERR_ARG, "device ids must be distinct (NCCL exchange)");
   CommSet* cs = nullptr;
-  int rc = comms_for(devs, &cs);
+  int rc = p2p ? SPMESL_OK : comms_for(devs, &cs);
   if (rc) return rc;
   const NcclApi& A = nccl_api();
   const size_t pp = (size_t)p * (size_t)p;
@@ -185,6 +202,13 @@ int fit_multi_device(const double* X, int64_t n, int64_t p, double lambda0, doub
   std::vector<int32_t> cr, cc;
   std::vector<double> cv, diag((size_t)p);
   double ms_comm = 0.0;
+  // peer-to-peer exchange: every device's published buffers, and its symmetrized entries
+  P2PBlocks pb;
+  std::memset(&pb, 0, sizeof(pb));
+  pb.p = p;
+  pb.G = G;
+  std::vector<std::vector<int32_t>> pcr(G), pcc(G);
+  std::vector<std::vector<double>> pcv(G);
   auto worker = [&](int d) {
     int code = 0;
     std::string msg;
@@ -201,6 +225,15 @@ int fit_multi_device(const double* X, int64_t n, int64_t p, double lambda0, doub
     if (r_ != ncclSuccess) err(SPMESL_ERR_NCCL, std::string(#expr) + ": " + A.GetErrorString(r_)); \
   } while (0)
     MTRY(cudaSetDevice(devs[d]));
+    if (p2p)
+      for (int e = 0; e < G; ++e) {
+        bool seen = devs[e] == devs[d];
+        for (int f = 0; f < e && !seen; ++f) seen = devs[f] == devs[e];
+        if (seen) continue;
+        const cudaError_t pe = cudaDeviceEnablePeerAccess(devs[e], 0);
+        if (pe == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else MTRY(pe);
+      }
     cudaStream_t s = nullptr;
     MTRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
@@ -210,7 +243,11 @@ int fit_multi_device(const double* X, int64_t n, int64_t p, double lambda0, doub
     column_range(p, d, G, &c0, &c1);
     const int64_t m = c1 - c0;
     DevBuf<double> dX, sig, scale, sig_all, vals, vals_all;
-    DevBuf<uint8_t> hit, conv;
+    DevBuf<uint8_t> hit, share, conv;
+    DevBuf<int64_t> cpb, cpt;              // (p2p) this block's CSC column pointers
+    DevBuf<int32_t> crow, ccol;            // (p2p) this block's symmetrized entries
+    DevBuf<double> cvals, dgb, sgb;
+    DevBuf<int> ccount;
     DevBuf<int32_t> cnt, cnt_all, rows, rows_all, it, sw;
     MTRY(dX.alloc((size_t)n * p)); MTRY(hit.alloc(p)); MTRY(sig.alloc(m_max));
     MTRY(scale.alloc(p)); MTRY(cnt.alloc(m_max)); MTRY(it.alloc(m)); MTRY(sw.alloc(m));
@@ -218,6 +255,7 @@ int fit_multi_device(const double* X, int64_t n, int64_t p, double lambda0, doub
     if (!code) {
       MTRY(cudaMemcpyAsync(dX.p, X, (size_t)n * p * 8, cudaMemcpyHostToDevice, s));
       MTRY(cudaMemsetAsync(hit.p, 0, p, s));
+      if (p2p) { MTRY(share.alloc(p)); if (!code) MTRY(cudaMemsetAsync(share.p, 0, p, s)); }
       MTRY(cudaMemsetAsync(cnt.p, 0, (size_t)m_max * 4, s));
       MTRY(cudaMemsetAsync(sig.p, 0, (size_t)m_max * 8, s));
     }
@@ -227,11 +265,19 @@ int fit_multi_device(const double* X, int64_t n, int64_t p, double lambda0, doub
       int64_t t0, t1;
       column_range(nt, d, G, &t0, &t1);
       spmesl_stats ss;
-      const int r = spmesl_gram_screen_device(dX.p, n, p, lambda0, t0, t1, &od, hit.p, s, &ss);
+      const int r = spmesl_gram_screen_device(dX.p, n, p, lambda0, t0, t1, &od,
+                                              p2p ? share.p : hit.p, s, &ss);
       if (r < 0) err(r, spmesl_last_error());
+      pb.flags[d] = share.p;
     }
     code = rv.meet(code, msg);
-    if (!code && gram) {
+    if (!code && gram && p2p) {   // flags of every share, read from the peers' memory
+      MTRY(cudaEventRecord(e0, s));
+      MTRY(launch_p2p_flag_max(pb, hit.p, s));
+      MTRY(cudaEventRecord(e1, s));
+      MTRY(cudaStreamSynchronize(s));
+    }
+    if (!code && gram && !p2p) {
       MTRY(cudaEventRecord(e0, s));
       NTRY(A.AllReduce(hit.p, hit.p, (size_t)p, ncclUint8, ncclMax, cs->comms[d], s));
       MTRY(cudaEventRecord(e1, s));
@@ -266,11 +312,52 @@ int fit_multi_device(const double* X, int64_t n, int64_t p, double lambda0, doub
       if (converged) MTRY(cudaMemcpyAsync(converged + c0, conv.p, (size_t)m, cudaMemcpyDeviceToHost, s));
       MTRY(cudaStreamSynchronize(s));
     }
-    code = rv.meet(code, msg);   // (every nnz[] is known past this point)
+    if (p2p) {
+      // publish this block's CSC for the peers, meet, and symmetrize the own columns by
+      // reading each partner b_kj (and sigma_j) on the device that owns column j
+      if (!code) {
+        MTRY(cpb.alloc(m + 1)); MTRY(cpt.alloc(1));
+        if (!code) MTRY(launch_csc_scan(cnt.p, (int)m, cpb.p, cpt.p, s));
+        MTRY(cudaStreamSynchronize(s));
+        pb.col_ptr[d] = cpb.p; pb.rows[d] = rows.p; pb.vals[d] = vals.p; pb.sigma_std[d] = sig.p;
+        MTRY(crow.alloc(nnz[d])); MTRY(ccol.alloc(nnz[d])); MTRY(cvals.alloc(nnz[d]));
+        MTRY(dgb.alloc(m)); MTRY(sgb.alloc(m)); MTRY(ccount.alloc(1));
+      }
+      code = rv.meet(code, msg);
+      if (!code) {
+        MTRY(cudaEventRecord(e2, s));
+        MTRY(launch_assemble_coo_p2p(pb, d, o.standardize ? scale.p : nullptr, o.symmetrize, crow.p,
+                                     ccol.p, cvals.p, ccount.p, dgb.p, sgb.p, s));
+        MTRY(cudaEventRecord(e3, s));
+        int ncoo = 0;
+        MTRY(cudaMemcpyAsync(&ncoo, ccount.p, 4, cudaMemcpyDeviceToHost, s));
+        MTRY(cudaStreamSynchronize(s));
+        if (!code) {
+          pcr[d].resize(ncoo); pcc[d].resize(ncoo); pcv[d].resize(ncoo);
+          if (ncoo) {
+            MTRY(cudaMemcpyAsync(pcr[d].data(), crow.p, (size_t)ncoo * 4, cudaMemcpyDeviceToHost, s));
+            MTRY(cudaMemcpyAsync(pcc[d].data(), ccol.p, (size_t)ncoo * 4, cudaMemcpyDeviceToHost, s));
+            MTRY(cudaMemcpyAsync(pcv[d].data(), cvals.p, (size_t)ncoo * 8, cudaMemcpyDeviceToHost, s));
+          }
+          MTRY(cudaMemcpyAsync(diag.data() + c0, dgb.p, (size_t)m * 8, cudaMemcpyDeviceToHost, s));
+          MTRY(cudaMemcpyAsync(sigma + c0, sgb.p, (size_t)m * 8, cudaMemcpyDeviceToHost, s));
+          MTRY(cudaStreamSynchronize(s));
+        }
+        if (!code && d == 0) {
+          float a = 0.f, b = 0.f;
+          if (gram && cudaEventElapsedTime(&a, e0, e1) != cudaSuccess) { cudaGetLastError(); a = 0.f; }
+          if (cudaEventElapsedTime(&b, e2, e3) != cudaSuccess) { cudaGetLastError(); b = 0.f; }
+          ms_comm = (double)a + (double)b;
+        }
+      }
+      // no device frees its buffers while a peer may still read them
+      code = rv.meet(code, msg);
+    }
+    if (!p2p) code = rv.meet(code, msg);   // (every nnz[] is known past this point)
     int64_t nnz_max = 1;
     for (int e = 0; e < G; ++e) nnz_max = std::max(nnz_max, nnz[e]);
     // (3) all-gather of the CSC blocks (padded to the largest block)
-    if (!code) {
+    if (!code && !p2p) {
       MTRY(cnt_all.alloc((size_t)G * m_max)); MTRY(sig_all.alloc((size_t)G * m_max));
       MTRY(rows_all.alloc((size_t)G * nnz_max)); MTRY(vals_all.alloc((size_t)G * nnz_max));
       if (nnz_max > nnz[d] && rows.p) {   // (grow this block's buffers to the padded size)
@@ -284,8 +371,8 @@ int fit_multi_device(const double* X, int64_t n, int64_t p, double lambda0, doub
         }
       }
     }
-    code = rv.meet(code, msg);
-    if (!code) {
+    if (!p2p) code = rv.meet(code, msg);
+    if (!code && !p2p) {
       MTRY(cudaEventRecord(e2, s));
       NTRY(A.AllGather(cnt.p, cnt_all.p, (size_t)m_max, ncclInt32, cs->comms[d], s));
       NTRY(A.AllGather(sig.p, sig_all.p, (size_t)m_max, ncclFloat64, cs->comms[d], s));
@@ -295,7 +382,7 @@ int fit_multi_device(const double* X, int64_t n, int64_t p, double lambda0, doub
       MTRY(cudaStreamSynchronize(s));
     }
     // (4) device 0: the global CSC (ranks in column order), symmetrized COO + diagonal
-    if (!code && d == 0) {
+    if (!code && d == 0 && !p2p) {
       DevBuf<int32_t> cnt_g, rows_g;
       DevBuf<double> sig_g, vals_g, cvals, dg, sg;
       DevBuf<int64_t> col_ptr, total;
@@ -368,6 +455,8 @@ int fit_multi_device(const double* X, int64_t n, int64_t p, double lambda0, doub
   if (prev >= 0) cudaSetDevice(prev);
   if (rv.code) return multi_fail(rv.code, rv.msg);
   for (size_t e = 0; e < cr.size(); ++e) Theta[(size_t)cc[e] * p + cr[e]] = cv[e];
+  for (int d = 0; d < G; ++d)
+    for (size_t e = 0; e < pcr[d].size(); ++e) Theta[(size_t)pcc[d][e] * p + pcr[d][e]] = pcv[d][e];
   for (int64_t k = 0; k < p; ++k) Theta[(size_t)k * p + k] = diag[k];
   int worst = SPMESL_OK;
   for (int d = 0; d < G; ++d) worst = std::max(worst, rcs[d]);
@@ -389,6 +478,7 @@ int fit_multi_device(const double* X, int64_t n, int64_t p, double lambda0, doub
     st->solver = dst[0].solver;
     st->ms_comm = ms_comm;
     st->num_devices = G;
+    st->exchange = p2p ? 2 : 1;
   }
   return worst;
 }

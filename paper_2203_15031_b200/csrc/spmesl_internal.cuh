@@ -330,6 +330,24 @@ cudaError_t launch_sparse_write(int64_t p, const int* cnt, const int* cur, const
                                 int64_t cap = -1);   // cap >= 0: write only if nnz <= cap
 cudaError_t launch_csc_scan(const int* cnt, int ncols, int64_t* col_ptr, int64_t* total,
                             cudaStream_t s);
+// Peer-to-peer exchange of the multi-device fit (assemble.cu; multi.cu): the column blocks of
+// all G devices as pointers valid on the launching device (its own, or peers' through
+// cudaDeviceEnablePeerAccess).  Block e holds columns column_range(p, e, G).
+constexpr int kP2PMax = 16;
+struct P2PBlocks {
+  int64_t p;
+  int G;
+  const uint8_t* flags[kP2PMax];       // screening flags of the device's tile share [p]
+  const int64_t* col_ptr[kP2PMax];     // block-local CSC column pointers [m_e + 1]
+  const int32_t* rows[kP2PMax];        // rows ascending per column
+  const double* vals[kP2PMax];         // b_jk
+  const double* sigma_std[kP2PMax];    // sigma_k of the block's columns [m_e]
+};
+cudaError_t launch_p2p_flag_max(const P2PBlocks& B, uint8_t* out, cudaStream_t s);
+cudaError_t launch_assemble_coo_p2p(const P2PBlocks& B, int self, const double* scale,
+                                    int symmetrize, int32_t* coo_row, int32_t* coo_col,
+                                    double* coo_val, int* coo_count, double* diag,
+                                    double* sigma_out, cudaStream_t s);
 cudaError_t launch_assemble_lists(int64_t p, const int* nz_count, const int* nz_cur,
                                   const int* nz_rows, const double* nz_vals, int nzcap,
                                   const double* sigma_std, const double* scale, int symmetrize,

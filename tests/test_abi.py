@@ -150,3 +150,6 @@ def test_multi_device_options_validated_before_cuda():
     with pytest.raises(S.SpmeslError) as e:
         S.fit(X, 0.3, num_devices=65)
     assert e.value.code == -1
+    with pytest.raises(S.SpmeslError) as e:       # options.exchange outside 0..2
+        S.fit(X, 0.3, num_devices=1, exchange=3)
+    assert e.value.code == -1
