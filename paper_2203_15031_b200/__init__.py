@@ -148,15 +148,56 @@ def as_colmajor(X):
     return X.t().contiguous().t()
 
 
+_OUT_KEYS = ("theta", "sigma", "iters", "sweeps", "conv")
+_STATS_NAMES = tuple(k for k, _ in Stats._fields_)
+_FAST = {}   # repeated device fits on the same buffers: the marshalled call, reused
+
+
+def _fast_key(X, lambda0, tol, max_iter, s, out, options):
+    try:
+        key = (X.data_ptr(), X.shape, X.stride(), X.dtype, X.device, float(lambda0), float(tol),
+               int(max_iter), s.cuda_stream, tuple(out[k].data_ptr() for k in _OUT_KEYS),
+               tuple(out[k].dtype for k in _OUT_KEYS), out["theta"].shape,
+               tuple(sorted(options.items())))
+        hash(key)
+        return key
+    except (TypeError, KeyError, AttributeError):
+        return None
+
+
+def _result(rc, out, st):
+    import torch
+    # the buffer holds Theta column-major: element (j, k) at j + k p -> view as its transpose
+    # (uint8 0/1 reinterpreted as bool: a view, no conversion kernel)
+    return FitResult(rc, out["theta"].t(), out["sigma"], out["iters"], out["sweeps"],
+                     out["conv"].view(torch.bool), {k: getattr(st, k) for k in _STATS_NAMES})
+
+
 def fit_device(X, lambda0: float, tol: float = 1e-4, max_iter: int = 100, *, stream=None,
                out=None, **options) -> FitResult:
-    """spmesl_fit_device on torch CUDA tensors.  X: (n, p) float64 on the current device."""
+    """spmesl_fit_device on torch CUDA tensors.  X: (n, p) float64 on the current device.
+    A repeat of an earlier call with the same tensors (`out` given), stream and options — a
+    fit loop on reused buffers — reuses the marshalled ctypes arguments (one native call)."""
     import torch
+    key = None
+    if out is not None and getattr(X, "is_cuda", False):
+        s = stream if stream is not None else torch.cuda.current_stream(X.device)
+        key = _fast_key(X, lambda0, tol, max_iter, s, out, options)
+        ent = _FAST.get(key) if key is not None else None
+        if ent is not None:
+            fn, args, st, dev = ent
+            if torch.cuda.current_device() != dev:
+                with torch.cuda.device(dev):
+                    rc = fn(*args)
+            else:
+                rc = fn(*args)
+            _lib.check(rc, st)
+            return _result(rc, out, st)
     if not X.is_cuda or X.dtype != torch.float64:
         raise TypeError("X must be a float64 CUDA tensor")
-    X = as_colmajor(X)
-    n, p = X.shape
-    dev = X.device
+    Xc = as_colmajor(X)
+    n, p = Xc.shape
+    dev = Xc.device
     if out is None:
         out = dict(
             theta=torch.empty((p, p), dtype=torch.float64, device=dev),
@@ -167,16 +208,18 @@ def fit_device(X, lambda0: float, tol: float = 1e-4, max_iter: int = 100, *, str
     s = stream if stream is not None else torch.cuda.current_stream(dev)
     st = Stats()
     o = _opts(**options)
+    fn = load().spmesl_fit_device
+    args = (_vp(Xc), n, p, float(lambda0), float(tol), int(max_iter), ctypes.byref(o),
+            _vp(out["theta"]), _vp(out["sigma"]), _vp(out["iters"]), _vp(out["sweeps"]),
+            _vp(out["conv"]), ctypes.c_void_p(s.cuda_stream), ctypes.byref(st))
     with torch.cuda.device(dev):
-        rc = load().spmesl_fit_device(_vp(X), n, p, float(lambda0), float(tol), int(max_iter),
-                                      ctypes.byref(o), _vp(out["theta"]), _vp(out["sigma"]),
-                                      _vp(out["iters"]), _vp(out["sweeps"]), _vp(out["conv"]),
-                                      ctypes.c_void_p(s.cuda_stream), ctypes.byref(st))
+        rc = fn(*args)
     _lib.check(rc, st)
-    # the buffer holds Theta column-major: element (j, k) at j + k p -> view as its transpose
-    # (uint8 0/1 reinterpreted as bool: a view, no conversion kernel)
-    return FitResult(rc, out["theta"].t(), out["sigma"], out["iters"], out["sweeps"],
-                     out["conv"].view(torch.bool), st.asdict())
+    # (cached only when X was used as given: the arguments hold raw pointers, valid for as
+    # long as tensors with these addresses, shapes and dtypes exist — which the key checks)
+    if key is not None and Xc is X and len(_FAST) < 64:
+        _FAST[key] = (fn, args, st, dev.index)
+    return _result(rc, out, st)
 
 
 def fit_sparse_device(X, lambda0: float, tol: float = 1e-4, max_iter: int = 100, *,
