@@ -239,6 +239,7 @@ def per_config_block(S, dev, stream, flush, seeds=3, fits=5):
     import torch
     from synth import generators as G
     fpk, fsrc = dfma_peak()
+    hpk, hsrc = hbm_peak_gbs()
     out = []
     for label, cfg, over, rule in PER_CONFIG:
         rows = []
@@ -272,6 +273,8 @@ def per_config_block(S, dev, stream, flush, seeds=3, fits=5):
                              sweeps=st["total_sweeps"], max_sweeps=st["max_sweeps"],
                              multi=st["tail_columns"], nnz=st["nnz"], sweep_ms=sweep_ms,
                              tf=(sweep_flops / (sweep_ms / 1000.0) / 1e12) if sweep_ms > 0 else None,
+                             gbs=(8.0 * p * st.get("tail_changes", 0) / (sweep_ms / 1000.0) / 1e9)
+                             if sweep_ms > 0 else None,
                              changes=st.get("tail_changes", 0), passes=st.get("tail_passes", 0),
                              cand=st.get("screen_candidates"),
                              seed=spec["seed"]))
@@ -295,6 +298,18 @@ def per_config_block(S, dev, stream, flush, seeds=3, fits=5):
                                      "achieved_tflops": [r["tf"] for r in rows],
                                      "frac_of_fp64": [(r["tf"] / fpk) if r["tf"] else None for r in rows],
                                      "peak_tflops": fpk, "peak_source": fsrc,
+                                     # the north_star's memory view: a row-at-a-time
+                                     # covariance-update CD reads one Gram column (8 p B) per
+                                     # coordinate change and S (8 p^2 B) exceeds L2 at these p;
+                                     # the multi-sweep passes read each support column once for
+                                     # up to 32 sweeps, so the bytes actually moved are well below
+                                     # these (ncu: profiles/r02_tail_*_ncu_summary.txt)
+                                     "memory_view": {
+                                         "algorithmic": "one Gram column (8 p B) per coordinate change",
+                                         "achieved_gbs": [r["gbs"] for r in rows],
+                                         "peak_gbs": hpk, "peak_source": hsrc,
+                                         "frac_of_hbm": [(r["gbs"] / hpk) if r["gbs"] else None
+                                                         for r in rows]},
                                      "timing": "eager fit (CUDA events around the kernel)"}})
     return out
 
