@@ -12,3 +12,7 @@ python scripts/tail_profile.py band3 > gpurun_out/tp_band.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:tail_sweep -s 1 -c 1 -o gpurun_out/prof_tail_band -f python scripts/tail_profile.py band3 > gpurun_out/ncu3.log 2>&1; echo "ncu tail band rc=$?"
 python scripts/tail_profile.py hub > gpurun_out/tp_hub.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:tail_sweep -s 1 -c 1 -o gpurun_out/prof_tail_hub -f python scripts/tail_profile.py hub > gpurun_out/ncu4.log 2>&1; echo "ncu tail hub rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:gram_cols -s 3 -c 1 -o gpurun_out/prof_gc -f $CMD > gpurun_out/ncu5.log 2>&1; echo "ncu gram_cols rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:standardize -s 3 -c 1 -o gpurun_out/prof_std -f $CMD > gpurun_out/ncu6.log 2>&1; echo "ncu standardize rc=$?"
+python scripts/tail_profile.py univ5 > gpurun_out/tp_univ.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:tail_sweep -s 1 -c 1 -o gpurun_out/prof_tail_univ -f python scripts/tail_profile.py univ5 > gpurun_out/ncu7.log 2>&1; echo "ncu tail univ rc=$?"
