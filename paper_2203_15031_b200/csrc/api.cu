@@ -800,11 +800,26 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
   T.order_bar = &dc->tail_ordered;
   set_tail_shape(W, T);
   const int tgrid = (int)std::min<int64_t>(W.sms, p * nlam);
-  if (!T.z2) {   // (the multi-sweep mode's second z buffer in global memory, one slice per CTA)
-    if ((rc = ensure(W.z2g, (size_t)tgrid * std::max(T.occ, 1) * p * 8))) return rc;
-    T.z2g = (double*)W.z2g.ptr;
+  // Without skewed hit counts (band-like workloads) three 160-thread column CTAs per SM with the
+  // multi-sweep mode's second z buffer in global memory beat two with it on chip (more chains
+  // interleave); with them (hub) the on-chip buffer wins by far (its per-segment passes).  The
+  // counts are on the device: both shapes are launched, gated, and one exits at once.
+  const bool dual = bhist && nlam == 1 && T.occ == 2 && T.z2 &&
+                    3 * (tail_smem_bytes((int)p, T.n_pad, T.nzcap) + 1024) <= (size_t)W.smem_sm;
+  if (!T.z2 || dual) {   // (the multi-sweep mode's second z buffer in global memory, one slice per CTA)
+    if ((rc = ensure(W.z2g, (size_t)tgrid * (dual ? 3 : std::max(T.occ, 1)) * p * 8))) return rc;
   }
-  CUDA_TRY(launch_tail_sweeps(T, tgrid, s));
+  if (!T.z2) T.z2g = (double*)W.z2g.ptr;
+  if (dual) {
+    TailParams T3 = T;
+    T3.occ = 3; T3.z2 = 0; T3.z2g = (double*)W.z2g.ptr; T3.gate = 2;
+    T.gate = 1;
+    CUDA_TRY(launch_tail_sweeps(T, tgrid, s));
+    CUDA_TRY(launch_tail_sweeps(T3, tgrid, s));
+    launches += 1;
+  } else {
+    CUDA_TRY(launch_tail_sweeps(T, tgrid, s));
+  }
   CUDA_TRY(ev_record(W, W.ev[6], s));
   CUDA_TRY(ev_record(W, W.ev[2], s));
   W.gram_launches = launches + 2;   // + gram_init, tail

@@ -126,6 +126,8 @@ struct TailParams {
   int z2;                  // 1: a second z buffer (tail_z2_bytes more shared memory): a pass
                            //    that finds no new row swaps in z + all chain changes
   double* z2g;             // (z2 == 0) optional [grid][p] global scratch for the multi-sweep mode
+  int gate;                // 0: run; 1: run only if the hit counts are skewed (tail_skewed),
+                           //   2: only if they are not (two launch shapes, one of which exits)
   int* flags;
   int* nz_rows;            // column coefficient lists (as in CDParams)
   double* nz_vals;

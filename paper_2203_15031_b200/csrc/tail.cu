@@ -778,8 +778,11 @@ __device__ __forceinline__ void mpass(const double* zs, double* zd, const uint32
 // only decides which CTA takes a column when; results do not depend on it.  Returns whether
 // the order is used (not when the counts are too even to matter: the most hits below twice
 // the median + 4, e.g. band(3): 6 vs 3; hub: 70 vs 12).
+// Are the per-column hit counts skewed (the most hits >= 2 x the median + 4)?  Every CTA reads
+// the same histogram, so every CTA reaches the same answer.  Leaves in off[0..1023] the
+// exclusive scan of the bucket sizes (bucket 0: the most hits), which order_tail places by.
 template <int NT>
-__device__ bool order_tail(const TailParams& P, int M, int* off) {
+__device__ bool tail_skewed(const TailParams& P, int M, int* off) {
   const int tid = threadIdx.x;
   for (int b = tid; b < 1024; b += NT) off[b] = P.bhist[b];   // (one round of loads)
   __syncthreads();
@@ -803,7 +806,13 @@ __device__ bool order_tail(const TailParams& P, int M, int* off) {
     if (tid == 0) off[1024] = (1023 - top) >= 2 * (1023 - med) + 4;   // hits: top vs median
   }
   __syncthreads();
-  if (!off[1024]) return false;   // (the same decision in every CTA)
+  return off[1024] != 0;
+}
+
+template <int NT>
+__device__ bool order_tail(const TailParams& P, int M, int* off) {
+  const int tid = threadIdx.x;
+  if (!tail_skewed<NT>(P, M, off)) return false;   // (the same decision in every CTA)
   const int per = (M + gridDim.x - 1) / gridDim.x;
   for (int k = blockIdx.x * per + tid; k < min(M, (int)(blockIdx.x + 1) * per); k += NT) {
     const int key = P.tail_key[k];
@@ -848,6 +857,9 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const size_t list_stride = (size_t)2 * nzcap;
   const int M = P.M_dev ? *(volatile const int*)P.M_dev : P.M;
+  // two launch shapes behind one another (launch_tail_sweeps): the one the hit counts do not
+  // call for exits at once (the same decision in every CTA of both)
+  if (P.gate && (tail_skewed<NT>(P, M, (int*)(sm + TS_BYTES)) != (P.gate == 1))) return;
   // (fewer columns than CTAs: all start at once; scratch: the tiles region, not in use yet)
   {
     const bool ordered = P.bhist && M > (int)gridDim.x && order_tail<NT>(P, M, (int*)(sm + TS_BYTES));
@@ -1626,6 +1638,7 @@ cudaError_t launch_tail_sweeps(const TailParams& P, int grid, cudaStream_t s) {
   const bool multi = (P.z2 || P.z2g) && !P.joint;
   if (P.occ == 1)
     return multi ? launch_tail_e<512, 1, true>(P, grid, smem, s) : launch_tail_e<512, 1, false>(P, grid, smem, s);
+  if (P.occ == 3 && multi) return launch_tail_e<160, 3, true>(P, grid, smem, s);
   return multi ? launch_tail_e<256, 2, true>(P, grid, smem, s) : launch_tail_e<256, 2, false>(P, grid, smem, s);
 }
 

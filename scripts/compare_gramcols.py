@@ -1,6 +1,6 @@
-"""Development check: two builds (paths) bit for bit on workloads that take the exact-Gram-column
-path of the certified screening (config 5 at lambda_ub: 65 candidates; lower penalties: several
-96-column vector groups), eager fits."""
+"""Development check: two builds (paths) bit for bit, eager fits: the exact-Gram-column path of the
+certified screening (config 5 at lambda_ub: 65 candidates; lower penalties: several 96-column
+vector groups) and the multi-sweep workloads (config 4 band(3) / hub, odd p)."""
 import ctypes
 import sys
 
@@ -42,8 +42,11 @@ def run(L, Xd, lam):
 
 
 bad = 0
-for cfg, over, scale in ((5, {}, 1.0), (5, {}, 0.9), (5, {}, 0.8), (3, {}, 1.0), (3, {}, 0.85),
-                         (5, dict(p=3001), 0.8)):
+CASES = ((5, {}, 1.0), (5, {}, 0.9), (5, {}, 0.8), (3, {}, 1.0), (3, {}, 0.85), (5, dict(p=3001), 0.8),
+         (4, dict(family="band3"), 1.0), (4, dict(family="hub"), 1.0),
+         (4, dict(family="hub", seed=3207), 1.0), (4, dict(family="band3"), 0.7),
+         (4, dict(family="band3", p=3001), 1.0), (4, dict(family="hub", p=1999), 0.8))
+for cfg, over, scale in CASES:
     X, _, spec = G.make_config(cfg, **over)
     n, p = X.shape
     lam = libs[0].spmesl_lambda_ub(n, p, 1.0) * scale
