@@ -739,10 +739,12 @@ __device__ __forceinline__ void run_mpass(const double* zs, double* zd, const ui
       }
     }
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int i = base + r * NT + tid;
-      if (i < p) zd[i] = acc[r];
-    }
+    if (zd)   // (NULL: the chain ends the column; z after the pass is not needed)
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int i = base + r * NT + tid;
+        if (i < p) zd[i] = acc[r];
+      }
     if (SPEC && best < best_in) atomicMin(mkey, best);
   }
 }
@@ -1132,8 +1134,13 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
         TPROF_C(c_chain += tp1 - tp0;)
         int best = 0x7fffffff;
         double bestw = 0.0;
-        mpass<NT, true>(z, use_z2 ? z2 : zG, oldmask, P.Gtab, TS, MD, KS, MDS, p, K, Msw, gc,
-                        TS.mlam, 0, 0, &TS.mkey, best, bestw);
+        // When the chain retires the column at its last sweep, z after the pass is never read
+        // (the column ends if every sweep holds; a new row rolls back from z itself): the pass
+        // then only tests, without writing z + changes (at p = 20000: 160 KB written to the
+        // global second buffer and read back per column)
+        const bool ends = TS.mret_e != 0;
+        mpass<NT, true>(z, ends ? nullptr : (use_z2 ? z2 : zG), oldmask, P.Gtab, TS, MD, KS, MDS,
+                        p, K, Msw, gc, TS.mlam, 0, 0, &TS.mkey, best, bestw);
         {
           const int wb = __reduce_min_sync(0xffffffffu, best);
           if (best == wb && best != 0x7fffffff) TS.wval[warp] = bestw;
@@ -1150,7 +1157,8 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
         TPROF_C(c_spec += tp2 - tp1;)
         if (jkey == 0x7fffffff) {
           // every speculated sweep holds: z2 is z after them; the list is the last sweep's
-          if (use_z2) { double* t = z; z = z2; z2 = t; }
+          if (ends) {
+          } else if (use_z2) { double* t = z; z = z2; z2 = t; }
           else {
             // (16 loads in flight per thread; the pass's global writes are this CTA's own,
             // ordered by the barrier above)
