@@ -9,9 +9,9 @@ timeout 300 $CMD > gpurun_out/plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu1.log 2>&1; echo "ncu launches rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:screen16 -s 3 -c 1 -o gpurun_out/prof_s16 -f $CMD > gpurun_out/ncu2.log 2>&1; echo "ncu screen16 rc=$?"
 python scripts/tail_profile.py band3 > gpurun_out/tp_band.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:tail_sweep -s 1 -c 1 -o gpurun_out/prof_tail_band -f python scripts/tail_profile.py band3 > gpurun_out/ncu3.log 2>&1; echo "ncu tail band rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:tail_sweep -s 3 -c 1 -o gpurun_out/prof_tail_band -f python scripts/tail_profile.py band3 > gpurun_out/ncu3.log 2>&1; echo "ncu tail band rc=$?"
 python scripts/tail_profile.py hub > gpurun_out/tp_hub.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:tail_sweep -s 1 -c 1 -o gpurun_out/prof_tail_hub -f python scripts/tail_profile.py hub > gpurun_out/ncu4.log 2>&1; echo "ncu tail hub rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:tail_sweep -s 2 -c 1 -o gpurun_out/prof_tail_hub -f python scripts/tail_profile.py hub > gpurun_out/ncu4.log 2>&1; echo "ncu tail hub rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gram_cols -s 3 -c 1 -o gpurun_out/prof_gc -f $CMD > gpurun_out/ncu5.log 2>&1; echo "ncu gram_cols rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:standardize -s 3 -c 1 -o gpurun_out/prof_std -f $CMD > gpurun_out/ncu6.log 2>&1; echo "ncu standardize rc=$?"
 python scripts/tail_profile.py univ5 > gpurun_out/tp_univ.log 2>&1 && \
