@@ -131,6 +131,10 @@ struct Workspace {
   bool zero_join = false;     // part of Theta's zero fill runs on `side` (join ev_join)
   int64_t screen_fill = 0;    // doubles of Theta the screening kernel zero-filled (last fit)
   int gram_launches = 0;      // kernels fit_gram_enqueue launched (last fit)
+  // auto solver: the arguments (X, n, p, lambda0, tol, max_iter, options, outputs) of the last
+  // fit whose certified screening fell back to the full FP64 Gram kernel — a repeat runs the full
+  // Gram path directly (fit_device_impl)
+  std::vector<unsigned char> auto_full_key;
   bool init = false;
 };
 
@@ -1107,7 +1111,8 @@ int fit_columns_core(Workspace& W, const double* dX, int64_t n, int64_t p, int64
 int gram_fit_enqueue_all(Workspace& W, const double* dX, int64_t n, int64_t p, double lambda0,
                          double tol, int32_t max_iter, const spmesl_options& o, double* dTheta,
                          double* dSigma, int32_t* dIters, int32_t* dSweeps, uint8_t* dConv,
-                         const FitOut& out, cudaStream_t cs, Layout& L, int nzcap) {
+                         const FitOut& out, cudaStream_t cs, Layout& L, int nzcap,
+                         bool screen16) {
   int rc;
   const size_t pp = (size_t)p * (size_t)p;
   // the screening kernel zero-fills Theta itself (bulk stores from its producer warp) when the
@@ -1117,7 +1122,7 @@ int gram_fit_enqueue_all(Workspace& W, const double* dX, int64_t n, int64_t p, d
   if (take) { W.take_zero = dTheta; W.take_count = pp; }
   else if (!sparse) { W.pending_zero = dTheta; W.pending_count = pp; }
   rc = fit_gram_enqueue(W, dX, n, p, lambda0, tol, max_iter, o, out, cs, L, nzcap, nullptr, 1,
-                        o.solver != 2);
+                        screen16);
   W.take_zero = nullptr;
   if (W.pending_zero) {    // (the solver failed before standardization)
     W.pending_zero = nullptr;
@@ -1224,14 +1229,31 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
   if (gram) {
     // (no side-stream work may be captured: the fill must be the screening kernel's own)
     const bool use_graph = !o.eager && o.solver != 2 && (((uintptr_t)dTheta & 15) == 0);
+    // Auto solver: the certified screening pays off only when it leaves few candidates; when
+    // the last fit on these very arguments fell back to the full FP64 Gram kernel (most columns
+    // candidates: band, hub, lambda_univ), this one runs the full-Gram path (solver 2) directly
+    // — no f16 screening pass, and Theta's zero fill rides inside the DMMA-bound Gram kernel.
+    // Solvers 2 and 3 give the same iterates bit for bit, so the history only decides speed; a
+    // full-Gram fit with few hit columns hands the choice back to the screening.
+    spmesl_options ko = o;   // (the choice is part of the captured graph's key)
+    std::vector<unsigned char> akey;
+    bool full = o.solver == 2;
+    if (o.solver == 0) {
+      spmesl_options ao = o;
+      ao.eager = 0;          // (eager and replayed fits share the history)
+      akey = graph_key(dX, n, p, lambda0, tol, max_iter, ao, dTheta, dSigma, dIters, dSweeps, dConv,
+                       0, s, W.sparse);
+      full = !W.auto_full_key.empty() && W.auto_full_key == akey;
+      if (full) ko.solver = 2;
+    }
     // the captured fit's list capacity if these are its arguments, else the initial one
     nzcap = initial_nzcap(n, p);
     if (W.gexec && W.graph_nzcap > 0 &&
-        graph_key(dX, n, p, lambda0, tol, max_iter, o, dTheta, dSigma, dIters, dSweeps, dConv,
+        graph_key(dX, n, p, lambda0, tol, max_iter, ko, dTheta, dSigma, dIters, dSweeps, dConv,
                   W.graph_nzcap, s, W.sparse) == W.gkey)
       nzcap = W.graph_nzcap;
     for (int attempt = 0; attempt < 4; ++attempt) {
-      std::vector<unsigned char> key = graph_key(dX, n, p, lambda0, tol, max_iter, o, dTheta,
+      std::vector<unsigned char> key = graph_key(dX, n, p, lambda0, tol, max_iter, ko, dTheta,
                                                  dSigma, dIters, dSweeps, dConv, nzcap, s, W.sparse);
       bool launched = false;
       if (use_graph && W.gexec && key == W.gkey) {
@@ -1249,7 +1271,7 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
         cudaError_t e = cudaStreamBeginCapture(W.cap, cudaStreamCaptureModeRelaxed);
         if (e == cudaSuccess) {
           rc = gram_fit_enqueue_all(W, dX, n, p, lambda0, tol, max_iter, o, dTheta, dSigma,
-                                    dIters, dSweeps, dConv, out, W.cap, L, nzcap);
+                                    dIters, dSweeps, dConv, out, W.cap, L, nzcap, !full);
           cudaGraph_t g = nullptr;
           e = cudaStreamEndCapture(W.cap, &g);
           W.capturing = false;
@@ -1276,15 +1298,20 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
       }
       if (!launched) {
         rc = gram_fit_enqueue_all(W, dX, n, p, lambda0, tol, max_iter, o, dTheta, dSigma,
-                                  dIters, dSweeps, dConv, out, s, L, nzcap);
+                                  dIters, dSweeps, dConv, out, s, L, nzcap, !full);
         if (rc) return rc;
         W.last_key = key;
       }
       CUDA_TRY(cudaStreamSynchronize(s));
       if (W.host_counters->err) return std_error(W, st);
       if (!W.host_counters->overflow) {
-        gram_stats(W, p, nzcap, st, o.solver != 2, launched);
+        gram_stats(W, p, nzcap, st, !full, launched);
         if (st) st->graph_replay = launched ? 1 : 0;
+        if (o.solver == 0) {   // (the screening history of these arguments)
+          if (!full && gram_fallback_taken(W.host_counters->s16_nU, p)) W.auto_full_key = akey;
+          else if (full && !gram_fallback_taken(W.host_counters->tail_count, p)) W.auto_full_key.clear();
+          if (full && st) st->gram_fallback = 1;
+        }
         break;
       }
       if (nzcap >= p) return fail(SPMESL_ERR_OOM, "coefficient list overflow");
