@@ -78,7 +78,11 @@ typedef struct {
   int32_t solver;         /* 0 (default): auto — solver 3 when mode = 0, the whole column range
                              is fitted on one device, p is at most ~26000 (the sweep kernel
                              keeps z[p] on chip) and 8 p^2 bytes fit in device memory; else
-                             the residual solver.  1: residual solver (persistent CD kernel on
+                             the residual solver; on the device path a repeat of a fit (same
+                             arguments) whose certified screening left most columns candidates
+                             runs solver 2's path directly (same iterates bit for bit; a
+                             full-Gram fit with few hit columns hands back to solver 3).
+                             1: residual solver (persistent CD kernel on
                              X~ streamed through shared memory).  2: Gram solver with the full
                              S = X~^T X~ / n (symmetric FP64 DMMA contraction, first-sweep
                              screening fused in), then covariance updates.  3: Gram solver with
