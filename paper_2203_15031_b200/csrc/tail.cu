@@ -1288,7 +1288,7 @@ __global__ void __launch_bounds__(NT, MINB) tail_sweep_kernel(const TailParams P
           if (tid == 0) { TS.prow[0] = istar; TS.pd[0] = d; }
           npend = 1;
           pos = istar + 1;
-          mult = min(MMAX, max(4, 2 * (sstar + 1)));
+          mult = min(MMAX, max(8, 2 * (sstar + 1)));   // (floor 8: hub seeds 2207 / 3207 / 4207 -0.4 / -2.3 / -0.2 % against 4)
           TPROF_ADD(6, 1);
           TPROF_C(++c_fail;)
           TPROF_ADD(8, sstar);
