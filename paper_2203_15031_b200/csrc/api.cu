@@ -185,6 +185,7 @@ int validate(const void* X, int64_t n, int64_t p, double lambda0, double tol, in
   if (n < 2) return fail(SPMESL_ERR_ARG, "n must be >= 2");
   if (p < 2) return fail(SPMESL_ERR_ARG, "p must be >= 2");
   if (p > (int64_t)0x7fffffff) return fail(SPMESL_ERR_ARG, "p must be < 2^31");
+  if (n > (int64_t)0x7fff0000) return fail(SPMESL_ERR_ARG, "n must be < 2^31 - 2^16");
   if (!(lambda0 >= 0.0) || !std::isfinite(lambda0)) return fail(SPMESL_ERR_ARG, "lambda0 must be finite and >= 0");
   if (!(tol > 0.0) || !std::isfinite(tol)) return fail(SPMESL_ERR_ARG, "tol must be finite and > 0");
   if (max_iter < 1) return fail(SPMESL_ERR_ARG, "max_iter must be >= 1");

@@ -91,7 +91,8 @@ __global__ void standardize_kernel(const double* __restrict__ X, int64_t n, int6
   }
   double sum = 0.0, mx = 0.0;
   bool finite = true;
-  for (int64_t i = lane; i < n; i += 32) {
+  const int ni = (int)n, npi = (int)n_pad, n64i = (int)n64;   // (32-bit sample indices)
+  for (int i = lane; i < ni; i += 32) {
     double v = x[i];
     finite = finite && isfinite(v);
     sum += v;
@@ -109,7 +110,7 @@ __global__ void standardize_kernel(const double* __restrict__ X, int64_t n, int6
   if (standardize) {
     m = sum / (double)n;
     double ss = 0.0;
-    for (int64_t i = lane; i < n; i += 32) {
+    for (int i = lane; i < ni; i += 32) {
       double c = x[i] - m;
       ss = fma(c, c, ss);
     }
@@ -127,10 +128,10 @@ __global__ void standardize_kernel(const double* __restrict__ X, int64_t n, int6
   double* xw = stage_n > 0 ? const_cast<double*>(x) : nullptr;
   // (row jl of column block k / J: element i = 32 q + lane sits at base + q J XS + xswz(jl, lane))
   double* xbk = Xb + xb_index(0, k, nchunk) - xswz((int)(k % J), 0) + xswz((int)(k % J), lane);
-  for (int64_t i = lane; i < n_pad; i += 32, xbk += J * XS) {
-    const double v = i < n ? (standardize ? div_rn(x[i] - m, s, rs) : x[i]) : 0.0;
+  for (int i = lane; i < npi; i += 32, xbk += J * XS) {
+    const double v = i < ni ? (standardize ? div_rn(x[i] - m, s, rs) : x[i]) : 0.0;
     *xbk = v;
-    if (xw && i < n) xw[i] = v;
+    if (xw && i < ni) xw[i] = v;
     g = fma(v, v, g);
   }
   __syncwarp();
@@ -148,9 +149,9 @@ __global__ void standardize_kernel(const double* __restrict__ X, int64_t n, int6
       // (staged column: convert lane-strided into the warp's f16 buffer after the column — no
       // bank conflicts — then store 16-byte chunks of 8 samples; the same values as below)
       __half* hb = (__half*)(xw + stage_n);
-      for (int64_t i = lane; i < n64; i += 32) hb[i] = __double2half(i < n ? xw[i] * sc : 0.0);
+      for (int i = lane; i < n64i; i += 32) hb[i] = __double2half(i < ni ? xw[i] * sc : 0.0);
       __syncwarp();
-      for (int64_t i0 = 8 * lane; i0 < n64; i0 += 256)
+      for (int i0 = 8 * lane; i0 < n64i; i0 += 256)
         *(uint4*)(y.Y16 + y16_index(k, i0, y.nchunk64)) = *(const uint4*)(hb + i0);
     } else
     for (int64_t i0 = 8 * lane; i0 < n64; i0 += 256) {   // 8 samples = one 16-byte chunk
