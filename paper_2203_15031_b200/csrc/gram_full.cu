@@ -309,9 +309,11 @@ __global__ void level_flags_kernel(const GramParams P) {
 // so outer iteration 1 ends with the fresh residual x~_c (reading g4).  Retire it or,
 // if sigma moved by >= tol (possible only without standardization), hand it to the sweep
 // kernel like every column with a hit.
+// PT (P.ssq given: x~_c^T x~_c is known, nothing to sum): one thread per column instead of a warp
+template <bool PT>
 __global__ void gram_init_kernel(const GramParams P) {
-  const int lane = threadIdx.x & 31;
-  const int q = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
+  const int lane = PT ? 0 : (int)(threadIdx.x & 31);
+  const int q = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> (PT ? 0 : 5));
   if (q >= P.ncols * P.nlam) return;
   const int l = q / P.ncols, c = q - l * P.ncols;                // penalty level, column
   const int slot = l * P.ncols + c;                              // output index
@@ -321,7 +323,7 @@ __global__ void gram_init_kernel(const GramParams P) {
   ts.lam = l; ts.sigma = 1.0;
   if (!P.hit[(size_t)l * P.p + gc]) {
     double ss = 0.0;
-    if (P.ssq) {
+    if (PT || P.ssq) {
       ss = P.ssq[gc];   // (summed by the standardization in this very order)
     } else {
       for (int i = lane; i < P.n; i += 32) {
@@ -390,7 +392,10 @@ cudaError_t launch_gram_init(const GramParams& P, cudaStream_t s) {
   if (P.ncols <= 0) return cudaSuccess;
   const int wpb = 8;
   const int w = P.ncols * P.nlam;
-  gram_init_kernel<<<(w + wpb - 1) / wpb, wpb * 32, 0, s>>>(P);
+  if (P.ssq)
+    gram_init_kernel<true><<<(w + 255) / 256, 256, 0, s>>>(P);
+  else
+    gram_init_kernel<false><<<(w + wpb - 1) / wpb, wpb * 32, 0, s>>>(P);
   return cudaGetLastError();
 }
 
