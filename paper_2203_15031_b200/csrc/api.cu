@@ -1151,15 +1151,18 @@ int gram_fit_enqueue_all(Workspace& W, const double* dX, int64_t n, int64_t p, d
                                  o.symmetrize, W.sparse->col_ptr, W.sparse->rows,
                                  W.sparse->vals, dSigma, cs, W.sparse->cap));
   } else {
-    // assembly + symmetrization straight from the coefficient lists (no CSC packing)
+    // assembly + symmetrization straight from the coefficient lists (no CSC packing), with
+    // the fit statistics (column_stats_kernel's work) fused in
+    const ColStats cst{dIters, dSweeps, dConv, &dc->st_sweeps, &dc->st_max_sweeps,
+                       &dc->st_max_outer, &dc->st_unconv, &dc->t_end};
     CUDA_TRY(launch_assemble_lists(p, (const int*)W.nz_count.ptr, (const int*)W.nz_cur.ptr,
                                    (const int*)W.nz_rows.ptr, (const double*)W.nz_vals.ptr, nzcap,
                                    (const double*)W.sigma_std.ptr,
                                    o.standardize ? (const double*)W.scale.ptr : nullptr,
-                                   o.symmetrize, dTheta, dSigma, &dc->csc_total, cs));
+                                   o.symmetrize, dTheta, dSigma, &dc->csc_total, cs, &cst));
   }
   CUDA_TRY(ev_record(W, W.ev[4], cs));
-  if ((rc = device_stats(W, dIters, dSweeps, dConv, p, cs))) return rc;
+  if (sparse && (rc = device_stats(W, dIters, dSweeps, dConv, p, cs))) return rc;
   CUDA_TRY(cudaMemcpyAsync(W.host_counters, W.counters.ptr, sizeof(DevCounters),
                            cudaMemcpyDeviceToHost, cs));
   return SPMESL_OK;
@@ -1322,7 +1325,9 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
     }
     int any_unconv = 0;
     // (standardize, assemble_lists, column_stats)
-    finish_stats(W, p, st, &any_unconv, 3, st && st->graph_replay);
+    // (standardize + assemble_lists with the statistics fused; the sparse output: standardize,
+    // sparse_count, csc_scan, sparse_write, column_stats)
+    finish_stats(W, p, st, &any_unconv, W.sparse ? 5 : 2, st && st->graph_replay);
     return any_unconv ? SPMESL_WARN_NOT_CONVERGED : SPMESL_OK;
   }
   // residual solver / joint mode: enqueue per call

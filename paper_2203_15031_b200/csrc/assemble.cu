@@ -103,6 +103,12 @@ __device__ __forceinline__ double theta1(double b, double sigma_k, double s_j, d
   return w;
 }
 
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // Binary search for row r in the sorted rows[lo, hi); returns the value or 0.
 __device__ __forceinline__ double csc_lookup(const int32_t* __restrict__ rows,
                                              const double* __restrict__ vals, int64_t lo,
@@ -154,10 +160,14 @@ __global__ void assemble_entries_kernel(int64_t p, int64_t col_begin, int64_t co
 }
 
 // Device-path assembly straight from the per-column coefficient lists (rows ascending; no CSC
-// packing): one warp per column k writes its off-diagonal entries (a8 + a10: the partner b_kj
-// is found by binary search in column j's list, exactly as in the CSC variant) and lane 0 the
-// diagonal and sigma; the column's entry count is added to
-// *nnz_total.  Bit-identical to csc_build + assemble_entries + assemble_diag.
+// packing): each warp owns 32 consecutive columns.  Lane l writes the diagonal and sigma of
+// column 32 w + l (coalesced) and, when `cs` is given, adds that column's
+// sweeps / outer iterations / converged flag to the fit statistics (what column_stats_kernel
+// does otherwise, fused here: the last kernel of the fit also stamps its end); then the warp
+// walks the columns of its 32 that have entries (most have none) and writes their off-diagonal
+// entries together (a8 + a10: the partner b_kj is found by binary search in column j's list,
+// exactly as in the CSC variant).  Each column's entry count is added to *nnz_total.
+// Bit-identical to csc_build + assemble_entries + assemble_diag.
 __global__ void assemble_lists_kernel(int64_t p, const int* __restrict__ cnt,
                                       const int* __restrict__ cur,
                                       const int* __restrict__ nz_rows,
@@ -166,45 +176,83 @@ __global__ void assemble_lists_kernel(int64_t p, const int* __restrict__ cnt,
                                       const double* __restrict__ scale, int symmetrize,
                                       int rescale, double* __restrict__ Theta,
                                       double* __restrict__ sigma_out,
-                                      unsigned long long* __restrict__ nnz_total) {
+                                      unsigned long long* __restrict__ nnz_total, ColStats cs) {
   const int lane = threadIdx.x & 31;
-  const int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (k >= p) return;
-  const int m = min(cnt[k], nzcap);
-  const double sk = rescale ? scale[k] : 1.0;
-  if (lane == 0) {
-    const double sg = sigma_std[k];
+  const int64_t k0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
+  if (k0 >= p) return;
+  const int64_t kl = k0 + lane;
+  int mine = 0;
+  unsigned long long tsw = 0;
+  int msw = 0, mo = 0, nu = 0;
+  if (kl < p) {
+    mine = min(cnt[kl], nzcap);
+    const double sk = rescale ? scale[kl] : 1.0;
+    const double sg = sigma_std[kl];
     double w = 1.0 / (sg * sg);
     if (rescale) w = w / (sk * sk);
-    Theta[(size_t)k * (size_t)p + (size_t)k] = w;
-    if (sigma_out) sigma_out[k] = rescale ? sk * sg : sg;
-    if (m) atomicAdd(nnz_total, (unsigned long long)m);
-  }
-  const size_t base = (size_t)k * 2 * nzcap + (size_t)cur[k] * nzcap;
-  for (int e = lane; e < m; e += 32) {
-    const int j = nz_rows[base + e];
-    const double sj = rescale ? scale[j] : 1.0;
-    const double t_jk = theta1(nz_vals[base + e], sigma_std[k], sj, sk, rescale != 0);
-    double out = t_jk;
-    if (symmetrize) {
-      const size_t bj = (size_t)j * 2 * nzcap + (size_t)cur[j] * nzcap;
-      const int mj = min(cnt[j], nzcap);
-      int lo = 0, hi = mj;
-      double b_kj = 0.0;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        const int v = nz_rows[bj + mid];
-        if (v == (int)k) { b_kj = nz_vals[bj + mid]; break; }
-        if (v < (int)k) lo = mid + 1;
-        else hi = mid;
-      }
-      if (b_kj == 0.0) continue;            // partner zero -> symmetrized value is zero
-      const double t_kj = theta1(b_kj, sigma_std[j], sk, sj, rescale != 0);
-      const double u = (j < k) ? t_jk : t_kj;   // Theta1[min, max]
-      const double l = (j < k) ? t_kj : t_jk;   // Theta1[max, min]
-      out = (fabs(u) > fabs(l)) ? l : u;
+    Theta[(size_t)kl * (size_t)p + (size_t)kl] = w;
+    if (sigma_out) sigma_out[kl] = rescale ? sk * sg : sg;
+    if (cs.sweeps) {
+      const int sw = cs.sweeps[kl];
+      tsw = (unsigned long long)sw;
+      msw = sw;
+      mo = cs.iters[kl];
+      nu = cs.conv[kl] ? 0 : 1;
     }
-    Theta[(size_t)k * (size_t)p + (size_t)j] = out;
+  }
+  unsigned long long tot = (unsigned long long)mine;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+  if (lane == 0 && tot) atomicAdd(nnz_total, tot);
+  if (cs.sweeps) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      tsw += __shfl_xor_sync(0xffffffffu, tsw, o);
+      msw = max(msw, __shfl_xor_sync(0xffffffffu, msw, o));
+      mo = max(mo, __shfl_xor_sync(0xffffffffu, mo, o));
+      nu += __shfl_xor_sync(0xffffffffu, nu, o);
+    }
+  }
+  unsigned todo = __ballot_sync(0xffffffffu, mine > 0);
+  while (todo) {
+    const int src = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const int64_t k = k0 + src;
+    const int m = __shfl_sync(0xffffffffu, mine, src);
+    const double sk = rescale ? scale[k] : 1.0;
+    const size_t base = (size_t)k * 2 * nzcap + (size_t)cur[k] * nzcap;
+    for (int e = lane; e < m; e += 32) {
+      const int j = nz_rows[base + e];
+      const double sj = rescale ? scale[j] : 1.0;
+      const double t_jk = theta1(nz_vals[base + e], sigma_std[k], sj, sk, rescale != 0);
+      double out = t_jk;
+      if (symmetrize) {
+        const size_t bj = (size_t)j * 2 * nzcap + (size_t)cur[j] * nzcap;
+        const int mj = min(cnt[j], nzcap);
+        int lo = 0, hi = mj;
+        double b_kj = 0.0;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          const int v = nz_rows[bj + mid];
+          if (v == (int)k) { b_kj = nz_vals[bj + mid]; break; }
+          if (v < (int)k) lo = mid + 1;
+          else hi = mid;
+        }
+        if (b_kj == 0.0) continue;            // partner zero -> symmetrized value is zero
+        const double t_kj = theta1(b_kj, sigma_std[j], sk, sj, rescale != 0);
+        const double u = (j < k) ? t_jk : t_kj;   // Theta1[min, max]
+        const double l = (j < k) ? t_kj : t_jk;   // Theta1[max, min]
+        out = (fabs(u) > fabs(l)) ? l : u;
+      }
+      Theta[(size_t)k * (size_t)p + (size_t)j] = out;
+    }
+  }
+  if (cs.sweeps && lane == 0) {
+    if (tsw) atomicAdd(cs.tot, tsw);
+    atomicMax(cs.mx_sweeps, msw);
+    atomicMax(cs.mx_outer, mo);
+    if (nu) atomicAdd(cs.nunc, nu);
+    if (cs.t_end) atomicMax(cs.t_end, global_ns());   // the fit's end (ms_total)
   }
 }
 
@@ -574,19 +622,17 @@ cudaError_t launch_assemble_lists(int64_t p, const int* nz_count, const int* nz_
                                   const int* nz_rows, const double* nz_vals, int nzcap,
                                   const double* sigma_std, const double* scale, int symmetrize,
                                   double* Theta, double* sigma_out, int64_t* nnz_total,
-                                  cudaStream_t s) {
-  const int wpb = 8;
-  assemble_lists_kernel<<<(unsigned)((p + wpb - 1) / wpb), wpb * 32, 0, s>>>(
+                                  cudaStream_t s, const ColStats* cs) {
+  const int wpb = 4;                     // (32 columns per warp)
+  const int64_t warps = (p + 31) / 32;
+  ColStats c{};
+  if (cs) c = *cs;
+  assemble_lists_kernel<<<(unsigned)((warps + wpb - 1) / wpb), wpb * 32, 0, s>>>(
       p, nz_count, nz_cur, nz_rows, nz_vals, nzcap, sigma_std, scale, symmetrize,
-      scale != nullptr, Theta, sigma_out, (unsigned long long*)nnz_total);
+      scale != nullptr, Theta, sigma_out, (unsigned long long*)nnz_total, c);
   return cudaGetLastError();
 }
 
-__device__ __forceinline__ unsigned long long global_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 
 // Per-column statistics on the device (no host copy of iters/sweeps/converged):
 // out[0] += sum sweeps (64-bit), out[2] = max sweeps, out[3] = max iters, out[4] += unconverged.

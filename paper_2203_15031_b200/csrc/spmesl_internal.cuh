@@ -350,11 +350,22 @@ cudaError_t launch_assemble_coo_p2p(const P2PBlocks& B, int self, const double* 
                                     int symmetrize, int32_t* coo_row, int32_t* coo_col,
                                     double* coo_val, int* coo_count, double* diag,
                                     double* sigma_out, cudaStream_t s);
+// fit statistics gathered by the assembly (fused column_stats_kernel; sweeps == NULL: none)
+struct ColStats {
+  const int32_t* iters;
+  const int32_t* sweeps;
+  const uint8_t* conv;
+  unsigned long long* tot;
+  int* mx_sweeps;
+  int* mx_outer;
+  int* nunc;
+  unsigned long long* t_end;
+};
 cudaError_t launch_assemble_lists(int64_t p, const int* nz_count, const int* nz_cur,
                                   const int* nz_rows, const double* nz_vals, int nzcap,
                                   const double* sigma_std, const double* scale, int symmetrize,
                                   double* Theta, double* sigma_out, int64_t* nnz_total,
-                                  cudaStream_t s);
+                                  cudaStream_t s, const ColStats* cs = nullptr);
 cudaError_t launch_assemble(int64_t p, int64_t col_begin, int64_t col_end, const int64_t* col_ptr,
                             const int32_t* rows, const double* vals, const double* sigma_std,
                             const double* scale, int symmetrize, double* Theta, double* sigma_out,
