@@ -426,6 +426,13 @@ def run_ours(args):
             updates += st["coord_updates"]
             stats_last = st
     step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
+    # the replayed steps time only the whole fit and the screening kernel: one eager fit after
+    # the timed region gives the other kernels' times (ms_breakdown, the sweep kernel)
+    eager_st = None
+    if world == 1:
+        eager_st = S.fit_device(Xd, lam, TOL, MAX_ITER, stream=stream, out=outbuf, mode=args.mode,
+                                solver=args.solver, eager=True).stats
+        torch.cuda.synchronize()
     print(f"[rank {rank}] step ms: {[round(x, 3) for x in step_ms]}  cd ms: {[round(x, 3) for x in cd_ms]}",
           file=sys.stderr, flush=True)
     tot_ms = sum(step_ms)
@@ -483,7 +490,8 @@ def run_ours(args):
                 "tensor_tflops": flops / (scr_ms / 1000.0) / 1e12,
                 "screen_candidates": stats_last.get("screen_candidates"),
                 "rest_of_step_ms": step_ms_mean - scr_ms,
-                "sweep_kernel_ms": stats_last.get("ms_tail", 0.0),
+                "sweep_kernel_ms": (eager_st or stats_last).get("ms_tail", 0.0),
+                "sweep_kernel_timing": "eager fit after the timed steps",
                 "sweep_columns": stats_last.get("tail_columns", 0)}
     elif stats_last.get("solver") in (2, 3):
         # Gram solver: the symmetric Gram kernel; algorithmic work n p (p + 1) flops (each of
@@ -637,10 +645,16 @@ def run_ours(args):
                 "roofline": roof, "clocks": clk.summary(), "e2e": e2e,
                 "gpu_launches": int(stats_last["kernel_launches"]) * args.steps,
                 "ms_breakdown": {k: (v if v is None or v >= 0 else None) for k, v in {
-                    "standardize": stats_last["ms_standardize"], "solve": stats_last["ms_cd"],
-                    "gram": stats_last.get("ms_gram", 0.0), "sweeps": stats_last.get("ms_tail", 0.0),
-                    "assemble": stats_last["ms_assemble"], "screen": stats_last.get("ms_screen"),
+                    "standardize": (eager_st or stats_last)["ms_standardize"],
+                    "solve": (eager_st or stats_last)["ms_cd"],
+                    "gram": (eager_st or stats_last).get("ms_gram", 0.0),
+                    "sweeps": (eager_st or stats_last).get("ms_tail", 0.0),
+                    "assemble": (eager_st or stats_last)["ms_assemble"],
+                    "screen": stats_last.get("ms_screen"),
                     "total_device": stats_last.get("ms_total")}.items()},
+                "ms_breakdown_source": ("phases from one eager fit after the timed steps; screen "
+                                        "and total_device from the replayed steps")
+                if eager_st else "the last timed step",
                 "graph_replay": bool(stats_last.get("graph_replay", 0))}
         if cpu:
             line["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
