@@ -135,6 +135,10 @@ struct Workspace {
   // fit whose certified screening fell back to the full FP64 Gram kernel — a repeat runs the full
   // Gram path directly (fit_device_impl)
   std::vector<unsigned char> auto_full_key;
+  // ... and of the last fit whose screening left few candidates: a repeat launches the exact
+  // Gram columns without the full Gram kernel behind them (which would only exit)
+  std::vector<unsigned char> auto_few_key;
+  bool no_fallback = false;   // (fit_gram_enqueue, screening path: no fallback launch)
   bool init = false;
 };
 
@@ -743,7 +747,10 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
                                  (int*)W.umap.ptr, s));
     G.zero_ptr = nullptr;              // (Theta's zero fill is already under way)
     G.cond_nU = nU_dev;
-    {
+    // (W.no_fallback: the exact Gram columns of every candidate, however many — correct for
+    // any count, and what the screening history of these arguments expects)
+    const bool fb = !W.no_fallback || nlam > 1;
+    if (fb) {
       const int nT = (int)((L.nblk + 3) / 4);
       const int ntiles = nT * (nT + 1) / 2;
       CUDA_TRY(launch_syrk_screen(G, std::min(W.sms, ntiles), s));
@@ -753,8 +760,8 @@ int fit_gram_enqueue(Workspace& W, const double* dX, int64_t n, int64_t p, doubl
                               (const int*)W.uvars.ptr, 0, nU_dev, W.sms, (double*)W.ondemand.ptr,
                               (uint8_t*)W.hit.ptr,
                               nlam > 1 ? (const double*)W.lam_dev.ptr : nullptr, nlam,
-                              (int*)W.umap.ptr, s, /*fallback=*/true, lambda0));
-    launches += 3 + (nlam > 1);
+                              (int*)W.umap.ptr, s, /*fallback=*/fb, lambda0));
+    launches += (fb ? 3 : 2) + (nlam > 1);
     CUDA_TRY(ev_record(W, W.ev[7], s));
   } else {
     const int nT = (int)((L.nblk + 3) / 4);
@@ -1241,14 +1248,16 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
     // full-Gram fit with few hit columns hands the choice back to the screening.
     spmesl_options ko = o;   // (the choice is part of the captured graph's key)
     std::vector<unsigned char> akey;
-    bool full = o.solver == 2;
+    bool full = o.solver == 2, few = false;
     if (o.solver == 0) {
       spmesl_options ao = o;
       ao.eager = 0;          // (eager and replayed fits share the history)
       akey = graph_key(dX, n, p, lambda0, tol, max_iter, ao, dTheta, dSigma, dIters, dSweeps, dConv,
                        0, s, W.sparse);
       full = !W.auto_full_key.empty() && W.auto_full_key == akey;
+      few = !full && !W.auto_few_key.empty() && W.auto_few_key == akey;
       if (full) ko.solver = 2;
+      else if (few) ko.solver = 5;   // (a key value of its own: no fallback launch)
     }
     // the captured fit's list capacity if these are its arguments, else the initial one
     nzcap = initial_nzcap(n, p);
@@ -1274,8 +1283,10 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
         W.capturing = true;
         cudaError_t e = cudaStreamBeginCapture(W.cap, cudaStreamCaptureModeRelaxed);
         if (e == cudaSuccess) {
+          W.no_fallback = few;
           rc = gram_fit_enqueue_all(W, dX, n, p, lambda0, tol, max_iter, o, dTheta, dSigma,
                                     dIters, dSweeps, dConv, out, W.cap, L, nzcap, !full);
+          W.no_fallback = false;
           cudaGraph_t g = nullptr;
           e = cudaStreamEndCapture(W.cap, &g);
           W.capturing = false;
@@ -1301,8 +1312,10 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
         }
       }
       if (!launched) {
+        W.no_fallback = few;
         rc = gram_fit_enqueue_all(W, dX, n, p, lambda0, tol, max_iter, o, dTheta, dSigma,
                                   dIters, dSweeps, dConv, out, s, L, nzcap, !full);
+        W.no_fallback = false;
         if (rc) return rc;
         W.last_key = key;
       }
@@ -1312,9 +1325,17 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
         gram_stats(W, p, nzcap, st, !full, launched);
         if (st) st->graph_replay = launched ? 1 : 0;
         if (o.solver == 0) {   // (the screening history of these arguments)
-          if (!full && gram_fallback_taken(W.host_counters->s16_nU, p)) W.auto_full_key = akey;
-          else if (full && !gram_fallback_taken(W.host_counters->tail_count, p)) W.auto_full_key.clear();
-          if (full && st) st->gram_fallback = 1;
+          if (!full) {
+            if (gram_fallback_taken(W.host_counters->s16_nU, p)) {
+              W.auto_full_key = akey;
+              W.auto_few_key.clear();
+            } else {
+              W.auto_few_key = akey;
+            }
+          } else if (!gram_fallback_taken(W.host_counters->tail_count, p)) {
+            W.auto_full_key.clear();
+          }
+          if (st) st->gram_fallback = full ? 1 : few ? 0 : st->gram_fallback;
         }
         break;
       }
