@@ -1346,9 +1346,9 @@ int fit_device_impl(const double* dX, int64_t n, int64_t p, double lambda0, doub
     }
     int any_unconv = 0;
     // (standardize, assemble_lists, column_stats)
-    // (standardize + assemble_lists with the statistics fused; the sparse output: standardize,
-    // sparse_count, csc_scan, sparse_write, column_stats)
-    finish_stats(W, p, st, &any_unconv, W.sparse ? 5 : 2, st && st->graph_replay);
+    // (reset + standardize + assemble_lists with the statistics fused; the sparse output: reset,
+    // standardize, sparse_count, csc_scan, sparse_write, column_stats)
+    finish_stats(W, p, st, &any_unconv, W.sparse ? 6 : 3, st && st->graph_replay);
     return any_unconv ? SPMESL_WARN_NOT_CONVERGED : SPMESL_OK;
   }
   // residual solver / joint mode: enqueue per call
